@@ -1,0 +1,818 @@
+/*
+ * smc_oracle.c -- TEST INFRASTRUCTURE ONLY (see smc_oracle.h).
+ *
+ * Plain FP64 CPU implementation of the hot path of Eele & Maciejowski (2015),
+ * written step by step in the paper's order and notation.  No blocking,
+ * fusion or reordering beyond what the paper's Algorithm 1 states.
+ * OpenMP is used only across independent particles (Alg.1 l.8).
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC
+ * (no fused multiply-add except the explicit fma() calls det_exp2 requires).
+ *
+ * Parity status per function (DESIGN.md section 4 lists the pinning tests):
+ *   philox, u24, box_muller, det_exp2, det_quant, derive (Rhat, Qhat, a),
+ *   trilinear, popdense, lift_drag, step, unary/landing/pair checks,
+ *   flow_heading, arc_length, beta, utilities, weight recursion, mh_accept,
+ *   resample_column, select, sample_schedule ........................ pinned
+ *   rolling-window averaging (R20), post-landing bonus (R18), removal of a
+ *   violated aircraft (R42), MH move semantics (R1) ...... parity unpinned
+ *   (pure conventions: only self-consistency with the CUDA path is checked)
+ */
+#include "smc_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Counter-based streams (R37): Philox4x32-10 (Salmon et al., SC'11).        */
+/* The paper used CURAND XORWOW with per-thread state; a stateless   */
+/* counter-based generator keys every draw by (particle, sample, step, ...). */
+/* ------------------------------------------------------------------------ */
+enum { TAG_INIT = 1, TAG_PERTURB = 2, TAG_WIND = 3, TAG_TURB = 4, TAG_MH = 5,
+       TAG_RESAMPLE = 6, TAG_PLANT_WIND = 7, TAG_PLANT_TURB = 8 };
+
+void ora_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)x0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)x2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t y0 = hi1 ^ x1 ^ k0;
+        uint32_t y1 = lo1;
+        uint32_t y2 = hi0 ^ x3 ^ k1;
+        uint32_t y3 = lo0;
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+    }
+    out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+static void draw(uint32_t tag, uint32_t x0, uint32_t x1, uint32_t x2, uint32_t mpc,
+                 uint64_t seed, uint32_t w[4])
+{
+    uint32_t ctr[4] = { x0, x1, x2, (mpc & 0xFFFFFFu) | (tag << 24) };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    ora_philox(ctr, key, w);
+}
+
+/* 23-bit uniform in (0,1): (2k+1) 2^-24 with k = w >> 9 < 2^23 has at most 24
+ * significant bits, so it is exactly representable in binary32 and binary64
+ * and both implementations see bit-identical uniforms (R37). */
+double ora_u24(uint32_t w) { return ((double)(w >> 9) + 0.5) * (1.0 / 8388608.0); }
+
+/* Box-Muller transform on one word pair. */
+void ora_box_muller(uint32_t w0, uint32_t w1, double *n0, double *n1)
+{
+    double u1 = ora_u24(w0), u2 = ora_u24(w1);
+    double r = sqrt(-2.0 * log(u1));
+    *n0 = r * cos(2.0 * M_PI * u2);
+    *n1 = r * sin(2.0 * M_PI * u2);
+}
+
+uint64_t ora_r64(uint32_t tag, uint32_t x0, uint32_t k, uint64_t seed, uint32_t mpc)
+{
+    uint32_t w[4];
+    draw(tag, x0, k << 16, 0, mpc, seed, w);
+    return (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+}
+
+/* ------------------------------------------------------------------------ */
+/* det_exp2 / det_quant (R26): 2^y from correctly rounded IEEE ops only, so  */
+/* an independent implementation with the same op sequence agrees bit-exact. */
+/* c_j = RN((ln 2)^j / j!), j = 0..16; Horner with fma; ldexp.               */
+/* ------------------------------------------------------------------------ */
+static const double DET_C[17] = {
+    0x1.0000000000000p+0,  0x1.62e42fefa39efp-1, 0x1.ebfbdff82c58fp-3,
+    0x1.c6b08d704a0c0p-5,  0x1.3b2ab6fba4e77p-7, 0x1.5d87fe78a6731p-10,
+    0x1.430912f86c787p-13, 0x1.ffcbfc588b0c7p-17, 0x1.62c0223a5c824p-20,
+    0x1.b5253d395e7c4p-24, 0x1.e4cf5158b8ecap-28, 0x1.e8cac7351bb25p-32,
+    0x1.c3bd650fc2986p-36, 0x1.816193166d0f9p-40, 0x1.314964d5878a9p-44,
+    0x1.c36e843b04022p-49, 0x1.38e89ae79f8b4p-53 };
+
+const double *ora_det_coeffs(void) { return DET_C; }
+
+double ora_det_exp2(double y)
+{
+    if (!(y >= -1022.0)) return 0.0;          /* keeps every result a normal number */
+    double n = floor(y);
+    double f = y - n;                          /* exact */
+    double p = DET_C[16];
+    for (int j = 15; j >= 0; --j) p = fma(p, f, DET_C[j]);
+    return ldexp(p, (int)n);
+}
+
+uint64_t ora_det_quant(double d)
+{
+    if (!(d >= -32.0)) return 0;               /* also -inf and NaN */
+    double v = ora_det_exp2(32.0 + d);
+    return (uint64_t)floor(v);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Sample schedule: floor(3 + 5 e^{0.05 J}).                         */
+/* ------------------------------------------------------------------------ */
+int ora_sample_schedule(int J) { return (int)floor(3.0 + 5.0 * exp(0.05 * (double)J)); }
+
+/* ------------------------------------------------------------------------ */
+/* Scenario precompute                                                       */
+/* ------------------------------------------------------------------------ */
+static void node_pos(const ora_problem *p, int n, double pos[3])
+{
+    int ix = n & 1, iy = (n >> 1) & 1, iz = (n >> 2) & 1;
+    pos[0] = ix ? p->wind_hi[0] : p->wind_lo[0];
+    pos[1] = iy ? p->wind_hi[1] : p->wind_lo[1];
+    pos[2] = iz ? p->wind_hi[2] : p->wind_lo[2];
+}
+
+static double sigma_z(const ora_problem *p, double z)
+{
+    double fz = (z - p->wind_lo[2]) / (p->wind_hi[2] - p->wind_lo[2]);
+    return p->sigma_lo + (p->sigma_hi - p->sigma_lo) * fz;
+}
+
+/* popdense: min(sum_i exp(-b_i^2/(2 c_i^2)) / (c_i sqrt(2 pi)), 1),
+ * b_i, c_i in km (R23). */
+double ora_popdense_point(const ora_problem *p, double x, double y)
+{
+    double sum = 0.0;
+    for (int c = 0; c < p->n_centres; ++c) {
+        double bx = (x - p->centres[3 * c + 0]) / 1000.0;
+        double by = (y - p->centres[3 * c + 1]) / 1000.0;
+        double ci = p->centres[3 * c + 2] / 1000.0;
+        double b2 = bx * bx + by * by;
+        sum += exp(-b2 / (2.0 * ci * ci)) / (ci * sqrt(2.0 * M_PI));
+    }
+    return sum < 1.0 ? sum : 1.0;
+}
+
+/* Cholesky factor L with L L^T = A (A SPD, row-major 8x8). */
+static int cholesky8(const double *A, double *Lo)
+{
+    memset(Lo, 0, 64 * sizeof(double));
+    for (int r = 0; r < 8; ++r) {
+        for (int c = 0; c <= r; ++c) {
+            double s = A[r * 8 + c];
+            for (int k = 0; k < c; ++k) s -= Lo[r * 8 + k] * Lo[c * 8 + k];
+            if (r == c) {
+                if (!(s > 0.0)) return -1;
+                Lo[r * 8 + r] = sqrt(s);
+            } else {
+                Lo[r * 8 + c] = s / Lo[c * 8 + c];
+            }
+        }
+    }
+    return 0;
+}
+
+int ora_derive(const ora_problem *p, ora_derived *d)
+{
+    memset(d, 0, sizeof(*d));
+    if (p->n < 0 || p->n > ORA_MAX_AC || p->H < 0 || p->H > 255) return -1;
+    /* Eq. cov, same-time entries of Rhat. */
+    for (int n = 0; n < 8; ++n) {
+        double pn[3]; node_pos(p, n, pn);
+        for (int m = 0; m < 8; ++m) {
+            double pm[3]; node_pos(p, m, pm);
+            double dxy = sqrt((pn[0] - pm[0]) * (pn[0] - pm[0]) + (pn[1] - pm[1]) * (pn[1] - pm[1]));
+            double dz = fabs(pn[2] - pm[2]);
+            d->Rhat[n * 8 + m] = sigma_z(p, pn[2]) * sigma_z(p, pm[2])
+                               * exp(-p->beta_w * dxy) * exp(-p->gamma_w * dz);
+        }
+    }
+    /* Qhat Qhat^T = Rhat.  sigma == 0 gives a zero field. */
+    int zero = 1;
+    for (int n = 0; n < 64; ++n) if (d->Rhat[n] != 0.0) zero = 0;
+    if (!zero && cholesky8(d->Rhat, d->Qhat) != 0) return -2;
+    /* a = e^{-dt/G_t}, G_t = 1/lambda_t (R14); Q = sqrt(1-a^2) Qhat. */
+    d->a = exp(-p->lambda_t * p->dt);
+    d->b = sqrt(1.0 - d->a * d->a);
+    /* Departure altitude term B: sup / inf by reachability with gamma_max, v_max (R21). */
+    for (int i = 0; i < p->n; ++i) {
+        int e = p->first_step[i];
+        int Ha = p->H - e;
+        double z0 = p->x0[6 * i + 2], zt = p->z_tf[i];
+        double ssum = 0.0, isum = 0.0;
+        for (int j = e + 1; j <= p->H; ++j) {
+            double reach = (double)(j - e) * p->dt * p->v_max[i] * sin(p->gamma_max[i]);
+            double lo = z0 - reach; if (lo < p->z_min[i]) lo = p->z_min[i];
+            double hi = z0 + reach; if (hi > p->z_max[i]) hi = p->z_max[i];
+            double sup = fabs(zt - lo) > fabs(zt - hi) ? fabs(zt - lo) : fabs(zt - hi);
+            double nearest = zt < lo ? lo : (zt > hi ? hi : zt);
+            ssum += sup;
+            isum += fabs(zt - nearest);
+        }
+        d->supB[i] = Ha > 0 ? ssum / Ha : 0.0;
+        d->infB[i] = Ha > 0 ? isum / Ha : 0.0;
+    }
+    /* 1 km population grid. */
+    if (p->pop_nx > 0 && p->pop_ny > 0) {
+        d->pop = (double *)malloc(sizeof(double) * (size_t)p->pop_nx * (size_t)p->pop_ny);
+        for (int iy = 0; iy < p->pop_ny; ++iy)
+            for (int ix = 0; ix < p->pop_nx; ++ix)
+                d->pop[iy * p->pop_nx + ix] =
+                    ora_popdense_point(p, p->pop_x0 + ix * p->pop_dx, p->pop_y0 + iy * p->pop_dx);
+    }
+    return 0;
+}
+
+void ora_free_derived(ora_derived *d) { free(d->pop); d->pop = NULL; }
+
+/* Bilinear lookup on the 1 km grid, clamped at its edge (R23). */
+double ora_popdense_grid(const ora_problem *p, const ora_derived *d, double x, double y)
+{
+    if (!d->pop) return 0.0;
+    double gx = (x - p->pop_x0) / p->pop_dx, gy = (y - p->pop_y0) / p->pop_dx;
+    double mx = (double)(p->pop_nx - 1), my = (double)(p->pop_ny - 1);
+    if (!(gx > 0.0)) gx = 0.0; if (gx > mx) gx = mx;
+    if (!(gy > 0.0)) gy = 0.0; if (gy > my) gy = my;
+    int ix = (int)floor(gx), iy = (int)floor(gy);
+    if (ix > p->pop_nx - 2) ix = p->pop_nx - 2; if (ix < 0) ix = 0;
+    if (iy > p->pop_ny - 2) iy = p->pop_ny - 2; if (iy < 0) iy = 0;
+    double fx = gx - ix, fy = gy - iy;
+    if (p->pop_nx == 1) fx = 0.0;
+    if (p->pop_ny == 1) fy = 0.0;
+    int ix1 = p->pop_nx > 1 ? ix + 1 : ix, iy1 = p->pop_ny > 1 ? iy + 1 : iy;
+    double v00 = d->pop[iy * p->pop_nx + ix], v10 = d->pop[iy * p->pop_nx + ix1];
+    double v01 = d->pop[iy1 * p->pop_nx + ix], v11 = d->pop[iy1 * p->pop_nx + ix1];
+    return (1 - fx) * (1 - fy) * v00 + fx * (1 - fy) * v10 + (1 - fx) * fy * v01 + fx * fy * v11;
+}
+
+/* "tri-linear interpolation between the grid points", position
+ * clamped to the grid box (R14). */
+void ora_trilinear(const ora_problem *p, const double W[8], const double pos[3], double *w)
+{
+    double f[3];
+    for (int a = 0; a < 3; ++a) {
+        double t = (pos[a] - p->wind_lo[a]) / (p->wind_hi[a] - p->wind_lo[a]);
+        if (!(t > 0.0)) t = 0.0;
+        if (t > 1.0) t = 1.0;
+        f[a] = t;
+    }
+    double acc = 0.0;
+    for (int n = 0; n < 8; ++n) {
+        double wx = (n & 1) ? f[0] : 1.0 - f[0];
+        double wy = (n & 2) ? f[1] : 1.0 - f[1];
+        double wz = (n & 4) ? f[2] : 1.0 - f[2];
+        acc += wx * wy * wz * W[n];
+    }
+    *w = acc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Aircraft model (Eq. hor)                                       */
+/* ------------------------------------------------------------------------ */
+static double density(const ora_problem *p, double z)
+{
+    if (p->density_mode == 1) return p->rho_const;
+    double base = 1.0 - 2.2558e-5 * z;                   /* ISA troposphere (R12) */
+    if (!(base > 0.0)) base = 0.0;
+    return 1.225 * pow(base, 4.2559);
+}
+
+/* "Lift L and drag D are calculated using the standard aerodynamic relations"
+ * -- read as coordinated-turn lift and a parabolic polar (R12). */
+void ora_lift_drag(const ora_problem *p, int i, const double st[6], double phi,
+                   double *lift, double *drag)
+{
+    double v = st[3], m = st[5];
+    double rho = density(p, st[2]);
+    double qd = 0.5 * rho * v * v * p->S[i];
+    double L = m * p->g / cos(phi);
+    double CL = L / qd;
+    *lift = L;
+    *drag = qd * (p->cd0[i] + p->cd2[i] * CL * CL);
+}
+
+/* Eq. hor, simultaneous explicit Euler (R41). st/out = x,y,z,v,chi,m. */
+void ora_step(const ora_problem *p, int i, const double st[6], const double u[3],
+              const double wind[2], double out[6])
+{
+    double T = u[0], phi = u[1], gam = u[2];
+    double x = st[0], y = st[1], z = st[2], v = st[3], chi = st[4], m = st[5];
+    double L, D;
+    ora_lift_drag(p, i, st, phi, &L, &D);
+    double dt = p->dt;
+    out[0] = x + dt * (v * cos(chi) * cos(gam)) + wind[0] * dt;
+    out[1] = y + dt * (v * sin(chi) * cos(gam)) + wind[1] * dt;
+    out[2] = z + dt * (v * sin(gam));
+    out[3] = v + dt * ((T - D) / m - p->g * sin(gam));
+    out[4] = chi + dt * (L * sin(phi) / (m * v));
+    out[5] = m - dt * (p->eta[i] * T);
+}
+
+/* |wrap(d)| in [0, pi] (R32). */
+double ora_angdist(double d)
+{
+    double r = fmod(fabs(d), 2.0 * M_PI);
+    return r > M_PI ? 2.0 * M_PI - r : r;
+}
+
+/* Flow-field heading (R8): the circle through the origin tangent to the
+ * runway axis, flown so as to arrive heading West: chi_hat = pi + 2 theta. */
+double ora_flow_heading(double x, double y) { return M_PI + 2.0 * atan2(y, x); }
+
+/* "distance remaining on the arc of the flow field" (R9). */
+double ora_arc_length(double x, double y)
+{
+    double rho = sqrt(x * x + y * y);
+    double th = fabs(atan2(y, x));
+    if (th == 0.0) return rho;
+    return rho * th / sin(th);
+}
+
+/* Eq. flow with the arc length of R9. */
+double ora_beta(double x, double y, double z) { return atan2(z, ora_arc_length(x, y)); }
+
+/* Landing sector (Eq. TO_init; R10). */
+int ora_landed(const ora_problem *p, const double st[6])
+{
+    double x = st[0], y = st[1], z = st[2], v = st[3], chi = st[4];
+    double rho = sqrt(x * x + y * y);
+    return rho <= p->P_runway
+        && ora_beta(x, y, z) <= p->P_beta
+        && fabs(atan2(y, x)) <= p->P_chi
+        && ora_angdist(chi - M_PI) <= p->P_chi
+        && v <= p->P_vs;
+}
+
+/* Unary constraints (R17): controls of the step and the new state. */
+int ora_unary_violation(const ora_problem *p, int i, const double u[3], const double st[6])
+{
+    for (int a = 0; a < 6; ++a) if (!isfinite(st[a])) return 1;
+    if (fabs(u[2]) > p->gamma_max[i]) return 1;
+    if (!(fabs(u[1]) < p->phi_max[i])) return 1;
+    if (u[0] < p->T_min[i] || u[0] > p->T_max[i]) return 1;
+    if (st[2] < p->z_min[i] || st[2] > p->z_max[i]) return 1;
+    if (st[3] < p->v_min[i] || st[3] > p->v_max[i]) return 1;
+    if (st[5] < p->m_empty[i]) return 1;
+    return 0;
+}
+
+/* Negation of Eq. avoidance: conflict iff both separations fail. */
+int ora_pair_conflict(const ora_problem *p, const double a[6], const double b[6])
+{
+    double dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+    double ok = (dx * dx + dy * dy >= (2.0 * p->P_r) * (2.0 * p->P_r)) || (fabs(dz) >= 2.0 * p->P_h);
+    return !ok && isfinite(dx) && isfinite(dy) && isfinite(dz);
+}
+
+static double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+static double fmin_abs(double cur, double m) { m = fabs(m); return m < cur ? m : cur; }
+
+/* ------------------------------------------------------------------------ */
+/* One rollout (Alg.1 l.10-16 for one particle, one sample)                  */
+/* ------------------------------------------------------------------------ */
+void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
+                 uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
+                 ora_rollout_out *out)
+{
+    const int n = p->n, H = p->H;
+    double st[ORA_MAX_AC][6], nx[ORA_MAX_AC][6];
+    double fuel[ORA_MAX_AC], sA[ORA_MAX_AC], sB[ORA_MAX_AC], sC[ORA_MAX_AC], sN[ORA_MAX_AC];
+    double marg[ORA_MAX_AC];
+    int landed[ORA_MAX_AC], viol[ORA_MAX_AC], fly[ORA_MAX_AC], vnow[ORA_MAX_AC];
+    double Z[2][8], W[2][8];
+
+    for (int i = 0; i < n; ++i) {
+        memcpy(st[i], &p->x0[6 * i], sizeof(st[i]));
+        fuel[i] = sA[i] = sB[i] = sC[i] = sN[i] = 0.0;
+        landed[i] = -1; viol[i] = 0; marg[i] = INFINITY;
+        if (out && out->traj) memcpy(&out->traj[((size_t)i * (H + 1)) * 6], st[i], sizeof(st[i]));
+    }
+    const double twoPr2 = (2.0 * p->P_r) * (2.0 * p->P_r), twoPh = 2.0 * p->P_h;
+
+    for (int t = 0; t < H; ++t) {
+        /* Alg.1 l.10: disturbance realisation for step t:
+         * W(0) = Qhat v(0); W(t) = a W(t-1) + Q v(t) with Q = b Qhat. */
+        double v[16];
+        for (int blk = 0; blk < 4; ++blk) {
+            uint32_t w[4];
+            draw(TAG_WIND, l, (s & 0xFFFFu) | (k << 16), (uint32_t)t | ((uint32_t)blk << 16), mpc, seed, w);
+            ora_box_muller(w[0], w[1], &v[4 * blk + 0], &v[4 * blk + 1]);
+            ora_box_muller(w[2], w[3], &v[4 * blk + 2], &v[4 * blk + 3]);
+        }
+        for (int c = 0; c < 2; ++c)
+            for (int m = 0; m < 8; ++m)
+                Z[c][m] = (t == 0) ? v[8 * c + m] : d->a * Z[c][m] + d->b * v[8 * c + m];
+        for (int c = 0; c < 2; ++c)
+            for (int r = 0; r < 8; ++r) {
+                double acc = 0.0;
+                for (int m = 0; m < 8; ++m) acc += d->Qhat[r * 8 + m] * Z[c][m];
+                W[c][r] = acc;
+            }
+
+        /* Alg.1 l.11: simulate every aircraft in the problem at step t. */
+        for (int i = 0; i < n; ++i) {
+            fly[i] = (p->first_step[i] <= t) && landed[i] < 0 && !viol[i];
+            vnow[i] = 0;
+            if (!fly[i]) { memcpy(nx[i], st[i], sizeof(nx[i])); continue; }
+            double wind[2];
+            ora_trilinear(p, W[0], st[i], &wind[0]);
+            ora_trilinear(p, W[1], st[i], &wind[1]);
+            wind[0] += p->nominal[0];
+            wind[1] += p->nominal[1];
+            if (p->turb_sigma > 0.0) {
+                uint32_t w[4];
+                draw(TAG_TURB, l, (s & 0xFFFFu) | (k << 16), ((uint32_t)t >> 1) | ((uint32_t)i << 8), mpc, seed, w);
+                double g0, g1;
+                if ((t & 1) == 0) ora_box_muller(w[0], w[1], &g0, &g1);
+                else              ora_box_muller(w[2], w[3], &g0, &g1);
+                wind[0] += p->turb_sigma * g0;
+                wind[1] += p->turb_sigma * g1;
+            }
+            const double *ut = &u[((size_t)i * H + t) * 3];
+            ora_step(p, i, st[i], ut, wind, nx[i]);
+            fuel[i] += p->dt * p->eta[i] * ut[0];
+        }
+
+        /* Alg.1 l.12-14: constraints at the new state j = t+1. */
+        for (int i = 0; i < n; ++i) {
+            if (!fly[i]) continue;
+            const double *ut = &u[((size_t)i * H + t) * 3];
+            vnow[i] = ora_unary_violation(p, i, ut, nx[i]);
+            if (out && out->margin) {
+                marg[i] = fmin_abs(marg[i], (p->gamma_max[i] - fabs(ut[2])) / p->gamma_max[i]);
+                marg[i] = fmin_abs(marg[i], (p->phi_max[i] - fabs(ut[1])) / p->phi_max[i]);
+                marg[i] = fmin_abs(marg[i], (nx[i][2] - p->z_min[i]) / fmax(1.0, fabs(p->z_max[i])));
+                marg[i] = fmin_abs(marg[i], (p->z_max[i] - nx[i][2]) / fmax(1.0, fabs(p->z_max[i])));
+                marg[i] = fmin_abs(marg[i], (nx[i][3] - p->v_min[i]) / p->v_max[i]);
+                marg[i] = fmin_abs(marg[i], (p->v_max[i] - nx[i][3]) / p->v_max[i]);
+                marg[i] = fmin_abs(marg[i], (nx[i][5] - p->m_empty[i]) / p->m_empty[i]);
+            }
+            if (p->kind[i] == 0 && landed[i] < 0) {
+                if (ora_landed(p, nx[i])) landed[i] = t + 1;
+                if (out && out->margin) {
+                    double x = nx[i][0], y = nx[i][1];
+                    double rho = sqrt(x * x + y * y);
+                    marg[i] = fmin_abs(marg[i], (p->P_runway - rho) / p->P_runway);
+                    marg[i] = fmin_abs(marg[i], (p->P_beta - ora_beta(x, y, nx[i][2])) / p->P_beta);
+                    marg[i] = fmin_abs(marg[i], (p->P_chi - fabs(atan2(y, x))) / p->P_chi);
+                    marg[i] = fmin_abs(marg[i], (p->P_chi - ora_angdist(nx[i][4] - M_PI)) / p->P_chi);
+                    marg[i] = fmin_abs(marg[i], (p->P_vs - nx[i][3]) / p->P_vs);
+                }
+            }
+        }
+        for (int i = 0; i < n; ++i) {
+            if (!fly[i]) continue;
+            for (int q = i + 1; q < n; ++q) {
+                if (!fly[q]) continue;
+                if (ora_pair_conflict(p, nx[i], nx[q])) { vnow[i] = 1; vnow[q] = 1; }
+                if (out && out->margin) {
+                    double dx = nx[i][0] - nx[q][0], dy = nx[i][1] - nx[q][1], dz = nx[i][2] - nx[q][2];
+                    double m1 = (dx * dx + dy * dy) / twoPr2 - 1.0, m2 = fabs(dz) / twoPh - 1.0;
+                    double mm = m1 > m2 ? m1 : m2;
+                    marg[i] = fmin_abs(marg[i], mm);
+                    marg[q] = fmin_abs(marg[q], mm);
+                }
+            }
+        }
+
+        /* Alg.1 l.15: per-step cost terms at j = t+1. */
+        for (int i = 0; i < n; ++i) {
+            if (p->first_step[i] > t) continue;
+            if (fly[i]) {
+                double x = nx[i][0], y = nx[i][1], z = nx[i][2];
+                double th = atan2(y, x);
+                if (p->kind[i] == 1) {
+                    sA[i] += ora_angdist(th - p->theta_F[i]);
+                    sB[i] += fabs(p->z_tf[i] - z);
+                    sC[i] += fabs(nx[i][3] - p->v_D[i]);
+                } else {
+                    sA[i] += ora_angdist(nx[i][4] - ora_flow_heading(x, y));
+                    sB[i] += fabs(ora_beta(x, y, z) - p->beta_f[i]);
+                }
+                if (p->noise_w > 0.0) {
+                    double q = 1.0 - (z / p->A_c) * (z / p->A_c);
+                    sN[i] += 1.0 - (q > 0.0 ? q : 0.0) * ora_popdense_grid(p, d, x, y);
+                }
+            } else if (landed[i] >= 0) {
+                /* landed earlier: "best possible cost, 1, for all remaining steps" */
+                sN[i] += 1.0;
+            }
+        }
+        for (int i = 0; i < n; ++i) {
+            if (fly[i] && vnow[i]) viol[i] = 1;     /* removed after this step (R42) */
+            memcpy(st[i], nx[i], sizeof(st[i]));
+            if (out && out->traj) memcpy(&out->traj[((size_t)i * (H + 1) + t + 1) * 6], st[i], sizeof(st[i]));
+        }
+    }
+
+    /* Objectives J^D_T and J^A_T in [0,1]; R4-R7, R21. */
+    for (int i = 0; i < n; ++i) {
+        int Ha = H - p->first_step[i];
+        double J = 1.0, c4[4] = { 1.0, 1.0, 1.0, 1.0 };
+        if (Ha > 0) {
+            double Fmax = p->dt * Ha * p->T_max[i] * p->eta[i];
+            double Jfuel = Fmax > 0.0 ? clamp01(1.0 - fuel[i] / Fmax) : 1.0;
+            if (p->kind[i] == 1) {
+                double J1 = clamp01(1.0 - (sA[i] / Ha) / M_PI);
+                double den = d->supB[i] - d->infB[i];
+                double J3 = den < 1.0 ? 1.0 : clamp01((d->supB[i] - sB[i] / Ha) / den);
+                double supC = fmax(p->v_max[i] - p->v_D[i], p->v_D[i] - p->v_min[i]);
+                double J4 = clamp01(1.0 - (sC[i] / Ha) / supC);
+                J = p->alpha_dep[0] * J1 + p->alpha_dep[1] * Jfuel + p->alpha_dep[2] * J3 + p->alpha_dep[3] * J4;
+                c4[0] = J1; c4[1] = Jfuel; c4[2] = J3; c4[3] = J4;
+            } else {
+                double J1 = clamp01(1.0 - (sA[i] / Ha) / M_PI);
+                double supE = fmax(p->beta_f[i], M_PI / 2.0 - p->beta_f[i]);
+                double Jalt = clamp01(1.0 - (sB[i] / Ha) / supE);
+                J = p->alpha_arr[0] * J1 + p->alpha_arr[1] * Jalt + p->alpha_arr[2] * Jfuel;
+                c4[0] = J1; c4[1] = Jalt; c4[2] = Jfuel; c4[3] = 0.0;
+            }
+            if (p->noise_w > 0.0) J = (1.0 - p->noise_w) * J + p->noise_w * (sN[i] / Ha);
+        }
+        if (out) {
+            if (out->J) out->J[i] = J;
+            if (out->viol) out->viol[i] = viol[i];
+            if (out->comp) memcpy(&out->comp[4 * i], c4, sizeof(c4));
+            if (out->fuel) out->fuel[i] = fuel[i];
+            if (out->landed_step) out->landed_step[i] = landed[i];
+            if (out->margin) out->margin[i] = marg[i];
+        }
+    }
+}
+
+/* Alg.1 l.8-17: every particle, S samples, W <- W * J in log2 (R24). */
+void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl,
+                  uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
+                  double *ell, int nthreads)
+{
+    const int n = p->n;
+    const size_t row = (size_t)n * p->H * 3;
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t l = 0; l < (int64_t)L; ++l) {
+        double J[ORA_MAX_AC];
+        int32_t viol[ORA_MAX_AC];
+        ora_rollout_out o;
+        memset(&o, 0, sizeof(o));
+        o.J = J; o.viol = viol;
+        for (uint32_t s = 0; s < S; ++s) {
+            ora_rollout(p, d, &ctrl[(size_t)l * row], (uint32_t)l, s, k, seed, mpc, &o);
+            for (int i = 0; i < n; ++i) {
+                double *e = &ell[(size_t)l * n + i];
+                if (viol[i] || !(J[i] > 0.0)) *e = -INFINITY;
+                else *e += log2(J[i]);
+            }
+        }
+    }
+}
+
+/* Alg.1 l.3-5: uniform controls in [min, max]. */
+void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc, double *ctrl)
+{
+    const int n = p->n, H = p->H;
+    for (uint32_t l = 0; l < L; ++l)
+        for (int i = 0; i < n; ++i)
+            for (int t = 0; t < H; ++t) {
+                uint32_t w[4];
+                draw(TAG_INIT, l, 0, (uint32_t)t | ((uint32_t)i << 8), mpc, seed, w);
+                double *c = &ctrl[(((size_t)l * n + i) * H + t) * 3];
+                c[0] = p->T_min[i] + (p->T_max[i] - p->T_min[i]) * ora_u24(w[0]);
+                c[1] = -p->phi_max[i] + 2.0 * p->phi_max[i] * ora_u24(w[1]);
+                c[2] = -p->gamma_max[i] + 2.0 * p->gamma_max[i] * ora_u24(w[2]);
+            }
+}
+
+/* MH accept/reject on the joint log2 weight (R1). */
+int ora_mh_accept(double lam_cur, double lam_prop, uint32_t l, uint32_t k, uint64_t seed, uint32_t mpc)
+{
+    if (lam_cur == -INFINITY) return 1;
+    if (lam_prop == -INFINITY) return 0;
+    double delta = lam_prop - lam_cur;
+    if (delta >= 0.0) return 1;
+    uint64_t r = ora_r64(TAG_MH, l, k, seed, mpc);
+    double u53 = (double)(r >> 11) * 0x1.0p-53;
+    return u53 < ora_det_exp2(delta);
+}
+
+/* Systematic resampling of one aircraft column (K96; R25):
+ * slot j takes min{ l : C_l > floor((j Q + R) / L) }. */
+int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
+                        uint64_t seed, uint32_t mpc, int32_t *anc,
+                        uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out)
+{
+    double m = -INFINITY;
+    for (uint32_t l = 0; l < L; ++l) if (ell[l] > m) m = ell[l];
+    int infeasible = (m == -INFINITY);
+    uint64_t *C = (uint64_t *)malloc(sizeof(uint64_t) * (L ? L : 1));
+    uint64_t acc = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+        uint64_t q = infeasible ? 1 : ora_det_quant(ell[l] - m);
+        if (q_out) q_out[l] = q;
+        acc += q;
+        C[l] = acc;
+    }
+    uint64_t Q = acc;
+    uint64_t r = ora_r64(TAG_RESAMPLE, i, k, seed, mpc);
+    uint64_t R = (uint64_t)(((unsigned __int128)r * (unsigned __int128)Q) >> 64);
+    for (uint32_t j = 0; j < L; ++j) {
+        unsigned __int128 num = (unsigned __int128)j * Q + R;
+        uint64_t tj = (uint64_t)(num / L);
+        /* plain linear search keeps the definition visible; bisection is equivalent */
+        uint32_t lo = 0, hi = L - 1;
+        while (lo < hi) {
+            uint32_t mid = lo + (hi - lo) / 2;
+            if (C[mid] > tj) hi = mid; else lo = mid + 1;
+        }
+        anc[j] = (int32_t)lo;
+    }
+    if (Q_out) *Q_out = Q;
+    if (R_out) *R_out = R;
+    free(C);
+    return infeasible;
+}
+
+/* Alg.1 l.23: controls + Gaussian white noise, sigma per
+ * component; optional clamp to the envelope (R16). */
+void ora_perturb_row(const ora_problem *p, int i, const double *parent_row, double *out_row,
+                     uint32_t l, uint32_t k, uint64_t seed, uint32_t mpc,
+                     const double sigma[3], int clamp)
+{
+    for (int t = 0; t < p->H; ++t) {
+        uint32_t w[4];
+        draw(TAG_PERTURB, l, k << 16, (uint32_t)t | ((uint32_t)i << 8), mpc, seed, w);
+        double z[4];
+        ora_box_muller(w[0], w[1], &z[0], &z[1]);
+        ora_box_muller(w[2], w[3], &z[2], &z[3]);
+        for (int c = 0; c < 3; ++c) {
+            double v = parent_row[3 * t + c] + sigma[c] * z[c];
+            if (clamp) {
+                double lo = c == 0 ? p->T_min[i] : (c == 1 ? -p->phi_max[i] : -p->gamma_max[i]);
+                double hi = c == 0 ? p->T_max[i] : (c == 1 ? p->phi_max[i] : p->gamma_max[i]);
+                if (v < lo) v = lo;
+                if (v > hi) v = hi;
+            }
+            out_row[3 * t + c] = v;
+        }
+    }
+}
+
+/* argmax_l prod_i W_il; a zero weight disqualifies; ties -> lowest l (R27). */
+int64_t ora_select(const double *lam, uint32_t L)
+{
+    int64_t best = -1;
+    for (uint32_t l = 0; l < L; ++l) {
+        if (lam[l] == -INFINITY) continue;
+        if (best < 0 || lam[l] > lam[best]) best = l;
+    }
+    return best;
+}
+
+static double lambda_of(const double *ell_row, int n)
+{
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += ell_row[i];
+    return s;
+}
+
+/* Algorithm 1 with the MH move of R1. */
+int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
+                double *best_lambda, int64_t *best_index, double *stats)
+{
+    ora_derived d;
+    if (ora_derive(p, &d) != 0) return -1;
+    const uint32_t L = cfg->L;
+    const int n = p->n, H = p->H;
+    const size_t row = (size_t)n * H * 3;
+    double *cur = (double *)calloc(L * row + 1, sizeof(double));   /* x'  */
+    double *prop = (double *)calloc(L * row + 1, sizeof(double));  /* x*  */
+    double *surv = (double *)calloc(L * row + 1, sizeof(double));
+    double *ell_c = (double *)malloc(sizeof(double) * (L * (size_t)n + 1));
+    double *ell_p = (double *)malloc(sizeof(double) * (L * (size_t)n + 1));
+    double *ell_s = (double *)malloc(sizeof(double) * (L * (size_t)n + 1));
+    double *lam = (double *)malloc(sizeof(double) * (L + 1));
+    double *col = (double *)malloc(sizeof(double) * (L + 1));
+    int32_t *anc = (int32_t *)malloc(sizeof(int32_t) * ((size_t)L * n + 1));
+    const double ell0 = -log2((double)L);
+
+    ora_init_population(p, L, cfg->seed, cfg->mpc, cur);           /* Alg.1 l.1-5 */
+    for (uint32_t k = 0; k < cfg->K; ++k) {
+        uint32_t S = cfg->sched_paper ? (uint32_t)ora_sample_schedule((int)k) : cfg->S;
+        uint64_t accepted = 0;
+        if (k == 0) {
+            for (size_t e = 0; e < L * (size_t)n; ++e) ell_s[e] = ell0;
+            ora_evaluate(p, &d, cur, L, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
+            memcpy(surv, cur, sizeof(double) * L * row);
+        } else if (!cfg->mh) {                                      /* paper-literal: x* replaces x' */
+            for (size_t e = 0; e < L * (size_t)n; ++e) ell_s[e] = ell0;
+            ora_evaluate(p, &d, prop, L, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
+            memcpy(surv, prop, sizeof(double) * L * row);
+            accepted = L;
+        } else {
+            for (size_t e = 0; e < L * (size_t)n; ++e) { ell_c[e] = ell0; ell_p[e] = ell0; }
+            ora_evaluate(p, &d, cur, L, S, k, cfg->seed, cfg->mpc, ell_c, cfg->nthreads);
+            ora_evaluate(p, &d, prop, L, S, k, cfg->seed, cfg->mpc, ell_p, cfg->nthreads);
+            for (uint32_t l = 0; l < L; ++l) {
+                double lc = lambda_of(&ell_c[(size_t)l * n], n);
+                double lp = lambda_of(&ell_p[(size_t)l * n], n);
+                int acc = ora_mh_accept(lc, lp, l, k, cfg->seed, cfg->mpc);
+                accepted += acc;
+                const double *src = acc ? &prop[l * row] : &cur[l * row];
+                memcpy(&surv[l * row], src, sizeof(double) * row);
+                memcpy(&ell_s[(size_t)l * n], acc ? &ell_p[(size_t)l * n] : &ell_c[(size_t)l * n], sizeof(double) * n);
+            }
+        }
+        for (uint32_t l = 0; l < L; ++l) lam[l] = lambda_of(&ell_s[(size_t)l * n], n);
+        double ess_min = INFINITY;
+        int n_inf = 0;
+        if (k + 1 < cfg->K) {
+            /* Alg.1 l.22: per-aircraft resampling */
+            for (int i = 0; i < n; ++i) {
+                for (uint32_t l = 0; l < L; ++l) col[l] = ell_s[(size_t)l * n + i];
+                n_inf += ora_resample_column(col, L, (uint32_t)i, k, cfg->seed, cfg->mpc,
+                                             &anc[(size_t)i * L], NULL, NULL, NULL);
+            }
+            /* recombine and perturb (Alg.1 l.23); weights reset happens at evaluation */
+            double sig[3];
+            double f = pow(cfg->anneal, (double)k);
+            for (int c = 0; c < 3; ++c) sig[c] = cfg->sigma[c] * f;
+            for (uint32_t j = 0; j < L; ++j)
+                for (int i = 0; i < n; ++i) {
+                    int32_t a = anc[(size_t)i * L + j];
+                    const double *src = &surv[(size_t)a * row + (size_t)i * H * 3];
+                    double *dst = &cur[(size_t)j * row + (size_t)i * H * 3];
+                    memcpy(dst, src, sizeof(double) * H * 3);
+                    ora_perturb_row(p, i, dst, &prop[(size_t)j * row + (size_t)i * H * 3],
+                                    j, k, cfg->seed, cfg->mpc, sig, (int)cfg->clamp);
+                }
+        }
+        for (int i = 0; i < n; ++i) {
+            double mx = -INFINITY, s1 = 0.0, s2 = 0.0;
+            for (uint32_t l = 0; l < L; ++l) if (ell_s[(size_t)l * n + i] > mx) mx = ell_s[(size_t)l * n + i];
+            if (mx == -INFINITY) { ess_min = 0.0; continue; }
+            for (uint32_t l = 0; l < L; ++l) {
+                double w = exp2(ell_s[(size_t)l * n + i] - mx);
+                s1 += w; s2 += w * w;
+            }
+            double ess = s1 * s1 / s2;
+            if (ess < ess_min) ess_min = ess;
+        }
+        if (stats) {
+            int64_t b = ora_select(lam, L);
+            stats[4 * k + 0] = b >= 0 ? lam[b] : -INFINITY;
+            stats[4 * k + 1] = k == 0 ? 1.0 : (double)accepted / (double)L;
+            stats[4 * k + 2] = ess_min;
+            stats[4 * k + 3] = (double)n_inf;
+        }
+    }
+    int64_t b = ora_select(lam, L);                                  /* Alg.1 l.27 */
+    if (best_index) *best_index = b;
+    if (best_lambda) *best_lambda = b >= 0 ? lam[b] : -INFINITY;
+    if (best_ctrl && b >= 0) memcpy(best_ctrl, &surv[(size_t)b * row], sizeof(double) * row);
+    free(cur); free(prop); free(surv); free(ell_c); free(ell_p); free(ell_s);
+    free(lam); free(col); free(anc);
+    ora_free_derived(&d);
+    return b >= 0 ? 0 : 2;
+}
+
+/* MPC apply: first control of the winner, realised wind (PLANT streams). */
+void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *states,
+                    const double *u0, uint64_t seed, uint32_t mpc, double *Zplant,
+                    int32_t *zinit, double *next, int32_t *flags)
+{
+    double v[16], W[2][8];
+    for (int blk = 0; blk < 4; ++blk) {
+        uint32_t w[4];
+        draw(TAG_PLANT_WIND, 0, 0, (uint32_t)blk << 16, mpc, seed, w);
+        ora_box_muller(w[0], w[1], &v[4 * blk + 0], &v[4 * blk + 1]);
+        ora_box_muller(w[2], w[3], &v[4 * blk + 2], &v[4 * blk + 3]);
+    }
+    for (int e = 0; e < 16; ++e) Zplant[e] = *zinit ? d->a * Zplant[e] + d->b * v[e] : v[e];
+    *zinit = 1;
+    for (int c = 0; c < 2; ++c)
+        for (int r = 0; r < 8; ++r) {
+            double acc = 0.0;
+            for (int m = 0; m < 8; ++m) acc += d->Qhat[r * 8 + m] * Zplant[8 * c + m];
+            W[c][r] = acc;
+        }
+    for (int i = 0; i < p->n; ++i) {
+        const double *st = &states[6 * i];
+        flags[i] = 0;
+        if (p->first_step[i] != 0) { memcpy(&next[6 * i], st, 6 * sizeof(double)); continue; }
+        double wind[2];
+        ora_trilinear(p, W[0], st, &wind[0]);
+        ora_trilinear(p, W[1], st, &wind[1]);
+        wind[0] += p->nominal[0];
+        wind[1] += p->nominal[1];
+        if (p->turb_sigma > 0.0) {
+            uint32_t w[4];
+            double g0, g1;
+            draw(TAG_PLANT_TURB, 0, 0, (uint32_t)i << 8, mpc, seed, w);
+            ora_box_muller(w[0], w[1], &g0, &g1);
+            wind[0] += p->turb_sigma * g0;
+            wind[1] += p->turb_sigma * g1;
+        }
+        ora_step(p, i, st, &u0[3 * i], wind, &next[6 * i]);
+        const double *nx = &next[6 * i];
+        if (p->kind[i] == 0 && ora_landed(p, nx)) flags[i] |= 1;
+        if (p->kind[i] == 1 && sqrt(nx[0] * nx[0] + nx[1] * nx[1]) >= p->tma_radius) flags[i] |= 2;
+        if (ora_unary_violation(p, i, &u0[3 * i], nx)) flags[i] |= 4;
+    }
+}

@@ -1,0 +1,342 @@
+"""Pins for the oracle's models: dynamics (Eq. hor), wind (Eq. cov + AR(1)),
+constraints, flow field / descent angle (Eq. flow) and objectives.
+
+Each check pins the oracle to the paper or to mathematics: closed forms of the
+difference equations, library factorisations, numerically integrated curves,
+brute force on hand-built scenarios and the paper's printed anchors.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1506_02869_b200 import scenarios as sc
+
+DEG = math.pi / 180.0
+
+
+def _calm(scn):
+    """No wind at all: zero random field, no nominal wind, no gusts."""
+    scn = dict(scn)
+    scn.update(sigma_lo=0.0, sigma_hi=0.0, nominal=[0.0, 0.0], turb_sigma=0.0)
+    return scn
+
+
+@pytest.fixture(scope="module")
+def one_dep(ora):
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    scn["density_mode"] = 1
+    return ora.Problem(scn)
+
+
+# ---------------------------------------------------------------- dynamics
+def test_lift_at_zero_bank(ora, one_dep):
+    """L = m g = 588 600 N at phi = 0, m = 60 000 kg."""
+    L, D = one_dep.lift_drag(0, [0, 0, 1000, 100, 0, 60000], 0.0)
+    assert L == pytest.approx(588600.0, rel=1e-15)
+    L2, D2 = one_dep.lift_drag(0, [0, 0, 1000, 100, 0, 60000], 0.3)
+    L3, D3 = one_dep.lift_drag(0, [0, 0, 1000, 100, 0, 60000], -0.3)
+    assert (L2, D2) == (L3, D3)                                  # even in phi
+    assert L2 == pytest.approx(588600.0 / math.cos(0.3), rel=1e-15)
+
+
+def test_drag_hand_value(ora, one_dep):
+    """Parabolic polar at rho=1.225, v=100, S=122.6, CD0=0.024, CD2=0.0375,
+    m=60000, phi=0: q = 750925 N, C_L = 588600/750925,
+    D = q (0.024 + 0.0375 C_L^2) = 35 323.3599... N (exact rational evaluation)."""
+    q = 0.5 * 1.225 * 100.0 ** 2 * 122.6
+    assert q == 750925.0
+    _, D = one_dep.lift_drag(0, [0, 0, 0, 100, 0, 60000], 0.0)
+    assert D == pytest.approx(35323.359902786564, rel=1e-12)
+
+
+def test_trimmed_level_flight(ora, one_dep):
+    """gamma = phi = 0, T_k = D_k: v constant, x_k = x_0 + k dt v cos(chi),
+    y, z unchanged, m_k = m_0 - dt eta sum_k T_k (Eq. hor)."""
+    st = np.array([1000.0, -2000.0, 3000.0, 130.0, 0.7, 65000.0])
+    x0 = st.copy()
+    fuel = 0.0
+    for k in range(1, 8):
+        _, D = one_dep.lift_drag(0, st, 0.0)
+        st = one_dep.step(0, st, [D, 0.0, 0.0])
+        fuel += 10.0 * 1.0e-5 * D
+        assert st[3] == pytest.approx(130.0, abs=1e-9)
+        assert st[0] == pytest.approx(x0[0] + k * 10.0 * 130.0 * math.cos(0.7), abs=1e-7)
+        assert st[1] == pytest.approx(x0[1] + k * 10.0 * 130.0 * math.sin(0.7), abs=1e-7)
+        assert st[2] == x0[2] and st[4] == x0[4]
+        assert st[5] == pytest.approx(x0[5] - fuel, abs=1e-9)
+
+
+def test_zero_thrust_keeps_mass(ora, one_dep):
+    st = one_dep.step(0, [0, 0, 3000, 130, 0.3, 65000], [0.0, 0.1, 0.02])
+    assert st[5] == 65000.0
+
+
+def test_constant_descent(ora, one_dep):
+    """gamma = -3 deg, T_k = D_k + m g sin(gamma): v constant, z linear, m exact."""
+    g = -3.0 * DEG
+    st = np.array([0.0, 0.0, 3000.0, 120.0, 0.0, 64000.0])
+    m0 = st[5]
+    fuel = 0.0
+    for k in range(1, 6):
+        _, D = one_dep.lift_drag(0, st, 0.0)
+        T = D + st[5] * 9.81 * math.sin(g)
+        st = one_dep.step(0, st, [T, 0.0, g])
+        fuel += 10.0 * 1e-5 * T
+        assert st[3] == pytest.approx(120.0, abs=1e-9)
+        assert st[2] == pytest.approx(3000.0 + k * 10.0 * 120.0 * math.sin(g), abs=1e-8)
+        assert st[0] == pytest.approx(k * 10.0 * 120.0 * math.cos(g), abs=1e-8)
+        assert st[5] == pytest.approx(m0 - fuel, abs=1e-9)
+
+
+def test_coordinated_turn_rate(ora, one_dep):
+    """Level turn at constant v: chi_k = chi_0 + k dt g tan(phi)/v (mass-free)."""
+    phi = 25.0 * DEG
+    st = np.array([0.0, 0.0, 2000.0, 120.0, 0.1, 64000.0])
+    for k in range(1, 6):
+        _, D = one_dep.lift_drag(0, st, phi)
+        st = one_dep.step(0, st, [D, phi, 0.0])
+        assert st[4] == pytest.approx(0.1 + k * 10.0 * 9.81 * math.tan(phi) / 120.0, abs=1e-12)
+    assert 10.0 * 9.81 * math.tan(phi) / 120.0 / DEG == pytest.approx(21.84, abs=0.01)
+
+
+def test_wind_offset_and_ground_speed(ora, one_dep):
+    """Eq. hor a,b: the wind adds w dt; |ground - wind| = v cos(gamma)."""
+    st = np.array([0.0, 0.0, 2000.0, 110.0, 1.1, 64000.0])
+    u = [40000.0, 0.1, 0.05]
+    a = one_dep.step(0, st, u, (0.0, 0.0))
+    b = one_dep.step(0, st, u, (7.0, -3.0))
+    assert b[0] - a[0] == pytest.approx(70.0, abs=1e-9)
+    assert b[1] - a[1] == pytest.approx(-30.0, abs=1e-9)
+    assert np.all(a[2:] == b[2:])
+    gs = math.hypot((b[0] - st[0]) / 10.0 - 7.0, (b[1] - st[1]) / 10.0 + 3.0)
+    assert gs == pytest.approx(110.0 * math.cos(0.05), rel=1e-12)
+
+
+def test_isa_density_mode(ora):
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    P = ora.Problem(scn)
+    # sea level ISA gives the constant-density drag
+    scn2 = dict(scn); scn2["density_mode"] = 1
+    P2 = ora.Problem(scn2)
+    assert P.lift_drag(0, [0, 0, 0, 100, 0, 60000], 0.0) == P2.lift_drag(0, [0, 0, 0, 100, 0, 60000], 0.0)
+    # drag decreases with altitude at fixed v (thinner air, P:255 'standard relations')
+    d = [P.lift_drag(0, [0, 0, z, 200, 0, 60000], 0.0)[1] for z in (0, 4000, 8000)]
+    assert d[0] > d[1] > d[2]
+
+
+# ---------------------------------------------------------------- wind model
+def test_covariance_and_cholesky(ora):
+    scn = sc.base_scenario()
+    scn = sc._finish(scn, [sc._departure_snapshot(0)])
+    P = ora.Problem(scn)
+    R, Q = P.Rhat, P.Qhat
+    # Eq. cov at the same point: sigma(z)^2; symmetric; decays with distance
+    sig = np.array([1.5, 1.5, 1.5, 1.5, 4.0, 4.0, 4.0, 4.0])
+    assert np.allclose(np.diag(R), sig ** 2, rtol=1e-15)
+    assert np.allclose(R, R.T, rtol=0, atol=0)
+    assert R[0, 1] == pytest.approx(1.5 * 1.5 * math.exp(-1.6e-6 * 60000.0), rel=1e-14)
+    assert R[0, 3] == pytest.approx(2.25 * math.exp(-1.6e-6 * 60000.0 * math.sqrt(2)), rel=1e-14)
+    assert R[0, 4] == pytest.approx(1.5 * 4.0 * math.exp(-1.5e-5 * 12000.0), rel=1e-14)
+    # Qhat Qhat^T = Rhat, lower triangular, equals LAPACK's factor
+    assert np.allclose(Q @ Q.T, R, rtol=0, atol=1e-12)
+    assert np.all(np.triu(Q, 1) == 0.0)
+    assert np.allclose(Q, np.linalg.cholesky(R), rtol=0, atol=1e-12)
+    a, b = P.ab
+    assert a == pytest.approx(math.exp(-6e-6 * 10.0), rel=1e-15)
+    # Q Q^T = (1-a^2) Rhat with Q = b Qhat
+    assert np.allclose((b * Q) @ (b * Q).T, (1 - a * a) * R, rtol=0, atol=1e-15)
+
+
+def test_trilinear_nodes_linear_fields_clamp(ora):
+    scn = sc._finish(sc.base_scenario(), [sc._departure_snapshot(0)])
+    P = ora.Problem(scn)
+    lo, hi = np.array(scn["wind_lo"]), np.array(scn["wind_hi"])
+    rng = np.random.default_rng(5)
+    W = rng.normal(size=8)
+    for n in range(8):
+        pos = [hi[a] if (n >> a) & 1 else lo[a] for a in range(3)]
+        assert P.trilinear(W, pos) == pytest.approx(W[n], abs=1e-15)
+    c = rng.normal(size=4)
+    lin = lambda p: c[0] + c[1] * p[0] / 1e4 + c[2] * p[1] / 1e4 + c[3] * p[2] / 1e4
+    Wl = [lin([hi[a] if (n >> a) & 1 else lo[a] for a in range(3)]) for n in range(8)]
+    for _ in range(50):
+        p = rng.uniform(lo, hi)
+        assert P.trilinear(Wl, p) == pytest.approx(lin(p), abs=1e-12)
+    # outside the box: clamped to the boundary value
+    assert P.trilinear(Wl, [1e6, 0.0, 5000.0]) == pytest.approx(lin([hi[0], 0.0, 5000.0]), abs=1e-12)
+
+
+def test_wind_field_statistics(ora):
+    """Stationary N(0, Rhat) field: sample covariance of W(0) over many
+    (particle, sample) draws matches Rhat within 5% of max|Rhat|."""
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    scn.update(sigma_lo=1.5, sigma_hi=4.0)
+    scn["x0"][0] = [-30000.0, -30000.0, 0.0, 130.0, 0.0, 70000.0]      # sits on node 0
+    P = ora.Problem(scn)
+    # a zero-thrust 1-step rollout exposes the node-0 wind through x1 - x0 - v dt cos
+    u = np.zeros((1, P.H, 3))
+    vals = []
+    for l in range(4000):
+        tr = P.rollout(u, l, 0, 0, 77)["traj"][0]
+        vals.append((tr[1, 0] - tr[0, 0] - 10 * 130.0) / 10.0)
+    vals = np.array(vals)
+    assert vals.mean() == pytest.approx(0.0, abs=4 * 1.5 / math.sqrt(len(vals)))
+    assert vals.var() == pytest.approx(1.5 ** 2, rel=0.08)
+
+
+# ---------------------------------------------------------------- constraints
+def test_envelope_boundaries(ora, one_dep):
+    P = one_dep
+    st = [0, 0, 3000, 130, 0, 65000]
+    assert not P.unary_violation(0, [60000, 0.1, 0.01], st)
+    assert P.unary_violation(0, [60000, 30 * DEG, 0.0], st)          # |phi| < phi_max strict
+    assert P.unary_violation(0, [60000, -30 * DEG, 0.0], st)
+    assert not P.unary_violation(0, [1.2e5, 0.0, 6 * DEG], st)      # T = T_max, gamma = gamma_max inclusive
+    assert P.unary_violation(0, [1.2e5 + 1, 0.0, 0.0], st)
+    assert P.unary_violation(0, [-1, 0.0, 0.0], st)
+    assert not P.unary_violation(0, [0, 0, 0], [0, 0, 12000, 180, 0, 58000])   # inclusive bounds
+    assert P.unary_violation(0, [0, 0, 0], [0, 0, 12000.01, 180, 0, 58000])
+    assert P.unary_violation(0, [0, 0, 0], [0, 0, 100, 69.99, 0, 65000])
+    assert P.unary_violation(0, [0, 0, 0], [0, 0, 100, 100, 0, 57999.99])      # m >= m_empty
+    assert P.unary_violation(0, [0, 0, 0], [0, 0, float("nan"), 100, 0, 65000])
+
+
+def test_separation_boundaries(ora, one_dep):
+    P = one_dep
+    a = np.array([0, 0, 3000, 100, 0, 1])
+    assert not P.pair_conflict(a, a + [5000, 0, 0, 0, 0, 0])       # exactly 2 P_r
+    assert P.pair_conflict(a, a + [4999.9, 0, 0, 0, 0, 0])
+    assert P.pair_conflict(a, a)                                     # co-located
+    assert not P.pair_conflict(a, a + [0, 0, 600, 0, 0, 0])        # |dz| = 2 P_h
+    assert P.pair_conflict(a, a + [3000, 3000, 599, 0, 0, 0])
+    rng = np.random.default_rng(6)
+    for _ in range(200):
+        b = a + np.r_[rng.uniform(-8000, 8000, 2), rng.uniform(-900, 900), 0, 0, 0]
+        assert P.pair_conflict(a, b) == P.pair_conflict(b, a)      # symmetric
+
+
+def test_landing_sector(ora, one_dep):
+    P = one_dep
+    on = [2000.0, 0.0, 2000.0 * math.tan(3 * DEG), 75.0, math.pi, 64000.0]
+    assert P.landed(on)
+    assert not P.landed([*on[:4], 0.0, 64000.0])                    # flying away
+    assert P.landed([*on[:4], math.pi + 14.9999 * DEG, 64000.0])     # heading bound
+    assert not P.landed([*on[:4], math.pi + 15.01 * DEG, 64000.0])
+    assert P.landed([*on[:3], 80.0, *on[4:]])                       # v = P_vs inclusive
+    assert not P.landed([*on[:3], 80.01, *on[4:]])
+    assert not P.landed([-2000.0, 0.0, 100.0, 75.0, math.pi, 64000.0])   # west of runway (R10)
+    assert not P.landed([4100.0, 0.0, 100.0, 75.0, math.pi, 64000.0])    # beyond P_runway
+    assert not P.landed([2000.0, 0.0, 2000 * math.tan(6.5 * DEG), 75.0, math.pi, 64000.0])  # too high
+    # monotone in v_s
+    for v in np.linspace(60, 80, 9):
+        assert P.landed([*on[:3], v, *on[4:]])
+
+
+# ---------------------------------------------------------------- flow field
+def test_flow_field_special_points(ora):
+    w = lambda a: a % (2 * math.pi)
+    assert w(ora.flow_heading(5000, 0)) == pytest.approx(math.pi)          # east of runway: head West
+    assert w(ora.flow_heading(0, 5000)) == pytest.approx(0.0, abs=1e-12)   # north: head East
+    assert w(ora.flow_heading(-5000, 0)) == pytest.approx(math.pi)         # due West: long diversion
+    assert w(ora.flow_heading(3000, 3000)) == pytest.approx(1.5 * math.pi)  # x = y > 0: head South
+
+
+def _follow(ora, x, y, h=5.0):
+    """Integrate dx/ds = (cos chi_hat, sin chi_hat) until within 50 m of the origin."""
+    s = 0.0
+    for _ in range(200000):
+        r = math.hypot(x, y)
+        if r < 50.0:
+            return s + r, ora.flow_heading(x, y)
+        c = ora.flow_heading(x, y)
+        # midpoint (RK2) step
+        xm, ym = x + 0.5 * h * math.cos(c), y + 0.5 * h * math.sin(c)
+        cm = ora.flow_heading(xm, ym)
+        x, y, s = x + h * math.cos(cm), y + h * math.sin(cm), s + h
+    raise AssertionError("did not converge")
+
+
+@pytest.mark.parametrize("start", [(20000, 5000), (10000, 15000), (-5000, 20000), (8000, -12000), (-15000, -9000)])
+def test_flow_field_reaches_runway_heading_west_and_arc_length(ora, start):
+    """Following chi_hat reaches the origin on the east side heading West,
+    and the distance flown equals the arc length used in beta (R9)."""
+    s_num, chi_end = _follow(ora, *start)
+    assert ora.angdist(chi_end - math.pi) < 0.05
+    assert s_num == pytest.approx(ora.arc_length(*start), rel=2e-3)
+
+
+def test_beta_limits(ora):
+    assert ora.beta(12000, 5000, 0.0) == 0.0
+    assert ora.beta(10000, 0, 10000 * math.tan(0.05)) == pytest.approx(0.05, rel=1e-12)
+    assert ora.arc_length(10000, 0) == 10000
+    assert ora.arc_length(0, 10000) == pytest.approx(10000 * math.pi / 2, rel=1e-12)   # quarter circle x2
+
+
+# ---------------------------------------------------------------- objectives
+def _radial_departure(ora, theta_F, bearing, H=6):
+    scn = _calm(sc.snapshot(0, 1, seed=1, H=H))
+    scn["x0"][0] = [5000 * math.cos(bearing), 5000 * math.sin(bearing), 1000.0, 150.0, bearing, 70000.0]
+    scn["theta_F"][0] = theta_F
+    return ora.Problem(scn)
+
+
+def test_departure_bearing_anchors(ora):
+    """on-bearing every step -> J1 = 1; 90 deg off every step -> 0.5."""
+    b = 30 * DEG
+    P = _radial_departure(ora, b, b)
+    u = np.zeros((1, 6, 3))
+    u[..., 0] = 38000.0
+    r = P.rollout(u, 0, 0, 0, 1)
+    assert r["comp"][0, 0] == pytest.approx(1.0, abs=1e-12)
+    P = _radial_departure(ora, b + 90 * DEG, b)
+    r = P.rollout(u, 0, 0, 0, 1)
+    assert r["comp"][0, 0] == pytest.approx(0.5, abs=1e-12)
+
+
+def test_fuel_term_zero_fuel_and_full_thrust(ora):
+    P = _radial_departure(ora, 0.0, 0.0)
+    u = np.zeros((1, 6, 3))
+    r = P.rollout(u, 0, 0, 0, 1)
+    assert r["comp"][0, 1] == 1.0 and r["fuel"][0] == 0.0
+    P1 = _radial_departure(ora, 0.0, 0.0, H=1)
+    u1 = np.zeros((1, 1, 3)); u1[..., 0] = 1.2e5
+    r = P1.rollout(u1, 0, 0, 0, 1)
+    assert not r["viol"][0]
+    assert r["comp"][0, 1] == pytest.approx(0.0, abs=1e-12)         # T_max over the whole horizon
+    assert r["fuel"][0] == pytest.approx(10 * 1e-5 * 1.2e5, rel=1e-14)
+
+
+def test_noise_term_and_popdense(ora):
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    scn["centres"] = np.array([[5000.0, 0.0, 1500.0]])
+    scn.update(noise_w=0.2, pop_nx=41, pop_ny=41, pop_x0=-20000.0, pop_y0=-20000.0, pop_dx=1000.0)
+    P = ora.Problem(scn)
+    assert P.popdense(5000, 0, grid=False) == pytest.approx(0.2659615202676218, rel=1e-14)  # P:1133, c = 1.5 km
+    assert P.popdense(5000, 0, grid=True) == pytest.approx(0.2659615202676218, rel=1e-14)   # on a grid node
+    assert P.popdense(40000, 40000, grid=False) < 1e-30
+    scn2 = dict(scn); scn2["centres"] = np.array([[0.0, 0.0, 300.0]])
+    assert ora.Problem(scn2).popdense(0, 0, grid=False) == 1.0      # clipped at 1
+    g = P.pop_grid()
+    assert g.shape == (41, 41) and g.max() <= 1.0 and g.min() >= 0.0
+    # J_noise = 1 above A_c regardless of density: a level departure at
+    # 5000 m over the centre has mean noise term 1 -> J = 0.8 J^D + 0.2
+    scn3 = dict(scn)
+    scn3["x0"] = np.array([[3000.0, 0.0, 5000.0, 150.0, 0.0, 70000.0]])
+    P3 = ora.Problem(scn3)
+    u = np.zeros((1, 6, 3)); u[..., 0] = 50000.0
+    r = P3.rollout(u, 0, 0, 0, 1)
+    a = np.array(scn["alpha_dep"])
+    JD = float(a @ r["comp"][0])
+    assert r["J"][0] == pytest.approx(0.8 * JD + 0.2, abs=1e-12)
+
+
+def test_costs_in_unit_interval(ora):
+    """Every component and total in [0,1]."""
+    scn, _ = sc.config(2)
+    P = ora.Problem(scn)
+    ctrl = sc.random_controls(scn, 300, seed=9, spread=1.3)
+    for l in range(300):
+        r = P.rollout(ctrl[l], l, 0, 0, 3)
+        assert np.all((r["J"] >= 0) & (r["J"] <= 1))
+        assert np.all((r["comp"] >= 0) & (r["comp"] <= 1))
