@@ -1,0 +1,317 @@
+#!/usr/bin/env python3
+"""Benchmark of the SMC-in-MPC hot path on B200 (contract: see DESIGN.md section 8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl smcatm|reference]
+                    [--config 2] [--no-cpu-baseline]
+
+A step is one MPC update of BASELINE.json's configs[1] workload (c2: 8
+aircraft, L = 16384 particles, S = 16 wind samples, K = 101 SMC rounds): fresh
+population, K rounds of rollout + MH + reduce + systematic resampling +
+proposal, final selection and the plant step -- every row of SURVEY.md 8(a).
+`value` is aircraft-step rollouts per second over the whole job (device
+time, inputs resident); `e2e` is the same metric through the public C ABI
+call mpc_step() with pinned host buffers, host<->device copies inside the
+timed region.  N > 1 (torchrun): each rank solves its own MPC problem
+(weak scaling, no data-path collective) -- see DESIGN.md section 9.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "aircraft-step rollouts/sec (MPC-step latency reported alongside)"
+UNIT = "aircraft-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="smcatm", choices=["smcatm", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if len(r) > 5 + j and "Active" in r[5 + j]
+                          and "Not" not in r[5 + j]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic(cfgname):
+    """dram bytes per K2 launch from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfgname)
+    except Exception:
+        return None
+
+
+def cpu_baseline(scn, cfg, seconds=12.0):
+    """The FP64 oracle, as it stands, on this host's cores: evaluation (Alg.1
+    l.9-18) of a bounded particle sample of the same workload, repeated for
+    ~`seconds`.  Returns aircraft-steps/s and the sample description."""
+    import numpy as np
+
+    import oracle as O
+    P = O.Problem(scn)
+    nthreads = os.cpu_count() or 1
+    Lp = min(cfg.L, 2048)
+    ctrl = P.init_population(Lp, cfg.seed)
+    Ha = int(sum(scn["H"] - e for e in scn["first_step"]))
+    done, t0 = 0, time.perf_counter()
+    k = 0
+    while True:
+        P.evaluate(ctrl, cfg.S, k + 1, cfg.seed, nthreads=nthreads)
+        done += Lp * cfg.S * Ha
+        k += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return done / el, nthreads, f"oracle evaluate of {Lp} particles x S={cfg.S} x {Ha} aircraft-steps, {k} reps, {el:.1f}s"
+
+
+def run_reference(args):
+    """--impl reference: the FP64 oracle timed on the host cores (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1506_02869_b200 import roofline, scenarios as sc
+    scn, cfg = sc.config(args.config)
+    import oracle as O
+    P = O.Problem(scn)
+    nthreads = os.cpu_count() or 1
+    Lp = min(cfg.L, 2048)
+    ctrl = P.init_population(Lp, cfg.seed)
+    Ha = int(sum(scn["H"] - e for e in scn["first_step"]))
+    per_step = Lp * cfg.S * Ha
+    for w in range(args.warmup):
+        P.evaluate(ctrl, cfg.S, 1, cfg.seed, nthreads=nthreads)
+    ts = []
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        P.evaluate(ctrl, cfg.S, 1 + s, cfg.seed, nthreads=nthreads)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    value = per_step * args.steps / tot
+    steps_full = roofline.aircraft_steps(scn, cfg.L, [cfg.S] * cfg.K, cfg.mh)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {scn['n']} aircraft, L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K}",
+                   "sample": f"one evaluation round of {Lp} particles per step"},
+        "mpc_step_latency_ms_extrapolated": 1000 * steps_full / value,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                         "sample": f"oracle evaluate of {Lp} particles x S={cfg.S} per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_02869_b200 import roofline, scenarios as sc, smcatm
+
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    scn, cfg = sc.config(args.config)
+    stream = torch.cuda.Stream(device=local)
+    sol = smcatm.Solver(scn, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed + rank,
+                        anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True)
+    S_list = [cfg.S] * cfg.K
+    ac_steps = roofline.aircraft_steps(scn, cfg.L, S_list, cfg.mh)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            sol.solve()
+        barrier()
+        sol.phase_times()                                   # reset phase accumulators
+        n0 = sol.launches
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            barrier()
+            for s in range(args.steps):
+                flush.fill_(s & 0xFF)                       # L2 flush between timed steps (outside events)
+                evs[s][0].record(stream)
+                sol.solve()
+                evs[s][1].record(stream)
+            barrier()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        launches = sol.launches - n0
+        phases = sol.phase_times()
+    tot_ms = sum(step_ms)
+    t_local = torch.tensor([tot_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    tmax_ms = float(t_local.item())
+    value = ac_steps * args.steps * world / (tmax_ms / 1000.0)
+
+    # ---- e2e: public C ABI mpc_step with pinned host buffers, copies inside the timed region
+    n = scn["n"]
+    meas = torch.from_numpy(np.ascontiguousarray(scn["x0"], dtype=np.float64)).pin_memory()
+    applied = torch.empty((n, 3), dtype=torch.float32).pin_memory()
+    nxt = torch.empty((n, 6), dtype=torch.float64).pin_memory()
+    flags = torch.empty((n,), dtype=torch.int32).pin_memory()
+    e2e_ms = []
+    with torch.cuda.stream(stream):
+        sol.mpc_step_ptr(meas.data_ptr(), applied.data_ptr(), nxt.data_ptr(), flags.data_ptr())   # warm
+        barrier()
+        for s in range(args.e2e_steps):
+            flush.fill_(s & 0xFF)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sol.mpc_step_ptr(meas.data_ptr(), applied.data_ptr(), nxt.data_ptr(), flags.data_ptr())
+            b.record(stream)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+        sol.phase_times()
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = ac_steps * args.e2e_steps * world / (float(e2e_t.item()) / 1000.0)
+    h2d = n * 6 * 8 + n * 156      # measured states + per-aircraft constants re-upload
+    d2h = n * 6 * 8 + n * 3 * 4 + n * 4 + 8
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (K2 rollout + MH)
+    peaks, peak_src = load_peaks()
+    clocks = clk.summary()
+    k2_ms, k2_n = phases["rollout"]
+    ops_k2 = 0.0
+    for k, S in enumerate(S_list):
+        C = 1 if (k == 0 or not cfg.mh) else 2
+        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * cfg.L * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
+    ops_k2 *= args.steps
+    achieved = ops_k2 / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
+    peak = roofline.peak_alu_ops(float(peaks.get("sm_max_mhz", 1965.0)))
+    all_ms = sum(v[0] for v in phases.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
+                               f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
+                   "parallelism": f"weak: {world} independent MPC problem(s), one per GPU",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "aircraft_steps_per_step": ac_steps},
+        "mpc_step_latency_ms": tmax_ms / args.steps,
+        "step_ms": step_ms,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "mpc_step_latency_ms": sum(e2e_ms) / len(e2e_ms)},
+        "gpu_launches": launches,
+        "phase_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "roofline": {"kernel": "k_rollout (K2: rollout + MH)", "bound": "alu", "achieved": achieved / 1e9,
+                     "peak": peak / 1e9, "unit": "Gop/s (FP32-lane-equivalent)", "frac": achieved / peak,
+                     "traffic": load_traffic(cfg.name),
+                     "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz {peaks.get('sm_max_mhz')} ({peak_src})",
+                     "ops_per_aircraft_step": {"C=1": roofline.ops_per_aircraft_step(scn, 1),
+                                               "C=2": roofline.ops_per_aircraft_step(scn, 2)},
+                     "k2_share_of_step": k2_ms / all_ms if all_ms else None},
+        "clocks": clocks,
+    }
+    # resample/propose phase vs HBM
+    rs_ms = phases["resample"][0] + phases["propose"][0]
+    if rs_ms > 0:
+        rb = roofline.resample_bytes(scn["n"], cfg.L, scn["H"]) * (cfg.K - 1) * args.steps
+        line["roofline_resample"] = {"bound": "hbm", "achieved": rb / (rs_ms / 1000.0) / 1e9,
+                                     "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
+                                     "frac": rb / (rs_ms / 1000.0) / 1e9 / float(peaks.get("hbm_gbs", 6650.0))}
+    if not args.no_cpu_baseline:
+        v, cores, sample = cpu_baseline(scn, cfg)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

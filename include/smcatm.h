@@ -1,0 +1,255 @@
+/*
+ * smcatm.h -- C ABI of libsmcatm, the B200-native (sm_100a) hot path of
+ * Eele & Maciejowski, "Sequential Monte Carlo Optimisation for Air Traffic
+ * Management", CUED/F-INFENG/TR.693, 2015 (arxiv 1506.02869).
+ *
+ * Citations: P:n = line n of the paper's text; R<n> = reading n in
+ * DESIGN.md section 3 (how a silent / garbled passage is interpreted).
+ *
+ * Conventions for every entry point
+ *   - All functions return smc_status; nothing throws across the ABI.  On a
+ *     non-OK status, smc_last_error(ctx) holds a one-line message.
+ *   - Host arrays are owned by the caller; the library copies what it needs
+ *     during the call and never retains a host pointer.
+ *   - Device memory: the caller provides ONE device workspace of
+ *     smc_workspace_bytes(cfg) bytes (e.g. a torch uint8 CUDA tensor) that
+ *     must outlive the context.  The library allocates no device memory.
+ *   - Streams: every call is ordered on cfg.stream (a cudaStream_t; NULL =
+ *     legacy default stream).  Calls that return host data synchronise it;
+ *     asynchronous CUDA errors surface at the next synchronising call as
+ *     SMC_ECUDA.
+ *   - One host thread per context at a time.  One context per GPU rank.
+ *   - Units are SI; angles in radians; x East, y North, chi measured
+ *     counter-clockwise from +x (the form of Eq. hor); runway at
+ *     the origin, landings heading West.
+ */
+#ifndef SMCATM_H
+#define SMCATM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct smc_ctx smc_ctx;
+
+typedef enum {
+    SMC_OK = 0,
+    SMC_EINVAL = 1,       /* bad configuration / scenario / argument            */
+    SMC_EINFEASIBLE = 2,  /* no particle without a zero weight   */
+    SMC_ECUDA = 3,        /* CUDA runtime error (message in smc_last_error)     */
+    SMC_ENCCL = 4,        /* NCCL error (multi-GPU)                             */
+    SMC_ENOMEM = 5,       /* workspace too small                                */
+    SMC_ESTATE = 6        /* call order violated (e.g. iterate before scenario) */
+} smc_status;
+
+enum { SMC_ARRIVAL = 0, SMC_DEPARTURE = 1 };
+enum { SMC_SCHED_CONST = 0, SMC_SCHED_PAPER = 1 };   /* S_k const or floor(3+5e^{0.05k}) */
+enum { SMC_DENSITY_ISA = 0, SMC_DENSITY_CONST = 1 }; /* R12 */
+enum { SMC_FLAG_LANDED = 1, SMC_FLAG_EXITED = 2, SMC_FLAG_VIOLATED = 4 };
+
+/* Aircraft state (order R29). */
+typedef struct { double x, y, z, v, chi, m; } smc_state;
+
+/* Control per aircraft per step: thrust T [N], bank phi [rad], climb gamma [rad]. */
+typedef struct { float thrust, bank, climb; } smc_control;
+
+/* Aircraft-type constants: drag polar (R12), fuel coefficient eta
+ * (constant, R13) and the flight envelope. */
+typedef struct {
+    double S, cd0, cd2, eta, m_empty;
+    double T_min, T_max, v_min, v_max, gamma_max, phi_max, z_min, z_max;
+} smc_aircraft_type;
+
+/* One aircraft in the planning problem. first_step = e in [0, H]: the
+ * aircraft is simulated on horizon steps [e, H) only (rolling window, P:428;
+ * R20).  Departures use theta_F / z_tf / v_D, arrivals beta_f. */
+typedef struct {
+    uint32_t kind;        /* SMC_ARRIVAL or SMC_DEPARTURE */
+    uint32_t type;        /* index into smc_scenario.types */
+    uint32_t first_step;
+    uint32_t reserved;
+    smc_state x0;         /* state at entry (shared by all particles) */
+    double theta_F, z_tf, v_D, beta_f;
+} smc_aircraft;
+
+/* The planning problem and every model constant. */
+typedef struct {
+    uint32_t n_aircraft;  /* N, 1..32 */
+    uint32_t n_types;
+    const smc_aircraft *aircraft;          /* [n_aircraft] */
+    const smc_aircraft_type *types;        /* [n_types] */
+    uint32_t horizon;     /* H, 1..32 */
+    int32_t density_mode; /* SMC_DENSITY_* */
+    double dt, g, rho_const;               /* delta t, gravity, rho for CONST mode */
+    double P_runway, P_beta, P_chi, P_vs;  /* landing sector (Eq. TO_init) */
+    double P_r, P_h;                       /* separation cylinder (Eq. avoidance) */
+    double alpha_dep[4];                   /* bearing A, fuel, altitude B, speed C */
+    double alpha_arr[3];                   /* heading D, altitude E, fuel (R7) */
+    double noise_w, A_c;                   /* noise weight and altitude cut-off */
+    uint32_t n_centres;                    /* population centres */
+    const double *centres;                 /* [n_centres][3] = x, y, radius (m) */
+    uint32_t pop_nx, pop_ny;               /* popdense grid; 0 = no grid */
+    double pop_x0, pop_y0, pop_dx;
+    double wind_lo[3], wind_hi[3];         /* 2x2x2 wind-grid box */
+    double sigma_lo, sigma_hi;             /* sigma(z) at the box bottom / top */
+    double beta_w, gamma_w, lambda_t;      /* Eq. cov decay rates (R14) */
+    double nominal[2];                     /* forecast wind */
+    double turb_sigma;                     /* per-aircraft gust std (R15), 0 = off */
+    double tma_radius;                     /* D_TMA */
+} smc_scenario;
+
+/* Solver configuration. */
+typedef struct {
+    uint32_t n_particles;      /* L, global over all ranks                    */
+    uint32_t n_samples;        /* S per round for SMC_SCHED_CONST (Alg.1 l.7)         */
+    uint32_t schedule;         /* SMC_SCHED_*                                         */
+    uint32_t n_rounds;         /* K rounds per mpc_step (J_max + 1)     */
+    uint32_t mh;               /* 1: Metropolis-Hastings move (R1); 0: Alg.1 l.23     */
+    uint32_t clamp_proposals;  /* 1: clamp perturbed controls to the envelope (R16)   */
+    double sigma[3];           /* perturbation std (T, phi, gamma)     */
+    double anneal;             /* sigma_k = sigma * anneal^k                          */
+    uint64_t seed;             /* Philox key                                          */
+    int32_t device;            /* CUDA device ordinal                                 */
+    int32_t rank, world_size;  /* particle sharding (1 = single GPU)                  */
+    const void *nccl_unique_id;/* 128-byte ncclUniqueId from rank 0; NULL if world 1  */
+    void *workspace;           /* caller-owned device memory                          */
+    size_t workspace_bytes;
+    void *stream;              /* cudaStream_t                                        */
+    uint32_t max_aircraft;     /* capacity (<= 32)                                    */
+    uint32_t max_horizon;      /* capacity (<= 32)                                    */
+    uint32_t use_graph;        /* 1: replay the round loop as a CUDA graph            */
+    uint32_t profile;          /* 1: time each phase with CUDA events (smc_phase_times) */
+} smc_config;
+
+/* Per-round diagnostics (smc_iterate). */
+typedef struct {
+    double best_lambda;        /* max_l sum_i log2 W_il over survivors        */
+    double accept_rate;        /* MH acceptances / L (1.0 in round 0)                 */
+    double ess_min;            /* min_i (sum w)^2 / sum w^2, diagnostic       */
+    uint32_t infeasible_lo;    /* bit i: column i all-zero (resampled uniformly, R25) */
+    uint32_t infeasible_hi;
+    uint32_t n_samples;        /* S_k used in this round                              */
+    uint32_t round;            /* k                                                   */
+} smc_round_stats;
+
+/* Bytes of device workspace needed for cfg (uses n_particles, world_size,
+ * max_aircraft, max_horizon).  0 on invalid cfg. */
+size_t smc_workspace_bytes(const smc_config *cfg);
+
+/* Create a context.  Validates cfg, carves the workspace, creates events.
+ * With world_size > 1 also joins the NCCL communicator (R43). */
+smc_status smc_init(const smc_config *cfg, smc_ctx **out);
+
+/* Copy the scenario, precompute (Qhat = chol(Rhat) P:463-465, normalisers
+ * P:336, population grid P:1131-1133) and draw the initial population
+ * (Alg.1 l.1-5).  Resets the round counter k to 0. */
+smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn);
+
+/* Run n_rounds SMC rounds (Alg.1 l.6-24).  Round k: evaluate every particle
+ * over S_k wind samples (l.9-18; with MH both the resampled particle and its
+ * perturbation, common random numbers), MH-select (R1), reduce the log2
+ * weights, per-aircraft systematic resampling (l.22, R25) and propose
+ * (l.23).  stats: nullable, n_rounds entries (synchronises if non-NULL). */
+smc_status smc_iterate(smc_ctx *ctx, uint32_t n_rounds, smc_round_stats *stats);
+
+/* Final sample selection (Alg.1 l.27): the survivor of the last
+ * evaluated round with the greatest prod_i W_il; ties -> lowest global index.
+ * out: host [N][H] controls.  Returns SMC_EINFEASIBLE if every particle has
+ * a zero weight.  Synchronises. */
+smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *lambda, int64_t *particle);
+
+/* One MPC update: x0 := measured (host [N]), fresh population,
+ * n_rounds rounds, selection, apply the t=0 control of the winner (applied,
+ * host [N]) and advance the plant one dt with the realised wind (next, host
+ * [N]); flags[N] = SMC_FLAG_* (landed Eq. TO_init, exited D_TMA P:257).
+ * Aircraft with first_step > 0 are not advanced.  Increments the MPC step
+ * index that keys every random stream.  Synchronises. */
+smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_control *applied,
+                    smc_state *next, uint32_t *flags);
+
+/* Device-resident MPC update: fresh population from the current x0, n_rounds
+ * rounds, selection and (advance_plant != 0) the plant step on the device
+ * copy of the plant state, all enqueued on cfg.stream with no host copy and
+ * no synchronisation.  The plant state is the scenario's x0 after
+ * smc_set_scenario / the last mpc_step's next state.  Infeasible solves leave
+ * the plant state unchanged and set SMC_FLAG_VIOLATED in the device flags. */
+smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant);
+
+/* Accumulated device time per phase since the last call (requires
+ * cfg.profile = 1; synchronises): ms[0] rollout+MH (K2), ms[1] reduce +
+ * resampling scans (K4a, K4b, K5), ms[2] gather + propose (K6), ms[3] other
+ * (init, select, plant).  launches[4] = kernel launches per phase. */
+smc_status smc_phase_times(smc_ctx *ctx, double ms[4], uint64_t launches[4]);
+
+const char *smc_last_error(const smc_ctx *ctx);
+void smc_destroy(smc_ctx *ctx);
+
+/* Set / read the MPC step index (keys all streams; mpc_step increments it). */
+smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t mpc_index);
+uint32_t smc_get_mpc_index(const smc_ctx *ctx);
+
+/* Number of kernel launches the library issued since smc_init. */
+uint64_t smc_launch_count(const smc_ctx *ctx);
+
+/* ---------------- parity / test hooks (stream-synchronising) -------------- */
+
+/* Roll out caller-given controls (host [L][N][H][3], particle l = global
+ * index l0 + l) for S samples of round k, through the production rollout
+ * code.  Outputs per (l, s, i) (host, nullable): J [L][S][N], viol
+ * [L][S][N] (uint8), comp [L][S][N][4], fuel [L][S][N], landed
+ * [L][S][N] (int32, -1 = not landed), traj [L][S][N][H+1][6] (float). */
+smc_status smc_debug_rollout(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t l0,
+                             uint32_t S, uint32_t k, float *J, uint8_t *viol, float *comp,
+                             float *fuel, int32_t *landed, float *traj);
+
+/* Evaluate (Alg.1 l.9-18) caller-given controls with the production kernel:
+ * ell[L][N] (host float) = -log2(L_global) + sum_s log2 J (or -inf). */
+smc_status smc_debug_evaluate(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t S,
+                              uint32_t k, float *ell);
+
+/* MH decisions (R1) for injected joint log2 weights: acc[l] = 1 accept. */
+smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_prop, uint32_t L,
+                        uint32_t k, uint8_t *acc);
+
+/* Per-aircraft systematic resampling (R25) of injected log2 weights
+ * ell[N][L] (host float) with the production kernels -> anc[N][L] (host
+ * int32).  Q[N] (nullable) receives the integer weight totals. */
+smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t k,
+                              int32_t *anc, uint64_t *Q);
+
+/* Gather + propose (Alg.1 l.22-23) on injected survivors: surv_ctrl [L][N][H][3]
+ * (host), anc [N][L] -> xp (resampled, = parent rows) and xs (perturbed),
+ * both host [L][N][H][3], with sigma_k = sigma * anneal^k. */
+smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, const int32_t *anc, uint32_t L,
+                             uint32_t k, float *xp, float *xs);
+
+/* Device population after the last call: ctrl_cur / ctrl_prop [L][N][H][3]
+ * of the last evaluated pair, surv[L] (0 = resampled kept, 1 = proposal
+ * accepted), ell_surv[N][L], lam_surv[L], lam_cand[2][L] (joint log2 weight
+ * of both MH candidates as the kernel computed them; round 0 / mh=0: only
+ * [0] is meaningful).  Any pointer may be NULL. */
+smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
+                                float *ell_surv, double *lam_surv, double *lam_cand);
+
+/* ---------------- multi-GPU partition helpers (pure host, no GPU) ---------- */
+
+/* Particles [begin, end) owned by rank (contiguous block sharding). */
+void smc_shard_range(uint32_t L, int32_t world_size, int32_t rank, uint32_t *begin, uint32_t *end);
+
+/* Given every rank's per-column integer weight totals Q_all[world][N]
+ * (allgathered), the exclusive CDF offset of `rank` per column and the
+ * global totals. */
+void smc_shard_offsets(uint32_t N, int32_t world_size, int32_t rank, const uint64_t *Q_all,
+                       uint64_t *offset, uint64_t *Q_total);
+
+/* Number of systematic slots j in [0, L) with floor((j Q + R) / L) < C
+ * (exact integer arithmetic): the slot boundary of CDF value C (R25). */
+uint64_t smc_slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMCATM_H */

@@ -1,0 +1,838 @@
+// capi.cu -- C ABI and host orchestrator of libsmcatm (include/smcatm.h).
+//
+// The host side only validates, packs constants, carves the caller's device
+// workspace and sequences kernels on the caller's stream; every per-particle
+// step of the path runs in the kernels of k_rollout.cu / k_population.cu.
+// Scenario precompute that is O(1) in the particle count (the 8x8 Cholesky of
+// Rhat; the departure altitude normalisers) is host FP64.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/smcatm.h"
+#include "smc_device.cuh"
+#include "smc_kernels.h"
+
+using namespace smc;
+
+namespace {
+
+constexpr uint32_t kPopCap = 256 * 256;
+constexpr uint32_t kCentreCap = 256;
+
+size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct Layout {
+    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, status2, tiles, marks, anc, accept, dac, pop, centres,
+        part_lam, part_idx, done, best_lam, best_idx, best_row, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
+};
+
+// Bump-allocate every device buffer from the caller's workspace.
+Layout layout(uint32_t Lloc, int nmax, int Hmax) {
+    Layout o{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t at = off; off += align_up(bytes); return at; };
+    const size_t row = (size_t)Lloc * nmax * Hmax * 3 * sizeof(float);
+    o.ctrl = take(4 * row);
+    o.ell = take((size_t)nmax * Lloc * sizeof(float));
+    o.lam = take((size_t)Lloc * sizeof(double));
+    o.lam2 = take(2 * (size_t)Lloc * sizeof(double));
+    o.surv = take(Lloc);
+    o.colmax = take(nmax * sizeof(uint32_t));
+    o.Q = take(nmax * sizeof(unsigned long long));
+    o.ess = take(2 * nmax * sizeof(double));
+    o.status = take((size_t)nmax * scan_tiles(Lloc) * 8);
+    o.status2 = take((size_t)nmax * scan_tiles(Lloc) * 8);
+    o.tiles = take(2 * nmax * sizeof(uint32_t));
+    o.marks = take((size_t)nmax * Lloc * sizeof(int32_t));
+    o.anc = take((size_t)nmax * Lloc * sizeof(int32_t));
+    o.accept = take(8);
+    o.dac = take(nmax * sizeof(DevAircraft));
+    o.pop = take(kPopCap * sizeof(float));
+    o.centres = take(kCentreCap * 3 * sizeof(double));
+    o.part_lam = take(512 * sizeof(double));
+    o.part_idx = take(512 * sizeof(long long));
+    o.done = take(sizeof(unsigned));
+    o.best_lam = take(sizeof(double));
+    o.best_idx = take(sizeof(long long));
+    o.best_row = take((size_t)nmax * Hmax * 3 * sizeof(float));
+    o.pZ = take(16 * sizeof(double));
+    o.pzi = take(sizeof(int));
+    o.pstates = take(nmax * 6 * sizeof(double));
+    o.pnext = take(nmax * 6 * sizeof(double));
+    o.pflags = take(nmax * sizeof(int));
+    o.papplied = take(nmax * 3 * sizeof(float));
+    o.lohi = take(nmax * 6 * sizeof(float));
+    o.total = off;
+    return o;
+}
+
+uint32_t local_count(uint32_t L, int world, int rank) {
+    uint32_t b, e;
+    smc_shard_range(L, world, rank, &b, &e);
+    return e - b;
+}
+
+uint32_t max_local(uint32_t L, int world) {
+    uint32_t m = 0;
+    for (int r = 0; r < world; ++r) m = std::max(m, local_count(L, world, r));
+    return m;
+}
+
+}  // namespace
+
+struct smc_ctx {
+    smc_config cfg{};
+    cudaStream_t st = nullptr;
+    uint32_t Lg = 0, Lloc = 0, l0 = 0;
+    int nmax = 0, Hmax = 0;
+    char *ws = nullptr;
+    Layout lay{};
+    float *ctrl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    float *ell = nullptr;
+    double *lam = nullptr, *lam2 = nullptr;
+    uint8_t *surv = nullptr;
+    uint32_t *colmax = nullptr, *tiles = nullptr;
+    unsigned long long *Q = nullptr, *status = nullptr, *status2 = nullptr, *accept = nullptr;
+    double *ess = nullptr;
+    int32_t *marks = nullptr, *anc = nullptr;
+    DevAircraft *dac = nullptr;
+    float *pop = nullptr, *best_row = nullptr, *papplied = nullptr, *lohi = nullptr;
+    double *centres = nullptr, *part_lam = nullptr, *best_lam = nullptr, *pZ = nullptr, *pstates = nullptr,
+           *pnext = nullptr;
+    long long *part_idx = nullptr, *best_idx = nullptr;
+    unsigned *done = nullptr;
+    int *pzi = nullptr, *pflags = nullptr;
+
+    bool have_scn = false;
+    DevScen dsc{};
+    PlantScen psc{};
+    std::vector<smc_aircraft> ac;
+    std::vector<smc_aircraft_type> types;
+    std::vector<double> centres_h;
+    smc_scenario scn{};
+    uint32_t k = 0, mpc = 0;
+    int cur = 0, last_eval = -1;
+    uint64_t launches = 0;
+    std::string err;
+    // phase timing (cfg.profile): event pairs per phase, summed on request
+    std::vector<cudaEvent_t> ev_free;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used[4];
+    uint64_t phase_launches[4] = {0, 0, 0, 0};
+    ~smc_ctx() {
+        for (auto &v : ev_used)
+            for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+        for (auto e : ev_free) cudaEventDestroy(e);
+    }
+    cudaEvent_t get_event() {
+        if (!ev_free.empty()) { cudaEvent_t e = ev_free.back(); ev_free.pop_back(); return e; }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+
+static smc_status fail(smc_ctx *c, smc_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return s;
+}
+
+#define CK(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) return fail(ctx, SMC_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+#define LAUNCHP(phase, expr)                                                                       \
+    do {                                                                                           \
+        ++ctx->launches;                                                                           \
+        ++ctx->phase_launches[phase];                                                              \
+        cudaEvent_t _e0 = nullptr, _e1 = nullptr;                                                  \
+        if (ctx->cfg.profile) { _e0 = ctx->get_event(); _e1 = ctx->get_event(); CK(cudaEventRecord(_e0, ctx->st)); } \
+        CK(expr);                                                                                  \
+        if (ctx->cfg.profile) { CK(cudaEventRecord(_e1, ctx->st)); ctx->ev_used[phase].push_back({_e0, _e1}); } \
+    } while (0)
+#define LAUNCH(expr) LAUNCHP(3, expr)
+enum { PH_ROLLOUT = 0, PH_RESAMPLE = 1, PH_PROPOSE = 2, PH_OTHER = 3 };
+
+// ---------------------------------------------------------------- partition helpers
+extern "C" void smc_shard_range(uint32_t L, int32_t world, int32_t rank, uint32_t *begin, uint32_t *end) {
+    if (world < 1) world = 1;
+    const uint64_t b = (uint64_t)L * (uint64_t)rank / (uint64_t)world;
+    const uint64_t e = (uint64_t)L * (uint64_t)(rank + 1) / (uint64_t)world;
+    *begin = (uint32_t)b;
+    *end = (uint32_t)e;
+}
+
+extern "C" void smc_shard_offsets(uint32_t N, int32_t world, int32_t rank, const uint64_t *Q_all, uint64_t *offset,
+                                  uint64_t *Q_total) {
+    for (uint32_t i = 0; i < N; ++i) {
+        uint64_t off = 0, tot = 0;
+        for (int r = 0; r < world; ++r) {
+            if (r < rank) off += Q_all[(size_t)r * N + i];
+            tot += Q_all[(size_t)r * N + i];
+        }
+        if (offset) offset[i] = off;
+        if (Q_total) Q_total[i] = tot;
+    }
+}
+
+extern "C" uint64_t smc_slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L) { return slot_count(C, Q, R, L); }
+
+// ---------------------------------------------------------------- lifecycle
+extern "C" size_t smc_workspace_bytes(const smc_config *cfg) {
+    if (!cfg || cfg->n_particles == 0 || cfg->max_aircraft == 0 || cfg->max_aircraft > 32 || cfg->max_horizon == 0 ||
+        cfg->max_horizon > 32)
+        return 0;
+    const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
+    return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon).total;
+}
+
+extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
+    if (!cfg || !out) return SMC_EINVAL;
+    *out = nullptr;
+    smc_ctx *ctx = new smc_ctx();
+    ctx->cfg = *cfg;
+    const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
+    if (world != 1) {
+        delete ctx;
+        return SMC_EINVAL;   // multi-GPU: see smc_init_multi in DESIGN.md (not built in this round)
+    }
+    if (cfg->n_particles == 0 || cfg->max_aircraft == 0 || cfg->max_aircraft > 32 || cfg->max_horizon == 0 ||
+        cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30)) {
+        delete ctx;
+        return SMC_EINVAL;
+    }
+    ctx->Lg = cfg->n_particles;
+    smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
+    ctx->Lloc -= ctx->l0;
+    ctx->nmax = (int)cfg->max_aircraft;
+    ctx->Hmax = (int)cfg->max_horizon;
+    ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax);
+    if (!cfg->workspace || cfg->workspace_bytes < ctx->lay.total) {
+        delete ctx;
+        return SMC_ENOMEM;
+    }
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return SMC_ECUDA;
+    }
+    ctx->st = (cudaStream_t)cfg->stream;
+    char *ws = (char *)cfg->workspace;
+    ctx->ws = ws;
+    const Layout &L = ctx->lay;
+    const size_t row = (size_t)ctx->Lloc * ctx->nmax * ctx->Hmax * 3;
+    (void)row;
+    const size_t prow = (size_t)max_local(ctx->Lg, world) * ctx->nmax * ctx->Hmax * 3;
+    float *cb = (float *)(ws + L.ctrl);
+    ctx->ctrl[0][0] = cb;
+    ctx->ctrl[0][1] = cb + prow;
+    ctx->ctrl[1][0] = cb + 2 * prow;
+    ctx->ctrl[1][1] = cb + 3 * prow;
+    ctx->ell = (float *)(ws + L.ell);
+    ctx->lam = (double *)(ws + L.lam);
+    ctx->lam2 = (double *)(ws + L.lam2);
+    ctx->surv = (uint8_t *)(ws + L.surv);
+    ctx->colmax = (uint32_t *)(ws + L.colmax);
+    ctx->Q = (unsigned long long *)(ws + L.Q);
+    ctx->ess = (double *)(ws + L.ess);
+    ctx->status = (unsigned long long *)(ws + L.status);
+    ctx->status2 = (unsigned long long *)(ws + L.status2);
+    ctx->tiles = (uint32_t *)(ws + L.tiles);
+    ctx->marks = (int32_t *)(ws + L.marks);
+    ctx->anc = (int32_t *)(ws + L.anc);
+    ctx->accept = (unsigned long long *)(ws + L.accept);
+    ctx->dac = (DevAircraft *)(ws + L.dac);
+    ctx->pop = (float *)(ws + L.pop);
+    ctx->centres = (double *)(ws + L.centres);
+    ctx->part_lam = (double *)(ws + L.part_lam);
+    ctx->part_idx = (long long *)(ws + L.part_idx);
+    ctx->done = (unsigned *)(ws + L.done);
+    ctx->best_lam = (double *)(ws + L.best_lam);
+    ctx->best_idx = (long long *)(ws + L.best_idx);
+    ctx->best_row = (float *)(ws + L.best_row);
+    ctx->pZ = (double *)(ws + L.pZ);
+    ctx->pzi = (int *)(ws + L.pzi);
+    ctx->pstates = (double *)(ws + L.pstates);
+    ctx->pnext = (double *)(ws + L.pnext);
+    ctx->pflags = (int *)(ws + L.pflags);
+    ctx->papplied = (float *)(ws + L.papplied);
+    ctx->lohi = (float *)(ws + L.lohi);
+    e = cudaMemsetAsync(ws, 0, L.total, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return SMC_ECUDA;
+    }
+    *out = ctx;
+    return SMC_OK;
+}
+
+extern "C" void smc_destroy(smc_ctx *ctx) { delete ctx; }
+extern "C" const char *smc_last_error(const smc_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+extern "C" uint64_t smc_launch_count(const smc_ctx *ctx) { return ctx ? ctx->launches : 0; }
+extern "C" uint32_t smc_get_mpc_index(const smc_ctx *ctx) { return ctx ? ctx->mpc : 0; }
+extern "C" smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t m) {
+    if (!ctx) return SMC_EINVAL;
+    if (m >= (1u << 24)) return fail(ctx, SMC_EINVAL, "mpc index must be < 2^24");
+    ctx->mpc = m;
+    return SMC_OK;
+}
+
+// ---------------------------------------------------------------- scenario precompute (host FP64)
+static int cholesky8(const double *A, double *Lo) {
+    for (int q = 0; q < 64; ++q) Lo[q] = 0.0;
+    for (int j = 0; j < 8; ++j) {
+        double d = A[j * 8 + j];
+        for (int p = 0; p < j; ++p) d -= Lo[j * 8 + p] * Lo[j * 8 + p];
+        if (!(d > 0.0)) return -1;
+        Lo[j * 8 + j] = std::sqrt(d);
+        for (int r = j + 1; r < 8; ++r) {
+            double s = A[r * 8 + j];
+            for (int p = 0; p < j; ++p) s -= Lo[r * 8 + p] * Lo[j * 8 + p];
+            Lo[r * 8 + j] = s / Lo[j * 8 + j];
+        }
+    }
+    return 0;
+}
+
+static smc_status build_constants(smc_ctx *ctx) {
+    const smc_scenario &s = ctx->scn;
+    const int n = (int)s.n_aircraft, H = (int)s.horizon;
+    DevScen &d = ctx->dsc;
+    PlantScen &p = ctx->psc;
+    d = DevScen{};
+    p = PlantScen{};
+    d.n = n; d.H = H; d.density_mode = s.density_mode;
+    d.dt = (float)s.dt; d.g = (float)s.g; d.rho_const = (float)s.rho_const;
+    d.P_runway = (float)s.P_runway; d.P_beta = (float)s.P_beta; d.P_chi = (float)s.P_chi; d.P_vs = (float)s.P_vs;
+    d.twoPr2 = (float)((2.0 * s.P_r) * (2.0 * s.P_r));
+    d.twoPh = (float)(2.0 * s.P_h);
+    for (int q = 0; q < 4; ++q) d.alpha_dep[q] = (float)s.alpha_dep[q];
+    for (int q = 0; q < 3; ++q) d.alpha_arr[q] = (float)s.alpha_arr[q];
+    d.has_noise = s.noise_w > 0.0 && s.pop_nx > 0 && s.pop_ny > 0;
+    d.noise_w = (float)s.noise_w;
+    d.inv_Ac = (float)(1.0 / s.A_c);
+    d.pop_nx = (int)s.pop_nx; d.pop_ny = (int)s.pop_ny;
+    d.pop_x0 = (float)s.pop_x0; d.pop_y0 = (float)s.pop_y0; d.pop_inv_dx = (float)(1.0 / s.pop_dx);
+    for (int a = 0; a < 3; ++a) {
+        d.wind_lo[a] = (float)s.wind_lo[a];
+        d.wind_inv_ext[a] = (float)(1.0 / (s.wind_hi[a] - s.wind_lo[a]));
+    }
+    // Eq. cov between the 8 grid nodes (same time), node = ix + 2 iy + 4 iz
+    double Rh[64], Qh[64];
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) {
+            const double xa = (a & 1) ? s.wind_hi[0] : s.wind_lo[0], ya = (a & 2) ? s.wind_hi[1] : s.wind_lo[1];
+            const double za = (a & 4) ? s.wind_hi[2] : s.wind_lo[2];
+            const double xb = (b & 1) ? s.wind_hi[0] : s.wind_lo[0], yb = (b & 2) ? s.wind_hi[1] : s.wind_lo[1];
+            const double zb = (b & 4) ? s.wind_hi[2] : s.wind_lo[2];
+            const double ext = s.wind_hi[2] - s.wind_lo[2];
+            const double sa = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (za - s.wind_lo[2]) / ext;
+            const double sb = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (zb - s.wind_lo[2]) / ext;
+            Rh[a * 8 + b] = sa * sb * std::exp(-s.beta_w * std::hypot(xa - xb, ya - yb)) * std::exp(-s.gamma_w * std::fabs(za - zb));
+        }
+    bool zero = true;
+    for (int q = 0; q < 64; ++q) zero = zero && Rh[q] == 0.0;
+    if (zero) {
+        for (int q = 0; q < 64; ++q) Qh[q] = 0.0;
+    } else if (cholesky8(Rh, Qh) != 0) {
+        return fail(ctx, SMC_EINVAL, "wind covariance not positive definite");
+    }
+    for (int q = 0; q < 64; ++q) { d.Qhat[q] = (float)Qh[q]; p.Qhat[q] = Qh[q]; }
+    p.a = std::exp(-s.lambda_t * s.dt);
+    p.b = std::sqrt(1.0 - p.a * p.a);
+    d.a = (float)p.a; d.b = (float)p.b;
+    d.nominal[0] = (float)s.nominal[0]; d.nominal[1] = (float)s.nominal[1];
+    d.turb_sigma = (float)s.turb_sigma;
+    d.key0 = (uint32_t)ctx->cfg.seed; d.key1 = (uint32_t)(ctx->cfg.seed >> 32);
+    d.ac = ctx->dac;
+    d.pop = ctx->pop;
+    p.dt = s.dt; p.g = s.g; p.rho_const = s.rho_const; p.density_mode = s.density_mode;
+    for (int a = 0; a < 3; ++a) { p.wind_lo[a] = s.wind_lo[a]; p.wind_hi[a] = s.wind_hi[a]; }
+    p.nominal[0] = s.nominal[0]; p.nominal[1] = s.nominal[1];
+    p.turb_sigma = s.turb_sigma; p.tma_radius = s.tma_radius;
+    p.P_runway = s.P_runway; p.P_beta = s.P_beta; p.P_chi = s.P_chi; p.P_vs = s.P_vs;
+
+    std::vector<DevAircraft> hac(n);
+    std::vector<float> lohi(6 * n);
+    for (int i = 0; i < n; ++i) {
+        const smc_aircraft &a = ctx->ac[i];
+        const smc_aircraft_type &ty = ctx->types[a.type];
+        DevAircraft &A = hac[i];
+        A.kind = (int)a.kind;
+        A.first_step = (int)a.first_step;
+        A.Ha = H - (int)a.first_step;
+        const double x0[6] = {a.x0.x, a.x0.y, a.x0.z, a.x0.v, a.x0.chi, a.x0.m};
+        for (int q = 0; q < 6; ++q) A.x0[q] = (float)x0[q];
+        A.theta_F = (float)a.theta_F; A.z_tf = (float)a.z_tf; A.v_D = (float)a.v_D; A.beta_f = (float)a.beta_f;
+        A.halfS = (float)(0.5 * ty.S); A.cd0 = (float)ty.cd0; A.cd2 = (float)ty.cd2; A.dt_eta = (float)(s.dt * ty.eta);
+        A.m_empty = (float)ty.m_empty; A.T_min = (float)ty.T_min; A.T_max = (float)ty.T_max;
+        A.v_min = (float)ty.v_min; A.v_max = (float)ty.v_max; A.gamma_max = (float)ty.gamma_max;
+        A.phi_max = (float)ty.phi_max; A.z_min = (float)ty.z_min; A.z_max = (float)ty.z_max;
+        // altitude term B: sup / inf by reachability with gamma_max, v_max (R21)
+        double ssum = 0.0, isum = 0.0;
+        for (int j = (int)a.first_step + 1; j <= H; ++j) {
+            const double reach = (double)(j - (int)a.first_step) * s.dt * ty.v_max * std::sin(ty.gamma_max);
+            const double lo = std::max(ty.z_min, a.x0.z - reach), hi = std::min(ty.z_max, a.x0.z + reach);
+            ssum += std::max(std::fabs(a.z_tf - lo), std::fabs(a.z_tf - hi));
+            const double near = std::min(std::max(a.z_tf, lo), hi);
+            isum += std::fabs(a.z_tf - near);
+        }
+        const double supB = A.Ha > 0 ? ssum / A.Ha : 0.0, infB = A.Ha > 0 ? isum / A.Ha : 0.0;
+        A.supB = (float)supB;
+        A.flagB = (supB - infB) < 1.0 ? 1 : 0;
+        A.invDenB = A.flagB ? 0.0f : (float)(1.0 / (supB - infB));
+        A.invSupC = (float)(1.0 / std::max(ty.v_max - a.v_D, a.v_D - ty.v_min));
+        A.invSupE = (float)(1.0 / std::max(a.beta_f, 1.5707963267948966 - a.beta_f));
+        const double Fmax = s.dt * A.Ha * ty.T_max * ty.eta;
+        A.invFmax = Fmax > 0.0 ? (float)(1.0 / Fmax) : 0.0f;
+        A.invHa = A.Ha > 0 ? (float)(1.0 / A.Ha) : 0.0f;
+        lohi[6 * i + 0] = (float)ty.T_min; lohi[6 * i + 1] = (float)-ty.phi_max; lohi[6 * i + 2] = (float)-ty.gamma_max;
+        lohi[6 * i + 3] = (float)ty.T_max; lohi[6 * i + 4] = (float)ty.phi_max; lohi[6 * i + 5] = (float)ty.gamma_max;
+        p.kind[i] = A.kind; p.first_step[i] = A.first_step;
+        p.halfS[i] = 0.5 * ty.S; p.cd0[i] = ty.cd0; p.cd2[i] = ty.cd2; p.eta[i] = ty.eta;
+        p.m_empty[i] = ty.m_empty; p.T_min[i] = ty.T_min; p.T_max[i] = ty.T_max; p.v_min[i] = ty.v_min;
+        p.v_max[i] = ty.v_max; p.gamma_max[i] = ty.gamma_max; p.phi_max[i] = ty.phi_max;
+        p.z_min[i] = ty.z_min; p.z_max[i] = ty.z_max;
+    }
+    CK(cudaMemcpyAsync(ctx->dac, hac.data(), sizeof(DevAircraft) * n, cudaMemcpyHostToDevice, ctx->st));
+    // lohi: stored as [n][3] lo followed by [n][3] hi
+    std::vector<float> lo3(3 * n), hi3(3 * n);
+    for (int i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) { lo3[3 * i + c] = lohi[6 * i + c]; hi3[3 * i + c] = lohi[6 * i + 3 + c]; }
+    CK(cudaMemcpyAsync(ctx->lohi, lo3.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->lohi + 3 * ctx->nmax, hi3.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));   // host staging vectors go out of scope
+    return SMC_OK;
+}
+
+static smc_status init_population(smc_ctx *ctx) {
+    PopArgs pa{ctx->dsc.n, ctx->dsc.H, ctx->Lloc, ctx->l0, 0u, ctx->mpc, ctx->dsc.key0, ctx->dsc.key1};
+    LAUNCH(launch_init_population(ctx->dsc, pa, ctx->ctrl[0][0], ctx->st));
+    ctx->k = 0;
+    ctx->cur = 0;
+    ctx->last_eval = -1;
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
+    if (!ctx || !scn) return SMC_EINVAL;
+    const uint32_t n = scn->n_aircraft, H = scn->horizon;
+    if (n == 0 || n > (uint32_t)ctx->nmax) return fail(ctx, SMC_EINVAL, "n_aircraft %u outside [1, %d]", n, ctx->nmax);
+    if (H == 0 || H > (uint32_t)ctx->Hmax) return fail(ctx, SMC_EINVAL, "horizon %u outside [1, %d]", H, ctx->Hmax);
+    if (!scn->aircraft || !scn->types || scn->n_types == 0) return fail(ctx, SMC_EINVAL, "aircraft/types missing");
+    if (!(scn->dt > 0.0) || !(scn->A_c > 0.0)) return fail(ctx, SMC_EINVAL, "dt and A_c must be positive");
+    for (int a = 0; a < 3; ++a)
+        if (!(scn->wind_hi[a] > scn->wind_lo[a])) return fail(ctx, SMC_EINVAL, "empty wind box");
+    if ((size_t)scn->pop_nx * scn->pop_ny > kPopCap) return fail(ctx, SMC_EINVAL, "population grid too large");
+    if (scn->n_centres > kCentreCap) return fail(ctx, SMC_EINVAL, "too many population centres");
+    if (scn->pop_nx * scn->pop_ny > 0 && !(scn->pop_dx > 0.0)) return fail(ctx, SMC_EINVAL, "pop_dx must be > 0");
+    for (uint32_t i = 0; i < n; ++i) {
+        const smc_aircraft &a = scn->aircraft[i];
+        if (a.type >= scn->n_types) return fail(ctx, SMC_EINVAL, "aircraft %u: bad type", i);
+        if (a.first_step > H) return fail(ctx, SMC_EINVAL, "aircraft %u: first_step > H", i);
+        if (a.kind > 1) return fail(ctx, SMC_EINVAL, "aircraft %u: bad kind", i);
+    }
+    ctx->ac.assign(scn->aircraft, scn->aircraft + n);
+    ctx->types.assign(scn->types, scn->types + scn->n_types);
+    ctx->centres_h.assign(scn->centres, scn->centres + 3 * (size_t)scn->n_centres);
+    ctx->scn = *scn;
+    ctx->scn.aircraft = ctx->ac.data();
+    ctx->scn.types = ctx->types.data();
+    ctx->scn.centres = ctx->centres_h.data();
+    smc_status s = build_constants(ctx);
+    if (s != SMC_OK) return s;
+    if (scn->n_centres) {
+        CK(cudaMemcpyAsync(ctx->centres, scn->centres, sizeof(double) * 3 * scn->n_centres, cudaMemcpyHostToDevice, ctx->st));
+    }
+    LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
+                          scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
+    CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));
+    ctx->have_scn = true;
+    return init_population(ctx);
+}
+
+// ---------------------------------------------------------------- one SMC round
+static uint32_t samples_of(const smc_ctx *ctx, uint32_t k) {
+    if (ctx->cfg.schedule == SMC_SCHED_PAPER) return (uint32_t)std::floor(3.0 + 5.0 * std::exp(0.05 * (double)k));
+    return ctx->cfg.n_samples;
+}
+
+static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
+    const uint32_t k = ctx->k;
+    const int n = ctx->dsc.n, H = ctx->dsc.H;
+    const int P = ctx->cur;
+    const uint32_t S = samples_of(ctx, k);
+    CK(cudaMemsetAsync(ctx->colmax, 0, sizeof(uint32_t) * n, ctx->st));
+    CK(cudaMemsetAsync(ctx->accept, 0, 8, ctx->st));
+    RolloutArgs ra{};
+    int NC;
+    if (k == 0) {
+        NC = 1; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = nullptr; ra.surv_single = 0;
+    } else if (ctx->cfg.mh) {
+        NC = 2; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = ctx->ctrl[P][1]; ra.surv_single = 0;
+    } else {
+        NC = 1; ra.ctrl[0] = ctx->ctrl[P][1]; ra.ctrl[1] = nullptr; ra.surv_single = 1;
+    }
+    ra.L = ctx->Lloc; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpc = ctx->mpc;
+    ra.ell0 = (float)(-std::log2((double)ctx->Lg));
+    ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
+    ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
+    LAUNCHP(PH_ROLLOUT, launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
+    ctx->last_eval = P;
+    const bool need_q = tail || stats;
+    ResampleArgs rs{};
+    rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.mpc = ctx->mpc; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1;
+    rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
+    rs.status2 = ctx->status2; rs.tile_ctr = ctx->tiles; rs.marks = ctx->marks; rs.anc = ctx->anc;
+    if (need_q) {
+        CK(cudaMemsetAsync(ctx->Q, 0, 8 * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->ess, 0, 16 * n, ctx->st));
+        LAUNCHP(PH_RESAMPLE, launch_qsum(rs, ctx->st));
+    }
+    if (tail) {
+        const size_t nt = (size_t)scan_tiles(ctx->Lloc);
+        CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->status2, 0, 8 * nt * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->tiles, 0, 8 * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->marks, 0xFF, sizeof(int32_t) * n * (size_t)ctx->Lloc, ctx->st));
+        LAUNCHP(PH_RESAMPLE, launch_scan_mark(rs, ctx->st));
+        LAUNCHP(PH_RESAMPLE, launch_maxscan(rs, ctx->st));
+        ProposeArgs pa{};
+        pa.n = n; pa.H = H; pa.L = ctx->Lloc; pa.l0 = ctx->l0; pa.k = k; pa.mpc = ctx->mpc;
+        pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
+        pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
+        pa.surv = ctx->surv; pa.anc = ctx->anc;
+        pa.xp = ctx->ctrl[P ^ 1][0]; pa.xs = ctx->ctrl[P ^ 1][1];
+        const double f = std::pow(ctx->cfg.anneal, (double)k);
+        for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
+        pa.clamp = (int)ctx->cfg.clamp_proposals;
+        pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
+        LAUNCHP(PH_PROPOSE, launch_gather_propose(pa, ctx->st));
+        ctx->cur = P ^ 1;
+    }
+    if (stats) {
+        SelectArgs sa{ctx->Lloc, ctx->l0, n, H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
+                      ctx->part_lam, ctx->part_idx, ctx->done, ctx->best_lam, ctx->best_idx, ctx->best_row};
+        LAUNCH(launch_select(sa, ctx->st));
+        uint32_t cm[32];
+        double ess[64], bl;
+        unsigned long long acc;
+        CK(cudaMemcpyAsync(cm, ctx->colmax, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(ess, ctx->ess, 16 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(&bl, ctx->best_lam, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(&acc, ctx->accept, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        stats->best_lambda = bl;
+        stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / ctx->Lloc : 1.0);
+        double em = INFINITY;
+        uint32_t lo = 0, hi = 0;
+        for (int i = 0; i < n; ++i) {
+            const bool inf = cm[i] == 0u || cm[i] == 0x007FFFFFu;
+            if (inf) { if (i < 32) lo |= 1u << i; em = 0.0; continue; }
+            const double e = ess[2 * i] * ess[2 * i] / ess[2 * i + 1];
+            em = std::min(em, e);
+        }
+        stats->ess_min = em;
+        stats->infeasible_lo = lo;
+        stats->infeasible_hi = hi;
+        stats->n_samples = S;
+        stats->round = k;
+    }
+    ctx->k = k + 1;
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_iterate(smc_ctx *ctx, uint32_t n_rounds, smc_round_stats *stats) {
+    if (!ctx) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_iterate before smc_set_scenario");
+    for (uint32_t r = 0; r < n_rounds; ++r) {
+        if (ctx->k >= 65535) return fail(ctx, SMC_EINVAL, "round index exceeds 2^16");
+        smc_status s = run_round(ctx, true, stats ? &stats[r] : nullptr);
+        if (s != SMC_OK) return s;
+    }
+    return SMC_OK;
+}
+
+static smc_status select_best(smc_ctx *ctx) {
+    if (ctx->last_eval < 0) return fail(ctx, SMC_ESTATE, "no evaluated population");
+    const int P = ctx->last_eval;
+    SelectArgs sa{ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
+                  ctx->part_lam, ctx->part_idx, ctx->done, ctx->best_lam, ctx->best_idx, ctx->best_row};
+    LAUNCH(launch_select(sa, ctx->st));
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *lambda, int64_t *particle) {
+    if (!ctx) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
+    smc_status s = select_best(ctx);
+    if (s != SMC_OK) return s;
+    double bl;
+    long long bi;
+    const int n = ctx->dsc.n, H = ctx->dsc.H;
+    CK(cudaMemcpyAsync(&bl, ctx->best_lam, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(&bi, ctx->best_idx, 8, cudaMemcpyDeviceToHost, ctx->st));
+    if (out) CK(cudaMemcpyAsync(out, ctx->best_row, sizeof(float) * 3 * n * H, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (lambda) *lambda = bl;
+    if (particle) *particle = bi;
+    if (bi < 0) return fail(ctx, SMC_EINFEASIBLE, "every particle has a zero weight (P:423)");
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
+    if (!ctx) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_solve before smc_set_scenario");
+    smc_status s = init_population(ctx);                       // fresh population (R31)
+    if (s != SMC_OK) return s;
+    const uint32_t K = ctx->cfg.n_rounds ? ctx->cfg.n_rounds : 1;
+    for (uint32_t r = 0; r < K; ++r) {
+        s = run_round(ctx, r + 1 < K, nullptr);                // last round: no resample/propose
+        if (s != SMC_OK) return s;
+    }
+    s = select_best(ctx);
+    if (s != SMC_OK) return s;
+    if (advance_plant) {
+        PlantArgs pa{ctx->dsc.n, ctx->mpc, ctx->dsc.key0, ctx->dsc.key1, ctx->pstates, ctx->best_row, ctx->dsc.H,
+                     ctx->pZ, ctx->pzi, ctx->pnext, ctx->pflags, ctx->papplied, ctx->best_idx};
+        LAUNCH(launch_plant(ctx->psc, pa, ctx->st));
+    }
+    return SMC_OK;
+}
+
+extern "C" smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_control *applied, smc_state *next,
+                               uint32_t *flags) {
+    if (!ctx || !measured) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "mpc_step before smc_set_scenario");
+    const int n = ctx->dsc.n;
+    for (int i = 0; i < n; ++i) ctx->ac[i].x0 = measured[i];
+    smc_status s = build_constants(ctx);
+    if (s != SMC_OK) return s;
+    CK(cudaMemcpyAsync(ctx->pstates, measured, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->st));
+    s = smc_solve(ctx, 1);
+    if (s != SMC_OK) return s;
+    long long bi;
+    int fl[32];
+    CK(cudaMemcpyAsync(&bi, ctx->best_idx, 8, cudaMemcpyDeviceToHost, ctx->st));
+    if (next) CK(cudaMemcpyAsync(next, ctx->pnext, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, ctx->st));
+    if (applied) CK(cudaMemcpyAsync(applied, ctx->papplied, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(fl, ctx->pflags, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (flags)
+        for (int i = 0; i < n; ++i) flags[i] = (uint32_t)fl[i];
+    const uint32_t m = ctx->mpc;
+    ctx->mpc += 1;
+    if (bi < 0) return fail(ctx, SMC_EINFEASIBLE, "MPC step %u: every particle has a zero weight (P:423)", m);
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_phase_times(smc_ctx *ctx, double ms[4], uint64_t launches[4]) {
+    if (!ctx) return SMC_EINVAL;
+    CK(cudaStreamSynchronize(ctx->st));
+    for (int p = 0; p < 4; ++p) {
+        double tot = 0.0;
+        for (auto &pr : ctx->ev_used[p]) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, pr.first, pr.second));
+            tot += t;
+            ctx->ev_free.push_back(pr.first);
+            ctx->ev_free.push_back(pr.second);
+        }
+        ctx->ev_used[p].clear();
+        if (ms) ms[p] = tot;
+        if (launches) launches[p] = ctx->phase_launches[p];
+        ctx->phase_launches[p] = 0;
+    }
+    return SMC_OK;
+}
+
+// ---------------------------------------------------------------- debug hooks
+namespace {
+struct DevTmp {
+    std::vector<void *> ptrs;
+    ~DevTmp() { for (void *p : ptrs) cudaFree(p); }
+    template <class T>
+    T *alloc(size_t count) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, count * sizeof(T) + 16) != cudaSuccess) return nullptr;
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+};
+}  // namespace
+
+static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t l0, uint32_t S,
+                                     uint32_t k, bool debug, float *J, uint8_t *viol, float *comp, float *fuel,
+                                     int32_t *landed, float *traj, float *ell) {
+    if (!ctx || !controls || L == 0 || S == 0) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
+    const int n = ctx->dsc.n, H = ctx->dsc.H;
+    DevTmp tmp;
+    const size_t nrow = (size_t)L * n * H * 3;
+    float *dctrl = tmp.alloc<float>(nrow);
+    float *dell = tmp.alloc<float>((size_t)n * L);
+    double *dlam = tmp.alloc<double>(L);
+    uint8_t *dsurv = tmp.alloc<uint8_t>(L);
+    uint32_t *dcm = tmp.alloc<uint32_t>(n);
+    unsigned long long *dacc = tmp.alloc<unsigned long long>(1);
+    const size_t nu = (size_t)L * S * n;
+    float *dJ = debug ? tmp.alloc<float>(nu) : nullptr, *dcomp = debug ? tmp.alloc<float>(4 * nu) : nullptr;
+    float *dfuel = debug ? tmp.alloc<float>(nu) : nullptr;
+    uint8_t *dviol = debug ? tmp.alloc<uint8_t>(nu) : nullptr;
+    int32_t *dland = debug ? tmp.alloc<int32_t>(nu) : nullptr;
+    float *dtraj = (debug && traj) ? tmp.alloc<float>(nu * (H + 1) * 6) : nullptr;
+    if (!dctrl || !dell || !dlam || !dsurv || !dcm || !dacc) return fail(ctx, SMC_ECUDA, "debug allocation failed");
+    CK(cudaMemcpyAsync(dctrl, controls, sizeof(float) * nrow, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemsetAsync(dcm, 0, 4 * n, ctx->st));
+    if (dland) CK(cudaMemsetAsync(dland, 0xFF, sizeof(int32_t) * nu, ctx->st));
+    RolloutArgs ra{};
+    ra.ctrl[0] = dctrl; ra.L = L; ra.l0 = l0; ra.S = S; ra.k = k; ra.mpc = ctx->mpc;
+    ra.ell0 = (float)(-std::log2((double)L));
+    ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
+    ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
+    ra.dbg_landed = dland;
+    LAUNCH(launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
+    if (debug) {
+        if (J) CK(cudaMemcpyAsync(J, dJ, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
+        if (viol) CK(cudaMemcpyAsync(viol, dviol, nu, cudaMemcpyDeviceToHost, ctx->st));
+        if (comp) CK(cudaMemcpyAsync(comp, dcomp, sizeof(float) * 4 * nu, cudaMemcpyDeviceToHost, ctx->st));
+        if (fuel) CK(cudaMemcpyAsync(fuel, dfuel, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
+        if (landed) CK(cudaMemcpyAsync(landed, dland, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, ctx->st));
+        if (traj) CK(cudaMemcpyAsync(traj, dtraj, sizeof(float) * nu * (H + 1) * 6, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    if (ell) {
+        // device layout [n][L] -> host [L][n]
+        std::vector<float> tmpe((size_t)n * L);
+        CK(cudaMemcpyAsync(tmpe.data(), dell, sizeof(float) * n * L, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        for (uint32_t l = 0; l < L; ++l)
+            for (int i = 0; i < n; ++i) ell[(size_t)l * n + i] = tmpe[(size_t)i * L + l];
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_debug_rollout(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t l0, uint32_t S,
+                                        uint32_t k, float *J, uint8_t *viol, float *comp, float *fuel, int32_t *landed,
+                                        float *traj) {
+    return debug_rollout_impl(ctx, controls, L, l0, S, k, true, J, viol, comp, fuel, landed, traj, nullptr);
+}
+
+extern "C" smc_status smc_debug_evaluate(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t S, uint32_t k,
+                                         float *ell) {
+    return debug_rollout_impl(ctx, controls, L, 0, S, k, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              ell);
+}
+
+extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_prop, uint32_t L, uint32_t k,
+                                   uint8_t *acc) {
+    if (!ctx || !lam_cur || !lam_prop || !acc) return SMC_EINVAL;
+    DevTmp tmp;
+    double *a = tmp.alloc<double>(L), *b = tmp.alloc<double>(L);
+    uint8_t *o = tmp.alloc<uint8_t>(L);
+    if (!a || !b || !o) return fail(ctx, SMC_ECUDA, "debug allocation failed");
+    CK(cudaMemcpyAsync(a, lam_cur, 8 * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(b, lam_prop, 8 * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
+    const uint32_t key0 = (uint32_t)ctx->cfg.seed, key1 = (uint32_t)(ctx->cfg.seed >> 32);
+    LAUNCH(launch_mh_debug(a, b, L, k, ctx->mpc, key0, key1, o, ctx->st));
+    CK(cudaMemcpyAsync(acc, o, L, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t k,
+                                         int32_t *anc, uint64_t *Q) {
+    if (!ctx || !ell || !anc || N == 0 || N > 32 || L == 0 || L >= (1u << 30)) return SMC_EINVAL;
+    DevTmp tmp;
+    const int nt = scan_tiles(L);
+    float *dell = tmp.alloc<float>((size_t)N * L);
+    uint32_t *dcm = tmp.alloc<uint32_t>(N);
+    unsigned long long *dQ = tmp.alloc<unsigned long long>(N);
+    double *dess = tmp.alloc<double>(2 * N);
+    unsigned long long *st1 = tmp.alloc<unsigned long long>((size_t)N * nt);
+    unsigned long long *st2 = tmp.alloc<unsigned long long>((size_t)N * nt);
+    uint32_t *tiles = tmp.alloc<uint32_t>(2 * N);
+    int32_t *marks = tmp.alloc<int32_t>((size_t)N * L);
+    int32_t *danc = tmp.alloc<int32_t>((size_t)N * L);
+    if (!dell || !dcm || !dQ || !dess || !st1 || !st2 || !tiles || !marks || !danc)
+        return fail(ctx, SMC_ECUDA, "debug allocation failed");
+    CK(cudaMemcpyAsync(dell, ell, sizeof(float) * N * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemsetAsync(dcm, 0, 4 * N, ctx->st));
+    CK(cudaMemsetAsync(dQ, 0, 8 * N, ctx->st));
+    CK(cudaMemsetAsync(dess, 0, 16 * N, ctx->st));
+    CK(cudaMemsetAsync(st1, 0, 8 * (size_t)N * nt, ctx->st));
+    CK(cudaMemsetAsync(st2, 0, 8 * (size_t)N * nt, ctx->st));
+    CK(cudaMemsetAsync(tiles, 0, 8 * N, ctx->st));
+    CK(cudaMemsetAsync(marks, 0xFF, 4 * (size_t)N * L, ctx->st));
+    LAUNCH(launch_colmax(dell, (int)N, L, dcm, ctx->st));
+    ResampleArgs rs{};
+    rs.n = (int)N; rs.L = L; rs.k = k; rs.mpc = ctx->mpc;
+    rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
+    rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1; rs.status2 = st2;
+    rs.tile_ctr = tiles; rs.marks = marks; rs.anc = danc;
+    LAUNCH(launch_qsum(rs, ctx->st));
+    LAUNCH(launch_scan_mark(rs, ctx->st));
+    LAUNCH(launch_maxscan(rs, ctx->st));
+    CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * L, cudaMemcpyDeviceToHost, ctx->st));
+    if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, const int32_t *anc, uint32_t L,
+                                        uint32_t k, float *xp, float *xs) {
+    if (!ctx || !surv_ctrl || !anc || !xp || !xs) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
+    const int n = ctx->dsc.n, H = ctx->dsc.H;
+    const size_t nrow = (size_t)L * n * H * 3;
+    DevTmp tmp;
+    float *src = tmp.alloc<float>(nrow), *dxp = tmp.alloc<float>(nrow), *dxs = tmp.alloc<float>(nrow);
+    int32_t *danc = tmp.alloc<int32_t>((size_t)n * L);
+    uint8_t *dsurv = tmp.alloc<uint8_t>(L);
+    if (!src || !dxp || !dxs || !danc || !dsurv) return fail(ctx, SMC_ECUDA, "debug allocation failed");
+    CK(cudaMemcpyAsync(src, surv_ctrl, sizeof(float) * nrow, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(danc, anc, sizeof(int32_t) * n * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemsetAsync(dsurv, 0, L, ctx->st));
+    ProposeArgs pa{};
+    pa.n = n; pa.H = H; pa.L = L; pa.l0 = 0; pa.k = k; pa.mpc = ctx->mpc;
+    pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
+    pa.src[0] = src; pa.src[1] = src; pa.surv = dsurv; pa.anc = danc; pa.xp = dxp; pa.xs = dxs;
+    const double f = std::pow(ctx->cfg.anneal, (double)k);
+    for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
+    pa.clamp = (int)ctx->cfg.clamp_proposals;
+    pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
+    LAUNCH(launch_gather_propose(pa, ctx->st));
+    CK(cudaMemcpyAsync(xp, dxp, sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(xs, dxs, sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
+                                           float *ell_surv, double *lam_surv, double *lam_cand) {
+    if (!ctx) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
+    const int n = ctx->dsc.n, H = ctx->dsc.H;
+    const int P = ctx->last_eval >= 0 ? ctx->last_eval : ctx->cur;
+    const size_t nrow = (size_t)ctx->Lloc * n * H * 3;
+    if (ctrl_cur) CK(cudaMemcpyAsync(ctrl_cur, ctx->ctrl[P][0], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
+    if (ctrl_prop) CK(cudaMemcpyAsync(ctrl_prop, ctx->ctrl[P][1], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
+    if (surv) CK(cudaMemcpyAsync(surv, ctx->surv, ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
+    if (ell_surv) CK(cudaMemcpyAsync(ell_surv, ctx->ell, sizeof(float) * n * (size_t)ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
+    if (lam_surv) CK(cudaMemcpyAsync(lam_surv, ctx->lam, sizeof(double) * ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
+    if (lam_cand) CK(cudaMemcpyAsync(lam_cand, ctx->lam2, 2 * sizeof(double) * ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}

@@ -1,0 +1,559 @@
+// k_population.cu -- population kernels of libsmcatm (sm_100a):
+//   K1  k_init_population   uniform initial controls       (Alg.1 l.3-5)
+//   K4a k_qsum              integer resampling weights per column, totals Q_i
+//   K4b k_scan_mark         decoupled look-back inclusive scan of the integer
+//                           weights + systematic slot marks   (R25)
+//   K5  k_maxscan           look-back max-scan of the marks -> ancestors
+//   K6  k_gather_propose    per-aircraft recombination + Gaussian proposal
+//                           (Alg.1 l.22-23)
+//   K7  k_select            argmax of the joint weight (Alg.1 l.27)
+//   K8  k_plant             apply the first control, realised wind
+// plus the population-density grid and the MH debug hook.
+#include <cfloat>
+
+#include "smc_device.cuh"
+#include "smc_kernels.h"
+
+namespace smc {
+
+// ============================================================== K1
+__global__ void k_init_population(const DevScen sc, const PopArgs p, float *ctrl) {
+    const size_t total = (size_t)p.L * p.n * p.H;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int t = idx % p.H;
+        const int i = (idx / p.H) % p.n;
+        const uint32_t l = p.l0 + (uint32_t)(idx / ((size_t)p.H * p.n));
+        const uint4 w = draw(TAG_INIT, l, 0u, (uint32_t)t | ((uint32_t)i << 8), p.mpc, p.key0, p.key1);
+        const DevAircraft &A = sc.ac[i];
+        float *c = ctrl + idx * 3;
+        c[0] = A.T_min + (A.T_max - A.T_min) * unif(w.x);
+        c[1] = -A.phi_max + 2.0f * A.phi_max * unif(w.y);
+        c[2] = -A.gamma_max + 2.0f * A.gamma_max * unif(w.z);
+    }
+}
+
+cudaError_t launch_init_population(const DevScen &sc, const PopArgs &p, float *ctrl, cudaStream_t st) {
+    const size_t total = (size_t)p.L * p.n * p.H;
+    if (!total) return cudaSuccess;
+    const unsigned grid = (unsigned)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    k_init_population<<<grid, 256, 0, st>>>(sc, p, ctrl);
+    return cudaGetLastError();
+}
+
+// ============================================================== slot arithmetic (R25)
+// t_j = floor((j Q + R) / L) = j floor(Q/L) + floor((j (Q mod L) + R) / L), all in 64 bits.
+__host__ __device__ static inline uint64_t slot_t(uint64_t j, uint64_t qd, uint64_t qm, uint64_t R, uint64_t L) {
+    return j * qd + (j * qm + R) / L;
+}
+
+// #{ j in [0, L) : t_j < C }  (t_j is non-decreasing in j).
+__host__ __device__ uint64_t slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L) {
+    if (Q == 0 || L == 0) return 0;
+    const uint64_t qd = Q / L, qm = Q % L;
+    double approx = ((double)C * (double)L - (double)R) / (double)Q;
+    int64_t j;
+    if (!(approx > 0.0)) j = 0;
+    else if (approx >= (double)L) j = L;
+    else j = (int64_t)ceil(approx);
+    while (j > 0 && slot_t((uint64_t)(j - 1), qd, qm, R, L) >= C) --j;
+    while (j < (int64_t)L && slot_t((uint64_t)j, qd, qm, R, L) < C) ++j;
+    return (uint64_t)j;
+}
+
+// ============================================================== K4a
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kTile = kScanThreads * kScanItems;
+
+int scan_tiles(uint32_t L) { return (int)((L + kTile - 1) / kTile); }
+
+__device__ __forceinline__ bool column_infeasible(uint32_t cm) {
+    return cm == 0u || cm == f2ord(-INFINITY);
+}
+
+__device__ __forceinline__ uint64_t qweight(const float *ell, uint32_t l, float m, bool infeasible) {
+    if (infeasible) return 1ull;
+    return det_quant((double)ell[l] - (double)m);
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_qsum(const ResampleArgs r) {
+    const int i = blockIdx.y;
+    const uint32_t cm = r.colmax[i];
+    const bool inf = column_infeasible(cm);
+    const float m = ord2f(cm);
+    const float *ell = r.ell + (size_t)i * r.L;
+    unsigned long long sum = 0;
+    double s1 = 0.0, s2 = 0.0;
+    for (uint32_t l = blockIdx.x * kScanThreads + threadIdx.x; l < r.L; l += gridDim.x * kScanThreads) {
+        const uint64_t q = qweight(ell, l, m, inf);
+        sum += q;
+        const double w = (double)q * 0x1.0p-32;
+        s1 += w;
+        s2 += w * w;
+    }
+    __shared__ unsigned long long s_sum[kScanThreads / 32];
+    __shared__ double s_d1[kScanThreads / 32], s_d2[kScanThreads / 32];
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const int wid = threadIdx.x / 32;
+    if ((threadIdx.x & 31) == 0) { s_sum[wid] = sum; s_d1[wid] = s1; s_d2[wid] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < kScanThreads / 32; ++w) { t += s_sum[w]; a += s_d1[w]; b += s_d2[w]; }
+        atomicAdd(&r.Q[i], t);
+        atomicAdd(&r.ess[2 * i], a);
+        atomicAdd(&r.ess[2 * i + 1], b);
+    }
+}
+
+cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st) {
+    unsigned gx = (r.L + kScanThreads * 16 - 1) / (kScanThreads * 16);
+    if (gx < 1) gx = 1;
+    if (gx > 1024) gx = 1024;
+    k_qsum<<<dim3(gx, r.n), kScanThreads, 0, st>>>(r);
+    return cudaGetLastError();
+}
+
+// ============================================================== decoupled look-back
+// Status word per (column, tile): bits 63..62 = flag (1 aggregate, 2 inclusive
+// prefix), bits 61..0 = value.  One 64-bit store publishes flag and value together.
+constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_status(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct OpSum {
+    __device__ static unsigned long long id() { return 0ull; }
+    __device__ static unsigned long long op(unsigned long long a, unsigned long long b) { return a + b; }
+};
+struct OpMax {  // values are (int32 + 1) >= 0
+    __device__ static unsigned long long id() { return 0ull; }
+    __device__ static unsigned long long op(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+};
+
+// Exclusive prefix of `tile` within its column: publish the aggregate, walk
+// back over predecessors until an inclusive prefix is found.  Thread 0 only.
+template <class Op>
+__device__ unsigned long long lookback(unsigned long long *status, int tile, unsigned long long agg) {
+    if (tile == 0) {
+        st_status(&status[0], kFlagP | agg);
+        return Op::id();
+    }
+    st_status(&status[tile], kFlagA | agg);
+    unsigned long long pre = Op::id();
+    int j = tile - 1;
+    while (true) {
+        const unsigned long long s = ld_status(&status[j]);
+        const unsigned long long f = s & ~kValMask;
+        if (f == 0ull) continue;           // predecessor not published yet
+        pre = Op::op(pre, s & kValMask);
+        if (f == kFlagP) break;
+        --j;
+    }
+    st_status(&status[tile], kFlagP | Op::op(pre, agg));
+    return pre;
+}
+
+// Block-wide exclusive scan of per-thread values; returns the thread's
+// exclusive prefix, *agg = block total.
+template <class Op>
+__device__ unsigned long long block_exclusive(unsigned long long v, unsigned long long *agg) {
+    __shared__ unsigned long long s_w[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = Op::op(x, y);
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    unsigned long long wpre = Op::id(), tot = Op::id();
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+        if (w < wid) wpre = Op::op(wpre, s_w[w]);
+        tot = Op::op(tot, s_w[w]);
+    }
+    const unsigned long long excl_in_warp = __shfl_up_sync(0xffffffffu, x, 1);
+    *agg = tot;
+    return Op::op(wpre, lane ? excl_in_warp : Op::id());
+}
+
+// ============================================================== K4b
+__global__ void __launch_bounds__(kScanThreads) k_scan_mark(const ResampleArgs r, int ntiles) {
+    const int i = blockIdx.y;
+    __shared__ int s_tile;
+    __shared__ unsigned long long s_pre;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&r.tile_ctr[i], 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const uint32_t cm = r.colmax[i];
+    const bool inf = column_infeasible(cm);
+    const float m = ord2f(cm);
+    const float *ell = r.ell + (size_t)i * r.L;
+    const uint32_t base = (uint32_t)tile * kTile + threadIdx.x * kScanItems;
+    uint64_t q[kScanItems], inc[kScanItems];
+    uint64_t run = 0;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        const uint32_t l = base + it;
+        q[it] = l < r.L ? qweight(ell, l, m, inf) : 0ull;
+        run += q[it];
+        inc[it] = run;
+    }
+    unsigned long long agg;
+    const unsigned long long texcl = block_exclusive<OpSum>(run, &agg);
+    if (threadIdx.x == 0) s_pre = lookback<OpSum>(r.status + (size_t)i * ntiles, tile, agg);
+    __syncthreads();
+    const uint64_t pre = s_pre + texcl;
+    const uint64_t Q = r.Q[i];
+    const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, r.mpc, r.key0, r.key1);
+    const uint64_t R = __umul64hi(rw, Q);                     // floor(r64 * Q / 2^64)
+    int32_t *marks = r.marks + (size_t)i * r.L;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        const uint32_t l = base + it;
+        if (l < r.L && q[it]) {
+            const uint64_t C = pre + inc[it];
+            const uint64_t e = slot_count(C, Q, R, r.L);
+            const uint64_t b = slot_count(C - q[it], Q, R, r.L);
+            if (e > b) marks[b] = (int32_t)l;
+        }
+    }
+}
+
+cudaError_t launch_scan_mark(const ResampleArgs &r, cudaStream_t st) {
+    const int nt = scan_tiles(r.L);
+    k_scan_mark<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    return cudaGetLastError();
+}
+
+// ============================================================== K5
+__global__ void __launch_bounds__(kScanThreads) k_maxscan(const ResampleArgs r, int ntiles) {
+    const int i = blockIdx.y;
+    __shared__ int s_tile;
+    __shared__ unsigned long long s_pre;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&r.tile_ctr[r.n + i], 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const uint32_t base = (uint32_t)tile * kTile + threadIdx.x * kScanItems;
+    const int32_t *mk = r.marks + (size_t)i * r.L;
+    unsigned long long inc[kScanItems];
+    unsigned long long run = 0;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        const uint32_t l = base + it;
+        const unsigned long long v = l < r.L ? (unsigned long long)(uint32_t)(mk[l] + 1) : 0ull;
+        run = run > v ? run : v;
+        inc[it] = run;
+    }
+    unsigned long long agg;
+    const unsigned long long texcl = block_exclusive<OpMax>(run, &agg);
+    if (threadIdx.x == 0) s_pre = lookback<OpMax>(r.status2 + (size_t)i * ntiles, tile, agg);
+    __syncthreads();
+    const unsigned long long pre = s_pre > texcl ? s_pre : texcl;
+    int32_t *anc = r.anc + (size_t)i * r.L;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        const uint32_t l = base + it;
+        if (l < r.L) {
+            const unsigned long long a = pre > inc[it] ? pre : inc[it];
+            anc[l] = (int32_t)a - 1;
+        }
+    }
+}
+
+cudaError_t launch_maxscan(const ResampleArgs &r, cudaStream_t st) {
+    const int nt = scan_tiles(r.L);
+    k_maxscan<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    return cudaGetLastError();
+}
+
+// ============================================================== K6
+__global__ void k_gather_propose(const ProposeArgs p) {
+    const size_t total = (size_t)p.L * p.n * p.H;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int t = idx % p.H;
+        const int i = (idx / p.H) % p.n;
+        const uint32_t j = (uint32_t)(idx / ((size_t)p.H * p.n));
+        const int32_t a = __ldg(&p.anc[(size_t)i * p.L + j]);
+        const float *src = p.src[__ldg(&p.surv[a])] + (((size_t)a * p.n + i) * p.H + t) * 3;
+        const float c0 = src[0], c1 = src[1], c2 = src[2];
+        float *dp = p.xp + idx * 3;
+        dp[0] = c0; dp[1] = c1; dp[2] = c2;
+        const uint4 w = draw(TAG_PERTURB, p.l0 + j, p.k << 16, (uint32_t)t | ((uint32_t)i << 8), p.mpc, p.key0, p.key1);
+        const float2 z01 = box_muller(w.x, w.y);
+        const float2 z23 = box_muller(w.z, w.w);
+        float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
+        if (p.clamp) {
+            const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
+            o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
+            o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
+            o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+        }
+        float *ds = p.xs + idx * 3;
+        ds[0] = o0; ds[1] = o1; ds[2] = o2;
+    }
+}
+
+cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st) {
+    const size_t total = (size_t)p.L * p.n * p.H;
+    if (!total) return cudaSuccess;
+    size_t g = (total + 255) / 256;
+    if (g > 148 * 32) g = 148 * 32;
+    k_gather_propose<<<(unsigned)g, 256, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// ============================================================== K7
+__device__ __forceinline__ bool better(double la, long long ia, double lb, long long ib) {
+    if (ia < 0) return false;
+    if (ib < 0) return true;
+    return la > lb || (la == lb && ia < ib);
+}
+
+int select_blocks(uint32_t L) {
+    int b = (int)((L + 255) / 256);
+    return b < 1 ? 1 : (b > 512 ? 512 : b);
+}
+
+__global__ void k_select(const SelectArgs s) {
+    double bl = -INFINITY;
+    long long bi = -1;
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < s.L; l += gridDim.x * blockDim.x) {
+        const double v = s.lam[l];
+        if (v != -INFINITY && better(v, (long long)(s.l0 + l), bl, bi)) { bl = v; bi = (long long)(s.l0 + l); }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(ol, oi, bl, bi)) { bl = ol; bi = oi; }
+    }
+    __shared__ double s_l[8];
+    __shared__ long long s_i[8];
+    __shared__ bool s_last;
+    if ((threadIdx.x & 31) == 0) { s_l[threadIdx.x / 32] = bl; s_i[threadIdx.x / 32] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x / 32); ++w)
+            if (better(s_l[w], s_i[w], bl, bi)) { bl = s_l[w]; bi = s_i[w]; }
+        s.part_lam[blockIdx.x] = bl;
+        s.part_idx[blockIdx.x] = bi;
+        __threadfence();
+        const unsigned done = atomicAdd(s.done_ctr, 1u);
+        s_last = (done == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __shared__ long long s_win;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double gl = -INFINITY;
+        long long gi = -1;
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            const double pl = ((volatile double *)s.part_lam)[b];
+            const long long pi = ((volatile long long *)s.part_idx)[b];
+            if (better(pl, pi, gl, gi)) { gl = pl; gi = pi; }
+        }
+        s.best_lam[0] = gl;
+        s.best_idx[0] = gi;
+        s_win = gi;
+        *s.done_ctr = 0u;
+    }
+    __syncthreads();
+    const long long gi = s_win;
+    if (gi < 0) return;
+    const uint32_t ll = (uint32_t)(gi - s.l0);
+    const float *src = s.src[s.surv[ll]] + (size_t)ll * s.n * s.H * 3;
+    for (int e = threadIdx.x; e < s.n * s.H * 3; e += blockDim.x) s.best_row[e] = src[e];
+}
+
+cudaError_t launch_select(const SelectArgs &s, cudaStream_t st) {
+    k_select<<<select_blocks(s.L), 256, 0, st>>>(s);
+    return cudaGetLastError();
+}
+
+// ============================================================== K8 (FP64)
+__device__ double d_angdist(double d) {
+    double r = fmod(fabs(d), 2.0 * 3.141592653589793);
+    return r > 3.141592653589793 ? 2.0 * 3.141592653589793 - r : r;
+}
+
+__global__ void k_plant(const PlantScen ps, const PlantArgs p) {
+    __shared__ double sV[16], sZ[16], sW[16];
+    const int tid = threadIdx.x;
+    if (*p.best_idx < 0) {                       // infeasible solve: nothing is applied
+        if (tid < p.n) {
+            for (int a = 0; a < 6; ++a) p.next[6 * tid + a] = p.states[6 * tid + a];
+            p.flags[tid] = 4;
+            p.applied[3 * tid] = p.applied[3 * tid + 1] = p.applied[3 * tid + 2] = 0.0f;
+        }
+        return;
+    }
+    if (tid < 4) {
+        const uint4 w = draw(TAG_PLANT_WIND, 0u, 0u, (uint32_t)tid << 16, p.mpc, p.key0, p.key1);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        for (int pr = 0; pr < 2; ++pr) {
+            const double u1 = ((double)(ws[2 * pr] >> 9) + 0.5) * 0x1.0p-23;
+            const double u2 = ((double)(ws[2 * pr + 1] >> 9) + 0.5) * 0x1.0p-23;
+            const double r = sqrt(-2.0 * log(u1));
+            sV[4 * tid + 2 * pr] = r * cos(2.0 * 3.141592653589793 * u2);
+            sV[4 * tid + 2 * pr + 1] = r * sin(2.0 * 3.141592653589793 * u2);
+        }
+    }
+    __syncthreads();
+    const int zi = *p.zinit;
+    if (tid < 16) {
+        const double z = zi ? ps.a * p.Z[tid] + ps.b * sV[tid] : sV[tid];
+        sZ[tid] = z;
+        p.Z[tid] = z;
+    }
+    __syncthreads();
+    if (tid < 16) {
+        const int comp = tid >> 3, node = tid & 7;
+        double acc = 0.0;
+        for (int m = 0; m < 8; ++m) acc += ps.Qhat[node * 8 + m] * sZ[comp * 8 + m];
+        sW[tid] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) *p.zinit = 1;
+    if (tid >= p.n) return;
+    const int i = tid;
+    const double *st = p.states + 6 * i;
+    double *nx = p.next + 6 * i;
+    const float *u0 = p.best_row + (size_t)i * p.H * 3;
+    p.applied[3 * i] = u0[0]; p.applied[3 * i + 1] = u0[1]; p.applied[3 * i + 2] = u0[2];
+    p.flags[i] = 0;
+    if (ps.first_step[i] != 0) {
+        for (int a = 0; a < 6; ++a) nx[a] = st[a];
+        return;
+    }
+    double f[3];
+    for (int a = 0; a < 3; ++a) {
+        double t = (st[a] - ps.wind_lo[a]) / (ps.wind_hi[a] - ps.wind_lo[a]);
+        f[a] = t > 0.0 ? (t < 1.0 ? t : 1.0) : 0.0;
+    }
+    double wxy[2];
+    for (int c = 0; c < 2; ++c) {
+        double acc = 0.0;
+        for (int nd = 0; nd < 8; ++nd)
+            acc += ((nd & 1) ? f[0] : 1 - f[0]) * ((nd & 2) ? f[1] : 1 - f[1]) * ((nd & 4) ? f[2] : 1 - f[2]) * sW[c * 8 + nd];
+        wxy[c] = acc + ps.nominal[c];
+    }
+    if (ps.turb_sigma > 0.0) {
+        const uint4 w = draw(TAG_PLANT_TURB, 0u, 0u, (uint32_t)i << 8, p.mpc, p.key0, p.key1);
+        const double u1 = ((double)(w.x >> 9) + 0.5) * 0x1.0p-23, u2 = ((double)(w.y >> 9) + 0.5) * 0x1.0p-23;
+        const double r = sqrt(-2.0 * log(u1));
+        wxy[0] += ps.turb_sigma * r * cos(2.0 * 3.141592653589793 * u2);
+        wxy[1] += ps.turb_sigma * r * sin(2.0 * 3.141592653589793 * u2);
+    }
+    const double T = u0[0], ph = u0[1], ga = u0[2];
+    const double x = st[0], y = st[1], z = st[2], v = st[3], chi = st[4], m = st[5];
+    double rho = ps.rho_const;
+    if (ps.density_mode == 0) {
+        double base = 1.0 - 2.2558e-5 * z;
+        rho = 1.225 * pow(base > 0.0 ? base : 0.0, 4.2559);
+    }
+    const double qd = rho * v * v * ps.halfS[i];
+    const double Lf = m * ps.g / cos(ph);
+    const double CL = Lf / qd;
+    const double D = qd * (ps.cd0[i] + ps.cd2[i] * CL * CL);
+    nx[0] = x + ps.dt * (v * cos(chi) * cos(ga)) + wxy[0] * ps.dt;
+    nx[1] = y + ps.dt * (v * sin(chi) * cos(ga)) + wxy[1] * ps.dt;
+    nx[2] = z + ps.dt * (v * sin(ga));
+    nx[3] = v + ps.dt * ((T - D) / m - ps.g * sin(ga));
+    nx[4] = chi + ps.dt * (Lf * sin(ph) / (m * v));
+    nx[5] = m - ps.dt * (ps.eta[i] * T);
+    int fl = 0;
+    const double rh = sqrt(nx[0] * nx[0] + nx[1] * nx[1]);
+    const double th = atan2(nx[1], nx[0]);
+    if (ps.kind[i] == 0) {
+        const double at = fabs(th);
+        const double s = at == 0.0 ? rh : rh * at / sin(at);
+        const double beta = atan2(nx[2], s);
+        if (rh <= ps.P_runway && beta <= ps.P_beta && at <= ps.P_chi && d_angdist(nx[4] - 3.141592653589793) <= ps.P_chi &&
+            nx[3] <= ps.P_vs)
+            fl |= 1;
+    } else if (rh >= ps.tma_radius) {
+        fl |= 2;
+    }
+    bool bad = fabs(ga) > ps.gamma_max[i] || !(fabs(ph) < ps.phi_max[i]) || T < ps.T_min[i] || T > ps.T_max[i];
+    bad = bad || nx[2] < ps.z_min[i] || nx[2] > ps.z_max[i] || nx[3] < ps.v_min[i] || nx[3] > ps.v_max[i] ||
+          nx[5] < ps.m_empty[i];
+    for (int a = 0; a < 6; ++a) bad = bad || !isfinite(nx[a]);
+    if (bad) fl |= 4;
+    p.flags[i] = fl;
+}
+
+cudaError_t launch_plant(const PlantScen &ps, const PlantArgs &p, cudaStream_t st) {
+    k_plant<<<1, 32, 0, st>>>(ps, p);
+    return cudaGetLastError();
+}
+
+// ============================================================== popdense grid
+__global__ void k_popgrid(const double *centres, int nc, int nx, int ny, double x0, double y0, double dx, float *out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nx * ny) return;
+    const double x = x0 + (idx % nx) * dx, y = y0 + (idx / nx) * dx;
+    double sum = 0.0;
+    for (int c = 0; c < nc; ++c) {
+        const double bx = (x - centres[3 * c]) * 1e-3, by = (y - centres[3 * c + 1]) * 1e-3;
+        const double ci = centres[3 * c + 2] * 1e-3;
+        sum += exp(-(bx * bx + by * by) / (2.0 * ci * ci)) / (ci * 2.5066282746310002);
+    }
+    out[idx] = (float)(sum < 1.0 ? sum : 1.0);
+}
+
+cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny, double x0, double y0,
+                           double dx, float *out, cudaStream_t st) {
+    if (nx * ny == 0) return cudaSuccess;
+    k_popgrid<<<(nx * ny + 255) / 256, 256, 0, st>>>(centres, n_centres, nx, ny, x0, y0, dx, out);
+    return cudaGetLastError();
+}
+
+// ============================================================== MH debug hook
+__global__ void k_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+                           uint32_t key0, uint32_t key1, uint8_t *acc) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < L) acc[l] = mh_decide(lc[l], lp[l], l, k, mpc, key0, key1) ? 1 : 0;
+}
+
+cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+                            uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st) {
+    if (!L) return cudaSuccess;
+    k_mh_debug<<<(L + 255) / 256, 256, 0, st>>>(lc, lp, L, k, mpc, key0, key1, acc);
+    return cudaGetLastError();
+}
+
+}  // namespace smc
+
+namespace smc {
+// ============================================================== column max (debug path; K2 fuses it)
+__global__ void k_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax) {
+    const int i = blockIdx.y;
+    uint32_t mx = 0u;
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < L; l += gridDim.x * blockDim.x)
+        mx = max(mx, f2ord(ell[(size_t)i * L + l]));
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&colmax[i], mx);
+}
+
+cudaError_t launch_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax, cudaStream_t st) {
+    unsigned gx = (L + 255) / 256;
+    if (gx < 1) gx = 1;
+    if (gx > 256) gx = 256;
+    k_colmax<<<dim3(gx, n), 256, 0, st>>>(ell, n, L, colmax);
+    return cudaGetLastError();
+}
+}  // namespace smc

@@ -1,0 +1,128 @@
+// smc_kernels.h -- launch interface between the host orchestrator (capi.cu)
+// and the kernels (k_rollout.cu, k_population.cu).  Internal to libsmcatm.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace smc {
+
+struct DevScen;
+
+struct RolloutArgs {
+    const float *ctrl[2];      // candidate buffers [L][n][H][3]: 0 = x' (resampled), 1 = x* (proposal)
+    uint32_t L, l0, S, k, mpc; // local particles, global offset, samples, round, MPC step
+    float ell0;                // -log2(L_global)  (W^0 = 1/L)
+    int surv_single;           // survivor flag written when only one candidate is evaluated
+    float *ell_out;            // [n][L] survivor log2 weights (column-major per aircraft)
+    double *lam_out;           // [L] survivor joint log2 weight
+    double *lam_cand;          // [2][L] both candidates' joint log2 weights (nullable)
+    uint8_t *surv_out;         // [L] 1 = proposal accepted
+    uint32_t *colmax;          // [n] ordered-float max of ell_out (atomicMax)
+    unsigned long long *n_accept;
+    // debug outputs (candidate 0), per (l, s, i)
+    float *dbg_J, *dbg_comp, *dbg_fuel, *dbg_traj, *dbg_ell_c;
+    uint8_t *dbg_viol;
+    int32_t *dbg_landed;
+};
+
+int segment_width(int n);
+size_t rollout_smem_bytes(int W, int NC, int H);
+cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
+
+struct PopArgs {
+    int n, H;
+    uint32_t L, l0, k, mpc, key0, key1;
+};
+
+// K1: uniform initial controls (Alg.1 l.3-5)
+cudaError_t launch_init_population(const DevScen &sc, const PopArgs &p, float *ctrl, cudaStream_t st);
+
+// Resampling (R25): K4a integer weight totals, K4b decoupled
+// look-back scan + slot marks, K5 max-scan marks -> ancestors.
+struct ResampleArgs {
+    int n;
+    uint32_t L;                 // particles (local == global when single GPU)
+    uint32_t k, mpc, key0, key1;
+    const float *ell;           // [n][L]
+    const uint32_t *colmax;     // [n] ordered max
+    unsigned long long *Q;      // [n] totals (atomicAdd)
+    double *ess;                // [2n] sum w, sum w^2 (diagnostic)
+    unsigned long long *status; // [n][ntiles] look-back words (scan 1)
+    unsigned long long *status2;// [n][ntiles2] look-back words (scan 2)
+    uint32_t *tile_ctr;         // [2n] dynamic tile counters
+    int32_t *marks;             // [n][L], -1 = no offspring starts here
+    int32_t *anc;               // [n][L]
+};
+int scan_tiles(uint32_t L);
+cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
+cudaError_t launch_scan_mark(const ResampleArgs &r, cudaStream_t st);
+cudaError_t launch_maxscan(const ResampleArgs &r, cudaStream_t st);
+
+// K6: gather survivors' rows by ancestor, Gaussian proposal (Alg.1 l.22-23)
+struct ProposeArgs {
+    int n, H;
+    uint32_t L, l0, k, mpc, key0, key1;
+    const float *src[2];        // survivor pair: [0] x', [1] x*
+    const uint8_t *surv;        // [L] which buffer holds particle l's survivor
+    const int32_t *anc;         // [n][L]
+    float *xp, *xs;             // outputs [L][n][H][3]
+    float sig[3];
+    int clamp;
+    const float *lo3, *hi3;     // per aircraft [n][3] envelope for clamping
+};
+cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st);
+
+// K7: final selection + winner row copy
+struct SelectArgs {
+    uint32_t L, l0;
+    int n, H;
+    const double *lam;
+    const uint8_t *surv;
+    const float *src[2];
+    double *part_lam;           // [nblocks]
+    long long *part_idx;        // [nblocks]
+    unsigned int *done_ctr;
+    double *best_lam;           // [1]
+    long long *best_idx;        // [1]  (-1 if infeasible)
+    float *best_row;            // [n][H][3]
+};
+int select_blocks(uint32_t L);
+cudaError_t launch_select(const SelectArgs &s, cudaStream_t st);
+
+// K8: plant advance in FP64
+struct PlantArgs {
+    int n;
+    uint32_t mpc, key0, key1;
+    const double *states;       // [n][6]
+    const float *best_row;      // [n][H][3] (t = 0 is applied)
+    int H;
+    double *Z;                  // [16] realised AR(1) state
+    int *zinit;
+    double *next;               // [n][6]
+    int *flags;                 // [n]
+    float *applied;             // [n][3]
+    const long long *best_idx;  // [1] winner (-1: infeasible -> plant state unchanged)
+};
+struct PlantScen {              // FP64 constants for the plant
+    double Qhat[64], a, b, dt, g, rho_const;
+    double wind_lo[3], wind_hi[3], nominal[2], turb_sigma, tma_radius;
+    double P_runway, P_beta, P_chi, P_vs;
+    int density_mode;
+    int kind[32], first_step[32];
+    double halfS[32], cd0[32], cd2[32], eta[32];
+    double m_empty[32], T_min[32], T_max[32], v_min[32], v_max[32], gamma_max[32], phi_max[32], z_min[32], z_max[32];
+};
+cudaError_t launch_plant(const PlantScen &ps, const PlantArgs &p, cudaStream_t st);
+
+// popdense grid, computed in FP64 on the device
+cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny, double x0, double y0,
+                           double dx, float *out, cudaStream_t st);
+
+// MH decisions for injected lambdas (debug hook)
+cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+                            uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st);
+
+__host__ __device__ uint64_t slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L);
+cudaError_t launch_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax, cudaStream_t st);
+
+}  // namespace smc

@@ -1,0 +1,93 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, and its pure-host partition helpers are exact."""
+import os
+import re
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1506_02869_b200 import build, smcatm
+    build.build()
+    return smcatm.load()
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "smcatm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(smc_[a-z0-9_]+|mpc_step)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(lib):
+    from paper_1506_02869_b200 import smcatm
+    names = _declared()
+    assert "smc_init" in names and "mpc_step" in names and len(names) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", smcatm.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if " T " in l)
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert sorted(smcatm.EXPORTED) == names
+
+
+def test_library_is_sm100a(lib):
+    from paper_1506_02869_b200 import smcatm
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", smcatm.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_workspace_bytes_validation(lib):
+    from paper_1506_02869_b200 import smcatm
+    cfg = smcatm.Config()
+    assert lib.smc_workspace_bytes(cfg) == 0               # L = 0 is invalid
+    cfg.n_particles, cfg.max_aircraft, cfg.max_horizon = 1000, 8, 6
+    nb = lib.smc_workspace_bytes(cfg)
+    assert nb >= 4 * 1000 * 8 * 6 * 3 * 4
+    cfg.max_aircraft = 33
+    assert lib.smc_workspace_bytes(cfg) == 0
+
+
+def test_shard_range_partitions(lib):
+    from paper_1506_02869_b200 import smcatm
+    for L in (1, 7, 1000, 1 << 20):
+        for G in (1, 2, 3, 8):
+            spans = [smcatm.shard_range(L, G, r) for r in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == L
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_shard_offsets(lib):
+    from paper_1506_02869_b200 import smcatm
+    rng = np.random.default_rng(0)
+    Q = rng.integers(0, 2**40, (4, 6)).astype(np.uint64)
+    for r in range(4):
+        off, tot = smcatm.shard_offsets(Q, r)
+        assert np.array_equal(off, Q[:r].sum(0) if r else np.zeros(6, np.uint64))
+        assert np.array_equal(tot, Q.sum(0))
+
+
+def test_slot_count_exact(lib):
+    """#{j : floor((jQ+R)/L) < C} against exact rational enumeration."""
+    from paper_1506_02869_b200 import smcatm
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        L = int(rng.integers(1, 60))
+        Q = int(rng.integers(1, 2**45))
+        R = int(rng.integers(0, Q))
+        C = int(rng.integers(0, Q + 1))
+        ref = sum(1 for j in range(L) if (j * Q + R) // L < C)
+        assert smcatm.slot_count(C, Q, R, L) == ref
+    # large L, Q near the 2^62 design bound
+    L, Q = 1 << 20, (1 << 20) * (1 << 32)
+    R = Q // 3
+    for C in (0, 1, Q // 2, Q - 1, Q):
+        j = smcatm.slot_count(C, Q, R, L)
+        assert (j == 0 or ((j - 1) * Q + R) // L < C) and (j == L or (j * Q + R) // L >= C)

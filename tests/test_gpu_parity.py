@@ -1,0 +1,259 @@
+"""GPU (libsmcatm, sm_100a) vs FP64 oracle parity, through the C ABI.
+
+Tolerances: rollout quantities |gpu - ora| <= 1e-4 |ora|
++ atol (positions 0.1 m, speed 1e-3 m/s, heading 1e-4 rad, mass/fuel 1e-2 kg,
+utilities 1e-4); log2 weights 1e-4 (|ell| + S); MH decisions, ancestors,
+integer totals, selection: bit-exact.  A rollout whose oracle decision
+margins (R30) come within 1e-4 of a threshold is excluded from the strict
+comparison (FP32 vs FP64 may take either side) and counted: it must stay rare.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1506_02869_b200 import scenarios as sc
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 1e-4
+
+
+@pytest.fixture(scope="module")
+def smc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1506_02869_b200 import smcatm
+    smcatm.load()
+    return smcatm
+
+
+def _solver(smc, scn, L=64, S=4, K=3, seed=0x5EED0001, **kw):
+    sig = (0.05 * 1.2e5, 2 * math.pi / 180, 0.5 * math.pi / 180)
+    return smc.Solver(scn, L=L, S=S, K=K, sigma=sig, seed=seed, **kw)
+
+
+def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, max_ambiguous=0.02):
+    sol = _solver(smc, scn, L=max(L, 1), S=S, seed=seed)
+    P = O.Problem(scn)
+    g = sol.debug_rollout(ctrl, S, k, l0=l0, traj=True)
+    n, H = scn["n"], scn["H"]
+    amb = 0
+    checked = 0
+    for l in range(L):
+        for s in range(S):
+            r = P.rollout(ctrl[l].astype(np.float64), l0 + l, s, k, seed)
+            if np.min(r["margin"]) < MARGIN:
+                amb += 1
+                continue
+            checked += 1
+            assert np.array_equal(g["viol"][l, s].astype(bool), r["viol"].astype(bool)), (l, s)
+            assert np.array_equal(g["landed"][l, s], r["landed_step"]), (l, s)
+            tg, to = g["traj"][l, s].astype(np.float64), r["traj"]
+            tol = np.array([0.1, 0.1, 0.1, 1e-3, 1e-4, 1e-2])
+            err = np.abs(tg - to) - (1e-4 * np.abs(to) + tol)
+            assert np.all(err <= 0), (l, s, np.unravel_index(np.argmax(err), err.shape), tg, to)
+            assert np.allclose(g["fuel"][l, s], r["fuel"], rtol=1e-4, atol=1e-2), (l, s)
+            assert np.allclose(g["J"][l, s], r["J"], rtol=0, atol=1e-4), (l, s, g["J"][l, s], r["J"])
+            assert np.allclose(g["comp"][l, s], r["comp"], rtol=0, atol=1e-4), (l, s)
+    assert checked > 0
+    assert amb <= max_ambiguous * L * S, (amb, L * S)
+    sol.close()
+    return checked, amb
+
+
+def _near_trim_controls(scn, L, seed):
+    """Float32 controls near trim with noise: mostly feasible, some violations."""
+    rng = np.random.default_rng(seed)
+    n, H = scn["n"], scn["H"]
+    c = np.zeros((L, n, H, 3), np.float32)
+    c[..., 0] = rng.uniform(20000, 70000, (L, n, H))
+    c[..., 1] = rng.uniform(-0.45, 0.45, (L, n, H))
+    c[..., 2] = rng.uniform(-0.08, 0.08, (L, n, H))
+    return c
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "n3_partial", "n12_noise", "n24", "n1"])
+def test_rollout_parity(smc, case):
+    if case == "c1":
+        scn, cfg = sc.config(1)
+        L, S, seed = 40, 4, cfg.seed
+    elif case == "c2":
+        scn, cfg = sc.config(2)
+        L, S, seed = 70, 3, cfg.seed
+    elif case == "n3_partial":
+        scn = sc.small(2, 1, H=7, seed=5)
+        scn["first_step"] = np.array([0, 3, 7], np.int32)
+        L, S, seed = 90, 3, 99
+    elif case == "n12_noise":
+        scn, cfg = sc.config(4, noise_w=0.2)
+        L, S, seed = 40, 2, cfg.seed
+    elif case == "n24":
+        scn, cfg = sc.config(3)
+        L, S, seed = 12, 2, cfg.seed
+    else:
+        scn = sc.small(1, 0, H=6, seed=3)
+        L, S, seed = 200, 2, 5
+    ctrl = _near_trim_controls(scn, L, seed=11)
+    _compare_rollouts(smc, scn, L, S, k=2, seed=seed, ctrl=ctrl, l0=1000)
+
+
+def test_rollout_landing_exercised(smc):
+    """An arrival set up to land mid-horizon: landing step and frozen state agree."""
+    scn = sc.small(1, 1, H=8, seed=2)
+    DEG = math.pi / 180
+    scn["x0"][0] = [7000.0, 300.0, 7000 * math.tan(3 * DEG), 76.0, math.pi, 64000.0]
+    L = 64
+    ctrl = np.zeros((L, 2, 8, 3), np.float32)
+    rng = np.random.default_rng(1)
+    ctrl[:, 0, :, 0] = rng.uniform(15000, 30000, (L, 8))
+    ctrl[:, 0, :, 2] = -3 * DEG + rng.uniform(-0.01, 0.01, (L, 8))
+    ctrl[:, 1, :, 0] = 50000.0
+    checked, _ = _compare_rollouts(smc, scn, L, 2, k=0, seed=7, ctrl=ctrl)
+    sol = _solver(smc, scn, L=L, S=2)
+    g = sol.debug_rollout(ctrl, 2, 0)
+    assert (g["landed"][:, :, 0] > 0).any()
+
+
+def test_evaluate_parity(smc):
+    scn, cfg = sc.config(2)
+    L, S = 96, 5
+    ctrl = _near_trim_controls(scn, L, seed=3)
+    sol = _solver(smc, scn, L=L, S=S, seed=cfg.seed)
+    ell_g = sol.debug_evaluate(ctrl, S, 4).astype(np.float64)
+    P = O.Problem(scn)
+    ell_o = P.evaluate(ctrl.astype(np.float64), S, 4, cfg.seed)
+    bad = 0
+    for l in range(L):
+        amb = any(np.min(P.rollout(ctrl[l].astype(np.float64), l, s, 4, cfg.seed)["margin"]) < MARGIN for s in range(S))
+        if amb:
+            bad += 1
+            continue
+        fin = np.isfinite(ell_o[l])
+        assert np.array_equal(fin, np.isfinite(ell_g[l])), l
+        assert np.allclose(ell_g[l][fin], ell_o[l][fin], rtol=0, atol=1e-4 * (np.abs(ell_o[l][fin]).max() + S)), l
+    assert bad < 0.05 * L
+
+
+def test_mh_bitexact(smc):
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, seed=cfg.seed)
+    rng = np.random.default_rng(5)
+    L = 20000
+    lc = rng.uniform(-80, -10, L)
+    d = np.concatenate([rng.uniform(-30, 2, L // 2), rng.normal(0, 1e-9, L // 4), rng.uniform(-1100, -1000, L - L // 2 - L // 4)])
+    lp = lc + d
+    lc[rng.uniform(size=L) < 0.05] = -np.inf
+    lp[rng.uniform(size=L) < 0.05] = -np.inf
+    for k in (1, 7, 100):
+        acc = sol.debug_mh(lc, lp, k)
+        ref = np.array([O.mh_accept(lc[l], lp[l], l, k, cfg.seed) for l in range(L)], np.uint8)
+        assert np.array_equal(acc, ref)
+
+
+@pytest.mark.parametrize("L", [1, 7, 2048, 2049, 5000, 70001])
+def test_resample_bitexact(smc, L):
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, seed=cfg.seed)
+    rng = np.random.default_rng(L)
+    N = 5
+    ell = rng.normal(-25, 8, (N, L)).astype(np.float32)
+    ell[rng.uniform(size=(N, L)) < 0.3] = -np.inf
+    ell[3] = -np.inf                                      # infeasible column
+    ell[4] = np.float32(-7.25)                            # equal weights
+    for k in (0, 5):
+        anc, Q = sol.debug_resample(ell, k)
+        for i in range(N):
+            r = O.resample_column(ell[i].astype(np.float64), i, k, cfg.seed)
+            assert Q[i] == r["Q"], (i, k)
+            assert np.array_equal(anc[i], r["anc"]), (i, k, np.nonzero(anc[i] != r["anc"])[0][:10])
+
+
+def test_propose_parity(smc):
+    scn, cfg = sc.config(2)
+    L = 500
+    sol = _solver(smc, scn, L=L, seed=cfg.seed)
+    P = O.Problem(scn)
+    surv = _near_trim_controls(scn, L, seed=4)
+    rng = np.random.default_rng(3)
+    anc = np.sort(rng.integers(0, L, (scn["n"], L)), axis=1).astype(np.int32)
+    k = 9
+    xp, xs = sol.debug_propose(surv, anc, k)
+    sig = np.array(cfg.sigma) * 0.98 ** k
+    for j in range(0, L, 7):
+        for i in range(scn["n"]):
+            parent = surv[anc[i, j], i]
+            assert np.array_equal(xp[j, i], parent)
+            ref = P.perturb_row(i, parent.astype(np.float64), j, k, cfg.seed, sig)
+            assert np.allclose(xs[j, i], ref, rtol=1e-5, atol=1e-4 * np.array([1.0, 1e-4, 1e-4])), (j, i)
+
+
+def test_init_population_parity(smc):
+    scn, cfg = sc.config(2)
+    L = 300
+    sol = _solver(smc, scn, L=L, seed=cfg.seed)
+    pop = sol.population()
+    ref = O.Problem(scn).init_population(L, cfg.seed)
+    assert np.allclose(pop["cur"], ref, rtol=1e-6, atol=1e-6)
+
+
+def test_round_replay_bitexact(smc):
+    """Real SMC rounds on the GPU (c1), replayed stage by stage through the
+    oracle: survivors' log-weights (tolerance), MH decisions on the GPU's
+    lambdas, ancestors on the GPU's ell, proposals on the GPU's survivors."""
+    scn, cfg = sc.config(1)
+    L, S = 256, 4
+    sol = _solver(smc, scn, L=L, S=S, K=10, seed=cfg.seed)
+    P = O.Problem(scn)
+    n = scn["n"]
+    for k in range(4):
+        before = sol.population() if k > 0 else None
+        sol.iterate(1)
+        pop = sol.population()
+        if k == 0:
+            ell_o = P.evaluate(pop["cur"].astype(np.float64), S, 0, cfg.seed)
+            assert np.all(pop["surv"] == 0)
+        else:
+            ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
+            ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
+            lam_c = np.where(np.isfinite(ell_c).all(1), ell_c.sum(1), -np.inf)
+            lam_p = np.where(np.isfinite(ell_p).all(1), ell_p.sum(1), -np.inf)
+            # MH replay on the GPU's own lambdas is bit-exact
+            lc_g, lp_g = pop["lam_cand"]
+            acc_ref = np.array([O.mh_accept(lc_g[l], lp_g[l], l, k, cfg.seed) for l in range(L)])
+            assert np.array_equal(pop["surv"].astype(bool), acc_ref)
+            # and the GPU's lambdas agree with the oracle's (tolerance) where both finite
+            for lg, lo in ((lc_g, lam_c), (lp_g, lam_p)):
+                f = np.isfinite(lg) & np.isfinite(lo)
+                assert (np.isfinite(lg) == np.isfinite(lo)).mean() > 0.99
+                assert np.allclose(lg[f], lo[f], rtol=0, atol=1e-4 * (np.abs(lo[f]).max() + n * S))
+            ell_o = np.where(pop["surv"][:, None] == 1, ell_p, ell_c)
+        ell_g = pop["ell"].T.astype(np.float64)
+        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
+        agree = np.isfinite(ell_o) == np.isfinite(ell_g)
+        assert agree.mean() > 0.99
+        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+        # resampling replay: the oracle on the GPU's survivor ell gives the GPU's ancestors
+        if k < 3:
+            anc_g, _ = sol.debug_resample(pop["ell"], k)
+            for i in range(n):
+                r = O.resample_column(pop["ell"][i].astype(np.float64), i, k, cfg.seed)
+                assert np.array_equal(anc_g[i], r["anc"])
+
+
+def test_select_and_plant_parity(smc):
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, L=256, S=4, K=6, seed=cfg.seed)
+    applied, nxt, flags = sol.mpc_step(scn["x0"])
+    pop = sol.population()
+    lam = pop["lam"]
+    best = O.select(lam)
+    assert best >= 0
+    P = O.Problem(scn)
+    ref_next, ref_flags, _, _ = P.plant_step(scn["x0"], applied.astype(np.float64), cfg.seed, 0)
+    assert np.allclose(nxt, ref_next, rtol=1e-12, atol=1e-9)
+    assert np.array_equal(flags.astype(np.int32), ref_flags)
+    ctrl = pop["prop"][best] if pop["surv"][best] else pop["cur"][best]
+    assert np.array_equal(applied, ctrl[:, 0, :])
