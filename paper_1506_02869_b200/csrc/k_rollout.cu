@@ -52,19 +52,52 @@ __device__ __forceinline__ float trilerp(const float *Wn, float fx, float fy, fl
     return lerp(lerp(a, b, fy), lerp(c, d, fy), fz);
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// atan2 on the MUFU reciprocal and a degree-15 odd polynomial (least-squares
+// fit of atan(a)/a on [0,1] in a^2; |error| < 1.5e-7 rad in binary32).
+__device__ __forceinline__ float fast_atan2(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mx > 0.0f ? mn * rcp_approx(mx) : 0.0f;
+    const float s = a * a;
+    float p = -0.0040731243789196014f;
+    p = fmaf(p, s, 0.021945973858237267f);
+    p = fmaf(p, s, -0.056062303483486176f);
+    p = fmaf(p, s, 0.0965619683265686f);
+    p = fmaf(p, s, -0.13915780186653137f);
+    p = fmaf(p, s, 0.19948504865169525f);
+    p = fmaf(p, s, -0.3333010673522949f);
+    p = fmaf(p, s, 0.999999463558197f);
+    float r = p * a;
+    r = ay > ax ? 1.57079632679489662f - r : r;
+    r = x < 0.0f ? kPi - r : r;
+    return copysignf(r, y);
+}
+
 template <int W, int NC, bool DEBUG>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 4)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
     constexpr int E = (16 + W - 1) / W;           // wind-field entries owned per lane
     extern __shared__ __align__(16) float smem[];
     const int H = sc.H, n = sc.n;
-    float *s_ctrl = smem;                                     // [H][NC][5][kBlock]
-    float *s_V = s_ctrl + H * NC * 5 * kBlock;                // [SEGS][16] normals
-    float *s_Z = s_V + SEGS * 16;                             // [SEGS][16] AR(1) state
-    float *s_W = s_Z + SEGS * 16;                             // [SEGS][16] wind at nodes
-    float4 *s_pos = reinterpret_cast<float4 *>(s_W + SEGS * 16);   // [NC][kBlock]
-    float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);   // [8][9]
+    float4 *s_ctrl = reinterpret_cast<float4 *>(smem);               // [H][NC][kBlock] (T, tan phi, sin g, cos g)
+    float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock); // [SEGS][16] normals
+    float *s_Z = s_V + SEGS * 16;                                     // [SEGS][16] AR(1) state
+    float *s_W = s_Z + SEGS * 16;                                     // [SEGS][16] wind at nodes
+    float4 *s_pos = reinterpret_cast<float4 *>(s_W + SEGS * 16);     // [NC][kBlock]
+    float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);     // [8][9]
 
     const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
     const uint32_t lloc = blockIdx.x * SEGS + seg;
@@ -75,32 +108,33 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
     if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Qhat[tid];
 
-    // ---- per-lane aircraft constants
-    DevAircraft A;
-    if (isac) A = sc.ac[lane];
-    else { A = sc.ac[0]; A.first_step = 1 << 20; A.Ha = 0; }
+    // ---- per-lane aircraft constants needed every step (the rest is read when needed)
+    const DevAircraft *Ap = sc.ac + (isac ? lane : 0);
+    const int kind = Ap->kind;
+    const int first = isac ? Ap->first_step : (1 << 20);
+    const float halfS = Ap->halfS, cd0 = Ap->cd0, cd2 = Ap->cd2, dt_eta = Ap->dt_eta;
+    const float zmin = Ap->z_min, zmax = Ap->z_max, vmin = Ap->v_min, vmax = Ap->v_max, mempty = Ap->m_empty;
+    const float gA = kind ? Ap->theta_F : Ap->beta_f;          // goal of the A/D term or the E term
+    const float z_tf = Ap->z_tf, v_D = Ap->v_D;
 
-    // ---- controls: derived trig terms to shared memory, envelope bits to registers
+    // ---- controls: (T, tan phi, sin gamma, cos gamma) to shared memory; envelope bits to registers
     uint32_t cbad[NC];
+    {
+        const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        cbad[c] = 0;
-        const float *src = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
-        for (int t = 0; t < H; ++t) {
-            float T = 0.f, ph = 0.f, ga = 0.f;
-            if (isac && valid) { T = src[3 * t]; ph = src[3 * t + 1]; ga = src[3 * t + 2]; }
-            float sph, cph, sga, cga;
-            sincosf(ph, &sph, &cph);
-            sincosf(ga, &sga, &cga);
-            float *d = s_ctrl + ((t * NC + c) * 5) * kBlock + tid;
-            d[0 * kBlock] = T;
-            d[1 * kBlock] = sph / cph;          // tan(phi): turn rate g tan(phi)/v
-            d[2 * kBlock] = 1.0f / cph;         // sec(phi): lift m g / cos(phi)
-            d[3 * kBlock] = sga;
-            d[4 * kBlock] = cga;
-            const bool bad = (fabsf(ga) > A.gamma_max) || !(fabsf(ph) < A.phi_max) ||
-                             (T < A.T_min) || (T > A.T_max);
-            cbad[c] |= (bad ? 1u : 0u) << t;
+        for (int c = 0; c < NC; ++c) {
+            cbad[c] = 0;
+            const float *src = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
+            for (int t = 0; t < H; ++t) {
+                float T = 0.f, ph = 0.f, ga = 0.f;
+                if (isac && valid) { T = src[3 * t]; ph = src[3 * t + 1]; ga = src[3 * t + 2]; }
+                float sph, cph, sga, cga;
+                sincosf(ph, &sph, &cph);
+                sincosf(ga, &sga, &cga);
+                s_ctrl[(t * NC + c) * kBlock + tid] = make_float4(T, sph / cph, sga, cga);
+                const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
+                cbad[c] |= (bad ? 1u : 0u) << t;
+            }
         }
     }
     __syncthreads();
@@ -110,21 +144,25 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     for (int c = 0; c < NC; ++c) ell[c] = args.ell0;
 
     const float dt = sc.dt, g = sc.g;
+    const float dtg = dt * g;
     for (uint32_t s = 0; s < args.S; ++s) {
         float x[NC], y[NC], z[NC], v[NC], chi[NC], m[NC], fuel[NC], sA[NC], sB[NC], sC[NC], sN[NC];
         bool landed[NC], viol[NC];
+        {
+            const float x0 = Ap->x0[0], y0 = Ap->x0[1], z0 = Ap->x0[2], v0 = Ap->x0[3], c0 = Ap->x0[4], m0 = Ap->x0[5];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            x[c] = A.x0[0]; y[c] = A.x0[1]; z[c] = A.x0[2]; v[c] = A.x0[3]; chi[c] = A.x0[4]; m[c] = A.x0[5];
-            fuel[c] = sA[c] = sB[c] = sC[c] = sN[c] = 0.0f;
-            landed[c] = false; viol[c] = false;
+            for (int c = 0; c < NC; ++c) {
+                x[c] = x0; y[c] = y0; z[c] = z0; v[c] = v0; chi[c] = c0; m[c] = m0;
+                fuel[c] = sA[c] = sB[c] = sC[c] = sN[c] = 0.0f;
+                landed[c] = false; viol[c] = false;
+            }
         }
         float Zr[E];
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
 
         for (int t = 0; t < H; ++t) {
-            // ---------------- 1. wind realisation for step t (Alg.1 l.10)
+            // ---------------- 1. wind realisation for step t (Alg.1 l.10, P:459-465)
             for (int b = lane; b < 4; b += W) {
                 const uint4 w = draw(TAG_WIND, l, x1, (uint32_t)t | ((uint32_t)b << 16), mpc, sc.key0, sc.key1);
                 const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
@@ -146,10 +184,13 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 const int e = lane + q * W;
                 if (e < 16) {
                     const int comp = e >> 3, node = e & 7;
-                    const float *zr = &s_Z[seg * 16 + comp * 8];
-                    float acc = 0.0f;
-#pragma unroll
-                    for (int mm = 0; mm < 8; ++mm) acc = fmaf(s_Q[node * 9 + mm], zr[mm], acc);
+                    const float4 z0 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8]);
+                    const float4 z1 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8 + 4]);
+                    const float *qr = &s_Q[node * 9];
+                    float acc = qr[0] * z0.x;
+                    acc = fmaf(qr[1], z0.y, acc); acc = fmaf(qr[2], z0.z, acc); acc = fmaf(qr[3], z0.w, acc);
+                    acc = fmaf(qr[4], z1.x, acc); acc = fmaf(qr[5], z1.y, acc); acc = fmaf(qr[6], z1.z, acc);
+                    acc = fmaf(qr[7], z1.w, acc);
                     s_W[seg * 16 + e] = acc;
                 }
             }
@@ -164,124 +205,121 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 }
             }
             // gusts (R15): one Philox call covers steps 2u and 2u+1
-            float gx = 0.0f, gy = 0.0f;
-            if (sc.turb_sigma > 0.0f && isac) {
+            float gx = sc.nominal[0], gy = sc.nominal[1];
+            if (sc.turb_sigma > 0.0f) {
+                float2 gg;
                 if ((t & 1) == 0) {
                     const uint4 w = draw(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.key0, sc.key1);
-                    const float2 g0 = box_muller(w.x, w.y);
+                    gg = box_muller(w.x, w.y);
                     gust_odd = box_muller(w.z, w.w);
-                    gx = g0.x; gy = g0.y;
                 } else {
-                    gx = gust_odd.x; gy = gust_odd.y;
+                    gg = gust_odd;
                 }
-                gx *= sc.turb_sigma; gy *= sc.turb_sigma;
+                gx = fmaf(sc.turb_sigma, gg.x, gx);
+                gy = fmaf(sc.turb_sigma, gg.y, gy);
             }
 
-            // ---------------- 2-3. dynamics and unary checks per candidate
-            const bool act = isac && (A.first_step <= t);
+            // ---------------- 2-3. dynamics, unary checks and geometry per candidate
+            const bool act = first <= t;
             bool fly[NC], vnow[NC], lnow[NC];
-            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC];
+            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 fly[c] = act && !landed[c] && !viol[c];
-                nx[c] = x[c]; ny[c] = y[c]; nz[c] = z[c]; nv[c] = v[c]; nchi[c] = chi[c]; nm[c] = m[c];
-                vnow[c] = false; lnow[c] = false; th[c] = 0.f; beta[c] = 0.f;
-                if (fly[c]) {
-                    const float *cc = s_ctrl + ((t * NC + c) * 5) * kBlock + tid;
-                    const float T = cc[0], tph = cc[kBlock], sec = cc[2 * kBlock], sga = cc[3 * kBlock], cga = cc[4 * kBlock];
-                    // wind at the pre-step position (trilinear, clamped to the box)
-                    const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
-                    const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
-                    const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
-                    const float wx = trilerp(Wn, fx, fy, fz) + sc.nominal[0] + gx;
-                    const float wy = trilerp(Wn + 8, fx, fy, fz) + sc.nominal[1] + gy;
-                    // Eq. hor with coordinated-turn lift and parabolic drag (R12)
-                    float rho = sc.rho_const;
-                    if (sc.density_mode == 0)
-                        rho = 1.225f * exp2f(4.2559f * __log2f(fmaxf(fmaf(-2.2558e-5f, z[c], 1.0f), 0.0f)));
-                    const float qd = rho * v[c] * v[c] * A.halfS;
-                    const float CL = __fdividef(m[c] * g * sec, qd);
-                    const float D = qd * fmaf(A.cd2, CL * CL, A.cd0);
-                    const float chr = chi[c] - kTwoPi * rintf(chi[c] * (1.0f / kTwoPi));
-                    float sch, cch;
-                    __sincosf(chr, &sch, &cch);
-                    const float vcg = v[c] * cga;
-                    nx[c] = x[c] + dt * fmaf(vcg, cch, wx);
-                    ny[c] = y[c] + dt * fmaf(vcg, sch, wy);
-                    nz[c] = z[c] + dt * v[c] * sga;
-                    nv[c] = v[c] + dt * (__fdividef(T - D, m[c]) - g * sga);
-                    nchi[c] = chi[c] + __fdividef(dt * g * tph, v[c]);
-                    nm[c] = m[c] - A.dt_eta * T;
-                    fuel[c] += A.dt_eta * T;
-                    // envelope and mass at j = t+1 (R17)
-                    bool bad = (cbad[c] >> t) & 1u;
-                    bad |= !(nz[c] >= A.z_min && nz[c] <= A.z_max);
-                    bad |= !(nv[c] >= A.v_min && nv[c] <= A.v_max);
-                    bad |= !(nm[c] >= A.m_empty);
-                    bad |= !(fabsf(nx[c]) <= 3.0e38f) || !(fabsf(ny[c]) <= 3.0e38f) || !(fabsf(nchi[c]) <= 3.0e38f);
-                    vnow[c] = bad;
-                    th[c] = atan2f(ny[c], nx[c]);
-                    if (A.kind == 0) {
-                        // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
-                        const float rh = sqrtf(fmaf(nx[c], nx[c], ny[c] * ny[c]));
-                        const float at = fabsf(th[c]);
-                        const float sarc = at > 1e-4f ? __fdividef(rh * at, __sinf(at)) : rh;
-                        beta[c] = atan2f(nz[c], sarc);
-                        if (!landed[c])
-                            lnow[c] = rh <= sc.P_runway && beta[c] <= sc.P_beta && at <= sc.P_chi &&
-                                      angdist(nchi[c] - kPi) <= sc.P_chi && nv[c] <= sc.P_vs;
-                    }
-                }
+                const float4 cc = s_ctrl[(t * NC + c) * kBlock + tid];
+                const float T = cc.x, tph = cc.y, sga = cc.z, cga = cc.w;
+                // wind at the pre-step position (trilinear, clamped to the box)
+                const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
+                const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
+                const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
+                const float wx = trilerp(Wn, fx, fy, fz) + gx;
+                const float wy = trilerp(Wn + 8, fx, fy, fz) + gy;
+                // Eq. hor, coordinated-turn lift and parabolic drag (R12):
+                // C_L^2 = (m g / q)^2 (1 + tan^2 phi)
+                float rho = sc.rho_const;
+                if (sc.density_mode == 0)
+                    rho = 1.225f * ex2_approx(4.2559f * __log2f(fmaxf(fmaf(-2.2558e-5f, z[c], 1.0f), 0.0f)));
+                const float qd = rho * v[c] * v[c] * halfS;
+                const float mgq = m[c] * g * rcp_approx(qd);
+                const float D = qd * fmaf(cd2 * mgq * mgq, fmaf(tph, tph, 1.0f), cd0);
+                const float chr = chi[c] - kTwoPi * rintf(chi[c] * (1.0f / kTwoPi));
+                float sch, cch;
+                __sincosf(chr, &sch, &cch);
+                const float vcg = v[c] * cga;
+                const float rm = rcp_approx(m[c]), rv = rcp_approx(v[c]);
+                nx[c] = fmaf(dt, fmaf(vcg, cch, wx), x[c]);
+                ny[c] = fmaf(dt, fmaf(vcg, sch, wy), y[c]);
+                nz[c] = fmaf(dt * v[c], sga, z[c]);
+                nv[c] = fmaf(dt, fmaf(T - D, rm, -g * sga), v[c]);
+                nchi[c] = fmaf(dtg * tph, rv, chi[c]);
+                nm[c] = fmaf(-dt_eta, T, m[c]);
+                // envelope and mass at j = t+1 (R17)
+                bool bad = (cbad[c] >> t) & 1u;
+                bad |= !(nz[c] >= zmin && nz[c] <= zmax);
+                bad |= !(nv[c] >= vmin && nv[c] <= vmax);
+                bad |= !(nm[c] >= mempty);
+                bad |= !(fabsf(nx[c]) <= 3.0e38f) || !(fabsf(ny[c]) <= 3.0e38f) || !(fabsf(nchi[c]) <= 3.0e38f);
+                vnow[c] = bad;
+                th[c] = fast_atan2(ny[c], nx[c]);
+                // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
+                const float r2 = fmaf(nx[c], nx[c], ny[c] * ny[c]);
+                rh[c] = r2 * rsqrtf(fmaxf(r2, 1e-30f));
+                const float at = fabsf(th[c]);
+                const float sarc = at > 1e-4f ? rh[c] * at * rcp_approx(__sinf(at)) : rh[c];
+                beta[c] = fast_atan2(nz[c], sarc);
+                lnow[c] = (kind == 0) && !landed[c] && rh[c] <= sc.P_runway && beta[c] <= sc.P_beta &&
+                          at <= sc.P_chi && angdist(nchi[c] - kPi) <= sc.P_chi && nv[c] <= sc.P_vs;
                 s_pos[c * kBlock + tid] = make_float4(nx[c], ny[c], nz[c], fly[c] ? 1.0f : 0.0f);
             }
             __syncwarp();
-            // ---------------- 4. separation (Eq. avoidance) against every other lane
+            // ---------------- 4. separation (Eq. avoidance) against every lane of the segment.
+            // The own lane always hits itself when present, so "conflict" = more than one hit.
+            int cnt[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                if (fly[c]) {
-                    const float4 *P = s_pos + c * kBlock + seg * W;
-                    bool conf = false;
-                    for (int p = 0; p < n; ++p) {
-                        const float4 q = P[p];
-                        const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
-                        const bool hit = (q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh);
-                        conf |= hit && (p != lane);
-                    }
-                    vnow[c] |= conf;
+            for (int c = 0; c < NC; ++c) cnt[c] = 0;
+#pragma unroll
+            for (int p = 0; p < W; ++p) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const float4 q = s_pos[c * kBlock + seg * W + p];
+                    const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
+                    cnt[c] += ((q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh)) ? 1 : 0;
                 }
             }
-            // ---------------- 5. per-step cost terms at j = t+1
+            // ---------------- 5. per-step cost terms at j = t+1, state update
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                if (act) {
-                    if (fly[c]) {
-                        if (A.kind == 1) {
-                            sA[c] += angdist(th[c] - A.theta_F);
-                            sB[c] += fabsf(A.z_tf - nz[c]);
-                            sC[c] += fabsf(nv[c] - A.v_D);
-                        } else {
-                            sA[c] += angdist(nchi[c] - kPi - 2.0f * th[c]);
-                            sB[c] += fabsf(beta[c] - A.beta_f);
-                        }
-                        if (sc.has_noise) {
-                            const float zz = nz[c] * sc.inv_Ac;
-                            sN[c] += 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, nx[c], ny[c]);
-                        }
-                    } else if (landed[c]) {
-                        sN[c] += 1.0f;      // "best possible cost, 1, for all remaining steps"
-                    }
+                vnow[c] = vnow[c] || (cnt[c] > 1);
+                // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
+                // arrival:   D = |wrap(chi - chi_hat)|, chi_hat = pi + 2 theta (R8); E = |beta - beta_f|
+                const float devA = angdist(kind ? th[c] - gA : nchi[c] - kPi - 2.0f * th[c]);
+                const float devB = kind ? fabsf(z_tf - nz[c]) : fabsf(beta[c] - gA);
+                const float devC = fabsf(nv[c] - v_D);
+                float nzs = 0.0f;
+                if (sc.has_noise) {
+                    const float zz = nz[c] * sc.inv_Ac;
+                    nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, nx[c], ny[c]);
                 }
-                if (fly[c]) {
-                    viol[c] = viol[c] || vnow[c];
-                    landed[c] = landed[c] || lnow[c];
-                    x[c] = nx[c]; y[c] = ny[c]; z[c] = nz[c]; v[c] = nv[c]; chi[c] = nchi[c]; m[c] = nm[c];
-                }
+                sA[c] += fly[c] ? devA : 0.0f;
+                sB[c] += fly[c] ? devB : 0.0f;
+                sC[c] += fly[c] ? devC : 0.0f;
+                // "best possible cost, 1, for all remaining steps" after landing
+                sN[c] += fly[c] ? nzs : ((act && landed[c]) ? 1.0f : 0.0f);
+                fuel[c] += fly[c] ? dt_eta * s_ctrl[(t * NC + c) * kBlock + tid].x : 0.0f;
+                viol[c] = viol[c] || (fly[c] && vnow[c]);
+                landed[c] = landed[c] || (fly[c] && lnow[c]);
+                x[c] = fly[c] ? nx[c] : x[c];
+                y[c] = fly[c] ? ny[c] : y[c];
+                z[c] = fly[c] ? nz[c] : z[c];
+                v[c] = fly[c] ? nv[c] : v[c];
+                chi[c] = fly[c] ? nchi[c] : chi[c];
+                m[c] = fly[c] ? nm[c] : m[c];
                 if (DEBUG && c == 0 && valid && isac && args.dbg_traj) {
                     float *tr = args.dbg_traj + ((((size_t)lloc * args.S + s) * n + lane) * (H + 1) + t + 1) * 6;
                     tr[0] = x[c]; tr[1] = y[c]; tr[2] = z[c]; tr[3] = v[c]; tr[4] = chi[c]; tr[5] = m[c];
                     if (t == 0) {
                         float *t0 = tr - 6;
-                        for (int a = 0; a < 6; ++a) t0[a] = A.x0[a];
+                        for (int a = 0; a < 6; ++a) t0[a] = Ap->x0[a];
                     }
                 }
                 if (DEBUG && c == 0 && valid && isac && args.dbg_landed && lnow[c] && fly[c])
@@ -290,33 +328,40 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         }  // t
 
         // ---------------- utility J_T and weight
+        {
+            const int Ha = Ap->Ha;
+            const float invHa = Ap->invHa, invFmax = Ap->invFmax;
+            const float supB = Ap->supB, invDenB = Ap->invDenB, invSupC = Ap->invSupC, invSupE = Ap->invSupE;
+            const int flagB = Ap->flagB;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            float J = 1.0f, c0 = 1.f, c1 = 1.f, c2 = 1.f, c3 = 1.f;
-            if (A.Ha > 0) {
-                const float Jfuel = clamp01(1.0f - fuel[c] * A.invFmax);
-                if (A.kind == 1) {
-                    c0 = clamp01(1.0f - sA[c] * A.invHa * (1.0f / kPi));
-                    c1 = Jfuel;
-                    c2 = A.flagB ? 1.0f : clamp01((A.supB - sB[c] * A.invHa) * A.invDenB);
-                    c3 = clamp01(1.0f - sC[c] * A.invHa * A.invSupC);
-                    J = sc.alpha_dep[0] * c0 + sc.alpha_dep[1] * c1 + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
-                } else {
-                    c0 = clamp01(1.0f - sA[c] * A.invHa * (1.0f / kPi));
-                    c1 = clamp01(1.0f - sB[c] * A.invHa * A.invSupE);
-                    c2 = Jfuel;
-                    c3 = 0.0f;
-                    J = sc.alpha_arr[0] * c0 + sc.alpha_arr[1] * c1 + sc.alpha_arr[2] * c2;
+            for (int c = 0; c < NC; ++c) {
+                float J = 1.0f, c0 = 1.f, c1 = 1.f, c2 = 1.f, c3 = 1.f;
+                if (Ha > 0 && isac) {
+                    const float Jfuel = clamp01(1.0f - fuel[c] * invFmax);
+                    const float J1 = clamp01(1.0f - sA[c] * invHa * (1.0f / kPi));
+                    if (kind == 1) {
+                        c0 = J1;
+                        c1 = Jfuel;
+                        c2 = flagB ? 1.0f : clamp01((supB - sB[c] * invHa) * invDenB);
+                        c3 = clamp01(1.0f - sC[c] * invHa * invSupC);
+                        J = sc.alpha_dep[0] * c0 + sc.alpha_dep[1] * c1 + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
+                    } else {
+                        c0 = J1;
+                        c1 = clamp01(1.0f - sB[c] * invHa * invSupE);
+                        c2 = Jfuel;
+                        c3 = 0.0f;
+                        J = sc.alpha_arr[0] * c0 + sc.alpha_arr[1] * c1 + sc.alpha_arr[2] * c2;
+                    }
+                    if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * sN[c] * invHa;
                 }
-                if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * sN[c] * A.invHa;
-            }
-            ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + log2f(J);
-            if (DEBUG && c == 0 && valid && isac) {
-                const size_t o = ((size_t)lloc * args.S + s) * n + lane;
-                if (args.dbg_J) args.dbg_J[o] = J;
-                if (args.dbg_viol) args.dbg_viol[o] = viol[c] ? 1 : 0;
-                if (args.dbg_fuel) args.dbg_fuel[o] = fuel[c];
-                if (args.dbg_comp) { float *cp = args.dbg_comp + 4 * o; cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3; }
+                ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + log2f(J);
+                if (DEBUG && c == 0 && valid && isac) {
+                    const size_t o = ((size_t)lloc * args.S + s) * n + lane;
+                    if (args.dbg_J) args.dbg_J[o] = J;
+                    if (args.dbg_viol) args.dbg_viol[o] = viol[c] ? 1 : 0;
+                    if (args.dbg_fuel) args.dbg_fuel[o] = fuel[c];
+                    if (args.dbg_comp) { float *cp = args.dbg_comp + 4 * o; cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3; }
+                }
             }
         }
     }  // s
@@ -372,8 +417,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
 size_t rollout_smem_bytes(int W, int NC, int H) {
     const int SEGS = kBlock / W;
-    return sizeof(float) * ((size_t)H * NC * 5 * kBlock + 3 * SEGS * 16) + sizeof(float4) * NC * kBlock +
-           sizeof(float) * 72 + 16;
+    return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * 3 * SEGS * 16 +
+           sizeof(float4) * NC * kBlock + sizeof(float) * 72 + 16;
 }
 
 template <int W, int NC, bool DEBUG>

@@ -35,7 +35,7 @@ def _solver(smc, scn, L=64, S=4, K=3, seed=0x5EED0001, **kw):
     return smc.Solver(scn, L=L, S=S, K=K, sigma=sig, seed=seed, **kw)
 
 
-def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, max_ambiguous=0.02):
+def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, max_ambiguous=0.05):
     sol = _solver(smc, scn, L=max(L, 1), S=S, seed=seed)
     P = O.Problem(scn)
     g = sol.debug_rollout(ctrl, S, k, l0=l0, traj=True)
@@ -101,20 +101,27 @@ def test_rollout_parity(smc, case):
 
 
 def test_rollout_landing_exercised(smc):
-    """An arrival set up to land mid-horizon: landing step and frozen state agree."""
+    """Arrivals set up to land mid-horizon (near-trimmed 3 deg descent along the
+    runway axis): landing step and frozen state agree with the oracle."""
     scn = sc.small(1, 1, H=8, seed=2)
     DEG = math.pi / 180
     scn["x0"][0] = [7000.0, 300.0, 7000 * math.tan(3 * DEG), 76.0, math.pi, 64000.0]
+    scn["x0"][1] = [-20000.0, -20000.0, 5000.0, 140.0, -2.3, 70000.0]
+    P = O.Problem(scn)
+    rng = np.random.default_rng(1)
     L = 64
     ctrl = np.zeros((L, 2, 8, 3), np.float32)
-    rng = np.random.default_rng(1)
-    ctrl[:, 0, :, 0] = rng.uniform(15000, 30000, (L, 8))
-    ctrl[:, 0, :, 2] = -3 * DEG + rng.uniform(-0.01, 0.01, (L, 8))
+    for l in range(L):
+        st = scn["x0"][0].copy()
+        for t in range(8):
+            _, D = P.lift_drag(0, st, 0.0)
+            g = -3 * DEG + rng.uniform(-0.005, 0.005)
+            ctrl[l, 0, t] = [D + st[5] * 9.81 * math.sin(g) + rng.uniform(-2000, 2000), rng.uniform(-0.01, 0.01), g]
+            st = P.step(0, st, ctrl[l, 0, t].astype(np.float64))
     ctrl[:, 1, :, 0] = 50000.0
-    checked, _ = _compare_rollouts(smc, scn, L, 2, k=0, seed=7, ctrl=ctrl)
-    sol = _solver(smc, scn, L=L, S=2)
-    g = sol.debug_rollout(ctrl, 2, 0)
-    assert (g["landed"][:, :, 0] > 0).any()
+    landed_o = sum(P.rollout(ctrl[l].astype(np.float64), l, 0, 0, 7)["landed_step"][0] > 0 for l in range(L))
+    assert landed_o > L // 4
+    _compare_rollouts(smc, scn, L, 2, k=0, seed=7, ctrl=ctrl)
 
 
 def test_evaluate_parity(smc):

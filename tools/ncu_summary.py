@@ -1,0 +1,29 @@
+"""Summarise an ncu launch-list CSV (gpu__time_duration.sum) into per-kernel totals/shares."""
+import csv
+import sys
+from collections import defaultdict
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = None
+tot = defaultdict(float)
+cnt = defaultdict(int)
+for r in rows:
+    if "Kernel Name" in r:
+        hdr = r
+        continue
+    if hdr is None or len(r) != len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    name = d["Kernel Name"].split("(")[0]
+    v = float(d["Metric Value"].replace(",", ""))
+    unit = d.get("Metric Unit", "")
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+    tot[name] += v * scale
+    cnt[name] += 1
+T = sum(tot.values())
+print(f"{'kernel':60s} {'launches':>8s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}")
+for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+    print(f"{k[:60]:60s} {cnt[k]:8d} {v:12.1f} {v / cnt[k]:10.2f} {v / T:7.3f}")
+print(f"{'TOTAL':60s} {sum(cnt.values()):8d} {T:12.1f}")
