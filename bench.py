@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-graph", action="store_true")
     return ap.parse_args()
 
 
@@ -194,7 +195,8 @@ def main():
     scn, cfg = sc.config(args.config)
     stream = torch.cuda.Stream(device=local)
     sol = smcatm.Solver(scn, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed + rank,
-                        anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True)
+                        anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True,
+                        use_graph=not args.no_graph)
     S_list = [cfg.S] * cfg.K
     ac_steps = roofline.aircraft_steps(scn, cfg.L, S_list, cfg.mh)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -281,6 +283,7 @@ def main():
                                f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
                    "parallelism": f"weak: {world} independent MPC problem(s), one per GPU",
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "cuda_graph": not args.no_graph,
                    "aircraft_steps_per_step": ac_steps},
         "mpc_step_latency_ms": tmax_ms / args.steps,
         "step_ms": step_ms,

@@ -28,7 +28,7 @@ constexpr uint32_t kCentreCap = 256;
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, status2, tiles, marks, anc, accept, dac, pop, centres,
+    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
 };
 
@@ -47,11 +47,12 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax) {
     o.Q = take(nmax * sizeof(unsigned long long));
     o.ess = take(2 * nmax * sizeof(double));
     o.status = take((size_t)nmax * scan_tiles(Lloc) * 8);
-    o.status2 = take((size_t)nmax * scan_tiles(Lloc) * 8);
     o.tiles = take(2 * nmax * sizeof(uint32_t));
-    o.marks = take((size_t)nmax * Lloc * sizeof(int32_t));
-    o.anc = take((size_t)nmax * Lloc * sizeof(int32_t));
+    o.C = take((size_t)nmax * Lloc * sizeof(unsigned long long));
+    o.QR = take(2 * nmax * sizeof(unsigned long long));
+    o.anc = 0;
     o.accept = take(8);
+    o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
     o.pop = take(kPopCap * sizeof(float));
     o.centres = take(kCentreCap * 3 * sizeof(double));
@@ -98,9 +99,9 @@ struct smc_ctx {
     double *lam = nullptr, *lam2 = nullptr;
     uint8_t *surv = nullptr;
     uint32_t *colmax = nullptr, *tiles = nullptr;
-    unsigned long long *Q = nullptr, *status = nullptr, *status2 = nullptr, *accept = nullptr;
+    unsigned long long *Q = nullptr, *status = nullptr, *accept = nullptr, *C = nullptr, *QR = nullptr;
     double *ess = nullptr;
-    int32_t *marks = nullptr, *anc = nullptr;
+    uint32_t *mpc_dev = nullptr;
     DevAircraft *dac = nullptr;
     float *pop = nullptr, *best_row = nullptr, *papplied = nullptr, *lohi = nullptr;
     double *centres = nullptr, *part_lam = nullptr, *best_lam = nullptr, *pZ = nullptr, *pstates = nullptr,
@@ -116,15 +117,36 @@ struct smc_ctx {
     std::vector<smc_aircraft_type> types;
     std::vector<double> centres_h;
     smc_scenario scn{};
-    uint32_t k = 0, mpc = 0;
+    uint32_t k = 0, mpc = 0, mpc_stage = 0;
+    bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used[4];
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_graph[4];   // timing nodes inside the captured graph
+    double phase_ms_acc[4] = {0, 0, 0, 0};
     uint64_t phase_launches[4] = {0, 0, 0, 0};
+    // CUDA graph of one device-resident MPC update (smc_solve)
+    bool capturing = false, graph_ok = false;
+    int graph_adv = -1;
+    uint32_t graph_K = 0, g_k = 0;
+    int g_cur = 0, g_last = -1;
+    uint64_t g_launches = 0, g_phase_launches[4] = {0, 0, 0, 0};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    void drop_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        gexec = nullptr; graph = nullptr; graph_ok = false;
+        for (auto &v : ev_graph) {
+            for (auto &p : v) { ev_free.push_back(p.first); ev_free.push_back(p.second); }
+            v.clear();
+        }
+    }
     ~smc_ctx() {
+        drop_graph();
         for (auto &v : ev_used)
             for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
         for (auto e : ev_free) cudaEventDestroy(e);
@@ -157,9 +179,11 @@ static smc_status fail(smc_ctx *c, smc_status s, const char *fmt, ...) {
         ++ctx->launches;                                                                           \
         ++ctx->phase_launches[phase];                                                              \
         cudaEvent_t _e0 = nullptr, _e1 = nullptr;                                                  \
-        if (ctx->cfg.profile) { _e0 = ctx->get_event(); _e1 = ctx->get_event(); CK(cudaEventRecord(_e0, ctx->st)); } \
+        if (ctx->cfg.profile) { _e0 = ctx->get_event(); _e1 = ctx->get_event();                   \
+                                CK(cudaEventRecordWithFlags(_e0, ctx->st, ctx->capturing ? cudaEventRecordExternal : 0)); } \
         CK(expr);                                                                                  \
-        if (ctx->cfg.profile) { CK(cudaEventRecord(_e1, ctx->st)); ctx->ev_used[phase].push_back({_e0, _e1}); } \
+        if (ctx->cfg.profile) { CK(cudaEventRecordWithFlags(_e1, ctx->st, ctx->capturing ? cudaEventRecordExternal : 0)); \
+                                (ctx->capturing ? ctx->ev_graph[phase] : ctx->ev_used[phase]).push_back({_e0, _e1}); } \
     } while (0)
 #define LAUNCH(expr) LAUNCHP(3, expr)
 enum { PH_ROLLOUT = 0, PH_RESAMPLE = 1, PH_PROPOSE = 2, PH_OTHER = 3 };
@@ -247,11 +271,11 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->Q = (unsigned long long *)(ws + L.Q);
     ctx->ess = (double *)(ws + L.ess);
     ctx->status = (unsigned long long *)(ws + L.status);
-    ctx->status2 = (unsigned long long *)(ws + L.status2);
     ctx->tiles = (uint32_t *)(ws + L.tiles);
-    ctx->marks = (int32_t *)(ws + L.marks);
-    ctx->anc = (int32_t *)(ws + L.anc);
+    ctx->C = (unsigned long long *)(ws + L.C);
+    ctx->QR = (unsigned long long *)(ws + L.QR);
     ctx->accept = (unsigned long long *)(ws + L.accept);
+    ctx->mpc_dev = (uint32_t *)(ws + L.mpc);
     ctx->dac = (DevAircraft *)(ws + L.dac);
     ctx->pop = (float *)(ws + L.pop);
     ctx->centres = (double *)(ws + L.centres);
@@ -286,6 +310,17 @@ extern "C" smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t m) {
     if (!ctx) return SMC_EINVAL;
     if (m >= (1u << 24)) return fail(ctx, SMC_EINVAL, "mpc index must be < 2^24");
     ctx->mpc = m;
+    ctx->mpc_dirty = true;
+    return SMC_OK;
+}
+
+// The MPC step index keys every stream; kernels read it from device memory so
+// a captured graph stays valid across MPC steps.
+static smc_status sync_mpc(smc_ctx *ctx) {
+    if (!ctx->mpc_dirty) return SMC_OK;
+    ctx->mpc_stage = ctx->mpc;
+    CK(cudaMemcpyAsync(ctx->mpc_dev, &ctx->mpc_stage, sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->st));
+    ctx->mpc_dirty = false;
     return SMC_OK;
 }
 
@@ -418,7 +453,9 @@ static smc_status build_constants(smc_ctx *ctx) {
 }
 
 static smc_status init_population(smc_ctx *ctx) {
-    PopArgs pa{ctx->dsc.n, ctx->dsc.H, ctx->Lloc, ctx->l0, 0u, ctx->mpc, ctx->dsc.key0, ctx->dsc.key1};
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
+    PopArgs pa{ctx->dsc.n, ctx->dsc.H, ctx->Lloc, ctx->l0, 0u, ctx->dsc.key0, ctx->dsc.key1, ctx->mpc_dev};
     LAUNCH(launch_init_population(ctx->dsc, pa, ctx->ctrl[0][0], ctx->st));
     ctx->k = 0;
     ctx->cur = 0;
@@ -459,6 +496,7 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));
+    ctx->drop_graph();
     ctx->have_scn = true;
     return init_population(ctx);
 }
@@ -473,6 +511,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     const uint32_t k = ctx->k;
     const int n = ctx->dsc.n, H = ctx->dsc.H;
     const int P = ctx->cur;
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
     const uint32_t S = samples_of(ctx, k);
     CK(cudaMemsetAsync(ctx->colmax, 0, sizeof(uint32_t) * n, ctx->st));
     CK(cudaMemsetAsync(ctx->accept, 0, 8, ctx->st));
@@ -485,35 +525,33 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     } else {
         NC = 1; ra.ctrl[0] = ctx->ctrl[P][1]; ra.ctrl[1] = nullptr; ra.surv_single = 1;
     }
-    ra.L = ctx->Lloc; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpc = ctx->mpc;
+    ra.L = ctx->Lloc; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpcp = ctx->mpc_dev;
     ra.ell0 = (float)(-std::log2((double)ctx->Lg));
     ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
     ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
     LAUNCHP(PH_ROLLOUT, launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
-    const bool need_q = tail || stats;
     ResampleArgs rs{};
-    rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.mpc = ctx->mpc; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1;
+    rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
     rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
-    rs.status2 = ctx->status2; rs.tile_ctr = ctx->tiles; rs.marks = ctx->marks; rs.anc = ctx->anc;
-    if (need_q) {
-        CK(cudaMemsetAsync(ctx->Q, 0, 8 * n, ctx->st));
+    rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR;
+    if (stats) {
         CK(cudaMemsetAsync(ctx->ess, 0, 16 * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->Q, 0, 8 * n, ctx->st));
+        rs.Q = ctx->Q;
         LAUNCHP(PH_RESAMPLE, launch_qsum(rs, ctx->st));
     }
     if (tail) {
         const size_t nt = (size_t)scan_tiles(ctx->Lloc);
         CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
-        CK(cudaMemsetAsync(ctx->status2, 0, 8 * nt * n, ctx->st));
-        CK(cudaMemsetAsync(ctx->tiles, 0, 8 * n, ctx->st));
-        CK(cudaMemsetAsync(ctx->marks, 0xFF, sizeof(int32_t) * n * (size_t)ctx->Lloc, ctx->st));
-        LAUNCHP(PH_RESAMPLE, launch_scan_mark(rs, ctx->st));
-        LAUNCHP(PH_RESAMPLE, launch_maxscan(rs, ctx->st));
+        CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
+        rs.Q = nullptr;
+        LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
         ProposeArgs pa{};
-        pa.n = n; pa.H = H; pa.L = ctx->Lloc; pa.l0 = ctx->l0; pa.k = k; pa.mpc = ctx->mpc;
+        pa.n = n; pa.H = H; pa.L = ctx->Lloc; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
-        pa.surv = ctx->surv; pa.anc = ctx->anc;
+        pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
         pa.xp = ctx->ctrl[P ^ 1][0]; pa.xs = ctx->ctrl[P ^ 1][1];
         const double f = std::pow(ctx->cfg.anneal, (double)k);
         for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
@@ -592,9 +630,7 @@ extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *
     return SMC_OK;
 }
 
-extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
-    if (!ctx) return SMC_EINVAL;
-    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_solve before smc_set_scenario");
+static smc_status solve_body(smc_ctx *ctx, uint32_t advance_plant) {
     smc_status s = init_population(ctx);                       // fresh population (R31)
     if (s != SMC_OK) return s;
     const uint32_t K = ctx->cfg.n_rounds ? ctx->cfg.n_rounds : 1;
@@ -605,9 +641,53 @@ extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
     s = select_best(ctx);
     if (s != SMC_OK) return s;
     if (advance_plant) {
-        PlantArgs pa{ctx->dsc.n, ctx->mpc, ctx->dsc.key0, ctx->dsc.key1, ctx->pstates, ctx->best_row, ctx->dsc.H,
+        PlantArgs pa{ctx->dsc.n, ctx->dsc.key0, ctx->dsc.key1, ctx->mpc_dev, ctx->pstates, ctx->best_row, ctx->dsc.H,
                      ctx->pZ, ctx->pzi, ctx->pnext, ctx->pflags, ctx->papplied, ctx->best_idx};
         LAUNCH(launch_plant(ctx->psc, pa, ctx->st));
+    }
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
+    if (!ctx) return SMC_EINVAL;
+    if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_solve before smc_set_scenario");
+    if (!ctx->cfg.use_graph || ctx->st == nullptr) return solve_body(ctx, advance_plant);
+    smc_status s = sync_mpc(ctx);                              // outside the graph: mpc is read from device memory
+    if (s != SMC_OK) return s;
+    const uint32_t K = ctx->cfg.n_rounds ? ctx->cfg.n_rounds : 1;
+    if (!ctx->graph_ok || ctx->graph_adv != (int)advance_plant || ctx->graph_K != K) {
+        ctx->drop_graph();
+        const uint64_t l0 = ctx->launches;
+        uint64_t p0[4];
+        for (int q = 0; q < 4; ++q) p0[q] = ctx->phase_launches[q];
+        CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        s = solve_body(ctx, advance_plant);
+        ctx->capturing = false;
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->st, &g);
+        if (s != SMC_OK) { if (g) cudaGraphDestroy(g); return s; }
+        if (e != cudaSuccess) return fail(ctx, SMC_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        ctx->graph = g;
+        CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+        ctx->g_k = ctx->k; ctx->g_cur = ctx->cur; ctx->g_last = ctx->last_eval;
+        ctx->g_launches = ctx->launches - l0;
+        ctx->launches = l0;
+        for (int q = 0; q < 4; ++q) { ctx->g_phase_launches[q] = ctx->phase_launches[q] - p0[q]; ctx->phase_launches[q] = p0[q]; }
+        ctx->graph_ok = true; ctx->graph_adv = (int)advance_plant; ctx->graph_K = K;
+    }
+    CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+    ctx->k = ctx->g_k; ctx->cur = ctx->g_cur; ctx->last_eval = ctx->g_last;
+    ctx->launches += ctx->g_launches;
+    for (int q = 0; q < 4; ++q) ctx->phase_launches[q] += ctx->g_phase_launches[q];
+    if (ctx->cfg.profile) {                                    // read the graph's timing nodes now (they are reused)
+        CK(cudaStreamSynchronize(ctx->st));
+        for (int q = 0; q < 4; ++q)
+            for (auto &pr : ctx->ev_graph[q]) {
+                float t = 0.f;
+                CK(cudaEventElapsedTime(&t, pr.first, pr.second));
+                ctx->phase_ms_acc[q] += t;
+            }
     }
     return SMC_OK;
 }
@@ -634,6 +714,7 @@ extern "C" smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_cont
         for (int i = 0; i < n; ++i) flags[i] = (uint32_t)fl[i];
     const uint32_t m = ctx->mpc;
     ctx->mpc += 1;
+    ctx->mpc_dirty = true;
     if (bi < 0) return fail(ctx, SMC_EINFEASIBLE, "MPC step %u: every particle has a zero weight (P:423)", m);
     return SMC_OK;
 }
@@ -651,6 +732,8 @@ extern "C" smc_status smc_phase_times(smc_ctx *ctx, double ms[4], uint64_t launc
             ctx->ev_free.push_back(pr.second);
         }
         ctx->ev_used[p].clear();
+        tot += ctx->phase_ms_acc[p];
+        ctx->phase_ms_acc[p] = 0.0;
         if (ms) ms[p] = tot;
         if (launches) launches[p] = ctx->phase_launches[p];
         ctx->phase_launches[p] = 0;
@@ -698,7 +781,9 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     CK(cudaMemsetAsync(dcm, 0, 4 * n, ctx->st));
     if (dland) CK(cudaMemsetAsync(dland, 0xFF, sizeof(int32_t) * nu, ctx->st));
     RolloutArgs ra{};
-    ra.ctrl[0] = dctrl; ra.L = L; ra.l0 = l0; ra.S = S; ra.k = k; ra.mpc = ctx->mpc;
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
+    ra.ctrl[0] = dctrl; ra.L = L; ra.l0 = l0; ra.S = S; ra.k = k; ra.mpcp = ctx->mpc_dev;
     ra.ell0 = (float)(-std::log2((double)L));
     ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
     ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
@@ -746,7 +831,9 @@ extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const do
     CK(cudaMemcpyAsync(a, lam_cur, 8 * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemcpyAsync(b, lam_prop, 8 * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
     const uint32_t key0 = (uint32_t)ctx->cfg.seed, key1 = (uint32_t)(ctx->cfg.seed >> 32);
-    LAUNCH(launch_mh_debug(a, b, L, k, ctx->mpc, key0, key1, o, ctx->st));
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
+    LAUNCH(launch_mh_debug(a, b, L, k, ctx->mpc_dev, key0, key1, o, ctx->st));
     CK(cudaMemcpyAsync(acc, o, L, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return SMC_OK;
@@ -755,36 +842,34 @@ extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const do
 extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t k,
                                          int32_t *anc, uint64_t *Q) {
     if (!ctx || !ell || !anc || N == 0 || N > 32 || L == 0 || L >= (1u << 30)) return SMC_EINVAL;
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
     DevTmp tmp;
     const int nt = scan_tiles(L);
     float *dell = tmp.alloc<float>((size_t)N * L);
     uint32_t *dcm = tmp.alloc<uint32_t>(N);
     unsigned long long *dQ = tmp.alloc<unsigned long long>(N);
+    unsigned long long *dQR = tmp.alloc<unsigned long long>(2 * N);
+    unsigned long long *dC = tmp.alloc<unsigned long long>((size_t)N * L);
     double *dess = tmp.alloc<double>(2 * N);
     unsigned long long *st1 = tmp.alloc<unsigned long long>((size_t)N * nt);
-    unsigned long long *st2 = tmp.alloc<unsigned long long>((size_t)N * nt);
     uint32_t *tiles = tmp.alloc<uint32_t>(2 * N);
-    int32_t *marks = tmp.alloc<int32_t>((size_t)N * L);
     int32_t *danc = tmp.alloc<int32_t>((size_t)N * L);
-    if (!dell || !dcm || !dQ || !dess || !st1 || !st2 || !tiles || !marks || !danc)
+    if (!dell || !dcm || !dQ || !dQR || !dC || !dess || !st1 || !tiles || !danc)
         return fail(ctx, SMC_ECUDA, "debug allocation failed");
     CK(cudaMemcpyAsync(dell, ell, sizeof(float) * N * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemsetAsync(dcm, 0, 4 * N, ctx->st));
     CK(cudaMemsetAsync(dQ, 0, 8 * N, ctx->st));
-    CK(cudaMemsetAsync(dess, 0, 16 * N, ctx->st));
     CK(cudaMemsetAsync(st1, 0, 8 * (size_t)N * nt, ctx->st));
-    CK(cudaMemsetAsync(st2, 0, 8 * (size_t)N * nt, ctx->st));
     CK(cudaMemsetAsync(tiles, 0, 8 * N, ctx->st));
-    CK(cudaMemsetAsync(marks, 0xFF, 4 * (size_t)N * L, ctx->st));
     LAUNCH(launch_colmax(dell, (int)N, L, dcm, ctx->st));
     ResampleArgs rs{};
-    rs.n = (int)N; rs.L = L; rs.k = k; rs.mpc = ctx->mpc;
+    rs.n = (int)N; rs.L = L; rs.k = k; rs.mpcp = ctx->mpc_dev;
     rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
-    rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1; rs.status2 = st2;
-    rs.tile_ctr = tiles; rs.marks = marks; rs.anc = danc;
-    LAUNCH(launch_qsum(rs, ctx->st));
-    LAUNCH(launch_scan_mark(rs, ctx->st));
-    LAUNCH(launch_maxscan(rs, ctx->st));
+    rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
+    rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc;
+    LAUNCH(launch_scan(rs, ctx->st));
+    LAUNCH(launch_ancestors(rs, ctx->st));
     CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * L, cudaMemcpyDeviceToHost, ctx->st));
     if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -806,7 +891,9 @@ extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, co
     CK(cudaMemcpyAsync(danc, anc, sizeof(int32_t) * n * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemsetAsync(dsurv, 0, L, ctx->st));
     ProposeArgs pa{};
-    pa.n = n; pa.H = H; pa.L = L; pa.l0 = 0; pa.k = k; pa.mpc = ctx->mpc;
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
+    pa.n = n; pa.H = H; pa.L = L; pa.l0 = 0; pa.k = k; pa.mpcp = ctx->mpc_dev;
     pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
     pa.src[0] = src; pa.src[1] = src; pa.surv = dsurv; pa.anc = danc; pa.xp = dxp; pa.xs = dxs;
     const double f = std::pow(ctx->cfg.anneal, (double)k);

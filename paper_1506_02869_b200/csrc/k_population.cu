@@ -24,7 +24,7 @@ __global__ void k_init_population(const DevScen sc, const PopArgs p, float *ctrl
         const int t = idx % p.H;
         const int i = (idx / p.H) % p.n;
         const uint32_t l = p.l0 + (uint32_t)(idx / ((size_t)p.H * p.n));
-        const uint4 w = draw(TAG_INIT, l, 0u, (uint32_t)t | ((uint32_t)i << 8), p.mpc, p.key0, p.key1);
+        const uint4 w = draw(TAG_INIT, l, 0u, (uint32_t)t | ((uint32_t)i << 8), *p.mpcp, p.key0, p.key1);
         const DevAircraft &A = sc.ac[i];
         float *c = ctrl + idx * 3;
         c[0] = A.T_min + (A.T_max - A.T_min) * unif(w.x);
@@ -190,7 +190,10 @@ __device__ unsigned long long block_exclusive(unsigned long long v, unsigned lon
 }
 
 // ============================================================== K4b
-__global__ void __launch_bounds__(kScanThreads) k_scan_mark(const ResampleArgs r, int ntiles) {
+// Inclusive scan C_l = sum_{l' <= l} q_l' per column (uint64, exact), single pass
+// with decoupled look-back.  The block that owns the last tile of a column also
+// publishes (Q, R): Q = C_{L-1}, R = floor(r64 * Q / 2^64) (RESAMPLE stream).
+__global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int ntiles) {
     const int i = blockIdx.y;
     __shared__ int s_tile;
     __shared__ unsigned long long s_pre;
@@ -202,13 +205,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_mark(const ResampleArgs r
     const float m = ord2f(cm);
     const float *ell = r.ell + (size_t)i * r.L;
     const uint32_t base = (uint32_t)tile * kTile + threadIdx.x * kScanItems;
-    uint64_t q[kScanItems], inc[kScanItems];
+    uint64_t inc[kScanItems];
     uint64_t run = 0;
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
         const uint32_t l = base + it;
-        q[it] = l < r.L ? qweight(ell, l, m, inf) : 0ull;
-        run += q[it];
+        run += l < r.L ? qweight(ell, l, m, inf) : 0ull;
         inc[it] = run;
     }
     unsigned long long agg;
@@ -216,103 +218,102 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_mark(const ResampleArgs r
     if (threadIdx.x == 0) s_pre = lookback<OpSum>(r.status + (size_t)i * ntiles, tile, agg);
     __syncthreads();
     const uint64_t pre = s_pre + texcl;
-    const uint64_t Q = r.Q[i];
-    const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, r.mpc, r.key0, r.key1);
-    const uint64_t R = __umul64hi(rw, Q);                     // floor(r64 * Q / 2^64)
-    int32_t *marks = r.marks + (size_t)i * r.L;
+    unsigned long long *C = r.C + (size_t)i * r.L;
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
         const uint32_t l = base + it;
-        if (l < r.L && q[it]) {
-            const uint64_t C = pre + inc[it];
-            const uint64_t e = slot_count(C, Q, R, r.L);
-            const uint64_t b = slot_count(C - q[it], Q, R, r.L);
-            if (e > b) marks[b] = (int32_t)l;
-        }
+        if (l < r.L) C[l] = pre + inc[it];
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const uint64_t Q = s_pre + agg;
+        const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
+        r.QR[2 * i] = Q;
+        r.QR[2 * i + 1] = __umul64hi(rw, Q);                  // R = floor(r64 Q / 2^64)
+        if (r.Q) r.Q[i] = Q;
     }
 }
 
-cudaError_t launch_scan_mark(const ResampleArgs &r, cudaStream_t st) {
+cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
     const int nt = scan_tiles(r.L);
-    k_scan_mark<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    k_scan<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
     return cudaGetLastError();
 }
 
-// ============================================================== K5
-__global__ void __launch_bounds__(kScanThreads) k_maxscan(const ResampleArgs r, int ntiles) {
-    const int i = blockIdx.y;
-    __shared__ int s_tile;
-    __shared__ unsigned long long s_pre;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(&r.tile_ctr[r.n + i], 1u);
-    __syncthreads();
-    const int tile = s_tile;
-    const uint32_t base = (uint32_t)tile * kTile + threadIdx.x * kScanItems;
-    const int32_t *mk = r.marks + (size_t)i * r.L;
-    unsigned long long inc[kScanItems];
-    unsigned long long run = 0;
-#pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-        const uint32_t l = base + it;
-        const unsigned long long v = l < r.L ? (unsigned long long)(uint32_t)(mk[l] + 1) : 0ull;
-        run = run > v ? run : v;
-        inc[it] = run;
+// Systematic slot j takes min{ l : C_l > t_j }, t_j = floor((j Q + R) / L) (R25).
+__device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, uint32_t L, uint64_t Q, uint64_t R,
+                                                 uint32_t j) {
+    const uint64_t tj = slot_t(j, Q / L, Q % L, R, L);
+    uint32_t lo = 0, hi = L - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&C[mid]) > tj) hi = mid; else lo = mid + 1;
     }
-    unsigned long long agg;
-    const unsigned long long texcl = block_exclusive<OpMax>(run, &agg);
-    if (threadIdx.x == 0) s_pre = lookback<OpMax>(r.status2 + (size_t)i * ntiles, tile, agg);
-    __syncthreads();
-    const unsigned long long pre = s_pre > texcl ? s_pre : texcl;
-    int32_t *anc = r.anc + (size_t)i * r.L;
-#pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-        const uint32_t l = base + it;
-        if (l < r.L) {
-            const unsigned long long a = pre > inc[it] ? pre : inc[it];
-            anc[l] = (int32_t)a - 1;
-        }
-    }
+    return (int32_t)lo;
 }
 
-cudaError_t launch_maxscan(const ResampleArgs &r, cudaStream_t st) {
-    const int nt = scan_tiles(r.L);
-    k_maxscan<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+__global__ void k_ancestors(const ResampleArgs r) {
+    const int i = blockIdx.y;
+    const uint64_t Q = r.QR[2 * i], R = r.QR[2 * i + 1];
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < r.L; j += gridDim.x * blockDim.x)
+        r.anc[(size_t)i * r.L + j] = find_ancestor(r.C + (size_t)i * r.L, r.L, Q, R, j);
+}
+
+cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
+    unsigned gx = (r.L + 255) / 256;
+    if (gx > 1024) gx = 1024;
+    k_ancestors<<<dim3(gx, r.n), 256, 0, st>>>(r);
     return cudaGetLastError();
 }
 
 // ============================================================== K6
+// One thread per (new particle j, aircraft i): find the ancestor by bisection
+// of the integer CDF, copy its control row (from x' or x* per its survivor
+// flag: no survivor copy is made), and write the Gaussian proposal.
 __global__ void k_gather_propose(const ProposeArgs p) {
-    const size_t total = (size_t)p.L * p.n * p.H;
+    const size_t total = (size_t)p.L * p.n;
+    const uint32_t mpc = *p.mpcp;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const int t = idx % p.H;
-        const int i = (idx / p.H) % p.n;
-        const uint32_t j = (uint32_t)(idx / ((size_t)p.H * p.n));
-        const int32_t a = __ldg(&p.anc[(size_t)i * p.L + j]);
-        const float *src = p.src[__ldg(&p.surv[a])] + (((size_t)a * p.n + i) * p.H + t) * 3;
-        const float c0 = src[0], c1 = src[1], c2 = src[2];
-        float *dp = p.xp + idx * 3;
-        dp[0] = c0; dp[1] = c1; dp[2] = c2;
-        const uint4 w = draw(TAG_PERTURB, p.l0 + j, p.k << 16, (uint32_t)t | ((uint32_t)i << 8), p.mpc, p.key0, p.key1);
-        const float2 z01 = box_muller(w.x, w.y);
-        const float2 z23 = box_muller(w.z, w.w);
-        float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
-        if (p.clamp) {
-            const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
-            o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
-            o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
-            o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+        const int i = (int)(idx % p.n);
+        const uint32_t j = (uint32_t)(idx / p.n);
+        int32_t a;
+        if (p.anc) {
+            a = __ldg(&p.anc[(size_t)i * p.L + j]);
+        } else {
+            const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
+            a = find_ancestor(p.C + (size_t)i * p.L, p.L, Q, R, j);
         }
-        float *ds = p.xs + idx * 3;
-        ds[0] = o0; ds[1] = o1; ds[2] = o2;
+        const float *src = p.src[__ldg(&p.surv[a])] + ((size_t)a * p.n + i) * p.H * 3;
+        float *dp = p.xp + idx * p.H * 3;
+        float *ds = p.xs + idx * p.H * 3;
+        const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
+        for (int t = 0; t < p.H; ++t) {
+            const float c0 = src[3 * t], c1 = src[3 * t + 1], c2 = src[3 * t + 2];
+            dp[3 * t] = c0; dp[3 * t + 1] = c1; dp[3 * t + 2] = c2;
+            const uint4 w = draw(TAG_PERTURB, p.l0 + j, p.k << 16, (uint32_t)t | ((uint32_t)i << 8), mpc, p.key0, p.key1);
+            const float2 z01 = box_muller(w.x, w.y);
+            const float2 z23 = box_muller(w.z, w.w);
+            float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
+            if (p.clamp) {
+                o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
+                o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
+                o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+            }
+            ds[3 * t] = o0; ds[3 * t + 1] = o1; ds[3 * t + 2] = o2;
+        }
+        if (idx == 0 && p.reset_n) {              // next round's accumulators (stream-ordered after K4b)
+            for (int q = 0; q < p.reset_n; ++q) p.reset_colmax[q] = 0u;
+            *p.reset_accept = 0ull;
+        }
     }
 }
 
 cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st) {
-    const size_t total = (size_t)p.L * p.n * p.H;
+    const size_t total = (size_t)p.L * p.n;
     if (!total) return cudaSuccess;
-    size_t g = (total + 255) / 256;
+    size_t g = (total + 127) / 128;
     if (g > 148 * 32) g = 148 * 32;
-    k_gather_propose<<<(unsigned)g, 256, 0, st>>>(p);
+    k_gather_propose<<<(unsigned)g, 128, 0, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -402,7 +403,7 @@ __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
         return;
     }
     if (tid < 4) {
-        const uint4 w = draw(TAG_PLANT_WIND, 0u, 0u, (uint32_t)tid << 16, p.mpc, p.key0, p.key1);
+        const uint4 w = draw(TAG_PLANT_WIND, 0u, 0u, (uint32_t)tid << 16, *p.mpcp, p.key0, p.key1);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
         for (int pr = 0; pr < 2; ++pr) {
             const double u1 = ((double)(ws[2 * pr] >> 9) + 0.5) * 0x1.0p-23;
@@ -452,7 +453,7 @@ __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
         wxy[c] = acc + ps.nominal[c];
     }
     if (ps.turb_sigma > 0.0) {
-        const uint4 w = draw(TAG_PLANT_TURB, 0u, 0u, (uint32_t)i << 8, p.mpc, p.key0, p.key1);
+        const uint4 w = draw(TAG_PLANT_TURB, 0u, 0u, (uint32_t)i << 8, *p.mpcp, p.key0, p.key1);
         const double u1 = ((double)(w.x >> 9) + 0.5) * 0x1.0p-23, u2 = ((double)(w.y >> 9) + 0.5) * 0x1.0p-23;
         const double r = sqrt(-2.0 * log(u1));
         wxy[0] += ps.turb_sigma * r * cos(2.0 * 3.141592653589793 * u2);
@@ -523,16 +524,16 @@ cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny,
 }
 
 // ============================================================== MH debug hook
-__global__ void k_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+__global__ void k_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,
                            uint32_t key0, uint32_t key1, uint8_t *acc) {
     const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < L) acc[l] = mh_decide(lc[l], lp[l], l, k, mpc, key0, key1) ? 1 : 0;
+    if (l < L) acc[l] = mh_decide(lc[l], lp[l], l, k, *mpcp, key0, key1) ? 1 : 0;
 }
 
-cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,
                             uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st) {
     if (!L) return cudaSuccess;
-    k_mh_debug<<<(L + 255) / 256, 256, 0, st>>>(lc, lp, L, k, mpc, key0, key1, acc);
+    k_mh_debug<<<(L + 255) / 256, 256, 0, st>>>(lc, lp, L, k, mpcp, key0, key1, acc);
     return cudaGetLastError();
 }
 

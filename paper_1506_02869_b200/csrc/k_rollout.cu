@@ -104,7 +104,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     const bool valid = lloc < args.L;
     const uint32_t l = args.l0 + lloc;                         // global particle index
     const bool isac = lane < n;
-    const uint32_t k = args.k, mpc = args.mpc;
+    const uint32_t k = args.k, mpc = *args.mpcp;
 
     if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Qhat[tid];
 

@@ -10,7 +10,8 @@ struct DevScen;
 
 struct RolloutArgs {
     const float *ctrl[2];      // candidate buffers [L][n][H][3]: 0 = x' (resampled), 1 = x* (proposal)
-    uint32_t L, l0, S, k, mpc; // local particles, global offset, samples, round, MPC step
+    uint32_t L, l0, S, k;      // local particles, global offset, samples, round
+    const uint32_t *mpcp;      // device: MPC step index (keys every stream)
     float ell0;                // -log2(L_global)  (W^0 = 1/L)
     int surv_single;           // survivor flag written when only one candidate is evaluated
     float *ell_out;            // [n][L] survivor log2 weights (column-major per aircraft)
@@ -31,40 +32,48 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
 
 struct PopArgs {
     int n, H;
-    uint32_t L, l0, k, mpc, key0, key1;
+    uint32_t L, l0, k, key0, key1;
+    const uint32_t *mpcp;
 };
 
 // K1: uniform initial controls (Alg.1 l.3-5)
 cudaError_t launch_init_population(const DevScen &sc, const PopArgs &p, float *ctrl, cudaStream_t st);
 
-// Resampling (R25): K4a integer weight totals, K4b decoupled
-// look-back scan + slot marks, K5 max-scan marks -> ancestors.
+// Resampling (R25): K4b decoupled look-back scan of the integer
+// weights -> CDF C and (Q, R); ancestors by bisection (in K6 or k_ancestors).
+// K4a (k_qsum) computes totals and ESS for diagnostics only.
 struct ResampleArgs {
     int n;
     uint32_t L;                 // particles (local == global when single GPU)
-    uint32_t k, mpc, key0, key1;
+    uint32_t k, key0, key1;
+    const uint32_t *mpcp;
     const float *ell;           // [n][L]
     const uint32_t *colmax;     // [n] ordered max
-    unsigned long long *Q;      // [n] totals (atomicAdd)
+    unsigned long long *Q;      // [n] totals (nullable)
     double *ess;                // [2n] sum w, sum w^2 (diagnostic)
-    unsigned long long *status; // [n][ntiles] look-back words (scan 1)
-    unsigned long long *status2;// [n][ntiles2] look-back words (scan 2)
-    uint32_t *tile_ctr;         // [2n] dynamic tile counters
-    int32_t *marks;             // [n][L], -1 = no offspring starts here
-    int32_t *anc;               // [n][L]
+    unsigned long long *status; // [n][ntiles] look-back words
+    uint32_t *tile_ctr;         // [n] dynamic tile counters
+    unsigned long long *C;      // [n][L] inclusive integer CDF
+    unsigned long long *QR;     // [n][2] (Q, R)
+    int32_t *anc;               // [n][L] (k_ancestors only)
 };
 int scan_tiles(uint32_t L);
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
-cudaError_t launch_scan_mark(const ResampleArgs &r, cudaStream_t st);
-cudaError_t launch_maxscan(const ResampleArgs &r, cudaStream_t st);
+cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st);
+cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);
 
 // K6: gather survivors' rows by ancestor, Gaussian proposal (Alg.1 l.22-23)
 struct ProposeArgs {
     int n, H;
-    uint32_t L, l0, k, mpc, key0, key1;
+    uint32_t L, l0, k, key0, key1;
+    const uint32_t *mpcp;
     const float *src[2];        // survivor pair: [0] x', [1] x*
     const uint8_t *surv;        // [L] which buffer holds particle l's survivor
-    const int32_t *anc;         // [n][L]
+    const int32_t *anc;         // [n][L] explicit ancestors (debug) or NULL -> bisection of C
+    const unsigned long long *C, *QR;
+    uint32_t *reset_colmax;     // zeroed for the next round (nullable)
+    unsigned long long *reset_accept;
+    int reset_n;
     float *xp, *xs;             // outputs [L][n][H][3]
     float sig[3];
     int clamp;
@@ -92,7 +101,8 @@ cudaError_t launch_select(const SelectArgs &s, cudaStream_t st);
 // K8: plant advance in FP64
 struct PlantArgs {
     int n;
-    uint32_t mpc, key0, key1;
+    uint32_t key0, key1;
+    const uint32_t *mpcp;
     const double *states;       // [n][6]
     const float *best_row;      // [n][H][3] (t = 0 is applied)
     int H;
@@ -119,7 +129,7 @@ cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny,
                            double dx, float *out, cudaStream_t st);
 
 // MH decisions for injected lambdas (debug hook)
-cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, uint32_t mpc,
+cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,
                             uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st);
 
 __host__ __device__ uint64_t slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L);

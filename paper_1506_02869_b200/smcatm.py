@@ -189,7 +189,8 @@ class Solver:
         self.lib = load()
         self.torch = torch
         self.device = torch.device("cuda", device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # a dedicated stream by default: the legacy default stream cannot be graph-captured
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
         cfg = Config()
         cfg.n_particles, cfg.n_samples, cfg.n_rounds = int(L), int(S), int(K)
         cfg.schedule = 1 if sched_paper else 0

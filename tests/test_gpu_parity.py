@@ -264,3 +264,50 @@ def test_select_and_plant_parity(smc):
     assert np.array_equal(flags.astype(np.int32), ref_flags)
     ctrl = pop["prop"][best] if pop["surv"][best] else pop["cur"][best]
     assert np.array_equal(applied, ctrl[:, 0, :])
+
+
+def test_graph_replay_matches_direct_launches(smc):
+    """The CUDA-graph replay of smc_solve is bit-identical to direct launches,
+    across MPC-step indices (the index is read from device memory)."""
+    scn, cfg = sc.config(2)
+    out = []
+    for use_graph in (False, True):
+        sol = smc.Solver(scn, L=2048, S=4, K=5, sigma=cfg.sigma, seed=cfg.seed, use_graph=use_graph)
+        res = []
+        for m in (0, 3, 3):
+            sol.mpc_index = m
+            sol.solve(advance_plant=False)
+            pop = sol.population()
+            res.append((pop["cur"].copy(), pop["ell"].copy(), pop["lam"].copy(), sol.best_controls(allow_infeasible=True)[0]))
+        out.append(res)
+        sol.close()
+    for a, b in zip(out[0], out[1]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    assert not np.array_equal(out[0][0][1], out[0][1][1])     # different MPC index, different streams
+
+
+def test_full_size_c5_sampled_parity(smc):
+    """c5 at full size (L = 2^20, N = 16, S = 64) in the bench's launch
+    configuration: one round on the GPU; 24 sampled particles re-evaluated by
+    the oracle one by one."""
+    scn, cfg = sc.config(5)
+    sol = smc.Solver(scn, L=cfg.L, S=cfg.S, K=2, sigma=cfg.sigma, seed=cfg.seed)
+    sol.iterate(1)
+    pop = sol.population()
+    P = O.Problem(scn)
+    rng = np.random.default_rng(0)
+    idx = rng.choice(cfg.L, 24, replace=False)
+    for l in idx:
+        ell_o = np.full(scn["n"], -np.log2(cfg.L))
+        amb = False
+        for s in range(cfg.S):
+            r = P.rollout(pop["cur"][l].astype(np.float64), int(l), s, 0, cfg.seed)
+            amb |= np.min(r["margin"]) < MARGIN
+            ell_o = np.where(r["viol"].astype(bool) | (r["J"] <= 0), -np.inf, ell_o + np.log2(np.maximum(r["J"], 1e-300)))
+        if amb:
+            continue
+        g = pop["ell"][:, l].astype(np.float64)
+        assert np.array_equal(np.isfinite(g), np.isfinite(ell_o)), l
+        f = np.isfinite(g)
+        assert np.allclose(g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + cfg.S)), l
