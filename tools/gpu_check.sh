@@ -9,3 +9,7 @@ if [ "$2" == "ncu" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rollout -s 2 -c 1 -o gpurun_out/prof_k2_$tag python tools/prof_step.py 2 4 > gpurun_out/ncu_k2_$tag.log 2>&1
 fi
 echo done
+if [ "$3" == "launches" ]; then
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_small_$tag.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_$tag.log 2>&1
+fi

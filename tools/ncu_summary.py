@@ -19,7 +19,7 @@ for r in rows:
     name = d["Kernel Name"].split("(")[0]
     v = float(d["Metric Value"].replace(",", ""))
     unit = d.get("Metric Unit", "")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}.get(unit, 1.0)
     tot[name] += v * scale
     cnt[name] += 1
 T = sum(tot.values())
