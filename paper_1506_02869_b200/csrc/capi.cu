@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -121,6 +122,7 @@ struct smc_ctx {
     bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
+    int layout = 1;                    // K2 layout: 1 transposed (default), 0 lane-per-aircraft segments
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -235,6 +237,10 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30)) {
         delete ctx;
         return SMC_EINVAL;
+    }
+    {
+        const char *lay = getenv("SMC_K2_LAYOUT");
+        ctx->layout = (lay && strcmp(lay, "segment") == 0) ? 0 : 1;
     }
     ctx->Lg = cfg->n_particles;
     smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
@@ -529,7 +535,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     ra.ell0 = (float)(-std::log2((double)ctx->Lg));
     ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
     ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
-    LAUNCHP(PH_ROLLOUT, launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
+    LAUNCHP(PH_ROLLOUT, ctx->layout ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
+                                     : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
     ResampleArgs rs{};
     rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
@@ -788,7 +795,7 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
     ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
     ra.dbg_landed = dland;
-    LAUNCH(launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
+    LAUNCH(ctx->layout ? launch_rollout_t(ctx->dsc, ra, 1, debug, ctx->st) : launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
     if (debug) {
         if (J) CK(cudaMemcpyAsync(J, dJ, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
         if (viol) CK(cudaMemcpyAsync(viol, dviol, nu, cudaMemcpyDeviceToHost, ctx->st));

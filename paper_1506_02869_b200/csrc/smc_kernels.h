@@ -29,6 +29,8 @@ struct RolloutArgs {
 int segment_width(int n);
 size_t rollout_smem_bytes(int W, int NC, int H);
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
+// transposed layout (warp = aircraft, lane = (candidate, particle)); k_rollout_t.cu
+cudaError_t launch_rollout_t(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
 
 struct PopArgs {
     int n, H;
