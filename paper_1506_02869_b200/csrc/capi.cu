@@ -29,9 +29,16 @@ constexpr uint32_t kCentreCap = 256;
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
+    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
 };
+
+// Partial log-weight buffer of chunked K2 launches: up to 8 sample chunks x 2
+// candidates, capped at 64 MiB (large populations fill the GPU without chunking).
+size_t part_bytes(uint32_t Lloc, int nmax) {
+    const size_t full = (size_t)8 * 2 * nmax * Lloc * sizeof(float);
+    return full < ((size_t)64 << 20) ? full : ((size_t)64 << 20);
+}
 
 // Bump-allocate every device buffer from the caller's workspace.
 Layout layout(uint32_t Lloc, int nmax, int Hmax) {
@@ -40,6 +47,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax) {
     auto take = [&](size_t bytes) { size_t at = off; off += align_up(bytes); return at; };
     const size_t row = (size_t)Lloc * nmax * Hmax * 3 * sizeof(float);
     o.ctrl = take(4 * row);
+    o.part = take(part_bytes(Lloc, nmax));
     o.ell = take((size_t)nmax * Lloc * sizeof(float));
     o.lam = take((size_t)Lloc * sizeof(double));
     o.lam2 = take(2 * (size_t)Lloc * sizeof(double));
@@ -96,7 +104,9 @@ struct smc_ctx {
     char *ws = nullptr;
     Layout lay{};
     float *ctrl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    float *ell = nullptr;
+    float *ell = nullptr, *part = nullptr;
+    size_t part_cap = 0;
+    int nsm = 148, bps[2] = {0, 0};
     double *lam = nullptr, *lam2 = nullptr;
     uint8_t *surv = nullptr;
     uint32_t *colmax = nullptr, *tiles = nullptr;
@@ -122,7 +132,7 @@ struct smc_ctx {
     bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
-    int layout = 1;                    // K2 layout: 1 transposed (default), 0 lane-per-aircraft segments
+    int layout = 0;                    // K2 layout: 0 lane-per-aircraft segments (default), 1 transposed
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -240,7 +250,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     }
     {
         const char *lay = getenv("SMC_K2_LAYOUT");
-        ctx->layout = (lay && strcmp(lay, "segment") == 0) ? 0 : 1;
+        ctx->layout = (lay && strcmp(lay, "transposed") == 0) ? 1 : 0;
     }
     ctx->Lg = cfg->n_particles;
     smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
@@ -270,6 +280,9 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->ctrl[1][0] = cb + 2 * prow;
     ctx->ctrl[1][1] = cb + 3 * prow;
     ctx->ell = (float *)(ws + L.ell);
+    ctx->part = (float *)(ws + L.part);
+    ctx->part_cap = part_bytes(max_local(ctx->Lg, world), ctx->nmax);
+    cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
     ctx->lam = (double *)(ws + L.lam);
     ctx->lam2 = (double *)(ws + L.lam2);
     ctx->surv = (uint8_t *)(ws + L.surv);
@@ -503,6 +516,8 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));
     ctx->drop_graph();
+    ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1);
+    ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2);
     ctx->have_scn = true;
     return init_population(ctx);
 }
@@ -535,6 +550,22 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     ra.ell0 = (float)(-std::log2((double)ctx->Lg));
     ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
     ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
+    {
+        // wave planning: split the S samples into chunks when the particle grid
+        // alone would leave a large partial wave (fixed-order partial sums)
+        const int W = segment_width(n);
+        const double B = std::ceil((double)ctx->Lloc / (double)(128 / W));
+        const double slots = (double)std::max(1, ctx->bps[NC - 1]) * ctx->nsm;
+        auto eff = [&](int c) { const double w = B * c / slots; return w / std::ceil(w); };
+        int best = 1;
+        double be = eff(1);
+        for (int c = 2; c <= 8 && (uint32_t)c <= S; ++c) {
+            const size_t need = (size_t)c * NC * n * ctx->Lloc * sizeof(float);
+            if (need > ctx->part_cap) break;
+            if (eff(c) > be + 0.03) { be = eff(c); best = c; }
+        }
+        if (ctx->layout == 0 && best > 1) { ra.part = ctx->part; ra.chunks = best; }
+    }
     LAUNCHP(PH_ROLLOUT, ctx->layout ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
                                      : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;

@@ -141,11 +141,14 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
     float ell[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) ell[c] = args.ell0;
+    for (int c = 0; c < NC; ++c) ell[c] = args.part ? 0.0f : args.ell0;
 
     const float dt = sc.dt, g = sc.g;
     const float dtg = dt * g;
-    for (uint32_t s = 0; s < args.S; ++s) {
+    // sample chunk of this block (gridDim.y > 1: partial sums, combined by k_combine)
+    const uint32_t s_lo = (uint32_t)(((uint64_t)args.S * blockIdx.y) / gridDim.y);
+    const uint32_t s_hi = (uint32_t)(((uint64_t)args.S * (blockIdx.y + 1)) / gridDim.y);
+    for (uint32_t s = s_lo; s < s_hi; ++s) {
         float x[NC], y[NC], z[NC], v[NC], chi[NC], m[NC], fuel[NC], sA[NC], sB[NC], sC[NC], sN[NC];
         bool landed[NC], viol[NC];
         {
@@ -366,6 +369,14 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         }
     }  // s
 
+    if (args.part) {      // chunked evaluation: partial log2 weights, MH in k_combine
+        if (valid && isac) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                args.part[(((size_t)blockIdx.y * NC + c) * n + lane) * args.L + lloc] = ell[c];
+        }
+        return;
+    }
     // ---------------- epilogue: lambda (double, ascending i), MH (R1), survivor
     __syncthreads();
     float *s_ell = reinterpret_cast<float *>(s_pos);          // reuse [NC][kBlock]
@@ -421,6 +432,48 @@ size_t rollout_smem_bytes(int W, int NC, int H) {
            sizeof(float4) * NC * kBlock + sizeof(float) * 72 + 16;
 }
 
+// Combine the sample chunks of a chunked K2 launch (fixed chunk order):
+// ell_c,i = ell0 + sum_y part[y][c][i] (-inf absorbs), lambda in double over
+// ascending i, MH decision (R1), survivor stores and the column max.
+template <int NC>
+__global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) {
+    const uint32_t lloc = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = lloc < args.L;
+    const int n = sc.n;
+    const uint32_t L = args.L;
+    double lam[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        lam[c] = 0.0;
+        for (int i = 0; i < n && valid; ++i) {
+            float e = args.ell0;
+            for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + c) * n + i) * L + lloc];
+            lam[c] += (double)e;
+        }
+    }
+    const uint32_t l = args.l0 + lloc;
+    int acc = args.surv_single;
+    if (NC == 2 && valid) acc = mh_decide(lam[0], lam[1], l, args.k, *args.mpcp, sc.key0, sc.key1) ? 1 : 0;
+    const int cs = (NC == 2 && acc) ? 1 : 0;
+    if (valid) {
+        args.lam_out[lloc] = lam[cs];
+        args.surv_out[lloc] = (uint8_t)acc;
+        if (args.lam_cand) { args.lam_cand[lloc] = lam[0]; args.lam_cand[L + lloc] = lam[NC - 1]; }
+    }
+    for (int i = 0; i < n; ++i) {
+        float e = args.ell0;
+        if (valid)
+            for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + cs) * n + i) * L + lloc];
+        if (valid) args.ell_out[(size_t)i * L + lloc] = e;
+        const uint32_t mx = __reduce_max_sync(0xffffffffu, valid ? f2ord(e) : 0u);
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(&args.colmax[i], mx);
+    }
+    if (NC == 2) {
+        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid && acc));
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(args.n_accept, (unsigned long long)cnt);
+    }
+}
+
 template <int W, int NC, bool DEBUG>
 static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     const size_t smem = rollout_smem_bytes(W, NC, sc.H);
@@ -430,8 +483,30 @@ static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_
     const int segs = kBlock / W;
     const unsigned grid = (a.L + segs - 1) / segs;
     if (grid == 0) return cudaSuccess;
-    kern<<<grid, kBlock, smem, st>>>(sc, a);
+    const int chunks = (a.part && !DEBUG) ? (a.chunks < 1 ? 1 : a.chunks) : 1;
+    RolloutArgs b = a;
+    if (chunks == 1) b.part = nullptr;
+    kern<<<dim3(grid, chunks), kBlock, smem, st>>>(sc, b);
+    e = cudaGetLastError();
+    if (e != cudaSuccess || chunks == 1) return e;
+    k_combine<NC><<<(a.L + 127) / 128, 128, 0, st>>>(sc, b, chunks);
     return cudaGetLastError();
+}
+
+// Resident K2 blocks per SM for this problem shape (wave-quantisation planning).
+int rollout_blocks_per_sm(int n, int H, int NC) {
+    const int W = segment_width(n);
+    const size_t smem = rollout_smem_bytes(W, NC, H);
+    int nb = 0;
+#define SMC_OCC(WW)                                                                                    \
+    if (W == WW) {                                                                                     \
+        auto kern = NC == 2 ? k_rollout<WW, 2, false> : k_rollout<WW, 1, false>;                       \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem);                        \
+    }
+    SMC_OCC(1) SMC_OCC(2) SMC_OCC(4) SMC_OCC(8) SMC_OCC(16) SMC_OCC(32)
+#undef SMC_OCC
+    return nb;
 }
 
 template <int NC, bool DEBUG>

@@ -99,7 +99,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     const uint32_t l = args.l0 + lloc;
     const uint32_t k = args.k, mpc = *args.mpcp;
 
-    if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Qhat[tid];
+    for (int q = tid; q < 64; q += blockDim.x) s_Q[(q >> 3) * 9 + (q & 7)] = sc.Qhat[q];
 
     const DevAircraft *Ap = sc.ac + i;
     const int kind = Ap->kind, first = Ap->first_step;

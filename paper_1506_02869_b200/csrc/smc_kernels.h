@@ -20,6 +20,8 @@ struct RolloutArgs {
     uint8_t *surv_out;         // [L] 1 = proposal accepted
     uint32_t *colmax;          // [n] ordered-float max of ell_out (atomicMax)
     unsigned long long *n_accept;
+    float *part;               // [chunks][NC][n][L] partial log2 weights (chunked launch) or NULL
+    int chunks;                // sample chunks (grid.y) when part != NULL
     // debug outputs (candidate 0), per (l, s, i)
     float *dbg_J, *dbg_comp, *dbg_fuel, *dbg_traj, *dbg_ell_c;
     uint8_t *dbg_viol;
@@ -27,6 +29,7 @@ struct RolloutArgs {
 };
 
 int segment_width(int n);
+int rollout_blocks_per_sm(int n, int H, int NC);
 size_t rollout_smem_bytes(int W, int NC, int H);
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
 // transposed layout (warp = aircraft, lane = (candidate, particle)); k_rollout_t.cu

@@ -287,22 +287,29 @@ def test_graph_replay_matches_direct_launches(smc):
     assert not np.array_equal(out[0][0][1], out[0][1][1])     # different MPC index, different streams
 
 
-def test_full_size_c5_sampled_parity(smc):
-    """c5 at full size (L = 2^20, N = 16, S = 64) in the bench's launch
-    configuration: one round on the GPU; 24 sampled particles re-evaluated by
-    the oracle one by one."""
-    scn, cfg = sc.config(5)
-    sol = smc.Solver(scn, L=cfg.L, S=cfg.S, K=2, sigma=cfg.sigma, seed=cfg.seed)
-    sol.iterate(1)
+@pytest.mark.parametrize("num", [2, 3, 4, 5])
+def test_full_size_sampled_parity(smc, num):
+    """Configs c2-c5 at full size (c5: L = 2^20, N = 16, S = 64) in the bench's
+    launch configuration (CUDA graph, chunked K2 where planned): two rounds on
+    the GPU; 24 sampled survivors of round 1 re-evaluated by the oracle one by
+    one, and their MH decisions replayed bit-exactly on the GPU's lambdas."""
+    scn, cfg = sc.config(num)
+    sol = smc.Solver(scn, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed, use_graph=True)
+    sol.iterate(2)
     pop = sol.population()
+    lc, lp = pop["lam_cand"]
+    rng0 = np.random.default_rng(1)
+    for l in rng0.choice(cfg.L, 2000, replace=False):
+        assert pop["surv"][l] == O.mh_accept(lc[l], lp[l], int(l), 1, cfg.seed)
     P = O.Problem(scn)
     rng = np.random.default_rng(0)
     idx = rng.choice(cfg.L, 24, replace=False)
     for l in idx:
         ell_o = np.full(scn["n"], -np.log2(cfg.L))
         amb = False
+        ctrl = (pop["prop"][l] if pop["surv"][l] else pop["cur"][l]).astype(np.float64)
         for s in range(cfg.S):
-            r = P.rollout(pop["cur"][l].astype(np.float64), int(l), s, 0, cfg.seed)
+            r = P.rollout(ctrl, int(l), s, 1, cfg.seed)
             amb |= np.min(r["margin"]) < MARGIN
             ell_o = np.where(r["viol"].astype(bool) | (r["J"] <= 0), -np.inf, ell_o + np.log2(np.maximum(r["J"], 1e-300)))
         if amb:
