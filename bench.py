@@ -11,8 +11,9 @@ proposal, final selection and the plant step -- every row of SURVEY.md 8(a).
 `value` is aircraft-step rollouts per second over the whole job (device
 time, inputs resident); `e2e` is the same metric through the public C ABI
 call mpc_step() with pinned host buffers, host<->device copies inside the
-timed region.  N > 1 (torchrun): each rank solves its own MPC problem
-(weak scaling, no data-path collective) -- see DESIGN.md section 9.
+timed region.  N > 1 (torchrun): one MPC problem with L particles per GPU
+sharded over the N GPUs, NCCL exchange each round (weak scaling) -- see
+DESIGN.md section 9.
 """
 from __future__ import annotations
 
@@ -194,11 +195,14 @@ def main():
     torch.cuda.set_device(local)
     scn, cfg = sc.config(args.config)
     stream = torch.cuda.Stream(device=local)
-    sol = smcatm.Solver(scn, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed + rank,
+    # N > 1: one MPC problem whose particles are sharded over the N GPUs (NCCL
+    # exchange each round), L = configs' L per GPU -> weak scaling
+    L_glob = cfg.L * world
+    sol = smcatm.Solver(scn, L=L_glob, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
                         anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True,
-                        use_graph=not args.no_graph)
+                        use_graph=not args.no_graph, rank=rank, world_size=world)
     S_list = [cfg.S] * cfg.K
-    ac_steps = roofline.aircraft_steps(scn, cfg.L, S_list, cfg.mh)
+    ac_steps = roofline.aircraft_steps(scn, L_glob, S_list, cfg.mh)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def barrier():
@@ -229,7 +233,7 @@ def main():
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     tmax_ms = float(t_local.item())
-    value = ac_steps * args.steps * world / (tmax_ms / 1000.0)
+    value = ac_steps * args.steps / (tmax_ms / 1000.0)
 
     # ---- e2e: public C ABI mpc_step with pinned host buffers, copies inside the timed region
     n = scn["n"]
@@ -254,7 +258,7 @@ def main():
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = ac_steps * args.e2e_steps * world / (float(e2e_t.item()) / 1000.0)
+    e2e_value = ac_steps * args.e2e_steps / (float(e2e_t.item()) / 1000.0)
     h2d = n * 6 * 8 + n * 156      # measured states + per-aircraft constants re-upload
     d2h = n * 6 * 8 + n * 3 * 4 + n * 4 + 8
 
@@ -270,7 +274,7 @@ def main():
     ops_k2 = 0.0
     for k, S in enumerate(S_list):
         C = 1 if (k == 0 or not cfg.mh) else 2
-        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * cfg.L * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
+        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * (L_glob // world) * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
     ops_k2 *= args.steps
     achieved = ops_k2 / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
     peak = roofline.peak_alu_ops(float(peaks.get("sm_max_mhz", 1965.0)))
@@ -281,7 +285,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
                                f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
-                   "parallelism": f"weak: {world} independent MPC problem(s), one per GPU",
+                   "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
+                                   "all-gathers per round)" if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "cuda_graph": not args.no_graph,
                    "aircraft_steps_per_step": ac_steps},
@@ -303,7 +308,7 @@ def main():
     # resample/propose phase vs HBM
     rs_ms = phases["resample"][0] + phases["propose"][0]
     if rs_ms > 0:
-        rb = roofline.resample_bytes(scn["n"], cfg.L, scn["H"]) * (cfg.K - 1) * args.steps
+        rb = roofline.resample_bytes(scn["n"], L_glob // world, scn["H"]) * (cfg.K - 1) * args.steps
         line["roofline_resample"] = {"bound": "hbm", "achieved": rb / (rs_ms / 1000.0) / 1e9,
                                      "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
                                      "frac": rb / (rs_ms / 1000.0) / 1e9 / float(peaks.get("hbm_gbs", 6650.0))}

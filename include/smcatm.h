@@ -140,7 +140,12 @@ typedef struct {
 size_t smc_workspace_bytes(const smc_config *cfg);
 
 /* Create a context.  Validates cfg, carves the workspace, creates events.
- * With world_size > 1 also joins the NCCL communicator (R43). */
+ * With world_size > 1 also joins the NCCL communicator (R43): rank r owns the
+ * global particles [L r / G, L (r+1) / G); every random stream is keyed by the
+ * global particle index, so rollouts, MH decisions and ancestors are identical
+ * for any world size.  Each round then exchanges the column maxima
+ * (all-reduce MAX), the per-rank integer CDFs and the compacted survivor rows
+ * (all-gather) on cfg.stream; selection all-gathers per-rank winners. */
 smc_status smc_init(const smc_config *cfg, smc_ctx **out);
 
 /* Copy the scenario, precompute (Qhat = chol(Rhat) P:463-465, normalisers
@@ -190,6 +195,11 @@ void smc_destroy(smc_ctx *ctx);
 /* Set / read the MPC step index (keys all streams; mpc_step increments it). */
 smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t mpc_index);
 uint32_t smc_get_mpc_index(const smc_ctx *ctx);
+
+/* 128-byte NCCL unique id for a multi-GPU context (call on rank 0, share
+ * with every rank, pass as smc_config.nccl_unique_id).  SMC_ENCCL if NCCL
+ * cannot be loaded. */
+smc_status smc_nccl_unique_id(void *out128);
 
 /* Number of kernel launches the library issued since smc_init. */
 uint64_t smc_launch_count(const smc_ctx *ctx);

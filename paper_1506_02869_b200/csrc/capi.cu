@@ -23,6 +23,43 @@ using namespace smc;
 
 namespace {
 
+// ---- NCCL, loaded at run time (only multi-GPU contexts need it; the ABI types are stable)
+typedef int ncclResult_t;
+struct ncclUniqueId { char internal[128]; };
+typedef void *ncclComm_t;
+enum { ncclUint8_ = 1, ncclUint32_ = 3, ncclUint64_ = 5, ncclFloat32_ = 7 };
+enum { ncclMax_ = 2 };
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi *nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            if (api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather)
+                api.h = h;
+        }
+    }
+    return api.h ? &api : nullptr;
+}
+
 constexpr uint32_t kPopCap = 256 * 256;
 constexpr uint32_t kCentreCap = 256;
 
@@ -30,7 +67,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
-        part_lam, part_idx, done, best_lam, best_idx, best_row, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
+        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
 };
 
 // Partial log-weight buffer of chunked K2 launches: up to 8 sample chunks x 2
@@ -41,7 +78,9 @@ size_t part_bytes(uint32_t Lloc, int nmax) {
 }
 
 // Bump-allocate every device buffer from the caller's workspace.
-Layout layout(uint32_t Lloc, int nmax, int Hmax) {
+size_t record_bytes(int nmax, int Hmax) { return (16 + (size_t)nmax * Hmax * 12 + 15) & ~(size_t)15; }
+
+Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1) {
     Layout o{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t at = off; off += align_up(bytes); return at; };
@@ -68,9 +107,12 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax) {
     o.part_lam = take(512 * sizeof(double));
     o.part_idx = take(512 * sizeof(long long));
     o.done = take(sizeof(unsigned));
-    o.best_lam = take(sizeof(double));
-    o.best_idx = take(sizeof(long long));
-    o.best_row = take((size_t)nmax * Hmax * 3 * sizeof(float));
+    o.best_lam = take(record_bytes(nmax, Hmax));               // local selection record
+    o.best_idx = take(record_bytes(nmax, Hmax));               // final (merged) record
+    o.best_row = take(world > 1 ? record_bytes(nmax, Hmax) * world : 0);   // all-gathered records
+    o.Call = take(world > 1 ? (size_t)world * nmax * Lloc * 8 : 0);
+    o.Sc = take(world > 1 ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.Sall = take(world > 1 ? (size_t)world * Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
     o.pZ = take(16 * sizeof(double));
     o.pzi = take(sizeof(int));
     o.pstates = take(nmax * 6 * sizeof(double));
@@ -120,6 +162,18 @@ struct smc_ctx {
     long long *part_idx = nullptr, *best_idx = nullptr;
     unsigned *done = nullptr;
     int *pzi = nullptr, *pflags = nullptr;
+    // selection records {lambda, index, row}: local (K7) and final (merged across ranks)
+    unsigned char *rec_local = nullptr, *rec_final = nullptr, *rec_all = nullptr;
+    size_t rec_bytes = 0;
+    double *sel_lam = nullptr;
+    long long *sel_idx = nullptr;
+    float *sel_row = nullptr;
+    // multi-GPU
+    int world = 1, rank = 0;
+    uint32_t Lmax = 0;
+    ncclComm_t comm = nullptr;
+    unsigned long long *Call = nullptr;
+    float *Sc = nullptr, *Sall = nullptr;
 
     bool have_scn = false;
     DevScen dsc{};
@@ -132,7 +186,9 @@ struct smc_ctx {
     bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
-    int layout = 0;                    // K2 layout: 0 lane-per-aircraft segments (default), 1 transposed
+    int layout = 0;                    // K2 layout: 0 lane-per-aircraft segments, 1 transposed (warp = aircraft)
+    int layout_env = -1;               // SMC_K2_LAYOUT override (-1: automatic)
+    bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -159,6 +215,7 @@ struct smc_ctx {
     }
     ~smc_ctx() {
         drop_graph();
+        if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
         for (auto &v : ev_used)
             for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
         for (auto e : ev_free) cudaEventDestroy(e);
@@ -185,6 +242,13 @@ static smc_status fail(smc_ctx *c, smc_status s, const char *fmt, ...) {
     do {                                                                                           \
         cudaError_t _e = (expr);                                                                   \
         if (_e != cudaSuccess) return fail(ctx, SMC_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+#define NCK(expr)                                                                                  \
+    do {                                                                                           \
+        ++ctx->launches;                                                                           \
+        ncclResult_t _r = (expr);                                                                  \
+        if (_r != 0) return fail(ctx, SMC_ENCCL, "%s: %s", #expr,                                  \
+                                 nccl_api()->GetErrorString ? nccl_api()->GetErrorString(_r) : "nccl error"); \
     } while (0)
 #define LAUNCHP(phase, expr)                                                                       \
     do {                                                                                           \
@@ -230,7 +294,7 @@ extern "C" size_t smc_workspace_bytes(const smc_config *cfg) {
         cfg->max_horizon > 32)
         return 0;
     const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
-    return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon).total;
+    return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon, world).total;
 }
 
 extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
@@ -239,10 +303,13 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     smc_ctx *ctx = new smc_ctx();
     ctx->cfg = *cfg;
     const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
-    if (world != 1) {
+    if (world > 8 || cfg->rank < 0 || cfg->rank >= world || (world > 1 && !cfg->nccl_unique_id) ||
+        cfg->n_particles < (uint32_t)world) {
         delete ctx;
-        return SMC_EINVAL;   // multi-GPU: see smc_init_multi in DESIGN.md (not built in this round)
+        return SMC_EINVAL;
     }
+    ctx->world = world;
+    ctx->rank = cfg->rank;
     if (cfg->n_particles == 0 || cfg->max_aircraft == 0 || cfg->max_aircraft > 32 || cfg->max_horizon == 0 ||
         cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30)) {
         delete ctx;
@@ -250,14 +317,16 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     }
     {
         const char *lay = getenv("SMC_K2_LAYOUT");
-        ctx->layout = (lay && strcmp(lay, "transposed") == 0) ? 1 : 0;
+        ctx->layout_env = lay ? ((strcmp(lay, "transposed") == 0) ? 1 : (strcmp(lay, "segment") == 0 ? 0 : -1)) : -1;
+        const char *ch = getenv("SMC_K2_CHUNKS");
+        ctx->chunking = ch && strcmp(ch, "1") == 0;
     }
     ctx->Lg = cfg->n_particles;
     smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
     ctx->Lloc -= ctx->l0;
     ctx->nmax = (int)cfg->max_aircraft;
     ctx->Hmax = (int)cfg->max_horizon;
-    ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax);
+    ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax, world);
     if (!cfg->workspace || cfg->workspace_bytes < ctx->lay.total) {
         delete ctx;
         return SMC_ENOMEM;
@@ -301,9 +370,20 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->part_lam = (double *)(ws + L.part_lam);
     ctx->part_idx = (long long *)(ws + L.part_idx);
     ctx->done = (unsigned *)(ws + L.done);
-    ctx->best_lam = (double *)(ws + L.best_lam);
-    ctx->best_idx = (long long *)(ws + L.best_idx);
-    ctx->best_row = (float *)(ws + L.best_row);
+    ctx->rec_bytes = record_bytes(ctx->nmax, ctx->Hmax);
+    ctx->rec_local = (unsigned char *)(ws + L.best_lam);
+    ctx->rec_final = world > 1 ? (unsigned char *)(ws + L.best_idx) : ctx->rec_local;
+    ctx->rec_all = (unsigned char *)(ws + L.best_row);
+    ctx->sel_lam = (double *)ctx->rec_local;
+    ctx->sel_idx = (long long *)(ctx->rec_local + 8);
+    ctx->sel_row = (float *)(ctx->rec_local + 16);
+    ctx->best_lam = (double *)ctx->rec_final;
+    ctx->best_idx = (long long *)(ctx->rec_final + 8);
+    ctx->best_row = (float *)(ctx->rec_final + 16);
+    ctx->Lmax = max_local(ctx->Lg, world);
+    ctx->Call = (unsigned long long *)(ws + L.Call);
+    ctx->Sc = (float *)(ws + L.Sc);
+    ctx->Sall = (float *)(ws + L.Sall);
     ctx->pZ = (double *)(ws + L.pZ);
     ctx->pzi = (int *)(ws + L.pzi);
     ctx->pstates = (double *)(ws + L.pstates);
@@ -317,7 +397,23 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         delete ctx;
         return SMC_ECUDA;
     }
+    if (world > 1) {
+        NcclApi *api = nccl_api();
+        if (!api) { delete ctx; return SMC_ENCCL; }
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        if (api->CommInitRank(&ctx->comm, world, id, cfg->rank) != 0) { ctx->comm = nullptr; delete ctx; return SMC_ENCCL; }
+    }
     *out = ctx;
+    return SMC_OK;
+}
+
+extern "C" smc_status smc_nccl_unique_id(void *out128) {
+    NcclApi *api = nccl_api();
+    if (!api || !out128) return SMC_ENCCL;
+    ncclUniqueId id;
+    if (api->GetUniqueId(&id) != 0) return SMC_ENCCL;
+    memcpy(out128, &id, sizeof(id));
     return SMC_OK;
 }
 
@@ -516,6 +612,9 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));
     ctx->drop_graph();
+    // automatic K2 layout: lane-per-aircraft segments when N is a power of two
+    // (no padded lanes), otherwise warp-per-aircraft (no 25-50% idle lanes)
+    ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : (segment_width((int)n) == (int)n ? 0 : 1);
     ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1);
     ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2);
     ctx->have_scn = true;
@@ -523,6 +622,8 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
 }
 
 // ---------------------------------------------------------------- one SMC round
+static smc_status select_best(smc_ctx *ctx);
+
 static uint32_t samples_of(const smc_ctx *ctx, uint32_t k) {
     if (ctx->cfg.schedule == SMC_SCHED_PAPER) return (uint32_t)std::floor(3.0 + 5.0 * std::exp(0.05 * (double)k));
     return ctx->cfg.n_samples;
@@ -564,15 +665,17 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
             if (need > ctx->part_cap) break;
             if (eff(c) > be + 0.03) { be = eff(c); best = c; }
         }
-        if (ctx->layout == 0 && best > 1) { ra.part = ctx->part; ra.chunks = best; }
+        if (ctx->layout == 0 && best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
     }
     LAUNCHP(PH_ROLLOUT, ctx->layout ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
                                      : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
+    if (ctx->world > 1)                    // global column maxima (reduce step 1)
+        NCK(nccl_api()->AllReduce(ctx->colmax, ctx->colmax, n, ncclUint32_, ncclMax_, ctx->comm, ctx->st));
     ResampleArgs rs{};
     rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
     rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
-    rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR;
+    rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR; rs.Cstride = ctx->world > 1 ? ctx->Lmax : 0;
     if (stats) {
         CK(cudaMemsetAsync(ctx->ess, 0, 16 * n, ctx->st));
         CK(cudaMemsetAsync(ctx->Q, 0, 8 * n, ctx->st));
@@ -595,13 +698,22 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
         pa.clamp = (int)ctx->cfg.clamp_proposals;
         pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
-        LAUNCHP(PH_PROPOSE, launch_gather_propose(pa, ctx->st));
+        if (ctx->world > 1) {
+            // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
+            NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
+            LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc,
+                                                         n * H * 3, ctx->Sc, ctx->st));
+            NCK(nccl_api()->AllGather(ctx->Sc, ctx->Sall, (size_t)ctx->Lmax * n * H * 3, ncclFloat32_, ctx->comm, ctx->st));
+            MultiArgs ma{pa, ctx->Lg, ctx->Lmax, ctx->world, ctx->Call, ctx->Sall};
+            LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
+        } else {
+            LAUNCHP(PH_PROPOSE, launch_gather_propose(pa, ctx->st));
+        }
         ctx->cur = P ^ 1;
     }
     if (stats) {
-        SelectArgs sa{ctx->Lloc, ctx->l0, n, H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
-                      ctx->part_lam, ctx->part_idx, ctx->done, ctx->best_lam, ctx->best_idx, ctx->best_row};
-        LAUNCH(launch_select(sa, ctx->st));
+        smc_status s2 = select_best(ctx);
+        if (s2 != SMC_OK) return s2;
         uint32_t cm[32];
         double ess[64], bl;
         unsigned long long acc;
@@ -645,8 +757,13 @@ static smc_status select_best(smc_ctx *ctx) {
     if (ctx->last_eval < 0) return fail(ctx, SMC_ESTATE, "no evaluated population");
     const int P = ctx->last_eval;
     SelectArgs sa{ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
-                  ctx->part_lam, ctx->part_idx, ctx->done, ctx->best_lam, ctx->best_idx, ctx->best_row};
+                  ctx->part_lam, ctx->part_idx, ctx->done, ctx->sel_lam, ctx->sel_idx, ctx->sel_row};
     LAUNCH(launch_select(sa, ctx->st));
+    if (ctx->world > 1) {                 // all-gather the per-rank records, merge on every rank
+        NCK(nccl_api()->AllGather(ctx->rec_local, ctx->rec_all, ctx->rec_bytes, ncclUint8_, ctx->comm, ctx->st));
+        LAUNCH(launch_select_merge(ctx->rec_all, ctx->world, ctx->rec_bytes, ctx->dsc.n * ctx->dsc.H * 3,
+                                   ctx->rec_final, ctx->st));
+    }
     return SMC_OK;
 }
 

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
     if (threadIdx.x == 0) s_pre = lookback<OpSum>(r.status + (size_t)i * ntiles, tile, agg);
     __syncthreads();
     const uint64_t pre = s_pre + texcl;
-    unsigned long long *C = r.C + (size_t)i * r.L;
+    unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : r.L);
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
         const uint32_t l = base + it;
@@ -555,6 +555,129 @@ cudaError_t launch_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax,
     if (gx < 1) gx = 1;
     if (gx > 256) gx = 256;
     k_colmax<<<dim3(gx, n), 256, 0, st>>>(ell, n, L, colmax);
+    return cudaGetLastError();
+}
+}  // namespace smc
+
+namespace smc {
+// ============================================================== multi-GPU (R43)
+// Particle sharding: rank r owns global particles [L r / G, L (r+1) / G).
+__host__ __device__ static inline uint32_t shard_begin(uint32_t L, int G, int r) {
+    return (uint32_t)((uint64_t)L * (uint64_t)r / (uint64_t)G);
+}
+
+// Compact this rank's survivor rows (x' or x* per survivor flag) for the all-gather.
+__global__ void k_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+                                    int rowlen, float *out) {
+    const size_t total = (size_t)Lloc * rowlen;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t l = (uint32_t)(e / rowlen);
+        out[e] = (surv[l] ? xs : xp)[e];
+    }
+}
+
+cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+                                     int rowlen, float *out, cudaStream_t st) {
+    const size_t total = (size_t)Lloc * rowlen;
+    if (!total) return cudaSuccess;
+    size_t g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_compact_survivors<<<(unsigned)g, 256, 0, st>>>(xp, xs, surv, Lloc, rowlen, out);
+    return cudaGetLastError();
+}
+
+// Gather + propose for this rank's new particles from the all-gathered
+// per-rank CDFs Call[G][n][Lmax] (local inclusive sums) and survivor rows
+// Sall[G][Lmax][n][H][3].  Global CDF = rank offset + local CDF, so the
+// ancestors equal the single-GPU ones bit for bit (G-invariance).
+__global__ void k_gather_propose_multi(const MultiArgs m) {
+    const ProposeArgs &p = m.p;
+    const size_t total = (size_t)p.L * p.n;
+    const uint32_t mpc = *p.mpcp;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % p.n);
+        const uint32_t jl = (uint32_t)(idx / p.n);
+        const uint32_t j = p.l0 + jl;
+        uint64_t Qr[8], Q = 0;
+        for (int r = 0; r < m.G; ++r) {
+            const uint32_t len = shard_begin(m.Lg, m.G, r + 1) - shard_begin(m.Lg, m.G, r);
+            Qr[r] = len ? m.Call[((size_t)r * p.n + i) * m.Lmax + len - 1] : 0ull;
+            Q += Qr[r];
+        }
+        const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, p.k, mpc, p.key0, p.key1);
+        const uint64_t R = __umul64hi(rw, Q);
+        const uint64_t t = slot_t(j, Q / m.Lg, Q % m.Lg, R, m.Lg);
+        int rho = 0;
+        uint64_t off = 0;
+        while (rho < m.G - 1 && t >= off + Qr[rho]) { off += Qr[rho]; ++rho; }
+        const uint32_t len = shard_begin(m.Lg, m.G, rho + 1) - shard_begin(m.Lg, m.G, rho);
+        const unsigned long long *C = m.Call + ((size_t)rho * p.n + i) * m.Lmax;
+        const uint64_t tl = t - off;
+        uint32_t lo = 0, hi = len - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&C[mid]) > tl) hi = mid; else lo = mid + 1;
+        }
+        const float *src = m.Sall + (((size_t)rho * m.Lmax + lo) * p.n + i) * p.H * 3;
+        float *dp = p.xp + idx * p.H * 3;
+        float *ds = p.xs + idx * p.H * 3;
+        const float *lo3 = p.lo3 + 3 * i, *hi3 = p.hi3 + 3 * i;
+        for (int tt = 0; tt < p.H; ++tt) {
+            const float c0 = src[3 * tt], c1 = src[3 * tt + 1], c2 = src[3 * tt + 2];
+            dp[3 * tt] = c0; dp[3 * tt + 1] = c1; dp[3 * tt + 2] = c2;
+            const uint4 w = draw(TAG_PERTURB, j, p.k << 16, (uint32_t)tt | ((uint32_t)i << 8), mpc, p.key0, p.key1);
+            const float2 z01 = box_muller(w.x, w.y);
+            const float2 z23 = box_muller(w.z, w.w);
+            float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
+            if (p.clamp) {
+                o0 = fminf(fmaxf(o0, lo3[0]), hi3[0]);
+                o1 = fminf(fmaxf(o1, lo3[1]), hi3[1]);
+                o2 = fminf(fmaxf(o2, lo3[2]), hi3[2]);
+            }
+            ds[3 * tt] = o0; ds[3 * tt + 1] = o1; ds[3 * tt + 2] = o2;
+        }
+    }
+}
+
+cudaError_t launch_gather_propose_multi(const MultiArgs &m, cudaStream_t st) {
+    const size_t total = (size_t)m.p.L * m.p.n;
+    if (!total) return cudaSuccess;
+    size_t g = (total + 127) / 128;
+    if (g > 148 * 32) g = 148 * 32;
+    k_gather_propose_multi<<<(unsigned)g, 128, 0, st>>>(m);
+    return cudaGetLastError();
+}
+
+// Global winner from the all-gathered per-rank selection records
+// {double lambda, int64 index, float row[n][H][3]}: greatest lambda, ties ->
+// lowest global index, -1 index = rank had no feasible particle.
+__global__ void k_select_merge(const unsigned char *recs, int G, size_t rec_bytes, int rowlen, unsigned char *out) {
+    __shared__ int s_best;
+    if (threadIdx.x == 0) {
+        int best = -1;
+        double bl = 0.0;
+        long long bi = -1;
+        for (int r = 0; r < G; ++r) {
+            const double lr = *reinterpret_cast<const double *>(recs + r * rec_bytes);
+            const long long ir = *reinterpret_cast<const long long *>(recs + r * rec_bytes + 8);
+            if (ir < 0) continue;
+            if (bi < 0 || lr > bl || (lr == bl && ir < bi)) { best = r; bl = lr; bi = ir; }
+        }
+        s_best = best;
+        *reinterpret_cast<double *>(out) = best >= 0 ? bl : -INFINITY;
+        *reinterpret_cast<long long *>(out + 8) = bi;
+    }
+    __syncthreads();
+    if (s_best < 0) return;
+    const float *src = reinterpret_cast<const float *>(recs + s_best * rec_bytes + 16);
+    float *dst = reinterpret_cast<float *>(out + 16);
+    for (int e = threadIdx.x; e < rowlen; e += blockDim.x) dst[e] = src[e];
+}
+
+cudaError_t launch_select_merge(const unsigned char *recs, int G, size_t rec_bytes, int rowlen, unsigned char *out,
+                                cudaStream_t st) {
+    k_select_merge<<<1, 128, 0, st>>>(recs, G, rec_bytes, rowlen, out);
     return cudaGetLastError();
 }
 }  // namespace smc

@@ -86,15 +86,16 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
 }
 
 template <int W, int NC, bool DEBUG>
-__global__ void __launch_bounds__(kBlock, 4)
+__global__ void __launch_bounds__(kBlock, 5)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
     constexpr int E = (16 + W - 1) / W;           // wind-field entries owned per lane
     extern __shared__ __align__(16) float smem[];
     const int H = sc.H, n = sc.n;
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);               // [H][NC][kBlock] (T, tan phi, sin g, cos g)
-    float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock); // [SEGS][16] normals
-    float *s_Z = s_V + SEGS * 16;                                     // [SEGS][16] AR(1) state
+    constexpr int GB = (W >= 8) ? W / 4 : 1;                       // steps whose normals one batch draws
+    float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock); // [SEGS][GB][16] normals
+    float *s_Z = s_V + SEGS * GB * 16;                                // [SEGS][16] AR(1) state
     float *s_W = s_Z + SEGS * 16;                                     // [SEGS][16] wind at nodes
     float4 *s_pos = reinterpret_cast<float4 *>(s_W + SEGS * 16);     // [NC][kBlock]
     float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);     // [8][9]
@@ -165,18 +166,27 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
 
         for (int t = 0; t < H; ++t) {
-            // ---------------- 1. wind realisation for step t (Alg.1 l.10)
-            for (int b = lane; b < 4; b += W) {
-                const uint4 w = draw(TAG_WIND, l, x1, (uint32_t)t | ((uint32_t)b << 16), mpc, sc.key0, sc.key1);
-                const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
-                *reinterpret_cast<float4 *>(&s_V[seg * 16 + 4 * b]) = make_float4(p0.x, p0.y, p1.x, p1.y);
+            // ---------------- 1. wind realisation for step t (Alg.1 l.10).
+            // Every GB steps the segment's lanes draw the 4 Philox blocks of GB
+            // consecutive steps at once (lane -> block lane&3 of step t + lane/4).
+            const int tb = t % GB;
+            if (tb == 0) {
+                for (int task = lane; task < 4 * GB; task += W) {
+                    const int b = task & 3, ts = t + (task >> 2);
+                    if (ts < H) {
+                        const uint4 w = draw(TAG_WIND, l, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.key0, sc.key1);
+                        const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
+                        *reinterpret_cast<float4 *>(&s_V[(seg * GB + (task >> 2)) * 16 + 4 * b]) =
+                            make_float4(p0.x, p0.y, p1.x, p1.y);
+                    }
+                }
             }
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int e = lane + q * W;
                 if (e < 16) {
-                    const float ve = s_V[seg * 16 + e];
+                    const float ve = s_V[(seg * GB + tb) * 16 + e];
                     Zr[q] = (t == 0) ? ve : fmaf(sc.a, Zr[q], sc.b * ve);
                     s_Z[seg * 16 + e] = Zr[q];
                 }
@@ -275,24 +285,28 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 s_pos[c * kBlock + tid] = make_float4(nx[c], ny[c], nz[c], fly[c] ? 1.0f : 0.0f);
             }
             __syncwarp();
-            // ---------------- 4. separation (Eq. avoidance) against every lane of the segment.
-            // The own lane always hits itself when present, so "conflict" = more than one hit.
-            int cnt[NC];
+            // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
+            // lane checks partner lane+d (d = 1..W/2) and hands the verdict to that
+            // partner with a segment-wide shuffle (for d = W/2 both lanes check).
+            bool conf[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) cnt[c] = 0;
+            for (int c = 0; c < NC; ++c) conf[c] = false;
 #pragma unroll
-            for (int p = 0; p < W; ++p) {
+            for (int d = 1; d <= W / 2; ++d) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const float4 q = s_pos[c * kBlock + seg * W + p];
+                    const float4 q = s_pos[c * kBlock + seg * W + ((lane + d) & (W - 1))];
                     const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
-                    cnt[c] += ((q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh)) ? 1 : 0;
+                    const bool hit = fly[c] && (q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) &&
+                                     (fabsf(dz) < sc.twoPh);
+                    conf[c] = conf[c] || hit;
+                    if (2 * d < W) conf[c] = conf[c] || (__shfl_sync(0xffffffffu, hit ? 1 : 0, (lane - d) & (W - 1), W) != 0);
                 }
             }
             // ---------------- 5. per-step cost terms at j = t+1, state update
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                vnow[c] = vnow[c] || (cnt[c] > 1);
+                vnow[c] = vnow[c] || conf[c];
                 // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
                 // arrival:   D = |wrap(chi - chi_hat)|, chi_hat = pi + 2 theta (R8); E = |beta - beta_f|
                 const float devA = angdist(kind ? th[c] - gA : nchi[c] - kPi - 2.0f * th[c]);
@@ -428,7 +442,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
 size_t rollout_smem_bytes(int W, int NC, int H) {
     const int SEGS = kBlock / W;
-    return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * 3 * SEGS * 16 +
+    const int GB = (W >= 8) ? W / 4 : 1;
+    return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * (SEGS * GB * 16 + 2 * SEGS * 16) +
            sizeof(float4) * NC * kBlock + sizeof(float) * 72 + 16;
 }
 

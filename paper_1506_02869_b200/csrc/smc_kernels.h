@@ -58,7 +58,8 @@ struct ResampleArgs {
     double *ess;                // [2n] sum w, sum w^2 (diagnostic)
     unsigned long long *status; // [n][ntiles] look-back words
     uint32_t *tile_ctr;         // [n] dynamic tile counters
-    unsigned long long *C;      // [n][L] inclusive integer CDF
+    unsigned long long *C;      // [n][Cstride] inclusive integer CDF
+    uint32_t Cstride;           // row stride of C (0 = L)
     unsigned long long *QR;     // [n][2] (Q, R)
     int32_t *anc;               // [n][L] (k_ancestors only)
 };
@@ -85,6 +86,20 @@ struct ProposeArgs {
     const float *lo3, *hi3;     // per aircraft [n][3] envelope for clamping
 };
 cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st);
+
+// Multi-GPU gather + propose
+struct MultiArgs {
+    ProposeArgs p;              // p.L = local particles, p.l0 = global offset
+    uint32_t Lg, Lmax;          // global particles, per-rank stride
+    int G;                      // ranks (<= 8)
+    const unsigned long long *Call;   // [G][n][Lmax] per-rank inclusive CDFs
+    const float *Sall;          // [G][Lmax][n][H][3] per-rank survivor rows
+};
+cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+                                     int rowlen, float *out, cudaStream_t st);
+cudaError_t launch_gather_propose_multi(const MultiArgs &m, cudaStream_t st);
+cudaError_t launch_select_merge(const unsigned char *recs, int G, size_t rec_bytes, int rowlen, unsigned char *out,
+                                cudaStream_t st);
 
 // K7: final selection + winner row copy
 struct SelectArgs {

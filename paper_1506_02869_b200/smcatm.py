@@ -109,6 +109,7 @@ def load():
         "smc_set_mpc_index": (st, [v, u32]),
         "smc_get_mpc_index": (u32, [v]),
         "smc_launch_count": (u64, [v]),
+        "smc_nccl_unique_id": (st, [v]),
         "smc_debug_rollout": (st, [v, f32p, u32, u32, u32, u32, f32p, P(C.c_uint8), f32p, f32p,
                                    P(C.c_int32), f32p]),
         "smc_debug_evaluate": (st, [v, f32p, u32, u32, u32, f32p]),
@@ -130,7 +131,7 @@ def load():
 
 EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate", "smc_best_controls",
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
-            "smc_launch_count", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
+            "smc_launch_count", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
             "smc_shard_offsets", "smc_slot_count"]
 
@@ -203,6 +204,16 @@ class Solver:
         cfg.use_graph = int(use_graph)
         cfg.profile = int(profile)
         cfg.stream = C.c_void_p(self.stream.cuda_stream)
+        if world_size > 1:
+            # rank 0 creates the NCCL id; torch.distributed (any backend) shares it
+            import torch.distributed as dist
+            buf = (C.c_char * 128)()
+            if rank == 0:
+                self._check_plain(self.lib.smc_nccl_unique_id(buf), "smc_nccl_unique_id")
+            obj = [bytes(buf) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            self._nccl_id = (C.c_char * 128).from_buffer_copy(obj[0])
+            cfg.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p)
         nbytes = self.lib.smc_workspace_bytes(C.byref(cfg))
         if nbytes == 0:
             raise SmcError(SMC_EINVAL, "invalid configuration")
@@ -218,6 +229,11 @@ class Solver:
         self.set_scenario(scn)
 
     # -- helpers -----------------------------------------------------------
+    @staticmethod
+    def _check_plain(rc, what):
+        if rc != SMC_OK:
+            raise SmcError(rc, what)
+
     def _check(self, rc):
         if rc != SMC_OK:
             raise SmcError(rc, self.lib.smc_last_error(self.ctx).decode())

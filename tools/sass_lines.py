@@ -1,0 +1,48 @@
+"""Attribute ncu per-SASS-instruction counts to CUDA source lines.
+
+usage: python tools/sass_lines.py <ncu-rep> <cubin> <mangled-function> [top]
+(cubin: cuobjdump -xelf all libsmcatm.so; needs -lineinfo builds)
+"""
+import csv
+import io
+import re
+import subprocess
+import sys
+from collections import defaultdict
+
+rep, cubin, fn = sys.argv[1:4]
+top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                        capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(csvtxt)))
+hdr = rows[1]
+ia, ie, ist = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+insts = [(int(r[ia], 16), int(r[ie] or 0), int(r[ist] or 0), r[1].strip()) for r in rows[2:] if len(r) == len(hdr)]
+base = insts[0][0]
+dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+cur = None
+off2line = {}
+inside = False
+for line in dis.splitlines():
+    if line.startswith(".text."):
+        inside = line.strip() == f".text.{fn}:"
+        continue
+    if not inside:
+        continue
+    m = re.search(r'//## File "([^"]+)", line (\d+)', line)
+    if m:
+        cur = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
+        continue
+    m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", line)
+    if m and cur:
+        off2line[int(m.group(1), 16)] = cur
+agg = defaultdict(lambda: [0, 0])
+tot = sum(x[1] for x in insts)
+stot = sum(x[2] for x in insts) or 1
+for a, n, st, src in insts:
+    ln = off2line.get(a - base, "?")
+    agg[ln][0] += n
+    agg[ln][1] += st
+for ln, (n, st) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    print(f"{n / tot:7.3f} {st / stot:7.3f}  {ln}")
+print("total", tot)
