@@ -610,8 +610,7 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     }
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
-    CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));
-    ctx->drop_graph();
+    ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
     // automatic K2 layout: lane-per-aircraft segments when N is a power of two
     // (no padded lanes), otherwise warp-per-aircraft (no 25-50% idle lanes)
     ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : (segment_width((int)n) == (int)n ? 0 : 1);

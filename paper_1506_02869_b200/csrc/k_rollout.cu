@@ -299,8 +299,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
                     const bool hit = fly[c] && (q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) &&
                                      (fabsf(dz) < sc.twoPh);
-                    conf[c] = conf[c] || hit;
-                    if (2 * d < W) conf[c] = conf[c] || (__shfl_sync(0xffffffffu, hit ? 1 : 0, (lane - d) & (W - 1), W) != 0);
+                    // all lanes must reach the shuffle: no short-circuit around it
+                    const int back = (2 * d < W) ? __shfl_sync(0xffffffffu, hit ? 1 : 0, (lane - d) & (W - 1), W) : 0;
+                    conf[c] = conf[c] | hit | (back != 0);
                 }
             }
             // ---------------- 5. per-step cost terms at j = t+1, state update

@@ -84,10 +84,10 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     const int n = sc.n, H = sc.H;
     const int nthr = blockDim.x;                      // 32 n
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);              // [H][nthr]
-    float *s_Z = reinterpret_cast<float *>(s_ctrl + H * nthr);      // [PPB][kRow] AR(1) state
-    float *s_W = s_Z + PPB * kRow;                                  // [PPB][kRow] wind at the nodes
-    float4 *s_pos = reinterpret_cast<float4 *>(s_W + PPB * kRow);   // [nthr] (x, y, z, present)
-    float *s_Q = reinterpret_cast<float *>(s_pos + nthr);           // [8][9]
+    float *s_Z = reinterpret_cast<float *>(s_ctrl + H * nthr);      // [H][PPB][kRow] normals -> AR(1) state
+    float *s_W = s_Z + H * PPB * kRow;                              // [H][PPB][kRow] wind at the nodes
+    float4 *s_pos = reinterpret_cast<float4 *>(s_W + H * PPB * kRow); // [2][nthr] (x, y, z, present)
+    float *s_Q = reinterpret_cast<float *>(s_pos + 2 * nthr);       // [8][9]
     __shared__ double s_lam[32];
     __shared__ int s_dec[32];
 
@@ -135,38 +135,46 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
         bool landed = false, viol = false;
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
+        // ---- 1. wind realisation of the whole horizon (Alg.1 l.10), block-wide:
+        //      (a) Philox: 4 blocks x H steps per particle
+        for (int task = tid; task < 4 * H * PPB; task += nthr) {
+            const int q = task % PPB, b = (task / PPB) & 3, ts = task / (4 * PPB);
+            const uint4 w = draw(TAG_WIND, args.l0 + pbase + q, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc,
+                                 sc.key0, sc.key1);
+            const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
+            *reinterpret_cast<float4 *>(&s_Z[(ts * PPB + q) * kRow + 4 * b]) = make_float4(p0.x, p0.y, p1.x, p1.y);
+        }
+        __syncthreads();
+        //      (b) AR(1) over t per (particle, entry), in place: Z(0) = v(0), Z(t) = a Z(t-1) + b v(t)
+        for (int task = tid; task < 16 * PPB; task += nthr) {
+            const int q = task % PPB, e = task / PPB;
+            float zz = s_Z[q * kRow + e];
+            for (int ts = 1; ts < H; ++ts) {
+                float *zp = &s_Z[(ts * PPB + q) * kRow + e];
+                zz = fmaf(sc.a, zz, sc.b * *zp);
+                *zp = zz;
+            }
+        }
+        __syncthreads();
+        //      (c) W(t) = Qhat Z(t) per component
+        for (int task = tid; task < 16 * H * PPB; task += nthr) {
+            const int q = task % PPB, e = (task / PPB) & 15, ts = task / (16 * PPB);
+            const int comp = e >> 3, node = e & 7;
+            const float *zrow = &s_Z[(ts * PPB + q) * kRow + comp * 8];
+            const float4 za = *reinterpret_cast<const float4 *>(zrow);
+            const float4 zb = *reinterpret_cast<const float4 *>(zrow + 4);
+            const float *qr = &s_Q[node * 9];
+            float acc = qr[0] * za.x;
+            acc = fmaf(qr[1], za.y, acc); acc = fmaf(qr[2], za.z, acc); acc = fmaf(qr[3], za.w, acc);
+            acc = fmaf(qr[4], zb.x, acc); acc = fmaf(qr[5], zb.y, acc); acc = fmaf(qr[6], zb.z, acc);
+            acc = fmaf(qr[7], zb.w, acc);
+            s_W[(ts * PPB + q) * kRow + e] = acc;
+        }
+        __syncthreads();
         for (int t = 0; t < H; ++t) {
-            // ---- 1. wind realisation (Alg.1 l.10): 4 Philox blocks per particle, AR(1) update in place
-            for (int task = tid; task < 4 * PPB; task += nthr) {
-                const int b = task / PPB, q = task % PPB;
-                const uint4 w = draw(TAG_WIND, args.l0 + pbase + q, x1, (uint32_t)t | ((uint32_t)b << 16), mpc,
-                                     sc.key0, sc.key1);
-                const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
-                float4 *zr = reinterpret_cast<float4 *>(&s_Z[q * kRow + 4 * b]);
-                float4 zz = *zr;
-                if (t == 0) zz = make_float4(p0.x, p0.y, p1.x, p1.y);
-                else zz = make_float4(fmaf(sc.a, zz.x, sc.b * p0.x), fmaf(sc.a, zz.y, sc.b * p0.y),
-                                      fmaf(sc.a, zz.z, sc.b * p1.x), fmaf(sc.a, zz.w, sc.b * p1.y));
-                *zr = zz;
-            }
-            __syncthreads();
-            // ---- W = Qhat Z per component
-            for (int task = tid; task < 16 * PPB; task += nthr) {
-                const int e = task / PPB, q = task % PPB;
-                const int comp = e >> 3, node = e & 7;
-                const float4 za = *reinterpret_cast<const float4 *>(&s_Z[q * kRow + comp * 8]);
-                const float4 zb = *reinterpret_cast<const float4 *>(&s_Z[q * kRow + comp * 8 + 4]);
-                const float *qr = &s_Q[node * 9];
-                float acc = qr[0] * za.x;
-                acc = fmaf(qr[1], za.y, acc); acc = fmaf(qr[2], za.z, acc); acc = fmaf(qr[3], za.w, acc);
-                acc = fmaf(qr[4], zb.x, acc); acc = fmaf(qr[5], zb.y, acc); acc = fmaf(qr[6], zb.z, acc);
-                acc = fmaf(qr[7], zb.w, acc);
-                s_W[q * kRow + e] = acc;
-            }
-            __syncthreads();
             float Wn[16];
             {
-                const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[p * kRow]);
+                const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[(t * PPB + p) * kRow]);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float4 a4 = w4[q];
@@ -240,13 +248,14 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
                 devA = angdist(th - gA);                          // bearing (R22)
                 devB = fabsf(z_tf - nz);
             }
-            s_pos[tid] = make_float4(nx, ny, nz, fly ? 1.0f : 0.0f);
+            float4 *pos = s_pos + (t & 1) * nthr;          // double-buffered: one barrier per step
+            pos[tid] = make_float4(nx, ny, nz, fly ? 1.0f : 0.0f);
             __syncthreads();
             // ---- 4. separation against the other aircraft of this (particle, candidate);
             //         the own entry always hits itself when present
             int cnt = 0;
             for (int q = 0; q < n; ++q) {
-                const float4 o = s_pos[q * 32 + lane];
+                const float4 o = pos[q * 32 + lane];
                 const float dx = nx - o.x, dy = ny - o.y, dz = nz - o.z;
                 cnt += ((o.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh)) ? 1 : 0;
             }
@@ -351,7 +360,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
 
 size_t rollout_t_smem_bytes(int n, int H) {
     const int nthr = 32 * n;
-    return sizeof(float4) * (size_t)H * nthr + sizeof(float) * 2 * 32 * kRow + sizeof(float4) * nthr +
+    return sizeof(float4) * (size_t)H * nthr + sizeof(float) * 2 * (size_t)H * 32 * kRow + sizeof(float4) * 2 * nthr +
            sizeof(float) * 72 + 16;
 }
 

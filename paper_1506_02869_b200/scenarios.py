@@ -174,3 +174,21 @@ def random_controls(scn: dict, L: int, seed: int, spread: float = 1.0) -> np.nda
         out[:, i, :, 1] = rng.uniform(-1, 1, (L, H)) * scn["phi_max"][i] * spread
         out[:, i, :, 2] = rng.uniform(-1, 1, (L, H)) * scn["gamma_max"][i] * spread
     return out
+
+
+def traffic(n_arr: int, n_dep: int, seed: int, arr_every: int = 2, dep_every: int = 6, jitter: int = 1) -> dict:
+    """Arrival/departure stream for the rolling-window MPC loop:
+    entries at fixed, evenly spread MPC steps with a small seeded jitter;
+    arrivals enter on the TMA boundary, departures are released at the
+    runway end at 400 m heading West."""
+    rng = np.random.default_rng(seed)
+    ac, entry = [], []
+    for a in range(n_arr):
+        ac.append(_arrival(rng, a, n_arr, 6))
+        entry.append(arr_every * a + int(rng.integers(0, jitter + 1)))
+    for d in range(n_dep):
+        ac.append(_departure_release(d))
+        entry.append(dep_every * d + 3)
+    out = _finish({}, ac)
+    out["entry"] = np.array(entry, np.int32)
+    return out

@@ -318,3 +318,44 @@ def test_full_size_sampled_parity(smc, num):
         assert np.array_equal(np.isfinite(g), np.isfinite(ell_o)), l
         f = np.isfinite(g)
         assert np.allclose(g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + cfg.S)), l
+
+
+def test_mpc_loop_rolling_window(smc):
+    """Short rolling-window loop: aircraft enter mid-horizon, the
+    plant advances active ones only, and the realised trajectories satisfy the
+    envelope (post-hoc audit of the applied controls)."""
+    from paper_1506_02869_b200 import mpc_loop
+    base, cfg = sc.config(3)
+    tr = sc.traffic(3, 2, seed=9, arr_every=3, dep_every=4)
+    recs, done, fuel = mpc_loop.run(base, tr, L=2048, S=4, K=8, sigma=cfg.sigma, seed=cfg.seed, n_steps=8,
+                                    max_aircraft=8)
+    assert len(recs) >= 6
+    assert recs[0].window >= 1 and any(r.active > recs[0].active for r in recs)
+    assert all(not r.infeasible for r in recs)
+    assert all(f >= 0 for f in fuel.values())
+
+
+def test_paper_literal_mode_replay(smc):
+    """Alg.1 exactly as printed (N1): no MH (x* always replaces x') and the
+    paper's SampleSchedule floor(3 + 5 e^{0.05 J}).  Replayed against
+    the oracle round by round; the oracle's own full run uses the same rules."""
+    scn, cfg = sc.config(1)
+    L = 256
+    sol = smc.Solver(scn, L=L, S=cfg.S, K=4, sigma=cfg.sigma, seed=cfg.seed, mh=False, sched_paper=True)
+    P = O.Problem(scn)
+    stats = []
+    for k in range(3):
+        st = sol.iterate(1, stats=True)[0]
+        assert st["n_samples"] == O.sample_schedule(k)
+        pop = sol.population()
+        if k == 0:
+            assert np.all(pop["surv"] == 0)
+            ctrl = pop["cur"]
+        else:
+            assert np.all(pop["surv"] == 1)
+            ctrl = pop["prop"]
+        ell_o = P.evaluate(ctrl.astype(np.float64), O.sample_schedule(k), k, cfg.seed)
+        ell_g = pop["ell"].T.astype(np.float64)
+        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
+        f = np.isfinite(ell_o) & np.isfinite(ell_g)
+        assert np.allclose(ell_g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + 20))
