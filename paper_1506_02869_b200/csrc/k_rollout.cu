@@ -22,6 +22,10 @@
 #include "smc_device.cuh"
 #include "smc_kernels.h"
 
+#ifndef SMC_K2_MINB
+#define SMC_K2_MINB 5   // resident 128-thread blocks per SM the register budget targets
+#endif
+
 namespace smc {
 
 __device__ __forceinline__ float clamp01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
@@ -86,7 +90,7 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
 }
 
 template <int W, int NC, bool DEBUG>
-__global__ void __launch_bounds__(kBlock, 5)
+__global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
     constexpr int E = (16 + W - 1) / W;           // wind-field entries owned per lane
@@ -235,12 +239,13 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             // ---------------- 2-3. dynamics, unary checks and geometry per candidate
             const bool act = first <= t;
             bool fly[NC], vnow[NC], lnow[NC];
-            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC];
+            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC], Tc[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 fly[c] = act && !landed[c] && !viol[c];
                 const float4 cc = s_ctrl[(t * NC + c) * kBlock + tid];
                 const float T = cc.x, tph = cc.y, sga = cc.z, cga = cc.w;
+                Tc[c] = T;
                 // wind at the pre-step position (trilinear, clamped to the box)
                 const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
                 const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
@@ -271,7 +276,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 bad |= !(nz[c] >= zmin && nz[c] <= zmax);
                 bad |= !(nv[c] >= vmin && nv[c] <= vmax);
                 bad |= !(nm[c] >= mempty);
-                bad |= !(fabsf(nx[c]) <= 3.0e38f) || !(fabsf(ny[c]) <= 3.0e38f) || !(fabsf(nchi[c]) <= 3.0e38f);
+                // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
                 vnow[c] = bad;
                 th[c] = fast_atan2(ny[c], nx[c]);
                 // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
@@ -323,7 +328,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 sC[c] += fly[c] ? devC : 0.0f;
                 // "best possible cost, 1, for all remaining steps" after landing
                 sN[c] += fly[c] ? nzs : ((act && landed[c]) ? 1.0f : 0.0f);
-                fuel[c] += fly[c] ? dt_eta * s_ctrl[(t * NC + c) * kBlock + tid].x : 0.0f;
+                fuel[c] += fly[c] ? dt_eta * Tc[c] : 0.0f;
                 viol[c] = viol[c] || (fly[c] && vnow[c]);
                 landed[c] = landed[c] || (fly[c] && lnow[c]);
                 x[c] = fly[c] ? nx[c] : x[c];
@@ -372,7 +377,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     }
                     if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * sN[c] * invHa;
                 }
-                ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + log2f(J);
+                ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
                 if (DEBUG && c == 0 && valid && isac) {
                     const size_t o = ((size_t)lloc * args.S + s) * n + lane;
                     if (args.dbg_J) args.dbg_J[o] = J;

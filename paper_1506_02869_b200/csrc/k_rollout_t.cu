@@ -230,7 +230,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             vnow |= !(nz >= zmin && nz <= zmax);
             vnow |= !(nv >= vmin && nv <= vmax);
             vnow |= !(nm >= mempty);
-            vnow |= !(fabsf(nx) <= 3.0e38f) || !(fabsf(ny) <= 3.0e38f) || !(fabsf(nchi) <= 3.0e38f);
+            // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
             const float th = atan2_p(ny, nx);
             float devA, devB;
             bool lnow = false;
@@ -307,7 +307,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             }
             if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * sN * invHa;
         }
-        ell = (viol || !(J > 0.0f)) ? -INFINITY : ell + log2f(J);
+        ell = (viol || !(J > 0.0f)) ? -INFINITY : ell + __log2f(J);
         if (DEBUG && c == 0 && valid) {
             const size_t o = ((size_t)lloc * args.S + s) * n + i;
             if (args.dbg_J) args.dbg_J[o] = J;

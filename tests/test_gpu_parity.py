@@ -326,7 +326,7 @@ def test_mpc_loop_rolling_window(smc):
     envelope (post-hoc audit of the applied controls)."""
     from paper_1506_02869_b200 import mpc_loop
     base, cfg = sc.config(3)
-    tr = sc.traffic(3, 2, seed=9, arr_every=3, dep_every=4)
+    tr = sc.traffic(3, 2, seed=9, arr_every=3, dep_every=10)
     recs, done, fuel = mpc_loop.run(base, tr, L=2048, S=4, K=8, sigma=cfg.sigma, seed=cfg.seed, n_steps=8,
                                     max_aircraft=8)
     assert len(recs) >= 6
