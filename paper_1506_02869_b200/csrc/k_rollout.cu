@@ -23,7 +23,7 @@
 #include "smc_kernels.h"
 
 #ifndef SMC_K2_MINB
-#define SMC_K2_MINB 5   // resident 128-thread blocks per SM the register budget targets
+#define SMC_K2_MINB 4   // resident 128-thread blocks per SM the register budget targets (A/B: 4 > 5 > 6)
 #endif
 
 namespace smc {

@@ -73,6 +73,7 @@ __device__ __forceinline__ float popdense_t(const DevScen &sc, float x, float y)
 }
 
 constexpr int kRow = 20;   // padded row of the 16 wind entries: conflict-free LDS.128 per lane
+constexpr int kHalfScanN = 6;   // from this many aircraft the half pair scan (+1 barrier) pays off
 
 }  // namespace
 
@@ -88,6 +89,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     float *s_W = s_Z + H * PPB * kRow;                              // [H][PPB][kRow] wind at the nodes
     float4 *s_pos = reinterpret_cast<float4 *>(s_W + H * PPB * kRow); // [2][nthr] (x, y, z, present)
     float *s_Q = reinterpret_cast<float *>(s_pos + 2 * nthr);       // [8][9]
+    unsigned char *s_flag = reinterpret_cast<unsigned char *>(s_Q + 72);   // [nthr][16] pair verdicts
     __shared__ double s_lam[32];
     __shared__ int s_dec[32];
 
@@ -100,6 +102,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     const uint32_t k = args.k, mpc = *args.mpcp;
 
     for (int q = tid; q < 64; q += blockDim.x) s_Q[(q >> 3) * 9 + (q & 7)] = sc.Qhat[q];
+    reinterpret_cast<uint4 *>(s_flag)[tid] = make_uint4(0u, 0u, 0u, 0u);
 
     const DevAircraft *Ap = sc.ac + i;
     const int kind = Ap->kind, first = Ap->first_step;
@@ -251,15 +254,35 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             float4 *pos = s_pos + (t & 1) * nthr;          // double-buffered: one barrier per step
             pos[tid] = make_float4(nx, ny, nz, fly ? 1.0f : 0.0f);
             __syncthreads();
-            // ---- 4. separation against the other aircraft of this (particle, candidate);
-            //         the own entry always hits itself when present
-            int cnt = 0;
-            for (int q = 0; q < n; ++q) {
-                const float4 o = pos[q * 32 + lane];
-                const float dx = nx - o.x, dy = ny - o.y, dz = nz - o.z;
-                cnt += ((o.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh)) ? 1 : 0;
+            // ---- 4. separation (Eq. avoidance) against the other aircraft of this (particle, candidate)
+            if (n >= kHalfScanN) {
+                // each unordered pair once: warp i checks aircraft i+d (mod n), d = 1..n/2, and leaves
+                // the verdict in a per-(partner, d) byte the partner reads after one more barrier
+                // (for even n the d = n/2 pair is checked by both warps and needs no hand-over)
+                const int D = (n - 1) / 2;
+                bool conf = false;
+                for (int d = 1; d <= n / 2; ++d) {
+                    int q = i + d;
+                    q = q >= n ? q - n : q;
+                    const float4 o = pos[q * 32 + lane];
+                    const float dx = nx - o.x, dy = ny - o.y, dz = nz - o.z;
+                    const bool hit = fly && (o.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh);
+                    conf = conf || hit;
+                    if (d <= D) s_flag[(q * 32 + lane) * 16 + d - 1] = hit ? 1 : 0;
+                }
+                __syncthreads();
+                const uint4 f = *reinterpret_cast<const uint4 *>(&s_flag[tid * 16]);
+                vnow = vnow || conf || ((f.x | f.y | f.z | f.w) != 0u);
+            } else {
+                // small n: full scan; the own entry always hits itself when present
+                int cnt = 0;
+                for (int q = 0; q < n; ++q) {
+                    const float4 o = pos[q * 32 + lane];
+                    const float dx = nx - o.x, dy = ny - o.y, dz = nz - o.z;
+                    cnt += ((o.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh)) ? 1 : 0;
+                }
+                vnow = vnow || (cnt > 1);
             }
-            vnow = vnow || (cnt > 1);
             // ---- 5. cost terms at j = t+1 and state update
             float nzs = 0.0f;
             if (sc.has_noise) {
@@ -361,7 +384,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
 size_t rollout_t_smem_bytes(int n, int H) {
     const int nthr = 32 * n;
     return sizeof(float4) * (size_t)H * nthr + sizeof(float) * 2 * (size_t)H * 32 * kRow + sizeof(float4) * 2 * nthr +
-           sizeof(float) * 72 + 16;
+           sizeof(float) * 72 + 16 * (size_t)nthr + 16;
 }
 
 template <int NC, int MAXT, int MINB, bool DEBUG>
