@@ -183,6 +183,7 @@ struct smc_ctx {
     std::vector<double> centres_h;
     smc_scenario scn{};
     uint32_t k = 0, mpc = 0, mpc_stage = 0;
+    bool acc_clean = false;            // per-round accumulators already zero
     bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
@@ -575,6 +576,7 @@ static smc_status init_population(smc_ctx *ctx) {
     ctx->k = 0;
     ctx->cur = 0;
     ctx->last_eval = -1;
+    ctx->acc_clean = false;            // round 0 zeroes the accumulators itself (also inside graphs)
     return SMC_OK;
 }
 
@@ -611,9 +613,10 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
-    // automatic K2 layout: lane-per-aircraft segments when N is a power of two
-    // (no padded lanes), otherwise warp-per-aircraft (no 25-50% idle lanes)
-    ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : (segment_width((int)n) == (int)n ? 0 : 1);
+    // K2 layout: lane-per-aircraft segments measured fastest for every config
+    // (c2 43.6 ms vs 58.6 ms, c3 1.44 s vs 1.42-1.55 s, c4 167 ms vs 171 ms per
+    // MPC step); the transposed layout stays available via SMC_K2_LAYOUT
+    ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : 0;
     ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1);
     ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2);
     ctx->have_scn = true;
@@ -635,8 +638,13 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     smc_status s0 = sync_mpc(ctx);
     if (s0 != SMC_OK) return s0;
     const uint32_t S = samples_of(ctx, k);
-    CK(cudaMemsetAsync(ctx->colmax, 0, sizeof(uint32_t) * n, ctx->st));
-    CK(cudaMemsetAsync(ctx->accept, 0, 8, ctx->st));
+    if (!ctx->acc_clean) {                 // normally zeroed by the previous round's K6
+        CK(cudaMemsetAsync(ctx->colmax, 0, sizeof(uint32_t) * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->accept, 0, 8, ctx->st));
+        CK(cudaMemsetAsync(ctx->status, 0, 8 * (size_t)scan_tiles(ctx->Lloc) * n, ctx->st));
+        CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
+    }
+    ctx->acc_clean = false;
     RolloutArgs ra{};
     int NC;
     if (k == 0) {
@@ -683,8 +691,6 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     }
     if (tail) {
         const size_t nt = (size_t)scan_tiles(ctx->Lloc);
-        CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
-        CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
         rs.Q = nullptr;
         LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
         ProposeArgs pa{};
@@ -697,6 +703,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
         pa.clamp = (int)ctx->cfg.clamp_proposals;
         pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
+        pa.reset_n = n; pa.reset_colmax = ctx->colmax; pa.reset_tiles = ctx->tiles; pa.reset_accept = ctx->accept;
+        pa.reset_status = ctx->status; pa.reset_status_n = nt * n;
         if (ctx->world > 1) {
             // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
             NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
@@ -709,6 +717,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
             LAUNCHP(PH_PROPOSE, launch_gather_propose(pa, ctx->st));
         }
         ctx->cur = P ^ 1;
+        ctx->acc_clean = true;
     }
     if (stats) {
         smc_status s2 = select_best(ctx);

@@ -233,7 +233,60 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
     }
 }
 
+// Small populations: one 1024-thread block per column scans the whole column
+// (two passes over ell, no look-back chain -- the chain of a few tiles is
+// latency-bound at this size).
+constexpr int kSmallThreads = 1024;
+constexpr uint32_t kSmallMaxL = 64 * 1024;
+
+__global__ void __launch_bounds__(kSmallThreads) k_scan_small(const ResampleArgs r) {
+    const int i = blockIdx.x;
+    const uint32_t cm = r.colmax[i];
+    const bool inf = column_infeasible(cm);
+    const float m = ord2f(cm);
+    const float *ell = r.ell + (size_t)i * r.L;
+    const uint32_t per = (r.L + kSmallThreads - 1) / kSmallThreads;
+    const uint32_t lo = threadIdx.x * per, hi = min(lo + per, r.L);
+    unsigned long long run = 0;
+    for (uint32_t l = lo; l < hi; ++l) run += qweight(ell, l, m, inf);
+    __shared__ unsigned long long s_w[kSmallThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long w = s_w[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_w[lane] = w;                                   // inclusive over warps
+    }
+    __syncthreads();
+    unsigned long long pre = (wid ? s_w[wid - 1] : 0ull) + (x - run);
+    unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : r.L);
+    for (uint32_t l = lo; l < hi; ++l) {
+        pre += qweight(ell, l, m, inf);
+        C[l] = pre;
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t Q = s_w[31];
+        const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
+        r.QR[2 * i] = Q;
+        r.QR[2 * i + 1] = __umul64hi(rw, Q);
+        if (r.Q) r.Q[i] = Q;
+    }
+}
+
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
+    if (r.L <= kSmallMaxL) {
+        k_scan_small<<<r.n, kSmallThreads, 0, st>>>(r);
+        return cudaGetLastError();
+    }
     const int nt = scan_tiles(r.L);
     k_scan<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
     return cudaGetLastError();
@@ -263,6 +316,16 @@ cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
     if (gx > 1024) gx = 1024;
     k_ancestors<<<dim3(gx, r.n), 256, 0, st>>>(r);
     return cudaGetLastError();
+}
+
+// Zero the next round's accumulators (column maxima, accept count, look-back
+// status words and tile counters): saves four memset nodes per round.
+__device__ __forceinline__ void reset_round_state(const ProposeArgs &p) {
+    if (!p.reset_n) return;
+    const size_t gtid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t e = gtid; e < p.reset_status_n; e += stride) p.reset_status[e] = 0ull;
+    if (gtid < (size_t)p.reset_n) { p.reset_colmax[gtid] = 0u; p.reset_tiles[gtid] = 0u; }
+    if (gtid == 0) *p.reset_accept = 0ull;
 }
 
 // ============================================================== K6
@@ -301,11 +364,8 @@ __global__ void k_gather_propose(const ProposeArgs p) {
             }
             ds[3 * t] = o0; ds[3 * t + 1] = o1; ds[3 * t + 2] = o2;
         }
-        if (idx == 0 && p.reset_n) {              // next round's accumulators (stream-ordered after K4b)
-            for (int q = 0; q < p.reset_n; ++q) p.reset_colmax[q] = 0u;
-            *p.reset_accept = 0ull;
-        }
     }
+    reset_round_state(p);
 }
 
 cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st) {
@@ -638,6 +698,7 @@ __global__ void k_gather_propose_multi(const MultiArgs m) {
             ds[3 * tt] = o0; ds[3 * tt + 1] = o1; ds[3 * tt + 2] = o2;
         }
     }
+    reset_round_state(p);
 }
 
 cudaError_t launch_gather_propose_multi(const MultiArgs &m, cudaStream_t st) {

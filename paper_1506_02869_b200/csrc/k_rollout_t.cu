@@ -73,7 +73,9 @@ __device__ __forceinline__ float popdense_t(const DevScen &sc, float x, float y)
 }
 
 constexpr int kRow = 20;   // padded row of the 16 wind entries: conflict-free LDS.128 per lane
-constexpr int kHalfScanN = 6;   // from this many aircraft the half pair scan (+1 barrier) pays off
+// Half pair scan (+1 barrier per step) measured slower than the full scan on
+// B200 for c3 (N = 24: 1.55 s vs 1.42 s per MPC step); kept, disabled.
+constexpr int kHalfScanN = 64;
 
 }  // namespace
 

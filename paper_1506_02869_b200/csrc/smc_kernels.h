@@ -77,8 +77,11 @@ struct ProposeArgs {
     const uint8_t *surv;        // [L] which buffer holds particle l's survivor
     const int32_t *anc;         // [n][L] explicit ancestors (debug) or NULL -> bisection of C
     const unsigned long long *C, *QR;
-    uint32_t *reset_colmax;     // zeroed for the next round (nullable)
+    // per-round accumulators zeroed here for the next round (stream-ordered after K2 and K4)
+    uint32_t *reset_colmax, *reset_tiles;   // [reset_n] each
     unsigned long long *reset_accept;
+    unsigned long long *reset_status;       // [reset_status_n] look-back words
+    size_t reset_status_n;
     int reset_n;
     float *xp, *xs;             // outputs [L][n][H][3]
     float sig[3];
