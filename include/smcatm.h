@@ -122,6 +122,11 @@ typedef struct {
     uint32_t max_horizon;      /* capacity (<= 32)                                    */
     uint32_t use_graph;        /* 1: replay the round loop as a CUDA graph            */
     uint32_t profile;          /* 1: time each phase with CUDA events (smc_phase_times) */
+    uint32_t virtual_world;    /* test mode (world_size 1): run the multi-GPU resampling and
+                                  selection path -- per-shard CDFs, survivor exchange layout,
+                                  shard-aware gather, record merge -- for this many virtual
+                                  ranks on one GPU; results are bit-identical to 1 / 0 */
+    uint32_t reserved;
 } smc_config;
 
 /* Per-round diagnostics (smc_iterate). */

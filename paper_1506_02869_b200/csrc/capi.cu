@@ -80,7 +80,11 @@ size_t part_bytes(uint32_t Lloc, int nmax) {
 // Bump-allocate every device buffer from the caller's workspace.
 size_t record_bytes(int nmax, int Hmax) { return (16 + (size_t)nmax * Hmax * 12 + 15) & ~(size_t)15; }
 
-Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1) {
+// world: real ranks (Lloc = this rank's share); vworld: virtual ranks inside one context
+// (test mode, Lloc = L).  G = ranks whose CDFs / survivors / records are exchanged.
+Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) {
+    const int G = world > 1 ? world : vworld;
+    const uint32_t Lx = world > 1 ? Lloc : (Lloc + vworld - 1) / vworld;   // per-rank stride
     Layout o{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t at = off; off += align_up(bytes); return at; };
@@ -94,7 +98,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1) {
     o.colmax = take(nmax * sizeof(uint32_t));
     o.Q = take(nmax * sizeof(unsigned long long));
     o.ess = take(2 * nmax * sizeof(double));
-    o.status = take((size_t)nmax * scan_tiles(Lloc) * 8);
+    o.status = take((size_t)nmax * scan_tiles_max(Lloc) * 8);
     o.tiles = take(2 * nmax * sizeof(uint32_t));
     o.C = take((size_t)nmax * Lloc * sizeof(unsigned long long));
     o.QR = take(2 * nmax * sizeof(unsigned long long));
@@ -109,10 +113,10 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1) {
     o.done = take(sizeof(unsigned));
     o.best_lam = take(record_bytes(nmax, Hmax));               // local selection record
     o.best_idx = take(record_bytes(nmax, Hmax));               // final (merged) record
-    o.best_row = take(world > 1 ? record_bytes(nmax, Hmax) * world : 0);   // all-gathered records
-    o.Call = take(world > 1 ? (size_t)world * nmax * Lloc * 8 : 0);
+    o.best_row = take(G > 1 ? record_bytes(nmax, Hmax) * G : 0);           // all-gathered records
+    o.Call = take(G > 1 ? (size_t)G * nmax * Lx * 8 : 0);
     o.Sc = take(world > 1 ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
-    o.Sall = take(world > 1 ? (size_t)world * Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.Sall = take(G > 1 ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
     o.pZ = take(16 * sizeof(double));
     o.pzi = take(sizeof(int));
     o.pstates = take(nmax * 6 * sizeof(double));
@@ -169,7 +173,7 @@ struct smc_ctx {
     long long *sel_idx = nullptr;
     float *sel_row = nullptr;
     // multi-GPU
-    int world = 1, rank = 0;
+    int world = 1, rank = 0, vworld = 1;
     uint32_t Lmax = 0;
     ncclComm_t comm = nullptr;
     unsigned long long *Call = nullptr;
@@ -295,7 +299,8 @@ extern "C" size_t smc_workspace_bytes(const smc_config *cfg) {
         cfg->max_horizon > 32)
         return 0;
     const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
-    return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon, world).total;
+    const int vw = (world == 1 && cfg->virtual_world > 1) ? (int)cfg->virtual_world : 1;
+    return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon, world, vw).total;
 }
 
 extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
@@ -327,7 +332,9 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->Lloc -= ctx->l0;
     ctx->nmax = (int)cfg->max_aircraft;
     ctx->Hmax = (int)cfg->max_horizon;
-    ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax, world);
+    ctx->vworld = (world == 1 && cfg->virtual_world > 1) ? (int)cfg->virtual_world : 1;
+    if (ctx->vworld > 8 || ctx->Lg < (uint32_t)ctx->vworld) { delete ctx; return SMC_EINVAL; }
+    ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax, world, ctx->vworld);
     if (!cfg->workspace || cfg->workspace_bytes < ctx->lay.total) {
         delete ctx;
         return SMC_ENOMEM;
@@ -373,7 +380,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->done = (unsigned *)(ws + L.done);
     ctx->rec_bytes = record_bytes(ctx->nmax, ctx->Hmax);
     ctx->rec_local = (unsigned char *)(ws + L.best_lam);
-    ctx->rec_final = world > 1 ? (unsigned char *)(ws + L.best_idx) : ctx->rec_local;
+    ctx->rec_final = (world > 1 || ctx->vworld > 1) ? (unsigned char *)(ws + L.best_idx) : ctx->rec_local;
     ctx->rec_all = (unsigned char *)(ws + L.best_row);
     ctx->sel_lam = (double *)ctx->rec_local;
     ctx->sel_idx = (long long *)(ctx->rec_local + 8);
@@ -381,7 +388,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->best_lam = (double *)ctx->rec_final;
     ctx->best_idx = (long long *)(ctx->rec_final + 8);
     ctx->best_row = (float *)(ctx->rec_final + 16);
-    ctx->Lmax = max_local(ctx->Lg, world);
+    ctx->Lmax = world > 1 ? max_local(ctx->Lg, world) : max_local(ctx->Lg, ctx->vworld);
     ctx->Call = (unsigned long long *)(ws + L.Call);
     ctx->Sc = (float *)(ws + L.Sc);
     ctx->Sall = (float *)(ws + L.Sall);
@@ -683,11 +690,19 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
     rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
     rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR; rs.Cstride = ctx->world > 1 ? ctx->Lmax : 0;
+    uint32_t cm[32];
+    double ess[64];
+    unsigned long long acc = 0;
     if (stats) {
         CK(cudaMemsetAsync(ctx->ess, 0, 16 * n, ctx->st));
         CK(cudaMemsetAsync(ctx->Q, 0, 8 * n, ctx->st));
         rs.Q = ctx->Q;
         LAUNCHP(PH_RESAMPLE, launch_qsum(rs, ctx->st));
+        // read the round's accumulators before K6 zeroes them for the next round
+        CK(cudaMemcpyAsync(cm, ctx->colmax, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(ess, ctx->ess, 16 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(&acc, ctx->accept, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
     }
     if (tail) {
         const size_t nt = (size_t)scan_tiles(ctx->Lloc);
@@ -705,7 +720,37 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
         pa.reset_n = n; pa.reset_colmax = ctx->colmax; pa.reset_tiles = ctx->tiles; pa.reset_accept = ctx->accept;
         pa.reset_status = ctx->status; pa.reset_status_n = nt * n;
-        if (ctx->world > 1) {
+        if (ctx->vworld > 1) {
+            // virtual ranks (test mode): the multi-GPU path with the exchange done in place
+            const int G = ctx->vworld;
+            const int rowlen = n * H * 3;
+            const size_t ntv = (size_t)scan_tiles(ctx->Lmax);
+            for (int r = 0; r < G; ++r) {
+                uint32_t b, e;
+                smc_shard_range(ctx->Lg, G, r, &b, &e);
+                ResampleArgs rr = rs;
+                rr.L = e - b; rr.ell = ctx->ell + b; rr.ell_stride = ctx->Lloc;
+                rr.C = ctx->Call + (size_t)r * n * ctx->Lmax; rr.Cstride = ctx->Lmax;
+                CK(cudaMemsetAsync(ctx->status, 0, 8 * ntv * n, ctx->st));
+                CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
+                LAUNCHP(PH_RESAMPLE, launch_scan(rr, ctx->st));
+                LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0] + (size_t)b * rowlen,
+                                                             ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b,
+                                                             rowlen, ctx->Sall + (size_t)r * ctx->Lmax * rowlen, ctx->st));
+            }
+            for (int r = 0; r < G; ++r) {
+                uint32_t b, e;
+                smc_shard_range(ctx->Lg, G, r, &b, &e);
+                ProposeArgs pr = pa;
+                pr.L = e - b; pr.l0 = b;
+                pr.xp = ctx->ctrl[P ^ 1][0] + (size_t)b * rowlen; pr.xs = ctx->ctrl[P ^ 1][1] + (size_t)b * rowlen;
+                pr.reset_status_n = 0;
+                MultiArgs ma{pr, ctx->Lg, ctx->Lmax, G, ctx->Call, ctx->Sall};
+                LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
+            }
+            CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
+            CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
+        } else if (ctx->world > 1) {
             // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
             NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
             LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc,
@@ -722,13 +767,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     if (stats) {
         smc_status s2 = select_best(ctx);
         if (s2 != SMC_OK) return s2;
-        uint32_t cm[32];
-        double ess[64], bl;
-        unsigned long long acc;
-        CK(cudaMemcpyAsync(cm, ctx->colmax, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CK(cudaMemcpyAsync(ess, ctx->ess, 16 * n, cudaMemcpyDeviceToHost, ctx->st));
+        double bl;
         CK(cudaMemcpyAsync(&bl, ctx->best_lam, 8, cudaMemcpyDeviceToHost, ctx->st));
-        CK(cudaMemcpyAsync(&acc, ctx->accept, 8, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         stats->best_lambda = bl;
         stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / ctx->Lloc : 1.0);
@@ -764,6 +804,21 @@ extern "C" smc_status smc_iterate(smc_ctx *ctx, uint32_t n_rounds, smc_round_sta
 static smc_status select_best(smc_ctx *ctx) {
     if (ctx->last_eval < 0) return fail(ctx, SMC_ESTATE, "no evaluated population");
     const int P = ctx->last_eval;
+    if (ctx->vworld > 1) {                // virtual ranks: per-shard records, then the multi-GPU merge
+        const int rowlen = ctx->dsc.n * ctx->dsc.H * 3;
+        for (int r = 0; r < ctx->vworld; ++r) {
+            uint32_t b, e;
+            smc_shard_range(ctx->Lg, ctx->vworld, r, &b, &e);
+            unsigned char *rec = ctx->rec_all + (size_t)r * ctx->rec_bytes;
+            SelectArgs sr{e - b, b, ctx->dsc.n, ctx->dsc.H, ctx->lam + b, ctx->surv + b,
+                          {ctx->ctrl[P][0] + (size_t)b * rowlen, ctx->ctrl[P][1] + (size_t)b * rowlen},
+                          ctx->part_lam, ctx->part_idx, ctx->done, (double *)rec, (long long *)(rec + 8),
+                          (float *)(rec + 16)};
+            LAUNCH(launch_select(sr, ctx->st));
+        }
+        LAUNCH(launch_select_merge(ctx->rec_all, ctx->vworld, ctx->rec_bytes, rowlen, ctx->rec_final, ctx->st));
+        return SMC_OK;
+    }
     SelectArgs sa{ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
                   ctx->part_lam, ctx->part_idx, ctx->done, ctx->sel_lam, ctx->sel_idx, ctx->sel_row};
     LAUNCH(launch_select(sa, ctx->st));

@@ -63,10 +63,14 @@ __host__ __device__ uint64_t slot_count(uint64_t C, uint64_t Q, uint64_t R, uint
 
 // ============================================================== K4a
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kTile = kScanThreads * kScanItems;
-
-int scan_tiles(uint32_t L) { return (int)((L + kTile - 1) / kTile); }
+// Items per thread of the look-back scan: 2 (512-element tiles, more blocks in
+// flight) for small populations, 8 (2048-element tiles) for large ones.
+int scan_items(uint32_t L) { return L < (1u << 17) ? 2 : 8; }
+int scan_tiles(uint32_t L) {
+    const uint32_t tile = (uint32_t)kScanThreads * scan_items(L);
+    return (int)((L + tile - 1) / tile);
+}
+int scan_tiles_max(uint32_t L) { return (int)((L + 511) / 512); }
 
 __device__ __forceinline__ bool column_infeasible(uint32_t cm) {
     return cm == 0u || cm == f2ord(-INFINITY);
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(kScanThreads) k_qsum(const ResampleArgs r) {
     const uint32_t cm = r.colmax[i];
     const bool inf = column_infeasible(cm);
     const float m = ord2f(cm);
-    const float *ell = r.ell + (size_t)i * r.L;
+    const float *ell = r.ell + (size_t)i * (r.ell_stride ? r.ell_stride : r.L);
     unsigned long long sum = 0;
     double s1 = 0.0, s2 = 0.0;
     for (uint32_t l = blockIdx.x * kScanThreads + threadIdx.x; l < r.L; l += gridDim.x * kScanThreads) {
@@ -193,7 +197,9 @@ __device__ unsigned long long block_exclusive(unsigned long long v, unsigned lon
 // Inclusive scan C_l = sum_{l' <= l} q_l' per column (uint64, exact), single pass
 // with decoupled look-back.  The block that owns the last tile of a column also
 // publishes (Q, R): Q = C_{L-1}, R = floor(r64 * Q / 2^64) (RESAMPLE stream).
+template <int kScanItems>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int ntiles) {
+    constexpr int kTile = kScanThreads * kScanItems;
     const int i = blockIdx.y;
     __shared__ int s_tile;
     __shared__ unsigned long long s_pre;
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
     const uint32_t cm = r.colmax[i];
     const bool inf = column_infeasible(cm);
     const float m = ord2f(cm);
-    const float *ell = r.ell + (size_t)i * r.L;
+    const float *ell = r.ell + (size_t)i * (r.ell_stride ? r.ell_stride : r.L);
     const uint32_t base = (uint32_t)tile * kTile + threadIdx.x * kScanItems;
     uint64_t inc[kScanItems];
     uint64_t run = 0;
@@ -233,62 +239,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
     }
 }
 
-// Small populations: one 1024-thread block per column scans the whole column
-// (two passes over ell, no look-back chain -- the chain of a few tiles is
-// latency-bound at this size).
-constexpr int kSmallThreads = 1024;
-constexpr uint32_t kSmallMaxL = 64 * 1024;
-
-__global__ void __launch_bounds__(kSmallThreads) k_scan_small(const ResampleArgs r) {
-    const int i = blockIdx.x;
-    const uint32_t cm = r.colmax[i];
-    const bool inf = column_infeasible(cm);
-    const float m = ord2f(cm);
-    const float *ell = r.ell + (size_t)i * r.L;
-    const uint32_t per = (r.L + kSmallThreads - 1) / kSmallThreads;
-    const uint32_t lo = threadIdx.x * per, hi = min(lo + per, r.L);
-    unsigned long long run = 0;
-    for (uint32_t l = lo; l < hi; ++l) run += qweight(ell, l, m, inf);
-    __shared__ unsigned long long s_w[kSmallThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long x = run;
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        unsigned long long w = s_w[lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        s_w[lane] = w;                                   // inclusive over warps
-    }
-    __syncthreads();
-    unsigned long long pre = (wid ? s_w[wid - 1] : 0ull) + (x - run);
-    unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : r.L);
-    for (uint32_t l = lo; l < hi; ++l) {
-        pre += qweight(ell, l, m, inf);
-        C[l] = pre;
-    }
-    if (threadIdx.x == 0) {
-        const uint64_t Q = s_w[31];
-        const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
-        r.QR[2 * i] = Q;
-        r.QR[2 * i + 1] = __umul64hi(rw, Q);
-        if (r.Q) r.Q[i] = Q;
-    }
-}
-
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
-    if (r.L <= kSmallMaxL) {
-        k_scan_small<<<r.n, kSmallThreads, 0, st>>>(r);
-        return cudaGetLastError();
-    }
     const int nt = scan_tiles(r.L);
-    k_scan<<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    if (scan_items(r.L) == 2) k_scan<2><<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    else k_scan<8><<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
     return cudaGetLastError();
 }
 
@@ -329,51 +283,71 @@ __device__ __forceinline__ void reset_round_state(const ProposeArgs &p) {
 }
 
 // ============================================================== K6
-// One thread per (new particle j, aircraft i): find the ancestor by bisection
-// of the integer CDF, copy its control row (from x' or x* per its survivor
-// flag: no survivor copy is made), and write the Gaussian proposal.
-__global__ void k_gather_propose(const ProposeArgs p) {
-    const size_t total = (size_t)p.L * p.n;
+// A block owns kRowsPerBlock rows (new particle j, aircraft i).  Phase 1: one
+// thread per row finds the ancestor by bisection of the integer CDF and the
+// buffer (x' or x*) that holds the ancestor's survivor row (no survivor copy
+// is made).  Phase 2: one thread per (row, step) copies the parent's control
+// triple and writes the Gaussian proposal -- consecutive threads write
+// consecutive 12-byte triples, so both output streams are coalesced.
+constexpr int kRowsPerBlock = 64;
+
+__global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
+    __shared__ const float *s_src[kRowsPerBlock];
+    const size_t rows = (size_t)p.L * p.n;
     const uint32_t mpc = *p.mpcp;
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx % p.n);
-        const uint32_t j = (uint32_t)(idx / p.n);
-        int32_t a;
-        if (p.anc) {
-            a = __ldg(&p.anc[(size_t)i * p.L + j]);
-        } else {
-            const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
-            a = find_ancestor(p.C + (size_t)i * p.L, p.L, Q, R, j);
+    const int H = p.H;
+    for (size_t q0 = (size_t)blockIdx.x * kRowsPerBlock; q0 < rows; q0 += (size_t)gridDim.x * kRowsPerBlock) {
+        if (threadIdx.x < kRowsPerBlock) {
+            const size_t q = q0 + threadIdx.x;
+            const float *src = nullptr;
+            if (q < rows) {
+                const int i = (int)(q % p.n);
+                const uint32_t j = (uint32_t)(q / p.n);
+                int32_t a;
+                if (p.anc) {
+                    a = __ldg(&p.anc[(size_t)i * p.L + j]);
+                } else {
+                    const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
+                    a = find_ancestor(p.C + (size_t)i * p.L, p.L, Q, R, j);
+                }
+                src = p.src[__ldg(&p.surv[a])] + ((size_t)a * p.n + i) * H * 3;
+            }
+            s_src[threadIdx.x] = src;
         }
-        const float *src = p.src[__ldg(&p.surv[a])] + ((size_t)a * p.n + i) * p.H * 3;
-        float *dp = p.xp + idx * p.H * 3;
-        float *ds = p.xs + idx * p.H * 3;
-        const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
-        for (int t = 0; t < p.H; ++t) {
-            const float c0 = src[3 * t], c1 = src[3 * t + 1], c2 = src[3 * t + 2];
-            dp[3 * t] = c0; dp[3 * t + 1] = c1; dp[3 * t + 2] = c2;
+        __syncthreads();
+        const size_t nrow = min((size_t)kRowsPerBlock, rows - q0);
+        for (int e = threadIdx.x; e < (int)(nrow * H); e += blockDim.x) {
+            const int r = e / H, t = e - r * H;
+            const size_t q = q0 + r;
+            const int i = (int)(q % p.n);
+            const uint32_t j = (uint32_t)(q / p.n);
+            const float *src = s_src[r] + 3 * t;
+            const float c0 = src[0], c1 = src[1], c2 = src[2];
+            const size_t o = (q * H + t) * 3;
+            p.xp[o] = c0; p.xp[o + 1] = c1; p.xp[o + 2] = c2;
             const uint4 w = draw(TAG_PERTURB, p.l0 + j, p.k << 16, (uint32_t)t | ((uint32_t)i << 8), mpc, p.key0, p.key1);
             const float2 z01 = box_muller(w.x, w.y);
             const float2 z23 = box_muller(w.z, w.w);
             float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
             if (p.clamp) {
+                const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
                 o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
                 o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
                 o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
             }
-            ds[3 * t] = o0; ds[3 * t + 1] = o1; ds[3 * t + 2] = o2;
+            p.xs[o] = o0; p.xs[o + 1] = o1; p.xs[o + 2] = o2;
         }
+        __syncthreads();
     }
     reset_round_state(p);
 }
 
 cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st) {
-    const size_t total = (size_t)p.L * p.n;
-    if (!total) return cudaSuccess;
-    size_t g = (total + 127) / 128;
-    if (g > 148 * 32) g = 148 * 32;
-    k_gather_propose<<<(unsigned)g, 128, 0, st>>>(p);
+    const size_t rows = (size_t)p.L * p.n;
+    if (!rows) return cudaSuccess;
+    size_t g = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
+    if (g > 148 * 16) g = 148 * 16;
+    k_gather_propose<<<(unsigned)g, 256, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -52,7 +52,8 @@ struct ResampleArgs {
     uint32_t L;                 // particles (local == global when single GPU)
     uint32_t k, key0, key1;
     const uint32_t *mpcp;
-    const float *ell;           // [n][L]
+    const float *ell;           // [n][ell_stride]
+    uint32_t ell_stride;        // row stride of ell (0 = L)
     const uint32_t *colmax;     // [n] ordered max
     unsigned long long *Q;      // [n] totals (nullable)
     double *ess;                // [2n] sum w, sum w^2 (diagnostic)
@@ -64,6 +65,7 @@ struct ResampleArgs {
     int32_t *anc;               // [n][L] (k_ancestors only)
 };
 int scan_tiles(uint32_t L);
+int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);

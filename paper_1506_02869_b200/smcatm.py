@@ -74,7 +74,8 @@ class Config(C.Structure):
         ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("stream", C.c_void_p), ("max_aircraft", C.c_uint32), ("max_horizon", C.c_uint32),
-        ("use_graph", C.c_uint32), ("profile", C.c_uint32),
+        ("use_graph", C.c_uint32), ("profile", C.c_uint32), ("virtual_world", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -185,7 +186,8 @@ class Solver:
     def __init__(self, scn: dict, L: int, S: int, K: int, sigma, seed: int, anneal: float = 0.98,
                  mh: bool = True, sched_paper: bool = False, clamp: bool = False, device: int = 0,
                  max_aircraft: int | None = None, max_horizon: int | None = None, stream=None,
-                 rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False):
+                 rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False,
+                 virtual_world: int = 0):
         import torch
         self.lib = load()
         self.torch = torch
@@ -203,6 +205,7 @@ class Solver:
         cfg.max_horizon = int(max_horizon or scn["H"])
         cfg.use_graph = int(use_graph)
         cfg.profile = int(profile)
+        cfg.virtual_world = int(virtual_world)
         cfg.stream = C.c_void_p(self.stream.cuda_stream)
         if world_size > 1:
             # rank 0 creates the NCCL id; torch.distributed (any backend) shares it
