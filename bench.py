@@ -246,6 +246,7 @@ def main():
         if args.e2e_steps > 0:
             sol.mpc_step_ptr(meas.data_ptr(), applied.data_ptr(), nxt.data_ptr(), flags.data_ptr())   # warm
         barrier()
+        sol.io_bytes()                                      # reset the library's copy counters
         for s in range(args.e2e_steps):
             flush.fill_(s & 0xFF)
             torch.cuda.synchronize()
@@ -256,12 +257,15 @@ def main():
             b.synchronize()
             e2e_ms.append(a.elapsed_time(b))
         sol.phase_times()
+        io_h2d, io_d2h = sol.io_bytes()
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = ac_steps * args.e2e_steps / (float(e2e_t.item()) / 1000.0) if e2e_ms else None
-    h2d = n * 6 * 8 + n * 156      # measured states + per-aircraft constants re-upload
-    d2h = n * 6 * 8 + n * 3 * 4 + n * 4 + 8
+    # bytes the library copied per e2e step (counted in libsmcatm: measured states, per-aircraft
+    # constants, MPC index up; winner index, next states, applied controls, flags down)
+    h2d = io_h2d // max(1, args.e2e_steps)
+    d2h = io_d2h // max(1, args.e2e_steps)
 
     if rank != 0:
         if world > 1:

@@ -209,6 +209,10 @@ smc_status smc_nccl_unique_id(void *out128);
 /* Number of kernel launches the library issued since smc_init. */
 uint64_t smc_launch_count(const smc_ctx *ctx);
 
+/* Host->device and device->host bytes the production entry points copied since
+ * the last call (debug hooks excluded); resets the counters. */
+void smc_io_bytes(smc_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes);
+
 /* ---------------- parity / test hooks (stream-synchronising) -------------- */
 
 /* Roll out caller-given controls (host [L][N][H][3], particle l = global

@@ -191,6 +191,7 @@ struct smc_ctx {
     bool mpc_dirty = true;
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
+    uint64_t io_h2d = 0, io_d2h = 0;   // host<->device bytes of the production path
     int layout = 0;                    // K2 layout: 0 lane-per-aircraft segments, 1 transposed (warp = aircraft)
     int layout_env = -1;               // SMC_K2_LAYOUT override (-1: automatic)
     bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
@@ -241,6 +242,15 @@ static smc_status fail(smc_ctx *c, smc_status s, const char *fmt, ...) {
     va_end(ap);
     if (c) c->err = buf;
     return s;
+}
+
+static cudaError_t h2d(smc_ctx *c, void *dst, const void *src, size_t bytes) {
+    c->io_h2d += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st);
+}
+static cudaError_t d2h(smc_ctx *c, void *dst, const void *src, size_t bytes) {
+    c->io_d2h += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st);
 }
 
 #define CK(expr)                                                                                   \
@@ -428,6 +438,12 @@ extern "C" smc_status smc_nccl_unique_id(void *out128) {
 extern "C" void smc_destroy(smc_ctx *ctx) { delete ctx; }
 extern "C" const char *smc_last_error(const smc_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 extern "C" uint64_t smc_launch_count(const smc_ctx *ctx) { return ctx ? ctx->launches : 0; }
+extern "C" void smc_io_bytes(smc_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
+    if (!ctx) return;
+    if (h2d_bytes) *h2d_bytes = ctx->io_h2d;
+    if (d2h_bytes) *d2h_bytes = ctx->io_d2h;
+    ctx->io_h2d = ctx->io_d2h = 0;
+}
 extern "C" uint32_t smc_get_mpc_index(const smc_ctx *ctx) { return ctx ? ctx->mpc : 0; }
 extern "C" smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t m) {
     if (!ctx) return SMC_EINVAL;
@@ -442,7 +458,7 @@ extern "C" smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t m) {
 static smc_status sync_mpc(smc_ctx *ctx) {
     if (!ctx->mpc_dirty) return SMC_OK;
     ctx->mpc_stage = ctx->mpc;
-    CK(cudaMemcpyAsync(ctx->mpc_dev, &ctx->mpc_stage, sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->st));
+    CK(h2d(ctx, ctx->mpc_dev, &ctx->mpc_stage, sizeof(uint32_t)));
     ctx->mpc_dirty = false;
     return SMC_OK;
 }
@@ -564,13 +580,13 @@ static smc_status build_constants(smc_ctx *ctx) {
         p.v_max[i] = ty.v_max; p.gamma_max[i] = ty.gamma_max; p.phi_max[i] = ty.phi_max;
         p.z_min[i] = ty.z_min; p.z_max[i] = ty.z_max;
     }
-    CK(cudaMemcpyAsync(ctx->dac, hac.data(), sizeof(DevAircraft) * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(h2d(ctx, ctx->dac, hac.data(), sizeof(DevAircraft) * n));
     // lohi: stored as [n][3] lo followed by [n][3] hi
     std::vector<float> lo3(3 * n), hi3(3 * n);
     for (int i = 0; i < n; ++i)
         for (int c = 0; c < 3; ++c) { lo3[3 * i + c] = lohi[6 * i + c]; hi3[3 * i + c] = lohi[6 * i + 3 + c]; }
-    CK(cudaMemcpyAsync(ctx->lohi, lo3.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemcpyAsync(ctx->lohi + 3 * ctx->nmax, hi3.data(), sizeof(float) * 3 * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(h2d(ctx, ctx->lohi, lo3.data(), sizeof(float) * 3 * n));
+    CK(h2d(ctx, ctx->lohi + 3 * ctx->nmax, hi3.data(), sizeof(float) * 3 * n));
     CK(cudaStreamSynchronize(ctx->st));   // host staging vectors go out of scope
     return SMC_OK;
 }
@@ -615,7 +631,7 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     smc_status s = build_constants(ctx);
     if (s != SMC_OK) return s;
     if (scn->n_centres) {
-        CK(cudaMemcpyAsync(ctx->centres, scn->centres, sizeof(double) * 3 * scn->n_centres, cudaMemcpyHostToDevice, ctx->st));
+        CK(h2d(ctx, ctx->centres, scn->centres, sizeof(double) * 3 * scn->n_centres));
     }
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
@@ -699,9 +715,9 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         rs.Q = ctx->Q;
         LAUNCHP(PH_RESAMPLE, launch_qsum(rs, ctx->st));
         // read the round's accumulators before K6 zeroes them for the next round
-        CK(cudaMemcpyAsync(cm, ctx->colmax, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CK(cudaMemcpyAsync(ess, ctx->ess, 16 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CK(cudaMemcpyAsync(&acc, ctx->accept, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(d2h(ctx, cm, ctx->colmax, 4 * n));
+        CK(d2h(ctx, ess, ctx->ess, 16 * n));
+        CK(d2h(ctx, &acc, ctx->accept, 8));
         CK(cudaStreamSynchronize(ctx->st));
     }
     if (tail) {
@@ -768,7 +784,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         smc_status s2 = select_best(ctx);
         if (s2 != SMC_OK) return s2;
         double bl;
-        CK(cudaMemcpyAsync(&bl, ctx->best_lam, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(d2h(ctx, &bl, ctx->best_lam, 8));
         CK(cudaStreamSynchronize(ctx->st));
         stats->best_lambda = bl;
         stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / ctx->Lloc : 1.0);
@@ -838,9 +854,9 @@ extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *
     double bl;
     long long bi;
     const int n = ctx->dsc.n, H = ctx->dsc.H;
-    CK(cudaMemcpyAsync(&bl, ctx->best_lam, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaMemcpyAsync(&bi, ctx->best_idx, 8, cudaMemcpyDeviceToHost, ctx->st));
-    if (out) CK(cudaMemcpyAsync(out, ctx->best_row, sizeof(float) * 3 * n * H, cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h(ctx, &bl, ctx->best_lam, 8));
+    CK(d2h(ctx, &bi, ctx->best_idx, 8));
+    if (out) CK(d2h(ctx, out, ctx->best_row, sizeof(float) * 3 * n * H));
     CK(cudaStreamSynchronize(ctx->st));
     if (lambda) *lambda = bl;
     if (particle) *particle = bi;
@@ -918,15 +934,15 @@ extern "C" smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_cont
     for (int i = 0; i < n; ++i) ctx->ac[i].x0 = measured[i];
     smc_status s = build_constants(ctx);
     if (s != SMC_OK) return s;
-    CK(cudaMemcpyAsync(ctx->pstates, measured, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->st));
+    CK(h2d(ctx, ctx->pstates, measured, sizeof(double) * 6 * n));
     s = smc_solve(ctx, 1);
     if (s != SMC_OK) return s;
     long long bi;
     int fl[32];
-    CK(cudaMemcpyAsync(&bi, ctx->best_idx, 8, cudaMemcpyDeviceToHost, ctx->st));
-    if (next) CK(cudaMemcpyAsync(next, ctx->pnext, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, ctx->st));
-    if (applied) CK(cudaMemcpyAsync(applied, ctx->papplied, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaMemcpyAsync(fl, ctx->pflags, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h(ctx, &bi, ctx->best_idx, 8));
+    if (next) CK(d2h(ctx, next, ctx->pnext, sizeof(double) * 6 * n));
+    if (applied) CK(d2h(ctx, applied, ctx->papplied, sizeof(float) * 3 * n));
+    CK(d2h(ctx, fl, ctx->pflags, sizeof(int) * n));
     CK(cudaStreamSynchronize(ctx->st));
     if (flags)
         for (int i = 0; i < n; ++i) flags[i] = (uint32_t)fl[i];

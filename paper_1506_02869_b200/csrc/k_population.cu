@@ -289,7 +289,7 @@ __device__ __forceinline__ void reset_round_state(const ProposeArgs &p) {
 // is made).  Phase 2: one thread per (row, step) copies the parent's control
 // triple and writes the Gaussian proposal -- consecutive threads write
 // consecutive 12-byte triples, so both output streams are coalesced.
-constexpr int kRowsPerBlock = 64;
+constexpr int kRowsPerBlock = 256;   // = blockDim: every thread runs one bisection in phase 1
 
 __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
     __shared__ const float *s_src[kRowsPerBlock];

@@ -111,6 +111,7 @@ def load():
         "smc_get_mpc_index": (u32, [v]),
         "smc_launch_count": (u64, [v]),
         "smc_nccl_unique_id": (st, [v]),
+        "smc_io_bytes": (None, [v, P(u64), P(u64)]),
         "smc_debug_rollout": (st, [v, f32p, u32, u32, u32, u32, f32p, P(C.c_uint8), f32p, f32p,
                                    P(C.c_int32), f32p]),
         "smc_debug_evaluate": (st, [v, f32p, u32, u32, u32, f32p]),
@@ -132,7 +133,7 @@ def load():
 
 EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate", "smc_best_controls",
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
-            "smc_launch_count", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
+            "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
             "smc_shard_offsets", "smc_slot_count"]
 
@@ -255,6 +256,12 @@ class Solver:
     @property
     def launches(self):
         return int(self.lib.smc_launch_count(self.ctx))
+
+    def io_bytes(self):
+        """(h2d, d2h) bytes copied by production calls since the last query."""
+        a, b = C.c_uint64(), C.c_uint64()
+        self.lib.smc_io_bytes(self.ctx, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     @property
     def mpc_index(self):
