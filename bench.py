@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--loop", type=int, default=0,
+                    help="run the rolling-window MPC loop of c3's traffic for this many steps instead")
     return ap.parse_args()
 
 
@@ -178,10 +180,30 @@ def run_reference(args):
     return 0
 
 
+def run_loop(args):
+    """Rolling-window MPC loop over c3-shaped traffic: per-step latency vs
+    number of active aircraft (SURVEY 8(d) c3 'full MPC receding-horizon loop')."""
+    from paper_1506_02869_b200 import mpc_loop, scenarios as sc
+    base, cfg = sc.config(args.config if args.config != 2 else 3)
+    tr = sc.traffic(16, 8, seed=1003, arr_every=2, dep_every=8)
+    recs, done, fuel = mpc_loop.run(base, tr, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
+                                    n_steps=args.loop, max_aircraft=24)
+    lat = [r.latency_ms for r in recs]
+    print(json.dumps({"mode": "mpc_loop", "config": f"{cfg.name} traffic: 16 arrivals / 8 departures, "
+                      f"L={cfg.L}, S={cfg.S}, K={cfg.K}", "steps": len(recs),
+                      "per_step": [{"step": r.step, "window": r.window, "active": r.active,
+                                    "latency_ms": round(r.latency_ms, 2), "infeasible": r.infeasible} for r in recs],
+                      "max_latency_ms": max(lat) if lat else None, "dt_s": float(base["dt"]),
+                      "completed": {str(k): v for k, v in done.items()}}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.loop:
+        return run_loop(args)
     import numpy as np
     import torch
     import torch.distributed as dist

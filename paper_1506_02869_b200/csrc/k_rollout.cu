@@ -144,6 +144,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     }
     __syncthreads();
 
+    // W >= 8: every wind entry a lane owns belongs to node lane & 7 -> keep that Qhat row in registers
+    float qrow[8];
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) qrow[mm] = (W >= 8) ? s_Q[(lane & 7) * 9 + mm] : 0.0f;
+
     float ell[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) ell[c] = args.part ? 0.0f : args.ell0;
@@ -203,7 +208,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const int comp = e >> 3, node = e & 7;
                     const float4 z0 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8]);
                     const float4 z1 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8 + 4]);
-                    const float *qr = &s_Q[node * 9];
+                    const float *qr = (W >= 8) ? qrow : &s_Q[node * 9];
                     float acc = qr[0] * z0.x;
                     acc = fmaf(qr[1], z0.y, acc); acc = fmaf(qr[2], z0.z, acc); acc = fmaf(qr[3], z0.w, acc);
                     acc = fmaf(qr[4], z1.x, acc); acc = fmaf(qr[5], z1.y, acc); acc = fmaf(qr[6], z1.z, acc);
@@ -298,15 +303,21 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             for (int c = 0; c < NC; ++c) conf[c] = false;
 #pragma unroll
             for (int d = 1; d <= W / 2; ++d) {
+                int hits = 0;
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const float4 q = s_pos[c * kBlock + seg * W + ((lane + d) & (W - 1))];
                     const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
                     const bool hit = fly[c] && (q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) &&
                                      (fabsf(dz) < sc.twoPh);
-                    // all lanes must reach the shuffle: no short-circuit around it
-                    const int back = (2 * d < W) ? __shfl_sync(0xffffffffu, hit ? 1 : 0, (lane - d) & (W - 1), W) : 0;
-                    conf[c] = conf[c] | hit | (back != 0);
+                    conf[c] = conf[c] | hit;
+                    hits |= (hit ? 1 : 0) << c;
+                }
+                // one shuffle hands both candidates' verdicts to the partner (every lane reaches it)
+                if (2 * d < W) {
+                    const int back = __shfl_sync(0xffffffffu, hits, (lane - d) & (W - 1), W);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) conf[c] = conf[c] | ((back >> c) & 1);
                 }
             }
             // ---------------- 5. per-step cost terms at j = t+1, state update

@@ -380,3 +380,11 @@ def test_virtual_ranks_bitexact(smc, num, vw):
     for key in ("cur", "prop", "surv", "ell", "lam"):
         assert np.array_equal(a[key], b[key]), key
     assert np.array_equal(ba[0], bb[0]) and ba[1] == bb[1] and ba[2] == bb[2]
+
+
+@pytest.mark.parametrize("case", ["n12_noise", "n24", "n3_partial"])
+def test_rollout_parity_transposed_layout(smc, case, monkeypatch):
+    """The alternative K2 layout (warp = aircraft; SMC_K2_LAYOUT=transposed)
+    passes the same rollout parity as the default segment layout."""
+    monkeypatch.setenv("SMC_K2_LAYOUT", "transposed")
+    test_rollout_parity(smc, case)
