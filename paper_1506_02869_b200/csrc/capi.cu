@@ -636,10 +636,16 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
-    // K2 layout: lane-per-aircraft segments measured fastest for every config
-    // (c2 43.6 ms vs 58.6 ms, c3 1.44 s vs 1.42-1.55 s, c4 167 ms vs 171 ms per
-    // MPC step); the transposed layout stays available via SMC_K2_LAYOUT
-    ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : 0;
+    // K2 layout.  Measured cost: segment layout ~ proportional to the padded width
+    // W = next_pow2(N) (c3, W = 32: 1.44 s; c2, W = 8: 43.6 ms per MPC step), transposed
+    // layout ~ proportional to N with a higher per-aircraft cost (c3: 1.42 s; c4 N = 12:
+    // 171 vs 167 ms; c2: 58.6 ms).  Break-even near N = 0.75 W, so the transposed layout
+    // is used when at most ~70 % of the segment's lanes would carry an aircraft
+    // (rolling-window MPC steps with, e.g., 17-22 aircraft).  SMC_K2_LAYOUT overrides.
+    {
+        const int W = segment_width((int)n);
+        ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : (10 * (int)n < 7 * W ? 1 : 0);
+    }
     ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1);
     ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2);
     ctx->have_scn = true;
