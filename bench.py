@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--lfinal", type=int, default=0,
+                    help="shrink the population linearly to this many particles by the last round (P:1225)")
     ap.add_argument("--loop", type=int, default=0,
                     help="run the rolling-window MPC loop of c3's traffic for this many steps instead")
     return ap.parse_args()
@@ -222,9 +224,9 @@ def main():
     L_glob = cfg.L * world
     sol = smcatm.Solver(scn, L=L_glob, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
                         anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True,
-                        use_graph=not args.no_graph, rank=rank, world_size=world)
+                        use_graph=not args.no_graph, rank=rank, world_size=world, L_final=args.lfinal)
     S_list = [cfg.S] * cfg.K
-    ac_steps = roofline.aircraft_steps(scn, L_glob, S_list, cfg.mh)
+    ac_steps = roofline.aircraft_steps(scn, L_glob, S_list, cfg.mh, args.lfinal)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def barrier():
@@ -301,7 +303,8 @@ def main():
     ops_k2 = 0.0
     for k, S in enumerate(S_list):
         C = 1 if (k == 0 or not cfg.mh) else 2
-        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * (L_glob // world) * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
+        Lk = roofline.particles_of(L_glob // world, args.lfinal, cfg.K, k)
+        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * Lk * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
     ops_k2 *= args.steps
     achieved = ops_k2 / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
     peak = roofline.peak_alu_ops(float(peaks.get("sm_max_mhz", 1965.0)))
@@ -311,7 +314,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
-                               f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
+                               f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
+                               + (f"->{args.lfinal}" if args.lfinal else "")
+                               + f", S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
                    "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
                                    "all-gathers per round)" if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",

@@ -126,7 +126,9 @@ typedef struct {
                                   selection path -- per-shard CDFs, survivor exchange layout,
                                   shard-aware gather, record merge -- for this many virtual
                                   ranks on one GPU; results are bit-identical to 1 / 0 */
-    uint32_t reserved;
+    uint32_t n_particles_final;/* particle count of the last round, decreasing linearly
+                                  L_k = L - (L - L_final) k / (K - 1) (integer);
+                                  0 = constant L.  Single-rank contexts only. */
 } smc_config;
 
 /* Per-round diagnostics (smc_iterate). */
@@ -234,9 +236,10 @@ smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_p
                         uint32_t k, uint8_t *acc);
 
 /* Per-aircraft systematic resampling (R25) of injected log2 weights
- * ell[N][L] (host float) with the production kernels -> anc[N][L] (host
- * int32).  Q[N] (nullable) receives the integer weight totals. */
-smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t k,
+ * ell[N][L] (host float) into M new particles (M = 0 means L) with the
+ * production kernels -> anc[N][M] (host int32).  Q[N] (nullable) receives the
+ * integer weight totals. */
+smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t M, uint32_t k,
                               int32_t *anc, uint64_t *Q);
 
 /* Gather + propose (Alg.1 l.22-23) on injected survivors: surv_ctrl [L][N][H][3]
@@ -245,13 +248,15 @@ smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32
 smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, const int32_t *anc, uint32_t L,
                              uint32_t k, float *xp, float *xs);
 
-/* Device population after the last call: ctrl_cur / ctrl_prop [L][N][H][3]
- * of the last evaluated pair, surv[L] (0 = resampled kept, 1 = proposal
- * accepted), ell_surv[N][L], lam_surv[L], lam_cand[2][L] (joint log2 weight
- * of both MH candidates as the kernel computed them; round 0 / mh=0: only
- * [0] is meaningful).  Any pointer may be NULL. */
+/* Device population after the last call, packed for the Lk particles the
+ * last round evaluated (Lk = L unless n_particles_final shrinks it; written
+ * to *n_eval, nullable; buffers are sized for L): ctrl_cur / ctrl_prop
+ * [Lk][N][H][3] of the last evaluated pair, surv[Lk] (0 = resampled kept,
+ * 1 = proposal accepted), ell_surv[N][Lk], lam_surv[Lk], lam_cand[2][Lk]
+ * (joint log2 weight of both MH candidates as the kernel computed them;
+ * round 0 / mh=0: only [0] is meaningful).  Any pointer may be NULL. */
 smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
-                                float *ell_surv, double *lam_surv, double *lam_cand);
+                                float *ell_surv, double *lam_surv, double *lam_cand, uint32_t *n_eval);
 
 /* ---------------- multi-GPU partition helpers (pure host, no GPU) ---------- */
 

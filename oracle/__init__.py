@@ -91,7 +91,7 @@ class _SmcCfg(C.Structure):
     _fields_ = [("L", C.c_uint32), ("S", C.c_uint32), ("K", C.c_uint32),
                 ("sched_paper", C.c_uint32), ("mh", C.c_uint32), ("clamp", C.c_uint32),
                 ("sigma", C.c_double * 3), ("anneal", C.c_double), ("seed", C.c_uint64),
-                ("mpc", C.c_uint32), ("nthreads", C.c_int)]
+                ("mpc", C.c_uint32), ("nthreads", C.c_int), ("L_final", C.c_uint32)]
 
 
 def _declare(L):
@@ -125,6 +125,8 @@ def _declare(L):
         "ora_init_population": (None, [P(_Problem), u32, u64, u32, _dp]),
         "ora_mh_accept": (C.c_int, [d, d, u32, u32, u64, u32]),
         "ora_resample_column": (C.c_int, [_dp, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
+        "ora_resample_column_m": (C.c_int, [_dp, u32, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
+        "ora_particles_of": (u32, [u32, u32, u32, u32]),
         "ora_perturb_row": (None, [P(_Problem), C.c_int, _dp, _dp, u32, u32, u64, u32, _dp, C.c_int]),
         "ora_select": (i64, [_dp, u32]),
         "ora_run_smc": (C.c_int, [P(_Problem), P(_SmcCfg), _dp, _dp, P(i64), _dp]),
@@ -286,13 +288,14 @@ class Problem:
         return out
 
     def run_smc(self, L, S, K, seed, sigma, anneal=0.98, mh=True, sched_paper=False, clamp=False,
-                mpc=0, nthreads=0):
+                mpc=0, nthreads=0, L_final=0):
         cfg = _SmcCfg()
         cfg.L, cfg.S, cfg.K = L, S, K
         cfg.sched_paper, cfg.mh, cfg.clamp = int(sched_paper), int(mh), int(clamp)
         cfg.sigma[:] = [float(v) for v in sigma]
         cfg.anneal, cfg.seed, cfg.mpc = float(anneal), int(seed), int(mpc)
         cfg.nthreads = nthreads or (os.cpu_count() or 1)
+        cfg.L_final = int(L_final)
         best = np.zeros((self.n, self.H, 3))
         lam = np.zeros(1)
         idx = C.c_int64(-1)
@@ -373,15 +376,21 @@ def mh_accept(lam_cur, lam_prop, l, k, seed, mpc=0):
     return bool(lib().ora_mh_accept(float(lam_cur), float(lam_prop), l, k, seed, mpc))
 
 
-def resample_column(ell, i, k, seed, mpc=0):
+def resample_column(ell, i, k, seed, mpc=0, M=None):
     ell = _f64(ell, (-1,))
     L = ell.shape[0]
-    anc = np.zeros(L, np.int32)
+    M = L if M is None else int(M)
+    anc = np.zeros(max(M, 1), np.int32)
     q = np.zeros(L, np.uint64)
     Q, R = C.c_uint64(), C.c_uint64()
-    inf = lib().ora_resample_column(_ptr(ell), L, i, k, seed, mpc, _ptr(anc, C.c_int32),
-                                    q.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(Q), C.byref(R))
+    inf = lib().ora_resample_column_m(_ptr(ell), L, M, i, k, seed, mpc, _ptr(anc, C.c_int32),
+                                      q.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(Q), C.byref(R))
+    anc = anc[:M]
     return {"anc": anc, "q": q, "Q": Q.value, "R": R.value, "infeasible": bool(inf)}
+
+
+def particles_of(L, L_final, K, k):
+    return int(lib().ora_particles_of(int(L), int(L_final), int(K), int(k)))
 
 
 def select(lam):

@@ -592,11 +592,12 @@ int ora_mh_accept(double lam_cur, double lam_prop, uint32_t l, uint32_t k, uint6
     return u53 < ora_det_exp2(delta);
 }
 
-/* Systematic resampling of one aircraft column (K96; R25):
- * slot j takes min{ l : C_l > floor((j Q + R) / L) }. */
-int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
-                        uint64_t seed, uint32_t mpc, int32_t *anc,
-                        uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out)
+/* Systematic resampling of one aircraft column (K96; R25) into M
+ * new particles: slot j in [0, M) takes min{ l : C_l > floor((j Q + R) / M) }
+ * (M = L normally; M < L when the particle count shrinks over rounds). */
+int ora_resample_column_m(const double *ell, uint32_t L, uint32_t M, uint32_t i, uint32_t k,
+                          uint64_t seed, uint32_t mpc, int32_t *anc,
+                          uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out)
 {
     double m = -INFINITY;
     for (uint32_t l = 0; l < L; ++l) if (ell[l] > m) m = ell[l];
@@ -612,9 +613,9 @@ int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
     uint64_t Q = acc;
     uint64_t r = ora_r64(TAG_RESAMPLE, i, k, seed, mpc);
     uint64_t R = (uint64_t)(((unsigned __int128)r * (unsigned __int128)Q) >> 64);
-    for (uint32_t j = 0; j < L; ++j) {
+    for (uint32_t j = 0; j < M; ++j) {
         unsigned __int128 num = (unsigned __int128)j * Q + R;
-        uint64_t tj = (uint64_t)(num / L);
+        uint64_t tj = (uint64_t)(num / M);
         /* plain linear search keeps the definition visible; bisection is equivalent */
         uint32_t lo = 0, hi = L - 1;
         while (lo < hi) {
@@ -627,6 +628,21 @@ int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
     if (R_out) *R_out = R;
     free(C);
     return infeasible;
+}
+
+int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
+                        uint64_t seed, uint32_t mpc, int32_t *anc,
+                        uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out)
+{
+    return ora_resample_column_m(ell, L, L, i, k, seed, mpc, anc, q_out, Q_out, R_out);
+}
+
+/* Particle count of round k (R44): linear from L to L_final over K rounds,
+ * exact integer arithmetic. */
+uint32_t ora_particles_of(uint32_t L, uint32_t L_final, uint32_t K, uint32_t k)
+{
+    if (L_final == 0 || L_final >= L || K < 2) return L;
+    return L - (uint32_t)(((uint64_t)(L - L_final) * k) / (K - 1));
 }
 
 /* Alg.1 l.23: controls + Gaussian white noise, sigma per
@@ -690,26 +706,29 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
     double *lam = (double *)malloc(sizeof(double) * (L + 1));
     double *col = (double *)malloc(sizeof(double) * (L + 1));
     int32_t *anc = (int32_t *)malloc(sizeof(int32_t) * ((size_t)L * n + 1));
-    const double ell0 = -log2((double)L);
 
     ora_init_population(p, L, cfg->seed, cfg->mpc, cur);           /* Alg.1 l.1-5 */
+    uint32_t Lk = L;
     for (uint32_t k = 0; k < cfg->K; ++k) {
         uint32_t S = cfg->sched_paper ? (uint32_t)ora_sample_schedule((int)k) : cfg->S;
+        Lk = ora_particles_of(L, cfg->L_final, cfg->K, k);
+        const uint32_t Ln = ora_particles_of(L, cfg->L_final, cfg->K, k + 1);
+        const double ell0 = -log2((double)Lk);
         uint64_t accepted = 0;
         if (k == 0) {
-            for (size_t e = 0; e < L * (size_t)n; ++e) ell_s[e] = ell0;
-            ora_evaluate(p, &d, cur, L, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
-            memcpy(surv, cur, sizeof(double) * L * row);
+            for (size_t e = 0; e < Lk * (size_t)n; ++e) ell_s[e] = ell0;
+            ora_evaluate(p, &d, cur, Lk, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
+            memcpy(surv, cur, sizeof(double) * Lk * row);
         } else if (!cfg->mh) {                                      /* paper-literal: x* replaces x' */
-            for (size_t e = 0; e < L * (size_t)n; ++e) ell_s[e] = ell0;
-            ora_evaluate(p, &d, prop, L, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
-            memcpy(surv, prop, sizeof(double) * L * row);
-            accepted = L;
+            for (size_t e = 0; e < Lk * (size_t)n; ++e) ell_s[e] = ell0;
+            ora_evaluate(p, &d, prop, Lk, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
+            memcpy(surv, prop, sizeof(double) * Lk * row);
+            accepted = Lk;
         } else {
-            for (size_t e = 0; e < L * (size_t)n; ++e) { ell_c[e] = ell0; ell_p[e] = ell0; }
-            ora_evaluate(p, &d, cur, L, S, k, cfg->seed, cfg->mpc, ell_c, cfg->nthreads);
-            ora_evaluate(p, &d, prop, L, S, k, cfg->seed, cfg->mpc, ell_p, cfg->nthreads);
-            for (uint32_t l = 0; l < L; ++l) {
+            for (size_t e = 0; e < Lk * (size_t)n; ++e) { ell_c[e] = ell0; ell_p[e] = ell0; }
+            ora_evaluate(p, &d, cur, Lk, S, k, cfg->seed, cfg->mpc, ell_c, cfg->nthreads);
+            ora_evaluate(p, &d, prop, Lk, S, k, cfg->seed, cfg->mpc, ell_p, cfg->nthreads);
+            for (uint32_t l = 0; l < Lk; ++l) {
                 double lc = lambda_of(&ell_c[(size_t)l * n], n);
                 double lp = lambda_of(&ell_p[(size_t)l * n], n);
                 int acc = ora_mh_accept(lc, lp, l, k, cfg->seed, cfg->mpc);
@@ -719,21 +738,21 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
                 memcpy(&ell_s[(size_t)l * n], acc ? &ell_p[(size_t)l * n] : &ell_c[(size_t)l * n], sizeof(double) * n);
             }
         }
-        for (uint32_t l = 0; l < L; ++l) lam[l] = lambda_of(&ell_s[(size_t)l * n], n);
+        for (uint32_t l = 0; l < Lk; ++l) lam[l] = lambda_of(&ell_s[(size_t)l * n], n);
         double ess_min = INFINITY;
         int n_inf = 0;
         if (k + 1 < cfg->K) {
             /* Alg.1 l.22: per-aircraft resampling */
             for (int i = 0; i < n; ++i) {
-                for (uint32_t l = 0; l < L; ++l) col[l] = ell_s[(size_t)l * n + i];
-                n_inf += ora_resample_column(col, L, (uint32_t)i, k, cfg->seed, cfg->mpc,
-                                             &anc[(size_t)i * L], NULL, NULL, NULL);
+                for (uint32_t l = 0; l < Lk; ++l) col[l] = ell_s[(size_t)l * n + i];
+                n_inf += ora_resample_column_m(col, Lk, Ln, (uint32_t)i, k, cfg->seed, cfg->mpc,
+                                               &anc[(size_t)i * L], NULL, NULL, NULL);
             }
             /* recombine and perturb (Alg.1 l.23); weights reset happens at evaluation */
             double sig[3];
             double f = pow(cfg->anneal, (double)k);
             for (int c = 0; c < 3; ++c) sig[c] = cfg->sigma[c] * f;
-            for (uint32_t j = 0; j < L; ++j)
+            for (uint32_t j = 0; j < Ln; ++j)
                 for (int i = 0; i < n; ++i) {
                     int32_t a = anc[(size_t)i * L + j];
                     const double *src = &surv[(size_t)a * row + (size_t)i * H * 3];
@@ -745,9 +764,9 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
         }
         for (int i = 0; i < n; ++i) {
             double mx = -INFINITY, s1 = 0.0, s2 = 0.0;
-            for (uint32_t l = 0; l < L; ++l) if (ell_s[(size_t)l * n + i] > mx) mx = ell_s[(size_t)l * n + i];
+            for (uint32_t l = 0; l < Lk; ++l) if (ell_s[(size_t)l * n + i] > mx) mx = ell_s[(size_t)l * n + i];
             if (mx == -INFINITY) { ess_min = 0.0; continue; }
-            for (uint32_t l = 0; l < L; ++l) {
+            for (uint32_t l = 0; l < Lk; ++l) {
                 double w = exp2(ell_s[(size_t)l * n + i] - mx);
                 s1 += w; s2 += w * w;
             }
@@ -755,14 +774,14 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
             if (ess < ess_min) ess_min = ess;
         }
         if (stats) {
-            int64_t b = ora_select(lam, L);
+            int64_t b = ora_select(lam, Lk);
             stats[4 * k + 0] = b >= 0 ? lam[b] : -INFINITY;
-            stats[4 * k + 1] = k == 0 ? 1.0 : (double)accepted / (double)L;
+            stats[4 * k + 1] = k == 0 ? 1.0 : (double)accepted / (double)Lk;
             stats[4 * k + 2] = ess_min;
             stats[4 * k + 3] = (double)n_inf;
         }
     }
-    int64_t b = ora_select(lam, L);                                  /* Alg.1 l.27 */
+    int64_t b = ora_select(lam, Lk);                                 /* Alg.1 l.27 */
     if (best_index) *best_index = b;
     if (best_lambda) *best_lambda = b >= 0 ? lam[b] : -INFINITY;
     if (best_ctrl && b >= 0) memcpy(best_ctrl, &surv[(size_t)b * row], sizeof(double) * row);

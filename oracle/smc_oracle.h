@@ -136,6 +136,11 @@ int ora_resample_column(const double *ell, uint32_t L, uint32_t i, uint32_t k,
                         uint64_t seed, uint32_t mpc, int32_t *anc,
                         uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out);
 
+int ora_resample_column_m(const double *ell, uint32_t L, uint32_t M, uint32_t i, uint32_t k,
+                          uint64_t seed, uint32_t mpc, int32_t *anc,
+                          uint64_t *q_out, uint64_t *Q_out, uint64_t *R_out);
+uint32_t ora_particles_of(uint32_t L, uint32_t L_final, uint32_t K, uint32_t k);
+
 /* Gaussian perturbation of one control row (Alg.1 l.23). */
 void ora_perturb_row(const ora_problem *p, int i, const double *parent_row /*[H][3]*/,
                      double *out_row, uint32_t l, uint32_t k, uint64_t seed, uint32_t mpc,
@@ -152,6 +157,7 @@ typedef struct {
     uint64_t seed;
     uint32_t mpc;
     int nthreads;
+    uint32_t L_final;               /* particle count of the last round (0 = constant L) */
 } ora_smc_cfg;
 
 int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,

@@ -174,6 +174,7 @@ struct smc_ctx {
     float *sel_row = nullptr;
     // multi-GPU
     int world = 1, rank = 0, vworld = 1;
+    uint32_t Lfinal = 0, Leval = 0;     // shrinking populations: final count, last evaluated
     uint32_t Lmax = 0;
     ncclComm_t comm = nullptr;
     unsigned long long *Call = nullptr;
@@ -343,6 +344,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->nmax = (int)cfg->max_aircraft;
     ctx->Hmax = (int)cfg->max_horizon;
     ctx->vworld = (world == 1 && cfg->virtual_world > 1) ? (int)cfg->virtual_world : 1;
+    ctx->Lfinal = (cfg->n_particles_final && cfg->n_particles_final < cfg->n_particles) ? cfg->n_particles_final : 0;
+    if (ctx->Lfinal && (world > 1 || ctx->vworld > 1)) { delete ctx; return SMC_EINVAL; }
     if (ctx->vworld > 8 || ctx->Lg < (uint32_t)ctx->vworld) { delete ctx; return SMC_EINVAL; }
     ctx->lay = layout(max_local(ctx->Lg, world), ctx->nmax, ctx->Hmax, world, ctx->vworld);
     if (!cfg->workspace || cfg->workspace_bytes < ctx->lay.total) {
@@ -655,6 +658,14 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
 // ---------------------------------------------------------------- one SMC round
 static smc_status select_best(smc_ctx *ctx);
 
+// Particle count of round k: linear from L to L_final over the K rounds of a solve.
+static uint32_t particles_of(const smc_ctx *ctx, uint32_t k) {
+    const uint32_t K = ctx->cfg.n_rounds;
+    if (!ctx->Lfinal || K < 2) return ctx->Lloc;
+    if (k >= K) k = K - 1;
+    return ctx->Lloc - (uint32_t)(((uint64_t)(ctx->Lloc - ctx->Lfinal) * k) / (K - 1));
+}
+
 static uint32_t samples_of(const smc_ctx *ctx, uint32_t k) {
     if (ctx->cfg.schedule == SMC_SCHED_PAPER) return (uint32_t)std::floor(3.0 + 5.0 * std::exp(0.05 * (double)k));
     return ctx->cfg.n_samples;
@@ -683,8 +694,9 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     } else {
         NC = 1; ra.ctrl[0] = ctx->ctrl[P][1]; ra.ctrl[1] = nullptr; ra.surv_single = 1;
     }
-    ra.L = ctx->Lloc; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpcp = ctx->mpc_dev;
-    ra.ell0 = (float)(-std::log2((double)ctx->Lg));
+    const uint32_t Lk = particles_of(ctx, k), Ln = particles_of(ctx, k + 1);
+    ra.L = Lk; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpcp = ctx->mpc_dev;
+    ra.ell0 = (float)(-std::log2((double)(ctx->Lfinal ? Lk : ctx->Lg)));
     ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
     ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
     {
@@ -706,10 +718,11 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     LAUNCHP(PH_ROLLOUT, ctx->layout ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
                                      : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
+    ctx->Leval = Lk;
     if (ctx->world > 1)                    // global column maxima (reduce step 1)
         NCK(nccl_api()->AllReduce(ctx->colmax, ctx->colmax, n, ncclUint32_, ncclMax_, ctx->comm, ctx->st));
     ResampleArgs rs{};
-    rs.n = n; rs.L = ctx->Lloc; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
+    rs.n = n; rs.L = Lk; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
     rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
     rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR; rs.Cstride = ctx->world > 1 ? ctx->Lmax : 0;
     uint32_t cm[32];
@@ -731,7 +744,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         rs.Q = nullptr;
         LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
         ProposeArgs pa{};
-        pa.n = n; pa.H = H; pa.L = ctx->Lloc; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
+        pa.n = n; pa.H = H; pa.L = Ln; pa.Lsrc = Lk; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
         pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
@@ -793,7 +806,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         CK(d2h(ctx, &bl, ctx->best_lam, 8));
         CK(cudaStreamSynchronize(ctx->st));
         stats->best_lambda = bl;
-        stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / ctx->Lloc : 1.0);
+        stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / Lk : 1.0);
         double em = INFINITY;
         uint32_t lo = 0, hi = 0;
         for (int i = 0; i < n; ++i) {
@@ -841,7 +854,8 @@ static smc_status select_best(smc_ctx *ctx) {
         LAUNCH(launch_select_merge(ctx->rec_all, ctx->vworld, ctx->rec_bytes, rowlen, ctx->rec_final, ctx->st));
         return SMC_OK;
     }
-    SelectArgs sa{ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv, {ctx->ctrl[P][0], ctx->ctrl[P][1]},
+    SelectArgs sa{ctx->Leval ? ctx->Leval : ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv,
+                  {ctx->ctrl[P][0], ctx->ctrl[P][1]},
                   ctx->part_lam, ctx->part_idx, ctx->done, ctx->sel_lam, ctx->sel_idx, ctx->sel_row};
     LAUNCH(launch_select(sa, ctx->st));
     if (ctx->world > 1) {                 // all-gather the per-rank records, merge on every rank
@@ -1079,9 +1093,10 @@ extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const do
     return SMC_OK;
 }
 
-extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t k,
-                                         int32_t *anc, uint64_t *Q) {
+extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t M,
+                                         uint32_t k, int32_t *anc, uint64_t *Q) {
     if (!ctx || !ell || !anc || N == 0 || N > 32 || L == 0 || L >= (1u << 30)) return SMC_EINVAL;
+    if (M == 0) M = L;
     smc_status s0 = sync_mpc(ctx);
     if (s0 != SMC_OK) return s0;
     DevTmp tmp;
@@ -1094,7 +1109,7 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     double *dess = tmp.alloc<double>(2 * N);
     unsigned long long *st1 = tmp.alloc<unsigned long long>((size_t)N * nt);
     uint32_t *tiles = tmp.alloc<uint32_t>(2 * N);
-    int32_t *danc = tmp.alloc<int32_t>((size_t)N * L);
+    int32_t *danc = tmp.alloc<int32_t>((size_t)N * M);
     if (!dell || !dcm || !dQ || !dQR || !dC || !dess || !st1 || !tiles || !danc)
         return fail(ctx, SMC_ECUDA, "debug allocation failed");
     CK(cudaMemcpyAsync(dell, ell, sizeof(float) * N * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
@@ -1107,10 +1122,10 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     rs.n = (int)N; rs.L = L; rs.k = k; rs.mpcp = ctx->mpc_dev;
     rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
     rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
-    rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc;
+    rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M;
     LAUNCH(launch_scan(rs, ctx->st));
     LAUNCH(launch_ancestors(rs, ctx->st));
-    CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * L, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * M, cudaMemcpyDeviceToHost, ctx->st));
     if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return SMC_OK;
@@ -1133,7 +1148,7 @@ extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, co
     ProposeArgs pa{};
     smc_status s0 = sync_mpc(ctx);
     if (s0 != SMC_OK) return s0;
-    pa.n = n; pa.H = H; pa.L = L; pa.l0 = 0; pa.k = k; pa.mpcp = ctx->mpc_dev;
+    pa.n = n; pa.H = H; pa.L = L; pa.Lsrc = L; pa.l0 = 0; pa.k = k; pa.mpcp = ctx->mpc_dev;
     pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
     pa.src[0] = src; pa.src[1] = src; pa.surv = dsurv; pa.anc = danc; pa.xp = dxp; pa.xs = dxs;
     const double f = std::pow(ctx->cfg.anneal, (double)k);
@@ -1148,18 +1163,20 @@ extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, co
 }
 
 extern "C" smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
-                                           float *ell_surv, double *lam_surv, double *lam_cand) {
+                                           float *ell_surv, double *lam_surv, double *lam_cand, uint32_t *n_eval) {
     if (!ctx) return SMC_EINVAL;
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
     const int n = ctx->dsc.n, H = ctx->dsc.H;
     const int P = ctx->last_eval >= 0 ? ctx->last_eval : ctx->cur;
-    const size_t nrow = (size_t)ctx->Lloc * n * H * 3;
+    const size_t Lk = (ctx->last_eval >= 0 && ctx->Leval) ? ctx->Leval : ctx->Lloc;
+    const size_t nrow = Lk * n * H * 3;
+    if (n_eval) *n_eval = (uint32_t)Lk;
     if (ctrl_cur) CK(cudaMemcpyAsync(ctrl_cur, ctx->ctrl[P][0], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
     if (ctrl_prop) CK(cudaMemcpyAsync(ctrl_prop, ctx->ctrl[P][1], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
-    if (surv) CK(cudaMemcpyAsync(surv, ctx->surv, ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
-    if (ell_surv) CK(cudaMemcpyAsync(ell_surv, ctx->ell, sizeof(float) * n * (size_t)ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
-    if (lam_surv) CK(cudaMemcpyAsync(lam_surv, ctx->lam, sizeof(double) * ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
-    if (lam_cand) CK(cudaMemcpyAsync(lam_cand, ctx->lam2, 2 * sizeof(double) * ctx->Lloc, cudaMemcpyDeviceToHost, ctx->st));
+    if (surv) CK(cudaMemcpyAsync(surv, ctx->surv, Lk, cudaMemcpyDeviceToHost, ctx->st));
+    if (ell_surv) CK(cudaMemcpyAsync(ell_surv, ctx->ell, sizeof(float) * n * Lk, cudaMemcpyDeviceToHost, ctx->st));
+    if (lam_surv) CK(cudaMemcpyAsync(lam_surv, ctx->lam, sizeof(double) * Lk, cudaMemcpyDeviceToHost, ctx->st));
+    if (lam_cand) CK(cudaMemcpyAsync(lam_cand, ctx->lam2, 2 * sizeof(double) * Lk, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return SMC_OK;
 }

@@ -247,9 +247,10 @@ cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
 }
 
 // Systematic slot j takes min{ l : C_l > t_j }, t_j = floor((j Q + R) / L) (R25).
-__device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, uint32_t L, uint64_t Q, uint64_t R,
-                                                 uint32_t j) {
-    const uint64_t tj = slot_t(j, Q / L, Q % L, R, L);
+// M new particles drawn from L (M = L unless the population shrinks).
+__device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, uint32_t L, uint32_t M, uint64_t Q,
+                                                 uint64_t R, uint32_t j) {
+    const uint64_t tj = slot_t(j, Q / M, Q % M, R, M);
     uint32_t lo = 0, hi = L - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -261,12 +262,12 @@ __device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, ui
 __global__ void k_ancestors(const ResampleArgs r) {
     const int i = blockIdx.y;
     const uint64_t Q = r.QR[2 * i], R = r.QR[2 * i + 1];
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < r.L; j += gridDim.x * blockDim.x)
-        r.anc[(size_t)i * r.L + j] = find_ancestor(r.C + (size_t)i * r.L, r.L, Q, R, j);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < r.M; j += gridDim.x * blockDim.x)
+        r.anc[(size_t)i * r.M + j] = find_ancestor(r.C + (size_t)i * r.L, r.L, r.M, Q, R, j);
 }
 
 cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
-    unsigned gx = (r.L + 255) / 256;
+    unsigned gx = (r.M + 255) / 256;
     if (gx > 1024) gx = 1024;
     k_ancestors<<<dim3(gx, r.n), 256, 0, st>>>(r);
     return cudaGetLastError();
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
                     a = __ldg(&p.anc[(size_t)i * p.L + j]);
                 } else {
                     const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
-                    a = find_ancestor(p.C + (size_t)i * p.L, p.L, Q, R, j);
+                    a = find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
                 }
                 src = p.src[__ldg(&p.surv[a])] + ((size_t)a * p.n + i) * H * 3;
             }

@@ -62,7 +62,8 @@ struct ResampleArgs {
     unsigned long long *C;      // [n][Cstride] inclusive integer CDF
     uint32_t Cstride;           // row stride of C (0 = L)
     unsigned long long *QR;     // [n][2] (Q, R)
-    int32_t *anc;               // [n][L] (k_ancestors only)
+    int32_t *anc;               // [n][M] (k_ancestors only)
+    uint32_t M;                 // new particles drawn (k_ancestors only)
 };
 int scan_tiles(uint32_t L);
 int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
@@ -77,6 +78,7 @@ struct ProposeArgs {
     const uint32_t *mpcp;
     const float *src[2];        // survivor pair: [0] x', [1] x*
     const uint8_t *surv;        // [L] which buffer holds particle l's survivor
+    uint32_t Lsrc;              // particles evaluated this round (CDF length); L = new particles
     const int32_t *anc;         // [n][L] explicit ancestors (debug) or NULL -> bisection of C
     const unsigned long long *C, *QR;
     // per-round accumulators zeroed here for the next round (stream-ordered after K2 and K4)

@@ -54,13 +54,21 @@ def ops_per_aircraft_step(scn: dict, C: int) -> float:
     return per
 
 
-def aircraft_steps(scn: dict, L: int, S_list, mh: bool = True) -> int:
-    """L * C_k * S_k * sum_i H_a,i summed over rounds (C_0 = 1, C_k = 2 with MH)."""
+def particles_of(L: int, L_final: int, K: int, k: int) -> int:
+    """Particle count of round k (smc_config.n_particles_final, include/smcatm.h)."""
+    if not L_final or L_final >= L or K < 2:
+        return L
+    return L - ((L - L_final) * min(k, K - 1)) // (K - 1)
+
+
+def aircraft_steps(scn: dict, L: int, S_list, mh: bool = True, L_final: int = 0) -> int:
+    """L_k * C_k * S_k * sum_i H_a,i summed over rounds (C_0 = 1, C_k = 2 with MH)."""
     Ha = int(sum(int(scn["H"]) - int(e) for e in scn["first_step"]))
     tot = 0
+    K = len(S_list)
     for k, S in enumerate(S_list):
         C = 1 if (k == 0 or not mh) else 2
-        tot += L * C * S * Ha
+        tot += particles_of(L, L_final, K, k) * C * S * Ha
     return tot
 
 

@@ -75,7 +75,7 @@ class Config(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("stream", C.c_void_p), ("max_aircraft", C.c_uint32), ("max_horizon", C.c_uint32),
         ("use_graph", C.c_uint32), ("profile", C.c_uint32), ("virtual_world", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("n_particles_final", C.c_uint32),
     ]
 
 
@@ -116,9 +116,9 @@ def load():
                                    P(C.c_int32), f32p]),
         "smc_debug_evaluate": (st, [v, f32p, u32, u32, u32, f32p]),
         "smc_debug_mh": (st, [v, f64p, f64p, u32, u32, P(C.c_uint8)]),
-        "smc_debug_resample": (st, [v, f32p, u32, u32, u32, P(C.c_int32), P(u64)]),
+        "smc_debug_resample": (st, [v, f32p, u32, u32, u32, u32, P(C.c_int32), P(u64)]),
         "smc_debug_propose": (st, [v, f32p, P(C.c_int32), u32, u32, f32p, f32p]),
-        "smc_debug_population": (st, [v, f32p, f32p, P(C.c_uint8), f32p, f64p, f64p]),
+        "smc_debug_population": (st, [v, f32p, f32p, P(C.c_uint8), f32p, f64p, f64p, P(C.c_uint32)]),
         "smc_shard_range": (None, [u32, C.c_int32, C.c_int32, P(u32), P(u32)]),
         "smc_shard_offsets": (None, [u32, C.c_int32, C.c_int32, P(u64), P(u64), P(u64)]),
         "smc_slot_count": (u64, [u64, u64, u64, u32]),
@@ -188,7 +188,7 @@ class Solver:
                  mh: bool = True, sched_paper: bool = False, clamp: bool = False, device: int = 0,
                  max_aircraft: int | None = None, max_horizon: int | None = None, stream=None,
                  rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False,
-                 virtual_world: int = 0):
+                 virtual_world: int = 0, L_final: int = 0):
         import torch
         self.lib = load()
         self.torch = torch
@@ -207,6 +207,7 @@ class Solver:
         cfg.use_graph = int(use_graph)
         cfg.profile = int(profile)
         cfg.virtual_world = int(virtual_world)
+        cfg.n_particles_final = int(L_final)
         cfg.stream = C.c_void_p(self.stream.cuda_stream)
         if world_size > 1:
             # rank 0 creates the NCCL id; torch.distributed (any backend) shares it
@@ -362,12 +363,13 @@ class Solver:
                                           _p(acc, C.c_uint8)))
         return acc
 
-    def debug_resample(self, ell, k):
+    def debug_resample(self, ell, k, M=None):
         e = np.ascontiguousarray(np.asarray(ell, dtype=np.float32))
         N, L = e.shape
-        anc = np.zeros((N, L), np.int32)
+        M = L if M is None else int(M)
+        anc = np.zeros((N, M), np.int32)
         Q = np.zeros(N, np.uint64)
-        self._check(self.lib.smc_debug_resample(self.ctx, _p(e, C.c_float), N, L, k, _p(anc, C.c_int32),
+        self._check(self.lib.smc_debug_resample(self.ctx, _p(e, C.c_float), N, L, M, k, _p(anc, C.c_int32),
                                                 _p(Q, C.c_uint64)))
         return anc, Q
 
@@ -387,10 +389,14 @@ class Solver:
         ell = np.zeros((n, L), np.float32)
         lam = np.zeros(L, np.float64)
         lam2 = np.zeros((2, L), np.float64)
+        nev = C.c_uint32()
         self._check(self.lib.smc_debug_population(self.ctx, _p(cur, C.c_float), _p(prop, C.c_float),
                                                   _p(surv, C.c_uint8), _p(ell, C.c_float), _p(lam, C.c_double),
-                                                  _p(lam2, C.c_double)))
-        return {"cur": cur, "prop": prop, "surv": surv, "ell": ell, "lam": lam, "lam_cand": lam2}
+                                                  _p(lam2, C.c_double), C.byref(nev)))
+        Lk = nev.value
+        return {"cur": cur[:Lk], "prop": prop[:Lk], "surv": surv[:Lk],
+                "ell": ell.reshape(-1)[:n * Lk].reshape(n, Lk), "lam": lam[:Lk],
+                "lam_cand": lam2.reshape(-1)[:2 * Lk].reshape(2, Lk)}
 
 
 def shard_range(L, world, rank):

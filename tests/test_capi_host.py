@@ -91,3 +91,13 @@ def test_slot_count_exact(lib):
     for C in (0, 1, Q // 2, Q - 1, Q):
         j = smcatm.slot_count(C, Q, R, L)
         assert (j == 0 or ((j - 1) * Q + R) // L < C) and (j == L or (j * Q + R) // L >= C)
+
+
+def test_bench_particle_schedule_matches_oracle():
+    """bench.py counts work with roofline.particles_of; it must be the schedule
+    the oracle (and smc_config.n_particles_final) defines (R44)."""
+    import oracle as O
+    from paper_1506_02869_b200 import roofline
+    for L, Lf, K in ((1000, 400, 4), (16384, 4096, 101), (256, 40, 6), (100, 0, 5), (100, 200, 5), (7, 3, 1)):
+        for k in range(K + 2):
+            assert roofline.particles_of(L, Lf, K, k) == O.particles_of(L, Lf, K, min(k, max(K - 1, 0))), (L, Lf, K, k)

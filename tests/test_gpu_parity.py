@@ -178,6 +178,63 @@ def test_resample_bitexact(smc, L):
             assert np.array_equal(anc[i], r["anc"]), (i, k, np.nonzero(anc[i] != r["anc"])[0][:10])
 
 
+@pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000)])
+def test_resample_to_fewer_bitexact(smc, L, M):
+    """Shrinking populations: M < L slots drawn from L particles."""
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, seed=cfg.seed)
+    rng = np.random.default_rng(L + M)
+    N = 3
+    ell = rng.normal(-25, 8, (N, L)).astype(np.float32)
+    ell[rng.uniform(size=(N, L)) < 0.3] = -np.inf
+    ell[2] = np.float32(-3.5)
+    for k in (0, 7):
+        anc, Q = sol.debug_resample(ell, k, M=M)
+        assert anc.shape == (N, M)
+        for i in range(N):
+            r = O.resample_column(ell[i].astype(np.float64), i, k, cfg.seed, M=M)
+            assert Q[i] == r["Q"], (i, k)
+            assert np.array_equal(anc[i], r["anc"]), (i, k)
+
+
+def test_shrinking_population_rounds(smc):
+    """Real rounds with L_k falling linearly to L_final: population
+    sizes follow the oracle's schedule, each round's ancestors (read back from
+    the next round's x' rows) are the oracle's resampling of the GPU's ell into
+    L_{k+1} slots, and the log-weights match the oracle's evaluation."""
+    scn, cfg = sc.config(1)
+    L, Lf, S, K = 256, 40, 4, 6
+    sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, L_final=Lf)
+    P = O.Problem(scn)
+    n = scn["n"]
+    prev = None
+    for k in range(K):
+        sol.iterate(1)
+        pop = sol.population()
+        Lk = O.particles_of(L, Lf, K, k)
+        assert pop["cur"].shape[0] == Lk and pop["ell"].shape == (n, Lk), (k, Lk)
+        if prev is not None:
+            chosen, ell_prev, kp = prev
+            for i in range(n):
+                r = O.resample_column(ell_prev[i].astype(np.float64), i, kp, cfg.seed, M=Lk)
+                if r["Q"] == 0:
+                    continue
+                assert np.array_equal(pop["cur"][:, i], chosen[r["anc"], i]), (k, i)
+        ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
+        if k > 0:
+            ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
+            ell_o = np.where(pop["surv"][:, None] == 1, ell_p, ell_c)
+        else:
+            ell_o = ell_c
+        ell_g = pop["ell"].T.astype(np.float64)
+        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
+        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
+        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+        chosen = np.where(pop["surv"][:, None, None, None] == 1, pop["prop"], pop["cur"])
+        prev = (chosen, pop["ell"], k)
+    sol.close()
+
+
 def test_propose_parity(smc):
     scn, cfg = sc.config(2)
     L = 500

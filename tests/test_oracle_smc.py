@@ -308,3 +308,40 @@ def test_toy_smc_vs_exhaustive_grid(ora):
     assert res["rc"] == 0
     best_smc = 2.0 ** (res["best_lambda"] + math.log2(1024))
     assert best_smc >= 0.98 * best_grid
+
+
+def _textbook_systematic_m(q, R, Q, M):
+    """Systematic resampling into M slots with offset u = R/Q (exact rationals)."""
+    cdf, acc = [], 0
+    for v in q:
+        acc += v
+        cdf.append(Fraction(acc, Q))
+    return [next(l for l in range(len(q)) if cdf[l] > (j + Fraction(R, Q)) / M) for j in range(M)]
+
+
+def test_resample_to_fewer_particles(ora):
+    """Shrinking populations (P:1225): M < L slots, same systematic definition;
+    counts lie in {floor(M q/Q), ceil(M q/Q)} and sum to M."""
+    rng = np.random.default_rng(12)
+    for trial in range(40):
+        L = int(rng.integers(2, 60))
+        M = int(rng.integers(1, L + 1))
+        ell = rng.uniform(-30, 0, L)
+        ell[rng.uniform(size=L) < 0.2] = -np.inf
+        r = ora.resample_column(ell, i=trial % 4, k=trial, seed=0x99, M=M)
+        q = [int(v) for v in r["q"]]
+        assert r["anc"].tolist() == _textbook_systematic_m(q, r["R"], r["Q"], M)
+        counts = np.bincount(r["anc"], minlength=L)
+        assert counts.sum() == M
+        for l in range(L):
+            e = Fraction(q[l] * M, r["Q"])
+            assert math.floor(e) <= counts[l] <= math.ceil(e)
+
+
+def test_particle_schedule(ora):
+    """Linear particle count from L to L_final over K rounds (integer arithmetic)."""
+    assert [ora.particles_of(1000, 400, 4, k) for k in range(4)] == [1000, 800, 600, 400]
+    assert ora.particles_of(1000, 0, 10, 5) == 1000
+    assert all(ora.particles_of(16384, 4096, 101, k) >= ora.particles_of(16384, 4096, 101, k + 1) for k in range(100))
+    res = ora.Problem(sc.config(1)[0]).run_smc(L=256, S=4, K=6, seed=1, sigma=(6000.0, 0.03, 0.008), L_final=64)
+    assert res["rc"] in (0, 2)
