@@ -128,18 +128,19 @@ def cpu_baseline(scn, cfg, seconds=12.0):
     P = O.Problem(scn)
     nthreads = os.cpu_count() or 1
     Lp = min(cfg.L, 2048)
+    S = cfg.S or 8                                          # paper schedule: S_0 = 8
     ctrl = P.init_population(Lp, cfg.seed)
     Ha = int(sum(scn["H"] - e for e in scn["first_step"]))
     done, t0 = 0, time.perf_counter()
     k = 0
     while True:
-        P.evaluate(ctrl, cfg.S, k + 1, cfg.seed, nthreads=nthreads)
-        done += Lp * cfg.S * Ha
+        P.evaluate(ctrl, S, k + 1, cfg.seed, nthreads=nthreads)
+        done += Lp * S * Ha
         k += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return done / el, nthreads, f"oracle evaluate of {Lp} particles x S={cfg.S} x {Ha} aircraft-steps, {k} reps, {el:.1f}s"
+    return done / el, nthreads, f"oracle evaluate of {Lp} particles x S={S} x {Ha} aircraft-steps, {k} reps, {el:.1f}s"
 
 
 def run_reference(args):
@@ -153,19 +154,20 @@ def run_reference(args):
     P = O.Problem(scn)
     nthreads = os.cpu_count() or 1
     Lp = min(cfg.L, 2048)
+    S = cfg.S or 8
     ctrl = P.init_population(Lp, cfg.seed)
     Ha = int(sum(scn["H"] - e for e in scn["first_step"]))
-    per_step = Lp * cfg.S * Ha
+    per_step = Lp * S * Ha
     for w in range(args.warmup):
-        P.evaluate(ctrl, cfg.S, 1, cfg.seed, nthreads=nthreads)
+        P.evaluate(ctrl, S, 1, cfg.seed, nthreads=nthreads)
     ts = []
     for s in range(args.steps):
         t0 = time.perf_counter()
-        P.evaluate(ctrl, cfg.S, 1 + s, cfg.seed, nthreads=nthreads)
+        P.evaluate(ctrl, S, 1 + s, cfg.seed, nthreads=nthreads)
         ts.append(time.perf_counter() - t0)
     tot = sum(ts)
     value = per_step * args.steps / tot
-    steps_full = roofline.aircraft_steps(scn, cfg.L, [cfg.S] * cfg.K, cfg.mh)
+    steps_full = roofline.aircraft_steps(scn, cfg.L, roofline.samples_list(cfg), cfg.mh)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
@@ -174,7 +176,7 @@ def run_reference(args):
                    "sample": f"one evaluation round of {Lp} particles per step"},
         "mpc_step_latency_ms_extrapolated": 1000 * steps_full / value,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-                         "sample": f"oracle evaluate of {Lp} particles x S={cfg.S} per step"},
+                         "sample": f"oracle evaluate of {Lp} particles x S={S} per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -223,9 +225,10 @@ def main():
     # exchange each round), L = configs' L per GPU -> weak scaling
     L_glob = cfg.L * world
     sol = smcatm.Solver(scn, L=L_glob, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
-                        anneal=cfg.anneal, mh=cfg.mh, device=local, stream=stream, profile=True,
+                        anneal=cfg.anneal, mh=cfg.mh, sched_paper=cfg.sched_paper, device=local, stream=stream,
+                        profile=True,
                         use_graph=not args.no_graph, rank=rank, world_size=world, L_final=args.lfinal)
-    S_list = [cfg.S] * cfg.K
+    S_list = roofline.samples_list(cfg)
     ac_steps = roofline.aircraft_steps(scn, L_glob, S_list, cfg.mh, args.lfinal)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
@@ -309,14 +312,18 @@ def main():
     achieved = ops_k2 / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
     peak = roofline.peak_alu_ops(float(peaks.get("sm_max_mhz", 1965.0)))
     all_ms = sum(v[0] for v in phases.values())
+    # Table 1's workload (config 6) is the one with a printed number: 56 s per MPC update on
+    # a GTX 580, i.e. ac_steps / 56 aircraft-steps/s
+    vs_baseline = value / (ac_steps / 56.0) if (cfg.name == "table1" and world == 1 and not args.lfinal) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": vs_baseline, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
                                f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
                                + (f"->{args.lfinal}" if args.lfinal else "")
-                               + f", S={cfg.S}, H={scn['H']}, K={cfg.K} rounds, MH on",
+                               + (", S_k=floor(3+5e^(0.05k))" if cfg.sched_paper else f", S={cfg.S}")
+                               + f", H={scn['H']}, K={cfg.K} rounds, " + ("MH on" if cfg.mh else "paper Alg.1 (no MH)"),
                    "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
                                    "all-gathers per round)" if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",

@@ -740,7 +740,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         CK(cudaStreamSynchronize(ctx->st));
     }
     if (tail) {
-        const size_t nt = (size_t)scan_tiles(ctx->Lloc);
+        // look-back status words the next round's scan (over Ln particles) will read
+        const size_t nt = (size_t)std::max(scan_tiles(Lk), scan_tiles(Ln));
         rs.Q = nullptr;
         LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
         ProposeArgs pa{};

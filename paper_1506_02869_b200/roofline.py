@@ -15,6 +15,8 @@ bytes per (aircraft, particle) per round are 8 + 36 H.
 """
 from __future__ import annotations
 
+import math
+
 MUFU_W = 8.0          # FP32-lane-op equivalent of one MUFU op
 SMS = 148
 FP32_LANES_PER_SM_CLK = 128
@@ -52,6 +54,15 @@ def ops_per_aircraft_step(scn: dict, C: int) -> float:
     if float(scn["turb_sigma"]) > 0:
         per += (GUST_INT + GUST_FP + MUFU_W * GUST_MUFU) / (2.0 * C)
     return per
+
+
+def sample_schedule(k: int) -> int:
+    """S_k of SMC_SCHED_PAPER: floor(3 + 5 e^{0.05 k}), as the library counts it."""
+    return int(math.floor(3.0 + 5.0 * math.exp(0.05 * k)))
+
+
+def samples_list(cfg) -> list:
+    return [sample_schedule(k) for k in range(cfg.K)] if cfg.sched_paper else [cfg.S] * cfg.K
 
 
 def particles_of(L: int, L_final: int, K: int, k: int) -> int:

@@ -151,6 +151,13 @@ def config(num: int, noise_w: float = 0.1):
     if num == 5:
         scn = snapshot(8, 8, seed)
         return scn, SmcConfig("c5", L=1 << 20, S=64, K=101, sigma=sig, seed=0x5EED0005)
+    if num == 6:
+        # Table 1's timing workload: 10 aircraft all active over the
+        # whole H = 6 horizon, L = 10 240, paper Alg.1 (no MH, S_k = floor(3 + 5 e^{0.05k}),
+        # J_max = 100).  Not a BASELINE.json config: a like-for-like latency line.
+        scn = snapshot(5, 5, seed)
+        return scn, SmcConfig("table1", L=10240, S=0, K=101, sigma=sig, mh=False, sched_paper=True,
+                              seed=0x5EED0006)
     raise ValueError(num)
 
 

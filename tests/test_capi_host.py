@@ -101,3 +101,11 @@ def test_bench_particle_schedule_matches_oracle():
     for L, Lf, K in ((1000, 400, 4), (16384, 4096, 101), (256, 40, 6), (100, 0, 5), (100, 200, 5), (7, 3, 1)):
         for k in range(K + 2):
             assert roofline.particles_of(L, Lf, K, k) == O.particles_of(L, Lf, K, min(k, max(K - 1, 0))), (L, Lf, K, k)
+
+
+def test_bench_sample_schedule_matches_oracle():
+    import oracle as O
+    from paper_1506_02869_b200 import roofline, scenarios as sc
+    assert [roofline.sample_schedule(k) for k in range(101)] == [O.sample_schedule(k) for k in range(101)]
+    _, cfg = sc.config(6)
+    assert sum(roofline.samples_list(cfg)) == 15370

@@ -197,13 +197,13 @@ def test_resample_to_fewer_bitexact(smc, L, M):
             assert np.array_equal(anc[i], r["anc"]), (i, k)
 
 
-def test_shrinking_population_rounds(smc):
+@pytest.mark.parametrize("L,Lf,S,K", [(256, 40, 4, 6), (140000, 60000, 2, 3)])
+def test_shrinking_population_rounds(smc, L, Lf, S, K):
     """Real rounds with L_k falling linearly to L_final: population
     sizes follow the oracle's schedule, each round's ancestors (read back from
     the next round's x' rows) are the oracle's resampling of the GPU's ell into
     L_{k+1} slots, and the log-weights match the oracle's evaluation."""
     scn, cfg = sc.config(1)
-    L, Lf, S, K = 256, 40, 4, 6
     sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, L_final=Lf)
     P = O.Problem(scn)
     n = scn["n"]
