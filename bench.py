@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--traffic", default="c3", choices=["c3", "mixed", "congested"],
+                    help="traffic stream of --loop")
     ap.add_argument("--lfinal", type=int, default=0,
                     help="shrink the population linearly to this many particles by the last round (P:1225)")
     ap.add_argument("--loop", type=int, default=0,
@@ -185,19 +187,29 @@ def run_reference(args):
 
 
 def run_loop(args):
-    """Rolling-window MPC loop over c3-shaped traffic: per-step latency vs
-    number of active aircraft (SURVEY 8(d) c3 'full MPC receding-horizon loop')."""
+    """Rolling-window MPC loop: per-step latency vs number of active aircraft
+    (SURVEY 8(d) c3 'full MPC receding-horizon loop') and the closed-loop audit (N2):
+    landings / exits, realised separation, fuel.  --traffic picks c3's stream (16 arr /
+    8 dep) or the paper's mixed (10 + 10) / congested (24 arrivals) shapes."""
     from paper_1506_02869_b200 import mpc_loop, scenarios as sc
     base, cfg = sc.config(args.config if args.config != 2 else 3)
-    tr = sc.traffic(16, 8, seed=1003, arr_every=2, dep_every=8)
-    recs, done, fuel = mpc_loop.run(base, tr, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
-                                    n_steps=args.loop, max_aircraft=24)
+    if args.traffic == "mixed":
+        tr, desc = sc.paper_mixed(), "paper mixed: 10 arrivals / 10 departures"
+    elif args.traffic == "congested":
+        tr, desc = sc.paper_congested(), "paper congested: 24 arrivals"
+    else:
+        tr, desc = sc.traffic(16, 8, seed=1003, arr_every=2, dep_every=8), "c3 traffic: 16 arrivals / 8 departures"
+    recs, done, fuel, aud = mpc_loop.run(base, tr, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
+                                         n_steps=args.loop, max_aircraft=32, return_audit=True)
     lat = [r.latency_ms for r in recs]
-    print(json.dumps({"mode": "mpc_loop", "config": f"{cfg.name} traffic: 16 arrivals / 8 departures, "
-                      f"L={cfg.L}, S={cfg.S}, K={cfg.K}", "steps": len(recs),
+    print(json.dumps({"mode": "mpc_loop", "config": f"{desc}, {cfg.name} solver: L={cfg.L}, S={cfg.S}, K={cfg.K}",
+                      "steps": len(recs),
                       "per_step": [{"step": r.step, "window": r.window, "active": r.active,
                                     "latency_ms": round(r.latency_ms, 2), "infeasible": r.infeasible} for r in recs],
                       "max_latency_ms": max(lat) if lat else None, "dt_s": float(base["dt"]),
+                      "audit": {"aircraft": aud.n_aircraft, "landed": aud.landed, "exited": aud.exited,
+                                "unfinished": aud.unfinished, "separation_violations": aud.sep_violations,
+                                "min_separation_m": aud.min_sep_m, "fuel_total_kg": aud.fuel_total_kg},
                       "completed": {str(k): v for k, v in done.items()}}), flush=True)
     return 0
 

@@ -123,6 +123,7 @@ def _declare(L):
         "ora_rollout": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, P(_RollOut)]),
         "ora_evaluate": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, _dp, C.c_int]),
         "ora_init_population": (None, [P(_Problem), u32, u64, u32, _dp]),
+        "ora_init_population_warm": (None, [P(_Problem), u32, u64, u32, _dp, _ip, u32, _dp, C.c_int, _dp]),
         "ora_mh_accept": (C.c_int, [d, d, u32, u32, u64, u32]),
         "ora_resample_column": (C.c_int, [_dp, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
         "ora_resample_column_m": (C.c_int, [_dp, u32, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
@@ -278,6 +279,16 @@ class Problem:
     def init_population(self, L, seed, mpc=0):
         out = np.zeros((L, self.n, self.H, 3))
         lib().ora_init_population(C.byref(self.p), L, seed, mpc, _ptr(out))
+        return out
+
+    def init_population_warm(self, L, seed, prev, has_prev, Lw, sigma, mpc=0, clamp=False):
+        """Warm start (R45): prev [n][H][3] previous winner rows mapped to this scenario."""
+        out = np.zeros((L, self.n, self.H, 3))
+        prev = _f64(prev, (self.n, self.H, 3))
+        hp = np.ascontiguousarray(np.asarray(has_prev, dtype=np.int32))
+        sig = _f64(sigma, (3,))
+        lib().ora_init_population_warm(C.byref(self.p), L, seed, mpc, _ptr(prev),
+                                       hp.ctypes.data_as(C.POINTER(C.c_int32)), Lw, _ptr(sig), int(clamp), _ptr(out))
         return out
 
     def perturb_row(self, i, row, l, k, seed, sigma, mpc=0, clamp=False):

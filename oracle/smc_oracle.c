@@ -580,6 +580,50 @@ void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32
             }
 }
 
+/* Warm start across MPC steps (reading R45): the previous
+ * winner, shifted one step (row t <- row t+1, last row repeated), seeds the
+ * first Lw particles of aircraft that were in the previous window; particle 0
+ * takes it exactly, particles 1..Lw-1 add N(0, sigma^2) per component from the
+ * INIT stream with x1 = 1<<16 (two Box-Muller pairs as in the proposal);
+ * clamp as for proposals (R16).  Every other (particle, aircraft) row is the
+ * fresh uniform draw of ora_init_population.
+ * prev: [n][H][3] previous winner rows mapped to the current aircraft index;
+ * has_prev[i] = 0 where aircraft i has none. */
+void ora_init_population_warm(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,
+                              const double *prev, const int32_t *has_prev, uint32_t Lw,
+                              const double sigma[3], int clamp, double *ctrl)
+{
+    const int n = p->n, H = p->H;
+    ora_init_population(p, L, seed, mpc, ctrl);
+    for (uint32_t l = 0; l < L && l < Lw; ++l)
+        for (int i = 0; i < n; ++i) {
+            if (!has_prev[i]) continue;
+            for (int t = 0; t < H; ++t) {
+                const double *base = &prev[((size_t)i * H + (t + 1 < H ? t + 1 : H - 1)) * 3];
+                double *c = &ctrl[(((size_t)l * n + i) * H + t) * 3];
+                if (l == 0) {
+                    c[0] = base[0]; c[1] = base[1]; c[2] = base[2];
+                    continue;
+                }
+                uint32_t w[4];
+                draw(TAG_INIT, l, 1u << 16, (uint32_t)t | ((uint32_t)i << 8), mpc, seed, w);
+                double z[4];
+                ora_box_muller(w[0], w[1], &z[0], &z[1]);
+                ora_box_muller(w[2], w[3], &z[2], &z[3]);
+                for (int q = 0; q < 3; ++q) {
+                    double v = base[q] + sigma[q] * z[q];
+                    if (clamp) {
+                        double lo = q == 0 ? p->T_min[i] : (q == 1 ? -p->phi_max[i] : -p->gamma_max[i]);
+                        double hi = q == 0 ? p->T_max[i] : (q == 1 ? p->phi_max[i] : p->gamma_max[i]);
+                        if (v < lo) v = lo;
+                        if (v > hi) v = hi;
+                    }
+                    c[q] = v;
+                }
+            }
+        }
+}
+
 /* MH accept/reject on the joint log2 weight (R1). */
 int ora_mh_accept(double lam_cur, double lam_prop, uint32_t l, uint32_t k, uint64_t seed, uint32_t mpc)
 {

@@ -126,6 +126,11 @@ void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl
 void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,
                          double *ctrl);
 
+/* Warm start (R45): first Lw particles from the shifted previous winner. */
+void ora_init_population_warm(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,
+                              const double *prev, const int32_t *has_prev, uint32_t Lw,
+                              const double sigma[3], int clamp, double *ctrl);
+
 /* MH accept for particle l in round k (R1). Returns 1 = accept proposal. */
 int ora_mh_accept(double lam_cur, double lam_prop, uint32_t l, uint32_t k,
                   uint64_t seed, uint32_t mpc);

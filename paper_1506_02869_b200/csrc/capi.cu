@@ -527,12 +527,27 @@ static smc_status build_constants(smc_ctx *ctx) {
         return fail(ctx, SMC_EINVAL, "wind covariance not positive definite");
     }
     for (int q = 0; q < 64; ++q) { d.Qhat[q] = (float)Qh[q]; p.Qhat[q] = Qh[q]; }
+    // trilinear basis change (tripoly): coefficient r = sum_n M[r][n] W_n
+    static const int Mtri[8][8] = {{1, 0, 0, 0, 0, 0, 0, 0},   {-1, 1, 0, 0, 0, 0, 0, 0},
+                                   {-1, 0, 1, 0, 0, 0, 0, 0},  {-1, 0, 0, 0, 1, 0, 0, 0},
+                                   {1, -1, -1, 1, 0, 0, 0, 0}, {1, -1, 0, 0, -1, 1, 0, 0},
+                                   {1, 0, -1, 0, -1, 0, 1, 0}, {-1, 1, 1, -1, 1, -1, -1, 1}};
+    for (int r = 0; r < 8; ++r)
+        for (int m = 0; m < 8; ++m) {
+            double acc = 0.0;
+            for (int nn = 0; nn < 8; ++nn) acc += Mtri[r][nn] * Qh[nn * 8 + m];
+            d.Cq[r * 8 + m] = (float)acc;
+        }
     p.a = std::exp(-s.lambda_t * s.dt);
     p.b = std::sqrt(1.0 - p.a * p.a);
     d.a = (float)p.a; d.b = (float)p.b;
     d.nominal[0] = (float)s.nominal[0]; d.nominal[1] = (float)s.nominal[1];
     d.turb_sigma = (float)s.turb_sigma;
     d.key0 = (uint32_t)ctx->cfg.seed; d.key1 = (uint32_t)(ctx->cfg.seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        d.ks[2 * r] = d.key0 + (uint32_t)r * 0x9E3779B9u;
+        d.ks[2 * r + 1] = d.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
     d.ac = ctx->dac;
     d.pop = ctx->pop;
     p.dt = s.dt; p.g = s.g; p.rho_const = s.rho_const; p.density_mode = s.density_mode;

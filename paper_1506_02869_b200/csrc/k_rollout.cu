@@ -7,8 +7,9 @@
 // both candidates see the same wind realisation (common random numbers).
 // Per step t the segment
 //   1. draws the 16 normals of the 2x2x2 wind field (Philox, Box-Muller),
-//      advances the AR(1) state Z and forms W = Qhat Z -- the 16
-//      entries are distributed over the lanes and exchanged via shared memory;
+//      advances the AR(1) state Z and forms W = Qhat Z, directly in
+//      trilinear-coefficient form (Cq = M Qhat, tripoly) -- the 16 entries are
+//      distributed over the lanes and exchanged via shared memory;
 //   2. every lane interpolates W at its aircraft, adds the nominal wind
 //      and gust, and applies Eq. hor to both candidates;
 //   3. checks the envelope / mass and the landing sector
@@ -45,15 +46,6 @@ __device__ __forceinline__ float popdense(const DevScen &sc, float x, float y) {
     const float v01 = __ldg(&sc.pop[iy1 * sc.pop_nx + ix]), v11 = __ldg(&sc.pop[iy1 * sc.pop_nx + ix1]);
     const float a = fmaf(fx, v10 - v00, v00), b = fmaf(fx, v11 - v01, v01);
     return fmaf(fy, b - a, a);
-}
-
-__device__ __forceinline__ float lerp(float a, float b, float t) { return fmaf(t, b - a, a); }
-
-// Trilinear interpolation of one wind component (8 node values).
-__device__ __forceinline__ float trilerp(const float *Wn, float fx, float fy, float fz) {
-    const float a = lerp(Wn[0], Wn[1], fx), b = lerp(Wn[2], Wn[3], fx);
-    const float c = lerp(Wn[4], Wn[5], fx), d = lerp(Wn[6], Wn[7], fx);
-    return lerp(lerp(a, b, fy), lerp(c, d, fy), fz);
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -111,7 +103,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     const bool isac = lane < n;
     const uint32_t k = args.k, mpc = *args.mpcp;
 
-    if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Qhat[tid];
+    if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Cq[tid];   // W = Cq Z: trilinear coefficients
 
     // ---- per-lane aircraft constants needed every step (the rest is read when needed)
     const DevAircraft *Ap = sc.ac + (isac ? lane : 0);
@@ -183,7 +175,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 for (int task = lane; task < 4 * GB; task += W) {
                     const int b = task & 3, ts = t + (task >> 2);
                     if (ts < H) {
-                        const uint4 w = draw(TAG_WIND, l, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.key0, sc.key1);
+                        const uint4 w = draw_ks(TAG_WIND, l, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
                         const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
                         *reinterpret_cast<float4 *>(&s_V[(seg * GB + (task >> 2)) * 16 + 4 * b]) =
                             make_float4(p0.x, p0.y, p1.x, p1.y);
@@ -231,7 +223,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             if (sc.turb_sigma > 0.0f) {
                 float2 gg;
                 if ((t & 1) == 0) {
-                    const uint4 w = draw(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.key0, sc.key1);
+                    const uint4 w = draw_ks(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
                     gg = box_muller(w.x, w.y);
                     gust_odd = box_muller(w.z, w.w);
                 } else {
@@ -240,11 +232,12 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 gx = fmaf(sc.turb_sigma, gg.x, gx);
                 gy = fmaf(sc.turb_sigma, gg.y, gy);
             }
+            const float c0x = Wn[0] + gx, c0y = Wn[8] + gy;    // nominal + gust folded into c0
 
             // ---------------- 2-3. dynamics, unary checks and geometry per candidate
             const bool act = first <= t;
             bool fly[NC], vnow[NC], lnow[NC];
-            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC], Tc[NC];
+            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC], Tc[NC], px[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 fly[c] = act && !landed[c] && !viol[c];
@@ -255,8 +248,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
                 const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
                 const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
-                const float wx = trilerp(Wn, fx, fy, fz) + gx;
-                const float wy = trilerp(Wn + 8, fx, fy, fz) + gy;
+                const float wx = tripoly(Wn, c0x, fx, fy, fz);
+                const float wy = tripoly(Wn + 8, c0y, fx, fy, fz);
                 // Eq. hor, coordinated-turn lift and parabolic drag (R12):
                 // C_L^2 = (m g / q)^2 (1 + tan^2 phi)
                 float rho = sc.rho_const;
@@ -292,7 +285,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 beta[c] = fast_atan2(nz[c], sarc);
                 lnow[c] = (kind == 0) && !landed[c] && rh[c] <= sc.P_runway && beta[c] <= sc.P_beta &&
                           at <= sc.P_chi && angdist(nchi[c] - kPi) <= sc.P_chi && nv[c] <= sc.P_vs;
-                s_pos[c * kBlock + tid] = make_float4(nx[c], ny[c], nz[c], fly[c] ? 1.0f : 0.0f);
+                // a grounded / inactive / violated aircraft is a NaN position: every comparison fails
+                px[c] = fly[c] ? nx[c] : __int_as_float(0x7fffffff);
+                s_pos[c * kBlock + tid] = make_float4(px[c], ny[c], nz[c], 0.0f);
             }
             __syncwarp();
             // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
@@ -307,9 +302,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const float4 q = s_pos[c * kBlock + seg * W + ((lane + d) & (W - 1))];
-                    const float dx = nx[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
-                    const bool hit = fly[c] && (q.w != 0.0f) && (fmaf(dx, dx, dy * dy) < sc.twoPr2) &&
-                                     (fabsf(dz) < sc.twoPh);
+                    const float dx = px[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
+                    const bool hit = (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh);
                     conf[c] = conf[c] | hit;
                     hits |= (hit ? 1 : 0) << c;
                 }

@@ -23,7 +23,6 @@ namespace smc {
 namespace {
 
 __device__ __forceinline__ float clamp01t(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
-__device__ __forceinline__ float lerpt(float a, float b, float t) { return fmaf(t, b - a, a); }
 
 __device__ __forceinline__ float rcp_a(float x) {
     float r;
@@ -103,7 +102,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     const uint32_t l = args.l0 + lloc;
     const uint32_t k = args.k, mpc = *args.mpcp;
 
-    for (int q = tid; q < 64; q += blockDim.x) s_Q[(q >> 3) * 9 + (q & 7)] = sc.Qhat[q];
+    for (int q = tid; q < 64; q += blockDim.x) s_Q[(q >> 3) * 9 + (q & 7)] = sc.Cq[q];   // trilinear-coefficient form
     reinterpret_cast<uint4 *>(s_flag)[tid] = make_uint4(0u, 0u, 0u, 0u);
 
     const DevAircraft *Ap = sc.ac + i;
@@ -144,8 +143,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
         //      (a) Philox: 4 blocks x H steps per particle
         for (int task = tid; task < 4 * H * PPB; task += nthr) {
             const int q = task % PPB, b = (task / PPB) & 3, ts = task / (4 * PPB);
-            const uint4 w = draw(TAG_WIND, args.l0 + pbase + q, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc,
-                                 sc.key0, sc.key1);
+            const uint4 w = draw_ks(TAG_WIND, args.l0 + pbase + q, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
             const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
             *reinterpret_cast<float4 *>(&s_Z[(ts * PPB + q) * kRow + 4 * b]) = make_float4(p0.x, p0.y, p1.x, p1.y);
         }
@@ -190,7 +188,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             if (sc.turb_sigma > 0.0f) {       // gusts (R15), shared by both candidates
                 float2 gg;
                 if ((t & 1) == 0) {
-                    const uint4 w = draw(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)i << 8), mpc, sc.key0, sc.key1);
+                    const uint4 w = draw_ks(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)i << 8), mpc, sc.ks);
                     gg = box_muller(w.x, w.y);
                     gust_odd = box_muller(w.z, w.w);
                 } else {
@@ -207,15 +205,8 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             const float fx = clamp01t((x - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
             const float fy = clamp01t((y - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
             const float fz = clamp01t((z - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
-            float wx, wy;
-            {
-                const float a = lerpt(Wn[0], Wn[1], fx), b = lerpt(Wn[2], Wn[3], fx);
-                const float cq = lerpt(Wn[4], Wn[5], fx), d = lerpt(Wn[6], Wn[7], fx);
-                wx = lerpt(lerpt(a, b, fy), lerpt(cq, d, fy), fz) + gx;
-                const float a2 = lerpt(Wn[8], Wn[9], fx), b2 = lerpt(Wn[10], Wn[11], fx);
-                const float c2 = lerpt(Wn[12], Wn[13], fx), d2 = lerpt(Wn[14], Wn[15], fx);
-                wy = lerpt(lerpt(a2, b2, fy), lerpt(c2, d2, fy), fz) + gy;
-            }
+            const float wx = tripoly(Wn, Wn[0] + gx, fx, fy, fz);
+            const float wy = tripoly(Wn + 8, Wn[8] + gy, fx, fy, fz);
             float rho = sc.rho_const;
             if (sc.density_mode == 0) rho = 1.225f * ex2_a(4.2559f * __log2f(fmaxf(fmaf(-2.2558e-5f, z, 1.0f), 0.0f)));
             const float qd = rho * v * v * halfS;

@@ -39,9 +39,12 @@ struct DevScen {
     float pop_x0, pop_y0, pop_inv_dx;
     float wind_lo[3], wind_inv_ext[3];
     float Qhat[64];                       // lower-triangular, row-major
+    float Cq[64];                         // M Qhat: row r gives coefficient r of the trilinear
+                                          // polynomial of the node field (see tripoly)
     float a, b;                           // AR(1) coefficients
     float nominal[2], turb_sigma;
     uint32_t key0, key1;                  // Philox key = seed
+    uint32_t ks[20];                      // Philox round keys (key0 + r W0, key1 + r W1), r = 0..9
     const DevAircraft *ac;
     const float *pop;                     // [pop_ny][pop_nx] popdense grid
 };
@@ -59,9 +62,36 @@ __device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
     return c;
 }
 
+// Same generator with the round keys precomputed (DevScen::ks, kernel-parameter
+// space): the key XORs read them as constant-bank operands.
+__device__ __forceinline__ uint4 philox_ks(uint4 c, const uint32_t *ks) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0);
+    }
+    return c;
+}
+
 __device__ __forceinline__ uint4 draw(uint32_t tag, uint32_t x0, uint32_t x1, uint32_t x2,
                                       uint32_t mpc, uint32_t k0, uint32_t k1) {
     return philox(make_uint4(x0, x1, x2, (mpc & 0xFFFFFFu) | (tag << 24)), k0, k1);
+}
+
+__device__ __forceinline__ uint4 draw_ks(uint32_t tag, uint32_t x0, uint32_t x1, uint32_t x2, uint32_t mpc,
+                                         const uint32_t *ks) {
+    return philox_ks(make_uint4(x0, x1, x2, (mpc & 0xFFFFFFu) | (tag << 24)), ks);
+}
+
+// Trilinear interpolation in polynomial form: with c = M W (node n = ix + 2 iy + 4 iz)
+//   f = c0 + c1 fx + c2 fy + c3 fz + c4 fx fy + c5 fx fz + c6 fy fz + c7 fx fy fz,
+// algebraically the 7-lerp form; 7 FMAs.  c0 is passed separately so a per-lane
+// offset (nominal wind + gust) can be folded in once per step.
+__device__ __forceinline__ float tripoly(const float *c, float c0, float fx, float fy, float fz) {
+    const float A = fmaf(fy, fmaf(fz, c[7], c[4]), fmaf(fz, c[5], c[1]));
+    const float B = fmaf(fy, fmaf(fz, c[6], c[2]), fmaf(fz, c[3], c0));
+    return fmaf(fx, A, B);
 }
 
 // Uniform (2k+1) 2^-24, k = w >> 9: exact in binary32 (R37).

@@ -156,7 +156,7 @@ def config(num: int, noise_w: float = 0.1):
         # whole H = 6 horizon, L = 10 240, paper Alg.1 (no MH, S_k = floor(3 + 5 e^{0.05k}),
         # J_max = 100).  Not a BASELINE.json config: a like-for-like latency line.
         scn = snapshot(5, 5, seed)
-        return scn, SmcConfig("table1", L=10240, S=0, K=101, sigma=sig, mh=False, sched_paper=True,
+        return scn, SmcConfig("table1", L=10240, S=8, K=101, sigma=sig, mh=False, sched_paper=True,
                               seed=0x5EED0006)
     raise ValueError(num)
 
@@ -181,6 +181,17 @@ def random_controls(scn: dict, L: int, seed: int, spread: float = 1.0) -> np.nda
         out[:, i, :, 1] = rng.uniform(-1, 1, (L, H)) * scn["phi_max"][i] * spread
         out[:, i, :, 2] = rng.uniform(-1, 1, (L, H)) * scn["gamma_max"][i] * spread
     return out
+
+
+def paper_mixed(seed: int = 2001) -> dict:
+    """The paper's mixed closed-loop scenario shape: 10 arrivals + 10 departures
+    (P:607-616), arrivals every 2 MPC steps, departures every 6."""
+    return traffic(10, 10, seed, arr_every=2, dep_every=6)
+
+
+def paper_congested(seed: int = 2002) -> dict:
+    """The paper's congested shape: 24 arrivals, no departures."""
+    return traffic(24, 0, seed, arr_every=2, dep_every=6)
 
 
 def traffic(n_arr: int, n_dep: int, seed: int, arr_every: int = 2, dep_every: int = 6, jitter: int = 1) -> dict:

@@ -109,3 +109,23 @@ def test_bench_sample_schedule_matches_oracle():
     assert [roofline.sample_schedule(k) for k in range(101)] == [O.sample_schedule(k) for k in range(101)]
     _, cfg = sc.config(6)
     assert sum(roofline.samples_list(cfg)) == 15370
+
+
+def test_closed_loop_audit_counts():
+    """mpc_loop.audit: Eq. avoidance on realised states, completion counts."""
+    import numpy as np
+    from paper_1506_02869_b200 import mpc_loop, scenarios as sc
+    base, _ = sc.config(3)
+    tr = sc.traffic(2, 1, seed=3)
+    Pr, Ph = float(base["P_r"]), float(base["P_h"])
+    st = lambda x, y, z: np.array([x, y, z, 100.0, 0.0, 6e4])
+    log = [
+        {0: st(0, 0, 1000), 1: st(2 * Pr - 1, 0, 1000), 2: st(0, 0, 1000 + 2 * Ph + 1)},   # 0-1 conflict only
+        {0: st(0, 0, 1000), 1: st(2 * Pr + 1, 0, 1000)},                                   # clear (boundary +1)
+        {0: st(0, 0, 1000), 2: st(10, 0, 1000 + 2 * Ph - 1)},                              # conflict
+    ]
+    a = mpc_loop.audit(base, tr, log, {0: (3, "landed"), 2: (5, "exited")}, {0: 10.0, 1: 5.5})
+    assert a.sep_violations == 2
+    assert a.min_sep_m == 10.0                    # step 2, pair 0-2 (step 0: 0-2 is 2 Ph + 1 apart vertically)
+    assert (a.landed, a.exited, a.unfinished, a.n_aircraft) == (1, 1, 1, 3)
+    assert a.fuel_total_kg == 15.5

@@ -384,12 +384,14 @@ def test_mpc_loop_rolling_window(smc):
     from paper_1506_02869_b200 import mpc_loop
     base, cfg = sc.config(3)
     tr = sc.traffic(3, 2, seed=9, arr_every=3, dep_every=10)
-    recs, done, fuel = mpc_loop.run(base, tr, L=2048, S=4, K=8, sigma=cfg.sigma, seed=cfg.seed, n_steps=8,
-                                    max_aircraft=8)
+    recs, done, fuel, aud = mpc_loop.run(base, tr, L=2048, S=4, K=8, sigma=cfg.sigma, seed=cfg.seed, n_steps=8,
+                                         max_aircraft=8, return_audit=True)
     assert len(recs) >= 6
     assert recs[0].window >= 1 and any(r.active > recs[0].active for r in recs)
     assert all(not r.infeasible for r in recs)
     assert all(f >= 0 for f in fuel.values())
+    assert aud.landed + aud.exited + aud.unfinished == aud.n_aircraft == 5
+    assert aud.sep_violations == 0 and aud.min_sep_m > 0
 
 
 def test_paper_literal_mode_replay(smc):

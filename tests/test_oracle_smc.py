@@ -345,3 +345,37 @@ def test_particle_schedule(ora):
     assert all(ora.particles_of(16384, 4096, 101, k) >= ora.particles_of(16384, 4096, 101, k + 1) for k in range(100))
     res = ora.Problem(sc.config(1)[0]).run_smc(L=256, S=4, K=6, seed=1, sigma=(6000.0, 0.03, 0.008), L_final=64)
     assert res["rc"] in (0, 2)
+
+
+def test_warm_start_init(ora):
+    """R45: shifted previous winner seeds the first Lw particles; everything else is
+    the fresh uniform draw."""
+    import numpy as np
+    from paper_1506_02869_b200 import scenarios as sc
+    scn = sc.small(n_arr=2, n_dep=1, H=6)
+    P = ora.Problem(scn)
+    n, H, L, seed = scn["n"], scn["H"], 300, 77
+    fresh = P.init_population(L, seed, mpc=3)
+    prev = np.zeros((n, H, 3))
+    for i in range(n):
+        for t in range(H):
+            prev[i, t] = [5e4 + 100 * t + i, 0.01 * t, -0.001 * t]
+    sig = (2000.0, 0.02, 0.005)
+    # no warm particles / no previous rows: identical to the fresh population
+    assert np.array_equal(P.init_population_warm(L, seed, prev, [1] * n, 0, sig, mpc=3), fresh)
+    assert np.array_equal(P.init_population_warm(L, seed, prev, [0] * n, 100, sig, mpc=3), fresh)
+    has = [1, 0, 1]
+    w = P.init_population_warm(L, seed, prev, has, 100, sig, mpc=3)
+    shifted = np.concatenate([prev[:, 1:], prev[:, -1:]], axis=1)
+    for i in range(n):
+        if has[i]:
+            assert np.array_equal(w[0, i], shifted[i])                 # particle 0: exact shifted winner
+        else:
+            assert np.array_equal(w[:, i], fresh[:, i])                # new aircraft: fresh rows
+    assert np.array_equal(w[100:], fresh[100:])                        # beyond Lw: fresh
+    z = (w[1:100][:, [0, 2]] - shifted[[0, 2]][None]) / np.array(sig)  # standardised perturbations
+    assert abs(z.mean()) < 0.05 and abs(z.std() - 1.0) < 0.05
+    wc = P.init_population_warm(L, seed, prev, has, 100, (1e6, 10.0, 10.0), mpc=3, clamp=True)
+    for i in (0, 2):
+        assert np.all(wc[:, i, :, 0] <= scn["T_max"][i]) and np.all(wc[:, i, :, 0] >= scn["T_min"][i])
+        assert np.all(np.abs(wc[:, i, :, 1]) <= scn["phi_max"][i]) and np.all(np.abs(wc[:, i, :, 2]) <= scn["gamma_max"][i])

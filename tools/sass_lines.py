@@ -15,9 +15,15 @@ top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(csvtxt)))
-hdr = rows[1]
+hi = next(j for j, r in enumerate(rows) if "Address" in r)      # first kernel of the report only
+hdr = rows[hi]
 ia, ie, ist = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
-insts = [(int(r[ia], 16), int(r[ie] or 0), int(r[ist] or 0), r[1].strip()) for r in rows[2:] if len(r) == len(hdr)]
+insts = []
+for r in rows[hi + 1:]:
+    if "Address" in r:
+        break
+    if len(r) == len(hdr) and r[ia].startswith("0x"):
+        insts.append((int(r[ia], 16), int(r[ie] or 0), int(r[ist] or 0), r[1].strip()))
 base = insts[0][0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 cur = None
