@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--traffic", default="c3", choices=["c3", "mixed", "congested"],
                     help="traffic stream of --loop")
+    ap.add_argument("--warm", type=float, default=0.0,
+                    help="warm-start fraction of the population from the previous winner (R45)")
     ap.add_argument("--lfinal", type=int, default=0,
                     help="shrink the population linearly to this many particles by the last round (P:1225)")
     ap.add_argument("--loop", type=int, default=0,
@@ -200,9 +202,11 @@ def run_loop(args):
     else:
         tr, desc = sc.traffic(16, 8, seed=1003, arr_every=2, dep_every=8), "c3 traffic: 16 arrivals / 8 departures"
     recs, done, fuel, aud = mpc_loop.run(base, tr, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
-                                         n_steps=args.loop, max_aircraft=32, return_audit=True)
+                                         n_steps=args.loop, max_aircraft=32, return_audit=True,
+                                         warm_fraction=args.warm, L_final=args.lfinal)
     lat = [r.latency_ms for r in recs]
-    print(json.dumps({"mode": "mpc_loop", "config": f"{desc}, {cfg.name} solver: L={cfg.L}, S={cfg.S}, K={cfg.K}",
+    print(json.dumps({"mode": "mpc_loop", "config": f"{desc}, {cfg.name} solver: L={cfg.L}, S={cfg.S}, K={cfg.K}"
+                      + (f", warm start {args.warm}" if args.warm else "") + (f", L_final {args.lfinal}" if args.lfinal else ""),
                       "steps": len(recs),
                       "per_step": [{"step": r.step, "window": r.window, "active": r.active,
                                     "latency_ms": round(r.latency_ms, 2), "infeasible": r.infeasible} for r in recs],

@@ -70,7 +70,8 @@ typedef struct {
     uint32_t kind;        /* SMC_ARRIVAL or SMC_DEPARTURE */
     uint32_t type;        /* index into smc_scenario.types */
     uint32_t first_step;
-    uint32_t reserved;
+    uint32_t id;          /* persistent aircraft identifier: matches rows of the previous
+                             winner to this window for warm starts (R45); else unused */
     smc_state x0;         /* state at entry (shared by all particles) */
     double theta_F, z_tf, v_D, beta_f;
 } smc_aircraft;
@@ -129,6 +130,10 @@ typedef struct {
     uint32_t n_particles_final;/* particle count of the last round, decreasing linearly
                                   L_k = L - (L - L_final) k / (K - 1) (integer);
                                   0 = constant L.  Single-rank contexts only. */
+    double warm_fraction;      /* warm start (R45): the first floor(warm_fraction L) particles of
+                                  each solve start from the previous solve's winner shifted one
+                                  step (aircraft matched by smc_aircraft.id; particle 0 exact, the
+                                  others + N(0, sigma^2)); 0 = fresh uniform init */
 } smc_config;
 
 /* Per-round diagnostics (smc_iterate). */

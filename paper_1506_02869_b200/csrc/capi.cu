@@ -67,7 +67,8 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
-        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, total;
+        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
+        total;
 };
 
 // Partial log-weight buffer of chunked K2 launches: up to 8 sample chunks x 2
@@ -124,6 +125,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.pflags = take(nmax * sizeof(int));
     o.papplied = take(nmax * 3 * sizeof(float));
     o.lohi = take(nmax * 6 * sizeof(float));
+    o.wmap = take(nmax * sizeof(int32_t));
     o.total = off;
     return o;
 }
@@ -175,6 +177,11 @@ struct smc_ctx {
     // multi-GPU
     int world = 1, rank = 0, vworld = 1;
     uint32_t Lfinal = 0, Leval = 0;     // shrinking populations: final count, last evaluated
+    // warm start (R45): ids of the current window and of the last solved one; device map
+    uint32_t Lw = 0;
+    int32_t *wmap = nullptr;
+    std::vector<uint32_t> cur_ids, solved_ids, wmap_h;
+    uint32_t solved_H = 0;
     uint32_t Lmax = 0;
     ncclComm_t comm = nullptr;
     unsigned long long *Call = nullptr;
@@ -412,12 +419,19 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->pflags = (int *)(ws + L.pflags);
     ctx->papplied = (float *)(ws + L.papplied);
     ctx->lohi = (float *)(ws + L.lohi);
+    ctx->wmap = (int32_t *)(ws + L.wmap);
+    if (cfg->warm_fraction > 0.0) {
+        const double w = cfg->warm_fraction < 1.0 ? cfg->warm_fraction : 1.0;
+        ctx->Lw = (uint32_t)std::floor(w * (double)ctx->Lg);
+    }
     e = cudaMemsetAsync(ws, 0, L.total, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->wmap, 0xFF, L.total - L.wmap, ctx->st);   // map = -1
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         delete ctx;
         return SMC_ECUDA;
     }
+    ctx->wmap_h.assign(ctx->nmax, 0xFFFFFFFFu);
     if (world > 1) {
         NcclApi *api = nccl_api();
         if (!api) { delete ctx; return SMC_ENCCL; }
@@ -609,10 +623,42 @@ static smc_status build_constants(smc_ctx *ctx) {
     return SMC_OK;
 }
 
+// Warm start (R45): map aircraft of this window to rows of the last solved window's
+// winner by id (host-side; uploaded only when it changes, outside any graph).
+static smc_status warm_prepare(smc_ctx *ctx) {
+    if (!ctx->Lw) return SMC_OK;
+    const int n = ctx->dsc.n;
+    std::vector<uint32_t> m(ctx->nmax, 0xFFFFFFFFu);
+    if (ctx->solved_H == (uint32_t)ctx->dsc.H)
+        for (int i = 0; i < n; ++i)
+            for (size_t j = 0; j < ctx->solved_ids.size(); ++j)
+                if (ctx->solved_ids[j] == ctx->cur_ids[i]) { m[i] = (uint32_t)j; break; }
+    if (m != ctx->wmap_h) {
+        ctx->wmap_h = m;
+        CK(h2d(ctx, ctx->wmap, m.data(), sizeof(int32_t) * ctx->nmax));
+    }
+    return SMC_OK;
+}
+
+static void warm_solved(smc_ctx *ctx) {
+    ctx->solved_ids = ctx->cur_ids;
+    ctx->solved_H = (uint32_t)ctx->dsc.H;
+}
+
 static smc_status init_population(smc_ctx *ctx) {
     smc_status s0 = sync_mpc(ctx);
     if (s0 != SMC_OK) return s0;
-    PopArgs pa{ctx->dsc.n, ctx->dsc.H, ctx->Lloc, ctx->l0, 0u, ctx->dsc.key0, ctx->dsc.key1, ctx->mpc_dev};
+    if (!ctx->capturing) {                 // graph replays: smc_solve prepares the map first
+        s0 = warm_prepare(ctx);
+        if (s0 != SMC_OK) return s0;
+    }
+    PopArgs pa{};
+    pa.n = ctx->dsc.n; pa.H = ctx->dsc.H; pa.L = ctx->Lloc; pa.l0 = ctx->l0; pa.k = 0u;
+    pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1; pa.mpcp = ctx->mpc_dev;
+    pa.Lw = ctx->Lw; pa.warm_row = ctx->best_row; pa.warm_ok = ctx->best_idx; pa.warm_map = ctx->wmap;
+    for (int c = 0; c < 3; ++c) pa.sig[c] = (float)ctx->cfg.sigma[c];
+    pa.clamp = (int)ctx->cfg.clamp_proposals;
+    pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
     LAUNCH(launch_init_population(ctx->dsc, pa, ctx->ctrl[0][0], ctx->st));
     ctx->k = 0;
     ctx->cur = 0;
@@ -640,6 +686,8 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
         if (a.kind > 1) return fail(ctx, SMC_EINVAL, "aircraft %u: bad kind", i);
     }
     ctx->ac.assign(scn->aircraft, scn->aircraft + n);
+    ctx->cur_ids.resize(n);
+    for (uint32_t i = 0; i < n; ++i) ctx->cur_ids[i] = scn->aircraft[i].id;
     ctx->types.assign(scn->types, scn->types + scn->n_types);
     ctx->centres_h.assign(scn->centres, scn->centres + 3 * (size_t)scn->n_centres);
     ctx->scn = *scn;
@@ -921,8 +969,14 @@ static smc_status solve_body(smc_ctx *ctx, uint32_t advance_plant) {
 extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
     if (!ctx) return SMC_EINVAL;
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_solve before smc_set_scenario");
-    if (!ctx->cfg.use_graph || ctx->st == nullptr) return solve_body(ctx, advance_plant);
+    if (!ctx->cfg.use_graph || ctx->st == nullptr) {
+        smc_status s = solve_body(ctx, advance_plant);
+        if (s == SMC_OK) warm_solved(ctx);
+        return s;
+    }
     smc_status s = sync_mpc(ctx);                              // outside the graph: mpc is read from device memory
+    if (s != SMC_OK) return s;
+    s = warm_prepare(ctx);
     if (s != SMC_OK) return s;
     const uint32_t K = ctx->cfg.n_rounds ? ctx->cfg.n_rounds : 1;
     if (!ctx->graph_ok || ctx->graph_adv != (int)advance_plant || ctx->graph_K != K) {
@@ -947,6 +1001,7 @@ extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
         ctx->graph_ok = true; ctx->graph_adv = (int)advance_plant; ctx->graph_K = K;
     }
     CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+    warm_solved(ctx);
     ctx->k = ctx->g_k; ctx->cur = ctx->g_cur; ctx->last_eval = ctx->g_last;
     ctx->launches += ctx->g_launches;
     for (int q = 0; q < 4; ++q) ctx->phase_launches[q] += ctx->g_phase_launches[q];

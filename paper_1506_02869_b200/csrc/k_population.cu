@@ -24,9 +24,28 @@ __global__ void k_init_population(const DevScen sc, const PopArgs p, float *ctrl
         const int t = idx % p.H;
         const int i = (idx / p.H) % p.n;
         const uint32_t l = p.l0 + (uint32_t)(idx / ((size_t)p.H * p.n));
+        float *c = ctrl + idx * 3;
+        const int wi = l < p.Lw ? p.warm_map[i] : -1;
+        if (wi >= 0 && *p.warm_ok >= 0) {
+            // warm start (R45): previous winner shifted one step, + N(0, sigma^2) for l > 0
+            const float *b = p.warm_row + ((size_t)wi * p.H + (t + 1 < p.H ? t + 1 : p.H - 1)) * 3;
+            float o0 = b[0], o1 = b[1], o2 = b[2];
+            if (l != 0) {
+                const uint4 w = draw(TAG_INIT, l, 1u << 16, (uint32_t)t | ((uint32_t)i << 8), *p.mpcp, p.key0, p.key1);
+                const float2 z01 = box_muller(w.x, w.y), z23 = box_muller(w.z, w.w);
+                o0 = fmaf(p.sig[0], z01.x, o0); o1 = fmaf(p.sig[1], z01.y, o1); o2 = fmaf(p.sig[2], z23.x, o2);
+                if (p.clamp) {
+                    const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
+                    o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
+                    o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
+                    o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+                }
+            }
+            c[0] = o0; c[1] = o1; c[2] = o2;
+            continue;
+        }
         const uint4 w = draw(TAG_INIT, l, 0u, (uint32_t)t | ((uint32_t)i << 8), *p.mpcp, p.key0, p.key1);
         const DevAircraft &A = sc.ac[i];
-        float *c = ctrl + idx * 3;
         c[0] = A.T_min + (A.T_max - A.T_min) * unif(w.x);
         c[1] = -A.phi_max + 2.0f * A.phi_max * unif(w.y);
         c[2] = -A.gamma_max + 2.0f * A.gamma_max * unif(w.z);

@@ -39,6 +39,15 @@ struct PopArgs {
     int n, H;
     uint32_t L, l0, k, key0, key1;
     const uint32_t *mpcp;
+    // warm start (R45): particles l < Lw of aircraft with warm_map[i] >= 0 start from the
+    // previous winner's row warm_map[i] (shifted one step) when *warm_ok >= 0
+    uint32_t Lw;
+    const float *warm_row;      // [n_prev][H][3]
+    const long long *warm_ok;   // previous winner index (< 0: none)
+    const int32_t *warm_map;    // [n]
+    float sig[3];
+    int clamp;
+    const float *lo3, *hi3;
 };
 
 // K1: uniform initial controls (Alg.1 l.3-5)

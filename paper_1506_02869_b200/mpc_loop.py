@@ -77,6 +77,7 @@ def window_scenario(base: dict, traffic: dict, ids, k: int, states: dict) -> dic
     H = int(base["H"])
     scn = {key: val for key, val in base.items() if key not in ("n", "kind", "first_step", "x0", *PER_AC)}
     scn["n"] = len(ids)
+    scn["id"] = np.array(ids, np.int64)           # persistent identity for warm starts (R45)
     scn["kind"] = np.array([traffic["kind"][a] for a in ids], np.int32)
     scn["first_step"] = np.array([min(H, max(0, int(traffic["entry"][a]) - k)) for a in ids], np.int32)
     scn["x0"] = np.array([states.get(a, traffic["x0"][a]) for a in ids], np.float64).reshape(-1, 6)

@@ -41,7 +41,7 @@ class AircraftType(C.Structure):
 
 
 class Aircraft(C.Structure):
-    _fields_ = [("kind", C.c_uint32), ("type", C.c_uint32), ("first_step", C.c_uint32), ("reserved", C.c_uint32),
+    _fields_ = [("kind", C.c_uint32), ("type", C.c_uint32), ("first_step", C.c_uint32), ("id", C.c_uint32),
                 ("x0", State), ("theta_F", C.c_double), ("z_tf", C.c_double), ("v_D", C.c_double),
                 ("beta_f", C.c_double)]
 
@@ -75,7 +75,7 @@ class Config(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("stream", C.c_void_p), ("max_aircraft", C.c_uint32), ("max_horizon", C.c_uint32),
         ("use_graph", C.c_uint32), ("profile", C.c_uint32), ("virtual_world", C.c_uint32),
-        ("n_particles_final", C.c_uint32),
+        ("n_particles_final", C.c_uint32), ("warm_fraction", C.c_double),
     ]
 
 
@@ -152,6 +152,7 @@ def pack_scenario(scn: dict):
         a.kind = int(scn["kind"][i])
         a.type = i
         a.first_step = int(scn["first_step"][i])
+        a.id = int(scn["id"][i]) if "id" in scn else i
         x0 = np.asarray(scn["x0"], dtype=np.float64).reshape(n, 6)[i]
         a.x0 = State(*[float(v) for v in x0])
         a.theta_F, a.z_tf, a.v_D, a.beta_f = (float(scn[k][i]) for k in ("theta_F", "z_tf", "v_D", "beta_f"))
@@ -188,7 +189,7 @@ class Solver:
                  mh: bool = True, sched_paper: bool = False, clamp: bool = False, device: int = 0,
                  max_aircraft: int | None = None, max_horizon: int | None = None, stream=None,
                  rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False,
-                 virtual_world: int = 0, L_final: int = 0):
+                 virtual_world: int = 0, L_final: int = 0, warm_fraction: float = 0.0):
         import torch
         self.lib = load()
         self.torch = torch
@@ -208,6 +209,7 @@ class Solver:
         cfg.profile = int(profile)
         cfg.virtual_world = int(virtual_world)
         cfg.n_particles_final = int(L_final)
+        cfg.warm_fraction = float(warm_fraction)
         cfg.stream = C.c_void_p(self.stream.cuda_stream)
         if world_size > 1:
             # rank 0 creates the NCCL id; torch.distributed (any backend) shares it

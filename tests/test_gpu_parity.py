@@ -447,3 +447,36 @@ def test_rollout_parity_transposed_layout(smc, case, monkeypatch):
     passes the same rollout parity as the default segment layout."""
     monkeypatch.setenv("SMC_K2_LAYOUT", "transposed")
     test_rollout_parity(smc, case)
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_warm_start_init_parity(smc, use_graph):
+    """Warm start (R45): after an MPC step, a new window sharing two aircraft (by id)
+    starts its first Lw particles from the shifted winner -- particle 0 exactly, the
+    rest perturbed -- and everything else from the fresh draw; vs the oracle."""
+    from paper_1506_02869_b200 import mpc_loop
+    base, cfg = sc.config(3)
+    tr = sc.traffic(3, 1, seed=5, arr_every=1, dep_every=1)
+    tr["entry"][:] = 0
+    scn1 = mpc_loop.window_scenario(base, tr, [0, 1, 2], 10, {})
+    scn2 = mpc_loop.window_scenario(base, tr, [1, 2, 3], 11, {})
+    L, Lw = 400, 100
+    sol = smc.Solver(scn1, L=L, S=4, K=4, sigma=cfg.sigma, seed=cfg.seed, warm_fraction=Lw / L,
+                     use_graph=use_graph, max_aircraft=4)
+    sol.mpc_step(scn1["x0"])
+    u_prev, lam, idx = sol.best_controls(allow_infeasible=True)
+    assert idx >= 0
+    sol.set_scenario(scn2)
+    pop = sol.population()
+    P2 = O.Problem(scn2)
+    prev = np.zeros((3, scn2["H"], 3))
+    prev[0], prev[1] = u_prev[1], u_prev[2]                  # ids 1, 2 were rows 1, 2; id 3 is new
+    ref = P2.init_population_warm(L, cfg.seed, prev, [1, 1, 0], Lw, cfg.sigma, mpc=sol.mpc_index)
+    g = pop["cur"].astype(np.float64)
+    shifted = np.concatenate([u_prev[1:3, 1:], u_prev[1:3, -1:]], axis=1)
+    assert np.array_equal(pop["cur"][0, :2], shifted)        # exact copy of the shifted winner
+    tol = np.array([1e-4 * cfg.sigma[0], 1e-4 * cfg.sigma[1], 1e-4 * cfg.sigma[2]]) + 1e-6 * np.abs(ref)
+    assert np.all(np.abs(g - ref) <= tol), np.unravel_index(np.argmax(np.abs(g - ref) - tol), g.shape)
+    # a solve from the warm population runs (and the next window maps again)
+    sol.mpc_step(scn2["x0"])
+    sol.close()
