@@ -73,11 +73,13 @@ class _Problem(C.Structure):
         ("sigma_lo", C.c_double), ("sigma_hi", C.c_double),
         ("beta_w", C.c_double), ("gamma_w", C.c_double), ("lambda_t", C.c_double),
         ("nominal", C.c_double * 2), ("turb_sigma", C.c_double), ("tma_radius", C.c_double),
+        ("wind_n", C.c_int32 * 3),
     ]
 
 
 class _Derived(C.Structure):
-    _fields_ = [("Rhat", C.c_double * 64), ("Qhat", C.c_double * 64), ("a", C.c_double),
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("ng", C.c_int32),
+                ("Rhat", C.c_double * 4096), ("Qhat", C.c_double * 4096), ("a", C.c_double),
                 ("b", C.c_double), ("supB", C.c_double * 64), ("infB", C.c_double * 64),
                 ("pop", _dp)]
 
@@ -110,7 +112,7 @@ def _declare(L):
         "ora_free_derived": (None, [P(_Derived)]),
         "ora_popdense_point": (d, [P(_Problem), d, d]),
         "ora_popdense_grid": (d, [P(_Problem), P(_Derived), d, d]),
-        "ora_trilinear": (None, [P(_Problem), _dp, _dp, _dp]),
+        "ora_trilinear": (None, [P(_Problem), P(_Derived), _dp, _dp, _dp]),
         "ora_lift_drag": (None, [P(_Problem), C.c_int, _dp, d, _dp, _dp]),
         "ora_step": (None, [P(_Problem), C.c_int, _dp, _dp, _dp, _dp]),
         "ora_landed": (C.c_int, [P(_Problem), _dp]),
@@ -191,6 +193,7 @@ class Problem:
         p.wind_lo[:] = [float(v) for v in scn["wind_lo"]]
         p.wind_hi[:] = [float(v) for v in scn["wind_hi"]]
         p.nominal[:] = [float(v) for v in scn["nominal"]]
+        p.wind_n[:] = [int(v) for v in scn.get("wind_n", (2, 2, 2))]
         self.p = p
         self.d = _Derived()
         rc = lib().ora_derive(C.byref(self.p), C.byref(self.d))
@@ -206,11 +209,17 @@ class Problem:
     # -- derived constants --------------------------------------------------
     @property
     def Rhat(self):
-        return np.array(self.d.Rhat[:]).reshape(8, 8)
+        g = self.d.ng
+        return np.array(self.d.Rhat[: g * g]).reshape(g, g)
 
     @property
     def Qhat(self):
-        return np.array(self.d.Qhat[:]).reshape(8, 8)
+        g = self.d.ng
+        return np.array(self.d.Qhat[: g * g]).reshape(g, g)
+
+    @property
+    def wind_grid(self):
+        return self.d.nx, self.d.ny, self.d.nz
 
     @property
     def ab(self):
@@ -231,9 +240,9 @@ class Problem:
             return lib().ora_popdense_grid(C.byref(self.p), C.byref(self.d), float(x), float(y))
         return lib().ora_popdense_point(C.byref(self.p), float(x), float(y))
 
-    def trilinear(self, W8, pos):
-        W8, pos, out = _f64(W8, (8,)), _f64(pos, (-1,)), np.zeros(1)
-        lib().ora_trilinear(C.byref(self.p), _ptr(W8), _ptr(pos), _ptr(out))
+    def trilinear(self, W, pos):
+        W, pos, out = _f64(W, (self.d.ng,)), _f64(pos, (-1,)), np.zeros(1)
+        lib().ora_trilinear(C.byref(self.p), C.byref(self.d), _ptr(W), _ptr(pos), _ptr(out))
         return float(out[0])
 
     def lift_drag(self, i, st, phi):
@@ -318,7 +327,9 @@ class Problem:
     def plant_step(self, states, u0, seed, mpc, Zplant=None, zinit=0):
         states = _f64(states, (self.n, 6))
         u0 = _f64(u0, (self.n, 3))
-        Z = np.zeros(16) if Zplant is None else _f64(Zplant, (16,)).copy()
+        Z = np.zeros(128) if Zplant is None else _f64(Zplant, (-1,)).copy()
+        if Z.size < 128:
+            Z = np.concatenate([Z, np.zeros(128 - Z.size)])
         zi = np.array([zinit], dtype=np.int32)
         nxt = np.zeros((self.n, 6))
         flags = np.zeros(self.n, np.int32)

@@ -123,12 +123,14 @@ int ora_sample_schedule(int J) { return (int)floor(3.0 + 5.0 * exp(0.05 * (doubl
 /* ------------------------------------------------------------------------ */
 /* Scenario precompute                                                       */
 /* ------------------------------------------------------------------------ */
-static void node_pos(const ora_problem *p, int n, double pos[3])
+/* Grid point n = ix + N_x (iy + N_y iz) of the N_x x N_y x N_z grid spanning
+ * the box [wind_lo, wind_hi] evenly (the paper's runs use 2x2x2). */
+static void node_pos(const ora_problem *p, const ora_derived *d, int n, double pos[3])
 {
-    int ix = n & 1, iy = (n >> 1) & 1, iz = (n >> 2) & 1;
-    pos[0] = ix ? p->wind_hi[0] : p->wind_lo[0];
-    pos[1] = iy ? p->wind_hi[1] : p->wind_lo[1];
-    pos[2] = iz ? p->wind_hi[2] : p->wind_lo[2];
+    int idx[3] = { n % d->nx, (n / d->nx) % d->ny, n / (d->nx * d->ny) };
+    int cnt[3] = { d->nx, d->ny, d->nz };
+    for (int a = 0; a < 3; ++a)
+        pos[a] = p->wind_lo[a] + (p->wind_hi[a] - p->wind_lo[a]) * (double)idx[a] / (double)(cnt[a] - 1);
 }
 
 static double sigma_z(const ora_problem *p, double z)
@@ -152,19 +154,19 @@ double ora_popdense_point(const ora_problem *p, double x, double y)
     return sum < 1.0 ? sum : 1.0;
 }
 
-/* Cholesky factor L with L L^T = A (A SPD, row-major 8x8). */
-static int cholesky8(const double *A, double *Lo)
+/* Cholesky factor L with L L^T = A (A SPD, row-major N x N). */
+static int cholesky(const double *A, double *Lo, int N)
 {
-    memset(Lo, 0, 64 * sizeof(double));
-    for (int r = 0; r < 8; ++r) {
+    memset(Lo, 0, (size_t)N * N * sizeof(double));
+    for (int r = 0; r < N; ++r) {
         for (int c = 0; c <= r; ++c) {
-            double s = A[r * 8 + c];
-            for (int k = 0; k < c; ++k) s -= Lo[r * 8 + k] * Lo[c * 8 + k];
+            double s = A[r * N + c];
+            for (int k = 0; k < c; ++k) s -= Lo[r * N + k] * Lo[c * N + k];
             if (r == c) {
                 if (!(s > 0.0)) return -1;
-                Lo[r * 8 + r] = sqrt(s);
+                Lo[r * N + r] = sqrt(s);
             } else {
-                Lo[r * 8 + c] = s / Lo[c * 8 + c];
+                Lo[r * N + c] = s / Lo[c * N + c];
             }
         }
     }
@@ -175,21 +177,28 @@ int ora_derive(const ora_problem *p, ora_derived *d)
 {
     memset(d, 0, sizeof(*d));
     if (p->n < 0 || p->n > ORA_MAX_AC || p->H < 0 || p->H > 255) return -1;
+    d->nx = p->wind_n[0] ? p->wind_n[0] : 2;
+    d->ny = p->wind_n[1] ? p->wind_n[1] : 2;
+    d->nz = p->wind_n[2] ? p->wind_n[2] : 2;
+    if (d->nx < 2 || d->ny < 2 || d->nz < 2) return -3;
+    d->ng = d->nx * d->ny * d->nz;
+    if (d->ng > ORA_MAX_NODES) return -3;
+    const int G = d->ng;
     /* Eq. cov, same-time entries of Rhat. */
-    for (int n = 0; n < 8; ++n) {
-        double pn[3]; node_pos(p, n, pn);
-        for (int m = 0; m < 8; ++m) {
-            double pm[3]; node_pos(p, m, pm);
+    for (int n = 0; n < G; ++n) {
+        double pn[3]; node_pos(p, d, n, pn);
+        for (int m = 0; m < G; ++m) {
+            double pm[3]; node_pos(p, d, m, pm);
             double dxy = sqrt((pn[0] - pm[0]) * (pn[0] - pm[0]) + (pn[1] - pm[1]) * (pn[1] - pm[1]));
             double dz = fabs(pn[2] - pm[2]);
-            d->Rhat[n * 8 + m] = sigma_z(p, pn[2]) * sigma_z(p, pm[2])
+            d->Rhat[n * G + m] = sigma_z(p, pn[2]) * sigma_z(p, pm[2])
                                * exp(-p->beta_w * dxy) * exp(-p->gamma_w * dz);
         }
     }
     /* Qhat Qhat^T = Rhat.  sigma == 0 gives a zero field. */
     int zero = 1;
-    for (int n = 0; n < 64; ++n) if (d->Rhat[n] != 0.0) zero = 0;
-    if (!zero && cholesky8(d->Rhat, d->Qhat) != 0) return -2;
+    for (int n = 0; n < G * G; ++n) if (d->Rhat[n] != 0.0) zero = 0;
+    if (!zero && cholesky(d->Rhat, d->Qhat, G) != 0) return -2;
     /* a = e^{-dt/G_t}, G_t = 1/lambda_t (R14); Q = sqrt(1-a^2) Qhat. */
     d->a = exp(-p->lambda_t * p->dt);
     d->b = sqrt(1.0 - d->a * d->a);
@@ -244,23 +253,31 @@ double ora_popdense_grid(const ora_problem *p, const ora_derived *d, double x, d
     return (1 - fx) * (1 - fy) * v00 + fx * (1 - fy) * v10 + (1 - fx) * fy * v01 + fx * fy * v11;
 }
 
-/* "tri-linear interpolation between the grid points", position
- * clamped to the grid box (R14). */
-void ora_trilinear(const ora_problem *p, const double W[8], const double pos[3], double *w)
+/* "tri-linear interpolation between the grid points" of the grid
+ * cell holding the position, clamped to the grid box (R14). */
+void ora_trilinear(const ora_problem *p, const ora_derived *d, const double *W, const double pos[3], double *w)
 {
+    const int cnt[3] = { d->nx, d->ny, d->nz };
+    int c0[3];
     double f[3];
     for (int a = 0; a < 3; ++a) {
         double t = (pos[a] - p->wind_lo[a]) / (p->wind_hi[a] - p->wind_lo[a]);
         if (!(t > 0.0)) t = 0.0;
         if (t > 1.0) t = 1.0;
-        f[a] = t;
+        double g = t * (double)(cnt[a] - 1);          /* grid coordinate in [0, N-1] */
+        int i0 = (int)floor(g);
+        if (i0 > cnt[a] - 2) i0 = cnt[a] - 2;
+        c0[a] = i0;
+        f[a] = g - (double)i0;
     }
     double acc = 0.0;
-    for (int n = 0; n < 8; ++n) {
-        double wx = (n & 1) ? f[0] : 1.0 - f[0];
-        double wy = (n & 2) ? f[1] : 1.0 - f[1];
-        double wz = (n & 4) ? f[2] : 1.0 - f[2];
-        acc += wx * wy * wz * W[n];
+    for (int corner = 0; corner < 8; ++corner) {
+        int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+        double wx = dx ? f[0] : 1.0 - f[0];
+        double wy = dy ? f[1] : 1.0 - f[1];
+        double wz = dz ? f[2] : 1.0 - f[2];
+        int node = (c0[0] + dx) + d->nx * ((c0[1] + dy) + d->ny * (c0[2] + dz));
+        acc += wx * wy * wz * W[node];
     }
     *w = acc;
 }
@@ -378,7 +395,8 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
     double fuel[ORA_MAX_AC], sA[ORA_MAX_AC], sB[ORA_MAX_AC], sC[ORA_MAX_AC], sN[ORA_MAX_AC];
     double marg[ORA_MAX_AC];
     int landed[ORA_MAX_AC], viol[ORA_MAX_AC], fly[ORA_MAX_AC], vnow[ORA_MAX_AC];
-    double Z[2][8], W[2][8];
+    double Z[2][ORA_MAX_NODES], W[2][ORA_MAX_NODES];
+    const int G = d->ng, nblk = (2 * d->ng + 3) / 4;
 
     for (int i = 0; i < n; ++i) {
         memcpy(st[i], &p->x0[6 * i], sizeof(st[i]));
@@ -390,21 +408,22 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
 
     for (int t = 0; t < H; ++t) {
         /* Alg.1 l.10: disturbance realisation for step t:
-         * W(0) = Qhat v(0); W(t) = a W(t-1) + Q v(t) with Q = b Qhat. */
-        double v[16];
-        for (int blk = 0; blk < 4; ++blk) {
+         * W(0) = Qhat v(0); W(t) = a W(t-1) + Q v(t) with Q = b Qhat.
+         * Normal e = 4 blk + j of step t: component e / ng (x, y), grid point e % ng. */
+        double v[4 * ((2 * ORA_MAX_NODES + 3) / 4)];
+        for (int blk = 0; blk < nblk; ++blk) {
             uint32_t w[4];
             draw(TAG_WIND, l, (s & 0xFFFFu) | (k << 16), (uint32_t)t | ((uint32_t)blk << 16), mpc, seed, w);
             ora_box_muller(w[0], w[1], &v[4 * blk + 0], &v[4 * blk + 1]);
             ora_box_muller(w[2], w[3], &v[4 * blk + 2], &v[4 * blk + 3]);
         }
         for (int c = 0; c < 2; ++c)
-            for (int m = 0; m < 8; ++m)
-                Z[c][m] = (t == 0) ? v[8 * c + m] : d->a * Z[c][m] + d->b * v[8 * c + m];
+            for (int m = 0; m < G; ++m)
+                Z[c][m] = (t == 0) ? v[G * c + m] : d->a * Z[c][m] + d->b * v[G * c + m];
         for (int c = 0; c < 2; ++c)
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < G; ++r) {
                 double acc = 0.0;
-                for (int m = 0; m < 8; ++m) acc += d->Qhat[r * 8 + m] * Z[c][m];
+                for (int m = 0; m < G; ++m) acc += d->Qhat[r * G + m] * Z[c][m];
                 W[c][r] = acc;
             }
 
@@ -414,8 +433,8 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
             vnow[i] = 0;
             if (!fly[i]) { memcpy(nx[i], st[i], sizeof(nx[i])); continue; }
             double wind[2];
-            ora_trilinear(p, W[0], st[i], &wind[0]);
-            ora_trilinear(p, W[1], st[i], &wind[1]);
+            ora_trilinear(p, d, W[0], st[i], &wind[0]);
+            ora_trilinear(p, d, W[1], st[i], &wind[1]);
             wind[0] += p->nominal[0];
             wind[1] += p->nominal[1];
             if (p->turb_sigma > 0.0) {
@@ -840,19 +859,20 @@ void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *st
                     const double *u0, uint64_t seed, uint32_t mpc, double *Zplant,
                     int32_t *zinit, double *next, int32_t *flags)
 {
-    double v[16], W[2][8];
-    for (int blk = 0; blk < 4; ++blk) {
+    const int G = d->ng, nblk = (2 * d->ng + 3) / 4;
+    double v[4 * ((2 * ORA_MAX_NODES + 3) / 4)], W[2][ORA_MAX_NODES];
+    for (int blk = 0; blk < nblk; ++blk) {
         uint32_t w[4];
         draw(TAG_PLANT_WIND, 0, 0, (uint32_t)blk << 16, mpc, seed, w);
         ora_box_muller(w[0], w[1], &v[4 * blk + 0], &v[4 * blk + 1]);
         ora_box_muller(w[2], w[3], &v[4 * blk + 2], &v[4 * blk + 3]);
     }
-    for (int e = 0; e < 16; ++e) Zplant[e] = *zinit ? d->a * Zplant[e] + d->b * v[e] : v[e];
+    for (int e = 0; e < 2 * G; ++e) Zplant[e] = *zinit ? d->a * Zplant[e] + d->b * v[e] : v[e];
     *zinit = 1;
     for (int c = 0; c < 2; ++c)
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < G; ++r) {
             double acc = 0.0;
-            for (int m = 0; m < 8; ++m) acc += d->Qhat[r * 8 + m] * Zplant[8 * c + m];
+            for (int m = 0; m < G; ++m) acc += d->Qhat[r * G + m] * Zplant[G * c + m];
             W[c][r] = acc;
         }
     for (int i = 0; i < p->n; ++i) {
@@ -860,8 +880,8 @@ void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *st
         flags[i] = 0;
         if (p->first_step[i] != 0) { memcpy(&next[6 * i], st, 6 * sizeof(double)); continue; }
         double wind[2];
-        ora_trilinear(p, W[0], st, &wind[0]);
-        ora_trilinear(p, W[1], st, &wind[1]);
+        ora_trilinear(p, d, W[0], st, &wind[0]);
+        ora_trilinear(p, d, W[1], st, &wind[1]);
         wind[0] += p->nominal[0];
         wind[1] += p->nominal[1];
         if (p->turb_sigma > 0.0) {

@@ -23,6 +23,7 @@ extern "C" {
 #endif
 
 #define ORA_MAX_AC 64
+#define ORA_MAX_NODES 64            /* wind-grid points N_x N_y N_z */
 
 /* One planning problem: N aircraft, horizon H, plus every
  * constant the method needs.  Per-aircraft arrays have length n. */
@@ -52,18 +53,21 @@ typedef struct {
     int32_t pop_nx, pop_ny;
     double pop_x0, pop_y0, pop_dx;  /* grid origin / spacing in metres */
     /* wind model */
-    double wind_lo[3], wind_hi[3];  /* grid box corners (2x2x2 nodes) */
+    double wind_lo[3], wind_hi[3];  /* grid box corners */
     double sigma_lo, sigma_hi;      /* sigma(z) at wind_lo[2] / wind_hi[2], linear */
     double beta_w, gamma_w, lambda_t;
     double nominal[2];              /* forecast (nominal) wind */
     double turb_sigma;              /* R15 */
     double tma_radius;              /* D_TMA */
+    int32_t wind_n[3];              /* grid points per axis N_x, N_y, N_z; 0 -> 2 (the
+                                       paper's eight-point grid) */
 } ora_problem;
 
 /* Derived, per-problem constants: Qhat = chol(Rhat), a, b,
  * departure B normalisers, population grid. */
 typedef struct {
-    double Rhat[64], Qhat[64];
+    int32_t nx, ny, nz, ng;         /* grid points per axis, ng = nx ny nz */
+    double Rhat[ORA_MAX_NODES * ORA_MAX_NODES], Qhat[ORA_MAX_NODES * ORA_MAX_NODES];   /* [ng][ng] */
     double a, b;
     double supB[ORA_MAX_AC], infB[ORA_MAX_AC];
     double *pop;                    /* [pop_ny][pop_nx] owned */
@@ -84,7 +88,8 @@ int    ora_derive(const ora_problem *p, ora_derived *d);
 void   ora_free_derived(ora_derived *d);
 double ora_popdense_point(const ora_problem *p, double x, double y);   /* P:1133 */
 double ora_popdense_grid(const ora_problem *p, const ora_derived *d, double x, double y);
-void   ora_trilinear(const ora_problem *p, const double W[8], const double pos[3], double *w);
+void   ora_trilinear(const ora_problem *p, const ora_derived *d, const double *W /*[ng]*/,
+                     const double pos[3], double *w);
 int    ora_sample_schedule(int J);                                      /* P:559 */
 
 /* ---- models ---- */
@@ -170,7 +175,7 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
 
 /* Plant advance for one MPC step: applies u0[n][3] to aircraft with
  * first_step == 0, realised wind from the PLANT streams (Z carried in
- * Zplant[16], *zinit = 0 on the first call).  flags: bit0 landed, bit1 exited. */
+ * Zplant[2][ng], *zinit = 0 on the first call).  flags: bit0 landed, bit1 exited. */
 void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *states,
                     const double *u0, uint64_t seed, uint32_t mpc, double *Zplant,
                     int32_t *zinit, double *next, int32_t *flags);

@@ -340,3 +340,81 @@ def test_costs_in_unit_interval(ora):
         r = P.rollout(ctrl[l], l, 0, 0, 3)
         assert np.all((r["J"] >= 0) & (r["J"] <= 1))
         assert np.all((r["comp"] >= 0) & (r["comp"] <= 1))
+
+
+# ---------------------------------------------------------------- denser wind grids (N3)
+def _grid_nodes(scn, nx, ny, nz):
+    lo, hi = np.array(scn["wind_lo"]), np.array(scn["wind_hi"])
+    pts = []
+    for iz in range(nz):
+        for iy in range(ny):
+            for ix in range(nx):
+                pts.append(lo + (hi - lo) * np.array([ix / (nx - 1), iy / (ny - 1), iz / (nz - 1)]))
+    return np.array(pts)
+
+
+def test_dense_grid_covariance(ora):
+    """N_x N_y N_z grid: Rhat entries are Eq. cov at the evenly
+    spaced grid points, node n = ix + N_x (iy + N_y iz); Qhat is its Cholesky factor."""
+    scn = sc._finish(sc.base_scenario(), [sc._departure_snapshot(0)])
+    scn["wind_n"] = (3, 4, 2)
+    P = ora.Problem(scn)
+    assert P.wind_grid == (3, 4, 2)
+    R, Q = P.Rhat, P.Qhat
+    assert R.shape == (24, 24)
+    pts = _grid_nodes(scn, 3, 4, 2)
+    zlo, zhi = scn["wind_lo"][2], scn["wind_hi"][2]
+    sig = lambda z: scn["sigma_lo"] + (scn["sigma_hi"] - scn["sigma_lo"]) * (z - zlo) / (zhi - zlo)
+    for a in range(24):
+        for b in range(24):
+            d = pts[a] - pts[b]
+            ref = sig(pts[a][2]) * sig(pts[b][2]) * math.exp(-scn["beta_w"] * math.hypot(d[0], d[1])) \
+                * math.exp(-scn["gamma_w"] * abs(d[2]))
+            assert R[a, b] == pytest.approx(ref, rel=1e-13)
+    assert np.allclose(Q, np.linalg.cholesky(R), rtol=0, atol=1e-12)
+
+
+def test_dense_grid_trilinear(ora):
+    """Cell-wise trilinear interpolation on a 4x3x3 grid: node values at nodes, exact
+    for any globally trilinear field (a + b x + ... + h x y z), clamped outside."""
+    scn = sc._finish(sc.base_scenario(), [sc._departure_snapshot(0)])
+    scn["wind_n"] = (4, 3, 3)
+    P = ora.Problem(scn)
+    pts = _grid_nodes(scn, 4, 3, 3)
+    rng = np.random.default_rng(3)
+    W = rng.normal(size=len(pts))
+    for n in (0, 5, 17, 35):
+        assert P.trilinear(W, pts[n]) == pytest.approx(W[n], abs=1e-14)
+    c = rng.normal(size=8)
+    f = lambda p: (c[0] + c[1] * p[0] / 1e4 + c[2] * p[1] / 1e4 + c[3] * p[2] / 1e4 + c[4] * p[0] * p[1] / 1e8
+                   + c[5] * p[0] * p[2] / 1e8 + c[6] * p[1] * p[2] / 1e8 + c[7] * p[0] * p[1] * p[2] / 1e12)
+    Wf = np.array([f(p) for p in pts])
+    lo, hi = np.array(scn["wind_lo"]), np.array(scn["wind_hi"])
+    for _ in range(100):
+        p = rng.uniform(lo, hi)
+        assert P.trilinear(Wf, p) == pytest.approx(f(p), abs=1e-10)
+    # a field that is trilinear per cell only: piecewise values differ from the global fit
+    Wk = np.abs(pts[:, 0] - pts[1, 0])                    # kink at the second x-node
+    mid = (pts[0] + pts[1]) / 2
+    assert P.trilinear(Wk, mid) == pytest.approx(abs(mid[0] - pts[1, 0]), rel=1e-12)
+    assert P.trilinear(Wf, [1e7, -1e7, 1e7]) == pytest.approx(f([hi[0], lo[1], hi[2]]), abs=1e-10)
+
+
+def test_dense_grid_field_statistics(ora):
+    """W(0) at an interior grid point of a 3x3x3 grid is N(0, sigma(z)^2): the
+    normal -> (component, node) mapping and the Qhat rows."""
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    scn.update(sigma_lo=1.5, sigma_hi=4.0, wind_n=(3, 3, 3))
+    mid = _grid_nodes(scn, 3, 3, 3)[13]                   # centre node
+    scn["x0"][0] = [mid[0], mid[1], mid[2], 130.0, 0.0, 70000.0]
+    P = ora.Problem(scn)
+    zlo, zhi = scn["wind_lo"][2], scn["wind_hi"][2]
+    s_mid = 1.5 + 2.5 * (mid[2] - zlo) / (zhi - zlo)
+    u = np.zeros((1, P.H, 3))
+    vals = []
+    for l in range(4000):
+        tr = P.rollout(u, l, 0, 0, 91)["traj"][0]
+        vals.append((tr[1, 1] - tr[0, 1]) / 10.0)           # y component: heading 0 -> no airspeed in y
+    vals = np.array(vals)
+    assert vals.mean() == pytest.approx(0.0, abs=4 * s_mid / math.sqrt(len(vals)))
+    assert vals.var() == pytest.approx(s_mid ** 2, rel=0.08)
