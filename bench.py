@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--traffic", default="c3", choices=["c3", "mixed", "congested"],
                     help="traffic stream of --loop")
+    ap.add_argument("--wind-grid", default="",
+                    help="N_x,N_y,N_z wind grid points (P:454; default the paper's 2,2,2)")
     ap.add_argument("--warm", type=float, default=0.0,
                     help="warm-start fraction of the population from the previous winner (R45)")
     ap.add_argument("--lfinal", type=int, default=0,
@@ -236,6 +238,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     scn, cfg = sc.config(args.config)
+    if args.wind_grid:
+        scn["wind_n"] = tuple(int(v) for v in args.wind_grid.split(","))
     stream = torch.cuda.Stream(device=local)
     # N > 1: one MPC problem whose particles are sharded over the N GPUs (NCCL
     # exchange each round), L = configs' L per GPU -> weak scaling
@@ -330,7 +334,8 @@ def main():
     all_ms = sum(v[0] for v in phases.values())
     # Table 1's workload (config 6) is the one with a printed number: 56 s per MPC update on
     # a GTX 580, i.e. ac_steps / 56 aircraft-steps/s
-    vs_baseline = value / (ac_steps / 56.0) if (cfg.name == "table1" and world == 1 and not args.lfinal) else None
+    vs_baseline = value / (ac_steps / 56.0) if (cfg.name == "table1" and world == 1 and not args.lfinal
+                                                   and not args.wind_grid) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
@@ -339,7 +344,8 @@ def main():
                                f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
                                + (f"->{args.lfinal}" if args.lfinal else "")
                                + (", S_k=floor(3+5e^(0.05k))" if cfg.sched_paper else f", S={cfg.S}")
-                               + f", H={scn['H']}, K={cfg.K} rounds, " + ("MH on" if cfg.mh else "paper Alg.1 (no MH)"),
+                               + f", H={scn['H']}, K={cfg.K} rounds, " + ("MH on" if cfg.mh else "paper Alg.1 (no MH)")
+                               + (f", wind grid {'x'.join(str(v) for v in scn['wind_n'])}" if args.wind_grid else ""),
                    "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
                                    "all-gathers per round)" if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",

@@ -94,12 +94,15 @@ typedef struct {
     const double *centres;                 /* [n_centres][3] = x, y, radius (m) */
     uint32_t pop_nx, pop_ny;               /* popdense grid; 0 = no grid */
     double pop_x0, pop_y0, pop_dx;
-    double wind_lo[3], wind_hi[3];         /* 2x2x2 wind-grid box */
+    double wind_lo[3], wind_hi[3];         /* wind-grid box */
     double sigma_lo, sigma_hi;             /* sigma(z) at the box bottom / top */
     double beta_w, gamma_w, lambda_t;      /* Eq. cov decay rates (R14) */
     double nominal[2];                     /* forecast wind */
     double turb_sigma;                     /* per-aircraft gust std (R15), 0 = off */
     double tma_radius;                     /* D_TMA */
+    uint32_t wind_n[3];                    /* wind grid points per axis N_x, N_y, N_z, evenly spaced
+                                              over the box; 0 = 2; product <= 64.  The
+                                              paper's runs use 2 x 2 x 2 */
 } smc_scenario;
 
 /* Solver configuration. */

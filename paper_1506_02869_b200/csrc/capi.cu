@@ -68,7 +68,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
-        total;
+        qf, qd, total;
 };
 
 // Partial log-weight buffer of chunked K2 launches: up to 8 sample chunks x 2
@@ -118,13 +118,15 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.Call = take(G > 1 ? (size_t)G * nmax * Lx * 8 : 0);
     o.Sc = take(world > 1 ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
     o.Sall = take(G > 1 ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
-    o.pZ = take(16 * sizeof(double));
+    o.pZ = take(2 * kMaxWindNodes * sizeof(double));
     o.pzi = take(sizeof(int));
     o.pstates = take(nmax * 6 * sizeof(double));
     o.pnext = take(nmax * 6 * sizeof(double));
     o.pflags = take(nmax * sizeof(int));
     o.papplied = take(nmax * 3 * sizeof(float));
     o.lohi = take(nmax * 6 * sizeof(float));
+    o.qf = take(kMaxWindNodes * kMaxWindNodes * sizeof(float));
+    o.qd = take(kMaxWindNodes * kMaxWindNodes * sizeof(double));
     o.wmap = take(nmax * sizeof(int32_t));
     o.total = off;
     return o;
@@ -180,6 +182,11 @@ struct smc_ctx {
     // warm start (R45): ids of the current window and of the last solved one; device map
     uint32_t Lw = 0;
     int32_t *wmap = nullptr;
+    // wind grid Qhat on the device (FP32 for K2's dense path, FP64 for the plant); host copy
+    // of the last upload so unchanged grids are not re-sent every MPC step
+    float *qf = nullptr;
+    double *qd = nullptr;
+    std::vector<double> qd_h;
     std::vector<uint32_t> cur_ids, solved_ids, wmap_h;
     uint32_t solved_H = 0;
     uint32_t Lmax = 0;
@@ -200,7 +207,8 @@ struct smc_ctx {
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
     uint64_t io_h2d = 0, io_d2h = 0;   // host<->device bytes of the production path
-    int layout = 0;                    // K2 layout: 0 lane-per-aircraft segments, 1 transposed (warp = aircraft)
+    int layout[2] = {0, 0};            // K2 layout per candidate count: 0 lane-per-aircraft segments,
+                                       // 1 transposed (warp = aircraft)
     int layout_env = -1;               // SMC_K2_LAYOUT override (-1: automatic)
     bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
     std::string err;
@@ -420,6 +428,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->papplied = (float *)(ws + L.papplied);
     ctx->lohi = (float *)(ws + L.lohi);
     ctx->wmap = (int32_t *)(ws + L.wmap);
+    ctx->qf = (float *)(ws + L.qf);
+    ctx->qd = (double *)(ws + L.qd);
     if (cfg->warm_fraction > 0.0) {
         const double w = cfg->warm_fraction < 1.0 ? cfg->warm_fraction : 1.0;
         ctx->Lw = (uint32_t)std::floor(w * (double)ctx->Lg);
@@ -481,21 +491,24 @@ static smc_status sync_mpc(smc_ctx *ctx) {
 }
 
 // ---------------------------------------------------------------- scenario precompute (host FP64)
-static int cholesky8(const double *A, double *Lo) {
-    for (int q = 0; q < 64; ++q) Lo[q] = 0.0;
-    for (int j = 0; j < 8; ++j) {
-        double d = A[j * 8 + j];
-        for (int p = 0; p < j; ++p) d -= Lo[j * 8 + p] * Lo[j * 8 + p];
+// Cholesky factor Lo Lo^T = A of an SPD N x N matrix (row-major).
+static int cholesky(const double *A, double *Lo, int N) {
+    for (int q = 0; q < N * N; ++q) Lo[q] = 0.0;
+    for (int j = 0; j < N; ++j) {
+        double d = A[j * N + j];
+        for (int p = 0; p < j; ++p) d -= Lo[j * N + p] * Lo[j * N + p];
         if (!(d > 0.0)) return -1;
-        Lo[j * 8 + j] = std::sqrt(d);
-        for (int r = j + 1; r < 8; ++r) {
-            double s = A[r * 8 + j];
-            for (int p = 0; p < j; ++p) s -= Lo[r * 8 + p] * Lo[j * 8 + p];
-            Lo[r * 8 + j] = s / Lo[j * 8 + j];
+        Lo[j * N + j] = std::sqrt(d);
+        for (int r = j + 1; r < N; ++r) {
+            double s = A[r * N + j];
+            for (int p = 0; p < j; ++p) s -= Lo[r * N + p] * Lo[j * N + p];
+            Lo[r * N + j] = s / Lo[j * N + j];
         }
     }
     return 0;
 }
+
+static int wind_axis(uint32_t v) { return v ? (int)v : 2; }
 
 static smc_status build_constants(smc_ctx *ctx) {
     const smc_scenario &s = ctx->scn;
@@ -520,27 +533,43 @@ static smc_status build_constants(smc_ctx *ctx) {
         d.wind_lo[a] = (float)s.wind_lo[a];
         d.wind_inv_ext[a] = (float)(1.0 / (s.wind_hi[a] - s.wind_lo[a]));
     }
-    // Eq. cov between the 8 grid nodes (same time), node = ix + 2 iy + 4 iz
-    double Rh[64], Qh[64];
-    for (int a = 0; a < 8; ++a)
-        for (int b = 0; b < 8; ++b) {
-            const double xa = (a & 1) ? s.wind_hi[0] : s.wind_lo[0], ya = (a & 2) ? s.wind_hi[1] : s.wind_lo[1];
-            const double za = (a & 4) ? s.wind_hi[2] : s.wind_lo[2];
-            const double xb = (b & 1) ? s.wind_hi[0] : s.wind_lo[0], yb = (b & 2) ? s.wind_hi[1] : s.wind_lo[1];
-            const double zb = (b & 4) ? s.wind_hi[2] : s.wind_lo[2];
-            const double ext = s.wind_hi[2] - s.wind_lo[2];
-            const double sa = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (za - s.wind_lo[2]) / ext;
-            const double sb = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (zb - s.wind_lo[2]) / ext;
-            Rh[a * 8 + b] = sa * sb * std::exp(-s.beta_w * std::hypot(xa - xb, ya - yb)) * std::exp(-s.gamma_w * std::fabs(za - zb));
+    // Eq. cov between the N_x N_y N_z grid points (same time),
+    // evenly spaced over the wind box, node = ix + N_x (iy + N_y iz)
+    const int wnx = wind_axis(s.wind_n[0]), wny = wind_axis(s.wind_n[1]), wnz = wind_axis(s.wind_n[2]);
+    const int G = wnx * wny * wnz;
+    std::vector<double> Rh((size_t)G * G), Qh((size_t)G * G, 0.0), pos((size_t)G * 3);
+    for (int a = 0; a < G; ++a) {
+        const int idx[3] = {a % wnx, (a / wnx) % wny, a / (wnx * wny)}, cnt[3] = {wnx, wny, wnz};
+        for (int c = 0; c < 3; ++c)
+            pos[3 * a + c] = s.wind_lo[c] + (s.wind_hi[c] - s.wind_lo[c]) * (double)idx[c] / (double)(cnt[c] - 1);
+    }
+    const double ext = s.wind_hi[2] - s.wind_lo[2];
+    for (int a = 0; a < G; ++a)
+        for (int b = 0; b < G; ++b) {
+            const double *pa = &pos[3 * a], *pb = &pos[3 * b];
+            const double sa = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (pa[2] - s.wind_lo[2]) / ext;
+            const double sb = s.sigma_lo + (s.sigma_hi - s.sigma_lo) * (pb[2] - s.wind_lo[2]) / ext;
+            Rh[(size_t)a * G + b] = sa * sb * std::exp(-s.beta_w * std::hypot(pa[0] - pb[0], pa[1] - pb[1])) *
+                                    std::exp(-s.gamma_w * std::fabs(pa[2] - pb[2]));
         }
     bool zero = true;
-    for (int q = 0; q < 64; ++q) zero = zero && Rh[q] == 0.0;
-    if (zero) {
-        for (int q = 0; q < 64; ++q) Qh[q] = 0.0;
-    } else if (cholesky8(Rh, Qh) != 0) {
+    for (double v : Rh) zero = zero && v == 0.0;
+    if (!zero && cholesky(Rh.data(), Qh.data(), G) != 0)
         return fail(ctx, SMC_EINVAL, "wind covariance not positive definite");
+    d.wn[0] = wnx; d.wn[1] = wny; d.wn[2] = wnz; d.wng = G;
+    p.wn[0] = wnx; p.wn[1] = wny; p.wn[2] = wnz; p.ng = G;
+    d.Qf = ctx->qf; p.Qd = ctx->qd;
+    if (Qh != ctx->qd_h) {                 // upload only when the grid constants change
+        std::vector<float> qf(Qh.size());
+        for (size_t q = 0; q < Qh.size(); ++q) qf[q] = (float)Qh[q];
+        CK(h2d(ctx, ctx->qd, Qh.data(), sizeof(double) * Qh.size()));
+        CK(h2d(ctx, ctx->qf, qf.data(), sizeof(float) * qf.size()));
+        CK(cudaMemsetAsync(ctx->pzi, 0, sizeof(int), ctx->st));   // new grid: plant field restarts
+        CK(cudaStreamSynchronize(ctx->st));  // host vectors go out of scope
+        ctx->qd_h = Qh;
     }
-    for (int q = 0; q < 64; ++q) { d.Qhat[q] = (float)Qh[q]; p.Qhat[q] = Qh[q]; }
+    if (G == 8)
+        for (int q = 0; q < 64; ++q) d.Qhat[q] = (float)Qh[q];
     // trilinear basis change (tripoly): coefficient r = sum_n M[r][n] W_n
     static const int Mtri[8][8] = {{1, 0, 0, 0, 0, 0, 0, 0},   {-1, 1, 0, 0, 0, 0, 0, 0},
                                    {-1, 0, 1, 0, 0, 0, 0, 0},  {-1, 0, 0, 0, 1, 0, 0, 0},
@@ -549,7 +578,8 @@ static smc_status build_constants(smc_ctx *ctx) {
     for (int r = 0; r < 8; ++r)
         for (int m = 0; m < 8; ++m) {
             double acc = 0.0;
-            for (int nn = 0; nn < 8; ++nn) acc += Mtri[r][nn] * Qh[nn * 8 + m];
+            if (G == 8)
+                for (int nn = 0; nn < 8; ++nn) acc += Mtri[r][nn] * Qh[nn * 8 + m];
             d.Cq[r * 8 + m] = (float)acc;
         }
     p.a = std::exp(-s.lambda_t * s.dt);
@@ -679,6 +709,11 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     if ((size_t)scn->pop_nx * scn->pop_ny > kPopCap) return fail(ctx, SMC_EINVAL, "population grid too large");
     if (scn->n_centres > kCentreCap) return fail(ctx, SMC_EINVAL, "too many population centres");
     if (scn->pop_nx * scn->pop_ny > 0 && !(scn->pop_dx > 0.0)) return fail(ctx, SMC_EINVAL, "pop_dx must be > 0");
+    for (int a = 0; a < 3; ++a)
+        if (scn->wind_n[a] == 1 || scn->wind_n[a] > (uint32_t)kMaxWindNodes)
+            return fail(ctx, SMC_EINVAL, "wind grid: %u points on axis %d", scn->wind_n[a], a);
+    if (wind_axis(scn->wind_n[0]) * wind_axis(scn->wind_n[1]) * wind_axis(scn->wind_n[2]) > kMaxWindNodes)
+        return fail(ctx, SMC_EINVAL, "wind grid: more than %d points", kMaxWindNodes);
     for (uint32_t i = 0; i < n; ++i) {
         const smc_aircraft &a = scn->aircraft[i];
         if (a.type >= scn->n_types) return fail(ctx, SMC_EINVAL, "aircraft %u: bad type", i);
@@ -707,13 +742,18 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     // layout ~ proportional to N with a higher per-aircraft cost (c3: 1.42 s; c4 N = 12:
     // 171 vs 167 ms; c2: 58.6 ms).  Break-even near N = 0.75 W, so the transposed layout
     // is used when at most ~70 % of the segment's lanes would carry an aircraft
-    // (rolling-window MPC steps with, e.g., 17-22 aircraft).  SMC_K2_LAYOUT overrides.
+    // (rolling-window MPC steps with, e.g., 17-22 aircraft).  That rule is for the two-
+    // candidate (MH) launches; single-candidate launches (round 0, paper mode) favour the
+    // segment layout (table-1 workload, N = 10, W = 16: 241 vs 309 ms of K2).
+    // SMC_K2_LAYOUT overrides both.
     {
         const int W = segment_width((int)n);
-        ctx->layout = ctx->layout_env >= 0 ? ctx->layout_env : (10 * (int)n < 7 * W ? 1 : 0);
+        ctx->layout[1] = ctx->layout_env >= 0 ? ctx->layout_env : (10 * (int)n < 7 * W ? 1 : 0);
+        ctx->layout[0] = ctx->layout_env >= 0 ? ctx->layout_env : 0;
+        if (ctx->dsc.wng > 8) ctx->layout[0] = ctx->layout[1] = 0;   // dense wind grids: segment layout only
     }
-    ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1);
-    ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2);
+    ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1, ctx->dsc.wng);
+    ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2, ctx->dsc.wng);
     ctx->have_scn = true;
     return init_population(ctx);
 }
@@ -765,7 +805,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     {
         // wave planning: split the S samples into chunks when the particle grid
         // alone would leave a large partial wave (fixed-order partial sums)
-        const int W = segment_width(n);
+        const int W = segment_width(n, ctx->dsc.wng > 8);
         const double B = std::ceil((double)ctx->Lloc / (double)(128 / W));
         const double slots = (double)std::max(1, ctx->bps[NC - 1]) * ctx->nsm;
         auto eff = [&](int c) { const double w = B * c / slots; return w / std::ceil(w); };
@@ -776,9 +816,9 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
             if (need > ctx->part_cap) break;
             if (eff(c) > be + 0.03) { be = eff(c); best = c; }
         }
-        if (ctx->layout == 0 && best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
+        if (ctx->layout[NC - 1] == 0 && best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
     }
-    LAUNCHP(PH_ROLLOUT, ctx->layout ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
+    LAUNCHP(PH_ROLLOUT, ctx->layout[NC - 1] ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
                                      : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
     ctx->Leval = Lk;
@@ -1113,7 +1153,7 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
     ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
     ra.dbg_landed = dland;
-    LAUNCH(ctx->layout ? launch_rollout_t(ctx->dsc, ra, 1, debug, ctx->st) : launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
+    LAUNCH(ctx->layout[0] ? launch_rollout_t(ctx->dsc, ra, 1, debug, ctx->st) : launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
     if (debug) {
         if (J) CK(cudaMemcpyAsync(J, dJ, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
         if (viol) CK(cudaMemcpyAsync(viol, dviol, nu, cudaMemcpyDeviceToHost, ctx->st));

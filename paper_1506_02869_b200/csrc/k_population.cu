@@ -446,8 +446,10 @@ __device__ double d_angdist(double d) {
 }
 
 __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
-    __shared__ double sV[16], sZ[16], sW[16];
+    constexpr int G2M = 2 * kMaxWindNodes;
+    __shared__ double sV[G2M + 4], sZ[G2M], sW[G2M];
     const int tid = threadIdx.x;
+    const int G = ps.ng, G2 = 2 * ps.ng, nblk = (G2 + 3) / 4;
     if (*p.best_idx < 0) {                       // infeasible solve: nothing is applied
         if (tid < p.n) {
             for (int a = 0; a < 6; ++a) p.next[6 * tid + a] = p.states[6 * tid + a];
@@ -456,30 +458,31 @@ __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
         }
         return;
     }
-    if (tid < 4) {
-        const uint4 w = draw(TAG_PLANT_WIND, 0u, 0u, (uint32_t)tid << 16, *p.mpcp, p.key0, p.key1);
+    // realised field: normal e = 4 blk + j -> component e / G, grid point e % G
+    for (int blk = tid; blk < nblk; blk += blockDim.x) {
+        const uint4 w = draw(TAG_PLANT_WIND, 0u, 0u, (uint32_t)blk << 16, *p.mpcp, p.key0, p.key1);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
         for (int pr = 0; pr < 2; ++pr) {
             const double u1 = ((double)(ws[2 * pr] >> 9) + 0.5) * 0x1.0p-23;
             const double u2 = ((double)(ws[2 * pr + 1] >> 9) + 0.5) * 0x1.0p-23;
             const double r = sqrt(-2.0 * log(u1));
-            sV[4 * tid + 2 * pr] = r * cos(2.0 * 3.141592653589793 * u2);
-            sV[4 * tid + 2 * pr + 1] = r * sin(2.0 * 3.141592653589793 * u2);
+            sV[4 * blk + 2 * pr] = r * cos(2.0 * 3.141592653589793 * u2);
+            sV[4 * blk + 2 * pr + 1] = r * sin(2.0 * 3.141592653589793 * u2);
         }
     }
     __syncthreads();
     const int zi = *p.zinit;
-    if (tid < 16) {
-        const double z = zi ? ps.a * p.Z[tid] + ps.b * sV[tid] : sV[tid];
-        sZ[tid] = z;
-        p.Z[tid] = z;
+    for (int e = tid; e < G2; e += blockDim.x) {
+        const double z = zi ? ps.a * p.Z[e] + ps.b * sV[e] : sV[e];
+        sZ[e] = z;
+        p.Z[e] = z;
     }
     __syncthreads();
-    if (tid < 16) {
-        const int comp = tid >> 3, node = tid & 7;
+    for (int e = tid; e < G2; e += blockDim.x) {
+        const int comp = e / G, node = e % G;
         double acc = 0.0;
-        for (int m = 0; m < 8; ++m) acc += ps.Qhat[node * 8 + m] * sZ[comp * 8 + m];
-        sW[tid] = acc;
+        for (int m = 0; m < G; ++m) acc += ps.Qd[node * G + m] * sZ[comp * G + m];
+        sW[e] = acc;
     }
     __syncthreads();
     if (tid == 0) *p.zinit = 1;
@@ -494,16 +497,25 @@ __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
         for (int a = 0; a < 6; ++a) nx[a] = st[a];
         return;
     }
+    // trilinear interpolation in the grid cell holding the aircraft, clamped
     double f[3];
+    int c0[3];
     for (int a = 0; a < 3; ++a) {
         double t = (st[a] - ps.wind_lo[a]) / (ps.wind_hi[a] - ps.wind_lo[a]);
-        f[a] = t > 0.0 ? (t < 1.0 ? t : 1.0) : 0.0;
+        t = t > 0.0 ? (t < 1.0 ? t : 1.0) : 0.0;
+        const double gcoord = t * (double)(ps.wn[a] - 1);
+        int i0 = (int)floor(gcoord);
+        if (i0 > ps.wn[a] - 2) i0 = ps.wn[a] - 2;
+        c0[a] = i0;
+        f[a] = gcoord - (double)i0;
     }
     double wxy[2];
     for (int c = 0; c < 2; ++c) {
         double acc = 0.0;
-        for (int nd = 0; nd < 8; ++nd)
-            acc += ((nd & 1) ? f[0] : 1 - f[0]) * ((nd & 2) ? f[1] : 1 - f[1]) * ((nd & 4) ? f[2] : 1 - f[2]) * sW[c * 8 + nd];
+        for (int nd = 0; nd < 8; ++nd) {
+            const int node = (c0[0] + (nd & 1)) + ps.wn[0] * ((c0[1] + ((nd >> 1) & 1)) + ps.wn[1] * (c0[2] + (nd >> 2)));
+            acc += ((nd & 1) ? f[0] : 1 - f[0]) * ((nd & 2) ? f[1] : 1 - f[1]) * ((nd & 4) ? f[2] : 1 - f[2]) * sW[c * G + node];
+        }
         wxy[c] = acc + ps.nominal[c];
     }
     if (ps.turb_sigma > 0.0) {
@@ -552,7 +564,7 @@ __global__ void k_plant(const PlantScen ps, const PlantArgs p) {
 }
 
 cudaError_t launch_plant(const PlantScen &ps, const PlantArgs &p, cudaStream_t st) {
-    k_plant<<<1, 32, 0, st>>>(ps, p);
+    k_plant<<<1, 128, 0, st>>>(ps, p);
     return cudaGetLastError();
 }
 

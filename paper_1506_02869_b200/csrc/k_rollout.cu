@@ -81,7 +81,12 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
     return copysignf(r, y);
 }
 
-template <int W, int NC, bool DEBUG>
+// Shared-memory strides of the wind field per segment: normals (VST) and
+// AR(1) state / node values (ZST, odd to spread segments over banks).
+__host__ __device__ constexpr int dense_vst(int G) { return 4 * ((2 * G + 3) / 4); }
+__host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 1; }
+
+template <int W, int NC, bool DEBUG, bool DENSE>
 __global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
@@ -89,12 +94,17 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     extern __shared__ __align__(16) float smem[];
     const int H = sc.H, n = sc.n;
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);               // [H][NC][kBlock] (T, tan phi, sin g, cos g)
-    constexpr int GB = (W >= 8) ? W / 4 : 1;                       // steps whose normals one batch draws
-    float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock); // [SEGS][GB][16] normals
-    float *s_Z = s_V + SEGS * GB * 16;                                // [SEGS][16] AR(1) state
-    float *s_W = s_Z + SEGS * 16;                                     // [SEGS][16] wind at nodes
-    float4 *s_pos = reinterpret_cast<float4 *>(s_W + SEGS * 16);     // [NC][kBlock]
-    float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);     // [8][9]
+    constexpr int GB = (W >= 8 && !DENSE) ? W / 4 : 1;             // steps whose normals one batch draws
+    // 2x2x2 grid: [SEGS][GB][16] normals, [SEGS][16] state, [SEGS][16] coefficients, Cq [8][9];
+    // dense grid (G = N_x N_y N_z > 8): [SEGS][VST] normals, [SEGS][ZST] state and node values,
+    // Qhat [G][G+1]
+    const int G = DENSE ? sc.wng : 8;
+    const int VST = DENSE ? dense_vst(G) : GB * 16, ZST = DENSE ? dense_zst(G) : 16;
+    float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock);
+    float *s_Z = s_V + SEGS * VST;
+    float *s_W = s_Z + SEGS * ZST;
+    float4 *s_pos = reinterpret_cast<float4 *>(s_W + ((SEGS * ZST + 3) & ~3));   // [NC][kBlock]
+    float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);
 
     const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
     const uint32_t lloc = blockIdx.x * SEGS + seg;
@@ -103,7 +113,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     const bool isac = lane < n;
     const uint32_t k = args.k, mpc = *args.mpcp;
 
-    if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Cq[tid];   // W = Cq Z: trilinear coefficients
+    if constexpr (DENSE) {
+        for (int q = tid; q < G * G; q += kBlock) s_Q[(q / G) * (G + 1) + q % G] = sc.Qf[q];
+    } else {
+        if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Cq[tid];   // W = Cq Z: trilinear coefficients
+    }
 
     // ---- per-lane aircraft constants needed every step (the rest is read when needed)
     const DevAircraft *Ap = sc.ac + (isac ? lane : 0);
@@ -139,7 +153,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     // W >= 8: every wind entry a lane owns belongs to node lane & 7 -> keep that Qhat row in registers
     float qrow[8];
 #pragma unroll
-    for (int mm = 0; mm < 8; ++mm) qrow[mm] = (W >= 8) ? s_Q[(lane & 7) * 9 + mm] : 0.0f;
+    for (int mm = 0; mm < 8; ++mm) qrow[mm] = (W >= 8 && !DENSE) ? s_Q[(lane & 7) * 9 + mm] : 0.0f;
 
     float ell[NC];
 #pragma unroll
@@ -168,6 +182,33 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
         for (int t = 0; t < H; ++t) {
             // ---------------- 1. wind realisation for step t (Alg.1 l.10).
+            float Wn[16];
+            float *const sWs = s_W + seg * ZST;
+            if constexpr (DENSE) {
+                // dense grid: 2G normals from ceil(2G/4) Philox blocks, AR(1) in shared
+                // memory, node values W = Qhat Z (lower-triangular rows) -- spread over the lanes
+                float *const sVs = s_V + seg * VST, *const sZs = s_Z + seg * ZST;
+                const int G2 = 2 * G, nblk = (G2 + 3) >> 2;
+                for (int b = lane; b < nblk; b += W) {
+                    const uint4 w = draw_ks(TAG_WIND, l, x1, (uint32_t)t | ((uint32_t)b << 16), mpc, sc.ks);
+                    const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
+                    *reinterpret_cast<float4 *>(&sVs[4 * b]) = make_float4(p0.x, p0.y, p1.x, p1.y);
+                }
+                __syncwarp();
+                for (int e = lane; e < G2; e += W) {
+                    const float ve = sVs[e];
+                    sZs[e] = (t == 0) ? ve : fmaf(sc.a, sZs[e], sc.b * ve);
+                }
+                __syncwarp();
+                for (int e = lane; e < G2; e += W) {
+                    const int comp = e >= G ? 1 : 0, r = e - comp * G;
+                    const float *zc = sZs + comp * G, *qr = s_Q + r * (G + 1);
+                    float acc = 0.0f;
+                    for (int m = 0; m <= r; ++m) acc = fmaf(qr[m], zc[m], acc);
+                    sWs[e] = acc;
+                }
+                __syncwarp();
+            } else {
             // Every GB steps the segment's lanes draw the 4 Philox blocks of GB
             // consecutive steps at once (lane -> block lane&3 of step t + lane/4).
             const int tb = t % GB;
@@ -209,7 +250,6 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 }
             }
             __syncwarp();
-            float Wn[16];
             {
                 const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[seg * 16]);
 #pragma unroll
@@ -217,6 +257,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const float4 a4 = w4[q];
                     Wn[4 * q] = a4.x; Wn[4 * q + 1] = a4.y; Wn[4 * q + 2] = a4.z; Wn[4 * q + 3] = a4.w;
                 }
+            }
             }
             // gusts (R15): one Philox call covers steps 2u and 2u+1
             float gx = sc.nominal[0], gy = sc.nominal[1];
@@ -232,7 +273,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 gx = fmaf(sc.turb_sigma, gg.x, gx);
                 gy = fmaf(sc.turb_sigma, gg.y, gy);
             }
-            const float c0x = Wn[0] + gx, c0y = Wn[8] + gy;    // nominal + gust folded into c0
+            const float c0x = DENSE ? gx : Wn[0] + gx, c0y = DENSE ? gy : Wn[8] + gy;   // nominal + gust (+ c0)
 
             // ---------------- 2-3. dynamics, unary checks and geometry per candidate
             const bool act = first <= t;
@@ -245,11 +286,39 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 const float T = cc.x, tph = cc.y, sga = cc.z, cga = cc.w;
                 Tc[c] = T;
                 // wind at the pre-step position (trilinear, clamped to the box)
-                const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
-                const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
-                const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
-                const float wx = tripoly(Wn, c0x, fx, fy, fz);
-                const float wy = tripoly(Wn + 8, c0y, fx, fy, fz);
+                float wx, wy;
+                if constexpr (DENSE) {
+                    // grid cell holding the aircraft (clamped), trilinear over its 8 corners
+                    float f3[3];
+                    int base = 0, mul = 1;
+                    const float p3[3] = {x[c], y[c], z[c]};
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const float gc = clamp01((p3[a] - sc.wind_lo[a]) * sc.wind_inv_ext[a]) * (float)(sc.wn[a] - 1);
+                        const int i0 = min((int)gc, sc.wn[a] - 2);
+                        f3[a] = gc - (float)i0;
+                        base += i0 * mul;
+                        mul *= sc.wn[a];
+                    }
+                    const int sy = sc.wn[0], sz = sc.wn[0] * sc.wn[1];
+#pragma unroll
+                    for (int comp = 0; comp < 2; ++comp) {
+                        const float *w0 = sWs + comp * G + base;
+                        const float a0 = fmaf(f3[0], w0[1] - w0[0], w0[0]);
+                        const float a1 = fmaf(f3[0], w0[sy + 1] - w0[sy], w0[sy]);
+                        const float a2 = fmaf(f3[0], w0[sz + 1] - w0[sz], w0[sz]);
+                        const float a3 = fmaf(f3[0], w0[sz + sy + 1] - w0[sz + sy], w0[sz + sy]);
+                        const float b0 = fmaf(f3[1], a1 - a0, a0), b1 = fmaf(f3[1], a3 - a2, a2);
+                        const float wv = fmaf(f3[2], b1 - b0, b0) + (comp ? c0y : c0x);
+                        if (comp) wy = wv; else wx = wv;
+                    }
+                } else {
+                    const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
+                    const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
+                    const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
+                    wx = tripoly(Wn, c0x, fx, fy, fz);
+                    wy = tripoly(Wn + 8, c0y, fx, fy, fz);
+                }
                 // Eq. hor, coordinated-turn lift and parabolic drag (R12):
                 // C_L^2 = (m g / q)^2 (1 + tan^2 phi)
                 float rho = sc.rho_const;
@@ -451,8 +520,14 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     }
 }
 
-size_t rollout_smem_bytes(int W, int NC, int H) {
+size_t rollout_smem_bytes(int W, int NC, int H, int ng) {
     const int SEGS = kBlock / W;
+    if (ng > 8) {
+        const size_t zs = ((size_t)SEGS * dense_zst(ng) + 3) & ~(size_t)3;
+        return sizeof(float4) * ((size_t)H * NC * kBlock) +
+               sizeof(float) * ((size_t)SEGS * dense_vst(ng) + SEGS * dense_zst(ng) + zs) +
+               sizeof(float4) * NC * kBlock + sizeof(float) * (size_t)ng * (ng + 1) + 16;
+    }
     const int GB = (W >= 8) ? W / 4 : 1;
     return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * (SEGS * GB * 16 + 2 * SEGS * 16) +
            sizeof(float4) * NC * kBlock + sizeof(float) * 72 + 16;
@@ -500,10 +575,10 @@ __global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) 
     }
 }
 
-template <int W, int NC, bool DEBUG>
+template <int W, int NC, bool DEBUG, bool DENSE>
 static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
-    const size_t smem = rollout_smem_bytes(W, NC, sc.H);
-    auto kern = k_rollout<W, NC, DEBUG>;
+    const size_t smem = rollout_smem_bytes(W, NC, sc.H, DENSE ? sc.wng : 8);
+    auto kern = k_rollout<W, NC, DEBUG, DENSE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int segs = kBlock / W;
@@ -520,44 +595,56 @@ static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_
 }
 
 // Resident K2 blocks per SM for this problem shape (wave-quantisation planning).
-int rollout_blocks_per_sm(int n, int H, int NC) {
-    const int W = segment_width(n);
-    const size_t smem = rollout_smem_bytes(W, NC, H);
+int rollout_blocks_per_sm(int n, int H, int NC, int ng) {
+    const bool dense = ng > 8;
+    const int W = segment_width(n, dense);
+    const size_t smem = rollout_smem_bytes(W, NC, H, ng);
     int nb = 0;
-#define SMC_OCC(WW)                                                                                    \
-    if (W == WW) {                                                                                     \
-        auto kern = NC == 2 ? k_rollout<WW, 2, false> : k_rollout<WW, 1, false>;                       \
+#define SMC_OCC(WW, DN)                                                                                \
+    if (W == WW && dense == DN) {                                                                      \
+        auto kern = NC == 2 ? k_rollout<WW, 2, false, DN> : k_rollout<WW, 1, false, DN>;               \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem);                        \
     }
-    SMC_OCC(1) SMC_OCC(2) SMC_OCC(4) SMC_OCC(8) SMC_OCC(16) SMC_OCC(32)
+    SMC_OCC(1, false) SMC_OCC(2, false) SMC_OCC(4, false) SMC_OCC(8, false) SMC_OCC(16, false) SMC_OCC(32, false)
+    SMC_OCC(4, true) SMC_OCC(8, true) SMC_OCC(16, true) SMC_OCC(32, true)
 #undef SMC_OCC
     return nb;
 }
 
 template <int NC, bool DEBUG>
-static cudaError_t launch_nc(int W, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+static cudaError_t launch_nc(int W, bool dense, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    if (dense) {
+        switch (W) {     // dense grids: W >= 4 (shared-memory budget of the per-segment field)
+            case 4: return launch_w<4, NC, DEBUG, true>(sc, a, st);
+            case 8: return launch_w<8, NC, DEBUG, true>(sc, a, st);
+            case 16: return launch_w<16, NC, DEBUG, true>(sc, a, st);
+            case 32: return launch_w<32, NC, DEBUG, true>(sc, a, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (W) {
-        case 1: return launch_w<1, NC, DEBUG>(sc, a, st);
-        case 2: return launch_w<2, NC, DEBUG>(sc, a, st);
-        case 4: return launch_w<4, NC, DEBUG>(sc, a, st);
-        case 8: return launch_w<8, NC, DEBUG>(sc, a, st);
-        case 16: return launch_w<16, NC, DEBUG>(sc, a, st);
-        case 32: return launch_w<32, NC, DEBUG>(sc, a, st);
+        case 1: return launch_w<1, NC, DEBUG, false>(sc, a, st);
+        case 2: return launch_w<2, NC, DEBUG, false>(sc, a, st);
+        case 4: return launch_w<4, NC, DEBUG, false>(sc, a, st);
+        case 8: return launch_w<8, NC, DEBUG, false>(sc, a, st);
+        case 16: return launch_w<16, NC, DEBUG, false>(sc, a, st);
+        case 32: return launch_w<32, NC, DEBUG, false>(sc, a, st);
     }
     return cudaErrorInvalidValue;
 }
 
-int segment_width(int n) {
-    int w = 1;
+int segment_width(int n, bool dense) {
+    int w = dense ? 4 : 1;
     while (w < n) w <<= 1;
     return w;
 }
 
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st) {
-    const int W = segment_width(sc.n);
-    if (debug) return NC == 2 ? launch_nc<2, true>(W, sc, a, st) : launch_nc<1, true>(W, sc, a, st);
-    return NC == 2 ? launch_nc<2, false>(W, sc, a, st) : launch_nc<1, false>(W, sc, a, st);
+    const bool dense = sc.wng > 8;
+    const int W = segment_width(sc.n, dense);
+    if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
+    return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }
 
 }  // namespace smc

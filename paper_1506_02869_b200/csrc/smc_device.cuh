@@ -45,6 +45,8 @@ struct DevScen {
     float nominal[2], turb_sigma;
     uint32_t key0, key1;                  // Philox key = seed
     uint32_t ks[20];                      // Philox round keys (key0 + r W0, key1 + r W1), r = 0..9
+    int wn[3], wng;                       // wind grid points per axis, wng = product
+    const float *Qf;                      // [wng][wng] Qhat (FP32), read by the dense-grid path (wng > 8)
     const DevAircraft *ac;
     const float *pop;                     // [pop_ny][pop_nx] popdense grid
 };

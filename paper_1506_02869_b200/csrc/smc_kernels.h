@@ -28,9 +28,10 @@ struct RolloutArgs {
     int32_t *dbg_landed;
 };
 
-int segment_width(int n);
-int rollout_blocks_per_sm(int n, int H, int NC);
-size_t rollout_smem_bytes(int W, int NC, int H);
+constexpr int kMaxWindNodes = 64;   // N_x N_y N_z
+int segment_width(int n, bool dense = false);
+int rollout_blocks_per_sm(int n, int H, int NC, int ng = 8);
+size_t rollout_smem_bytes(int W, int NC, int H, int ng = 8);
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
 // transposed layout (warp = aircraft, lane = (candidate, particle)); k_rollout_t.cu
 cudaError_t launch_rollout_t(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
@@ -150,7 +151,9 @@ struct PlantArgs {
     const long long *best_idx;  // [1] winner (-1: infeasible -> plant state unchanged)
 };
 struct PlantScen {              // FP64 constants for the plant
-    double Qhat[64], a, b, dt, g, rho_const;
+    const double *Qd;           // [ng][ng] Qhat (FP64)
+    int wn[3], ng;
+    double a, b, dt, g, rho_const;
     double wind_lo[3], wind_hi[3], nominal[2], turb_sigma, tma_radius;
     double P_runway, P_beta, P_chi, P_vs;
     int density_mode;

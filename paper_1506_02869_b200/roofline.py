@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
+
 MUFU_W = 8.0          # FP32-lane-op equivalent of one MUFU op
 SMS = 148
 FP32_LANES_PER_SM_CLK = 128
@@ -49,7 +51,16 @@ def ops_per_aircraft_step(scn: dict, C: int) -> float:
     if float(scn["noise_w"]) > 0 and int(scn["pop_nx"]) > 0:
         per += NOISE_FP
     per += PAIR_OPS * (n - 1) / 2.0
-    per += (WINDGEN_INT + WINDGEN_FP + MUFU_W * WINDGEN_MUFU) / (n * C)
+    G = int(np.prod(scn.get("wind_n", (2, 2, 2)))) if "wind_n" in scn else 8
+    if G == 8:
+        per += (WINDGEN_INT + WINDGEN_FP + MUFU_W * WINDGEN_MUFU) / (n * C)
+    else:
+        # dense grid: ceil(2G/4) Philox calls, G Box-Muller pairs (6 FP + 4 MUFU each),
+        # 2G AR(1) updates (2 FP), W = Qhat Z over the lower triangle (2 x G(G+1)/2 FMA = 2 ops),
+        # plus the cell index per candidate step (9 FP)
+        nblk = (2 * G + 3) // 4
+        gen = nblk * 80 + G * 6 + MUFU_W * G * 4 + 2 * G * 2 + 2 * G * (G + 1)
+        per += gen / (n * C) + 9
     per += (END_FP + MUFU_W * END_MUFU) / H
     if float(scn["turb_sigma"]) > 0:
         per += (GUST_INT + GUST_FP + MUFU_W * GUST_MUFU) / (2.0 * C)

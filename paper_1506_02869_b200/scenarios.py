@@ -51,6 +51,7 @@ def base_scenario(H: int = 6, dt: float = 10.0) -> dict:
         noise_w=0.0, A_c=4000.0, centres=np.zeros((0, 3)),
         pop_nx=0, pop_ny=0, pop_x0=0.0, pop_y0=0.0, pop_dx=1000.0,
         wind_lo=[-30000.0, -30000.0, 0.0], wind_hi=[30000.0, 30000.0, 12000.0],
+        wind_n=(2, 2, 2),             # grid points per axis; the paper uses 2x2x2
         sigma_lo=1.5, sigma_hi=4.0,
         beta_w=1.6e-6, gamma_w=1.5e-5, lambda_t=6.0e-6,   # P:451 (lambda read as s^-1)
         nominal=[0.0, 0.0], turb_sigma=0.0, tma_radius=30000.0,

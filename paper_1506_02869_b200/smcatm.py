@@ -63,6 +63,7 @@ class Scenario(C.Structure):
         ("sigma_lo", C.c_double), ("sigma_hi", C.c_double),
         ("beta_w", C.c_double), ("gamma_w", C.c_double), ("lambda_t", C.c_double),
         ("nominal", C.c_double * 2), ("turb_sigma", C.c_double), ("tma_radius", C.c_double),
+        ("wind_n", C.c_uint32 * 3),
     ]
 
 
@@ -179,6 +180,7 @@ def pack_scenario(scn: dict):
     s.wind_lo[:] = [float(v) for v in scn["wind_lo"]]
     s.wind_hi[:] = [float(v) for v in scn["wind_hi"]]
     s.nominal[:] = [float(v) for v in scn["nominal"]]
+    s.wind_n[:] = [int(v) for v in scn.get("wind_n", (2, 2, 2))]
     return s, [ac, ty, cen]
 
 

@@ -75,7 +75,8 @@ def _near_trim_controls(scn, L, seed):
     return c
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "n3_partial", "n12_noise", "n24", "n1"])
+@pytest.mark.parametrize("case", ["c1", "c2", "n3_partial", "n12_noise", "n24", "n1", "dense332_n3",
+                                  "dense444_c2", "dense442_n1", "dense_n20"])
 def test_rollout_parity(smc, case):
     if case == "c1":
         scn, cfg = sc.config(1)
@@ -93,6 +94,22 @@ def test_rollout_parity(smc, case):
     elif case == "n24":
         scn, cfg = sc.config(3)
         L, S, seed = 12, 2, cfg.seed
+    elif case == "dense332_n3":            # denser wind grids (N3): 18 points, W = 4
+        scn = sc.small(2, 1, H=7, seed=5)
+        scn.update(wind_n=(3, 3, 2), sigma_lo=3.0, sigma_hi=6.0)
+        L, S, seed = 90, 3, 99
+    elif case == "dense444_c2":            # 64 points, W = 8
+        scn, cfg = sc.config(2)
+        scn.update(wind_n=(4, 4, 4), sigma_lo=3.0, sigma_hi=6.0)
+        L, S, seed = 70, 3, cfg.seed
+    elif case == "dense442_n1":            # one aircraft: segment padded to W = 4
+        scn = sc.small(1, 0, H=6, seed=3)
+        scn.update(wind_n=(4, 4, 2), sigma_lo=3.0, sigma_hi=6.0)
+        L, S, seed = 200, 2, 5
+    elif case == "dense_n20":              # 5x3x2 grid, 20 aircraft (W = 32)
+        scn = sc.snapshot(12, 8, seed=21)
+        scn.update(wind_n=(5, 3, 2), sigma_lo=3.0, sigma_hi=6.0)
+        L, S, seed = 16, 2, 31
     else:
         scn = sc.small(1, 0, H=6, seed=3)
         L, S, seed = 200, 2, 5
@@ -321,6 +338,22 @@ def test_select_and_plant_parity(smc):
     assert np.array_equal(flags.astype(np.int32), ref_flags)
     ctrl = pop["prop"][best] if pop["surv"][best] else pop["cur"][best]
     assert np.array_equal(applied, ctrl[:, 0, :])
+
+
+def test_plant_parity_dense_grid(smc):
+    """K8 (FP64 plant) on a 4x3x2 wind grid, two consecutive MPC steps (AR(1) carry)."""
+    scn, cfg = sc.config(1)
+    scn.update(wind_n=(4, 3, 2), sigma_lo=3.0, sigma_hi=6.0)
+    sol = _solver(smc, scn, L=256, S=4, K=4, seed=cfg.seed)
+    P = O.Problem(scn)
+    Z, zi, x = None, 0, scn["x0"].copy()
+    for m in range(2):
+        applied, nxt, flags = sol.mpc_step(x)
+        ref_next, ref_flags, Z, zi = P.plant_step(x, applied.astype(np.float64), cfg.seed, m, Z, zi)
+        assert np.allclose(nxt, ref_next, rtol=1e-12, atol=1e-9), m
+        assert np.array_equal(flags.astype(np.int32), ref_flags)
+        x = nxt
+    sol.close()
 
 
 def test_graph_replay_matches_direct_launches(smc):
