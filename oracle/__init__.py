@@ -125,6 +125,8 @@ def _declare(L):
         "ora_rollout": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, P(_RollOut)]),
         "ora_evaluate": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, _dp, C.c_int]),
         "ora_init_population": (None, [P(_Problem), u32, u64, u32, _dp]),
+        "ora_fuel_estimate1": (C.c_int, [P(_Problem), C.c_int, _dp, _dp, C.c_int, d, d, _dp, _dp]),
+        "ora_fuel_estimate2": (C.c_int, [P(_Problem), C.c_int, _dp, _dp, C.c_int, d, d, _dp]),
         "ora_init_population_warm": (None, [P(_Problem), u32, u64, u32, _dp, _ip, u32, _dp, C.c_int, _dp]),
         "ora_mh_accept": (C.c_int, [d, d, u32, u32, u64, u32]),
         "ora_resample_column": (C.c_int, [_dp, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
@@ -299,6 +301,24 @@ class Problem:
         lib().ora_init_population_warm(C.byref(self.p), L, seed, mpc, _ptr(prev),
                                        hp.ctypes.data_as(C.POINTER(C.c_int32)), Lw, _ptr(sig), int(clamp), _ptr(out))
         return out
+
+    def fuel_estimate1(self, i, trace, dt, m1, Cf):
+        """Section 5 fuel estimate 1 -> (mass series, wind residuals, flags)."""
+        tr = _f64(trace, (-1, 5))
+        K = tr.shape[0]
+        m, w = np.zeros(K), np.zeros((K, 2))
+        fl = lib().ora_fuel_estimate1(C.byref(self.p), i, _ptr(_f64(Cf, (2,))), _ptr(tr), K, float(dt), float(m1),
+                                      _ptr(m), _ptr(w))
+        return m, w, fl
+
+    def fuel_estimate2(self, i, trace, dt, m1, Cf):
+        """Section 5 fuel estimate 2 -> (mass series, flags)."""
+        tr = _f64(trace, (-1, 5))
+        K = tr.shape[0]
+        m = np.zeros(K)
+        fl = lib().ora_fuel_estimate2(C.byref(self.p), i, _ptr(_f64(Cf, (2,))), _ptr(tr), K, float(dt), float(m1),
+                                      _ptr(m))
+        return m, fl
 
     def perturb_row(self, i, row, l, k, seed, sigma, mpc=0, clamp=False):
         row = _f64(row, (self.H, 3))

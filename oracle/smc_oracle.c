@@ -899,3 +899,82 @@ void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *st
         if (ora_unary_violation(p, i, &u0[3 * i], nx)) flags[i] |= 4;
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Fuel estimates from recorded traces (section 5).    */
+/* ------------------------------------------------------------------------ */
+static double clamp_gamma(double sg, double gmax, int *flag)
+{
+    /* gamma = asin(dz / (dt v)); |sin gamma| > 1 (degenerate data) -> +-gamma_max (R47) */
+    if (sg > 1.0 || sg < -1.0 || sg != sg) { *flag = 1; return sg > 0.0 ? gmax : -gmax; }
+    return asin(sg);
+}
+
+static double wrap_pi(double d) { return d - 2.0 * M_PI * floor((d + M_PI) / (2.0 * M_PI)); }
+
+/* Fuel estimate 1: fly the recorded heading, match the next
+ * airspeed; the position mismatch is the wind residual.  Mass runs forward
+ * with eta = Cf1 (1 + v / Cf2) and T from the airspeed change (bank 0);
+ * negative burn is clamped to 0.  Returns flags (bit0 gamma clamped). */
+int ora_fuel_estimate1(const ora_problem *p, int i, const double *Cf, const double *trace, int K, double dt,
+                       double m1, double *m_out, double *w_out)
+{
+    int flags = 0;
+    double m = m1;
+    m_out[0] = m;
+    for (int k = 0; k + 1 < K; ++k) {
+        const double *a = &trace[5 * k], *b = &trace[5 * (k + 1)];
+        double vs = a[3];
+        double eta = Cf[0] * (1.0 + vs / Cf[1]);
+        int fl = 0;
+        double gam = clamp_gamma((b[2] - a[2]) / (dt * vs), p->gamma_max[i], &fl);
+        flags |= fl;
+        w_out[2 * k] = (b[0] - a[0]) / dt - vs * cos(a[4]) * cos(gam);
+        w_out[2 * k + 1] = (b[1] - a[1]) / dt - vs * sin(a[4]) * cos(gam);
+        double st[6] = { a[0], a[1], a[2], vs, a[4], m };
+        double L, D;
+        ora_lift_drag(p, i, st, 0.0, &L, &D);
+        double T = m * (b[3] - vs) / dt + D + m * p->g * sin(gam);
+        double burn = dt * eta * T;
+        if (burn < 0.0) burn = 0.0;
+        m -= burn;
+        m_out[k + 1] = m;
+    }
+    if (K >= 1) { w_out[2 * (K - 1)] = 0.0; w_out[2 * (K - 1) + 1] = 0.0; }
+    return flags;
+}
+
+/* Fuel estimate 2: dead reckoning, no wind.  Airspeed from the
+ * 3-D distance, track angle from the two positions, bank from the heading
+ * change; T from the airspeed change to the next sample.  A zero-distance
+ * interval burns nothing and is flagged (bit1).  Returns flags. */
+int ora_fuel_estimate2(const ora_problem *p, int i, const double *Cf, const double *trace, int K, double dt,
+                       double m1, double *m_out)
+{
+    int flags = 0;
+    double m = m1;
+    m_out[0] = m;
+    for (int k = 0; k + 1 < K; ++k) {
+        const double *a = &trace[5 * k], *b = &trace[5 * (k + 1)];
+        double dx = b[0] - a[0], dy = b[1] - a[1], dz = b[2] - a[2];
+        double d = sqrt(dx * dx + dy * dy + dz * dz);
+        if (!(d > 0.0)) { flags |= 2; m_out[k + 1] = m; continue; }
+        double vh = d / dt;
+        double eta = Cf[0] * (1.0 + vh / Cf[1]);
+        int fl = 0;
+        double gam = clamp_gamma(dz / (dt * vh), p->gamma_max[i], &fl);
+        flags |= fl;
+        double chih = atan2(dy, dx);                   /* tan^-1(dy/dx) on the full circle (R47) */
+        double dchi = wrap_pi(chih - a[4]);
+        double phi = atan(dchi * vh / (p->g * dt));
+        double st[6] = { a[0], a[1], a[2], vh, a[4], m };
+        double L, D;
+        ora_lift_drag(p, i, st, phi, &L, &D);
+        double T = m * (b[3] - vh) / dt + D + m * p->g * sin(gam);
+        double burn = dt * eta * T;
+        if (burn < 0.0) burn = 0.0;
+        m -= burn;
+        m_out[k + 1] = m;
+    }
+    return flags;
+}

@@ -180,6 +180,16 @@ void ora_plant_step(const ora_problem *p, const ora_derived *d, const double *st
                     const double *u0, uint64_t seed, uint32_t mpc, double *Zplant,
                     int32_t *zinit, double *next, int32_t *flags);
 
+/* Fuel estimates on a recorded trace (section 5): trace [K][5] =
+ * x, y, z, v_s, chi per sample at spacing dt, aircraft constants of problem
+ * aircraft i (drag polar, gamma_max, density), Cf = {Cf1, Cf2}.  m_out [K]
+ * mass series; w_out [K][2] wind residuals of estimate 1 (last row 0).
+ * Return flags: bit0 gamma clamped, bit1 zero-distance interval (estimate 2). */
+int ora_fuel_estimate1(const ora_problem *p, int i, const double *Cf, const double *trace, int K, double dt,
+                       double m1, double *m_out, double *w_out);
+int ora_fuel_estimate2(const ora_problem *p, int i, const double *Cf, const double *trace, int K, double dt,
+                       double m1, double *m_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -418,3 +418,67 @@ def test_dense_grid_field_statistics(ora):
     vals = np.array(vals)
     assert vals.mean() == pytest.approx(0.0, abs=4 * s_mid / math.sqrt(len(vals)))
     assert vals.var() == pytest.approx(s_mid ** 2, rel=0.08)
+
+
+# ---------------------------------------------------------------- fuel estimators (section 5, N4)
+def _fuel_forward(P, i, x0, T, gam, wind, dt, Cf):
+    """Forward Euler of Eq. hor with zero bank and eta(v) = Cf1 (1 + v/Cf2)
+    (P:709): the trace a recorder would see, and the true mass series."""
+    st = np.array(x0, float)
+    tr, ms = [st[:5].copy()], [st[5]]
+    for k in range(len(T)):
+        x, y, z, v, chi, m = st
+        _, D = P.lift_drag(i, st, 0.0)
+        eta = Cf[0] * (1.0 + v / Cf[1])
+        st = np.array([x + dt * (v * math.cos(chi) * math.cos(gam[k]) + wind[0]),
+                       y + dt * (v * math.sin(chi) * math.cos(gam[k]) + wind[1]),
+                       z + dt * v * math.sin(gam[k]),
+                       v + dt * ((T[k] - D) / m - 9.81 * math.sin(gam[k])),
+                       chi, m - dt * eta * T[k]])
+        tr.append(st[:5].copy())
+        ms.append(st[5])
+    return np.array(tr), np.array(ms)
+
+
+def test_fuel_estimate1_roundtrip(ora):
+    """Estimate 1 inverts the forward model: a trace simulated with known thrust and a
+    constant wind gives back the wind (residuals) and the mass series."""
+    scn = sc.snapshot(0, 1, seed=1)
+    scn["density_mode"] = 0
+    P = ora.Problem(scn)
+    rng = np.random.default_rng(2)
+    K, dt, Cf = 25, 60.0, (1.1e-5, 500.0)
+    T = rng.uniform(3e4, 9e4, K)
+    gam = rng.uniform(-0.03, 0.05, K)
+    tr, ms = _fuel_forward(P, 0, [-5000.0, 2000.0, 3000.0, 150.0, 0.7, 70000.0], T, gam, (4.5, -2.25), dt, Cf)
+    m, w, fl = P.fuel_estimate1(0, tr, dt, ms[0], Cf)
+    assert fl == 0
+    assert np.allclose(m, ms, rtol=1e-9, atol=0)
+    assert np.allclose(w[:-1], [4.5, -2.25], rtol=0, atol=1e-6)
+    assert np.all(w[-1] == 0.0)
+    # zero thrust: no burn (the estimate sees T = 0 up to rounding; negative burn clamped, P:755)
+    tr0, ms0 = _fuel_forward(P, 0, [0.0, 0.0, 3000.0, 150.0, 0.0, 70000.0], np.zeros(5), np.zeros(5), (0.0, 0.0), dt, Cf)
+    m0, _, _ = P.fuel_estimate1(0, tr0, dt, ms0[0], Cf)
+    assert np.allclose(m0, 70000.0, rtol=1e-12)
+
+
+def test_fuel_estimate2_properties(ora):
+    scn = sc.snapshot(0, 1, seed=1)
+    P = ora.Problem(scn)
+    dt, Cf = 60.0, (1.1e-5, 500.0)
+    # straight, level, constant speed, no wind: both estimates reduce to trimmed flight (S:580)
+    v, chi = 160.0, 0.4
+    tr = np.array([[k * dt * v * math.cos(chi), k * dt * v * math.sin(chi), 4000.0, v, chi] for k in range(6)])
+    m1, _, f1 = P.fuel_estimate1(0, tr, dt, 68000.0, Cf)
+    m2, f2 = P.fuel_estimate2(0, tr, dt, 68000.0, Cf)
+    assert f1 == 0 and f2 == 0
+    assert np.allclose(m2, m1, rtol=1e-12)
+    assert m1[-1] < 68000.0                                       # level flight burns fuel against drag
+    # circling: same position every sample -> zero-distance intervals flagged, no burn
+    circ = np.array([[1000.0, 2000.0, 3000.0, 140.0, 0.3 * k] for k in range(4)])
+    m3, f3 = P.fuel_estimate2(0, circ, dt, 68000.0, Cf)
+    assert f3 & 2 and np.all(m3 == 68000.0)
+    # implausible climb (dz > dt v): gamma clamped to gamma_max and flagged
+    bad = np.array([[0.0, 0.0, 0.0, 10.0, 0.0], [600.0, 0.0, 5000.0, 10.0, 0.0]])
+    _, _, f4 = P.fuel_estimate1(0, bad, dt, 68000.0, Cf)
+    assert f4 & 1
