@@ -281,6 +281,39 @@ void smc_shard_offsets(uint32_t N, int32_t world_size, int32_t rank, const uint6
  * (exact integer arithmetic): the slot boundary of CDF value C (R25). */
 uint64_t smc_slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L);
 
+/* ---------------- fuel estimates on recorded traces (section 5) ---------------- */
+/* Aircraft constants of one trace: drag polar (R12), fuel-flow coefficients
+ * eta = Cf1 (1 + v / Cf2) in kg/(N s) and m/s, and the |gamma|
+ * clamp for degenerate intervals (R47). */
+typedef struct {
+    double S, cd0, cd2, Cf1, Cf2, gamma_max;
+} smc_fuel_type;
+
+/* A batch of traces, every pointer DEVICE memory owned by the caller.
+ * trace[n][max_len][5] = x, y, z, v_s, chi per sample at spacing dt; len[n]
+ * samples used (>= 1).  Outputs: m1 / m2 [n][max_len] mass series of
+ * estimate 1 / 2, wres[n][max_len][2] estimate-1 wind
+ * residuals (0 in the last sample), fuel[n][2] total burn, flags[n] (bit0
+ * gamma clamped, bit1 zero-distance interval in estimate 2).  Negative burn is
+ * clamped to 0. */
+typedef struct {
+    uint32_t n_traces, max_len;
+    const uint32_t *len;
+    const double *trace;
+    const double *m0;
+    const smc_fuel_type *type;
+    double dt, g;
+    int32_t density_mode;      /* SMC_DENSITY_* */
+    double rho_const;
+    double *m1, *m2, *wres, *fuel;
+    uint32_t *flags;
+} smc_fuel_args;
+
+/* One thread per trace (sequential in time, independent across aircraft),
+ * FP64; ordered on `stream` (cudaStream_t, NULL = legacy default).  Errors:
+ * SMC_EINVAL for a NULL pointer or zero sizes, SMC_ECUDA on launch failure. */
+smc_status smc_fuel_estimates(const smc_fuel_args *args, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,13 @@ class Scenario(C.Structure):
     ]
 
 
+class FuelArgs(C.Structure):
+    _fields_ = [("n_traces", C.c_uint32), ("max_len", C.c_uint32), ("len", C.c_void_p), ("trace", C.c_void_p),
+                ("m0", C.c_void_p), ("type", C.c_void_p), ("dt", C.c_double), ("g", C.c_double),
+                ("density_mode", C.c_int32), ("rho_const", C.c_double), ("m1", C.c_void_p), ("m2", C.c_void_p),
+                ("wres", C.c_void_p), ("fuel", C.c_void_p), ("flags", C.c_void_p)]
+
+
 class Config(C.Structure):
     _fields_ = [
         ("n_particles", C.c_uint32), ("n_samples", C.c_uint32), ("schedule", C.c_uint32),
@@ -123,6 +130,7 @@ def load():
         "smc_shard_range": (None, [u32, C.c_int32, C.c_int32, P(u32), P(u32)]),
         "smc_shard_offsets": (None, [u32, C.c_int32, C.c_int32, P(u64), P(u64), P(u64)]),
         "smc_slot_count": (u64, [u64, u64, u64, u32]),
+        "smc_fuel_estimates": (st, [C.POINTER(FuelArgs), v]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -136,7 +144,7 @@ EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate"
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
             "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
-            "smc_shard_offsets", "smc_slot_count"]
+            "smc_shard_offsets", "smc_slot_count", "smc_fuel_estimates"]
 
 
 def _p(a, ct):
@@ -422,3 +430,33 @@ def shard_offsets(Q_all, rank):
 
 def slot_count(Cv, Q, R, L):
     return int(load().smc_slot_count(int(Cv), int(Q), int(R), int(L)))
+
+
+def fuel_estimates(traces, lens, m0, types, dt, g=9.81, density_mode=0, rho_const=1.225, device=0):
+    """Section-5 fuel estimates 1 and 2 for a batch of recorded traces on
+    the GPU (smc_fuel_estimates).  traces [n][max_len][5] (x, y, z, v_s, chi), lens [n],
+    m0 [n], types [n][6] (S, cd0, cd2, Cf1, Cf2, gamma_max).  Device memory comes from
+    torch; the arithmetic runs in k_fuel.  Returns a dict of numpy arrays."""
+    import torch
+    lib = load()
+    dev = torch.device("cuda", device)
+    tr = torch.as_tensor(np.ascontiguousarray(traces, dtype=np.float64), device=dev)
+    n, max_len = int(tr.shape[0]), int(tr.shape[1])
+    ln = torch.as_tensor(np.ascontiguousarray(lens, dtype=np.uint32).astype(np.int32), device=dev)
+    m0_t = torch.as_tensor(np.ascontiguousarray(m0, dtype=np.float64), device=dev)
+    ty = torch.as_tensor(np.ascontiguousarray(types, dtype=np.float64).reshape(n, 6), device=dev)
+    m1 = torch.zeros((n, max_len), dtype=torch.float64, device=dev)
+    m2 = torch.zeros_like(m1)
+    w = torch.zeros((n, max_len, 2), dtype=torch.float64, device=dev)
+    fuel = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+    flags = torch.zeros(n, dtype=torch.int32, device=dev)
+    a = FuelArgs(n, max_len, ln.data_ptr(), tr.data_ptr(), m0_t.data_ptr(), ty.data_ptr(), float(dt), float(g),
+                 int(density_mode), float(rho_const), m1.data_ptr(), m2.data_ptr(), w.data_ptr(), fuel.data_ptr(),
+                 flags.data_ptr())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = lib.smc_fuel_estimates(C.byref(a), C.c_void_p(stream))
+    if rc != SMC_OK:
+        raise SmcError(rc, "smc_fuel_estimates failed")
+    torch.cuda.synchronize(dev)
+    return {"m1": m1.cpu().numpy(), "m2": m2.cpu().numpy(), "wres": w.cpu().numpy(), "fuel": fuel.cpu().numpy(),
+            "flags": flags.cpu().numpy().astype(np.uint32)}

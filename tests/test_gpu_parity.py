@@ -513,3 +513,41 @@ def test_warm_start_init_parity(smc, use_graph):
     # a solve from the warm population runs (and the next window maps again)
     sol.mpc_step(scn2["x0"])
     sol.close()
+
+
+def test_fuel_estimates_parity(smc):
+    """Section-5 fuel estimates (N4) on 300 synthetic traces of ragged
+    length -- forward-simulated, circling and degenerate ones -- vs the oracle."""
+    scn = sc.snapshot(0, 1, seed=1)
+    P = O.Problem(scn)
+    rng = np.random.default_rng(8)
+    n, max_len, dt, Cf = 300, 40, 60.0, (1.1e-5, 500.0)
+    traces = np.zeros((n, max_len, 5))
+    lens = rng.integers(1, max_len + 1, n)
+    lens[:3] = [1, 2, max_len]
+    m0 = rng.uniform(55000, 75000, n)
+    for j in range(n):
+        K = int(lens[j])
+        st = np.array([rng.uniform(-2e4, 2e4), rng.uniform(-2e4, 2e4), rng.uniform(500, 8000),
+                       rng.uniform(90, 200), rng.uniform(-3, 3)])
+        for k in range(K):
+            traces[j, k] = st
+            if j % 50 == 7:                       # circling: no displacement
+                st = st.copy(); st[4] += 0.5
+                continue
+            st = st + [dt * st[3] * math.cos(st[4]) + rng.normal(0, 60), dt * st[3] * math.sin(st[4]) + rng.normal(0, 60),
+                       rng.normal(0, 150), rng.normal(0, 4), rng.normal(0, 0.1)]
+            if j % 50 == 11:                      # implausible climb
+                st[2] += 1e5
+    ty = np.array([scn["S"][0], scn["cd0"][0], scn["cd2"][0], Cf[0], Cf[1], scn["gamma_max"][0]])
+    out = smc.fuel_estimates(traces, lens, m0, np.tile(ty, (n, 1)), dt, g=scn["g"], density_mode=scn["density_mode"])
+    for j in range(n):
+        K = int(lens[j])
+        m1, w, f1 = P.fuel_estimate1(0, traces[j, :K], dt, m0[j], Cf)
+        m2, f2 = P.fuel_estimate2(0, traces[j, :K], dt, m0[j], Cf)
+        assert np.allclose(out["m1"][j, :K], m1, rtol=1e-12, atol=0), j
+        assert np.allclose(out["m2"][j, :K], m2, rtol=1e-12, atol=0), j
+        assert np.allclose(out["wres"][j, :K], w, rtol=1e-10, atol=1e-9), j
+        assert out["flags"][j] == (f1 | f2), j
+        assert out["fuel"][j, 0] == pytest.approx(m0[j] - m1[-1], rel=1e-12, abs=1e-9)
+    assert (out["flags"] & 2).any() and (out["flags"] & 1).any()
