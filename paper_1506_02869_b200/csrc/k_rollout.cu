@@ -85,6 +85,8 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
 // AR(1) state / node values (ZST, odd to spread segments over banks).
 __host__ __device__ constexpr int dense_vst(int G) { return 4 * ((2 * G + 3) / 4); }
 __host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 1; }
+// row stride of the transposed factor Qhat^T [G][QTS] (multiple of 4 for 16-byte rows, zero padded)
+__host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 4; }
 
 template <int W, int NC, bool DEBUG, bool DENSE>
 __global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
@@ -114,7 +116,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     const uint32_t k = args.k, mpc = *args.mpcp;
 
     if constexpr (DENSE) {
-        for (int q = tid; q < G * G; q += kBlock) s_Q[(q / G) * (G + 1) + q % G] = sc.Qf[q];
+        const int qts = dense_qts(G);
+        for (int q = tid; q < G * qts; q += kBlock) {
+            const int m = q / qts, r = q % qts;                 // s_Q[m][r] = Qhat[r][m]
+            s_Q[q] = r < G ? sc.Qf[r * G + m] : 0.0f;
+        }
     } else {
         if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Cq[tid];   // W = Cq Z: trilinear coefficients
     }
@@ -200,12 +206,25 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     sZs[e] = (t == 0) ? ve : fmaf(sc.a, sZs[e], sc.b * ve);
                 }
                 __syncwarp();
-                for (int e = lane; e < G2; e += W) {
-                    const int comp = e >= G ? 1 : 0, r = e - comp * G;
-                    const float *zc = sZs + comp * G, *qr = s_Q + r * (G + 1);
-                    float acc = 0.0f;
-                    for (int m = 0; m <= r; ++m) acc = fmaf(qr[m], zc[m], acc);
-                    sWs[e] = acc;
+                // four consecutive rows per task from the transposed factor: one 16-byte load of
+                // Qhat^T[m][r0..r0+3] and one (segment-broadcast) load of Z[m] per 4 FMAs
+                const int nq = (G + 3) >> 2;
+                for (int task = lane; task < 2 * nq; task += W) {
+                    const int comp = task >= nq ? 1 : 0, r0 = 4 * (task - comp * nq);
+                    const float *zc = sZs + comp * G;
+                    const int mend = min(r0 + 4, G);             // Qhat lower triangular: m <= r
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int m = 0; m < mend; ++m) {
+                        const float4 q4 = *reinterpret_cast<const float4 *>(&s_Q[m * dense_qts(G) + r0]);
+                        const float zm = zc[m];
+                        acc.x = fmaf(q4.x, zm, acc.x); acc.y = fmaf(q4.y, zm, acc.y);
+                        acc.z = fmaf(q4.z, zm, acc.z); acc.w = fmaf(q4.w, zm, acc.w);
+                    }
+                    float *wo = sWs + comp * G + r0;
+                    wo[0] = acc.x;
+                    if (r0 + 1 < G) wo[1] = acc.y;
+                    if (r0 + 2 < G) wo[2] = acc.z;
+                    if (r0 + 3 < G) wo[3] = acc.w;
                 }
                 __syncwarp();
             } else {
@@ -526,7 +545,7 @@ size_t rollout_smem_bytes(int W, int NC, int H, int ng) {
         const size_t zs = ((size_t)SEGS * dense_zst(ng) + 3) & ~(size_t)3;
         return sizeof(float4) * ((size_t)H * NC * kBlock) +
                sizeof(float) * ((size_t)SEGS * dense_vst(ng) + SEGS * dense_zst(ng) + zs) +
-               sizeof(float4) * NC * kBlock + sizeof(float) * (size_t)ng * (ng + 1) + 16;
+               sizeof(float4) * NC * kBlock + sizeof(float) * (size_t)ng * dense_qts(ng) + 16;
     }
     const int GB = (W >= 8) ? W / 4 : 1;
     return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * (SEGS * GB * 16 + 2 * SEGS * 16) +
