@@ -129,6 +129,7 @@ def _declare(L):
         "ora_fuel_estimate2": (C.c_int, [P(_Problem), C.c_int, _dp, _dp, C.c_int, d, d, _dp]),
         "ora_init_population_warm": (None, [P(_Problem), u32, u64, u32, _dp, _ip, u32, _dp, C.c_int, _dp]),
         "ora_mh_accept": (C.c_int, [d, d, u32, u32, u64, u32]),
+        "ora_mh_accept_aircraft": (C.c_int, [d, d, u32, u32, u32, u64, u32]),
         "ora_resample_column": (C.c_int, [_dp, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
         "ora_resample_column_m": (C.c_int, [_dp, u32, u32, u32, u32, u64, u32, _ip, P(u64), P(u64), P(u64)]),
         "ora_particles_of": (u32, [u32, u32, u32, u32]),
@@ -416,6 +417,10 @@ def angdist(d):
 
 def mh_accept(lam_cur, lam_prop, l, k, seed, mpc=0):
     return bool(lib().ora_mh_accept(float(lam_cur), float(lam_prop), l, k, seed, mpc))
+
+
+def mh_accept_aircraft(ell_cur, ell_prop, l, i, k, seed, mpc=0):
+    return bool(lib().ora_mh_accept_aircraft(float(ell_cur), float(ell_prop), l, i, k, seed, mpc))
 
 
 def resample_column(ell, i, k, seed, mpc=0, M=None):

@@ -599,6 +599,23 @@ void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32
             }
 }
 
+/* Per-aircraft MH acceptance (SURVEY Q1 variant / N2, reading R46): the
+ * joint rules of ora_mh_accept applied to one aircraft's log2 weights, with
+ * the uniform from the MH stream at counter (l, k<<16, i). */
+int ora_mh_accept_aircraft(double ell_cur, double ell_prop, uint32_t l, uint32_t i, uint32_t k, uint64_t seed,
+                           uint32_t mpc)
+{
+    if (ell_cur == -INFINITY) return 1;
+    if (ell_prop == -INFINITY) return 0;
+    double delta = ell_prop - ell_cur;
+    if (delta >= 0.0) return 1;
+    uint32_t w[4];
+    draw(TAG_MH, l, k << 16, i, mpc, seed, w);
+    uint64_t r = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+    double u53 = (double)(r >> 11) * 0x1.0p-53;
+    return u53 < ora_det_exp2(delta);
+}
+
 /* Warm start across MPC steps (reading R45): the previous
  * winner, shifted one step (row t <- row t+1, last row repeated), seeds the
  * first Lw particles of aircraft that were in the previous window; particle 0
@@ -767,6 +784,8 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
     double *ell_p = (double *)malloc(sizeof(double) * (L * (size_t)n + 1));
     double *ell_s = (double *)malloc(sizeof(double) * (L * (size_t)n + 1));
     double *lam = (double *)malloc(sizeof(double) * (L + 1));
+    double *lam_c = (double *)malloc(sizeof(double) * (L + 1));
+    double *lam_p = (double *)malloc(sizeof(double) * (L + 1));
     double *col = (double *)malloc(sizeof(double) * (L + 1));
     int32_t *anc = (int32_t *)malloc(sizeof(int32_t) * ((size_t)L * n + 1));
 
@@ -787,6 +806,22 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
             ora_evaluate(p, &d, prop, Lk, S, k, cfg->seed, cfg->mpc, ell_s, cfg->nthreads);
             memcpy(surv, prop, sizeof(double) * Lk * row);
             accepted = Lk;
+        } else if (cfg->mh == 2) {                                  /* per-aircraft MH (R46) */
+            for (size_t e = 0; e < Lk * (size_t)n; ++e) { ell_c[e] = ell0; ell_p[e] = ell0; }
+            ora_evaluate(p, &d, cur, Lk, S, k, cfg->seed, cfg->mpc, ell_c, cfg->nthreads);
+            ora_evaluate(p, &d, prop, Lk, S, k, cfg->seed, cfg->mpc, ell_p, cfg->nthreads);
+            for (uint32_t l = 0; l < Lk; ++l) {
+                lam_c[l] = lambda_of(&ell_c[(size_t)l * n], n);
+                lam_p[l] = lambda_of(&ell_p[(size_t)l * n], n);
+                for (int i = 0; i < n; ++i) {
+                    const size_t e = (size_t)l * n + i;
+                    int acc = ora_mh_accept_aircraft(ell_c[e], ell_p[e], l, (uint32_t)i, k, cfg->seed, cfg->mpc);
+                    accepted += acc;
+                    const size_t o = (size_t)l * row + (size_t)i * H * 3;
+                    memcpy(&surv[o], acc ? &prop[o] : &cur[o], sizeof(double) * H * 3);
+                    ell_s[e] = acc ? ell_p[e] : ell_c[e];
+                }
+            }
         } else {
             for (size_t e = 0; e < Lk * (size_t)n; ++e) { ell_c[e] = ell0; ell_p[e] = ell0; }
             ora_evaluate(p, &d, cur, Lk, S, k, cfg->seed, cfg->mpc, ell_c, cfg->nthreads);
@@ -839,17 +874,37 @@ int ora_run_smc(const ora_problem *p, const ora_smc_cfg *cfg, double *best_ctrl,
         if (stats) {
             int64_t b = ora_select(lam, Lk);
             stats[4 * k + 0] = b >= 0 ? lam[b] : -INFINITY;
-            stats[4 * k + 1] = k == 0 ? 1.0 : (double)accepted / (double)Lk;
+            stats[4 * k + 1] = k == 0 ? 1.0 : (double)accepted / ((double)Lk * (cfg->mh == 2 ? n : 1));
             stats[4 * k + 2] = ess_min;
             stats[4 * k + 3] = (double)n_inf;
         }
     }
-    int64_t b = ora_select(lam, Lk);                                 /* Alg.1 l.27 */
-    if (best_index) *best_index = b;
-    if (best_lambda) *best_lambda = b >= 0 ? lam[b] : -INFINITY;
-    if (best_ctrl && b >= 0) memcpy(best_ctrl, &surv[(size_t)b * row], sizeof(double) * row);
+    int64_t b;
+    if (cfg->mh == 2 && cfg->K >= 2) {
+        /* per-aircraft survivors mix two joint evaluations; the pick is made over
+         * the jointly evaluated candidates of the last round: lambda of x'_l and x*_l, ties ->
+         * lowest l, then x' before x* (R46) */
+        int64_t bc = -1;
+        double bl = -INFINITY;
+        for (uint32_t l = 0; l < Lk; ++l)
+            for (int c = 0; c < 2; ++c) {
+                double v = c ? lam_p[l] : lam_c[l];
+                if (v == -INFINITY) continue;
+                if (bc < 0 || v > bl) { bl = v; bc = 2 * (int64_t)l + c; }
+            }
+        b = bc >= 0 ? bc / 2 : -1;
+        if (best_index) *best_index = b;
+        if (best_lambda) *best_lambda = bl;
+        if (best_ctrl && bc >= 0) memcpy(best_ctrl, (bc & 1) ? &prop[(size_t)b * row] : &cur[(size_t)b * row],
+                                         sizeof(double) * row);
+    } else {
+        b = ora_select(lam, Lk);                                     /* Alg.1 l.27 */
+        if (best_index) *best_index = b;
+        if (best_lambda) *best_lambda = b >= 0 ? lam[b] : -INFINITY;
+        if (best_ctrl && b >= 0) memcpy(best_ctrl, &surv[(size_t)b * row], sizeof(double) * row);
+    }
     free(cur); free(prop); free(surv); free(ell_c); free(ell_p); free(ell_s);
-    free(lam); free(col); free(anc);
+    free(lam); free(lam_c); free(lam_p); free(col); free(anc);
     ora_free_derived(&d);
     return b >= 0 ? 0 : 2;
 }

@@ -131,6 +131,11 @@ void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl
 void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,
                          double *ctrl);
 
+/* Per-aircraft MH acceptance (R46): joint rules on one aircraft's log2 weights,
+ * uniform from the MH stream at counter (l, k<<16, i). Returns 1 = accept x*_i. */
+int ora_mh_accept_aircraft(double ell_cur, double ell_prop, uint32_t l, uint32_t i, uint32_t k, uint64_t seed,
+                           uint32_t mpc);
+
 /* Warm start (R45): first Lw particles from the shifted previous winner. */
 void ora_init_population_warm(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,
                               const double *prev, const int32_t *has_prev, uint32_t Lw,
@@ -162,7 +167,7 @@ int64_t ora_select(const double *lam, uint32_t L);
 /* Full Alg.1 (+ MH move, R1) for K rounds.  best_ctrl: [n][H][3].
  * stats (nullable): per round {best_lambda, accept_rate, ess_min, n_infeasible}. */
 typedef struct {
-    uint32_t L, S, K, sched_paper, mh, clamp;
+    uint32_t L, S, K, sched_paper, mh, clamp;   /* mh: 0 paper Alg.1, 1 joint MH (R1), 2 per-aircraft (R46) */
     double sigma[3], anneal;
     uint64_t seed;
     uint32_t mpc;

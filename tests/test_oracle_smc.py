@@ -379,3 +379,36 @@ def test_warm_start_init(ora):
     for i in (0, 2):
         assert np.all(wc[:, i, :, 0] <= scn["T_max"][i]) and np.all(wc[:, i, :, 0] >= scn["T_min"][i])
         assert np.all(np.abs(wc[:, i, :, 1]) <= scn["phi_max"][i]) and np.all(np.abs(wc[:, i, :, 2]) <= scn["gamma_max"][i])
+
+
+def test_mh_accept_aircraft_rules(ora):
+    """R46: the joint rules (R1) on one aircraft's weights; acceptance frequency 2^Delta."""
+    import numpy as np
+    inf = float("inf")
+    assert ora.mh_accept_aircraft(-inf, -inf, 3, 1, 2, 9)
+    assert not ora.mh_accept_aircraft(-5.0, -inf, 3, 1, 2, 9)
+    assert ora.mh_accept_aircraft(-5.0, -5.0, 3, 1, 2, 9)
+    acc = np.mean([ora.mh_accept_aircraft(-3.0, -4.0, l, 2, 5, 11) for l in range(20000)])
+    assert abs(acc - 0.5) < 0.02
+    # aircraft index enters the counter: decisions of different aircraft are not copies
+    a = [ora.mh_accept_aircraft(-3.0, -4.0, l, 0, 5, 11) for l in range(2000)]
+    b = [ora.mh_accept_aircraft(-3.0, -4.0, l, 1, 5, 11) for l in range(2000)]
+    assert a != b
+    # aircraft 0 uses the joint stream's counter: same decision as the joint rule on equal values
+    assert all(ora.mh_accept_aircraft(-3.0, -3.7, l, 0, 4, 13) == ora.mh_accept(-3.0, -3.7, l, 4, 13)
+               for l in range(500))
+
+
+def test_per_aircraft_mh_single_aircraft_reduces_to_joint(ora):
+    """With one aircraft the per-aircraft move is the joint move (same decisions, same
+    survivors): identical round statistics; its final pick over both candidates can
+    only be at least as good."""
+    import numpy as np
+    from paper_1506_02869_b200 import scenarios as sc
+    scn = sc.small(n_arr=1, n_dep=0, H=6, seed=3)
+    P = ora.Problem(scn)
+    sig = (0.05 * 1.2e5, 0.035, 0.0087)
+    r1 = P.run_smc(128, 3, 5, 77, sig, mh=1)
+    r2 = P.run_smc(128, 3, 5, 77, sig, mh=2)
+    assert np.array_equal(r1["stats"], r2["stats"])
+    assert r2["best_lambda"] >= r1["best_lambda"]
