@@ -111,7 +111,9 @@ typedef struct {
     uint32_t n_samples;        /* S per round for SMC_SCHED_CONST (Alg.1 l.7)         */
     uint32_t schedule;         /* SMC_SCHED_*                                         */
     uint32_t n_rounds;         /* K rounds per mpc_step (J_max + 1)     */
-    uint32_t mh;               /* 1: Metropolis-Hastings move (R1); 0: Alg.1 l.23     */
+    uint32_t mh;               /* 0: Alg.1 l.23 as printed; 1: joint Metropolis-Hastings
+                                  move (R1); 2: per-aircraft acceptance (R46) with the
+                                  final pick over the jointly evaluated candidates     */
     uint32_t clamp_proposals;  /* 1: clamp perturbed controls to the envelope (R16)   */
     double sigma[3];           /* perturbation std (T, phi, gamma)     */
     double anneal;             /* sigma_k = sigma * anneal^k                          */
@@ -243,6 +245,12 @@ smc_status smc_debug_evaluate(smc_ctx *ctx, const float *controls, uint32_t L, u
 smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_prop, uint32_t L,
                         uint32_t k, uint8_t *acc);
 
+/* Per-aircraft MH decisions (R46) on injected log2 weights ell_cur / ell_prop
+ * [L][N] (host float) with the production device function -> mask[L] (bit i =
+ * accept x*_i). */
+smc_status smc_debug_mh_aircraft(smc_ctx *ctx, const float *ell_cur, const float *ell_prop, uint32_t L,
+                                 uint32_t N, uint32_t k, uint32_t *mask);
+
 /* Per-aircraft systematic resampling (R25) of injected log2 weights
  * ell[N][L] (host float) into M new particles (M = 0 means L) with the
  * production kernels -> anc[N][M] (host int32).  Q[N] (nullable) receives the
@@ -259,11 +267,11 @@ smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, const int32_t
 /* Device population after the last call, packed for the Lk particles the
  * last round evaluated (Lk = L unless n_particles_final shrinks it; written
  * to *n_eval, nullable; buffers are sized for L): ctrl_cur / ctrl_prop
- * [Lk][N][H][3] of the last evaluated pair, surv[Lk] (0 = resampled kept,
- * 1 = proposal accepted), ell_surv[N][Lk], lam_surv[Lk], lam_cand[2][Lk]
+ * [Lk][N][H][3] of the last evaluated pair, surv[Lk] survivor masks (bit i
+ * set = aircraft i's row is the proposal x*; joint MH: all bits alike), ell_surv[N][Lk], lam_surv[Lk], lam_cand[2][Lk]
  * (joint log2 weight of both MH candidates as the kernel computed them;
  * round 0 / mh=0: only [0] is meaningful).  Any pointer may be NULL. */
-smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
+smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint32_t *surv,
                                 float *ell_surv, double *lam_surv, double *lam_cand, uint32_t *n_eval);
 
 /* ---------------- multi-GPU partition helpers (pure host, no GPU) ---------- */

@@ -95,7 +95,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.ell = take((size_t)nmax * Lloc * sizeof(float));
     o.lam = take((size_t)Lloc * sizeof(double));
     o.lam2 = take(2 * (size_t)Lloc * sizeof(double));
-    o.surv = take(Lloc);
+    o.surv = take((size_t)Lloc * sizeof(uint32_t));
     o.colmax = take(nmax * sizeof(uint32_t));
     o.Q = take(nmax * sizeof(unsigned long long));
     o.ess = take(2 * nmax * sizeof(double));
@@ -158,7 +158,8 @@ struct smc_ctx {
     size_t part_cap = 0;
     int nsm = 148, bps[2] = {0, 0};
     double *lam = nullptr, *lam2 = nullptr;
-    uint8_t *surv = nullptr;
+    uint32_t *surv = nullptr;          // survivor masks (bit i: aircraft i's row from x*)
+    int last_nc = 1;                   // candidates evaluated by the last round
     uint32_t *colmax = nullptr, *tiles = nullptr;
     unsigned long long *Q = nullptr, *status = nullptr, *accept = nullptr, *C = nullptr, *QR = nullptr;
     double *ess = nullptr;
@@ -343,7 +344,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->world = world;
     ctx->rank = cfg->rank;
     if (cfg->n_particles == 0 || cfg->max_aircraft == 0 || cfg->max_aircraft > 32 || cfg->max_horizon == 0 ||
-        cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30)) {
+        cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30) ||
+        cfg->mh > 2) {
         delete ctx;
         return SMC_EINVAL;
     }
@@ -390,7 +392,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
     ctx->lam = (double *)(ws + L.lam);
     ctx->lam2 = (double *)(ws + L.lam2);
-    ctx->surv = (uint8_t *)(ws + L.surv);
+    ctx->surv = (uint32_t *)(ws + L.surv);
     ctx->colmax = (uint32_t *)(ws + L.colmax);
     ctx->Q = (unsigned long long *)(ws + L.Q);
     ctx->ess = (double *)(ws + L.ess);
@@ -791,12 +793,14 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     RolloutArgs ra{};
     int NC;
     if (k == 0) {
-        NC = 1; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = nullptr; ra.surv_single = 0;
+        NC = 1; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = nullptr; ra.surv_single = 0u;
     } else if (ctx->cfg.mh) {
-        NC = 2; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = ctx->ctrl[P][1]; ra.surv_single = 0;
+        NC = 2; ra.ctrl[0] = ctx->ctrl[P][0]; ra.ctrl[1] = ctx->ctrl[P][1]; ra.surv_single = 0u;
     } else {
-        NC = 1; ra.ctrl[0] = ctx->ctrl[P][1]; ra.ctrl[1] = nullptr; ra.surv_single = 1;
+        NC = 1; ra.ctrl[0] = ctx->ctrl[P][1]; ra.ctrl[1] = nullptr; ra.surv_single = 0xFFFFFFFFu;
     }
+    ra.mh_mode = ctx->cfg.mh == 2 ? 2 : 1;
+    ctx->last_nc = NC;
     const uint32_t Lk = particles_of(ctx, k), Ln = particles_of(ctx, k + 1);
     ra.L = Lk; ra.l0 = ctx->l0; ra.S = S; ra.k = k; ra.mpcp = ctx->mpc_dev;
     ra.ell0 = (float)(-std::log2((double)(ctx->Lfinal ? Lk : ctx->Lg)));
@@ -874,7 +878,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
                 CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
                 LAUNCHP(PH_RESAMPLE, launch_scan(rr, ctx->st));
                 LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0] + (size_t)b * rowlen,
-                                                             ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b,
+                                                             ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b, n,
                                                              rowlen, ctx->Sall + (size_t)r * ctx->Lmax * rowlen, ctx->st));
             }
             for (int r = 0; r < G; ++r) {
@@ -892,7 +896,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         } else if (ctx->world > 1) {
             // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
             NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
-            LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc,
+            LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc, n,
                                                          n * H * 3, ctx->Sc, ctx->st));
             NCK(nccl_api()->AllGather(ctx->Sc, ctx->Sall, (size_t)ctx->Lmax * n * H * 3, ncclFloat32_, ctx->comm, ctx->st));
             MultiArgs ma{pa, ctx->Lg, ctx->Lmax, ctx->world, ctx->Call, ctx->Sall};
@@ -910,7 +914,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         CK(d2h(ctx, &bl, ctx->best_lam, 8));
         CK(cudaStreamSynchronize(ctx->st));
         stats->best_lambda = bl;
-        stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / Lk : 1.0);
+        stats->accept_rate = (k == 0) ? 1.0 : (ctx->cfg.mh ? (double)acc / ((double)Lk * (ctx->cfg.mh == 2 ? n : 1)) : 1.0);
         double em = INFINITY;
         uint32_t lo = 0, hi = 0;
         for (int i = 0; i < n; ++i) {
@@ -943,6 +947,8 @@ extern "C" smc_status smc_iterate(smc_ctx *ctx, uint32_t n_rounds, smc_round_sta
 static smc_status select_best(smc_ctx *ctx) {
     if (ctx->last_eval < 0) return fail(ctx, SMC_ESTATE, "no evaluated population");
     const int P = ctx->last_eval;
+    // per-aircraft MH (R46): survivors mix two joint evaluations -> pick among the candidates
+    const bool cand = ctx->cfg.mh == 2 && ctx->last_nc == 2;
     if (ctx->vworld > 1) {                // virtual ranks: per-shard records, then the multi-GPU merge
         const int rowlen = ctx->dsc.n * ctx->dsc.H * 3;
         for (int r = 0; r < ctx->vworld; ++r) {
@@ -952,7 +958,7 @@ static smc_status select_best(smc_ctx *ctx) {
             SelectArgs sr{e - b, b, ctx->dsc.n, ctx->dsc.H, ctx->lam + b, ctx->surv + b,
                           {ctx->ctrl[P][0] + (size_t)b * rowlen, ctx->ctrl[P][1] + (size_t)b * rowlen},
                           ctx->part_lam, ctx->part_idx, ctx->done, (double *)rec, (long long *)(rec + 8),
-                          (float *)(rec + 16)};
+                          (float *)(rec + 16), cand ? ctx->lam2 + b : nullptr, ctx->Lloc};
             LAUNCH(launch_select(sr, ctx->st));
         }
         LAUNCH(launch_select_merge(ctx->rec_all, ctx->vworld, ctx->rec_bytes, rowlen, ctx->rec_final, ctx->st));
@@ -960,7 +966,8 @@ static smc_status select_best(smc_ctx *ctx) {
     }
     SelectArgs sa{ctx->Leval ? ctx->Leval : ctx->Lloc, ctx->l0, ctx->dsc.n, ctx->dsc.H, ctx->lam, ctx->surv,
                   {ctx->ctrl[P][0], ctx->ctrl[P][1]},
-                  ctx->part_lam, ctx->part_idx, ctx->done, ctx->sel_lam, ctx->sel_idx, ctx->sel_row};
+                  ctx->part_lam, ctx->part_idx, ctx->done, ctx->sel_lam, ctx->sel_idx, ctx->sel_row,
+                  cand ? ctx->lam2 : nullptr, ctx->Leval ? ctx->Leval : ctx->Lloc};
     LAUNCH(launch_select(sa, ctx->st));
     if (ctx->world > 1) {                 // all-gather the per-rank records, merge on every rank
         NCK(nccl_api()->AllGather(ctx->rec_local, ctx->rec_all, ctx->rec_bytes, ncclUint8_, ctx->comm, ctx->st));
@@ -1132,7 +1139,7 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     float *dctrl = tmp.alloc<float>(nrow);
     float *dell = tmp.alloc<float>((size_t)n * L);
     double *dlam = tmp.alloc<double>(L);
-    uint8_t *dsurv = tmp.alloc<uint8_t>(L);
+    uint32_t *dsurv = tmp.alloc<uint32_t>(L);
     uint32_t *dcm = tmp.alloc<uint32_t>(n);
     unsigned long long *dacc = tmp.alloc<unsigned long long>(1);
     const size_t nu = (size_t)L * S * n;
@@ -1204,6 +1211,24 @@ extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const do
     return SMC_OK;
 }
 
+extern "C" smc_status smc_debug_mh_aircraft(smc_ctx *ctx, const float *ell_cur, const float *ell_prop, uint32_t L,
+                                            uint32_t N, uint32_t k, uint32_t *mask) {
+    if (!ctx || !ell_cur || !ell_prop || !mask || N == 0 || N > 32) return SMC_EINVAL;
+    DevTmp tmp;
+    float *a = tmp.alloc<float>((size_t)L * N), *b = tmp.alloc<float>((size_t)L * N);
+    uint32_t *o = tmp.alloc<uint32_t>(L);
+    if (!a || !b || !o) return fail(ctx, SMC_ECUDA, "debug allocation failed");
+    CK(cudaMemcpyAsync(a, ell_cur, sizeof(float) * L * N, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(b, ell_prop, sizeof(float) * L * N, cudaMemcpyHostToDevice, ctx->st));
+    const uint32_t key0 = (uint32_t)ctx->cfg.seed, key1 = (uint32_t)(ctx->cfg.seed >> 32);
+    smc_status s0 = sync_mpc(ctx);
+    if (s0 != SMC_OK) return s0;
+    LAUNCH(launch_mh_aircraft_debug(a, b, L, (int)N, k, ctx->mpc_dev, key0, key1, o, ctx->st));
+    CK(cudaMemcpyAsync(mask, o, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return SMC_OK;
+}
+
 extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_t N, uint32_t L, uint32_t M,
                                          uint32_t k, int32_t *anc, uint64_t *Q) {
     if (!ctx || !ell || !anc || N == 0 || N > 32 || L == 0 || L >= (1u << 30)) return SMC_EINVAL;
@@ -1251,11 +1276,11 @@ extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, co
     DevTmp tmp;
     float *src = tmp.alloc<float>(nrow), *dxp = tmp.alloc<float>(nrow), *dxs = tmp.alloc<float>(nrow);
     int32_t *danc = tmp.alloc<int32_t>((size_t)n * L);
-    uint8_t *dsurv = tmp.alloc<uint8_t>(L);
+    uint32_t *dsurv = tmp.alloc<uint32_t>(L);
     if (!src || !dxp || !dxs || !danc || !dsurv) return fail(ctx, SMC_ECUDA, "debug allocation failed");
     CK(cudaMemcpyAsync(src, surv_ctrl, sizeof(float) * nrow, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemcpyAsync(danc, anc, sizeof(int32_t) * n * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
-    CK(cudaMemsetAsync(dsurv, 0, L, ctx->st));
+    CK(cudaMemsetAsync(dsurv, 0, sizeof(uint32_t) * L, ctx->st));
     ProposeArgs pa{};
     smc_status s0 = sync_mpc(ctx);
     if (s0 != SMC_OK) return s0;
@@ -1273,7 +1298,7 @@ extern "C" smc_status smc_debug_propose(smc_ctx *ctx, const float *surv_ctrl, co
     return SMC_OK;
 }
 
-extern "C" smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint8_t *surv,
+extern "C" smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float *ctrl_prop, uint32_t *surv,
                                            float *ell_surv, double *lam_surv, double *lam_cand, uint32_t *n_eval) {
     if (!ctx) return SMC_EINVAL;
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
@@ -1284,7 +1309,7 @@ extern "C" smc_status smc_debug_population(smc_ctx *ctx, float *ctrl_cur, float 
     if (n_eval) *n_eval = (uint32_t)Lk;
     if (ctrl_cur) CK(cudaMemcpyAsync(ctrl_cur, ctx->ctrl[P][0], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
     if (ctrl_prop) CK(cudaMemcpyAsync(ctrl_prop, ctx->ctrl[P][1], sizeof(float) * nrow, cudaMemcpyDeviceToHost, ctx->st));
-    if (surv) CK(cudaMemcpyAsync(surv, ctx->surv, Lk, cudaMemcpyDeviceToHost, ctx->st));
+    if (surv) CK(cudaMemcpyAsync(surv, ctx->surv, sizeof(uint32_t) * Lk, cudaMemcpyDeviceToHost, ctx->st));
     if (ell_surv) CK(cudaMemcpyAsync(ell_surv, ctx->ell, sizeof(float) * n * Lk, cudaMemcpyDeviceToHost, ctx->st));
     if (lam_surv) CK(cudaMemcpyAsync(lam_surv, ctx->lam, sizeof(double) * Lk, cudaMemcpyDeviceToHost, ctx->st));
     if (lam_cand) CK(cudaMemcpyAsync(lam_cand, ctx->lam2, 2 * sizeof(double) * Lk, cudaMemcpyDeviceToHost, ctx->st));

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
                     const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
                     a = find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
                 }
-                src = p.src[__ldg(&p.surv[a])] + ((size_t)a * p.n + i) * H * 3;
+                src = p.src[(__ldg(&p.surv[a]) >> i) & 1u] + ((size_t)a * p.n + i) * H * 3;
             }
             s_src[threadIdx.x] = src;
         }
@@ -383,12 +383,16 @@ int select_blocks(uint32_t L) {
     return b < 1 ? 1 : (b > 512 ? 512 : b);
 }
 
+// Keys: survivors l -> l0 + l; per-aircraft MH (lam2 != NULL) candidates (l, c) -> 2 (l0 + l) + c,
+// so ties go to the lowest particle, then x' before x* (R27, R46).
 __global__ void k_select(const SelectArgs s) {
     double bl = -INFINITY;
     long long bi = -1;
-    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < s.L; l += gridDim.x * blockDim.x) {
-        const double v = s.lam[l];
-        if (v != -INFINITY && better(v, (long long)(s.l0 + l), bl, bi)) { bl = v; bi = (long long)(s.l0 + l); }
+    const uint32_t ne = s.lam2 ? 2 * s.L : s.L;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+        const double v = s.lam2 ? s.lam2[(e & 1u) * s.lam2_stride + (e >> 1)] : s.lam[e];
+        const long long key = s.lam2 ? 2 * (long long)(s.l0 + (e >> 1)) + (e & 1u) : (long long)(s.l0 + e);
+        if (v != -INFINITY && better(v, key, bl, bi)) { bl = v; bi = key; }
     }
     for (int o = 16; o; o >>= 1) {
         const double ol = __shfl_xor_sync(0xffffffffu, bl, o);
@@ -422,15 +426,16 @@ __global__ void k_select(const SelectArgs s) {
             if (better(pl, pi, gl, gi)) { gl = pl; gi = pi; }
         }
         s.best_lam[0] = gl;
-        s.best_idx[0] = gi;
+        s.best_idx[0] = (s.lam2 && gi >= 0) ? gi >> 1 : gi;   // reported: particle index
         s_win = gi;
         *s.done_ctr = 0u;
     }
     __syncthreads();
     const long long gi = s_win;
     if (gi < 0) return;
-    const uint32_t ll = (uint32_t)(gi - s.l0);
-    const float *src = s.src[s.surv[ll]] + (size_t)ll * s.n * s.H * 3;
+    const uint32_t ll = (uint32_t)((s.lam2 ? gi >> 1 : gi) - s.l0);
+    const int cbuf = s.lam2 ? (int)(gi & 1) : (int)(s.surv[ll] & 1u);
+    const float *src = s.src[cbuf] + (size_t)ll * s.n * s.H * 3;
     for (int e = threadIdx.x; e < s.n * s.H * 3; e += blockDim.x) s.best_row[e] = src[e];
 }
 
@@ -596,6 +601,26 @@ __global__ void k_mh_debug(const double *lc, const double *lp, uint32_t L, uint3
     if (l < L) acc[l] = mh_decide(lc[l], lp[l], l, k, *mpcp, key0, key1) ? 1 : 0;
 }
 
+__global__ void k_mh_aircraft_debug(const float *ec, const float *ep, uint32_t L, int n, uint32_t k,
+                                    const uint32_t *mpcp, uint32_t key0, uint32_t key1, uint32_t *mask) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    uint32_t m = 0u;
+    for (int i = 0; i < n; ++i)
+        if (mh_decide_aircraft((double)ec[(size_t)l * n + i], (double)ep[(size_t)l * n + i], l, (uint32_t)i, k, *mpcp,
+                               key0, key1))
+            m |= 1u << i;
+    mask[l] = m;
+}
+
+cudaError_t launch_mh_aircraft_debug(const float *ec, const float *ep, uint32_t L, int n, uint32_t k,
+                                     const uint32_t *mpcp, uint32_t key0, uint32_t key1, uint32_t *mask,
+                                     cudaStream_t st) {
+    if (!L) return cudaSuccess;
+    k_mh_aircraft_debug<<<(L + 255) / 256, 256, 0, st>>>(ec, ep, L, n, k, mpcp, key0, key1, mask);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,
                             uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st) {
     if (!L) return cudaSuccess;
@@ -633,22 +658,24 @@ __host__ __device__ static inline uint32_t shard_begin(uint32_t L, int G, int r)
 }
 
 // Compact this rank's survivor rows (x' or x* per survivor flag) for the all-gather.
-__global__ void k_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+__global__ void k_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
                                     int rowlen, float *out) {
     const size_t total = (size_t)Lloc * rowlen;
+    const int arow = rowlen / n;                         // H * 3 floats per aircraft
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
         const uint32_t l = (uint32_t)(e / rowlen);
-        out[e] = (surv[l] ? xs : xp)[e];
+        const int i = (int)((e % rowlen) / arow);
+        out[e] = (((surv[l] >> i) & 1u) ? xs : xp)[e];
     }
 }
 
-cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
                                      int rowlen, float *out, cudaStream_t st) {
     const size_t total = (size_t)Lloc * rowlen;
     if (!total) return cudaSuccess;
     size_t g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    k_compact_survivors<<<(unsigned)g, 256, 0, st>>>(xp, xs, surv, Lloc, rowlen, out);
+    k_compact_survivors<<<(unsigned)g, 256, 0, st>>>(xp, xs, surv, Lloc, n, rowlen, out);
     return cudaGetLastError();
 }
 

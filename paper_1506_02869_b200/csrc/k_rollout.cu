@@ -503,14 +503,34 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         lam[c] = 0.0;
         for (int i = 0; i < n; ++i) lam[c] += (double)s_ell[c * kBlock + seg * W + i];
     }
-    int acc = args.surv_single;
-    if (NC == 2) acc = mh_decide(lam[0], lam[1], l, k, mpc, sc.key0, sc.key1) ? 1 : 0;
-    const float ell_s = (NC == 2 && acc) ? ell[NC - 1] : ell[0];
-    const double lam_s = (NC == 2 && acc) ? lam[NC - 1] : lam[0];
+    // survivor mask: bit i set = aircraft i keeps the proposal x* (joint MH: all bits alike)
+    uint32_t mask = args.surv_single;
+    int nacc = 0;
+    float ell_s = ell[0];
+    double lam_s = lam[0];
+    if (NC == 2) {
+        if (args.mh_mode == 2) {
+            // per-aircraft MH (R46): every lane decides for its own aircraft
+            const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[NC - 1], l, (uint32_t)lane, k, mpc,
+                                                       sc.key0, sc.key1);
+            const unsigned b = __ballot_sync(0xffffffffu, ai);
+            mask = (W == 32) ? b : ((b >> ((tid & 31) & ~(W - 1))) & ((1u << (W & 31)) - 1u));
+            ell_s = ai ? ell[NC - 1] : ell[0];
+            lam_s = 0.0;
+            for (int i = 0; i < n; ++i) lam_s += (double)s_ell[(((mask >> i) & 1u) ? NC - 1 : 0) * kBlock + seg * W + i];
+            nacc = __popc(mask);
+        } else {
+            const bool acc = mh_decide(lam[0], lam[1], l, k, mpc, sc.key0, sc.key1);
+            mask = acc ? 0xFFFFFFFFu : 0u;
+            ell_s = acc ? ell[NC - 1] : ell[0];
+            lam_s = acc ? lam[NC - 1] : lam[0];
+            nacc = acc ? 1 : 0;
+        }
+    }
     if (valid && isac) args.ell_out[(size_t)lane * args.L + lloc] = ell_s;
     if (valid && lane == 0) {
         args.lam_out[lloc] = lam_s;
-        args.surv_out[lloc] = (uint8_t)acc;
+        args.surv_out[lloc] = mask;
         if (args.lam_cand) {
             args.lam_cand[lloc] = lam[0];
             args.lam_cand[args.L + lloc] = lam[NC - 1];
@@ -521,7 +541,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     args.dbg_ell_c[((size_t)c * args.L + lloc) * n + i] = s_ell[c * kBlock + seg * W + i];
         }
     }
-    if (lane == 0) s_dec[seg] = (valid && NC == 2) ? acc : 0;
+    if (lane == 0) s_dec[seg] = (valid && NC == 2) ? nacc : 0;
     // per-column max of the survivor log-weights (K3, first half)
     __syncthreads();
     uint32_t *s_cm = reinterpret_cast<uint32_t *>(s_ctrl);
@@ -572,24 +592,44 @@ __global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) 
         }
     }
     const uint32_t l = args.l0 + lloc;
-    int acc = args.surv_single;
-    if (NC == 2 && valid) acc = mh_decide(lam[0], lam[1], l, args.k, *args.mpcp, sc.key0, sc.key1) ? 1 : 0;
-    const int cs = (NC == 2 && acc) ? 1 : 0;
-    if (valid) {
-        args.lam_out[lloc] = lam[cs];
-        args.surv_out[lloc] = (uint8_t)acc;
-        if (args.lam_cand) { args.lam_cand[lloc] = lam[0]; args.lam_cand[L + lloc] = lam[NC - 1]; }
-    }
-    for (int i = 0; i < n; ++i) {
+    auto ell_of = [&](int c, int i) {
         float e = args.ell0;
-        if (valid)
-            for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + cs) * n + i) * L + lloc];
-        if (valid) args.ell_out[(size_t)i * L + lloc] = e;
+        for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + c) * n + i) * L + lloc];
+        return e;
+    };
+    uint32_t mask = args.surv_single;
+    if (NC == 2 && valid) {
+        if (args.mh_mode == 2) {             // per-aircraft MH (R46)
+            mask = 0u;
+            for (int i = 0; i < n; ++i)
+                if (mh_decide_aircraft((double)ell_of(0, i), (double)ell_of(1, i), l, (uint32_t)i, args.k, *args.mpcp,
+                                       sc.key0, sc.key1))
+                    mask |= 1u << i;
+        } else {
+            mask = mh_decide(lam[0], lam[1], l, args.k, *args.mpcp, sc.key0, sc.key1) ? 0xFFFFFFFFu : 0u;
+        }
+    }
+    double lam_s = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const int cs = (NC == 2 && ((mask >> i) & 1u)) ? 1 : 0;
+        float e = args.ell0;
+        if (valid) {
+            e = ell_of(cs, i);
+            args.ell_out[(size_t)i * L + lloc] = e;
+            lam_s += (double)e;
+        }
         const uint32_t mx = __reduce_max_sync(0xffffffffu, valid ? f2ord(e) : 0u);
         if ((threadIdx.x & 31) == 0 && mx) atomicMax(&args.colmax[i], mx);
     }
+    if (valid) {
+        args.lam_out[lloc] = lam_s;
+        args.surv_out[lloc] = mask;
+        if (args.lam_cand) { args.lam_cand[lloc] = lam[0]; args.lam_cand[L + lloc] = lam[NC - 1]; }
+    }
     if (NC == 2) {
-        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid && acc));
+        const int mine = valid ? (args.mh_mode == 2 ? __popc(mask & (n == 32 ? 0xFFFFFFFFu : ((1u << n) - 1u)))
+                                                    : (mask ? 1 : 0)) : 0;
+        const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)mine);
         if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(args.n_accept, (unsigned long long)cnt);
     }
 }

@@ -92,7 +92,7 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
     float *s_Q = reinterpret_cast<float *>(s_pos + 2 * nthr);       // [8][9]
     unsigned char *s_flag = reinterpret_cast<unsigned char *>(s_Q + 72);   // [nthr][16] pair verdicts
     __shared__ double s_lam[32];
-    __shared__ int s_dec[32];
+    __shared__ uint32_t s_dec[32];                 // survivor masks of the block's particles
 
     const int tid = threadIdx.x, lane = tid & 31, i = tid >> 5;
     const int p = lane % PPB, c = lane / PPB;
@@ -333,24 +333,42 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
         }
     }  // s
 
-    // ---- epilogue: lambda = sum_i ell (double, ascending i), MH (R1), survivors
+    // ---- epilogue: lambda = sum_i ell (double, ascending i), MH (R1 / R46), survivors
     float *s_ell = reinterpret_cast<float *>(s_pos);              // reuse [nthr]
+    const bool per_ac = (NC == 2) && args.mh_mode == 2;
     __syncthreads();
     s_ell[tid] = ell;
+    if (tid < 32) s_dec[tid] = 0u;
     __syncthreads();
+    if (per_ac) {                      // per-aircraft MH (R46): warp i decides for aircraft i
+        const float e1 = __shfl_sync(0xffffffffu, ell, p + PPB);
+        if (c == 0 && mh_decide_aircraft((double)ell, (double)e1, l, (uint32_t)i, k, mpc, sc.key0, sc.key1))
+            atomicOr(&s_dec[p], 1u << i);
+        __syncthreads();
+    }
     if (i == 0) {
         double lam = 0.0;
         for (int a = 0; a < n; ++a) lam += (double)s_ell[a * 32 + lane];
         s_lam[lane] = lam;                                          // lane = (c, p)
         double lam_c0 = __shfl_sync(0xffffffffu, lam, p);
         double lam_c1 = __shfl_sync(0xffffffffu, lam, p + (NC - 1) * PPB);
-        int acc = args.surv_single;
-        if (NC == 2) acc = mh_decide(lam_c0, lam_c1, l, k, mpc, sc.key0, sc.key1) ? 1 : 0;
+        uint32_t mask = args.surv_single;
+        double lam_s = lam_c0;
+        if (per_ac) {
+            mask = s_dec[p];
+            lam_s = 0.0;
+            for (int a = 0; a < n; ++a) lam_s += (double)s_ell[a * 32 + p + (((mask >> a) & 1u) ? PPB : 0)];
+        } else if (NC == 2) {
+            const bool acc = mh_decide(lam_c0, lam_c1, l, k, mpc, sc.key0, sc.key1);
+            mask = acc ? 0xFFFFFFFFu : 0u;
+            lam_s = acc ? lam_c1 : lam_c0;
+        }
+        __syncwarp();
         if (c == 0) {
-            s_dec[p] = acc;
+            s_dec[p] = mask;
             if (valid) {
-                args.lam_out[lloc] = (NC == 2 && acc) ? lam_c1 : lam_c0;
-                args.surv_out[lloc] = (uint8_t)acc;
+                args.lam_out[lloc] = lam_s;
+                args.surv_out[lloc] = mask;
                 if (args.lam_cand) {
                     args.lam_cand[lloc] = lam_c0;
                     args.lam_cand[args.L + lloc] = lam_c1;
@@ -358,15 +376,16 @@ k_rollout_t(const DevScen sc, const RolloutArgs args) {
             }
         }
         if (NC == 2) {
-            const unsigned cntv = __popc(__ballot_sync(0xffffffffu, c == 0 && valid && acc));
+            const unsigned mine = (c == 0 && valid) ? (per_ac ? __popc(mask) : (mask ? 1u : 0u)) : 0u;
+            const unsigned cntv = __reduce_add_sync(0xffffffffu, mine);
             if (lane == 0 && cntv) atomicAdd(args.n_accept, (unsigned long long)cntv);
         }
         if (DEBUG && args.dbg_ell_c && valid)
             for (int a = 0; a < n; ++a) args.dbg_ell_c[((size_t)c * args.L + lloc) * n + a] = s_ell[a * 32 + lane];
     }
     __syncthreads();
-    const int acc = s_dec[p];
-    const bool mine = (NC == 1) || (c == acc);
+    const uint32_t mbit = (s_dec[p] >> i) & 1u;
+    const bool mine = (NC == 1) || ((uint32_t)c == mbit);
     if (valid && mine) args.ell_out[(size_t)i * args.L + lloc] = ell;
     // per-column max of the survivor log-weights (first half of the reduce, K3)
     const uint32_t key = (valid && mine) ? f2ord(ell) : 0u;

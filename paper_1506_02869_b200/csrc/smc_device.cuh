@@ -162,6 +162,20 @@ __device__ __forceinline__ bool mh_decide(double lam_cur, double lam_prop, uint3
     return u53 < det_exp2(delta);
 }
 
+// Per-aircraft MH decision (R46): the joint rules on one aircraft's log2 weights, uniform
+// from the MH stream at counter (l, k<<16, i).
+__device__ __forceinline__ bool mh_decide_aircraft(double ell_cur, double ell_prop, uint32_t l, uint32_t i,
+                                                   uint32_t k, uint32_t mpc, uint32_t k0, uint32_t k1) {
+    if (ell_cur == -INFINITY) return true;
+    if (ell_prop == -INFINITY) return false;
+    const double delta = ell_prop - ell_cur;
+    if (delta >= 0.0) return true;
+    const uint4 w = draw(TAG_MH, l, k << 16, i, mpc, k0, k1);
+    const uint64_t r = (uint64_t)w.x | ((uint64_t)w.y << 32);
+    const double u53 = (double)(r >> 11) * 0x1.0p-53;
+    return u53 < det_exp2(delta);
+}
+
 // ---------------------------------------------------------------- angles
 // |wrap(d)| in [0, pi].
 __device__ __forceinline__ float angdist(float d) {

@@ -13,11 +13,12 @@ struct RolloutArgs {
     uint32_t L, l0, S, k;      // local particles, global offset, samples, round
     const uint32_t *mpcp;      // device: MPC step index (keys every stream)
     float ell0;                // -log2(L_global)  (W^0 = 1/L)
-    int surv_single;           // survivor flag written when only one candidate is evaluated
+    uint32_t surv_single;      // survivor mask written when only one candidate is evaluated (0 or ~0)
+    int mh_mode;               // 1: joint MH on lambda (R1); 2: per-aircraft MH (R46)
     float *ell_out;            // [n][L] survivor log2 weights (column-major per aircraft)
     double *lam_out;           // [L] survivor joint log2 weight
     double *lam_cand;          // [2][L] both candidates' joint log2 weights (nullable)
-    uint8_t *surv_out;         // [L] 1 = proposal accepted
+    uint32_t *surv_out;        // [L] survivor mask: bit i set = aircraft i's row comes from x*
     uint32_t *colmax;          // [n] ordered-float max of ell_out (atomicMax)
     unsigned long long *n_accept;
     float *part;               // [chunks][NC][n][L] partial log2 weights (chunked launch) or NULL
@@ -87,7 +88,7 @@ struct ProposeArgs {
     uint32_t L, l0, k, key0, key1;
     const uint32_t *mpcp;
     const float *src[2];        // survivor pair: [0] x', [1] x*
-    const uint8_t *surv;        // [L] which buffer holds particle l's survivor
+    const uint32_t *surv;       // [L] survivor masks: bit i = buffer holding aircraft i's row
     uint32_t Lsrc;              // particles evaluated this round (CDF length); L = new particles
     const int32_t *anc;         // [n][L] explicit ancestors (debug) or NULL -> bisection of C
     const unsigned long long *C, *QR;
@@ -112,7 +113,7 @@ struct MultiArgs {
     const unsigned long long *Call;   // [G][n][Lmax] per-rank inclusive CDFs
     const float *Sall;          // [G][Lmax][n][H][3] per-rank survivor rows
 };
-cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint8_t *surv, uint32_t Lloc,
+cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
                                      int rowlen, float *out, cudaStream_t st);
 cudaError_t launch_gather_propose_multi(const MultiArgs &m, cudaStream_t st);
 cudaError_t launch_select_merge(const unsigned char *recs, int G, size_t rec_bytes, int rowlen, unsigned char *out,
@@ -123,7 +124,7 @@ struct SelectArgs {
     uint32_t L, l0;
     int n, H;
     const double *lam;
-    const uint8_t *surv;
+    const uint32_t *surv;
     const float *src[2];
     double *part_lam;           // [nblocks]
     long long *part_idx;        // [nblocks]
@@ -131,6 +132,8 @@ struct SelectArgs {
     double *best_lam;           // [1]
     long long *best_idx;        // [1]  (-1 if infeasible)
     float *best_row;            // [n][H][3]
+    const double *lam2;         // [2][lam2_stride] candidates' joint lambdas (per-aircraft MH pick) or NULL
+    uint32_t lam2_stride;
 };
 int select_blocks(uint32_t L);
 cudaError_t launch_select(const SelectArgs &s, cudaStream_t st);
@@ -170,6 +173,10 @@ cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny,
 // MH decisions for injected lambdas (debug hook)
 cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,
                             uint32_t key0, uint32_t key1, uint8_t *acc, cudaStream_t st);
+// per-aircraft MH decisions on injected float log2 weights [L][n] -> masks (debug hook)
+cudaError_t launch_mh_aircraft_debug(const float *ec, const float *ep, uint32_t L, int n, uint32_t k,
+                                     const uint32_t *mpcp, uint32_t key0, uint32_t key1, uint32_t *mask,
+                                     cudaStream_t st);
 
 __host__ __device__ uint64_t slot_count(uint64_t C, uint64_t Q, uint64_t R, uint32_t L);
 cudaError_t launch_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax, cudaStream_t st);

@@ -126,7 +126,8 @@ def load():
         "smc_debug_mh": (st, [v, f64p, f64p, u32, u32, P(C.c_uint8)]),
         "smc_debug_resample": (st, [v, f32p, u32, u32, u32, u32, P(C.c_int32), P(u64)]),
         "smc_debug_propose": (st, [v, f32p, P(C.c_int32), u32, u32, f32p, f32p]),
-        "smc_debug_population": (st, [v, f32p, f32p, P(C.c_uint8), f32p, f64p, f64p, P(C.c_uint32)]),
+        "smc_debug_population": (st, [v, f32p, f32p, P(C.c_uint32), f32p, f64p, f64p, P(C.c_uint32)]),
+        "smc_debug_mh_aircraft": (st, [v, f32p, f32p, u32, u32, u32, P(C.c_uint32)]),
         "smc_shard_range": (None, [u32, C.c_int32, C.c_int32, P(u32), P(u32)]),
         "smc_shard_offsets": (None, [u32, C.c_int32, C.c_int32, P(u64), P(u64), P(u64)]),
         "smc_slot_count": (u64, [u64, u64, u64, u32]),
@@ -142,7 +143,7 @@ def load():
 
 EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate", "smc_best_controls",
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
-            "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh",
+            "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh", "smc_debug_mh_aircraft",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
             "smc_shard_offsets", "smc_slot_count", "smc_fuel_estimates"]
 
@@ -196,7 +197,7 @@ class Solver:
     """One libsmcatm context on one GPU (rank)."""
 
     def __init__(self, scn: dict, L: int, S: int, K: int, sigma, seed: int, anneal: float = 0.98,
-                 mh: bool = True, sched_paper: bool = False, clamp: bool = False, device: int = 0,
+                 mh: int = 1, sched_paper: bool = False, clamp: bool = False, device: int = 0,
                  max_aircraft: int | None = None, max_horizon: int | None = None, stream=None,
                  rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False,
                  virtual_world: int = 0, L_final: int = 0, warm_fraction: float = 0.0):
@@ -375,6 +376,16 @@ class Solver:
                                           _p(acc, C.c_uint8)))
         return acc
 
+    def debug_mh_aircraft(self, ell_cur, ell_prop, k):
+        """Per-aircraft MH masks (R46) for injected float log2 weights [L][n]."""
+        a = np.ascontiguousarray(np.asarray(ell_cur, dtype=np.float32))
+        b = np.ascontiguousarray(np.asarray(ell_prop, dtype=np.float32))
+        L, N = a.shape
+        mask = np.zeros(L, np.uint32)
+        self._check(self.lib.smc_debug_mh_aircraft(self.ctx, _p(a, C.c_float), _p(b, C.c_float), L, N, k,
+                                                   _p(mask, C.c_uint32)))
+        return mask
+
     def debug_resample(self, ell, k, M=None):
         e = np.ascontiguousarray(np.asarray(ell, dtype=np.float32))
         N, L = e.shape
@@ -397,16 +408,18 @@ class Solver:
         L, n, H = self.L, self.n, self.H
         cur = np.zeros((L, n, H, 3), np.float32)
         prop = np.zeros_like(cur)
-        surv = np.zeros(L, np.uint8)
+        surv = np.zeros(L, np.uint32)
         ell = np.zeros((n, L), np.float32)
         lam = np.zeros(L, np.float64)
         lam2 = np.zeros((2, L), np.float64)
         nev = C.c_uint32()
         self._check(self.lib.smc_debug_population(self.ctx, _p(cur, C.c_float), _p(prop, C.c_float),
-                                                  _p(surv, C.c_uint8), _p(ell, C.c_float), _p(lam, C.c_double),
+                                                  _p(surv, C.c_uint32), _p(ell, C.c_float), _p(lam, C.c_double),
                                                   _p(lam2, C.c_double), C.byref(nev)))
         Lk = nev.value
-        return {"cur": cur[:Lk], "prop": prop[:Lk], "surv": surv[:Lk],
+        # surv: bit 0 of the survivor masks (the joint decision; all bits alike outside mh=2)
+        return {"cur": cur[:Lk], "prop": prop[:Lk], "surv": (surv[:Lk] & 1).astype(np.uint8),
+                "surv_mask": surv[:Lk],
                 "ell": ell.reshape(-1)[:n * Lk].reshape(n, Lk), "lam": lam[:Lk],
                 "lam_cand": lam2.reshape(-1)[:2 * Lk].reshape(2, Lk)}
 

@@ -177,6 +177,61 @@ def test_mh_bitexact(smc):
         assert np.array_equal(acc, ref)
 
 
+def test_mh_aircraft_bitexact(smc):
+    """Per-aircraft MH decisions (R46) of the production device function vs the oracle."""
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, seed=cfg.seed)
+    rng = np.random.default_rng(6)
+    L, N = 6000, 7
+    ec = rng.uniform(-40, -2, (L, N)).astype(np.float32)
+    ep = (ec + np.concatenate([rng.uniform(-8, 1, (L // 2, N)), rng.normal(0, 1e-6, (L - L // 2, N))])).astype(np.float32)
+    ec[rng.uniform(size=(L, N)) < 0.05] = -np.inf
+    ep[rng.uniform(size=(L, N)) < 0.05] = -np.inf
+    for k in (1, 9):
+        mask = sol.debug_mh_aircraft(ec, ep, k)
+        for l in range(0, L, 3):
+            ref = sum(O.mh_accept_aircraft(float(ec[l, i]), float(ep[l, i]), l, i, k, cfg.seed) << i for i in range(N))
+            assert mask[l] == ref, (l, k)
+
+
+@pytest.mark.parametrize("layout", ["segment", "transposed"])
+def test_per_aircraft_mh_rounds(smc, layout, monkeypatch):
+    """mh = 2 (R46) in real rounds: every survivor row is the candidate its mask bit names,
+    its log-weight is the oracle's for that candidate, the decisions replay on the GPU's
+    candidate weights, and the final pick is the best jointly evaluated candidate."""
+    monkeypatch.setenv("SMC_K2_LAYOUT", layout)
+    scn, cfg = sc.config(2)
+    L, S, K = 512, 3, 4
+    sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, mh=2)
+    P = O.Problem(scn)
+    n = scn["n"]
+    sol.iterate(1)
+    for k in range(1, K):
+        sol.iterate(1)
+        pop = sol.population()
+        mask = pop["surv_mask"]
+        ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
+        ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
+        bits = ((mask[:, None] >> np.arange(n)[None, :]) & 1).astype(bool)
+        ell_o = np.where(bits, ell_p, ell_c)
+        ell_g = pop["ell"].T.astype(np.float64)
+        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
+        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
+        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+        assert np.allclose(pop["lam"], np.where(np.isfinite(ell_g).all(1), ell_g.sum(1), -np.inf), rtol=1e-12)
+        # oracle decisions on the oracle's weights agree except at near-ties
+        dec = np.array([[O.mh_accept_aircraft(ell_c[l, i], ell_p[l, i], l, i, k, cfg.seed) for i in range(n)]
+                        for l in range(L)])
+        assert (dec == bits).mean() > 0.98
+        assert 0.02 < bits.mean() < 0.98                 # both outcomes occur
+    _, lam_best, idx = sol.best_controls(allow_infeasible=True)
+    pop = sol.population()
+    lc, lp = pop["lam_cand"]
+    both = np.concatenate([lc, lp])
+    assert lam_best == np.max(both[np.isfinite(both)])
+    sol.close()
+
+
 @pytest.mark.parametrize("L", [1, 7, 2048, 2049, 5000, 70001])
 def test_resample_bitexact(smc, L):
     scn, cfg = sc.config(1)
@@ -453,8 +508,8 @@ def test_paper_literal_mode_replay(smc):
         assert np.allclose(ell_g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + 20))
 
 
-@pytest.mark.parametrize("num,vw", [(1, 2), (2, 3), (5, 4)])
-def test_virtual_ranks_bitexact(smc, num, vw):
+@pytest.mark.parametrize("num,vw,mh", [(1, 2, 1), (2, 3, 1), (5, 4, 1), (2, 3, 2)])
+def test_virtual_ranks_bitexact(smc, num, vw, mh):
     """G-invariance on one GPU: the multi-GPU resampling path (per-rank CDFs,
     rank-offset bisection, survivor exchange layout, record merge) run for vw
     virtual ranks reproduces the single-rank populations bit for bit."""
@@ -462,14 +517,14 @@ def test_virtual_ranks_bitexact(smc, num, vw):
     L = min(cfg.L, 65536 + 123)
     res = []
     for v in (0, vw):
-        sol = smc.Solver(scn, L=L, S=min(cfg.S, 4), K=4, sigma=cfg.sigma, seed=cfg.seed, virtual_world=v)
+        sol = smc.Solver(scn, L=L, S=min(cfg.S, 4), K=4, sigma=cfg.sigma, seed=cfg.seed, virtual_world=v, mh=mh)
         sol.iterate(3)
         pop = sol.population()
         best = sol.best_controls(allow_infeasible=True)
         res.append((pop, best))
         sol.close()
     (a, ba), (b, bb) = res
-    for key in ("cur", "prop", "surv", "ell", "lam"):
+    for key in ("cur", "prop", "surv_mask", "ell", "lam"):
         assert np.array_equal(a[key], b[key]), key
     assert np.array_equal(ba[0], bb[0]) and ba[1] == bb[1] and ba[2] == bb[2]
 
