@@ -991,7 +991,7 @@ int ora_fuel_estimate1(const ora_problem *p, int i, const double *Cf, const doub
         ora_lift_drag(p, i, st, 0.0, &L, &D);
         double T = m * (b[3] - vs) / dt + D + m * p->g * sin(gam);
         double burn = dt * eta * T;
-        if (burn < 0.0) burn = 0.0;
+        if (!(burn > 0.0)) burn = 0.0;                 /* negative or undefined (R47): none */
         m -= burn;
         m_out[k + 1] = m;
     }
@@ -1027,7 +1027,7 @@ int ora_fuel_estimate2(const ora_problem *p, int i, const double *Cf, const doub
         ora_lift_drag(p, i, st, phi, &L, &D);
         double T = m * (b[3] - vh) / dt + D + m * p->g * sin(gam);
         double burn = dt * eta * T;
-        if (burn < 0.0) burn = 0.0;
+        if (!(burn > 0.0)) burn = 0.0;                 /* negative or undefined (R47): none */
         m -= burn;
         m_out[k + 1] = m;
     }
