@@ -18,6 +18,7 @@ DESIGN.md section 9.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -47,6 +48,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--traffic", default="c3", choices=["c3", "mixed", "congested"],
                     help="traffic stream of --loop")
+    ap.add_argument("--mh", type=int, default=-1, choices=[-1, 0, 1, 2],
+                    help="move: 0 paper Alg.1, 1 joint MH (R1), 2 per-aircraft MH (R46); -1 = the config's")
     ap.add_argument("--wind-grid", default="",
                     help="N_x,N_y,N_z wind grid points (P:454; default the paper's 2,2,2)")
     ap.add_argument("--warm", type=float, default=0.0,
@@ -197,6 +200,8 @@ def run_loop(args):
     8 dep) or the paper's mixed (10 + 10) / congested (24 arrivals) shapes."""
     from paper_1506_02869_b200 import mpc_loop, scenarios as sc
     base, cfg = sc.config(args.config if args.config != 2 else 3)
+    if args.mh >= 0:
+        cfg = dataclasses.replace(cfg, mh=args.mh)
     if args.traffic == "mixed":
         tr, desc = sc.paper_mixed(), "paper mixed: 10 arrivals / 10 departures"
     elif args.traffic == "congested":
@@ -205,9 +210,9 @@ def run_loop(args):
         tr, desc = sc.traffic(16, 8, seed=1003, arr_every=2, dep_every=8), "c3 traffic: 16 arrivals / 8 departures"
     recs, done, fuel, aud = mpc_loop.run(base, tr, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
                                          n_steps=args.loop, max_aircraft=32, return_audit=True,
-                                         warm_fraction=args.warm, L_final=args.lfinal)
+                                         warm_fraction=args.warm, L_final=args.lfinal, mh=int(cfg.mh))
     lat = [r.latency_ms for r in recs]
-    print(json.dumps({"mode": "mpc_loop", "config": f"{desc}, {cfg.name} solver: L={cfg.L}, S={cfg.S}, K={cfg.K}"
+    print(json.dumps({"mode": "mpc_loop", "config": f"{desc}, {cfg.name} solver: L={cfg.L}, S={cfg.S}, K={cfg.K}, mh={int(cfg.mh)}"
                       + (f", warm start {args.warm}" if args.warm else "") + (f", L_final {args.lfinal}" if args.lfinal else ""),
                       "steps": len(recs),
                       "per_step": [{"step": r.step, "window": r.window, "active": r.active,
@@ -238,6 +243,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     scn, cfg = sc.config(args.config)
+    if args.mh >= 0:
+        cfg = dataclasses.replace(cfg, mh=args.mh)
     if args.wind_grid:
         scn["wind_n"] = tuple(int(v) for v in args.wind_grid.split(","))
     stream = torch.cuda.Stream(device=local)
@@ -344,7 +351,8 @@ def main():
                                f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
                                + (f"->{args.lfinal}" if args.lfinal else "")
                                + (", S_k=floor(3+5e^(0.05k))" if cfg.sched_paper else f", S={cfg.S}")
-                               + f", H={scn['H']}, K={cfg.K} rounds, " + ("MH on" if cfg.mh else "paper Alg.1 (no MH)")
+                               + f", H={scn['H']}, K={cfg.K} rounds, "
+                               + {0: "paper Alg.1 (no MH)", 1: "MH on", 2: "per-aircraft MH"}[int(cfg.mh)]
                                + (f", wind grid {'x'.join(str(v) for v in scn['wind_n'])}" if args.wind_grid else ""),
                    "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
                                    "all-gathers per round)" if world > 1 else "single GPU"),
