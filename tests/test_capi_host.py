@@ -129,3 +129,29 @@ def test_closed_loop_audit_counts():
     assert a.min_sep_m == 10.0                    # step 2, pair 0-2 (step 0: 0-2 is 2 Ph + 1 apart vertically)
     assert (a.landed, a.exited, a.unfinished, a.n_aircraft) == (1, 1, 1, 3)
     assert a.fuel_total_kg == 15.5
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the oracle on the host cores) prints one JSON line with
+    the driver's keys; N > 1 ranks other than 0 print nothing."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
+                          "--config", "1"], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e", "impl"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 2
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                          "--config", "1"], cwd=root, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0 and not out.stdout.strip()
