@@ -22,6 +22,7 @@
 // max of ell folded into an atomicMax (first step of the resampling reduce).
 #include "smc_device.cuh"
 #include "smc_kernels.h"
+#include "smc_vec.cuh"
 
 #ifndef SMC_K2_MINB
 #define SMC_K2_MINB 4   // resident 128-thread blocks per SM the register budget targets (A/B: 4 > 5 > 6)
@@ -61,24 +62,38 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // atan2 on the MUFU reciprocal and a degree-15 odd polynomial (least-squares
-// fit of atan(a)/a on [0,1] in a^2; |error| < 1.5e-7 rad in binary32).
-__device__ __forceinline__ float fast_atan2(float y, float x) {
-    const float ax = fabsf(x), ay = fabsf(y);
-    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    const float a = mx > 0.0f ? mn * rcp_approx(mx) : 0.0f;
-    const float s = a * a;
-    float p = -0.0040731243789196014f;
-    p = fmaf(p, s, 0.021945973858237267f);
-    p = fmaf(p, s, -0.056062303483486176f);
-    p = fmaf(p, s, 0.0965619683265686f);
-    p = fmaf(p, s, -0.13915780186653137f);
-    p = fmaf(p, s, 0.19948504865169525f);
-    p = fmaf(p, s, -0.3333010673522949f);
-    p = fmaf(p, s, 0.999999463558197f);
-    float r = p * a;
-    r = ay > ax ? 1.57079632679489662f - r : r;
-    r = x < 0.0f ? kPi - r : r;
-    return copysignf(r, y);
+// fit of atan(a)/a on [0,1] in a^2; |error| < 1.5e-7 rad in binary32), both
+// candidates at once (packed polynomial, per-candidate octant selects).
+template <class V>
+__device__ __forceinline__ V fast_atan2(V y, V x) {
+    const V ax = vabs(x), ay = vabs(y);
+    V mx, mn;
+#pragma unroll
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c) {
+        cset(mx, c, fmaxf(cget(ax, c), cget(ay, c)));
+        cset(mn, c, fminf(cget(ax, c), cget(ay, c)));
+    }
+    const V a = mn * vmap(mx, [](float u) { return u > 0.0f ? rcp_approx(u) : 0.0f; });
+    const V s = a * a;
+    V p = vfma(s, -0.0040731243789196014f, 0.021945973858237267f);
+    p = vfma(p, s, -0.056062303483486176f);
+    p = vfma(p, s, 0.0965619683265686f);
+    p = vfma(p, s, -0.13915780186653137f);
+    p = vfma(p, s, 0.19948504865169525f);
+    p = vfma(p, s, -0.3333010673522949f);
+    p = vfma(p, s, 0.999999463558197f);
+    const V r = p * a;
+    const V r1 = 1.57079632679489662f - r;
+    V q;
+#pragma unroll
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c)
+        cset(q, c, cget(ay, c) > cget(ax, c) ? cget(r1, c) : cget(r, c));
+    const V q1 = kPi - q;
+    V out;
+#pragma unroll
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c)
+        cset(out, c, copysignf(cget(x, c) < 0.0f ? cget(q1, c) : cget(q, c), cget(y, c)));
+    return out;
 }
 
 // Shared-memory strides of the wind field per segment: normals (VST) and
@@ -134,23 +149,37 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     const float gA = kind ? Ap->theta_F : Ap->beta_f;          // goal of the A/D term or the E term
     const float z_tf = Ap->z_tf, v_D = Ap->v_D;
 
-    // ---- controls: (T, tan phi, sin gamma, cos gamma) to shared memory; envelope bits to registers
+    // ---- controls: (T, tan phi, sin gamma, cos gamma) to shared memory; envelope bits to registers.
+    // NC = 1: one float4 (T, tan phi, sin g, cos g) per (t, lane).  NC = 2: the candidates
+    // interleaved so each quantity loads as a float2 pair -- (T0, T1, tphi0, tphi1) and
+    // (sg0, sg1, cg0, cg1) at s_ctrl[(2t + h) kBlock + tid], h = 0, 1.
     uint32_t cbad[NC];
     {
         const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
+        const float *src[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             cbad[c] = 0;
-            const float *src = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
-            for (int t = 0; t < H; ++t) {
+            src[c] = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
+        }
+        for (int t = 0; t < H; ++t) {
+            float q[NC][4];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
                 float T = 0.f, ph = 0.f, ga = 0.f;
-                if (isac && valid) { T = src[3 * t]; ph = src[3 * t + 1]; ga = src[3 * t + 2]; }
+                if (isac && valid) { T = src[c][3 * t]; ph = src[c][3 * t + 1]; ga = src[c][3 * t + 2]; }
                 float sph, cph, sga, cga;
                 sincosf(ph, &sph, &cph);
                 sincosf(ga, &sga, &cga);
-                s_ctrl[(t * NC + c) * kBlock + tid] = make_float4(T, sph / cph, sga, cga);
+                q[c][0] = T; q[c][1] = sph / cph; q[c][2] = sga; q[c][3] = cga;
                 const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
                 cbad[c] |= (bad ? 1u : 0u) << t;
+            }
+            if constexpr (NC == 2) {
+                s_ctrl[(2 * t) * kBlock + tid] = make_float4(q[0][0], q[1][0], q[0][1], q[1][1]);
+                s_ctrl[(2 * t + 1) * kBlock + tid] = make_float4(q[0][2], q[1][2], q[0][3], q[1][3]);
+            } else {
+                s_ctrl[t * kBlock + tid] = make_float4(q[0][0], q[0][1], q[0][2], q[0][3]);
             }
         }
     }
@@ -165,23 +194,27 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) ell[c] = args.part ? 0.0f : args.ell0;
 
+    using V = vec_t<NC>;
     const float dt = sc.dt, g = sc.g;
-    const float dtg = dt * g;
+    // wind-box coordinates f = sat(p inv + nlo) (clamped to the box, R14)
+    const float inv0 = sc.wind_inv_ext[0], inv1 = sc.wind_inv_ext[1], inv2 = sc.wind_inv_ext[2];
+    const float nlo0 = -sc.wind_lo[0] * inv0, nlo1 = -sc.wind_lo[1] * inv1, nlo2 = -sc.wind_lo[2] * inv2;
+    // dynamic pressure factor: q = rho v^2 S / 2 = cq e(z) v^2, e(z) the ISA ratio or 1
+    const float cq = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
+    // The deviation arguments as FMA chains with per-lane coefficients (kind is per aircraft):
+    //   departure A = theta - theta_F, B = z_tf - z;  arrival A = chi - pi - 2 theta (R8), B = beta - beta_f
+    const float cA_th = kind ? 1.0f : -2.0f, cA_chi = kind ? 0.0f : 1.0f, cA_0 = kind ? -gA : -kPi;
+    const float cB_z = kind ? -1.0f : 0.0f, cB_b = kind ? 0.0f : 1.0f, cB_0 = kind ? z_tf : -gA;
     // sample chunk of this block (gridDim.y > 1: partial sums, combined by k_combine)
     const uint32_t s_lo = (uint32_t)(((uint64_t)args.S * blockIdx.y) / gridDim.y);
     const uint32_t s_hi = (uint32_t)(((uint64_t)args.S * (blockIdx.y + 1)) / gridDim.y);
     for (uint32_t s = s_lo; s < s_hi; ++s) {
-        float x[NC], y[NC], z[NC], v[NC], chi[NC], m[NC], fuel[NC], sA[NC], sB[NC], sC[NC], sN[NC];
+        V x = vsplat<V>(Ap->x0[0]), y = vsplat<V>(Ap->x0[1]), z = vsplat<V>(Ap->x0[2]);
+        V v = vsplat<V>(Ap->x0[3]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
+        V fuel = vsplat<V>(0.0f), sA = fuel, sB = fuel, sC = fuel, sN = fuel;
         bool landed[NC], viol[NC];
-        {
-            const float x0 = Ap->x0[0], y0 = Ap->x0[1], z0 = Ap->x0[2], v0 = Ap->x0[3], c0 = Ap->x0[4], m0 = Ap->x0[5];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                x[c] = x0; y[c] = y0; z[c] = z0; v[c] = v0; chi[c] = c0; m[c] = m0;
-                fuel[c] = sA[c] = sB[c] = sC[c] = sN[c] = 0.0f;
-                landed[c] = false; viol[c] = false;
-            }
-        }
+        for (int c = 0; c < NC; ++c) { landed[c] = false; viol[c] = false; }
         float Zr[E];
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
@@ -294,23 +327,33 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             }
             const float c0x = DENSE ? gx : Wn[0] + gx, c0y = DENSE ? gy : Wn[8] + gy;   // nominal + gust (+ c0)
 
-            // ---------------- 2-3. dynamics, unary checks and geometry per candidate
+            // ---------------- 2-3. dynamics, unary checks and geometry, both candidates at once
             const bool act = first <= t;
             bool fly[NC], vnow[NC], lnow[NC];
-            float nx[NC], ny[NC], nz[NC], nv[NC], nchi[NC], nm[NC], th[NC], beta[NC], rh[NC], Tc[NC], px[NC];
+            V flyf;                                   // 1 while the candidate's aircraft flies, else 0
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 fly[c] = act && !landed[c] && !viol[c];
-                const float4 cc = s_ctrl[(t * NC + c) * kBlock + tid];
-                const float T = cc.x, tph = cc.y, sga = cc.z, cga = cc.w;
-                Tc[c] = T;
-                // wind at the pre-step position (trilinear, clamped to the box)
-                float wx, wy;
-                if constexpr (DENSE) {
+                cset(flyf, c, fly[c] ? 1.0f : 0.0f);
+            }
+            V T, tph, sga, cga;
+            if constexpr (NC == 2) {
+                const float4 a = s_ctrl[(2 * t) * kBlock + tid], b = s_ctrl[(2 * t + 1) * kBlock + tid];
+                T = make_float2(a.x, a.y); tph = make_float2(a.z, a.w);
+                sga = make_float2(b.x, b.y); cga = make_float2(b.z, b.w);
+            } else {
+                const float4 a = s_ctrl[t * kBlock + tid];
+                T = a.x; tph = a.y; sga = a.z; cga = a.w;
+            }
+            // wind at the pre-step position (trilinear, clamped to the box)
+            V wx, wy;
+            if constexpr (DENSE) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
                     // grid cell holding the aircraft (clamped), trilinear over its 8 corners
                     float f3[3];
                     int base = 0, mul = 1;
-                    const float p3[3] = {x[c], y[c], z[c]};
+                    const float p3[3] = {cget(x, c), cget(y, c), cget(z, c)};
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         const float gc = clamp01((p3[a] - sc.wind_lo[a]) * sc.wind_inv_ext[a]) * (float)(sc.wn[a] - 1);
@@ -320,6 +363,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                         mul *= sc.wn[a];
                     }
                     const int sy = sc.wn[0], sz = sc.wn[0] * sc.wn[1];
+                    const float *sWs = s_W + seg * ZST;
 #pragma unroll
                     for (int comp = 0; comp < 2; ++comp) {
                         const float *w0 = sWs + comp * G + base;
@@ -329,53 +373,77 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                         const float a3 = fmaf(f3[0], w0[sz + sy + 1] - w0[sz + sy], w0[sz + sy]);
                         const float b0 = fmaf(f3[1], a1 - a0, a0), b1 = fmaf(f3[1], a3 - a2, a2);
                         const float wv = fmaf(f3[2], b1 - b0, b0) + (comp ? c0y : c0x);
-                        if (comp) wy = wv; else wx = wv;
+                        if (comp) cset(wy, c, wv); else cset(wx, c, wv);
                     }
-                } else {
-                    const float fx = clamp01((x[c] - sc.wind_lo[0]) * sc.wind_inv_ext[0]);
-                    const float fy = clamp01((y[c] - sc.wind_lo[1]) * sc.wind_inv_ext[1]);
-                    const float fz = clamp01((z[c] - sc.wind_lo[2]) * sc.wind_inv_ext[2]);
-                    wx = tripoly(Wn, c0x, fx, fy, fz);
-                    wy = tripoly(Wn + 8, c0y, fx, fy, fz);
                 }
-                // Eq. hor, coordinated-turn lift and parabolic drag (R12):
-                // C_L^2 = (m g / q)^2 (1 + tan^2 phi)
-                float rho = sc.rho_const;
-                if (sc.density_mode == 0)
-                    rho = 1.225f * ex2_approx(4.2559f * __log2f(fmaxf(fmaf(-2.2558e-5f, z[c], 1.0f), 0.0f)));
-                const float qd = rho * v[c] * v[c] * halfS;
-                const float mgq = m[c] * g * rcp_approx(qd);
-                const float D = qd * fmaf(cd2 * mgq * mgq, fmaf(tph, tph, 1.0f), cd0);
-                const float chr = chi[c] - kTwoPi * rintf(chi[c] * (1.0f / kTwoPi));
-                float sch, cch;
-                __sincosf(chr, &sch, &cch);
-                const float vcg = v[c] * cga;
-                const float rm = rcp_approx(m[c]), rv = rcp_approx(v[c]);
-                nx[c] = fmaf(dt, fmaf(vcg, cch, wx), x[c]);
-                ny[c] = fmaf(dt, fmaf(vcg, sch, wy), y[c]);
-                nz[c] = fmaf(dt * v[c], sga, z[c]);
-                nv[c] = fmaf(dt, fmaf(T - D, rm, -g * sga), v[c]);
-                nchi[c] = fmaf(dtg * tph, rv, chi[c]);
-                nm[c] = fmaf(-dt_eta, T, m[c]);
-                // envelope and mass at j = t+1 (R17)
+            } else {
+                const V fx = vmap(x, [&](float p) { return __saturatef(fmaf(p, inv0, nlo0)); });
+                const V fy = vmap(y, [&](float p) { return __saturatef(fmaf(p, inv1, nlo1)); });
+                const V fz = vmap(z, [&](float p) { return __saturatef(fmaf(p, inv2, nlo2)); });
+                wx = tripoly(Wn, c0x, fx, fy, fz);
+                wy = tripoly(Wn + 8, c0y, fx, fy, fz);
+            }
+            // Eq. hor, coordinated-turn lift and parabolic drag (R12):
+            // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a grounded / inactive / violated aircraft
+            // advances with dt_f = 0 (its state stays frozen, R18/R42)
+            V qd = cq * v * v;
+            if (sc.density_mode == 0) {
+                const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
+                qd = qd * vmap(vmap(base, [](float a) { return __log2f(a); }) * 4.2559f, ex2_approx);
+            }
+            const V mgq = (m * g) * vmap(qd, rcp_approx);
+            const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
+            const V chr = vfma(vmap(chi * (1.0f / kTwoPi), [](float a) { return rintf(a); }), -kTwoPi, chi);
+            V sch, cch;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float s_, c_;
+                __sincosf(cget(chr, c), &s_, &c_);
+                cset(sch, c, s_); cset(cch, c, c_);
+            }
+            const V dtf = flyf * dt, dtef = flyf * dt_eta;
+            const V vcg = v * cga;
+            const V nx = vfma(dtf, vfma(vcg, cch, wx), x);
+            const V ny = vfma(dtf, vfma(vcg, sch, wy), y);
+            const V nz = vfma(dtf * v, sga, z);
+            const V nv = vfma(dtf, vfma(T - D, vmap(m, rcp_approx), sga * (-g)), v);
+            const V nchi = vfma((dtf * g) * tph, vmap(v, rcp_approx), chi);
+            const V nm = vfma(-dtef, T, m);
+            // envelope and mass at j = t+1 (R17)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const float zc = cget(nz, c), vc = cget(nv, c);
                 bool bad = (cbad[c] >> t) & 1u;
-                bad |= !(nz[c] >= zmin && nz[c] <= zmax);
-                bad |= !(nv[c] >= vmin && nv[c] <= vmax);
-                bad |= !(nm[c] >= mempty);
+                bad |= !(zc >= zmin && zc <= zmax);
+                bad |= !(vc >= vmin && vc <= vmax);
+                bad |= !(cget(nm, c) >= mempty);
                 // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
                 vnow[c] = bad;
-                th[c] = fast_atan2(ny[c], nx[c]);
-                // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
-                const float r2 = fmaf(nx[c], nx[c], ny[c] * ny[c]);
-                rh[c] = r2 * rsqrtf(fmaxf(r2, 1e-30f));
-                const float at = fabsf(th[c]);
-                const float sarc = at > 1e-4f ? rh[c] * at * rcp_approx(__sinf(at)) : rh[c];
-                beta[c] = fast_atan2(nz[c], sarc);
-                lnow[c] = (kind == 0) && !landed[c] && rh[c] <= sc.P_runway && beta[c] <= sc.P_beta &&
-                          at <= sc.P_chi && angdist(nchi[c] - kPi) <= sc.P_chi && nv[c] <= sc.P_vs;
-                // a grounded / inactive / violated aircraft is a NaN position: every comparison fails
-                px[c] = fly[c] ? nx[c] : __int_as_float(0x7fffffff);
-                s_pos[c * kBlock + tid] = make_float4(px[c], ny[c], nz[c], 0.0f);
+            }
+            const V th = fast_atan2(ny, nx);
+            // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
+            const V r2 = vfma(nx, nx, ny * ny);
+            const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
+            const V at = vabs(th);
+            const V sarc = rh * vmap(at, [](float a) { return a > 1e-4f ? a * rcp_approx(__sinf(a)) : 1.0f; });
+            const V beta = fast_atan2(nz, sarc);
+            const V hd = nchi - kPi;                              // heading relative to the runway (West)
+            const V hdw = vfma(vmap(hd * (1.0f / kTwoPi), [](float a) { return rintf(a); }), -kTwoPi, hd);
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                lnow[c] = (kind == 0) && !landed[c] && cget(rh, c) <= sc.P_runway && cget(beta, c) <= sc.P_beta &&
+                          cget(at, c) <= sc.P_chi && fabsf(cget(hdw, c)) <= sc.P_chi && cget(nv, c) <= sc.P_vs;
+            // a grounded / inactive / violated aircraft is a NaN position: every comparison fails
+            V px;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) cset(px, c, fly[c] ? cget(nx, c) : __int_as_float(0x7fffffff));
+            float4 *s_pxy = s_pos;                                  // NC = 2: (x0, x1, y0, y1)
+            float2 *s_pz = reinterpret_cast<float2 *>(s_pos + kBlock);   // NC = 2: (z0, z1)
+            if constexpr (NC == 2) {
+                s_pxy[tid] = make_float4(px.x, px.y, ny.x, ny.y);
+                s_pz[tid] = nz;
+            } else {
+                s_pos[tid] = make_float4(px, ny, nz, 0.0f);
             }
             __syncwarp();
             // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
@@ -386,12 +454,22 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             for (int c = 0; c < NC; ++c) conf[c] = false;
 #pragma unroll
             for (int d = 1; d <= W / 2; ++d) {
+                const int pl = seg * W + ((lane + d) & (W - 1));
+                V dx, dy, dz;
+                if constexpr (NC == 2) {
+                    const float4 q = s_pxy[pl];
+                    dx = px - make_float2(q.x, q.y);
+                    dy = ny - make_float2(q.z, q.w);
+                    dz = nz - s_pz[pl];
+                } else {
+                    const float4 q = s_pos[pl];
+                    dx = px - q.x; dy = ny - q.y; dz = nz - q.z;
+                }
+                const V d2 = vfma(dx, dx, dy * dy);
                 int hits = 0;
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const float4 q = s_pos[c * kBlock + seg * W + ((lane + d) & (W - 1))];
-                    const float dx = px[c] - q.x, dy = ny[c] - q.y, dz = nz[c] - q.z;
-                    const bool hit = (fmaf(dx, dx, dy * dy) < sc.twoPr2) && (fabsf(dz) < sc.twoPh);
+                    const bool hit = (cget(d2, c) < sc.twoPr2) && (fabsf(cget(dz, c)) < sc.twoPh);
                     conf[c] = conf[c] | hit;
                     hits |= (hit ? 1 : 0) << c;
                 }
@@ -402,45 +480,42 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     for (int c = 0; c < NC; ++c) conf[c] = conf[c] | ((back >> c) & 1);
                 }
             }
-            // ---------------- 5. per-step cost terms at j = t+1, state update
+            // ---------------- 5. per-step cost terms at j = t+1 (frozen aircraft add 0), state update
+            // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
+            // arrival:   D = |wrap(chi - chi_hat)|, chi_hat = pi + 2 theta (R8); E = |beta - beta_f|
+            const V argA = vfma(th, cA_th, vfma(nchi, cA_chi, cA_0));
+            const V wA = vfma(vmap(argA * (1.0f / kTwoPi), [](float a) { return rintf(a); }), -kTwoPi, argA);
+            sA = vfma(vabs(wA), flyf, sA);
+            sB = vfma(vabs(vfma(nz, cB_z, vfma(beta, cB_b, cB_0))), flyf, sB);
+            sC = vfma(vabs(nv - v_D), flyf, sC);
+            fuel = vfma(dtef, T, fuel);
+            if (sc.has_noise) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const float zz = cget(nz, c) * sc.inv_Ac;
+                    const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, cget(nx, c), cget(ny, c));
+                    // "best possible cost, 1, for all remaining steps" after landing
+                    cset(sN, c, cget(sN, c) + (fly[c] ? nzs : ((act && landed[c]) ? 1.0f : 0.0f)));
+                }
+            }
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 vnow[c] = vnow[c] || conf[c];
-                // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
-                // arrival:   D = |wrap(chi - chi_hat)|, chi_hat = pi + 2 theta (R8); E = |beta - beta_f|
-                const float devA = angdist(kind ? th[c] - gA : nchi[c] - kPi - 2.0f * th[c]);
-                const float devB = kind ? fabsf(z_tf - nz[c]) : fabsf(beta[c] - gA);
-                const float devC = fabsf(nv[c] - v_D);
-                float nzs = 0.0f;
-                if (sc.has_noise) {
-                    const float zz = nz[c] * sc.inv_Ac;
-                    nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, nx[c], ny[c]);
-                }
-                sA[c] += fly[c] ? devA : 0.0f;
-                sB[c] += fly[c] ? devB : 0.0f;
-                sC[c] += fly[c] ? devC : 0.0f;
-                // "best possible cost, 1, for all remaining steps" after landing
-                sN[c] += fly[c] ? nzs : ((act && landed[c]) ? 1.0f : 0.0f);
-                fuel[c] += fly[c] ? dt_eta * Tc[c] : 0.0f;
                 viol[c] = viol[c] || (fly[c] && vnow[c]);
                 landed[c] = landed[c] || (fly[c] && lnow[c]);
-                x[c] = fly[c] ? nx[c] : x[c];
-                y[c] = fly[c] ? ny[c] : y[c];
-                z[c] = fly[c] ? nz[c] : z[c];
-                v[c] = fly[c] ? nv[c] : v[c];
-                chi[c] = fly[c] ? nchi[c] : chi[c];
-                m[c] = fly[c] ? nm[c] : m[c];
-                if (DEBUG && c == 0 && valid && isac && args.dbg_traj) {
-                    float *tr = args.dbg_traj + ((((size_t)lloc * args.S + s) * n + lane) * (H + 1) + t + 1) * 6;
-                    tr[0] = x[c]; tr[1] = y[c]; tr[2] = z[c]; tr[3] = v[c]; tr[4] = chi[c]; tr[5] = m[c];
-                    if (t == 0) {
-                        float *t0 = tr - 6;
-                        for (int a = 0; a < 6; ++a) t0[a] = Ap->x0[a];
-                    }
-                }
-                if (DEBUG && c == 0 && valid && isac && args.dbg_landed && lnow[c] && fly[c])
-                    args.dbg_landed[((size_t)lloc * args.S + s) * n + lane] = t + 1;
             }
+            x = nx; y = ny; z = nz; v = nv; chi = nchi; m = nm;
+            if (DEBUG && valid && isac && args.dbg_traj) {
+                float *tr = args.dbg_traj + ((((size_t)lloc * args.S + s) * n + lane) * (H + 1) + t + 1) * 6;
+                tr[0] = cget(x, 0); tr[1] = cget(y, 0); tr[2] = cget(z, 0);
+                tr[3] = cget(v, 0); tr[4] = cget(chi, 0); tr[5] = cget(m, 0);
+                if (t == 0) {
+                    float *t0 = tr - 6;
+                    for (int a = 0; a < 6; ++a) t0[a] = Ap->x0[a];
+                }
+            }
+            if (DEBUG && valid && isac && args.dbg_landed && lnow[0] && fly[0])
+                args.dbg_landed[((size_t)lloc * args.S + s) * n + lane] = t + 1;
         }  // t
 
         // ---------------- utility J_T and weight
@@ -453,29 +528,29 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             for (int c = 0; c < NC; ++c) {
                 float J = 1.0f, c0 = 1.f, c1 = 1.f, c2 = 1.f, c3 = 1.f;
                 if (Ha > 0 && isac) {
-                    const float Jfuel = clamp01(1.0f - fuel[c] * invFmax);
-                    const float J1 = clamp01(1.0f - sA[c] * invHa * (1.0f / kPi));
+                    const float Jfuel = clamp01(1.0f - cget(fuel, c) * invFmax);
+                    const float J1 = clamp01(1.0f - cget(sA, c) * invHa * (1.0f / kPi));
                     if (kind == 1) {
                         c0 = J1;
                         c1 = Jfuel;
-                        c2 = flagB ? 1.0f : clamp01((supB - sB[c] * invHa) * invDenB);
-                        c3 = clamp01(1.0f - sC[c] * invHa * invSupC);
+                        c2 = flagB ? 1.0f : clamp01((supB - cget(sB, c) * invHa) * invDenB);
+                        c3 = clamp01(1.0f - cget(sC, c) * invHa * invSupC);
                         J = sc.alpha_dep[0] * c0 + sc.alpha_dep[1] * c1 + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
                     } else {
                         c0 = J1;
-                        c1 = clamp01(1.0f - sB[c] * invHa * invSupE);
+                        c1 = clamp01(1.0f - cget(sB, c) * invHa * invSupE);
                         c2 = Jfuel;
                         c3 = 0.0f;
                         J = sc.alpha_arr[0] * c0 + sc.alpha_arr[1] * c1 + sc.alpha_arr[2] * c2;
                     }
-                    if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * sN[c] * invHa;
+                    if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * cget(sN, c) * invHa;
                 }
                 ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
                 if (DEBUG && c == 0 && valid && isac) {
                     const size_t o = ((size_t)lloc * args.S + s) * n + lane;
                     if (args.dbg_J) args.dbg_J[o] = J;
                     if (args.dbg_viol) args.dbg_viol[o] = viol[c] ? 1 : 0;
-                    if (args.dbg_fuel) args.dbg_fuel[o] = fuel[c];
+                    if (args.dbg_fuel) args.dbg_fuel[o] = cget(fuel, c);
                     if (args.dbg_comp) { float *cp = args.dbg_comp + 4 * o; cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3; }
                 }
             }

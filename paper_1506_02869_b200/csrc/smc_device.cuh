@@ -5,6 +5,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "smc_vec.cuh"
 
 namespace smc {
 
@@ -88,12 +89,13 @@ __device__ __forceinline__ uint4 draw_ks(uint32_t tag, uint32_t x0, uint32_t x1,
 
 // Trilinear interpolation in polynomial form: with c = M W (node n = ix + 2 iy + 4 iz)
 //   f = c0 + c1 fx + c2 fy + c3 fz + c4 fx fy + c5 fx fz + c6 fy fz + c7 fx fy fz,
-// algebraically the 7-lerp form; 7 FMAs.  c0 is passed separately so a per-lane
+// algebraically the 7-lerp form; 7 FMAs (packed over the candidates when V = float2).  c0 is passed separately so a per-lane
 // offset (nominal wind + gust) can be folded in once per step.
-__device__ __forceinline__ float tripoly(const float *c, float c0, float fx, float fy, float fz) {
-    const float A = fmaf(fy, fmaf(fz, c[7], c[4]), fmaf(fz, c[5], c[1]));
-    const float B = fmaf(fy, fmaf(fz, c[6], c[2]), fmaf(fz, c[3], c0));
-    return fmaf(fx, A, B);
+template <class V>
+__device__ __forceinline__ V tripoly(const float *c, float c0, V fx, V fy, V fz) {
+    const V A = vfma(fy, vfma(fz, c[7], c[4]), vfma(fz, c[5], c[1]));
+    const V B = vfma(fy, vfma(fz, c[6], c[2]), vfma(fz, c[3], c0));
+    return vfma(fx, A, B);
 }
 
 // Uniform (2k+1) 2^-24, k = w >> 9: exact in binary32 (R37).
