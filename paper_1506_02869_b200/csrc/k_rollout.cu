@@ -96,6 +96,34 @@ __device__ __forceinline__ V fast_atan2(V y, V x) {
     return out;
 }
 
+// atan2(y, x) for x >= 0 (right half-plane: no x < 0 fix-up), same polynomial.
+template <class V>
+__device__ __forceinline__ V fast_atan2_xpos(V y, V x) {
+    const V ax = x, ay = vabs(y);
+    V mx, mn;
+#pragma unroll
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c) {
+        cset(mx, c, fmaxf(cget(ax, c), cget(ay, c)));
+        cset(mn, c, fminf(cget(ax, c), cget(ay, c)));
+    }
+    const V a = mn * vmap(mx, [](float u) { return u > 0.0f ? rcp_approx(u) : 0.0f; });
+    const V s = a * a;
+    V p = vfma(s, -0.0040731243789196014f, 0.021945973858237267f);
+    p = vfma(p, s, -0.056062303483486176f);
+    p = vfma(p, s, 0.0965619683265686f);
+    p = vfma(p, s, -0.13915780186653137f);
+    p = vfma(p, s, 0.19948504865169525f);
+    p = vfma(p, s, -0.3333010673522949f);
+    p = vfma(p, s, 0.999999463558197f);
+    const V r = p * a;
+    const V r1 = 1.57079632679489662f - r;
+    V out;
+#pragma unroll
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c)
+        cset(out, c, copysignf(cget(ay, c) > cget(ax, c) ? cget(r1, c) : cget(r, c), cget(y, c)));
+    return out;
+}
+
 // Shared-memory strides of the wind field per segment: normals (VST) and
 // AR(1) state / node values (ZST, odd to spread segments over banks).
 __host__ __device__ constexpr int dense_vst(int G) { return 4 * ((2 * G + 3) / 4); }
@@ -120,8 +148,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock);
     float *s_Z = s_V + SEGS * VST;
     float *s_W = s_Z + SEGS * ZST;
-    float4 *s_pos = reinterpret_cast<float4 *>(s_W + ((SEGS * ZST + 3) & ~3));   // [NC][kBlock]
-    float *s_Q = reinterpret_cast<float *>(s_pos + NC * kBlock);
+    // positions for the separation scan, each segment's entries stored twice so partner
+    // lane + d is a constant offset: [2 kBlock] float4 (NC = 2: (x0, x1, y0, y1)) + [2 kBlock] float2 (z0, z1)
+    float4 *s_pos = reinterpret_cast<float4 *>(s_W + ((SEGS * ZST + 3) & ~3));
+    float *s_Q = reinterpret_cast<float *>(s_pos + 3 * kBlock);
 
     const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
     const uint32_t lloc = blockIdx.x * SEGS + seg;
@@ -212,9 +242,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         V x = vsplat<V>(Ap->x0[0]), y = vsplat<V>(Ap->x0[1]), z = vsplat<V>(Ap->x0[2]);
         V v = vsplat<V>(Ap->x0[3]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
         V fuel = vsplat<V>(0.0f), sA = fuel, sB = fuel, sC = fuel, sN = fuel;
-        bool landed[NC], viol[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) { landed[c] = false; viol[c] = false; }
+        // per-candidate flags as bit masks (bit c = candidate c)
+        constexpr int ALLC = (1 << NC) - 1;
+        int landedm = 0, violm = 0;
         float Zr[E];
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
@@ -230,8 +260,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 const int G2 = 2 * G, nblk = (G2 + 3) >> 2;
                 for (int b = lane; b < nblk; b += W) {
                     const uint4 w = draw_ks(TAG_WIND, l, x1, (uint32_t)t | ((uint32_t)b << 16), mpc, sc.ks);
-                    const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
-                    *reinterpret_cast<float4 *>(&sVs[4 * b]) = make_float4(p0.x, p0.y, p1.x, p1.y);
+                    *reinterpret_cast<float4 *>(&sVs[4 * b]) = box_muller4(w);
                 }
                 __syncwarp();
                 for (int e = lane; e < G2; e += W) {
@@ -269,9 +298,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const int b = task & 3, ts = t + (task >> 2);
                     if (ts < H) {
                         const uint4 w = draw_ks(TAG_WIND, l, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
-                        const float2 p0 = box_muller(w.x, w.y), p1 = box_muller(w.z, w.w);
-                        *reinterpret_cast<float4 *>(&s_V[(seg * GB + (task >> 2)) * 16 + 4 * b]) =
-                            make_float4(p0.x, p0.y, p1.x, p1.y);
+                        *reinterpret_cast<float4 *>(&s_V[(seg * GB + (task >> 2)) * 16 + 4 * b]) = box_muller4(w);
                     }
                 }
             }
@@ -317,8 +344,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 float2 gg;
                 if ((t & 1) == 0) {
                     const uint4 w = draw_ks(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
-                    gg = box_muller(w.x, w.y);
-                    gust_odd = box_muller(w.z, w.w);
+                    const float4 g4 = box_muller4(w);
+                    gg = make_float2(g4.x, g4.y);
+                    gust_odd = make_float2(g4.z, g4.w);
                 } else {
                     gg = gust_odd;
                 }
@@ -329,13 +357,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
             // ---------------- 2-3. dynamics, unary checks and geometry, both candidates at once
             const bool act = first <= t;
-            bool fly[NC], vnow[NC], lnow[NC];
+            const int flym = act ? (~(landedm | violm) & ALLC) : 0;
             V flyf;                                   // 1 while the candidate's aircraft flies, else 0
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                fly[c] = act && !landed[c] && !viol[c];
-                cset(flyf, c, fly[c] ? 1.0f : 0.0f);
-            }
+            for (int c = 0; c < NC; ++c) cset(flyf, c, ((flym >> c) & 1) ? 1.0f : 0.0f);
             V T, tph, sga, cga;
             if constexpr (NC == 2) {
                 const float4 a = s_ctrl[(2 * t) * kBlock + tid], b = s_ctrl[(2 * t + 1) * kBlock + tid];
@@ -410,75 +435,77 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const V nchi = vfma((dtf * g) * tph, vmap(v, rcp_approx), chi);
             const V nm = vfma(-dtef, T, m);
             // envelope and mass at j = t+1 (R17)
+            int vnowm = 0;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const float zc = cget(nz, c), vc = cget(nv, c);
-                bool bad = (cbad[c] >> t) & 1u;
-                bad |= !(zc >= zmin && zc <= zmax);
-                bad |= !(vc >= vmin && vc <= vmax);
-                bad |= !(cget(nm, c) >= mempty);
+                const bool bad = ((cbad[c] >> t) & 1u) || !(zc >= zmin && zc <= zmax) || !(vc >= vmin && vc <= vmax) ||
+                                 !(cget(nm, c) >= mempty);
                 // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
-                vnow[c] = bad;
+                vnowm |= (bad ? 1 : 0) << c;
             }
             const V th = fast_atan2(ny, nx);
-            // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10)
+            // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10):
+            // s = rho_h |theta| / sin|theta| with sin|theta| = |y| / rho_h, i.e. s = rho_h^2 |theta| / |y|
             const V r2 = vfma(nx, nx, ny * ny);
             const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
             const V at = vabs(th);
-            const V sarc = rh * vmap(at, [](float a) { return a > 1e-4f ? a * rcp_approx(__sinf(a)) : 1.0f; });
-            const V beta = fast_atan2(nz, sarc);
-            const V hd = nchi - kPi;                              // heading relative to the runway (West)
-            const V hdw = vfma(vmap(hd * (1.0f / kTwoPi), [](float a) { return rintf(a); }), -kTwoPi, hd);
+            V sarc;
 #pragma unroll
             for (int c = 0; c < NC; ++c)
-                lnow[c] = (kind == 0) && !landed[c] && cget(rh, c) <= sc.P_runway && cget(beta, c) <= sc.P_beta &&
-                          cget(at, c) <= sc.P_chi && fabsf(cget(hdw, c)) <= sc.P_chi && cget(nv, c) <= sc.P_vs;
+                cset(sarc, c, cget(at, c) > 1e-4f ? cget(r2, c) * cget(at, c) * rcp_approx(fabsf(cget(ny, c))) : cget(rh, c));
+            const V beta = fast_atan2_xpos(nz, sarc);              // s >= 0: right half-plane
+            const V hd = nchi - kPi;                              // heading relative to the runway (West)
+            const V hdw = vfma(vmap(hd * (1.0f / kTwoPi), [](float a) { return rintf(a); }), -kTwoPi, hd);
+            int lnowm = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const bool ln = cget(rh, c) <= sc.P_runway && cget(beta, c) <= sc.P_beta && cget(at, c) <= sc.P_chi &&
+                                fabsf(cget(hdw, c)) <= sc.P_chi && cget(nv, c) <= sc.P_vs;
+                lnowm |= (ln ? 1 : 0) << c;
+            }
+            if (kind != 0) lnowm = 0;                            // only arrivals land (Eq. TO_init)
             // a grounded / inactive / violated aircraft is a NaN position: every comparison fails
             V px;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) cset(px, c, fly[c] ? cget(nx, c) : __int_as_float(0x7fffffff));
-            float4 *s_pxy = s_pos;                                  // NC = 2: (x0, x1, y0, y1)
-            float2 *s_pz = reinterpret_cast<float2 *>(s_pos + kBlock);   // NC = 2: (z0, z1)
+            for (int c = 0; c < NC; ++c) cset(px, c, ((flym >> c) & 1) ? cget(nx, c) : __int_as_float(0x7fffffff));
+            // own entry at seg*2W + lane and + W: partner lane + d (mod W) sits at offset d
+            const int pb = seg * 2 * W + lane;
+            float4 *s_pxy = s_pos;                                           // [2 kBlock]
+            float2 *s_pz = reinterpret_cast<float2 *>(s_pos + 2 * kBlock);   // [2 kBlock] (NC = 2)
             if constexpr (NC == 2) {
-                s_pxy[tid] = make_float4(px.x, px.y, ny.x, ny.y);
-                s_pz[tid] = nz;
+                const float4 e = make_float4(px.x, px.y, ny.x, ny.y);
+                s_pxy[pb] = e; s_pxy[pb + W] = e;
+                s_pz[pb] = nz; s_pz[pb + W] = nz;
             } else {
-                s_pos[tid] = make_float4(px, ny, nz, 0.0f);
+                const float4 e = make_float4(px, ny, nz, 0.0f);
+                s_pxy[pb] = e; s_pxy[pb + W] = e;
             }
             __syncwarp();
             // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
             // lane checks partner lane+d (d = 1..W/2) and hands the verdict to that
             // partner with a segment-wide shuffle (for d = W/2 both lanes check).
-            bool conf[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) conf[c] = false;
+            int confm = 0;
 #pragma unroll
             for (int d = 1; d <= W / 2; ++d) {
-                const int pl = seg * W + ((lane + d) & (W - 1));
                 V dx, dy, dz;
                 if constexpr (NC == 2) {
-                    const float4 q = s_pxy[pl];
+                    const float4 q = s_pxy[pb + d];
                     dx = px - make_float2(q.x, q.y);
                     dy = ny - make_float2(q.z, q.w);
-                    dz = nz - s_pz[pl];
+                    dz = nz - s_pz[pb + d];
                 } else {
-                    const float4 q = s_pos[pl];
+                    const float4 q = s_pxy[pb + d];
                     dx = px - q.x; dy = ny - q.y; dz = nz - q.z;
                 }
                 const V d2 = vfma(dx, dx, dy * dy);
                 int hits = 0;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const bool hit = (cget(d2, c) < sc.twoPr2) && (fabsf(cget(dz, c)) < sc.twoPh);
-                    conf[c] = conf[c] | hit;
-                    hits |= (hit ? 1 : 0) << c;
-                }
-                // one shuffle hands both candidates' verdicts to the partner (every lane reaches it)
-                if (2 * d < W) {
-                    const int back = __shfl_sync(0xffffffffu, hits, (lane - d) & (W - 1), W);
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) conf[c] = conf[c] | ((back >> c) & 1);
-                }
+                for (int c = 0; c < NC; ++c)
+                    hits |= ((cget(d2, c) < sc.twoPr2) && (fabsf(cget(dz, c)) < sc.twoPh) ? 1 : 0) << c;
+                confm |= hits;
+                // one shuffle hands both candidates' verdicts to the partner (source lane taken mod W)
+                if (2 * d < W) confm |= __shfl_sync(0xffffffffu, hits, lane + W - d, W);
             }
             // ---------------- 5. per-step cost terms at j = t+1 (frozen aircraft add 0), state update
             // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
@@ -495,15 +522,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const float zz = cget(nz, c) * sc.inv_Ac;
                     const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, cget(nx, c), cget(ny, c));
                     // "best possible cost, 1, for all remaining steps" after landing
-                    cset(sN, c, cget(sN, c) + (fly[c] ? nzs : ((act && landed[c]) ? 1.0f : 0.0f)));
+                    cset(sN, c, cget(sN, c) + (((flym >> c) & 1) ? nzs : ((act && ((landedm >> c) & 1)) ? 1.0f : 0.0f)));
                 }
             }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                vnow[c] = vnow[c] || conf[c];
-                viol[c] = viol[c] || (fly[c] && vnow[c]);
-                landed[c] = landed[c] || (fly[c] && lnow[c]);
-            }
+            violm |= flym & (vnowm | confm);
+            landedm |= flym & lnowm;
             x = nx; y = ny; z = nz; v = nv; chi = nchi; m = nm;
             if (DEBUG && valid && isac && args.dbg_traj) {
                 float *tr = args.dbg_traj + ((((size_t)lloc * args.S + s) * n + lane) * (H + 1) + t + 1) * 6;
@@ -514,7 +537,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     for (int a = 0; a < 6; ++a) t0[a] = Ap->x0[a];
                 }
             }
-            if (DEBUG && valid && isac && args.dbg_landed && lnow[0] && fly[0])
+            if (DEBUG && valid && isac && args.dbg_landed && (lnowm & flym & 1))
                 args.dbg_landed[((size_t)lloc * args.S + s) * n + lane] = t + 1;
         }  // t
 
@@ -545,11 +568,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     }
                     if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * cget(sN, c) * invHa;
                 }
-                ell[c] = (viol[c] || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
+                ell[c] = (((violm >> c) & 1) || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
                 if (DEBUG && c == 0 && valid && isac) {
                     const size_t o = ((size_t)lloc * args.S + s) * n + lane;
                     if (args.dbg_J) args.dbg_J[o] = J;
-                    if (args.dbg_viol) args.dbg_viol[o] = viol[c] ? 1 : 0;
+                    if (args.dbg_viol) args.dbg_viol[o] = (violm >> c) & 1;
                     if (args.dbg_fuel) args.dbg_fuel[o] = cget(fuel, c);
                     if (args.dbg_comp) { float *cp = args.dbg_comp + 4 * o; cp[0] = c0; cp[1] = c1; cp[2] = c2; cp[3] = c3; }
                 }
@@ -640,11 +663,11 @@ size_t rollout_smem_bytes(int W, int NC, int H, int ng) {
         const size_t zs = ((size_t)SEGS * dense_zst(ng) + 3) & ~(size_t)3;
         return sizeof(float4) * ((size_t)H * NC * kBlock) +
                sizeof(float) * ((size_t)SEGS * dense_vst(ng) + SEGS * dense_zst(ng) + zs) +
-               sizeof(float4) * NC * kBlock + sizeof(float) * (size_t)ng * dense_qts(ng) + 16;
+               sizeof(float4) * 3 * kBlock + sizeof(float) * (size_t)ng * dense_qts(ng) + 16;
     }
     const int GB = (W >= 8) ? W / 4 : 1;
     return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * (SEGS * GB * 16 + 2 * SEGS * 16) +
-           sizeof(float4) * NC * kBlock + sizeof(float) * 72 + 16;
+           sizeof(float4) * 3 * kBlock + sizeof(float) * 72 + 16;
 }
 
 // Combine the sample chunks of a chunked K2 launch (fixed chunk order):

@@ -114,6 +114,22 @@ __device__ __forceinline__ float2 box_muller(uint32_t w0, uint32_t w1) {
     return make_float2(-r * c, -r * s);
 }
 
+// The two Box-Muller pairs of one Philox block, (w.x, w.y) -> (.x, .y) and (w.z, w.w) -> (.z, .w),
+// evaluated as packed pairs; bit-identical to two box_muller calls (2 pi u2 - pi = 2 pi (u2 - 1/2)
+// exactly: pi_f is half of (2 pi)_f and u2 - 1/2 is exact on the 2^-24 grid).
+__device__ __forceinline__ float4 box_muller4(uint4 w) {
+    const float2 u1 = vfma(make_float2(__uint2float_rn(w.x >> 9), __uint2float_rn(w.z >> 9)), 0x1.0p-23f, 0x1.0p-24f);
+    const float2 u2 = vfma(make_float2(__uint2float_rn(w.y >> 9), __uint2float_rn(w.w >> 9)), 0x1.0p-23f, 0x1.0p-24f);
+    const float2 r2 = make_float2(__log2f(u1.x), __log2f(u1.y)) * (-2.0f * 0.69314718055994531f);
+    const float2 r = r2 * make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+    const float2 ang = vfma(u2, kTwoPi, -kPi);
+    float2 sn, cs;
+    __sincosf(ang.x, &sn.x, &cs.x);
+    __sincosf(ang.y, &sn.y, &cs.y);
+    const float2 a = -r * cs, b = -r * sn;
+    return make_float4(a.x, b.x, a.y, b.y);
+}
+
 __device__ __forceinline__ uint64_t r64(uint32_t tag, uint32_t x0, uint32_t k, uint32_t mpc,
                                         uint32_t k0, uint32_t k1) {
     const uint4 w = draw(tag, x0, k << 16, 0u, mpc, k0, k1);
