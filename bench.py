@@ -251,10 +251,16 @@ def main():
     # N > 1: one MPC problem whose particles are sharded over the N GPUs (NCCL
     # exchange each round), L = configs' L per GPU -> weak scaling
     L_glob = cfg.L * world
-    sol = smcatm.Solver(scn, L=L_glob, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
-                        anneal=cfg.anneal, mh=cfg.mh, sched_paper=cfg.sched_paper, device=local, stream=stream,
-                        profile=True,
-                        use_graph=not args.no_graph, rank=rank, world_size=world, L_final=args.lfinal)
+
+    def make_solver(profile):
+        # profile=True brackets every kernel with CUDA events on the library's stream (graph
+        # event nodes, ~5 us each between dependent kernels): used only for the per-kernel pass
+        return smcatm.Solver(scn, L=L_glob, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed,
+                             anneal=cfg.anneal, mh=cfg.mh, sched_paper=cfg.sched_paper, device=local, stream=stream,
+                             profile=profile, use_graph=not args.no_graph, rank=rank, world_size=world,
+                             L_final=args.lfinal)
+
+    sol = make_solver(False)
     S_list = roofline.samples_list(cfg)
     ac_steps = roofline.aircraft_steps(scn, L_glob, S_list, cfg.mh, args.lfinal)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -268,7 +274,6 @@ def main():
         for _ in range(args.warmup):
             sol.solve()
         barrier()
-        sol.phase_times()                                   # reset phase accumulators
         n0 = sol.launches
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         with ClockSampler(local) as clk:
@@ -281,7 +286,23 @@ def main():
             barrier()
         step_ms = [a.elapsed_time(b) for a, b in evs]
         launches = sol.launches - n0
-        phases = sol.phase_times()
+        # per-kernel pass: the same W + K steps with CUDA events around every launch on the
+        # launching stream (smc_phase_times) -> K2's average launch duration for the roofline
+        psol = make_solver(True)
+        for _ in range(args.warmup):
+            psol.solve()
+        barrier()
+        psol.phase_times()                                  # reset phase accumulators
+        pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            pevs[s][0].record(stream)
+            psol.solve()
+            pevs[s][1].record(stream)
+        barrier()
+        phases = psol.phase_times()
+        pstep_ms = [a.elapsed_time(b) for a, b in pevs]
+        del psol
     tot_ms = sum(step_ms)
     t_local = torch.tensor([tot_ms], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
@@ -365,6 +386,9 @@ def main():
                  "mpc_step_latency_ms": sum(e2e_ms) / len(e2e_ms)} if e2e_ms else None),
         "gpu_launches": launches,
         "phase_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "phase_pass": {"what": "second pass of the same warmup + steps with CUDA events around every kernel "
+                               "launch (its event nodes lengthen the step, so value is timed without them)",
+                       "ms_per_step": sum(pstep_ms) / len(pstep_ms)},
         "roofline": {"kernel": "k_rollout (K2: rollout + MH)", "bound": "alu", "achieved": achieved / 1e9,
                      "peak": peak / 1e9, "unit": "Gop/s (FP32-lane-equivalent)", "frac": achieved / peak,
                      "traffic": load_traffic(cfg.name),

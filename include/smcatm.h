@@ -107,7 +107,8 @@ typedef struct {
 
 /* Solver configuration. */
 typedef struct {
-    uint32_t n_particles;      /* L, global over all ranks                    */
+    uint32_t n_particles;      /* L, global over all ranks; L < 2^30 and
+                                  L * max_aircraft < 2^31, else SMC_EINVAL           */
     uint32_t n_samples;        /* S per round for SMC_SCHED_CONST (Alg.1 l.7)         */
     uint32_t schedule;         /* SMC_SCHED_*                                         */
     uint32_t n_rounds;         /* K rounds per mpc_step (J_max + 1)     */

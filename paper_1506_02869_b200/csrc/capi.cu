@@ -345,7 +345,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->rank = cfg->rank;
     if (cfg->n_particles == 0 || cfg->max_aircraft == 0 || cfg->max_aircraft > 32 || cfg->max_horizon == 0 ||
         cfg->max_horizon > 32 || cfg->n_samples == 0 || cfg->n_samples > 65535 || cfg->n_particles >= (1u << 30) ||
-        cfg->mh > 2) {
+        (uint64_t)cfg->n_particles * cfg->max_aircraft >= (1ull << 31) || cfg->mh > 2) {
         delete ctx;
         return SMC_EINVAL;
     }

@@ -189,6 +189,36 @@ __device__ unsigned long long lookback(unsigned long long *status, int tile, uns
     return pre;
 }
 
+// The same look-back run by one warp: lane k probes predecessor tile - 1 - k, so a
+// window of 32 predecessors costs one round of loads (the serial walk above costs
+// one load latency per predecessor).  All 32 lanes of warp 0 call it.
+template <class Op>
+__device__ unsigned long long lookback_warp(unsigned long long *status, int tile, unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_status(&status[0], kFlagP | agg);
+        return Op::id();
+    }
+    if (lane == 0) st_status(&status[tile], kFlagA | agg);
+    unsigned long long pre = Op::id();
+    int j = tile - 1;
+    while (true) {
+        const int jj = j - lane;
+        unsigned long long s = jj >= 0 ? ld_status(&status[jj]) : kFlagP;   // before tile 0: prefix 0
+        while (__any_sync(0xffffffffu, (s & ~kValMask) == 0ull))
+            if ((s & ~kValMask) == 0ull) s = ld_status(&status[jj]);        // predecessor not published yet
+        const unsigned pm = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagP);
+        const int stop = pm ? __ffs(pm) - 1 : 31;                           // nearest inclusive prefix
+        unsigned long long v = lane <= stop ? (s & kValMask) : Op::id();
+        for (int o = 16; o; o >>= 1) v = Op::op(v, __shfl_xor_sync(0xffffffffu, v, o));
+        pre = Op::op(pre, v);
+        if (pm) break;
+        j -= 32;
+    }
+    if (lane == 0) st_status(&status[tile], kFlagP | Op::op(pre, agg));
+    return pre;
+}
+
 // Block-wide exclusive scan of per-thread values; returns the thread's
 // exclusive prefix, *agg = block total.
 template <class Op>
@@ -240,7 +270,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
     }
     unsigned long long agg;
     const unsigned long long texcl = block_exclusive<OpSum>(run, &agg);
-    if (threadIdx.x == 0) s_pre = lookback<OpSum>(r.status + (size_t)i * ntiles, tile, agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pw = lookback_warp<OpSum>(r.status + (size_t)i * ntiles, tile, agg);
+        if (threadIdx.x == 0) s_pre = pw;
+    }
     __syncthreads();
     const uint64_t pre = s_pre + texcl;
     unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : r.L);
@@ -313,16 +346,19 @@ constexpr int kRowsPerBlock = 256;   // = blockDim: every thread runs one bisect
 
 __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
     __shared__ const float *s_src[kRowsPerBlock];
-    const size_t rows = (size_t)p.L * p.n;
+    __shared__ uint32_t s_j[kRowsPerBlock];
+    __shared__ uint32_t s_perturb_x2[kRowsPerBlock];     // (i << 8): the aircraft part of the PERTURB counter
+    const uint32_t rows = p.L * (uint32_t)p.n;            // < 2^31 (smc_init bounds L n)
     const uint32_t mpc = *p.mpcp;
     const int H = p.H;
-    for (size_t q0 = (size_t)blockIdx.x * kRowsPerBlock; q0 < rows; q0 += (size_t)gridDim.x * kRowsPerBlock) {
-        if (threadIdx.x < kRowsPerBlock) {
-            const size_t q = q0 + threadIdx.x;
+    const uint32_t invH = 0xFFFFFFFFu / (uint32_t)H + 1u;    // e / H = umulhi(e, invH) for e < 2^32 / H^2
+    for (uint32_t q0 = blockIdx.x * kRowsPerBlock; q0 < rows; q0 += gridDim.x * kRowsPerBlock) {
+        {
+            const uint32_t q = q0 + threadIdx.x;
             const float *src = nullptr;
             if (q < rows) {
-                const int i = (int)(q % p.n);
-                const uint32_t j = (uint32_t)(q / p.n);
+                const uint32_t j = q / (uint32_t)p.n;
+                const int i = (int)(q - j * (uint32_t)p.n);
                 int32_t a;
                 if (p.anc) {
                     a = __ldg(&p.anc[(size_t)i * p.L + j]);
@@ -331,31 +367,48 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
                     a = find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
                 }
                 src = p.src[(__ldg(&p.surv[a]) >> i) & 1u] + ((size_t)a * p.n + i) * H * 3;
+                s_j[threadIdx.x] = j;
+                s_perturb_x2[threadIdx.x] = (uint32_t)i << 8;
             }
             s_src[threadIdx.x] = src;
         }
         __syncthreads();
-        const size_t nrow = min((size_t)kRowsPerBlock, rows - q0);
-        for (int e = threadIdx.x; e < (int)(nrow * H); e += blockDim.x) {
-            const int r = e / H, t = e - r * H;
-            const size_t q = q0 + r;
-            const int i = (int)(q % p.n);
-            const uint32_t j = (uint32_t)(q / p.n);
-            const float *src = s_src[r] + 3 * t;
-            const float c0 = src[0], c1 = src[1], c2 = src[2];
-            const size_t o = (q * H + t) * 3;
-            p.xp[o] = c0; p.xp[o + 1] = c1; p.xp[o + 2] = c2;
-            const uint4 w = draw(TAG_PERTURB, p.l0 + j, p.k << 16, (uint32_t)t | ((uint32_t)i << 8), mpc, p.key0, p.key1);
-            const float2 z01 = box_muller(w.x, w.y);
-            const float2 z23 = box_muller(w.z, w.w);
-            float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
-            if (p.clamp) {
-                const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
-                o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
-                o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
-                o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+        const int tot = (int)(min((uint32_t)kRowsPerBlock, rows - q0) * (uint32_t)H);
+        float *const xp = p.xp + (size_t)q0 * H * 3, *const xs = p.xs + (size_t)q0 * H * 3;
+        // batches of kBatch elements per thread: all parent loads (read-only path) are issued
+        // before any store, so their latencies overlap
+        constexpr int kBatch = 4;
+        for (int e0 = 0; e0 < tot; e0 += kBatch * (int)blockDim.x) {
+            float cv[kBatch][3];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+                if (e < tot) {
+                    const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
+                    const float *src = s_src[r] + 3 * t;
+                    cv[u][0] = __ldg(src); cv[u][1] = __ldg(src + 1); cv[u][2] = __ldg(src + 2);
+                }
             }
-            p.xs[o] = o0; p.xs[o + 1] = o1; p.xs[o + 2] = o2;
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+                if (e >= tot) break;
+                const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
+                const uint32_t x2 = s_perturb_x2[r];
+                const float c0 = cv[u][0], c1 = cv[u][1], c2 = cv[u][2];
+                xp[3 * e] = c0; xp[3 * e + 1] = c1; xp[3 * e + 2] = c2;
+                const uint4 w = draw(TAG_PERTURB, p.l0 + s_j[r], p.k << 16, (uint32_t)t | x2, mpc, p.key0, p.key1);
+                const float4 z = box_muller4(w);
+                float o0 = fmaf(p.sig[0], z.x, c0), o1 = fmaf(p.sig[1], z.y, c1), o2 = fmaf(p.sig[2], z.z, c2);
+                if (p.clamp) {
+                    const int i = (int)(x2 >> 8);
+                    const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
+                    o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
+                    o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
+                    o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+                }
+                xs[3 * e] = o0; xs[3 * e + 1] = o1; xs[3 * e + 2] = o2;
+            }
         }
         __syncthreads();
     }

@@ -135,7 +135,7 @@ template <int W, int NC, bool DEBUG, bool DENSE>
 __global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
-    constexpr int E = (16 + W - 1) / W;           // wind-field entries owned per lane
+    constexpr int EN = W >= 8 ? 1 : 8 / W;          // wind-grid nodes owned per lane (lanes >= 8 idle)
     extern __shared__ __align__(16) float smem[];
     const int H = sc.H, n = sc.n;
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);               // [H][NC][kBlock] (T, tan phi, sin g, cos g)
@@ -245,7 +245,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         // per-candidate flags as bit masks (bit c = candidate c)
         constexpr int ALLC = (1 << NC) - 1;
         int landedm = 0, violm = 0;
-        float Zr[E];
+        float2 Zr[EN];                                   // AR(1) state of the lane's nodes, (x, y)
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
 
@@ -303,29 +303,35 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 }
             }
             __syncwarp();
+            // AR(1) and W = Cq Z with both components of a node packed in one float2:
+            // lane owns node lane + q W (q < EN); Z is kept node-major [node](x, y) in shared memory
+            float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16);
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int e = lane + q * W;
-                if (e < 16) {
-                    const float ve = s_V[(seg * GB + tb) * 16 + e];
-                    Zr[q] = (t == 0) ? ve : fmaf(sc.a, Zr[q], sc.b * ve);
-                    s_Z[seg * 16 + e] = Zr[q];
+            for (int q = 0; q < EN; ++q) {
+                const int node = lane + q * W;
+                if (node < 8) {
+                    const float *vv = &s_V[(seg * GB + tb) * 16];
+                    const float2 ve = make_float2(vv[node], vv[8 + node]);
+                    Zr[q] = (t == 0) ? ve : vfma(Zr[q], sc.a, ve * sc.b);
+                    sZ2[node] = Zr[q];
                 }
             }
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int e = lane + q * W;
-                if (e < 16) {
-                    const int comp = e >> 3, node = e & 7;
-                    const float4 z0 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8]);
-                    const float4 z1 = *reinterpret_cast<const float4 *>(&s_Z[seg * 16 + comp * 8 + 4]);
+            for (int q = 0; q < EN; ++q) {
+                const int node = lane + q * W;
+                if (node < 8) {
+                    const float4 *z4 = reinterpret_cast<const float4 *>(sZ2);
                     const float *qr = (W >= 8) ? qrow : &s_Q[node * 9];
-                    float acc = qr[0] * z0.x;
-                    acc = fmaf(qr[1], z0.y, acc); acc = fmaf(qr[2], z0.z, acc); acc = fmaf(qr[3], z0.w, acc);
-                    acc = fmaf(qr[4], z1.x, acc); acc = fmaf(qr[5], z1.y, acc); acc = fmaf(qr[6], z1.z, acc);
-                    acc = fmaf(qr[7], z1.w, acc);
-                    s_W[seg * 16 + e] = acc;
+                    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float4 zz = z4[mm];
+                        acc = vfma(make_float2(zz.x, zz.y), qr[2 * mm], acc);
+                        acc = vfma(make_float2(zz.z, zz.w), qr[2 * mm + 1], acc);
+                    }
+                    s_W[seg * 16 + node] = acc.x;
+                    s_W[seg * 16 + 8 + node] = acc.y;
                 }
             }
             __syncwarp();
