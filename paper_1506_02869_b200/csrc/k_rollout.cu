@@ -24,11 +24,16 @@
 #include "smc_kernels.h"
 #include "smc_vec.cuh"
 
+#ifndef SMC_K2_TUNROLL
+#define SMC_K2_TUNROLL 2   // unroll factor of the horizon loop (A/B on c2: 1 -> 29.2, 2 -> 28.2, 3 -> 29.0 ms of K2)
+#endif
 #ifndef SMC_K2_MINB
 #define SMC_K2_MINB 4   // resident 128-thread blocks per SM the register budget targets (A/B: 4 > 5 > 6)
 #endif
 
 namespace smc {
+
+constexpr int kTUnroll = SMC_K2_TUNROLL;
 
 __device__ __forceinline__ float clamp01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
 
@@ -135,6 +140,7 @@ template <int W, int NC, bool DEBUG, bool DENSE>
 __global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
+    constexpr int TU = W >= 32 ? 1 : kTUnroll;      // W = 32 spills when unrolled
     constexpr int EN = W >= 8 ? 1 : 8 / W;          // wind-grid nodes owned per lane (lanes >= 8 idle)
     extern __shared__ __align__(16) float smem[];
     const int H = sc.H, n = sc.n;
@@ -249,6 +255,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         float2 gust_odd = make_float2(0.f, 0.f);
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
 
+#pragma unroll TU
         for (int t = 0; t < H; ++t) {
             // ---------------- 1. wind realisation for step t (Alg.1 l.10).
             float Wn[16];
