@@ -103,7 +103,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.tiles = take(2 * nmax * sizeof(uint32_t));
     o.C = take((size_t)nmax * Lloc * sizeof(unsigned long long));
     o.QR = take(2 * nmax * sizeof(unsigned long long));
-    o.anc = 0;
+    o.anc = take(world > 1 ? 0 : (size_t)nmax * Lloc * sizeof(int32_t));   // K5 ancestors (single rank)
     o.accept = take(8);
     o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
@@ -212,6 +212,8 @@ struct smc_ctx {
                                        // 1 transposed (warp = aircraft)
     int layout_env = -1;               // SMC_K2_LAYOUT override (-1: automatic)
     bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
+    int anc_mode = -1;                 // SMC_ANC: 1 merge-path K5, 0 bisection in K6, -1 by size
+    int32_t *anc = nullptr;            // [n][Lloc] K5 ancestors
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -354,6 +356,10 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         ctx->layout_env = lay ? ((strcmp(lay, "transposed") == 0) ? 1 : (strcmp(lay, "segment") == 0 ? 0 : -1)) : -1;
         const char *ch = getenv("SMC_K2_CHUNKS");
         ctx->chunking = ch && strcmp(ch, "1") == 0;
+        // ancestors: merge-path K5 + K6 reading them ("mp"), or bisection inside K6 ("bisect");
+        // default by population size
+        const char *am = getenv("SMC_ANC");
+        ctx->anc_mode = am ? (strcmp(am, "mp") == 0 ? 1 : (strcmp(am, "bisect") == 0 ? 0 : -1)) : -1;
     }
     ctx->Lg = cfg->n_particles;
     smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
@@ -400,6 +406,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->tiles = (uint32_t *)(ws + L.tiles);
     ctx->C = (unsigned long long *)(ws + L.C);
     ctx->QR = (unsigned long long *)(ws + L.QR);
+    ctx->anc = (int32_t *)(ws + L.anc);
     ctx->accept = (unsigned long long *)(ws + L.accept);
     ctx->mpc_dev = (uint32_t *)(ws + L.mpc);
     ctx->dac = (DevAircraft *)(ws + L.dac);
@@ -776,6 +783,13 @@ static uint32_t samples_of(const smc_ctx *ctx, uint32_t k) {
     return ctx->cfg.n_samples;
 }
 
+// Merge-path ancestors (K5) pay once the CDF no longer sits in L2 and a bisection per
+// slot turns into DRAM misses; below that the extra launch costs more than it saves.
+static bool use_merge_path(const smc_ctx *ctx, uint32_t Lk) {
+    if (ctx->anc_mode >= 0) return ctx->anc_mode == 1;
+    return Lk >= (1u << 17);
+}
+
 static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     const uint32_t k = ctx->k;
     const int n = ctx->dsc.n, H = ctx->dsc.H;
@@ -856,6 +870,11 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
         pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
+        if (ctx->world == 1 && ctx->vworld == 1 && use_merge_path(ctx, Lk)) {
+            rs.anc = ctx->anc; rs.M = Ln;
+            LAUNCHP(PH_RESAMPLE, launch_ancestors(rs, ctx->st));
+            pa.anc = ctx->anc;
+        }
         pa.xp = ctx->ctrl[P ^ 1][0]; pa.xs = ctx->ctrl[P ^ 1][1];
         const double f = std::pow(ctx->cfg.anneal, (double)k);
         for (int c = 0; c < 3; ++c) pa.sig[c] = (float)(ctx->cfg.sigma[c] * f);
@@ -1260,7 +1279,7 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
     rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M;
     LAUNCH(launch_scan(rs, ctx->st));
-    LAUNCH(launch_ancestors(rs, ctx->st));
+    LAUNCH(ctx->anc_mode == 0 ? launch_ancestors_bisect(rs, ctx->st) : launch_ancestors(rs, ctx->st));
     CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * M, cudaMemcpyDeviceToHost, ctx->st));
     if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));

@@ -318,10 +318,86 @@ __global__ void k_ancestors(const ResampleArgs r) {
         r.anc[(size_t)i * r.M + j] = find_ancestor(r.C + (size_t)i * r.L, r.L, r.M, Q, R, j);
 }
 
-cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
+cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st) {
     unsigned gx = (r.M + 255) / 256;
     if (gx > 1024) gx = 1024;
     k_ancestors<<<dim3(gx, r.n), 256, 0, st>>>(r);
+    return cudaGetLastError();
+}
+
+// ============================================================== K5 (merge path)
+// The same ancestors as find_ancestor, without a bisection over the whole CDF per
+// slot.  Both C (sources) and t_j (slots) are non-decreasing, so a(j) =
+// #{l : C_l <= t_j} is the position of slot j in the merge of the two sequences
+// (a source goes first on ties).  Block b owns diagonals [bT, (b+1)T) of that
+// merge: it finds its two split points (a0, j0), (a1, j1) by a 32-ary warp search,
+// loads the window C[a0, a1) (<= T entries, coalesced) into shared memory and
+// gives every slot j in [j0, j1) the ancestor a0 + #{a in window : C_a <= t_j}
+// (bisection in shared memory).  Traffic: C read once, anc written once.
+constexpr int kMpThreads = 256, kMpTile = 2048;
+
+struct SlotGen {
+    uint64_t qd, qm, R, M;
+    __device__ uint64_t t(uint64_t j) const { return slot_t(j, qd, qm, R, M); }
+};
+
+// First a in [lo, hi) with C[a] > t(d - 1 - a) (hi if none): the merge-path split
+// at diagonal d.  All 32 lanes of a warp call it; each round probes 32 points.
+__device__ uint32_t mp_split(const unsigned long long *C, const SlotGen &g, uint64_t d, uint32_t lo, uint32_t hi) {
+    const int lane = threadIdx.x & 31;
+    while (lo < hi) {
+        const uint32_t span = hi - lo, step = (span + 31) / 32;
+        const uint32_t a = lo + (uint32_t)lane * step;
+        const bool ok = a < hi && __ldg(&C[a]) <= g.t(d - 1 - a);      // source a precedes slot d-1-a
+        const unsigned b = __ballot_sync(0xffffffffu, ok);
+        const int c = __popc(b);                                         // predicate true on a lane prefix
+        if (c == 0) break;                                               // answer = lo
+        const uint32_t last = lo + (uint32_t)(c - 1) * step;
+        lo = last + 1;
+        if (c < 32) hi = min(hi, lo - 1 + step);
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kMpThreads) k_ancestors_mp(const ResampleArgs r) {
+    __shared__ unsigned long long s_c[kMpTile];
+    __shared__ uint32_t s_split[2];
+    const int i = blockIdx.y;
+    const uint32_t L = r.L, M = r.M;
+    const unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : L);
+    const uint64_t Q = r.QR[2 * i];
+    const SlotGen g{Q / M, Q % M, r.QR[2 * i + 1], M};
+    const uint64_t total = (uint64_t)L + M;
+    const int w = threadIdx.x >> 5;
+    if (w < 2) {
+        const uint64_t d = min(total, (uint64_t)(blockIdx.x + w) * kMpTile);
+        const uint32_t lo = d > M ? (uint32_t)(d - M) : 0u, hi = (uint32_t)min(d, (uint64_t)L);
+        const uint32_t a = mp_split(C, g, d, lo, hi);
+        if ((threadIdx.x & 31) == 0) s_split[w] = a;
+    }
+    __syncthreads();
+    const uint32_t a0 = s_split[0], a1 = s_split[1];
+    const uint64_t d0 = (uint64_t)blockIdx.x * kMpTile, d1 = min(total, d0 + kMpTile);
+    const uint32_t j0 = (uint32_t)(d0 - a0), j1 = (uint32_t)(d1 - a1);
+    const int nw = (int)(a1 - a0);
+    for (int e = threadIdx.x; e < nw; e += kMpThreads) s_c[e] = __ldg(&C[a0 + e]);
+    __syncthreads();
+    int32_t *anc = r.anc + (size_t)i * M;
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kMpThreads) {
+        const uint64_t tj = g.t(j);
+        int lo = 0, hi = nw;                                             // first window entry with C > t_j
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_c[mid] > tj) hi = mid; else lo = mid + 1;
+        }
+        anc[j] = (int32_t)(a0 + (uint32_t)lo);
+    }
+}
+
+cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
+    if (!r.M || !r.L) return cudaSuccess;
+    const uint64_t blocks = ((uint64_t)r.L + r.M + kMpTile - 1) / kMpTile;
+    k_ancestors_mp<<<dim3((unsigned)blocks, r.n), kMpThreads, 0, st>>>(r);
     return cudaGetLastError();
 }
 

@@ -73,14 +73,15 @@ struct ResampleArgs {
     unsigned long long *C;      // [n][Cstride] inclusive integer CDF
     uint32_t Cstride;           // row stride of C (0 = L)
     unsigned long long *QR;     // [n][2] (Q, R)
-    int32_t *anc;               // [n][M] (k_ancestors only)
-    uint32_t M;                 // new particles drawn (k_ancestors only)
+    int32_t *anc;               // [n][M] (K5 ancestors only)
+    uint32_t M;                 // new particles drawn (K5 ancestors only)
 };
 int scan_tiles(uint32_t L);
 int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st);
-cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);
+cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);          // K5 merge path
+cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st);   // one bisection per slot
 
 // K6: gather survivors' rows by ancestor, Gaussian proposal (Alg.1 l.22-23)
 struct ProposeArgs {

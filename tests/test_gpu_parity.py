@@ -232,8 +232,12 @@ def test_per_aircraft_mh_rounds(smc, layout, monkeypatch):
     sol.close()
 
 
-@pytest.mark.parametrize("L", [1, 7, 2048, 2049, 5000, 70001])
-def test_resample_bitexact(smc, L):
+@pytest.mark.parametrize("mode", ["mp", "bisect"])
+@pytest.mark.parametrize("L", [1, 7, 2048, 2049, 5000, 70001, 300001])
+def test_resample_bitexact(smc, L, mode, monkeypatch):
+    """Ancestors bit-exact against the oracle, by the merge-path K5 and by the
+    per-slot bisection (SMC_ANC)."""
+    monkeypatch.setenv("SMC_ANC", mode)
     scn, cfg = sc.config(1)
     sol = _solver(smc, scn, seed=cfg.seed)
     rng = np.random.default_rng(L)
@@ -250,9 +254,11 @@ def test_resample_bitexact(smc, L):
             assert np.array_equal(anc[i], r["anc"]), (i, k, np.nonzero(anc[i] != r["anc"])[0][:10])
 
 
-@pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000)])
-def test_resample_to_fewer_bitexact(smc, L, M):
+@pytest.mark.parametrize("mode", ["mp", "bisect"])
+@pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000), (1, 1), (3, 1)])
+def test_resample_to_fewer_bitexact(smc, L, M, mode, monkeypatch):
     """Shrinking populations: M < L slots drawn from L particles."""
+    monkeypatch.setenv("SMC_ANC", mode)
     scn, cfg = sc.config(1)
     sol = _solver(smc, scn, seed=cfg.seed)
     rng = np.random.default_rng(L + M)
@@ -269,12 +275,16 @@ def test_resample_to_fewer_bitexact(smc, L, M):
             assert np.array_equal(anc[i], r["anc"]), (i, k)
 
 
-@pytest.mark.parametrize("L,Lf,S,K", [(256, 40, 4, 6), (140000, 60000, 2, 3)])
-def test_shrinking_population_rounds(smc, L, Lf, S, K):
+@pytest.mark.parametrize("L,Lf,S,K,mode", [(256, 40, 4, 6, None), (140000, 60000, 2, 3, None),
+                                           (256, 40, 4, 6, "mp"), (140000, 60000, 2, 3, "bisect")])
+def test_shrinking_population_rounds(smc, L, Lf, S, K, mode, monkeypatch):
     """Real rounds with L_k falling linearly to L_final: population
     sizes follow the oracle's schedule, each round's ancestors (read back from
     the next round's x' rows) are the oracle's resampling of the GPU's ell into
-    L_{k+1} slots, and the log-weights match the oracle's evaluation."""
+    L_{k+1} slots, and the log-weights match the oracle's evaluation.  Both
+    ancestor paths: merge-path K5 (default from 2^17 particles) and bisection."""
+    if mode:
+        monkeypatch.setenv("SMC_ANC", mode)
     scn, cfg = sc.config(1)
     sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, L_final=Lf)
     P = O.Problem(scn)
