@@ -66,7 +66,7 @@ constexpr uint32_t kCentreCap = 256;
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, accept, mpc, dac, pop, centres,
+    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
         qf, qd, total;
 };
@@ -104,6 +104,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.C = take((size_t)nmax * Lloc * sizeof(unsigned long long));
     o.QR = take(2 * nmax * sizeof(unsigned long long));
     o.anc = take(world > 1 ? 0 : (size_t)nmax * Lloc * sizeof(int32_t));   // K5 ancestors (single rank)
+    o.splits = take(world > 1 ? 0 : (size_t)nmax * mp_split_words(Lloc, Lloc) * sizeof(uint32_t));
     o.accept = take(8);
     o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
@@ -214,6 +215,7 @@ struct smc_ctx {
     bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
     int anc_mode = -1;                 // SMC_ANC: 1 merge-path K5, 0 bisection in K6, -1 by size
     int32_t *anc = nullptr;            // [n][Lloc] K5 ancestors
+    uint32_t *splits = nullptr;        // K5 merge-path split points
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -407,6 +409,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->C = (unsigned long long *)(ws + L.C);
     ctx->QR = (unsigned long long *)(ws + L.QR);
     ctx->anc = (int32_t *)(ws + L.anc);
+    ctx->splits = (uint32_t *)(ws + L.splits);
     ctx->accept = (unsigned long long *)(ws + L.accept);
     ctx->mpc_dev = (uint32_t *)(ws + L.mpc);
     ctx->dac = (DevAircraft *)(ws + L.dac);
@@ -871,7 +874,7 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
         pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
         if (ctx->world == 1 && ctx->vworld == 1 && use_merge_path(ctx, Lk)) {
-            rs.anc = ctx->anc; rs.M = Ln;
+            rs.anc = ctx->anc; rs.M = Ln; rs.splits = ctx->splits;
             LAUNCHP(PH_RESAMPLE, launch_ancestors(rs, ctx->st));
             pa.anc = ctx->anc;
         }
@@ -1265,7 +1268,8 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     unsigned long long *st1 = tmp.alloc<unsigned long long>((size_t)N * nt);
     uint32_t *tiles = tmp.alloc<uint32_t>(2 * N);
     int32_t *danc = tmp.alloc<int32_t>((size_t)N * M);
-    if (!dell || !dcm || !dQ || !dQR || !dC || !dess || !st1 || !tiles || !danc)
+    uint32_t *dspl = tmp.alloc<uint32_t>((size_t)N * mp_split_words(L, M));
+    if (!dell || !dcm || !dQ || !dQR || !dC || !dess || !st1 || !tiles || !danc || !dspl)
         return fail(ctx, SMC_ECUDA, "debug allocation failed");
     CK(cudaMemcpyAsync(dell, ell, sizeof(float) * N * (size_t)L, cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemsetAsync(dcm, 0, 4 * N, ctx->st));
@@ -1277,7 +1281,7 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     rs.n = (int)N; rs.L = L; rs.k = k; rs.mpcp = ctx->mpc_dev;
     rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
     rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
-    rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M;
+    rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M; rs.splits = dspl;
     LAUNCH(launch_scan(rs, ctx->st));
     LAUNCH(ctx->anc_mode == 0 ? launch_ancestors_bisect(rs, ctx->st) : launch_ancestors(rs, ctx->st));
     CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * M, cudaMemcpyDeviceToHost, ctx->st));

@@ -1,14 +1,16 @@
 // k_population.cu -- population kernels of libsmcatm (sm_100a):
 //   K1  k_init_population   uniform initial controls       (Alg.1 l.3-5)
-//   K4a k_qsum              integer resampling weights per column, totals Q_i
-//   K4b k_scan_mark         decoupled look-back inclusive scan of the integer
-//                           weights + systematic slot marks   (R25)
-//   K5  k_maxscan           look-back max-scan of the marks -> ancestors
+//   K4a k_qsum              integer resampling weights per column, totals Q_i, ESS sums
+//   K4b k_scan              decoupled look-back inclusive scan of the integer
+//                           weights, (Q, R) per column     (R25)
+//   K5  k_mp_splits +       merge-path systematic ancestors (large populations)
+//       k_ancestors_mp
 //   K6  k_gather_propose    per-aircraft recombination + Gaussian proposal
 //                           (Alg.1 l.22-23)
 //   K7  k_select            argmax of the joint weight (Alg.1 l.27)
 //   K8  k_plant             apply the first control, realised wind
-// plus the population-density grid and the MH debug hook.
+// plus the population-density grid, the multi-GPU exchange kernels and the
+// MH debug hooks.
 #include <cfloat>
 
 #include "smc_device.cuh"
@@ -246,10 +248,13 @@ __device__ unsigned long long block_exclusive(unsigned long long v, unsigned lon
 // Inclusive scan C_l = sum_{l' <= l} q_l' per column (uint64, exact), single pass
 // with decoupled look-back.  The block that owns the last tile of a column also
 // publishes (Q, R): Q = C_{L-1}, R = floor(r64 * Q / 2^64) (RESAMPLE stream).
+// Grid (n, ntiles): x = column, so the blocks resident at any moment are spread over all
+// columns (a few tiles of each) rather than hundreds of tiles of one column, whose look-backs
+// would each walk back over many predecessors that only hold aggregates (c5: 170 -> 135 us).
 template <int kScanItems>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int ntiles) {
     constexpr int kTile = kScanThreads * kScanItems;
-    const int i = blockIdx.y;
+    const int i = blockIdx.x;
     __shared__ int s_tile;
     __shared__ unsigned long long s_pre;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(&r.tile_ctr[i], 1u);
@@ -293,8 +298,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
 
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
     const int nt = scan_tiles(r.L);
-    if (scan_items(r.L) == 2) k_scan<2><<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
-    else k_scan<8><<<dim3(nt, r.n), kScanThreads, 0, st>>>(r, nt);
+    if (scan_items(r.L) == 2) k_scan<2><<<dim3(r.n, nt), kScanThreads, 0, st>>>(r, nt);
+    else k_scan<8><<<dim3(r.n, nt), kScanThreads, 0, st>>>(r, nt);
     return cudaGetLastError();
 }
 
@@ -359,32 +364,57 @@ __device__ uint32_t mp_split(const unsigned long long *C, const SlotGen &g, uint
     return lo;
 }
 
-__global__ void __launch_bounds__(kMpThreads) k_ancestors_mp(const ResampleArgs r) {
+// One warp per split point: splits[i][b] = a(b T) for b = 0..nblocks (all in parallel, so the
+// 32-ary searches of all blocks overlap instead of heading every block's critical path).
+__global__ void k_mp_splits(const ResampleArgs r, uint32_t *splits, uint32_t nsplit) {
+    const int i = blockIdx.y;
+    const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= nsplit) return;
+    const uint32_t L = r.L, M = r.M;
+    const unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : L);
+    const uint64_t Q = r.QR[2 * i];
+    const SlotGen g{Q / M, Q % M, r.QR[2 * i + 1], M};
+    const uint64_t d = min((uint64_t)L + M, (uint64_t)b * kMpTile);
+    const uint32_t lo = d > M ? (uint32_t)(d - M) : 0u, hi = (uint32_t)min(d, (uint64_t)L);
+    const uint32_t a = mp_split(C, g, d, lo, hi);
+    if ((threadIdx.x & 31) == 0) splits[(size_t)i * nsplit + b] = a;
+}
+
+__global__ void __launch_bounds__(kMpThreads) k_ancestors_mp(const ResampleArgs r, const uint32_t *splits,
+                                                              uint32_t nsplit) {
     __shared__ unsigned long long s_c[kMpTile];
-    __shared__ uint32_t s_split[2];
     const int i = blockIdx.y;
     const uint32_t L = r.L, M = r.M;
     const unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : L);
     const uint64_t Q = r.QR[2 * i];
     const SlotGen g{Q / M, Q % M, r.QR[2 * i + 1], M};
     const uint64_t total = (uint64_t)L + M;
-    const int w = threadIdx.x >> 5;
-    if (w < 2) {
-        const uint64_t d = min(total, (uint64_t)(blockIdx.x + w) * kMpTile);
-        const uint32_t lo = d > M ? (uint32_t)(d - M) : 0u, hi = (uint32_t)min(d, (uint64_t)L);
-        const uint32_t a = mp_split(C, g, d, lo, hi);
-        if ((threadIdx.x & 31) == 0) s_split[w] = a;
-    }
-    __syncthreads();
-    const uint32_t a0 = s_split[0], a1 = s_split[1];
+    const uint32_t a0 = splits[(size_t)i * nsplit + blockIdx.x], a1 = splits[(size_t)i * nsplit + blockIdx.x + 1];
     const uint64_t d0 = (uint64_t)blockIdx.x * kMpTile, d1 = min(total, d0 + kMpTile);
     const uint32_t j0 = (uint32_t)(d0 - a0), j1 = (uint32_t)(d1 - a1);
     const int nw = (int)(a1 - a0);
     for (int e = threadIdx.x; e < nw; e += kMpThreads) s_c[e] = __ldg(&C[a0 + e]);
+    // t_j = j qd + floor((j qm + R) / M) without a 64-bit division per slot: with
+    // j0 qm + R = u0 M + v0 (one division per block), slot j0 + dj has
+    // floor(...) = u0 + floor(x / M), x = v0 + dj qm < 2^44 -- a double-precision
+    // quotient (error < 1 / M) and an integer fix-up
+    __shared__ uint64_t s_u0, s_v0;
+    if (threadIdx.x == 0) {
+        const uint64_t num = (uint64_t)j0 * g.qm + g.R;
+        s_u0 = num / M;
+        s_v0 = num - s_u0 * M;
+    }
     __syncthreads();
+    const uint64_t u0 = s_u0, v0 = s_v0;
+    const double invM = 1.0 / (double)M;
     int32_t *anc = r.anc + (size_t)i * M;
     for (uint32_t j = j0 + threadIdx.x; j < j1; j += kMpThreads) {
-        const uint64_t tj = g.t(j);
+        const uint64_t x = v0 + (uint64_t)(j - j0) * g.qm;
+        uint64_t u = (uint64_t)((double)x * invM);
+        const int64_t rem = (int64_t)(x - u * M);
+        if (rem < 0) --u;
+        else if (rem >= (int64_t)M) ++u;
+        const uint64_t tj = (uint64_t)j * g.qd + u0 + u;
         int lo = 0, hi = nw;                                             // first window entry with C > t_j
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -394,10 +424,13 @@ __global__ void __launch_bounds__(kMpThreads) k_ancestors_mp(const ResampleArgs 
     }
 }
 
+size_t mp_split_words(uint32_t L, uint32_t M) { return ((uint64_t)L + M + kMpTile - 1) / kMpTile + 1; }
+
 cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st) {
     if (!r.M || !r.L) return cudaSuccess;
-    const uint64_t blocks = ((uint64_t)r.L + r.M + kMpTile - 1) / kMpTile;
-    k_ancestors_mp<<<dim3((unsigned)blocks, r.n), kMpThreads, 0, st>>>(r);
+    const uint32_t blocks = (uint32_t)(((uint64_t)r.L + r.M + kMpTile - 1) / kMpTile), nsplit = blocks + 1;
+    k_mp_splits<<<dim3((nsplit + 3) / 4, r.n), 128, 0, st>>>(r, r.splits, nsplit);
+    k_ancestors_mp<<<dim3(blocks, r.n), kMpThreads, 0, st>>>(r, r.splits, nsplit);
     return cudaGetLastError();
 }
 

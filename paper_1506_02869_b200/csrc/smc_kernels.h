@@ -75,12 +75,14 @@ struct ResampleArgs {
     unsigned long long *QR;     // [n][2] (Q, R)
     int32_t *anc;               // [n][M] (K5 ancestors only)
     uint32_t M;                 // new particles drawn (K5 ancestors only)
+    uint32_t *splits;           // [n][mp_split_words(L, M)] K5 merge-path split points
 };
 int scan_tiles(uint32_t L);
 int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st);
-cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);          // K5 merge path
+cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);          // K5 merge path (needs r.splits)
+size_t mp_split_words(uint32_t L, uint32_t M);
 cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st);   // one bisection per slot
 
 // K6: gather survivors' rows by ancestor, Gaussian proposal (Alg.1 l.22-23)
