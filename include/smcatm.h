@@ -162,8 +162,15 @@ size_t smc_workspace_bytes(const smc_config *cfg);
  * global particles [L r / G, L (r+1) / G); every random stream is keyed by the
  * global particle index, so rollouts, MH decisions and ancestors are identical
  * for any world size.  Each round then exchanges the column maxima
- * (all-reduce MAX), the per-rank integer CDFs and the compacted survivor rows
- * (all-gather) on cfg.stream; selection all-gathers per-rank winners. */
+ * (all-reduce MAX) and the per-rank integer CDFs (all-gather) on cfg.stream,
+ * and each rank's gather reads its parents' control rows where their owner
+ * keeps them (peer mode, the default): smc_init exports the allocation holding
+ * cfg.workspace as a CUDA IPC handle, all-gathers the handles and maps every
+ * peer's workspace (NVLink/NVSwitch loads; the mappings are closed by
+ * smc_destroy, so every rank's workspace must outlive every rank's context).
+ * With the environment variable SMC_P2P=0 (read by smc_workspace_bytes and
+ * smc_init alike) the compacted survivor rows are all-gathered instead.
+ * Selection all-gathers per-rank winners.  SMC_ECUDA if the IPC mapping fails. */
 smc_status smc_init(const smc_config *cfg, smc_ctx **out);
 
 /* Copy the scenario, precompute (Qhat = chol(Rhat) P:463-465, normalisers
@@ -213,6 +220,14 @@ void smc_destroy(smc_ctx *ctx);
 /* Set / read the MPC step index (keys all streams; mpc_step increments it). */
 smc_status smc_set_mpc_index(smc_ctx *ctx, uint32_t mpc_index);
 uint32_t smc_get_mpc_index(const smc_ctx *ctx);
+
+/* Peer-mode test hooks.  smc_ipc_record writes the 128-byte record a rank
+ * publishes in peer mode (CUDA IPC handle of the allocation holding the
+ * workspace + the workspace's offset in it).  smc_ipc_peek, called in ANOTHER
+ * process, maps such a record, copies `bytes` bytes from workspace offset
+ * `offset` to host_out and unmaps.  SMC_ECUDA on any CUDA IPC failure. */
+smc_status smc_ipc_record(const smc_ctx *ctx, void *out128);
+smc_status smc_ipc_peek(const void *rec128, uint64_t offset, void *host_out, size_t bytes);
 
 /* 128-byte NCCL unique id for a multi-GPU context (call on rank 0, share
  * with every rank, pass as smc_config.nccl_unique_id).  SMC_ENCCL if NCCL

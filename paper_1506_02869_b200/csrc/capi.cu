@@ -62,12 +62,13 @@ NcclApi *nccl_api() {
 
 constexpr uint32_t kPopCap = 256 * 256;
 constexpr uint32_t kCentreCap = 256;
+constexpr size_t kIpcRec = 128;     // cudaIpcMemHandle_t (64 B) + workspace offset in its allocation
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, accept, mpc, dac, pop, centres,
-        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
+        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, survp, ipc, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
         qf, qd, total;
 };
 
@@ -83,7 +84,16 @@ size_t record_bytes(int nmax, int Hmax) { return (16 + (size_t)nmax * Hmax * 12 
 
 // world: real ranks (Lloc = this rank's share); vworld: virtual ranks inside one context
 // (test mode, Lloc = L).  G = ranks whose CDFs / survivors / records are exchanged.
+// Multi-rank exchange of parent rows: in place from the owner (peer mode: NVLink reads
+// through CUDA IPC mappings, or slices of one buffer for virtual ranks -- the default), or
+// an all-gather of every rank's compacted survivor rows (SMC_P2P=0).
+bool p2p_mode() {
+    const char *e = getenv("SMC_P2P");
+    return !(e && strcmp(e, "0") == 0);
+}
+
 Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) {
+    const bool p2p = p2p_mode();
     const int G = world > 1 ? world : vworld;
     const uint32_t Lx = world > 1 ? Lloc : (Lloc + vworld - 1) / vworld;   // per-rank stride
     Layout o{};
@@ -117,8 +127,10 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.best_idx = take(record_bytes(nmax, Hmax));               // final (merged) record
     o.best_row = take(G > 1 ? record_bytes(nmax, Hmax) * G : 0);           // all-gathered records
     o.Call = take(G > 1 ? (size_t)G * nmax * Lx * 8 : 0);
-    o.Sc = take(world > 1 ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
-    o.Sall = take(G > 1 ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.Sc = take(world > 1 && !p2p ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.Sall = take(G > 1 && !p2p ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.survp = take(world > 1 && p2p ? 2 * (size_t)Lloc * sizeof(uint32_t) : 0);   // published masks, by round parity
+    o.ipc = take(world > 1 && p2p ? (size_t)(G + 1) * kIpcRec : 0);              // IPC handle exchange
     o.pZ = take(2 * kMaxWindNodes * sizeof(double));
     o.pzi = take(sizeof(int));
     o.pstates = take(nmax * 6 * sizeof(double));
@@ -195,6 +207,12 @@ struct smc_ctx {
     ncclComm_t comm = nullptr;
     unsigned long long *Call = nullptr;
     float *Sc = nullptr, *Sall = nullptr;
+    // peer mode (world > 1): every rank's population buffers mapped into this process
+    bool p2p = false;
+    uint32_t *survp = nullptr;                 // [2][Lmax] this rank's published survivor masks
+    const float *peer_ctrl[8] = {};            // rank r's control buffers (4 x prow floats)
+    const uint32_t *peer_survp[8] = {};        // rank r's published masks
+    void *peer_open[8] = {};                   // IPC mappings to close
 
     bool have_scn = false;
     DevScen dsc{};
@@ -242,6 +260,8 @@ struct smc_ctx {
     }
     ~smc_ctx() {
         drop_graph();
+        for (void *p : peer_open)
+            if (p) cudaIpcCloseMemHandle(p);
         if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
         for (auto &v : ev_used)
             for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -332,6 +352,81 @@ extern "C" size_t smc_workspace_bytes(const smc_config *cfg) {
     const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
     const int vw = (world == 1 && cfg->virtual_world > 1) ? (int)cfg->virtual_world : 1;
     return layout(max_local(cfg->n_particles, world), cfg->max_aircraft, cfg->max_horizon, world, vw).total;
+}
+
+// Peer mode: export this rank's workspace allocation as a CUDA IPC handle, all-gather the
+// handles (NCCL, through the ipc scratch), and map every other rank's allocation.  The
+// workspace is a sub-range of a caller (torch) allocation, so each record carries the
+// workspace's offset from its allocation base (driver cuMemGetAddressRange).
+static cudaError_t ipc_record(const void *ws, unsigned char rec[kIpcRec]) {
+    typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        if (h) get_range = (GetRange)dlsym(h, "cuMemGetAddressRange_v2");
+    }
+    if (!get_range) return cudaErrorNotSupported;
+    unsigned long long base = 0;
+    size_t bytes = 0;
+    if (get_range(&base, &bytes, (unsigned long long)(uintptr_t)ws) != 0) return cudaErrorInvalidDevicePointer;
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (e != cudaSuccess) return e;
+    const uint64_t off = (uint64_t)((uintptr_t)ws - base);
+    memset(rec, 0, kIpcRec);
+    memcpy(rec, &h, sizeof(h));
+    memcpy(rec + sizeof(h), &off, sizeof(off));
+    return cudaSuccess;
+}
+
+// Map a peer's record: *mapping = the opened allocation (to close), *ws = its workspace.
+static cudaError_t ipc_open(const unsigned char *rec, void **mapping, char **ws) {
+    cudaIpcMemHandle_t h;
+    uint64_t off;
+    memcpy(&h, rec, sizeof(h));
+    memcpy(&off, rec + sizeof(h), sizeof(off));
+    void *p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return e;
+    *mapping = p;
+    *ws = (char *)p + off;
+    return cudaSuccess;
+}
+
+static smc_status map_peers(smc_ctx *ctx) {
+    unsigned char rec[kIpcRec];
+    CK(ipc_record(ctx->ws, rec));
+    const int G = ctx->world;
+    unsigned char *dipc = (unsigned char *)ctx->ws + ctx->lay.ipc;
+    CK(cudaMemcpyAsync(dipc + (size_t)G * kIpcRec, rec, kIpcRec, cudaMemcpyHostToDevice, ctx->st));
+    NCK(nccl_api()->AllGather(dipc + (size_t)G * kIpcRec, dipc, kIpcRec, ncclUint8_, ctx->comm, ctx->st));
+    std::vector<unsigned char> all((size_t)G * kIpcRec);
+    CK(cudaMemcpyAsync(all.data(), dipc, all.size(), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    for (int r = 0; r < G; ++r) {
+        char *pws = (char *)ctx->ws;
+        if (r != ctx->rank) CK(ipc_open(all.data() + (size_t)r * kIpcRec, &ctx->peer_open[r], &pws));
+        // every rank carves the same layout (same config), so offsets agree
+        ctx->peer_ctrl[r] = (const float *)(pws + ctx->lay.ctrl);
+        ctx->peer_survp[r] = (const uint32_t *)(pws + ctx->lay.survp);
+    }
+    return SMC_OK;
+}
+
+// Test hooks of the peer mapping (one GPU, two processes, no kernel waits on another).
+extern "C" smc_status smc_ipc_record(const smc_ctx *ctx, void *out128) {
+    if (!ctx || !out128) return SMC_EINVAL;
+    return ipc_record(ctx->ws, (unsigned char *)out128) == cudaSuccess ? SMC_OK : SMC_ECUDA;
+}
+
+extern "C" smc_status smc_ipc_peek(const void *rec128, uint64_t offset, void *host_out, size_t bytes) {
+    if (!rec128 || !host_out) return SMC_EINVAL;
+    void *map = nullptr;
+    char *ws = nullptr;
+    if (ipc_open((const unsigned char *)rec128, &map, &ws) != cudaSuccess) return SMC_ECUDA;
+    const cudaError_t e = cudaMemcpy(host_out, ws + offset, bytes, cudaMemcpyDeviceToHost);
+    cudaIpcCloseMemHandle(map);
+    return e == cudaSuccess ? SMC_OK : SMC_ECUDA;
 }
 
 extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
@@ -432,6 +527,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->Call = (unsigned long long *)(ws + L.Call);
     ctx->Sc = (float *)(ws + L.Sc);
     ctx->Sall = (float *)(ws + L.Sall);
+    ctx->p2p = p2p_mode() && (world > 1 || ctx->vworld > 1);
+    ctx->survp = (uint32_t *)(ws + L.survp);
     ctx->pZ = (double *)(ws + L.pZ);
     ctx->pzi = (int *)(ws + L.pzi);
     ctx->pstates = (double *)(ws + L.pstates);
@@ -460,6 +557,10 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_unique_id, sizeof(id));
         if (api->CommInitRank(&ctx->comm, world, id, cfg->rank) != 0) { ctx->comm = nullptr; delete ctx; return SMC_ENCCL; }
+        if (ctx->p2p) {
+            const smc_status s = map_peers(ctx);
+            if (s != SMC_OK) { delete ctx; return s; }
+        }
     }
     *out = ctx;
     return SMC_OK;
@@ -843,6 +944,12 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
                                      : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
     ctx->Leval = Lk;
+    if (ctx->world > 1 && ctx->p2p && tail)
+        // publish this round's survivor masks for the peers' gathers (by round parity: a peer
+        // may still read the previous round's copy; the one before is fenced by this round's
+        // all-reduce, which no peer passes before finishing its previous gather)
+        CK(cudaMemcpyAsync(ctx->survp + (size_t)(k & 1) * ctx->Lmax, ctx->surv, 4 * (size_t)ctx->Lloc,
+                           cudaMemcpyDeviceToDevice, ctx->st));
     if (ctx->world > 1)                    // global column maxima (reduce step 1)
         NCK(nccl_api()->AllReduce(ctx->colmax, ctx->colmax, n, ncclUint32_, ncclMax_, ctx->comm, ctx->st));
     ResampleArgs rs{};
@@ -899,9 +1006,11 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
                 CK(cudaMemsetAsync(ctx->status, 0, 8 * ntv * n, ctx->st));
                 CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
                 LAUNCHP(PH_RESAMPLE, launch_scan(rr, ctx->st));
-                LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0] + (size_t)b * rowlen,
-                                                             ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b, n,
-                                                             rowlen, ctx->Sall + (size_t)r * ctx->Lmax * rowlen, ctx->st));
+                if (!ctx->p2p)
+                    LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0] + (size_t)b * rowlen,
+                                                                 ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b,
+                                                                 n, rowlen, ctx->Sall + (size_t)r * ctx->Lmax * rowlen,
+                                                                 ctx->st));
             }
             for (int r = 0; r < G; ++r) {
                 uint32_t b, e;
@@ -910,7 +1019,17 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
                 pr.L = e - b; pr.l0 = b;
                 pr.xp = ctx->ctrl[P ^ 1][0] + (size_t)b * rowlen; pr.xs = ctx->ctrl[P ^ 1][1] + (size_t)b * rowlen;
                 pr.reset_status_n = 0;
-                MultiArgs ma{pr, ctx->Lg, ctx->Lmax, G, ctx->Call, ctx->Sall};
+                MultiArgs ma{pr, ctx->Lg, ctx->Lmax, G, ctx->Call, ctx->p2p ? nullptr : ctx->Sall, {}, {}, 0};
+                if (ctx->p2p) {
+                    // virtual rank q's buffers are the row slice [b_q, e_q) of this context's own
+                    ma.prow = (size_t)(ctx->ctrl[P][1] - ctx->ctrl[P][0]);
+                    for (int q = 0; q < G; ++q) {
+                        uint32_t bq, eq;
+                        smc_shard_range(ctx->Lg, G, q, &bq, &eq);
+                        ma.peer_ctrl[q] = ctx->ctrl[P][0] + (size_t)bq * rowlen;
+                        ma.peer_surv[q] = ctx->surv + bq;
+                    }
+                }
                 LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
             }
             CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
@@ -918,10 +1037,22 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         } else if (ctx->world > 1) {
             // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
             NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
-            LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc, n,
-                                                         n * H * 3, ctx->Sc, ctx->st));
-            NCK(nccl_api()->AllGather(ctx->Sc, ctx->Sall, (size_t)ctx->Lmax * n * H * 3, ncclFloat32_, ctx->comm, ctx->st));
-            MultiArgs ma{pa, ctx->Lg, ctx->Lmax, ctx->world, ctx->Call, ctx->Sall};
+            MultiArgs ma{pa, ctx->Lg, ctx->Lmax, ctx->world, ctx->Call, nullptr, {}, {}, 0};
+            if (ctx->p2p) {
+                // parents read in place over NVLink: rank r's current pair and published masks
+                const size_t prow = (size_t)(ctx->ctrl[0][1] - ctx->ctrl[0][0]);
+                ma.prow = prow;
+                for (int r = 0; r < ctx->world; ++r) {
+                    ma.peer_ctrl[r] = ctx->peer_ctrl[r] + (size_t)(2 * P) * prow;
+                    ma.peer_surv[r] = ctx->peer_survp[r] + (size_t)(k & 1) * ctx->Lmax;
+                }
+            } else {
+                LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc, n,
+                                                             n * H * 3, ctx->Sc, ctx->st));
+                NCK(nccl_api()->AllGather(ctx->Sc, ctx->Sall, (size_t)ctx->Lmax * n * H * 3, ncclFloat32_, ctx->comm,
+                                          ctx->st));
+                ma.Sall = ctx->Sall;
+            }
             LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
         } else {
             LAUNCHP(PH_PROPOSE, launch_gather_propose(pa, ctx->st));

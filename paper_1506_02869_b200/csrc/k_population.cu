@@ -842,9 +842,10 @@ cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uin
 }
 
 // Gather + propose for this rank's new particles from the all-gathered
-// per-rank CDFs Call[G][n][Lmax] (local inclusive sums) and survivor rows
-// Sall[G][Lmax][n][H][3].  Global CDF = rank offset + local CDF, so the
-// ancestors equal the single-GPU ones bit for bit (G-invariance).
+// per-rank CDFs Call[G][n][Lmax] (local inclusive sums) and the parents'
+// survivor rows -- read in place from their owner (peer mode) or from the
+// all-gathered compacted rows Sall[G][Lmax][n][H][3].  Global CDF = rank offset
+// + local CDF, so the ancestors equal the single-GPU ones bit for bit (G-invariance).
 __global__ void k_gather_propose_multi(const MultiArgs m) {
     const ProposeArgs &p = m.p;
     const size_t total = (size_t)p.L * p.n;
@@ -874,7 +875,14 @@ __global__ void k_gather_propose_multi(const MultiArgs m) {
             const uint32_t mid = (lo + hi) >> 1;
             if (__ldg(&C[mid]) > tl) hi = mid; else lo = mid + 1;
         }
-        const float *src = m.Sall + (((size_t)rho * m.Lmax + lo) * p.n + i) * p.H * 3;
+        const float *src;
+        if (m.Sall) {
+            src = m.Sall + (((size_t)rho * m.Lmax + lo) * p.n + i) * p.H * 3;
+        } else {
+            // the parent's survivor row where its owner keeps it: x' or x* by its mask bit
+            const uint32_t bit = (__ldg(&m.peer_surv[rho][lo]) >> i) & 1u;
+            src = m.peer_ctrl[rho] + bit * m.prow + ((size_t)lo * p.n + i) * p.H * 3;
+        }
         float *dp = p.xp + idx * p.H * 3;
         float *ds = p.xs + idx * p.H * 3;
         const float *lo3 = p.lo3 + 3 * i, *hi3 = p.hi3 + 3 * i;

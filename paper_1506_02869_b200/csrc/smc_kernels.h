@@ -114,7 +114,14 @@ struct MultiArgs {
     uint32_t Lg, Lmax;          // global particles, per-rank stride
     int G;                      // ranks (<= 8)
     const unsigned long long *Call;   // [G][n][Lmax] per-rank inclusive CDFs
-    const float *Sall;          // [G][Lmax][n][H][3] per-rank survivor rows
+    const float *Sall;          // [G][Lmax][n][H][3] per-rank survivor rows (all-gather mode)
+    // peer mode (Sall == NULL): parent rows read in place from the owning rank's population
+    // buffers -- over NVLink through CUDA IPC mappings, or slices of one buffer (virtual ranks).
+    // Rank r's survivor pair is peer_ctrl[r] + c * prow (c = 0: x', 1: x*, rows [Lmax][n][H][3]);
+    // its survivor masks peer_surv[r][0, Lmax).
+    const float *peer_ctrl[8];
+    const uint32_t *peer_surv[8];
+    size_t prow;                // floats between x' and x* of one pair
 };
 cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
                                      int rowlen, float *out, cudaStream_t st);

@@ -132,6 +132,8 @@ def load():
         "smc_shard_offsets": (None, [u32, C.c_int32, C.c_int32, P(u64), P(u64), P(u64)]),
         "smc_slot_count": (u64, [u64, u64, u64, u32]),
         "smc_fuel_estimates": (st, [C.POINTER(FuelArgs), v]),
+        "smc_ipc_record": (st, [v, v]),
+        "smc_ipc_peek": (st, [v, u64, v, C.c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -145,7 +147,7 @@ EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate"
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
             "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh", "smc_debug_mh_aircraft",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
-            "smc_shard_offsets", "smc_slot_count", "smc_fuel_estimates"]
+            "smc_shard_offsets", "smc_slot_count", "smc_fuel_estimates", "smc_ipc_record", "smc_ipc_peek"]
 
 
 def _p(a, ct):
@@ -191,6 +193,16 @@ def pack_scenario(scn: dict):
     s.nominal[:] = [float(v) for v in scn["nominal"]]
     s.wind_n[:] = [int(v) for v in scn.get("wind_n", (2, 2, 2))]
     return s, [ac, ty, cen]
+
+
+def ipc_peek(record: bytes, offset: int, nbytes: int) -> bytes:
+    """Map another process's peer-mode record and copy nbytes from its workspace."""
+    lib = load()
+    out = C.create_string_buffer(nbytes)
+    rc = lib.smc_ipc_peek(C.create_string_buffer(record, 128), int(offset), out, int(nbytes))
+    if rc != SMC_OK:
+        raise SmcError(rc, "smc_ipc_peek failed")
+    return out.raw
 
 
 class Solver:
@@ -276,6 +288,12 @@ class Solver:
         a, b = C.c_uint64(), C.c_uint64()
         self.lib.smc_io_bytes(self.ctx, C.byref(a), C.byref(b))
         return a.value, b.value
+
+    def ipc_record(self) -> bytes:
+        """128-byte peer-mode record of this context's workspace (CUDA IPC handle + offset)."""
+        buf = C.create_string_buffer(128)
+        self._check(self.lib.smc_ipc_record(self.ctx, buf))
+        return buf.raw
 
     @property
     def mpc_index(self):

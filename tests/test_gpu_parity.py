@@ -519,10 +519,14 @@ def test_paper_literal_mode_replay(smc):
 
 
 @pytest.mark.parametrize("num,vw,mh", [(1, 2, 1), (2, 3, 1), (5, 4, 1), (2, 3, 2)])
-def test_virtual_ranks_bitexact(smc, num, vw, mh):
+@pytest.mark.parametrize("exchange", ["peer", "allgather"])
+def test_virtual_ranks_bitexact(smc, num, vw, mh, exchange, monkeypatch):
     """G-invariance on one GPU: the multi-GPU resampling path (per-rank CDFs,
-    rank-offset bisection, survivor exchange layout, record merge) run for vw
-    virtual ranks reproduces the single-rank populations bit for bit."""
+    rank-offset bisection, record merge; parent rows read in place from their
+    owner's buffers -- the NVLink peer mode -- or from the all-gathered compacted
+    survivor rows) run for vw virtual ranks reproduces the single-rank
+    populations bit for bit."""
+    monkeypatch.setenv("SMC_P2P", "1" if exchange == "peer" else "0")
     scn, cfg = sc.config(num)
     L = min(cfg.L, 65536 + 123)
     res = []
@@ -616,3 +620,25 @@ def test_fuel_estimates_parity(smc):
         assert out["flags"][j] == (f1 | f2), j
         assert out["fuel"][j, 0] == pytest.approx(m0[j] - m1[-1], rel=1e-12, abs=1e-9)
     assert (out["flags"] & 2).any() and (out["flags"] & 1).any()
+
+
+def test_peer_mapping_ipc(smc, tmp_path):
+    """The CUDA IPC export/map that peer mode uses (smc_init with world_size > 1
+    maps every peer's workspace this way): a second process maps this
+    context's record -- handle of the torch allocation holding the workspace
+    plus the workspace's offset in it -- and reads the initial population at
+    workspace offset 0 (the x' buffer) byte for byte."""
+    import os
+    import subprocess
+    import sys
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, L=300, seed=cfg.seed)
+    pop = sol.population()
+    rec = sol.ipc_record()
+    out = tmp_path / "peek.bin"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (f"import sys; sys.path.insert(0, {root!r}); from paper_1506_02869_b200 import smcatm; "
+            f"open({str(out)!r}, 'wb').write(smcatm.ipc_peek(bytes.fromhex({rec.hex()!r}), 0, {pop['cur'].nbytes}))")
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=300)
+    assert out.read_bytes() == pop["cur"].tobytes()
+    sol.close()
