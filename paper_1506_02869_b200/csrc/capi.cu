@@ -21,6 +21,8 @@
 
 using namespace smc;
 
+static void ipc_release(void *mapping);
+
 namespace {
 
 // ---- NCCL, loaded at run time (only multi-GPU contexts need it; the ABI types are stable)
@@ -261,7 +263,7 @@ struct smc_ctx {
     ~smc_ctx() {
         drop_graph();
         for (void *p : peer_open)
-            if (p) cudaIpcCloseMemHandle(p);
+            if (p) ipc_release(p);
         if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
         for (auto &v : ev_used)
             for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -379,18 +381,44 @@ static cudaError_t ipc_record(const void *ws, unsigned char rec[kIpcRec]) {
     return cudaSuccess;
 }
 
-// Map a peer's record: *mapping = the opened allocation (to close), *ws = its workspace.
+// A handle may be opened once per process: mappings are shared and reference-counted
+// (two contexts -- e.g. bench.py's timed and profiled solvers -- may map the same peer
+// allocation when the peer's caching allocator placed both workspaces in one segment).
+struct IpcMapping { cudaIpcMemHandle_t h; void *p; int refs; };
+static std::vector<IpcMapping> &ipc_cache() { static std::vector<IpcMapping> c; return c; }
+
+// Map a peer's record: *mapping = the opened allocation (to release), *ws = its workspace.
 static cudaError_t ipc_open(const unsigned char *rec, void **mapping, char **ws) {
     cudaIpcMemHandle_t h;
     uint64_t off;
     memcpy(&h, rec, sizeof(h));
     memcpy(&off, rec + sizeof(h), sizeof(off));
+    for (auto &m : ipc_cache())
+        if (memcmp(&m.h, &h, sizeof(h)) == 0) {
+            ++m.refs;
+            *mapping = m.p;
+            *ws = (char *)m.p + off;
+            return cudaSuccess;
+        }
     void *p = nullptr;
     const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return e;
+    ipc_cache().push_back({h, p, 1});
     *mapping = p;
     *ws = (char *)p + off;
     return cudaSuccess;
+}
+
+static void ipc_release(void *mapping) {
+    auto &c = ipc_cache();
+    for (size_t q = 0; q < c.size(); ++q)
+        if (c[q].p == mapping) {
+            if (--c[q].refs == 0) {
+                cudaIpcCloseMemHandle(mapping);
+                c.erase(c.begin() + (long)q);
+            }
+            return;
+        }
 }
 
 static smc_status map_peers(smc_ctx *ctx) {
@@ -425,7 +453,7 @@ extern "C" smc_status smc_ipc_peek(const void *rec128, uint64_t offset, void *ho
     char *ws = nullptr;
     if (ipc_open((const unsigned char *)rec128, &map, &ws) != cudaSuccess) return SMC_ECUDA;
     const cudaError_t e = cudaMemcpy(host_out, ws + offset, bytes, cudaMemcpyDeviceToHost);
-    cudaIpcCloseMemHandle(map);
+    ipc_release(map);
     return e == cudaSuccess ? SMC_OK : SMC_ECUDA;
 }
 
