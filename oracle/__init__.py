@@ -9,7 +9,8 @@ FP64), written from PAPER.md (Eele & Maciejowski 2015) and pinned by the
 
 Parity status: see the header of ``smc_oracle.c``.  The rolling-window
 averaging (R20), post-landing bonus (R18), removal of violated aircraft (R42)
-and the MH move (R1) are conventions: *parity unpinned*.
+and the MH move (R1) are conventions the paper states in prose only; they are
+pinned by invariants and closed forms in ``tests/test_oracle_conventions.py``.
 """
 from __future__ import annotations
 

@@ -15,8 +15,11 @@
  *   flow_heading, arc_length, beta, utilities, weight recursion, mh_accept,
  *   resample_column, select, sample_schedule ........................ pinned
  *   rolling-window averaging (R20), post-landing bonus (R18), removal of a
- *   violated aircraft (R42), MH move semantics (R1) ...... parity unpinned
- *   (pure conventions: only self-consistency with the CUDA path is checked)
+ *   violated aircraft (R42), MH move semantics (R1) ................ pinned
+ *   (conventions the paper states in prose only: pinned by invariants and
+ *   closed forms in tests/test_oracle_conventions.py -- shorter-horizon
+ *   equivalence, hand-computed post-landing means, violator-absent
+ *   equivalence, sigma = 0 reduction of the MH move to Alg.1 l.23)
  */
 #include "smc_oracle.h"
 #include <math.h>
