@@ -37,8 +37,8 @@ constexpr int kTUnroll = SMC_K2_TUNROLL;
 
 __device__ __forceinline__ float clamp01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
 
-// a - 2 pi rint(a / 2 pi) (rounding by FRND; the magic-number form -- one packed FMA adding
-// 1.5 * 2^23, one packed subtract -- measured no faster on B200: 28.219 vs 28.219 ms of K2)
+// a - 2 pi rint(a / 2 pi) by FRND per candidate.  (The magic-number form -- one packed FMA
+// adding 1.5 * 2^23, one packed subtract -- measured slower on B200: 28.62 vs 28.13 ms of K2.)
 template <class V>
 __device__ __forceinline__ V wrap_pi(V a) {
     return vfma(vmap(a * (1.0f / kTwoPi), [](float u) { return rintf(u); }), -kTwoPi, a);

@@ -3,7 +3,7 @@
 tag=$1; shift; mkdir -p gpurun_out; i=0
 for fl in "$@"; do
   mkdir -p /tmp/v$i
-  SMC_NVCC_FLAGS="$fl" python -m paper_1506_02869_b200.build > gpurun_out/build_${tag}_$i.log 2>&1
+  SMC_NVCC_FLAGS="$fl" python -m paper_1506_02869_b200.build --force > gpurun_out/build_${tag}_$i.log 2>&1
   cp paper_1506_02869_b200/libsmcatm.so /tmp/v$i/
   i=$((i+1))
 done
