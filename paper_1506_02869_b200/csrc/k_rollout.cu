@@ -137,9 +137,10 @@ __device__ __forceinline__ V fast_atan2_xpos(V y, V x) {
 }
 
 // Shared-memory strides of the wind field per segment: normals (VST) and
-// AR(1) state / node values (ZST, odd to spread segments over banks).
+// AR(1) state / node values (ZST: even, so the node-major (x, y) state loads as float2;
+// the + 2 shifts neighbouring segments by two banks).
 __host__ __device__ constexpr int dense_vst(int G) { return 4 * ((2 * G + 3) / 4); }
-__host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 1; }
+__host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 2; }
 // row stride of the transposed factor Qhat^T [G][QTS] (multiple of 4 for 16-byte rows, zero padded)
 __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 4; }
 
@@ -277,30 +278,62 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     *reinterpret_cast<float4 *>(&sVs[4 * b]) = box_muller4(w);
                 }
                 __syncwarp();
-                for (int e = lane; e < G2; e += W) {
-                    const float ve = sVs[e];
-                    sZs[e] = (t == 0) ? ve : fmaf(sc.a, sZs[e], sc.b * ve);
+                // AR(1) state node-major, both components of a node in one float2 (normal e of
+                // the step is component e / G, node e mod G, R48)
+                float2 *const sZ2 = reinterpret_cast<float2 *>(sZs);
+                for (int nd = lane; nd < G; nd += W) {
+                    const float2 ve = make_float2(sVs[nd], sVs[G + nd]);
+                    sZ2[nd] = (t == 0) ? ve : vfma(sZ2[nd], sc.a, ve * sc.b);
                 }
                 __syncwarp();
-                // four consecutive rows per task from the transposed factor: one 16-byte load of
-                // Qhat^T[m][r0..r0+3] and one (segment-broadcast) load of Z[m] per 4 FMAs
-                const int nq = (G + 3) >> 2;
-                for (int task = lane; task < 2 * nq; task += W) {
-                    const int comp = task >= nq ? 1 : 0, r0 = 4 * (task - comp * nq);
-                    const float *zc = sZs + comp * G;
-                    const int mend = min(r0 + 4, G);             // Qhat lower triangular: m <= r
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int m = 0; m < mend; ++m) {
-                        const float4 q4 = *reinterpret_cast<const float4 *>(&s_Q[m * dense_qts(G) + r0]);
-                        const float zm = zc[m];
-                        acc.x = fmaf(q4.x, zm, acc.x); acc.y = fmaf(q4.y, zm, acc.y);
-                        acc.z = fmaf(q4.z, zm, acc.z); acc.w = fmaf(q4.w, zm, acc.w);
+                // W = Qhat Z from the transposed factor, four consecutive rows per task: one
+                // 16-byte load of Qhat^T[m][r0..r0+3] per 4 FMAs of each component the task
+                // covers.  The lower triangle makes row block q cost 4q + 4 iterations, so a lane
+                // takes the blocks q and nq - 1 - q together (every pair costs the same).  With
+                // more pairs than lanes a task covers both components (one Z (x, y) float2 load
+                // per 8 FMAs: half the shared-memory traffic); otherwise one component, so that
+                // more lanes work (4x4x4 in 8 lanes: 207 -> 143 ms per c2 MPC step)
+                const int nq = (G + 3) >> 2, half = (nq + 1) >> 1;
+                const bool both = 2 * half > W;
+                const int ntask = both ? half : 2 * half;
+                for (int pt = lane; pt < ntask; pt += W) {
+                    const int comp = (!both && pt >= half) ? 1 : 0, qa = pt - comp * half;
+                    for (int side = 0; side < 2; ++side) {
+                        const int q = side ? nq - 1 - qa : qa;
+                        if (side && q == qa) break;
+                        const int r0 = 4 * q;
+                        const int mend = min(r0 + 4, G);         // Qhat lower triangular: m <= r
+                        float4 ax = make_float4(0.f, 0.f, 0.f, 0.f), ay = ax;
+                        if (both) {
+                            for (int m = 0; m < mend; ++m) {
+                                const float4 q4 = *reinterpret_cast<const float4 *>(&s_Q[m * dense_qts(G) + r0]);
+                                const float2 zm = sZ2[m];
+                                ax.x = fmaf(q4.x, zm.x, ax.x); ax.y = fmaf(q4.y, zm.x, ax.y);
+                                ax.z = fmaf(q4.z, zm.x, ax.z); ax.w = fmaf(q4.w, zm.x, ax.w);
+                                ay.x = fmaf(q4.x, zm.y, ay.x); ay.y = fmaf(q4.y, zm.y, ay.y);
+                                ay.z = fmaf(q4.z, zm.y, ay.z); ay.w = fmaf(q4.w, zm.y, ay.w);
+                            }
+                        } else {
+                            const float *zc = sZs + comp;                // node-major: Z[m].comp
+                            for (int m = 0; m < mend; ++m) {
+                                const float4 q4 = *reinterpret_cast<const float4 *>(&s_Q[m * dense_qts(G) + r0]);
+                                const float zm = zc[2 * m];
+                                ax.x = fmaf(q4.x, zm, ax.x); ax.y = fmaf(q4.y, zm, ax.y);
+                                ax.z = fmaf(q4.z, zm, ax.z); ax.w = fmaf(q4.w, zm, ax.w);
+                            }
+                        }
+                        float *wx = sWs + comp * G + r0, *wy = sWs + G + r0;
+                        wx[0] = ax.x;
+                        if (r0 + 1 < G) wx[1] = ax.y;
+                        if (r0 + 2 < G) wx[2] = ax.z;
+                        if (r0 + 3 < G) wx[3] = ax.w;
+                        if (both) {
+                            wy[0] = ay.x;
+                            if (r0 + 1 < G) wy[1] = ay.y;
+                            if (r0 + 2 < G) wy[2] = ay.z;
+                            if (r0 + 3 < G) wy[3] = ay.w;
+                        }
                     }
-                    float *wo = sWs + comp * G + r0;
-                    wo[0] = acc.x;
-                    if (r0 + 1 < G) wo[1] = acc.y;
-                    if (r0 + 2 < G) wo[2] = acc.z;
-                    if (r0 + 3 < G) wo[3] = acc.w;
                 }
                 __syncwarp();
             } else {

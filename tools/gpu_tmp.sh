@@ -1,8 +1,6 @@
-python -m paper_1506_02869_b200.build > gpurun_out/build_ch.log 2>&1
-for rep in 1 2; do
-for ch in 0 1; do
-  SMC_K2_CHUNKS=$ch timeout 300 python bench.py --config 2 --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('chunks=$ch', d['ms_per_step'], d['phase_ms_per_step'])" >> gpurun_out/ab_ch.txt
-  SMC_K2_CHUNKS=$ch timeout 300 python bench.py --config 4 --steps 2 --warmup 2 --no-cpu-baseline --e2e-steps 0 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c4 chunks=$ch', d['ms_per_step'], d['phase_ms_per_step'])" >> gpurun_out/ab_ch.txt
-done
+python -m paper_1506_02869_b200.build > gpurun_out/build_dn4.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "dense" > gpurun_out/pytest_dn4.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_dn4.log
+for g in 3,3,2 4,4,4; do
+  timeout 600 python bench.py --config 2 --steps 2 --warmup 2 --no-cpu-baseline --e2e-steps 0 --wind-grid $g 2>&1 | grep '^{' >> gpurun_out/bench_dn4.jsonl
 done
 echo done
