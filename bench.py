@@ -375,8 +375,11 @@ def main():
                                + f", H={scn['H']}, K={cfg.K} rounds, "
                                + {0: "paper Alg.1 (no MH)", 1: "MH on", 2: "per-aircraft MH"}[int(cfg.mh)]
                                + (f", wind grid {'x'.join(str(v) for v in scn['wind_n'])}" if args.wind_grid else ""),
-                   "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU, NCCL all-reduce + "
-                                   "all-gathers per round)" if world > 1 else "single GPU"),
+                   "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU; per round NCCL "
+                                   "all-reduce of column maxima + all-gather of integer CDFs, parent rows "
+                                   + ("all-gathered" if os.environ.get("SMC_P2P") == "0"
+                                      else "read in place from their owner over NVLink (CUDA IPC peer mappings)")
+                                   + ")" if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "cuda_graph": not args.no_graph,
                    "aircraft_steps_per_step": ac_steps},
