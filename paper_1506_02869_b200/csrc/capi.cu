@@ -69,7 +69,7 @@ constexpr size_t kIpcRec = 128;     // cudaIpcMemHandle_t (64 B) + workspace off
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, accept, mpc, dac, pop, centres,
+    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, survp, ipc, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
         qf, qd, total;
 };
@@ -117,6 +117,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.QR = take(2 * nmax * sizeof(unsigned long long));
     o.anc = take(world > 1 ? 0 : (size_t)nmax * Lloc * sizeof(int32_t));   // K5 ancestors (single rank)
     o.splits = take(world > 1 ? 0 : (size_t)nmax * mp_split_words(Lloc, Lloc) * sizeof(uint32_t));
+    o.Cs = take(world > 1 ? 0 : (size_t)nmax * cdf_samples(Lloc) * sizeof(unsigned long long));   // CDF samples
     o.accept = take(8);
     o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
@@ -236,6 +237,8 @@ struct smc_ctx {
     int anc_mode = -1;                 // SMC_ANC: 1 merge-path K5, 0 bisection in K6, -1 by size
     int32_t *anc = nullptr;            // [n][Lloc] K5 ancestors
     uint32_t *splits = nullptr;        // K5 merge-path split points
+    unsigned long long *Cs = nullptr;  // [n][cdf_samples(Lmax)] CDF samples for K6's two-level search
+    bool cdf_sample = true;            // SMC_CDF_SAMPLE=0: plain bisection in K6
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -483,6 +486,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         ctx->chunking = ch && strcmp(ch, "1") == 0;
         // ancestors: merge-path K5 + K6 reading them ("mp"), or bisection inside K6 ("bisect");
         // default by population size
+        const char *cs = getenv("SMC_CDF_SAMPLE");          // K6 two-level search (default on)
+        ctx->cdf_sample = !(cs && strcmp(cs, "0") == 0);
         const char *am = getenv("SMC_ANC");
         ctx->anc_mode = am ? (strcmp(am, "mp") == 0 ? 1 : (strcmp(am, "bisect") == 0 ? 0 : -1)) : -1;
     }
@@ -533,6 +538,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->QR = (unsigned long long *)(ws + L.QR);
     ctx->anc = (int32_t *)(ws + L.anc);
     ctx->splits = (uint32_t *)(ws + L.splits);
+    ctx->Cs = (unsigned long long *)(ws + L.Cs);
     ctx->accept = (unsigned long long *)(ws + L.accept);
     ctx->mpc_dev = (uint32_t *)(ws + L.mpc);
     ctx->dac = (DevAircraft *)(ws + L.dac);
@@ -1002,13 +1008,18 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         // look-back status words the next round's scan (over Ln particles) will read
         const size_t nt = (size_t)std::max(scan_tiles(Lk), scan_tiles(Ln));
         rs.Q = nullptr;
+        // single rank, bisection in K6: K4 also writes every 16th prefix for the two-level search
+        const bool single = ctx->world == 1 && ctx->vworld == 1, mp = single && use_merge_path(ctx, Lk);
+        const bool two_level = single && !mp && ctx->cdf_sample;
+        if (two_level) { rs.Cs = ctx->Cs; rs.Cs_stride = cdf_samples(Lk); }
         LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
         ProposeArgs pa{};
         pa.n = n; pa.H = H; pa.L = Ln; pa.Lsrc = Lk; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
         pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
-        if (ctx->world == 1 && ctx->vworld == 1 && use_merge_path(ctx, Lk)) {
+        if (two_level) { pa.Cs = ctx->Cs; pa.Cs_stride = cdf_samples(Lk); }
+        if (mp) {
             rs.anc = ctx->anc; rs.M = Ln; rs.splits = ctx->splits;
             LAUNCHP(PH_RESAMPLE, launch_ancestors(rs, ctx->st));
             pa.anc = ctx->anc;

@@ -285,7 +285,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
         const uint32_t l = base + it;
-        if (l < r.L) C[l] = pre + inc[it];
+        if (l < r.L) {
+            C[l] = pre + inc[it];
+            if (r.Cs && ((l % kCdfSample) == kCdfSample - 1 || l == r.L - 1))
+                r.Cs[(size_t)i * r.Cs_stride + l / kCdfSample] = pre + inc[it];
+        }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const uint64_t Q = s_pre + agg;
@@ -314,6 +318,25 @@ __device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, ui
         if (__ldg(&C[mid]) > tj) hi = mid; else lo = mid + 1;
     }
     return (int32_t)lo;
+}
+
+// Two-level search: the group g of kCdfSample entries whose sample Cs[g] first exceeds t_j
+// (bisection over L / 16 samples: a small, cache-resident array), then the slot's ancestor
+// inside that group (four steps within one 128-byte line).  Same result as find_ancestor.
+__device__ __forceinline__ int32_t find_ancestor2(const unsigned long long *C, const unsigned long long *Cs,
+                                                  uint32_t L, uint32_t M, uint64_t Q, uint64_t R, uint32_t j) {
+    const uint64_t tj = slot_t(j, Q / M, Q % M, R, M);
+    uint32_t lo = 0, hi = cdf_samples(L) - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&Cs[mid]) > tj) hi = mid; else lo = mid + 1;
+    }
+    uint32_t a = lo * kCdfSample, b = min(a + kCdfSample, L) - 1;
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (__ldg(&C[mid]) > tj) b = mid; else a = mid + 1;
+    }
+    return (int32_t)a;
 }
 
 __global__ void k_ancestors(const ResampleArgs r) {
@@ -473,7 +496,9 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
                     a = __ldg(&p.anc[(size_t)i * p.L + j]);
                 } else {
                     const uint64_t Q = p.QR[2 * i], R = p.QR[2 * i + 1];
-                    a = find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
+                    a = p.Cs ? find_ancestor2(p.C + (size_t)i * p.Lsrc, p.Cs + (size_t)i * p.Cs_stride, p.Lsrc, p.L,
+                                              Q, R, j)
+                             : find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
                 }
                 src = p.src[(__ldg(&p.surv[a]) >> i) & 1u] + ((size_t)a * p.n + i) * H * 3;
                 s_j[threadIdx.x] = j;

@@ -76,7 +76,11 @@ struct ResampleArgs {
     int32_t *anc;               // [n][M] (K5 ancestors only)
     uint32_t M;                 // new particles drawn (K5 ancestors only)
     uint32_t *splits;           // [n][mp_split_words(L, M)] K5 merge-path split points
+    unsigned long long *Cs;     // [n][Cs_stride] every kCdfSample-th inclusive prefix (nullable):
+    uint32_t Cs_stride;         //   Cs[g] = C[min(16 g + 15, L - 1)], for K6's two-level search
 };
+constexpr int kCdfSample = 16;
+__host__ __device__ inline uint32_t cdf_samples(uint32_t L) { return (L + kCdfSample - 1) / kCdfSample; }
 int scan_tiles(uint32_t L);
 int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
@@ -95,6 +99,8 @@ struct ProposeArgs {
     uint32_t Lsrc;              // particles evaluated this round (CDF length); L = new particles
     const int32_t *anc;         // [n][L] explicit ancestors (debug) or NULL -> bisection of C
     const unsigned long long *C, *QR;
+    const unsigned long long *Cs;   // [n][Cs_stride] CDF samples (nullable: plain bisection)
+    uint32_t Cs_stride;
     // per-round accumulators zeroed here for the next round (stream-ordered after K2 and K4)
     uint32_t *reset_colmax, *reset_tiles;   // [reset_n] each
     unsigned long long *reset_accept;

@@ -276,14 +276,19 @@ def test_resample_to_fewer_bitexact(smc, L, M, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("L,Lf,S,K,mode", [(256, 40, 4, 6, None), (140000, 60000, 2, 3, None),
-                                           (256, 40, 4, 6, "mp"), (140000, 60000, 2, 3, "bisect")])
+                                           (256, 40, 4, 6, "mp"), (140000, 60000, 2, 3, "bisect"),
+                                           (5000, 3001, 2, 3, "plain")])
 def test_shrinking_population_rounds(smc, L, Lf, S, K, mode, monkeypatch):
     """Real rounds with L_k falling linearly to L_final: population
     sizes follow the oracle's schedule, each round's ancestors (read back from
     the next round's x' rows) are the oracle's resampling of the GPU's ell into
     L_{k+1} slots, and the log-weights match the oracle's evaluation.  Both
-    ancestor paths: merge-path K5 (default from 2^17 particles) and bisection."""
-    if mode:
+    ancestor paths: merge-path K5 (default from 2^17 particles) and bisection in
+    K6 (two-level through K4's every-16th-prefix samples by default, or plain)."""
+    if mode == "plain":                     # bisection over the whole CDF, no 16-entry samples
+        monkeypatch.setenv("SMC_ANC", "bisect")
+        monkeypatch.setenv("SMC_CDF_SAMPLE", "0")
+    elif mode:
         monkeypatch.setenv("SMC_ANC", mode)
     scn, cfg = sc.config(1)
     sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, L_final=Lf)

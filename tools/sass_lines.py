@@ -1,6 +1,6 @@
 """Attribute ncu per-SASS-instruction counts to CUDA source lines.
 
-usage: python tools/sass_lines.py <ncu-rep> <cubin> <mangled-function> [top] [outer-file]
+usage: python tools/sass_lines.py <ncu-rep> <cubin> <mangled-function> [top] [outer-file] [ncu-kernel-filter]
 (cubin: cuobjdump -xelf all libsmcatm.so; needs -lineinfo builds)
 """
 import csv
@@ -13,8 +13,9 @@ from collections import defaultdict
 rep, cubin, fn = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 OUTER = sys.argv[5] if len(sys.argv) > 5 else None     # e.g. k_rollout.cu
-csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                        capture_output=True, text=True).stdout
+KFILTER = sys.argv[6] if len(sys.argv) > 6 else None   # ncu -k filter (kernel of a multi-kernel report)
+csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+                        + (["-k", KFILTER] if KFILTER else []), capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(csvtxt)))
 hi = next(j for j, r in enumerate(rows) if "Address" in r)      # first kernel of the report only
 hdr = rows[hi]
