@@ -239,6 +239,7 @@ struct smc_ctx {
     uint32_t *splits = nullptr;        // K5 merge-path split points
     unsigned long long *Cs = nullptr;  // [n][cdf_samples(Lmax)] CDF samples for K6's two-level search
     bool cdf_sample = true;            // SMC_CDF_SAMPLE=0: plain bisection in K6
+    bool scan_cluster = true;          // SMC_SCAN=lookback: decoupled look-back scan only
     std::string err;
     // phase timing (cfg.profile): event pairs per phase, summed on request
     std::vector<cudaEvent_t> ev_free;
@@ -486,6 +487,8 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         ctx->chunking = ch && strcmp(ch, "1") == 0;
         // ancestors: merge-path K5 + K6 reading them ("mp"), or bisection inside K6 ("bisect");
         // default by population size
+        const char *sm = getenv("SMC_SCAN");
+        ctx->scan_cluster = !(sm && strcmp(sm, "lookback") == 0);
         const char *cs = getenv("SMC_CDF_SAMPLE");          // K6 two-level search (default on)
         ctx->cdf_sample = !(cs && strcmp(cs, "0") == 0);
         const char *am = getenv("SMC_ANC");
@@ -923,6 +926,12 @@ static uint32_t samples_of(const smc_ctx *ctx, uint32_t k) {
 
 // Merge-path ancestors (K5) pay once the CDF no longer sits in L2 and a bisection per
 // slot turns into DRAM misses; below that the extra launch costs more than it saves.
+// Cluster scan (one 8-CTA cluster per column, DSMEM) up to 65 536 particles, else the
+// decoupled look-back scan; SMC_SCAN=lookback forces the latter.
+static bool use_cluster_scan(const smc_ctx *ctx, uint32_t Lk) {
+    return ctx->scan_cluster && cluster_scan_fits(Lk);
+}
+
 static bool use_merge_path(const smc_ctx *ctx, uint32_t Lk) {
     if (ctx->anc_mode >= 0) return ctx->anc_mode == 1;
     return Lk >= (1u << 17);
@@ -1012,7 +1021,8 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         const bool single = ctx->world == 1 && ctx->vworld == 1, mp = single && use_merge_path(ctx, Lk);
         const bool two_level = single && !mp && ctx->cdf_sample;
         if (two_level) { rs.Cs = ctx->Cs; rs.Cs_stride = cdf_samples(Lk); }
-        LAUNCHP(PH_RESAMPLE, launch_scan(rs, ctx->st));
+        LAUNCHP(PH_RESAMPLE, single && use_cluster_scan(ctx, Lk) ? launch_scan_cluster(rs, ctx->st)
+                                                                 : launch_scan(rs, ctx->st));
         ProposeArgs pa{};
         pa.n = n; pa.H = H; pa.L = Ln; pa.Lsrc = Lk; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
@@ -1452,7 +1462,7 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
     rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
     rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M; rs.splits = dspl;
-    LAUNCH(launch_scan(rs, ctx->st));
+    LAUNCH(use_cluster_scan(ctx, L) ? launch_scan_cluster(rs, ctx->st) : launch_scan(rs, ctx->st));
     LAUNCH(ctx->anc_mode == 0 ? launch_ancestors_bisect(rs, ctx->st) : launch_ancestors(rs, ctx->st));
     CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * M, cudaMemcpyDeviceToHost, ctx->st));
     if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));

@@ -1,8 +1,9 @@
 // k_population.cu -- population kernels of libsmcatm (sm_100a):
 //   K1  k_init_population   uniform initial controls       (Alg.1 l.3-5)
 //   K4a k_qsum              integer resampling weights per column, totals Q_i, ESS sums
-//   K4b k_scan              decoupled look-back inclusive scan of the integer
-//                           weights, (Q, R) per column     (R25)
+//   K4b k_scan / k_scan_cluster  inclusive scan of the integer weights: decoupled
+//                           look-back, or one 8-CTA cluster per column (DSMEM); (Q, R)
+//                           per column     (R25)
 //   K5  k_mp_splits +       merge-path systematic ancestors (large populations)
 //       k_ancestors_mp
 //   K6  k_gather_propose    per-aircraft recombination + Gaussian proposal
@@ -12,6 +13,8 @@
 // plus the population-density grid, the multi-GPU exchange kernels and the
 // MH debug hooks.
 #include <cfloat>
+
+#include <cooperative_groups.h>
 
 #include "smc_device.cuh"
 #include "smc_kernels.h"
@@ -304,6 +307,91 @@ cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st) {
     const int nt = scan_tiles(r.L);
     if (scan_items(r.L) == 2) k_scan<2><<<dim3(r.n, nt), kScanThreads, 0, st>>>(r, nt);
     else k_scan<8><<<dim3(r.n, nt), kScanThreads, 0, st>>>(r, nt);
+    return cudaGetLastError();
+}
+
+// ============================================================== K4b' (cluster scan)
+// Populations up to kClusterScanMax: one 8-CTA thread-block cluster per column, no global
+// atomics and no look-back.  CTA r scans its contiguous eighth of the column into shared
+// memory (sub-tiles of 2048 with a running carry), publishes its total, and after a
+// cluster barrier reads the totals of CTAs 0..r-1 through distributed shared memory
+// (DSMEM) for its exclusive offset; every CTA also forms Q.  One pass over ell, one over C.
+constexpr int kClusterCtas = 8, kClusterSeg = 8192;
+constexpr uint32_t kClusterScanMax = (uint32_t)kClusterCtas * kClusterSeg;
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kScanThreads)
+k_scan_cluster(const ResampleArgs r) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ unsigned long long s_loc[];                // [seg] local inclusive sums
+    __shared__ unsigned long long s_agg;
+    const int i = blockIdx.y;
+    const int rank = (int)cluster.block_rank();
+    const uint32_t L = r.L;
+    const uint32_t seg = (((L + kClusterCtas - 1) / kClusterCtas) + 7u) & ~7u;
+    const uint32_t b = min(L, (uint32_t)rank * seg), e = min(L, b + seg);
+    const uint32_t cm = r.colmax[i];
+    const bool inf = column_infeasible(cm);
+    const float m = ord2f(cm);
+    const float *ell = r.ell + (size_t)i * (r.ell_stride ? r.ell_stride : L);
+    constexpr int kIt = 8, kSub = kScanThreads * kIt;
+    unsigned long long carry = 0;
+    for (uint32_t s0 = b; s0 < e; s0 += kSub) {
+        const uint32_t base = s0 + threadIdx.x * kIt;
+        uint64_t inc[kIt];
+        uint64_t run = 0;
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const uint32_t l = base + it;
+            run += l < e ? qweight(ell, l, m, inf) : 0ull;
+            inc[it] = run;
+        }
+        unsigned long long agg;
+        const unsigned long long texcl = block_exclusive<OpSum>(run, &agg);
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const uint32_t l = base + it;
+            if (l < e) s_loc[l - b] = carry + texcl + inc[it];
+        }
+        carry += agg;
+        __syncthreads();                                         // s_w of block_exclusive reused
+    }
+    if (threadIdx.x == 0) s_agg = carry;
+    cluster.sync();
+    unsigned long long pre = 0, Q = 0;
+    for (int q = 0; q < kClusterCtas; ++q) {
+        const unsigned long long aq = *cluster.map_shared_rank(&s_agg, q);
+        if (q < rank) pre += aq;
+        Q += aq;
+    }
+    cluster.sync();                                              // no CTA leaves while its s_agg is read
+    unsigned long long *C = r.C + (size_t)i * (r.Cstride ? r.Cstride : L);
+    for (uint32_t l = b + threadIdx.x; l < e; l += kScanThreads) {
+        const unsigned long long v = pre + s_loc[l - b];
+        C[l] = v;
+        if (r.Cs && ((l % kCdfSample) == kCdfSample - 1 || l == L - 1))
+            r.Cs[(size_t)i * r.Cs_stride + l / kCdfSample] = v;
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
+        r.QR[2 * i] = Q;
+        r.QR[2 * i + 1] = __umul64hi(rw, Q);                  // R = floor(r64 Q / 2^64)
+        if (r.Q) r.Q[i] = Q;
+    }
+}
+
+bool cluster_scan_fits(uint32_t L) { return L >= 1 && L <= kClusterScanMax; }
+
+cudaError_t launch_scan_cluster(const ResampleArgs &r, cudaStream_t st) {
+    const uint32_t seg = (((r.L + kClusterCtas - 1) / kClusterCtas) + 7u) & ~7u;
+    const size_t smem = (size_t)seg * sizeof(unsigned long long);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_scan_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kClusterSeg * sizeof(unsigned long long)));
+        attr = true;
+    }
+    k_scan_cluster<<<dim3(kClusterCtas, r.n), kScanThreads, smem, st>>>(r);
     return cudaGetLastError();
 }
 

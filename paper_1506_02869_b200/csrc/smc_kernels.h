@@ -85,6 +85,9 @@ int scan_tiles(uint32_t L);
 int scan_tiles_max(uint32_t L);    // upper bound over all tile sizes (status allocation)
 cudaError_t launch_qsum(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_scan(const ResampleArgs &r, cudaStream_t st);
+// single-pass scan by one 8-CTA cluster per column (DSMEM exchange of CTA totals), L <= 65536
+bool cluster_scan_fits(uint32_t L);
+cudaError_t launch_scan_cluster(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);          // K5 merge path (needs r.splits)
 size_t mp_split_words(uint32_t L, uint32_t M);
 cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st);   // one bisection per slot

@@ -254,6 +254,25 @@ def test_resample_bitexact(smc, L, mode, monkeypatch):
             assert np.array_equal(anc[i], r["anc"]), (i, k, np.nonzero(anc[i] != r["anc"])[0][:10])
 
 
+@pytest.mark.parametrize("scan", ["cluster", "lookback"])
+@pytest.mark.parametrize("L", [1, 9, 2049, 16384, 65536])
+def test_resample_scan_variants_bitexact(smc, L, scan, monkeypatch):
+    """The integer CDF by the 8-CTA cluster scan (DSMEM exchange, default up to 65 536
+    particles) and by the decoupled look-back scan: ancestors and totals bit-exact."""
+    monkeypatch.setenv("SMC_SCAN", scan)
+    scn, cfg = sc.config(1)
+    sol = _solver(smc, scn, seed=cfg.seed)
+    rng = np.random.default_rng(L + 17)
+    N = 3
+    ell = rng.normal(-25, 8, (N, L)).astype(np.float32)
+    ell[rng.uniform(size=(N, L)) < 0.3] = -np.inf
+    ell[2] = -np.inf
+    anc, Q = sol.debug_resample(ell, 4)
+    for i in range(N):
+        r = O.resample_column(ell[i].astype(np.float64), i, 4, cfg.seed)
+        assert Q[i] == r["Q"] and np.array_equal(anc[i], r["anc"]), i
+
+
 @pytest.mark.parametrize("mode", ["mp", "bisect"])
 @pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000), (1, 1), (3, 1)])
 def test_resample_to_fewer_bitexact(smc, L, M, mode, monkeypatch):
