@@ -10,5 +10,5 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_small_$tag.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_$tag.log 2>&1
 timeout 120 python tools/prof_step.py 2 4 > gpurun_out/prof_plain_$tag.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rollout|k_gather|k_scan" -s 3 -c 3 -o gpurun_out/prof_$tag python tools/prof_step.py 2 4 > gpurun_out/ncu_$tag.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rollout|k_gather|k_scan" -s 2 -c 4 -o gpurun_out/prof_$tag python tools/prof_step.py 2 4 > gpurun_out/ncu_$tag.log 2>&1
 echo done
