@@ -28,7 +28,13 @@
 #define SMC_K2_TUNROLL 2   // unroll factor of the horizon loop (A/B on c2: 1 -> 29.2, 2 -> 28.2, 3 -> 29.0 ms of K2)
 #endif
 #ifndef SMC_K2_MINB
-#define SMC_K2_MINB 4   // resident 128-thread blocks per SM the register budget targets (A/B: 4 > 5 > 6)
+#define SMC_K2_MINB 4   // resident 128-thread blocks per SM the register budget targets, two candidates
+#endif
+#ifndef SMC_K2_MINB1
+#define SMC_K2_MINB1 5  // the same for single-candidate launches (round 0, paper mode; sweep: 5 > 6 > 4)
+#endif
+#ifndef SMC_K2_MINB32
+#define SMC_K2_MINB32 SMC_K2_MINB  // two candidates in 32-lane segments (N > 16)
 #endif
 
 namespace smc {
@@ -145,7 +151,7 @@ __host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 2; }
 __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 4; }
 
 template <int W, int NC, bool DEBUG, bool DENSE>
-__global__ void __launch_bounds__(kBlock, SMC_K2_MINB)
+__global__ void __launch_bounds__(kBlock, NC == 1 ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB))
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
     constexpr int TU = W >= 32 ? 1 : kTUnroll;      // W = 32 spills when unrolled

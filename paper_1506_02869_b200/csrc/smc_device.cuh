@@ -11,7 +11,10 @@ namespace smc {
 
 constexpr int kMaxAc = 32;
 constexpr int kMaxH = 32;
-constexpr int kBlock = 128;           // threads per rollout block
+#ifndef SMC_K2_BLOCK
+#define SMC_K2_BLOCK 128
+#endif
+constexpr int kBlock = SMC_K2_BLOCK;  // threads per rollout block (launch-geometry sweep: 64-512)
 constexpr float kPi = 3.14159265358979323846f;
 constexpr float kTwoPi = 6.28318530717958647692f;
 
