@@ -20,6 +20,9 @@
 // After S samples: ell += sum_s log2 J_T (R24); lambda = sum_i ell in
 // double; MH decision (R1); survivor ell / lambda / flag written; per-column
 // max of ell folded into an atomicMax (first step of the resampling reduce).
+#include <cstdlib>
+#include <cstring>
+
 #include "smc_device.cuh"
 #include "smc_kernels.h"
 #include "smc_vec.cuh"
@@ -150,7 +153,10 @@ __host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 2; }
 // row stride of the transposed factor Qhat^T [G][QTS] (multiple of 4 for 16-byte rows, zero padded)
 __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 4; }
 
-template <int W, int NC, bool DEBUG, bool DENSE>
+// R: separation ring size -- W (every lane of the segment, idle lanes publish NaN), or the exact
+// aircraft count n < W for the benchmark shapes (partners d = 1..R/2 at compile time, idle lanes
+// publish nothing)
+template <int W, int NC, bool DEBUG, bool DENSE, int R = W>
 __global__ void __launch_bounds__(kBlock, NC == 1 ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB))
 k_rollout(const DevScen sc, const RolloutArgs args) {
     constexpr int SEGS = kBlock / W;
@@ -528,25 +534,27 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             V px;
 #pragma unroll
             for (int c = 0; c < NC; ++c) cset(px, c, ((flym >> c) & 1) ? cget(nx, c) : __int_as_float(0x7fffffff));
-            // own entry at seg*2W + lane and + W: partner lane + d (mod W) sits at offset d
+            // own entry at seg*2W + lane and + R: partner lane + d (mod R) sits at offset d
             const int pb = seg * 2 * W + lane;
             float4 *s_pxy = s_pos;                                           // [2 kBlock]
             float2 *s_pz = reinterpret_cast<float2 *>(s_pos + 2 * kBlock);   // [2 kBlock] (NC = 2)
-            if constexpr (NC == 2) {
-                const float4 e = make_float4(px.x, px.y, ny.x, ny.y);
-                s_pxy[pb] = e; s_pxy[pb + W] = e;
-                s_pz[pb] = nz; s_pz[pb + W] = nz;
-            } else {
-                const float4 e = make_float4(px, ny, nz, 0.0f);
-                s_pxy[pb] = e; s_pxy[pb + W] = e;
+            if (R == W || isac) {
+                if constexpr (NC == 2) {
+                    const float4 e = make_float4(px.x, px.y, ny.x, ny.y);
+                    s_pxy[pb] = e; s_pxy[pb + R] = e;
+                    s_pz[pb] = nz; s_pz[pb + R] = nz;
+                } else {
+                    const float4 e = make_float4(px, ny, nz, 0.0f);
+                    s_pxy[pb] = e; s_pxy[pb + R] = e;
+                }
             }
             __syncwarp();
             // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
-            // lane checks partner lane+d (d = 1..W/2) and hands the verdict to that
-            // partner with a segment-wide shuffle (for d = W/2 both lanes check).
+            // lane checks partner lane+d (d = 1..R/2) and hands the verdict to that
+            // partner with a segment-wide shuffle (for d = R/2, R even, both lanes check).
             int confm = 0;
 #pragma unroll
-            for (int d = 1; d <= W / 2; ++d) {
+            for (int d = 1; d <= R / 2; ++d) {
                 V dx, dy, dz;
                 if constexpr (NC == 2) {
                     const float4 q = s_pxy[pb + d];
@@ -563,8 +571,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 for (int c = 0; c < NC; ++c)
                     hits |= ((cget(d2, c) < sc.twoPr2) && (fabsf(cget(dz, c)) < sc.twoPh) ? 1 : 0) << c;
                 confm |= hits;
-                // one shuffle hands both candidates' verdicts to the partner (source lane taken mod W)
-                if (2 * d < W) confm |= __shfl_sync(0xffffffffu, hits, lane + W - d, W);
+                // one shuffle hands both candidates' verdicts to the partner, from lane - d (mod R);
+                // lanes >= R (R < W) compute ignored verdicts
+                if (2 * d < R)
+                    confm |= __shfl_sync(0xffffffffu, hits, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
             }
             // ---------------- 5. per-step cost terms at j = t+1 (frozen aircraft add 0), state update
             // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
@@ -791,10 +801,10 @@ __global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) 
     }
 }
 
-template <int W, int NC, bool DEBUG, bool DENSE>
+template <int W, int NC, bool DEBUG, bool DENSE, int R = W>
 static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     const size_t smem = rollout_smem_bytes(W, NC, sc.H, DENSE ? sc.wng : 8);
-    auto kern = k_rollout<W, NC, DEBUG, DENSE>;
+    auto kern = k_rollout<W, NC, DEBUG, DENSE, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int segs = kBlock / W;
@@ -828,6 +838,11 @@ int rollout_blocks_per_sm(int n, int H, int NC, int ng) {
     return nb;
 }
 
+static bool ring_enabled() {
+    static const bool on = [] { const char *e = getenv("SMC_K2_RING"); return !(e && strcmp(e, "0") == 0); }();
+    return on;
+}
+
 template <int NC, bool DEBUG>
 static cudaError_t launch_nc(int W, bool dense, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     if (dense) {
@@ -838,6 +853,13 @@ static cudaError_t launch_nc(int W, bool dense, const DevScen &sc, const Rollout
             case 32: return launch_w<32, NC, DEBUG, true>(sc, a, st);
         }
         return cudaErrorInvalidValue;
+    }
+    // separation rings of the exact aircraft count for the benchmark shapes (c3: 24, c4: 12,
+    // Table 1: 10) -- the scan needs n/2 partner offsets instead of W/2 (SMC_K2_RING=0: off)
+    if (ring_enabled()) {
+        if (W == 32 && sc.n == 24) return launch_w<32, NC, DEBUG, false, 24>(sc, a, st);
+        if (W == 16 && sc.n == 12) return launch_w<16, NC, DEBUG, false, 12>(sc, a, st);
+        if (W == 16 && sc.n == 10) return launch_w<16, NC, DEBUG, false, 10>(sc, a, st);
     }
     switch (W) {
         case 1: return launch_w<1, NC, DEBUG, false>(sc, a, st);
