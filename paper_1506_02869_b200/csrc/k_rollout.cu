@@ -156,9 +156,14 @@ __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 
 // R: separation ring size -- W (every lane of the segment, idle lanes publish NaN), or the exact
 // aircraft count n < W for the benchmark shapes (partners d = 1..R/2 at compile time, idle lanes
 // publish nothing)
-template <int W, int NC, bool DEBUG, bool DENSE, int R = W>
-__global__ void __launch_bounds__(kBlock, NC == 1 ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB))
+// SP (sample pairs, single-candidate launches): the two float2 slots carry samples s and s+1 of
+// the same particle instead of two MH candidates -- each slot its own wind / gust draws, the
+// two log-weights summed at the end; launched as NC = 2 with both control pointers equal.
+template <int W, int NC, bool DEBUG, bool DENSE, int R = W, bool SP = false>
+__global__ void __launch_bounds__(kBlock, (NC == 1 || SP) ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB))
 k_rollout(const DevScen sc, const RolloutArgs args) {
+    static_assert(!SP || (NC == 2 && !DENSE && !DEBUG && W >= 8), "sample pairs: two slots, 2x2x2 grid, W >= 8");
+    constexpr int NSL = SP ? 2 : 1;                 // wind realisations per segment and step
     constexpr int SEGS = kBlock / W;
     constexpr int TU = W >= 32 ? 1 : kTUnroll;      // W = 32 spills when unrolled
     constexpr int EN = W >= 8 ? 1 : 8 / W;          // wind-grid nodes owned per lane (lanes >= 8 idle)
@@ -170,7 +175,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     // dense grid (G = N_x N_y N_z > 8): [SEGS][VST] normals, [SEGS][ZST] state and node values,
     // Qhat [G][G+1]
     const int G = DENSE ? sc.wng : 8;
-    const int VST = DENSE ? dense_vst(G) : GB * 16, ZST = DENSE ? dense_zst(G) : 16;
+    const int VST = DENSE ? dense_vst(G) : GB * 16 * NSL, ZST = DENSE ? dense_zst(G) : 16 * NSL;
     float *s_V = reinterpret_cast<float *>(s_ctrl + H * NC * kBlock);
     float *s_Z = s_V + SEGS * VST;
     float *s_W = s_Z + SEGS * ZST;
@@ -248,7 +253,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
     float ell[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) ell[c] = args.part ? 0.0f : args.ell0;
+    for (int c = 0; c < NC; ++c) ell[c] = (args.part || (SP && c == 1)) ? 0.0f : args.ell0;
 
     using V = vec_t<NC>;
     const float dt = sc.dt, g = sc.g;
@@ -264,16 +269,18 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     // sample chunk of this block (gridDim.y > 1: partial sums, combined by k_combine)
     const uint32_t s_lo = (uint32_t)(((uint64_t)args.S * blockIdx.y) / gridDim.y);
     const uint32_t s_hi = (uint32_t)(((uint64_t)args.S * (blockIdx.y + 1)) / gridDim.y);
-    for (uint32_t s = s_lo; s < s_hi; ++s) {
+    for (uint32_t s = s_lo; s < s_hi; s += NSL) {
         V x = vsplat<V>(Ap->x0[0]), y = vsplat<V>(Ap->x0[1]), z = vsplat<V>(Ap->x0[2]);
         V v = vsplat<V>(Ap->x0[3]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
         V fuel = vsplat<V>(0.0f), sA = fuel, sB = fuel, sC = fuel, sN = fuel;
         // per-candidate flags as bit masks (bit c = candidate c)
         constexpr int ALLC = (1 << NC) - 1;
         int landedm = 0, violm = 0;
-        float2 Zr[EN];                                   // AR(1) state of the lane's nodes, (x, y)
-        float2 gust_odd = make_float2(0.f, 0.f);
+        constexpr int ENS = SP ? (W >= 16 ? 1 : 2) : EN;   // (node, slot) pairs a lane owns
+        float2 Zr[ENS];                                  // AR(1) state of the lane's nodes, (x, y)
+        float2 gust_odd = make_float2(0.f, 0.f), gust_odd_b = gust_odd;
         const uint32_t x1 = (s & 0xFFFFu) | (k << 16);
+        const uint32_t x1b = ((s + 1) & 0xFFFFu) | (k << 16);   // SP: the second slot's sample
 
 #pragma unroll TU
         for (int t = 0; t < H; ++t) {
@@ -350,37 +357,40 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 __syncwarp();
             } else {
             // Every GB steps the segment's lanes draw the 4 Philox blocks of GB
-            // consecutive steps at once (lane -> block lane&3 of step t + lane/4).
+            // consecutive steps at once (lane -> block lane&3 of step t + lane/4); SP: the
+            // blocks of both slots' samples (slot = task / (4 GB)).
             const int tb = t % GB;
             if (tb == 0) {
-                for (int task = lane; task < 4 * GB; task += W) {
-                    const int b = task & 3, ts = t + (task >> 2);
+                for (int task = lane; task < 4 * GB * NSL; task += W) {
+                    const int sl = SP ? task / (4 * GB) : 0, tk = task - sl * 4 * GB;
+                    const int b = tk & 3, ts = t + (tk >> 2);
                     if (ts < H) {
-                        const uint4 w = draw_ks(TAG_WIND, l, x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
-                        *reinterpret_cast<float4 *>(&s_V[(seg * GB + (task >> 2)) * 16 + 4 * b]) = box_muller4(w);
+                        const uint4 w = draw_ks(TAG_WIND, l, sl ? x1b : x1, (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
+                        *reinterpret_cast<float4 *>(&s_V[((seg * NSL + sl) * GB + (tk >> 2)) * 16 + 4 * b]) = box_muller4(w);
                     }
                 }
             }
             __syncwarp();
             // AR(1) and W = Cq Z with both components of a node packed in one float2:
-            // lane owns node lane + q W (q < EN); Z is kept node-major [node](x, y) in shared memory
-            float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16);
+            // lane owns (node, slot) pair lane + q W (q < ENS; node = pair & 7, slot = pair >> 3);
+            // Z is kept node-major [slot][node](x, y) in shared memory
+            float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16 * NSL);
 #pragma unroll
-            for (int q = 0; q < EN; ++q) {
-                const int node = lane + q * W;
-                if (node < 8) {
-                    const float *vv = &s_V[(seg * GB + tb) * 16];
+            for (int q = 0; q < ENS; ++q) {
+                const int pq = lane + q * W, node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
+                if (pq < 8 * NSL) {
+                    const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
                     const float2 ve = make_float2(vv[node], vv[8 + node]);
                     Zr[q] = (t == 0) ? ve : vfma(Zr[q], sc.a, ve * sc.b);
-                    sZ2[node] = Zr[q];
+                    sZ2[sl * 8 + node] = Zr[q];
                 }
             }
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < EN; ++q) {
-                const int node = lane + q * W;
-                if (node < 8) {
-                    const float4 *z4 = reinterpret_cast<const float4 *>(sZ2);
+            for (int q = 0; q < ENS; ++q) {
+                const int pq = lane + q * W, node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
+                if (pq < 8 * NSL) {
+                    const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
                     const float *qr = (W >= 8) ? qrow : &s_Q[node * 9];
                     float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -389,12 +399,17 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                         acc = vfma(make_float2(zz.x, zz.y), qr[2 * mm], acc);
                         acc = vfma(make_float2(zz.z, zz.w), qr[2 * mm + 1], acc);
                     }
-                    s_W[seg * 16 + node] = acc.x;
-                    s_W[seg * 16 + 8 + node] = acc.y;
+                    if constexpr (SP) {                          // interleaved [coefficient][slot]
+                        s_W[(seg * 16 + node) * 2 + sl] = acc.x;
+                        s_W[(seg * 16 + 8 + node) * 2 + sl] = acc.y;
+                    } else {
+                        s_W[seg * 16 + node] = acc.x;
+                        s_W[seg * 16 + 8 + node] = acc.y;
+                    }
                 }
             }
             __syncwarp();
-            {
+            if constexpr (!SP) {
                 const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[seg * 16]);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -403,22 +418,32 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 }
             }
             }
-            // gusts (R15): one Philox call covers steps 2u and 2u+1
-            float gx = sc.nominal[0], gy = sc.nominal[1];
+            // gusts (R15): one Philox call covers steps 2u and 2u+1 (SP: one per slot)
+            float gx = sc.nominal[0], gy = sc.nominal[1], gxb = gx, gyb = gy;
             if (sc.turb_sigma > 0.0f) {
-                float2 gg;
+                float2 gg, ggb = make_float2(0.f, 0.f);
                 if ((t & 1) == 0) {
                     const uint4 w = draw_ks(TAG_TURB, l, x1, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
                     const float4 g4 = box_muller4(w);
                     gg = make_float2(g4.x, g4.y);
                     gust_odd = make_float2(g4.z, g4.w);
+                    if constexpr (SP) {
+                        const uint4 wb = draw_ks(TAG_TURB, l, x1b, ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
+                        const float4 g4b = box_muller4(wb);
+                        ggb = make_float2(g4b.x, g4b.y);
+                        gust_odd_b = make_float2(g4b.z, g4b.w);
+                    }
                 } else {
                     gg = gust_odd;
+                    ggb = gust_odd_b;
                 }
                 gx = fmaf(sc.turb_sigma, gg.x, gx);
                 gy = fmaf(sc.turb_sigma, gg.y, gy);
+                gxb = fmaf(sc.turb_sigma, ggb.x, gxb);
+                gyb = fmaf(sc.turb_sigma, ggb.y, gyb);
             }
-            const float c0x = DENSE ? gx : Wn[0] + gx, c0y = DENSE ? gy : Wn[8] + gy;   // nominal + gust (+ c0)
+            const float c0x = (DENSE || SP) ? gx : Wn[0] + gx, c0y = (DENSE || SP) ? gy : Wn[8] + gy;   // nominal + gust (+ c0)
+            const float2 *const sW2 = reinterpret_cast<const float2 *>(&s_W[seg * 32]);   // SP: [k](slot a, slot b)
 
             // ---------------- 2-3. dynamics, unary checks and geometry, both candidates at once
             const bool act = first <= t;
@@ -470,8 +495,14 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 const V fx = vmap(x, [&](float p) { return __saturatef(fmaf(p, inv0, nlo0)); });
                 const V fy = vmap(y, [&](float p) { return __saturatef(fmaf(p, inv1, nlo1)); });
                 const V fz = vmap(z, [&](float p) { return __saturatef(fmaf(p, inv2, nlo2)); });
-                wx = tripoly(Wn, c0x, fx, fy, fz);
-                wy = tripoly(Wn + 8, c0y, fx, fy, fz);
+                if constexpr (SP) {
+                    const float2 cx0 = sW2[0], cy0 = sW2[8];
+                    wx = tripoly2(sW2, make_float2(cx0.x + c0x, cx0.y + gxb), fx, fy, fz);
+                    wy = tripoly2(sW2 + 8, make_float2(cy0.x + c0y, cy0.y + gyb), fx, fy, fz);
+                } else {
+                    wx = tripoly(Wn, c0x, fx, fy, fz);
+                    wy = tripoly(Wn + 8, c0y, fx, fy, fz);
+                }
             }
             // Eq. hor, coordinated-turn lift and parabolic drag (R12):
             // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a grounded / inactive / violated aircraft
@@ -618,6 +649,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const int flagB = Ap->flagB;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
+                if (SP && c == 1 && s + 1 >= s_hi) continue;         // odd sample count: no second sample
                 float J = 1.0f, c0 = 1.f, c1 = 1.f, c2 = 1.f, c3 = 1.f;
                 if (Ha > 0 && isac) {
                     const float Jfuel = clamp01(1.0f - cget(fuel, c) * invFmax);
@@ -649,11 +681,13 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         }
     }  // s
 
+    constexpr int ENC = SP ? 1 : NC;               // candidates in the epilogue
+    if constexpr (SP) ell[0] = ell[0] + ell[1];    // both slots' samples of the single candidate
     if (args.part) {      // chunked evaluation: partial log2 weights, MH in k_combine
         if (valid && isac) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-                args.part[(((size_t)blockIdx.y * NC + c) * n + lane) * args.L + lloc] = ell[c];
+            for (int c = 0; c < ENC; ++c)
+                args.part[(((size_t)blockIdx.y * ENC + c) * n + lane) * args.L + lloc] = ell[c];
         }
         return;
     }
@@ -662,11 +696,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     float *s_ell = reinterpret_cast<float *>(s_pos);          // reuse [NC][kBlock]
     int *s_dec = reinterpret_cast<int *>(s_V);                 // [SEGS]
 #pragma unroll
-    for (int c = 0; c < NC; ++c) s_ell[c * kBlock + tid] = ell[c];
+    for (int c = 0; c < ENC; ++c) s_ell[c * kBlock + tid] = ell[c];
     __syncwarp();
-    double lam[NC];
+    double lam[ENC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
+    for (int c = 0; c < ENC; ++c) {
         lam[c] = 0.0;
         for (int i = 0; i < n; ++i) lam[c] += (double)s_ell[c * kBlock + seg * W + i];
     }
@@ -675,22 +709,22 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     int nacc = 0;
     float ell_s = ell[0];
     double lam_s = lam[0];
-    if (NC == 2) {
+    if constexpr (ENC == 2) {
         if (args.mh_mode == 2) {
             // per-aircraft MH (R46): every lane decides for its own aircraft
-            const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[NC - 1], l, (uint32_t)lane, k, mpc,
+            const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[ENC - 1], l, (uint32_t)lane, k, mpc,
                                                        sc.key0, sc.key1);
             const unsigned b = __ballot_sync(0xffffffffu, ai);
             mask = (W == 32) ? b : ((b >> ((tid & 31) & ~(W - 1))) & ((1u << (W & 31)) - 1u));
-            ell_s = ai ? ell[NC - 1] : ell[0];
+            ell_s = ai ? ell[ENC - 1] : ell[0];
             lam_s = 0.0;
-            for (int i = 0; i < n; ++i) lam_s += (double)s_ell[(((mask >> i) & 1u) ? NC - 1 : 0) * kBlock + seg * W + i];
+            for (int i = 0; i < n; ++i) lam_s += (double)s_ell[(((mask >> i) & 1u) ? ENC - 1 : 0) * kBlock + seg * W + i];
             nacc = __popc(mask);
         } else {
             const bool acc = mh_decide(lam[0], lam[1], l, k, mpc, sc.key0, sc.key1);
             mask = acc ? 0xFFFFFFFFu : 0u;
-            ell_s = acc ? ell[NC - 1] : ell[0];
-            lam_s = acc ? lam[NC - 1] : lam[0];
+            ell_s = acc ? ell[ENC - 1] : ell[0];
+            lam_s = acc ? lam[ENC - 1] : lam[0];
             nacc = acc ? 1 : 0;
         }
     }
@@ -700,15 +734,15 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         args.surv_out[lloc] = mask;
         if (args.lam_cand) {
             args.lam_cand[lloc] = lam[0];
-            args.lam_cand[args.L + lloc] = lam[NC - 1];
+            args.lam_cand[args.L + lloc] = lam[ENC - 1];
         }
         if (DEBUG && args.dbg_ell_c) {
-            for (int c = 0; c < NC; ++c)
+            for (int c = 0; c < ENC; ++c)
                 for (int i = 0; i < n; ++i)
                     args.dbg_ell_c[((size_t)c * args.L + lloc) * n + i] = s_ell[c * kBlock + seg * W + i];
         }
     }
-    if (lane == 0) s_dec[seg] = (valid && NC == 2) ? nacc : 0;
+    if (lane == 0) s_dec[seg] = (valid && ENC == 2) ? nacc : 0;
     // per-column max of the survivor log-weights (K3, first half)
     __syncthreads();
     uint32_t *s_cm = reinterpret_cast<uint32_t *>(s_ctrl);
@@ -719,15 +753,15 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
         for (int sg = 0; sg < SEGS; ++sg) mx = max(mx, s_cm[sg * W + tid]);
         if (mx) atomicMax(&args.colmax[tid], mx);
     }
-    if (NC == 2 && tid == 0) {
+    if (ENC == 2 && tid == 0) {
         unsigned long long cnt = 0;
         for (int sg = 0; sg < SEGS; ++sg) cnt += s_dec[sg];
         if (cnt) atomicAdd(args.n_accept, cnt);
     }
 }
 
-size_t rollout_smem_bytes(int W, int NC, int H, int ng) {
-    const int SEGS = kBlock / W;
+size_t rollout_smem_bytes(int W, int NC, int H, int ng, bool sp) {
+    const int SEGS = kBlock / W, NSL = sp ? 2 : 1;
     if (ng > 8) {
         const size_t zs = ((size_t)SEGS * dense_zst(ng) + 3) & ~(size_t)3;
         return sizeof(float4) * ((size_t)H * NC * kBlock) +
@@ -735,7 +769,7 @@ size_t rollout_smem_bytes(int W, int NC, int H, int ng) {
                sizeof(float4) * 3 * kBlock + sizeof(float) * (size_t)ng * dense_qts(ng) + 16;
     }
     const int GB = (W >= 8) ? W / 4 : 1;
-    return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * (SEGS * GB * 16 + 2 * SEGS * 16) +
+    return sizeof(float4) * ((size_t)H * NC * kBlock) + sizeof(float) * NSL * (SEGS * GB * 16 + 2 * SEGS * 16) +
            sizeof(float4) * 3 * kBlock + sizeof(float) * 72 + 16;
 }
 
@@ -801,10 +835,10 @@ __global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) 
     }
 }
 
-template <int W, int NC, bool DEBUG, bool DENSE, int R = W>
+template <int W, int NC, bool DEBUG, bool DENSE, int R = W, bool SP = false>
 static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
-    const size_t smem = rollout_smem_bytes(W, NC, sc.H, DENSE ? sc.wng : 8);
-    auto kern = k_rollout<W, NC, DEBUG, DENSE, R>;
+    const size_t smem = rollout_smem_bytes(W, NC, sc.H, DENSE ? sc.wng : 8, SP);
+    auto kern = k_rollout<W, NC, DEBUG, DENSE, R, SP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int segs = kBlock / W;
@@ -816,7 +850,7 @@ static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_
     kern<<<dim3(grid, chunks), kBlock, smem, st>>>(sc, b);
     e = cudaGetLastError();
     if (e != cudaSuccess || chunks == 1) return e;
-    k_combine<NC><<<(a.L + 127) / 128, 128, 0, st>>>(sc, b, chunks);
+    k_combine<SP ? 1 : NC><<<(a.L + 127) / 128, 128, 0, st>>>(sc, b, chunks);
     return cudaGetLastError();
 }
 
@@ -841,6 +875,29 @@ int rollout_blocks_per_sm(int n, int H, int NC, int ng) {
 static bool ring_enabled() {
     static const bool on = [] { const char *e = getenv("SMC_K2_RING"); return !(e && strcmp(e, "0") == 0); }();
     return on;
+}
+
+static bool sp_enabled() {
+    static const bool on = [] { const char *e = getenv("SMC_K2_SP"); return !(e && strcmp(e, "0") == 0); }();
+    return on;
+}
+
+// Single-candidate launches on the 2x2x2 grid with W >= 8: sample pairs in the float2 slots
+// (both control pointers = the one candidate); SMC_K2_SP=0 runs them one sample per lane.
+static cudaError_t launch_sp(int W, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    RolloutArgs b = a;
+    b.ctrl[1] = a.ctrl[0];
+    if (ring_enabled()) {
+        if (W == 32 && sc.n == 24) return launch_w<32, 2, false, false, 24, true>(sc, b, st);
+        if (W == 16 && sc.n == 12) return launch_w<16, 2, false, false, 12, true>(sc, b, st);
+        if (W == 16 && sc.n == 10) return launch_w<16, 2, false, false, 10, true>(sc, b, st);
+    }
+    switch (W) {
+        case 8: return launch_w<8, 2, false, false, 8, true>(sc, b, st);
+        case 16: return launch_w<16, 2, false, false, 16, true>(sc, b, st);
+        case 32: return launch_w<32, 2, false, false, 32, true>(sc, b, st);
+    }
+    return cudaErrorInvalidValue;
 }
 
 template <int NC, bool DEBUG>
@@ -881,6 +938,7 @@ int segment_width(int n, bool dense) {
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st) {
     const bool dense = sc.wng > 8;
     const int W = segment_width(sc.n, dense);
+    if (NC == 1 && !debug && !dense && W >= 8 && sp_enabled()) return launch_sp(W, sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }

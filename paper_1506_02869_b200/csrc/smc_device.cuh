@@ -101,6 +101,13 @@ __device__ __forceinline__ V tripoly(const float *c, float c0, V fx, V fy, V fz)
     return vfma(fx, A, B);
 }
 
+// The same with per-slot coefficients (sample pairs: slot a in .x, slot b in .y).
+__device__ __forceinline__ float2 tripoly2(const float2 *c, float2 c0, float2 fx, float2 fy, float2 fz) {
+    const float2 A = vfma(fy, vfma(fz, c[7], c[4]), vfma(fz, c[5], c[1]));
+    const float2 B = vfma(fy, vfma(fz, c[6], c[2]), vfma(fz, c[3], c0));
+    return vfma(fx, A, B);
+}
+
 // Uniform (2k+1) 2^-24, k = w >> 9: exact in binary32 (R37).
 __device__ __forceinline__ float unif(uint32_t w) {
     return __fmaf_rn(__uint2float_rn(w >> 9), 0x1.0p-23f, 0x1.0p-24f);
