@@ -141,9 +141,22 @@ def test_rollout_landing_exercised(smc):
     _compare_rollouts(smc, scn, L, 2, k=0, seed=7, ctrl=ctrl)
 
 
-def test_evaluate_parity(smc):
-    scn, cfg = sc.config(2)
-    L, S = 96, 5
+@pytest.mark.parametrize("case,sp", [("c2", "1"), ("c2", "0"), ("table1", "1"), ("n24", "1"), ("n12_noise", "1"),
+                                     ("n24", "0")])
+def test_evaluate_parity(smc, case, sp, monkeypatch):
+    """Single-candidate evaluation (round 0 / paper mode) against the oracle: sample pairs in
+    the float2 slots (SMC_K2_SP, default) or one sample per lane, S odd (last pair half
+    used), and the exact-count separation rings (n = 10, 12, 24)."""
+    monkeypatch.setenv("SMC_K2_SP", sp)
+    if case == "table1":
+        scn, cfg = sc.config(6)
+    elif case == "n24":
+        scn, cfg = sc.config(3)
+    elif case == "n12_noise":
+        scn, cfg = sc.config(4, noise_w=0.2)
+    else:
+        scn, cfg = sc.config(2)
+    L, S = (96, 5) if scn["n"] <= 12 else (24, 3)
     ctrl = _near_trim_controls(scn, L, seed=3)
     sol = _solver(smc, scn, L=L, S=S, seed=cfg.seed)
     ell_g = sol.debug_evaluate(ctrl, S, 4).astype(np.float64)
@@ -158,7 +171,9 @@ def test_evaluate_parity(smc):
         fin = np.isfinite(ell_o[l])
         assert np.array_equal(fin, np.isfinite(ell_g[l])), l
         assert np.allclose(ell_g[l][fin], ell_o[l][fin], rtol=0, atol=1e-4 * (np.abs(ell_o[l][fin]).max() + S)), l
-    assert bad < 0.05 * L
+    # R30: rollouts within 1e-4 of a decision threshold are excluded and must stay rare (the
+    # 12-aircraft noise scenario has more thresholds: landing cone, envelope and noise kink)
+    assert bad < (0.1 if case == "n12_noise" else 0.05) * L
 
 
 def test_mh_bitexact(smc):
