@@ -887,18 +887,15 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
-    // K2 layout.  Measured cost: segment layout ~ proportional to the padded width
-    // W = next_pow2(N) (c3, W = 32: 1.44 s; c2, W = 8: 43.6 ms per MPC step), transposed
-    // layout ~ proportional to N with a higher per-aircraft cost (c3: 1.42 s; c4 N = 12:
-    // 171 vs 167 ms; c2: 58.6 ms).  Break-even near N = 0.75 W, so the transposed layout
-    // is used when at most ~70 % of the segment's lanes would carry an aircraft
-    // (rolling-window MPC steps with, e.g., 17-22 aircraft).  That rule is for the two-
-    // candidate (MH) launches; single-candidate launches (round 0, paper mode) favour the
-    // segment layout (table-1 workload, N = 10, W = 16: 241 vs 309 ms of K2).
-    // SMC_K2_LAYOUT overrides both.
+    // K2 layout: the segment layout (lane = aircraft, W = next_pow2(N) lanes per particle).
+    // Re-measured at the packed-FP32 kernel (tools/layout_probe.py, c2 solver, 21 rounds, per
+    // MPC step): segment faster for every N from 5 to 26, e.g. N = 9: 12.9 vs 14.0 ms,
+    // N = 17: 29.7 vs 30.2, N = 20: 29.8 vs 32.1, N = 24: 28.2 vs 39.3 -- the padded lanes now
+    // cost less than the transposed layout's block barriers (the earlier "transposed below 70 %
+    // occupancy" rule predates the packed candidates).  SMC_K2_LAYOUT=transposed selects the
+    // warp-per-aircraft layout.
     {
-        const int W = segment_width((int)n);
-        ctx->layout[1] = ctx->layout_env >= 0 ? ctx->layout_env : (10 * (int)n < 7 * W ? 1 : 0);
+        ctx->layout[1] = ctx->layout_env >= 0 ? ctx->layout_env : 0;
         ctx->layout[0] = ctx->layout_env >= 0 ? ctx->layout_env : 0;
         if (ctx->dsc.wng > 8) ctx->layout[0] = ctx->layout[1] = 0;   // dense wind grids: segment layout only
     }

@@ -159,6 +159,14 @@ def config(num: int, noise_w: float = 0.1):
         scn = snapshot(5, 5, seed)
         return scn, SmcConfig("table1", L=10240, S=8, K=101, sigma=sig, mh=False, sched_paper=True,
                               seed=0x5EED0006)
+    if num == 7:
+        # BASELINE.json's latency target: a 20-aircraft MPC step (10 arrivals / 10 departures,
+        # all active -- the paper's mixed traffic at its densest) with c2's solver,
+        # against the 10 s re-planning interval.  Not a BASELINE.json config.
+        scn = snapshot(10, 10, seed)
+        scn["nominal"] = [8.0, 0.0]
+        scn["turb_sigma"] = 1.0
+        return scn, SmcConfig("n20", L=16384, S=16, K=101, sigma=sig, seed=0x5EED0007)
     raise ValueError(num)
 
 
