@@ -153,9 +153,9 @@ __host__ __device__ constexpr int dense_zst(int G) { return 2 * G + 2; }
 // row stride of the transposed factor Qhat^T [G][QTS] (multiple of 4 for 16-byte rows, zero padded)
 __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 4; }
 
-// R: separation ring size -- W (every lane of the segment, idle lanes publish NaN), or the exact
-// aircraft count n < W for the benchmark shapes (partners d = 1..R/2 at compile time, idle lanes
-// publish nothing)
+// R: separation ring size, n <= R <= W: lanes < R publish their position (NaN when they carry no
+// flying aircraft) and scan partners d = 1..R/2 (mod R) at compile time; lanes >= R publish
+// nothing.  R = W is the plain segment ring.
 // SP (sample pairs, single-candidate launches): the two float2 slots carry samples s and s+1 of
 // the same particle instead of two MH candidates -- each slot its own wind / gust draws, the
 // two log-weights summed at the end; launched as NC = 2 with both control pointers equal.
@@ -569,7 +569,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const int pb = seg * 2 * W + lane;
             float4 *s_pxy = s_pos;                                           // [2 kBlock]
             float2 *s_pz = reinterpret_cast<float2 *>(s_pos + 2 * kBlock);   // [2 kBlock] (NC = 2)
-            if (R == W || isac) {
+            if (R == W || lane < R) {
                 if constexpr (NC == 2) {
                     const float4 e = make_float4(px.x, px.y, ny.x, ny.y);
                     s_pxy[pb] = e; s_pxy[pb + R] = e;
@@ -884,18 +884,44 @@ static bool sp_enabled() {
 
 // Single-candidate launches on the 2x2x2 grid with W >= 8: sample pairs in the float2 slots
 // (both control pointers = the one candidate); SMC_K2_SP=0 runs them one sample per lane.
+// Ring sizes with instances below W (smallest R >= n is used): N = 5-6 in W = 8, 9-14 in 16,
+// 17-28 in 32 -- the separation scan needs R/2 partner offsets instead of W/2.
+static int ring_for(int W, int n) {
+    if (!ring_enabled()) return W;
+    static const int r8[] = {6}, r16[] = {10, 12, 14}, r32[] = {20, 24, 28};
+    const int *r = W == 8 ? r8 : (W == 16 ? r16 : (W == 32 ? r32 : nullptr));
+    const int m = W == 8 ? 1 : (W == 16 || W == 32 ? 3 : 0);
+    for (int q = 0; q < m; ++q)
+        if (n <= r[q]) return r[q];
+    return W;
+}
+
+template <int W, int NC, bool DEBUG, bool SP>
+static cudaError_t launch_ring(int R, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    if constexpr (W == 8) {
+        if (R == 6) return launch_w<8, NC, DEBUG, false, 6, SP>(sc, a, st);
+    } else if constexpr (W == 16) {
+        if (R == 10) return launch_w<16, NC, DEBUG, false, 10, SP>(sc, a, st);
+        if (R == 12) return launch_w<16, NC, DEBUG, false, 12, SP>(sc, a, st);
+        if (R == 14) return launch_w<16, NC, DEBUG, false, 14, SP>(sc, a, st);
+    } else if constexpr (W == 32) {
+        if (R == 20) return launch_w<32, NC, DEBUG, false, 20, SP>(sc, a, st);
+        if (R == 24) return launch_w<32, NC, DEBUG, false, 24, SP>(sc, a, st);
+        if (R == 28) return launch_w<32, NC, DEBUG, false, 28, SP>(sc, a, st);
+    }
+    return launch_w<W, NC, DEBUG, false, W, SP>(sc, a, st);
+}
+
+// Single-candidate launches on the 2x2x2 grid with W >= 8: sample pairs in the float2 slots
+// (both control pointers = the one candidate); SMC_K2_SP=0 runs them one sample per lane.
 static cudaError_t launch_sp(int W, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     RolloutArgs b = a;
     b.ctrl[1] = a.ctrl[0];
-    if (ring_enabled()) {
-        if (W == 32 && sc.n == 24) return launch_w<32, 2, false, false, 24, true>(sc, b, st);
-        if (W == 16 && sc.n == 12) return launch_w<16, 2, false, false, 12, true>(sc, b, st);
-        if (W == 16 && sc.n == 10) return launch_w<16, 2, false, false, 10, true>(sc, b, st);
-    }
+    const int R = ring_for(W, sc.n);
     switch (W) {
-        case 8: return launch_w<8, 2, false, false, 8, true>(sc, b, st);
-        case 16: return launch_w<16, 2, false, false, 16, true>(sc, b, st);
-        case 32: return launch_w<32, 2, false, false, 32, true>(sc, b, st);
+        case 8: return launch_ring<8, 2, false, true>(R, sc, b, st);
+        case 16: return launch_ring<16, 2, false, true>(R, sc, b, st);
+        case 32: return launch_ring<32, 2, false, true>(R, sc, b, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -911,20 +937,15 @@ static cudaError_t launch_nc(int W, bool dense, const DevScen &sc, const Rollout
         }
         return cudaErrorInvalidValue;
     }
-    // separation rings of the exact aircraft count for the benchmark shapes (c3: 24, c4: 12,
-    // Table 1: 10) -- the scan needs n/2 partner offsets instead of W/2 (SMC_K2_RING=0: off)
-    if (ring_enabled()) {
-        if (W == 32 && sc.n == 24) return launch_w<32, NC, DEBUG, false, 24>(sc, a, st);
-        if (W == 16 && sc.n == 12) return launch_w<16, NC, DEBUG, false, 12>(sc, a, st);
-        if (W == 16 && sc.n == 10) return launch_w<16, NC, DEBUG, false, 10>(sc, a, st);
-    }
+    // separation rings smaller than the segment (SMC_K2_RING=0: off)
+    const int R = ring_for(W, sc.n);
     switch (W) {
         case 1: return launch_w<1, NC, DEBUG, false>(sc, a, st);
         case 2: return launch_w<2, NC, DEBUG, false>(sc, a, st);
         case 4: return launch_w<4, NC, DEBUG, false>(sc, a, st);
-        case 8: return launch_w<8, NC, DEBUG, false>(sc, a, st);
-        case 16: return launch_w<16, NC, DEBUG, false>(sc, a, st);
-        case 32: return launch_w<32, NC, DEBUG, false>(sc, a, st);
+        case 8: return launch_ring<8, NC, DEBUG, false>(R, sc, a, st);
+        case 16: return launch_ring<16, NC, DEBUG, false>(R, sc, a, st);
+        case 32: return launch_ring<32, NC, DEBUG, false>(R, sc, a, st);
     }
     return cudaErrorInvalidValue;
 }
