@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
                 const uint32_t x2 = s_perturb_x2[r];
                 const float c0 = cv[u][0], c1 = cv[u][1], c2 = cv[u][2];
                 xp[3 * e] = c0; xp[3 * e + 1] = c1; xp[3 * e + 2] = c2;
-                const uint4 w = draw(TAG_PERTURB, p.l0 + s_j[r], p.k << 16, (uint32_t)t | x2, mpc, p.key0, p.key1);
+                const uint4 w = draw_ks(TAG_PERTURB, p.l0 + s_j[r], p.k << 16, (uint32_t)t | x2, mpc, p.ks);
                 const float4 z = box_muller4(w);
                 float o0 = fmaf(p.sig[0], z.x, c0), o1 = fmaf(p.sig[1], z.y, c1), o2 = fmaf(p.sig[2], z.z, c2);
                 if (p.clamp) {
@@ -637,9 +637,14 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
     reset_round_state(p);
 }
 
-cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st) {
-    const size_t rows = (size_t)p.L * p.n;
+cudaError_t launch_gather_propose(const ProposeArgs &p0, cudaStream_t st) {
+    const size_t rows = (size_t)p0.L * p0.n;
     if (!rows) return cudaSuccess;
+    ProposeArgs p = p0;                     // Philox round keys as kernel parameters (as in K2)
+    for (int r = 0; r < 10; ++r) {
+        p.ks[2 * r] = p.key0 + (uint32_t)r * 0x9E3779B9u;
+        p.ks[2 * r + 1] = p.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
     size_t g = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
     if (g > 148 * 16) g = 148 * 16;
     k_gather_propose<<<(unsigned)g, 256, 0, st>>>(p);

@@ -111,6 +111,7 @@ struct ProposeArgs {
     size_t reset_status_n;
     int reset_n;
     float *xp, *xs;             // outputs [L][n][H][3]
+    uint32_t ks[20];            // Philox round keys of (key0, key1) (nullable use: all zero -> computed)
     float sig[3];
     int clamp;
     const float *lo3, *hi3;     // per aircraft [n][3] envelope for clamping
