@@ -36,6 +36,9 @@
 #ifndef SMC_K2_MINB1
 #define SMC_K2_MINB1 5  // the same for single-candidate launches (round 0, paper mode; sweep: 5 > 6 > 4)
 #endif
+#ifndef SMC_K2_MINBSP
+#define SMC_K2_MINBSP 3   // sample-pair launches (Table-1 workload: 3 -> 181.4, 5 -> 184.1, 4 -> 188.5 ms)
+#endif
 #ifndef SMC_K2_MINB32
 #define SMC_K2_MINB32 SMC_K2_MINB  // two candidates in 32-lane segments (N > 16)
 #endif
@@ -160,7 +163,7 @@ __host__ __device__ constexpr int dense_qts(int G) { return 4 * ((G + 3) / 4) + 
 // the same particle instead of two MH candidates -- each slot its own wind / gust draws, the
 // two log-weights summed at the end; launched as NC = 2 with both control pointers equal.
 template <int W, int NC, bool DEBUG, bool DENSE, int R = W, bool SP = false>
-__global__ void __launch_bounds__(kBlock, (NC == 1 || SP) ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB))
+__global__ void __launch_bounds__(kBlock, SP ? SMC_K2_MINBSP : (NC == 1 ? SMC_K2_MINB1 : (W >= 32 ? SMC_K2_MINB32 : SMC_K2_MINB)))
 k_rollout(const DevScen sc, const RolloutArgs args) {
     static_assert(!SP || (NC == 2 && !DENSE && !DEBUG && W >= 8), "sample pairs: two slots, 2x2x2 grid, W >= 8");
     constexpr int NSL = SP ? 2 : 1;                 // wind realisations per segment and step
