@@ -36,6 +36,9 @@
 #ifndef SMC_K2_MINB1
 #define SMC_K2_MINB1 5  // the same for single-candidate launches (round 0, paper mode; sweep: 5 > 6 > 4)
 #endif
+#ifndef SMC_K2_FASTTRIG
+#define SMC_K2_FASTTRIG 1   // control staging: MUFU sin/cos (A/B on c2: 27.80 vs 28.11 ms of K2)
+#endif
 #ifndef SMC_K2_MINBSP
 #define SMC_K2_MINBSP 3   // sample-pair launches (Table-1 workload: 3 -> 181.4, 5 -> 184.1, 4 -> 188.5 ms)
 #endif
@@ -233,9 +236,14 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 float T = 0.f, ph = 0.f, ga = 0.f;
                 if (isac && valid) { T = src[c][3 * t]; ph = src[c][3 * t + 1]; ga = src[c][3 * t + 2]; }
                 float sph, cph, sga, cga;
+#if SMC_K2_FASTTRIG
+                __sincosf(ph, &sph, &cph);                    // |phi| < 30 deg, |gamma| < 6 deg: MUFU
+                __sincosf(ga, &sga, &cga);
+#else
                 sincosf(ph, &sph, &cph);
                 sincosf(ga, &sga, &cga);
-                q[c][0] = T; q[c][1] = sph / cph; q[c][2] = sga; q[c][3] = cga;
+#endif
+                q[c][0] = T; q[c][1] = SMC_K2_FASTTRIG ? sph * rcp_approx(cph) : sph / cph; q[c][2] = sga; q[c][3] = cga;
                 const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
                 cbad[c] |= (bad ? 1u : 0u) << t;
             }
