@@ -562,9 +562,15 @@ __device__ __forceinline__ void reset_round_state(const ProposeArgs &p) {
 // is made).  Phase 2: one thread per (row, step) copies the parent's control
 // triple and writes the Gaussian proposal -- consecutive threads write
 // consecutive 12-byte triples, so both output streams are coalesced.
-constexpr int kRowsPerBlock = 256;   // = blockDim: every thread runs one bisection in phase 1
+#ifndef SMC_K6_ROWS
+#define SMC_K6_ROWS 128   // c2 A/B (MPC step, 3 repeats): 256 rows 29.24 ms, 128 rows 29.17, 128 rows + batch 6 29.15
+#endif
+#ifndef SMC_K6_BATCH
+#define SMC_K6_BATCH 6    // 256 rows + batch 6: 29.72 ms; 512 rows + batch 6: 29.83 ms
+#endif
+constexpr int kRowsPerBlock = SMC_K6_ROWS;   // = blockDim: every thread runs one bisection in phase 1
 
-__global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
+__global__ void __launch_bounds__(kRowsPerBlock) k_gather_propose(const ProposeArgs p) {
     __shared__ const float *s_src[kRowsPerBlock];
     __shared__ uint32_t s_j[kRowsPerBlock];
     __shared__ uint32_t s_perturb_x2[kRowsPerBlock];     // (i << 8): the aircraft part of the PERTURB counter
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(256) k_gather_propose(const ProposeArgs p) {
         float *const xp = p.xp + (size_t)q0 * H * 3, *const xs = p.xs + (size_t)q0 * H * 3;
         // batches of kBatch elements per thread: all parent loads (read-only path) are issued
         // before any store, so their latencies overlap
-        constexpr int kBatch = 4;
+        constexpr int kBatch = SMC_K6_BATCH;
         for (int e0 = 0; e0 < tot; e0 += kBatch * (int)blockDim.x) {
             float cv[kBatch][3];
 #pragma unroll
@@ -646,8 +652,8 @@ cudaError_t launch_gather_propose(const ProposeArgs &p0, cudaStream_t st) {
         p.ks[2 * r + 1] = p.key1 + (uint32_t)r * 0xBB67AE85u;
     }
     size_t g = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
-    if (g > 148 * 16) g = 148 * 16;
-    k_gather_propose<<<(unsigned)g, 256, 0, st>>>(p);
+    if (g > 148 * 16 * 256 / kRowsPerBlock) g = 148 * 16 * 256 / kRowsPerBlock;   // same thread count for any block size
+    k_gather_propose<<<(unsigned)g, kRowsPerBlock, 0, st>>>(p);
     return cudaGetLastError();
 }
 
