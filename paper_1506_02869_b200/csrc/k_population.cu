@@ -411,20 +411,45 @@ __device__ __forceinline__ int32_t find_ancestor(const unsigned long long *C, ui
 // Two-level search: the group g of kCdfSample entries whose sample Cs[g] first exceeds t_j
 // (bisection over L / 16 samples: a small, cache-resident array), then the slot's ancestor
 // inside that group (four steps within one 128-byte line).  Same result as find_ancestor.
+#ifndef SMC_K6_ARY
+#define SMC_K6_ARY 3   // c2 A/B (MPC step, 3 repeats): 2 -> 29.233 ms, 3 -> 29.209, 4 -> 29.257, 8 -> 29.527
+#endif
+// First index in [lo, hi] whose entry exceeds tj (hi if none), for a non-decreasing array.
+// K-ary rounds: the K - 1 probes of a round are independent loads, so a search over n
+// entries waits on ~log_K(n) load latencies instead of log_2(n); same result as bisection.
+template <int K>
+__device__ __forceinline__ uint32_t first_above(const unsigned long long *A, uint32_t lo, uint32_t hi, uint64_t tj) {
+    if constexpr (K > 2) {
+        while (hi - lo >= (uint32_t)K) {
+            const uint32_t span = hi - lo;
+            uint32_t p[K - 1];
+            unsigned long long c[K - 1];
+#pragma unroll
+            for (int q = 0; q < K - 1; ++q) {
+                p[q] = lo + (uint32_t)(((uint64_t)span * (uint32_t)(q + 1)) / (uint32_t)K);
+                c[q] = __ldg(&A[p[q]]);
+            }
+            uint32_t nlo = p[K - 2] + 1, nhi = hi;
+#pragma unroll
+            for (int q = K - 2; q >= 0; --q) {
+                if (c[q] > tj) { nhi = p[q]; nlo = q ? p[q - 1] + 1 : lo; }
+            }
+            lo = nlo; hi = nhi;
+        }
+    }
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&A[mid]) > tj) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ int32_t find_ancestor2(const unsigned long long *C, const unsigned long long *Cs,
                                                   uint32_t L, uint32_t M, uint64_t Q, uint64_t R, uint32_t j) {
     const uint64_t tj = slot_t(j, Q / M, Q % M, R, M);
-    uint32_t lo = 0, hi = cdf_samples(L) - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(&Cs[mid]) > tj) hi = mid; else lo = mid + 1;
-    }
-    uint32_t a = lo * kCdfSample, b = min(a + kCdfSample, L) - 1;
-    while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (__ldg(&C[mid]) > tj) b = mid; else a = mid + 1;
-    }
-    return (int32_t)a;
+    const uint32_t g = first_above<SMC_K6_ARY>(Cs, 0, cdf_samples(L) - 1, tj);
+    const uint32_t a = g * kCdfSample, b = min(a + kCdfSample, L) - 1;
+    return (int32_t)first_above<SMC_K6_ARY>(C, a, b, tj);
 }
 
 __global__ void k_ancestors(const ResampleArgs r) {
