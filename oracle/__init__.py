@@ -8,9 +8,11 @@ FP64), written from PAPER.md (Eele & Maciejowski 2015) and pinned by the
 ``-m "not gpu"`` tests under ``tests/test_oracle_*.py``.
 
 Parity status: see the header of ``smc_oracle.c``.  The rolling-window
-averaging (R20), post-landing bonus (R18), removal of violated aircraft (R42)
-and the MH move (R1) are conventions the paper states in prose only; they are
-pinned by invariants and closed forms in ``tests/test_oracle_conventions.py``.
+averaging (R20), post-landing bonus (R18), constraint handling after a
+violation (Alg.1 l.11-13: the violator keeps flying and stays in
+every pair test) and the MH move (R1) are conventions the paper states in
+prose; they are pinned by invariants and closed forms in
+``tests/test_oracle_conventions.py``.
 """
 from __future__ import annotations
 
@@ -86,8 +88,12 @@ class _Derived(C.Structure):
 
 
 class _RollOut(C.Structure):
-    _fields_ = [("J", _dp), ("comp", _dp), ("traj", _dp), ("fuel", _dp), ("margin", _dp),
-                ("viol", _ip), ("landed_step", _ip)]
+    _fields_ = [("J", _dp), ("comp", _dp), ("traj", _dp), ("fuel", _dp), ("margin", _dp), ("margin_land", _dp),
+                ("viol", _ip), ("landed_step", _ip), ("replayed", _ip)]
+
+
+class _Replay(C.Structure):
+    _fields_ = [("landed_step", _ip), ("viol", _ip), ("eps", C.c_double)]
 
 
 class _SmcCfg(C.Structure):
@@ -124,7 +130,10 @@ def _declare(L):
         "ora_beta": (d, [d, d, d]),
         "ora_angdist": (d, [d]),
         "ora_rollout": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, P(_RollOut)]),
+        "ora_rollout_replay": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, P(_Replay),
+                                      P(_RollOut)]),
         "ora_evaluate": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, _dp, C.c_int]),
+        "ora_evaluate_margin": (None, [P(_Problem), P(_Derived), _dp, u32, u32, u32, u64, u32, _dp, _dp, C.c_int]),
         "ora_init_population": (None, [P(_Problem), u32, u64, u32, _dp]),
         "ora_fuel_estimate1": (C.c_int, [P(_Problem), C.c_int, _dp, _dp, C.c_int, d, d, _dp, _dp]),
         "ora_fuel_estimate2": (C.c_int, [P(_Problem), C.c_int, _dp, _dp, C.c_int, d, d, _dp]),
@@ -269,25 +278,43 @@ class Problem:
         return bool(lib().ora_pair_conflict(C.byref(self.p), _ptr(_f64(a, (6,))), _ptr(_f64(b, (6,)))))
 
     # -- rollout / population ---------------------------------------------
-    def rollout(self, u, l, s, k, seed, mpc=0):
+    def rollout(self, u, l, s, k, seed, mpc=0, replay=None):
+        """One rollout.  replay = (landed_step[n], viol[n], eps): decisions whose own
+        margin is below eps follow the given ones (R30 decision replay)."""
         n, H = self.n, self.H
         u = _f64(u, (n, H, 3))
         res = {"J": np.zeros(n), "comp": np.zeros((n, 4)), "traj": np.zeros((n, H + 1, 6)),
-               "fuel": np.zeros(n), "margin": np.zeros(n),
-               "viol": np.zeros(n, np.int32), "landed_step": np.zeros(n, np.int32)}
+               "fuel": np.zeros(n), "margin": np.zeros(n), "margin_land": np.zeros(n),
+               "viol": np.zeros(n, np.int32), "landed_step": np.zeros(n, np.int32),
+               "replayed": np.zeros(n, np.int32)}
         o = _RollOut(_ptr(res["J"]), _ptr(res["comp"]), _ptr(res["traj"]), _ptr(res["fuel"]),
-                     _ptr(res["margin"]), _ptr(res["viol"], C.c_int32), _ptr(res["landed_step"], C.c_int32))
-        lib().ora_rollout(C.byref(self.p), C.byref(self.d), _ptr(u), l, s, k, seed, mpc, C.byref(o))
+                     _ptr(res["margin"]), _ptr(res["margin_land"]), _ptr(res["viol"], C.c_int32),
+                     _ptr(res["landed_step"], C.c_int32), _ptr(res["replayed"], C.c_int32))
+        if replay is None:
+            lib().ora_rollout(C.byref(self.p), C.byref(self.d), _ptr(u), l, s, k, seed, mpc, C.byref(o))
+        else:
+            ls = np.ascontiguousarray(np.asarray(replay[0], dtype=np.int32).reshape(n))
+            vi = np.ascontiguousarray(np.asarray(replay[1], dtype=np.int32).reshape(n))
+            rp = _Replay(_ptr(ls, C.c_int32), _ptr(vi, C.c_int32), float(replay[2]))
+            lib().ora_rollout_replay(C.byref(self.p), C.byref(self.d), _ptr(u), l, s, k, seed, mpc, C.byref(rp),
+                                     C.byref(o))
         return res
 
-    def evaluate(self, ctrl, S, k, seed, mpc=0, ell0=None, nthreads=0):
+    def evaluate(self, ctrl, S, k, seed, mpc=0, ell0=None, nthreads=0, margin=False):
+        """ell [L][n] after S samples (Alg.1 l.9-18); with margin=True also the
+        per-(particle, aircraft) decision margin [L][n] (R30)."""
         n, H = self.n, self.H
         ctrl = _f64(ctrl).reshape(-1, n, H, 3)
         L = ctrl.shape[0]
         ell = np.full((L, n), -np.log2(L) if ell0 is None else ell0, dtype=np.float64)
         nt = nthreads or (os.cpu_count() or 1)
-        lib().ora_evaluate(C.byref(self.p), C.byref(self.d), _ptr(ctrl), L, S, k, seed, mpc, _ptr(ell), nt)
-        return ell
+        if not margin:
+            lib().ora_evaluate(C.byref(self.p), C.byref(self.d), _ptr(ctrl), L, S, k, seed, mpc, _ptr(ell), nt)
+            return ell
+        mg = np.zeros((L, n))
+        lib().ora_evaluate_margin(C.byref(self.p), C.byref(self.d), _ptr(ctrl), L, S, k, seed, mpc, _ptr(ell),
+                                  _ptr(mg), nt)
+        return ell, mg
 
     def init_population(self, L, seed, mpc=0):
         out = np.zeros((L, self.n, self.H, 3))

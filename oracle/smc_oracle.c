@@ -10,16 +10,20 @@
  * (no fused multiply-add except the explicit fma() calls det_exp2 requires).
  *
  * Parity status per function (DESIGN.md section 4 lists the pinning tests):
- *   philox, u24, box_muller, det_exp2, det_quant, derive (Rhat, Qhat, a),
- *   trilinear, popdense, lift_drag, step, unary/landing/pair checks,
- *   flow_heading, arc_length, beta, utilities, weight recursion, mh_accept,
- *   resample_column, select, sample_schedule ........................ pinned
- *   rolling-window averaging (R20), post-landing bonus (R18), removal of a
- *   violated aircraft (R42), MH move semantics (R1) ................ pinned
+ *   philox, u24, box_muller, det_exp2, det_quant, derive (Rhat, Qhat, a, b,
+ *   supB/infB), trilinear, popdense, density, lift_drag, step, unary/landing/
+ *   pair checks, flow_heading, arc_length, beta, utilities (J1..J4, Jalt,
+ *   Jfuel, noise), AR(1) propagation, weight recursion, mh_accept,
+ *   resample_column, select, sample_schedule, init_population, perturb_row,
+ *   plant_step, fuel estimates ........................................ pinned
+ *   rolling-window averaging (R20), post-landing bonus (R18), constraint
+ *   handling after a violation (Alg.1 l.11-13: the violator keeps flying and
+ *   stays in every pair test), MH move semantics (R1) ............... pinned
  *   (conventions the paper states in prose only: pinned by invariants and
  *   closed forms in tests/test_oracle_conventions.py -- shorter-horizon
- *   equivalence, hand-computed post-landing means, violator-absent
- *   equivalence, sigma = 0 reduction of the MH move to Alg.1 l.23)
+ *   equivalence, hand-computed post-landing means, a violator that later
+ *   conflicts with a neighbour zeroes it, sigma = 0 reduction of the MH move
+ *   to Alg.1 l.23)
  */
 #include "smc_oracle.h"
 #include <math.h>
@@ -242,11 +246,15 @@ double ora_popdense_grid(const ora_problem *p, const ora_derived *d, double x, d
     if (!d->pop) return 0.0;
     double gx = (x - p->pop_x0) / p->pop_dx, gy = (y - p->pop_y0) / p->pop_dx;
     double mx = (double)(p->pop_nx - 1), my = (double)(p->pop_ny - 1);
-    if (!(gx > 0.0)) gx = 0.0; if (gx > mx) gx = mx;
-    if (!(gy > 0.0)) gy = 0.0; if (gy > my) gy = my;
+    if (!(gx > 0.0)) gx = 0.0;
+    if (gx > mx) gx = mx;
+    if (!(gy > 0.0)) gy = 0.0;
+    if (gy > my) gy = my;
     int ix = (int)floor(gx), iy = (int)floor(gy);
-    if (ix > p->pop_nx - 2) ix = p->pop_nx - 2; if (ix < 0) ix = 0;
-    if (iy > p->pop_ny - 2) iy = p->pop_ny - 2; if (iy < 0) iy = 0;
+    if (ix > p->pop_nx - 2) ix = p->pop_nx - 2;
+    if (ix < 0) ix = 0;
+    if (iy > p->pop_ny - 2) iy = p->pop_ny - 2;
+    if (iy < 0) iy = 0;
     double fx = gx - ix, fy = gy - iy;
     if (p->pop_nx == 1) fx = 0.0;
     if (p->pop_ny == 1) fy = 0.0;
@@ -384,27 +392,72 @@ int ora_pair_conflict(const ora_problem *p, const double a[6], const double b[6]
 }
 
 static double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
-static double fmin_abs(double cur, double m) { m = fabs(m); return m < cur ? m : cur; }
+
+/* ------------------------------------------------------------------------ */
+/* Decision margins (R30).  Every discrete decision of a rollout  */
+/* is a Boolean combination of comparisons; comparison c holds iff mu_c >= 0 */
+/* (mu_c > 0 for a strict bound), mu_c a relative distance to its threshold. */
+/* An OR of conditions (a violation: any bound fails) changes outcome under  */
+/* a perturbation smaller than e only if every failing condition flips (when */
+/* it is true) or some condition flips (when it is false), so its margin is  */
+/* max_{failing} |mu| if true, min_all |mu| if false.  An AND (landing, a    */
+/* separation conflict) is the OR of the negations: the same formula with    */
+/* "failing" read as "not holding".  Not-a-number never flips (margin inf).  */
+/* ------------------------------------------------------------------------ */
+typedef struct { int any; double true_max, all_min; } ora_or;
+
+static void or_init(ora_or *o) { o->any = 0; o->true_max = 0.0; o->all_min = INFINITY; }
+
+/* one member of an OR: val = its outcome, mu = its margin (>= 0) */
+static void or_add(ora_or *o, int val, double mu)
+{
+    if (mu != mu) mu = INFINITY;
+    if (mu < o->all_min) o->all_min = mu;
+    if (val) { o->any = 1; if (mu > o->true_max) o->true_max = mu; }
+}
+
+static double or_margin(const ora_or *o) { return o->any ? o->true_max : o->all_min; }
+
+/* a bound that must hold: fails iff !(mu >= 0) (strict: !(mu > 0)) */
+static void or_fail_unless(ora_or *o, double mu, int strict)
+{
+    int holds = strict ? (mu > 0.0) : (mu >= 0.0);
+    or_add(o, !holds, fabs(mu));
+}
 
 /* ------------------------------------------------------------------------ */
 /* One rollout (Alg.1 l.10-16 for one particle, one sample)                  */
 /* ------------------------------------------------------------------------ */
-void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
-                 uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
-                 ora_rollout_out *out)
+/* Alg.1 l.10-11 simulate ALL agents to the horizon and only then test the
+ * constraints (l.12-14): a constraint failure sets the aircraft's
+ * weight to 0 and does not change the simulation.  Every active
+ * aircraft therefore flies its own controls to H and stays in every pair test
+ * of Eq. avoidance ("for every time step in the MPC horizon ... for all
+ * i != j") whether or not it has already failed a constraint; a
+ * failing pair zeroes both aircraft.  Only landing removes an arrival
+ * from the simulation ("future time steps within that horizon will not be
+ * planned for that aircraft", R18).  A state that has left the model's
+ * domain (v <= 0 in Eq. hor's L sin(phi)/(m v)) keeps being propagated
+ * literally; once non-finite it fails the envelope and can no longer conflict
+ * (a comparison with a non-finite coordinate is false). */
+void ora_rollout_replay(const ora_problem *p, const ora_derived *d, const double *u,
+                        uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
+                        const ora_replay *rp, ora_rollout_out *out)
 {
     const int n = p->n, H = p->H;
     double st[ORA_MAX_AC][6], nx[ORA_MAX_AC][6];
     double fuel[ORA_MAX_AC], sA[ORA_MAX_AC], sB[ORA_MAX_AC], sC[ORA_MAX_AC], sN[ORA_MAX_AC];
-    double marg[ORA_MAX_AC];
-    int landed[ORA_MAX_AC], viol[ORA_MAX_AC], fly[ORA_MAX_AC], vnow[ORA_MAX_AC];
+    double mland[ORA_MAX_AC];
+    int landed[ORA_MAX_AC], fly[ORA_MAX_AC], replayed[ORA_MAX_AC];
+    ora_or vio[ORA_MAX_AC];
     double Z[2][ORA_MAX_NODES], W[2][ORA_MAX_NODES];
     const int G = d->ng, nblk = (2 * d->ng + 3) / 4;
 
     for (int i = 0; i < n; ++i) {
         memcpy(st[i], &p->x0[6 * i], sizeof(st[i]));
         fuel[i] = sA[i] = sB[i] = sC[i] = sN[i] = 0.0;
-        landed[i] = -1; viol[i] = 0; marg[i] = INFINITY;
+        landed[i] = -1; mland[i] = INFINITY; replayed[i] = 0;
+        or_init(&vio[i]);
         if (out && out->traj) memcpy(&out->traj[((size_t)i * (H + 1)) * 6], st[i], sizeof(st[i]));
     }
     const double twoPr2 = (2.0 * p->P_r) * (2.0 * p->P_r), twoPh = 2.0 * p->P_h;
@@ -430,10 +483,9 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
                 W[c][r] = acc;
             }
 
-        /* Alg.1 l.11: simulate every aircraft in the problem at step t. */
+        /* Alg.1 l.11: simulate every active, not yet landed aircraft at step t. */
         for (int i = 0; i < n; ++i) {
-            fly[i] = (p->first_step[i] <= t) && landed[i] < 0 && !viol[i];
-            vnow[i] = 0;
+            fly[i] = (p->first_step[i] <= t) && landed[i] < 0;
             if (!fly[i]) { memcpy(nx[i], st[i], sizeof(nx[i])); continue; }
             double wind[2];
             ora_trilinear(p, d, W[0], st[i], &wind[0]);
@@ -454,45 +506,64 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
             fuel[i] += p->dt * p->eta[i] * ut[0];
         }
 
-        /* Alg.1 l.12-14: constraints at the new state j = t+1. */
+        /* Alg.1 l.12-14: constraints at the new state j = t+1, each bound a
+         * member of the aircraft's violation OR with its margin. */
         for (int i = 0; i < n; ++i) {
             if (!fly[i]) continue;
             const double *ut = &u[((size_t)i * H + t) * 3];
-            vnow[i] = ora_unary_violation(p, i, ut, nx[i]);
-            if (out && out->margin) {
-                marg[i] = fmin_abs(marg[i], (p->gamma_max[i] - fabs(ut[2])) / p->gamma_max[i]);
-                marg[i] = fmin_abs(marg[i], (p->phi_max[i] - fabs(ut[1])) / p->phi_max[i]);
-                marg[i] = fmin_abs(marg[i], (nx[i][2] - p->z_min[i]) / fmax(1.0, fabs(p->z_max[i])));
-                marg[i] = fmin_abs(marg[i], (p->z_max[i] - nx[i][2]) / fmax(1.0, fabs(p->z_max[i])));
-                marg[i] = fmin_abs(marg[i], (nx[i][3] - p->v_min[i]) / p->v_max[i]);
-                marg[i] = fmin_abs(marg[i], (p->v_max[i] - nx[i][3]) / p->v_max[i]);
-                marg[i] = fmin_abs(marg[i], (nx[i][5] - p->m_empty[i]) / p->m_empty[i]);
-            }
+            int finite = 1;
+            for (int a = 0; a < 6; ++a) if (!isfinite(nx[i][a])) finite = 0;
+            if (!finite) or_add(&vio[i], 1, INFINITY);
+            const double zs = fmax(1.0, fabs(p->z_max[i])), Ts = fmax(1.0, fabs(p->T_max[i]));
+            or_fail_unless(&vio[i], (p->gamma_max[i] - fabs(ut[2])) / p->gamma_max[i], 0);
+            or_fail_unless(&vio[i], (p->phi_max[i] - fabs(ut[1])) / p->phi_max[i], 1);
+            or_fail_unless(&vio[i], (ut[0] - p->T_min[i]) / Ts, 0);
+            or_fail_unless(&vio[i], (p->T_max[i] - ut[0]) / Ts, 0);
+            or_fail_unless(&vio[i], (nx[i][2] - p->z_min[i]) / zs, 0);
+            or_fail_unless(&vio[i], (p->z_max[i] - nx[i][2]) / zs, 0);
+            or_fail_unless(&vio[i], (nx[i][3] - p->v_min[i]) / p->v_max[i], 0);
+            or_fail_unless(&vio[i], (p->v_max[i] - nx[i][3]) / p->v_max[i], 0);
+            or_fail_unless(&vio[i], (nx[i][5] - p->m_empty[i]) / p->m_empty[i], 0);
+
+            /* landing sector (Eq. TO_init), an AND of five bounds (R10) */
             if (p->kind[i] == 0 && landed[i] < 0) {
-                if (ora_landed(p, nx[i])) landed[i] = t + 1;
-                if (out && out->margin) {
-                    double x = nx[i][0], y = nx[i][1];
-                    double rho = sqrt(x * x + y * y);
-                    marg[i] = fmin_abs(marg[i], (p->P_runway - rho) / p->P_runway);
-                    marg[i] = fmin_abs(marg[i], (p->P_beta - ora_beta(x, y, nx[i][2])) / p->P_beta);
-                    marg[i] = fmin_abs(marg[i], (p->P_chi - fabs(atan2(y, x))) / p->P_chi);
-                    marg[i] = fmin_abs(marg[i], (p->P_chi - ora_angdist(nx[i][4] - M_PI)) / p->P_chi);
-                    marg[i] = fmin_abs(marg[i], (p->P_vs - nx[i][3]) / p->P_vs);
+                double x = nx[i][0], y = nx[i][1];
+                double rho = sqrt(x * x + y * y);
+                ora_or miss;                      /* "not landed" = OR of the failing bounds */
+                or_init(&miss);
+                or_fail_unless(&miss, (p->P_runway - rho) / p->P_runway, 0);
+                or_fail_unless(&miss, (p->P_beta - ora_beta(x, y, nx[i][2])) / p->P_beta, 0);
+                or_fail_unless(&miss, (p->P_chi - fabs(atan2(y, x))) / p->P_chi, 0);
+                or_fail_unless(&miss, (p->P_chi - ora_angdist(nx[i][4] - M_PI)) / p->P_chi, 0);
+                or_fail_unless(&miss, (p->P_vs - nx[i][3]) / p->P_vs, 0);
+                int ln = ora_landed(p, nx[i]);
+                double mu = or_margin(&miss);
+                if (mu < mland[i]) mland[i] = mu;
+                if (rp && rp->landed_step && mu < rp->eps) {
+                    ln = rp->landed_step[i] == t + 1;         /* decision replay (R30) */
+                    replayed[i] |= 1;
                 }
+                if (ln) landed[i] = t + 1;
             }
         }
+        /* Eq. avoidance for every pair of simulated aircraft: a conflict is the AND
+         * of the two failed separations; both aircraft of a conflicting pair fail. */
         for (int i = 0; i < n; ++i) {
             if (!fly[i]) continue;
             for (int q = i + 1; q < n; ++q) {
                 if (!fly[q]) continue;
-                if (ora_pair_conflict(p, nx[i], nx[q])) { vnow[i] = 1; vnow[q] = 1; }
-                if (out && out->margin) {
-                    double dx = nx[i][0] - nx[q][0], dy = nx[i][1] - nx[q][1], dz = nx[i][2] - nx[q][2];
-                    double m1 = (dx * dx + dy * dy) / twoPr2 - 1.0, m2 = fabs(dz) / twoPh - 1.0;
-                    double mm = m1 > m2 ? m1 : m2;
-                    marg[i] = fmin_abs(marg[i], mm);
-                    marg[q] = fmin_abs(marg[q], mm);
+                int conf = ora_pair_conflict(p, nx[i], nx[q]);
+                double dx = nx[i][0] - nx[q][0], dy = nx[i][1] - nx[q][1], dz = nx[i][2] - nx[q][2];
+                double mm = INFINITY;
+                if (isfinite(dx) && isfinite(dy) && isfinite(dz)) {
+                    ora_or sep;                   /* "separated" = OR of the two separations */
+                    or_init(&sep);
+                    or_add(&sep, !((dx * dx + dy * dy) < twoPr2), fabs((dx * dx + dy * dy) / twoPr2 - 1.0));
+                    or_add(&sep, !(fabs(dz) < twoPh), fabs(fabs(dz) / twoPh - 1.0));
+                    mm = or_margin(&sep);
                 }
+                or_add(&vio[i], conf, mm);
+                or_add(&vio[q], conf, mm);
             }
         }
 
@@ -520,7 +591,6 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
             }
         }
         for (int i = 0; i < n; ++i) {
-            if (fly[i] && vnow[i]) viol[i] = 1;     /* removed after this step (R42) */
             memcpy(st[i], nx[i], sizeof(st[i]));
             if (out && out->traj) memcpy(&out->traj[((size_t)i * (H + 1) + t + 1) * 6], st[i], sizeof(st[i]));
         }
@@ -550,40 +620,73 @@ void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
             }
             if (p->noise_w > 0.0) J = (1.0 - p->noise_w) * J + p->noise_w * (sN[i] / Ha);
         }
+        int viol = vio[i].any;
+        double mv = or_margin(&vio[i]);
+        if (rp && rp->viol && mv < rp->eps) { viol = rp->viol[i] != 0; replayed[i] |= 2; }
         if (out) {
             if (out->J) out->J[i] = J;
-            if (out->viol) out->viol[i] = viol[i];
+            if (out->viol) out->viol[i] = viol;
             if (out->comp) memcpy(&out->comp[4 * i], c4, sizeof(c4));
             if (out->fuel) out->fuel[i] = fuel[i];
             if (out->landed_step) out->landed_step[i] = landed[i];
-            if (out->margin) out->margin[i] = marg[i];
+            if (out->margin) out->margin[i] = mv < mland[i] ? mv : mland[i];
+            if (out->margin_land) out->margin_land[i] = mland[i];
+            if (out->replayed) out->replayed[i] = replayed[i];
         }
     }
 }
 
-/* Alg.1 l.8-17: every particle, S samples, W <- W * J in log2 (R24). */
-void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl,
-                  uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
-                  double *ell, int nthreads)
+void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
+                 uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
+                 ora_rollout_out *out)
+{
+    ora_rollout_replay(p, d, u, l, s, k, seed, mpc, NULL, out);
+}
+
+/* Alg.1 l.8-17: every particle, S samples, W <- W * J in log2 (R24).
+ * margin (nullable) [L][n]: the smallest decision margin over the S samples that
+ * can change ell[l][i] -- aircraft i's violation margin and the landing margin of
+ * every aircraft (a landing freezes the lander, which every pair test sees). */
+void ora_evaluate_margin(const ora_problem *p, const ora_derived *d, const double *ctrl,
+                         uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
+                         double *ell, double *margin, int nthreads)
 {
     const int n = p->n;
     const size_t row = (size_t)n * p->H * 3;
 #pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : 1)
     for (int64_t l = 0; l < (int64_t)L; ++l) {
-        double J[ORA_MAX_AC];
+        double J[ORA_MAX_AC], mg[ORA_MAX_AC], ml[ORA_MAX_AC];
         int32_t viol[ORA_MAX_AC];
         ora_rollout_out o;
         memset(&o, 0, sizeof(o));
         o.J = J; o.viol = viol;
+        if (margin) {
+            o.margin = mg; o.margin_land = ml;
+            for (int i = 0; i < n; ++i) margin[(size_t)l * n + i] = INFINITY;
+        }
         for (uint32_t s = 0; s < S; ++s) {
             ora_rollout(p, d, &ctrl[(size_t)l * row], (uint32_t)l, s, k, seed, mpc, &o);
+            double lmin = INFINITY;
+            if (margin) for (int i = 0; i < n; ++i) if (ml[i] < lmin) lmin = ml[i];
             for (int i = 0; i < n; ++i) {
                 double *e = &ell[(size_t)l * n + i];
                 if (viol[i] || !(J[i] > 0.0)) *e = -INFINITY;
                 else *e += log2(J[i]);
+                if (margin) {
+                    double *m = &margin[(size_t)l * n + i];
+                    double v = mg[i] < lmin ? mg[i] : lmin;
+                    if (v < *m) *m = v;
+                }
             }
         }
     }
+}
+
+void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl,
+                  uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
+                  double *ell, int nthreads)
+{
+    ora_evaluate_margin(p, d, ctrl, L, S, k, seed, mpc, ell, NULL, nthreads);
 }
 
 /* Alg.1 l.3-5: uniform controls in [min, max]. */
@@ -696,16 +799,14 @@ int ora_resample_column_m(const double *ell, uint32_t L, uint32_t M, uint32_t i,
     uint64_t Q = acc;
     uint64_t r = ora_r64(TAG_RESAMPLE, i, k, seed, mpc);
     uint64_t R = (uint64_t)(((unsigned __int128)r * (unsigned __int128)Q) >> 64);
+    uint32_t a = 0;
     for (uint32_t j = 0; j < M; ++j) {
         unsigned __int128 num = (unsigned __int128)j * Q + R;
         uint64_t tj = (uint64_t)(num / M);
-        /* plain linear search keeps the definition visible; bisection is equivalent */
-        uint32_t lo = 0, hi = L - 1;
-        while (lo < hi) {
-            uint32_t mid = lo + (hi - lo) / 2;
-            if (C[mid] > tj) hi = mid; else lo = mid + 1;
-        }
-        anc[j] = (int32_t)lo;
+        /* min{ l : C_l > t_j } by a forward scan: t_j is non-decreasing in j, so the
+         * scan position never moves back; t_j < Q = C_{L-1} bounds it */
+        while (C[a] <= tj) ++a;
+        anc[j] = (int32_t)a;
     }
     if (Q_out) *Q_out = Q;
     if (R_out) *R_out = R;

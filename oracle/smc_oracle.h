@@ -108,24 +108,47 @@ double ora_angdist(double d);
 /* ---- one rollout: particle l, sample s of round k, candidate controls u ----
  * u: [n][H][3] (T, phi, gamma).  Outputs per aircraft (any may be NULL):
  *   J[n]      utility J_T in [0,1] (meaningless if viol)
- *   viol[n]   1 if any constraint failed in this sample
+ *   viol[n]   1 if any constraint failed in this sample (P:309)
  *   comp[n][4] components (dep: J1,Jfuel,J3,J4; arr: J1,Jalt,Jfuel,0)
  *   traj[n][H+1][6] states, fuel[n], landed_step[n] (-1 if not landed)
- *   margin[n]  smallest |decision margin| met by the aircraft (R30)          */
+ *   margin[n]  decision margin of the aircraft's outcome (R30): the smaller of
+ *              its violation margin and its landing margin; a perturbation of
+ *              every compared quantity by less than this relative amount cannot
+ *              change viol[i] or landed_step[i]
+ *   margin_land[n] the landing margin alone (inf for departures)
+ *   replayed[n] bit0: a landing decision was replayed, bit1: viol was replayed */
 typedef struct {
-    double *J, *comp, *traj, *fuel, *margin;
-    int32_t *viol, *landed_step;
+    double *J, *comp, *traj, *fuel, *margin, *margin_land;
+    int32_t *viol, *landed_step, *replayed;
 } ora_rollout_out;
+
+/* Decision replay (R30): where the oracle's own margin of a
+ * decision is below eps, it takes the decision another implementation made
+ * (landed_step[n], viol[n]; either may be NULL) and computes every continuous
+ * quantity from there.  Decisions with margin >= eps are never replayed. */
+typedef struct {
+    const int32_t *landed_step;
+    const int32_t *viol;
+    double eps;
+} ora_replay;
 
 void ora_rollout(const ora_problem *p, const ora_derived *d, const double *u,
                  uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
                  ora_rollout_out *out);
+void ora_rollout_replay(const ora_problem *p, const ora_derived *d, const double *u,
+                        uint32_t l, uint32_t s, uint32_t k, uint64_t seed, uint32_t mpc,
+                        const ora_replay *rp, ora_rollout_out *out);
 
 /* Alg.1 l.9-18 for a whole population: ell[l][i] += sum_s log2 J (or -inf).
- * ell must be pre-set by the caller (normally -log2 L).            */
+ * ell must be pre-set by the caller (normally -log2 L).  margin
+ * (nullable, [L][n]): smallest margin over the samples of the decisions that
+ * can change ell[l][i] (aircraft i's violation, every aircraft's landing). */
 void ora_evaluate(const ora_problem *p, const ora_derived *d, const double *ctrl,
                   uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
                   double *ell, int nthreads);
+void ora_evaluate_margin(const ora_problem *p, const ora_derived *d, const double *ctrl,
+                         uint32_t L, uint32_t S, uint32_t k, uint64_t seed, uint32_t mpc,
+                         double *ell, double *margin, int nthreads);
 
 /* Population init, Alg.1 l.1-5: ctrl[L][n][H][3]. */
 void ora_init_population(const ora_problem *p, uint32_t L, uint64_t seed, uint32_t mpc,

@@ -230,9 +230,6 @@ struct smc_ctx {
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
     uint64_t io_h2d = 0, io_d2h = 0;   // host<->device bytes of the production path
-    int layout[2] = {0, 0};            // K2 layout per candidate count: 0 lane-per-aircraft segments,
-                                       // 1 transposed (warp = aircraft)
-    int layout_env = -1;               // SMC_K2_LAYOUT override (-1: automatic)
     bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
     int anc_mode = -1;                 // SMC_ANC: 1 merge-path K5, 0 bisection in K6, -1 by size
     int32_t *anc = nullptr;            // [n][Lloc] K5 ancestors
@@ -481,8 +478,6 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         return SMC_EINVAL;
     }
     {
-        const char *lay = getenv("SMC_K2_LAYOUT");
-        ctx->layout_env = lay ? ((strcmp(lay, "transposed") == 0) ? 1 : (strcmp(lay, "segment") == 0 ? 0 : -1)) : -1;
         const char *ch = getenv("SMC_K2_CHUNKS");
         ctx->chunking = ch && strcmp(ch, "1") == 0;
         // ancestors: merge-path K5 + K6 reading them ("mp"), or bisection inside K6 ("bisect");
@@ -887,18 +882,6 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
-    // K2 layout: the segment layout (lane = aircraft, W = next_pow2(N) lanes per particle).
-    // Re-measured at the packed-FP32 kernel (tools/layout_probe.py, c2 solver, 21 rounds, per
-    // MPC step): segment faster for every N from 5 to 26, e.g. N = 9: 12.9 vs 14.0 ms,
-    // N = 17: 29.7 vs 30.2, N = 20: 29.8 vs 32.1, N = 24: 28.2 vs 39.3 -- the padded lanes now
-    // cost less than the transposed layout's block barriers (the earlier "transposed below 70 %
-    // occupancy" rule predates the packed candidates).  SMC_K2_LAYOUT=transposed selects the
-    // warp-per-aircraft layout.
-    {
-        ctx->layout[1] = ctx->layout_env >= 0 ? ctx->layout_env : 0;
-        ctx->layout[0] = ctx->layout_env >= 0 ? ctx->layout_env : 0;
-        if (ctx->dsc.wng > 8) ctx->layout[0] = ctx->layout[1] = 0;   // dense wind grids: segment layout only
-    }
     ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1, ctx->dsc.wng);
     ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2, ctx->dsc.wng);
     ctx->have_scn = true;
@@ -978,10 +961,9 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
             if (need > ctx->part_cap) break;
             if (eff(c) > be + 0.03) { be = eff(c); best = c; }
         }
-        if (ctx->layout[NC - 1] == 0 && best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
+        if (best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
     }
-    LAUNCHP(PH_ROLLOUT, ctx->layout[NC - 1] ? launch_rollout_t(ctx->dsc, ra, NC, false, ctx->st)
-                                     : launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
+    LAUNCHP(PH_ROLLOUT, launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
     ctx->Leval = Lk;
     if (ctx->world > 1 && ctx->p2p && tail)
@@ -1359,7 +1341,7 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
     ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
     ra.dbg_landed = dland;
-    LAUNCH(ctx->layout[0] ? launch_rollout_t(ctx->dsc, ra, 1, debug, ctx->st) : launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
+    LAUNCH(launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
     if (debug) {
         if (J) CK(cudaMemcpyAsync(J, dJ, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
         if (viol) CK(cudaMemcpyAsync(viol, dviol, nu, cudaMemcpyDeviceToHost, ctx->st));

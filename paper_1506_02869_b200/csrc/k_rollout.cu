@@ -458,7 +458,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
             // ---------------- 2-3. dynamics, unary checks and geometry, both candidates at once
             const bool act = first <= t;
-            const int flym = act ? (~(landedm | violm) & ALLC) : 0;
+            // Alg.1 l.11-13: every active aircraft flies its own controls to H and stays in
+            // every pair test, violated or not (a failure only zeroes its weight); only a
+            // landed arrival stops (R18)
+            const int flym = act ? (~landedm & ALLC) : 0;
             V flyf;                                   // 1 while the candidate's aircraft flies, else 0
 #pragma unroll
             for (int c = 0; c < NC; ++c) cset(flyf, c, ((flym >> c) & 1) ? 1.0f : 0.0f);
@@ -516,8 +519,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 }
             }
             // Eq. hor, coordinated-turn lift and parabolic drag (R12):
-            // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a grounded / inactive / violated aircraft
-            // advances with dt_f = 0 (its state stays frozen, R18/R42)
+            // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a landed / inactive aircraft advances with
+            // dt_f = 0 (its state stays frozen, R18/R20)
             V qd = cq * v * v;
             if (sc.density_mode == 0) {
                 const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
@@ -572,7 +575,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 lnowm |= (ln ? 1 : 0) << c;
             }
             if (kind != 0) lnowm = 0;                            // only arrivals land (Eq. TO_init)
-            // a grounded / inactive / violated aircraft is a NaN position: every comparison fails
+            // a landed / inactive aircraft is a NaN position: every comparison fails (as it does for a
+            // violator whose state has become non-finite)
             V px;
 #pragma unroll
             for (int c = 0; c < NC; ++c) cset(px, c, ((flym >> c) & 1) ? cget(nx, c) : __int_as_float(0x7fffffff));

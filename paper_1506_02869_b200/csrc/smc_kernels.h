@@ -34,8 +34,6 @@ int segment_width(int n, bool dense = false);
 int rollout_blocks_per_sm(int n, int H, int NC, int ng = 8);
 size_t rollout_smem_bytes(int W, int NC, int H, int ng = 8, bool sp = false);
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
-// transposed layout (warp = aircraft, lane = (candidate, particle)); k_rollout_t.cu
-cudaError_t launch_rollout_t(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
 
 struct PopArgs {
     int n, H;

@@ -1,11 +1,21 @@
 """GPU (libsmcatm, sm_100a) vs FP64 oracle parity, through the C ABI.
 
-Tolerances: rollout quantities |gpu - ora| <= 1e-4 |ora|
-+ atol (positions 0.1 m, speed 1e-3 m/s, heading 1e-4 rad, mass/fuel 1e-2 kg,
-utilities 1e-4); log2 weights 1e-4 (|ell| + S); MH decisions, ancestors,
-integer totals, selection: bit-exact.  A rollout whose oracle decision
-margins (R30) come within 1e-4 of a threshold is excluded from the strict
-comparison (FP32 vs FP64 may take either side) and counted: it must stay rare.
+Tolerances (SURVEY 8(c) parity metric): rollout
+quantities |gpu - ora| <= 1e-4 |ora| + atol (positions 0.1 m, speed 1e-3 m/s,
+heading 1e-4 rad, mass/fuel 1e-2 kg, utilities 1e-4); log2 weights, element
+by element, |d ell| <= 1e-4 (|ell| + S); MH decisions, ancestors, integer
+totals, selection: bit-exact.
+
+Discrete decisions (violation, landing) are compared exactly.  The oracle
+reports a conjunction-aware margin for each (R30); where it is below
+EPS = 1e-5 FP32 and FP64 may legitimately take either side, so:
+  * rollouts dumped by the debug hook are re-run by the oracle in decision-
+    replay mode (it takes the GPU's decision only for those events) and every
+    continuous quantity is then compared;
+  * production launches (weights only) exclude the (particle, aircraft)
+    entries whose margin is below EPS.
+Replayed decisions and excluded entries are counted (parity_log, printed in
+the pytest summary) and must stay below 1e-3 of the units compared.
 """
 import math
 
@@ -13,11 +23,13 @@ import numpy as np
 import pytest
 
 import oracle as O
+import parity_log
 from paper_1506_02869_b200 import scenarios as sc
 
 pytestmark = pytest.mark.gpu
 
-MARGIN = 1e-4
+EPS = 1e-5
+RATE = 1e-3            # bound on replayed / excluded units
 
 
 @pytest.fixture(scope="module")
@@ -35,33 +47,73 @@ def _solver(smc, scn, L=64, S=4, K=3, seed=0x5EED0001, **kw):
     return smc.Solver(scn, L=L, S=S, K=K, sigma=sig, seed=seed, **kw)
 
 
-def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, max_ambiguous=0.05):
+def _in_domain(traj):
+    """[n][H+1] mask: steps up to which the oracle state stays where FP32 and FP64
+    evaluate Eq. hor alike (finite, airspeed above 20 m/s -- the turn rate g tan(phi)/v
+    and the induced drag blow up as v -> 0, P:250-255 -- and inside 1000 km)."""
+    v = traj[..., 3]
+    ok = np.isfinite(traj).all(-1) & (v > 20.0) & (np.abs(traj[..., :3]) < 1e6).all(-1)
+    return np.logical_and.accumulate(ok, axis=1)
+
+
+def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, name=None):
+    """Per-(particle, sample, aircraft) states, fuel, utilities and decisions of the
+    debug rollout vs the oracle run in decision-replay mode (R30)."""
     sol = _solver(smc, scn, L=max(L, 1), S=S, seed=seed)
     P = O.Problem(scn)
     g = sol.debug_rollout(ctrl, S, k, l0=l0, traj=True)
-    n, H = scn["n"], scn["H"]
-    amb = 0
-    checked = 0
+    n = scn["n"]
+    replayed = units = 0
+    tol = np.array([0.1, 0.1, 0.1, 1e-3, 1e-4, 1e-2])
     for l in range(L):
         for s in range(S):
-            r = P.rollout(ctrl[l].astype(np.float64), l0 + l, s, k, seed)
-            if np.min(r["margin"]) < MARGIN:
-                amb += 1
-                continue
-            checked += 1
-            assert np.array_equal(g["viol"][l, s].astype(bool), r["viol"].astype(bool)), (l, s)
+            r = P.rollout(ctrl[l].astype(np.float64), l0 + l, s, k, seed,
+                          replay=(g["landed"][l, s], g["viol"][l, s].astype(np.int32), EPS))
+            units += n
+            replayed += int(np.count_nonzero(r["replayed"]))
+            assert np.array_equal(g["viol"][l, s].astype(bool), r["viol"].astype(bool)), (l, s, r["margin"])
             assert np.array_equal(g["landed"][l, s], r["landed_step"]), (l, s)
             tg, to = g["traj"][l, s].astype(np.float64), r["traj"]
-            tol = np.array([0.1, 0.1, 0.1, 1e-3, 1e-4, 1e-2])
+            dom = _in_domain(to)
             err = np.abs(tg - to) - (1e-4 * np.abs(to) + tol)
+            err[~dom] = -1.0
             assert np.all(err <= 0), (l, s, np.unravel_index(np.argmax(err), err.shape), tg, to)
-            assert np.allclose(g["fuel"][l, s], r["fuel"], rtol=1e-4, atol=1e-2), (l, s)
-            assert np.allclose(g["J"][l, s], r["J"], rtol=0, atol=1e-4), (l, s, g["J"][l, s], r["J"])
-            assert np.allclose(g["comp"][l, s], r["comp"], rtol=0, atol=1e-4), (l, s)
-    assert checked > 0
-    assert amb <= max_ambiguous * L * S, (amb, L * S)
+            full = dom.all(1)                      # aircraft whose whole rollout stayed in the domain
+            assert np.allclose(g["fuel"][l, s][full], r["fuel"][full], rtol=1e-4, atol=1e-2), (l, s)
+            assert np.allclose(g["J"][l, s][full], r["J"][full], rtol=0, atol=1e-4), (l, s, g["J"][l, s], r["J"])
+            assert np.allclose(g["comp"][l, s][full], r["comp"][full], rtol=0, atol=1e-4), (l, s)
+    parity_log.record(name or f"rollout n={n}", units, replayed=replayed)
+    assert replayed <= RATE * units, (replayed, units)
     sol.close()
-    return checked, amb
+    return units, replayed
+
+
+def _check_ell(ell_g, ell_o, margin, S, name, lam_g=None):
+    """Element-by-element log2 weights: finiteness exact and |d ell| <= 1e-4 (|ell| + S)
+    wherever the oracle's decision margin is at least EPS; the rest is excluded and
+    counted.  lam_g (optional): the GPU's lambda per particle, checked against the
+    oracle's sum over aircraft where no entry of the particle is excluded."""
+    ell_g = np.asarray(ell_g, np.float64)
+    amb = margin < EPS
+    ok = ~amb
+    fin_g, fin_o = np.isfinite(ell_g), np.isfinite(ell_o)
+    bad = ok & (fin_g != fin_o)
+    assert not bad.any(), (name, np.argwhere(bad)[:5], ell_g[bad][:5], ell_o[bad][:5], margin[bad][:5])
+    both = ok & fin_g & fin_o
+    err = np.abs(ell_g - ell_o) - 1e-4 * (np.abs(ell_o) + S)
+    err[~both] = -1.0
+    assert np.all(err <= 0), (name, np.unravel_index(np.argmax(err), err.shape), err.max())
+    if lam_g is not None:
+        rows = ~amb.any(1)
+        lam_o = np.where(fin_o.all(1), np.where(fin_o, ell_o, 0.0).sum(1), -np.inf)
+        lg = np.asarray(lam_g)[rows]
+        lo = lam_o[rows]
+        assert np.array_equal(np.isfinite(lg), np.isfinite(lo)), name
+        f = np.isfinite(lo)
+        n = ell_o.shape[1]
+        assert np.all(np.abs(lg[f] - lo[f]) <= 1e-4 * (np.abs(lo[f]) + n * S)), name
+    parity_log.record(name, ell_o.size, excluded=int(amb.sum()))
+    assert amb.sum() <= RATE * ell_o.size + 0, (name, int(amb.sum()), ell_o.size)
 
 
 def _near_trim_controls(scn, L, seed):
@@ -75,46 +127,67 @@ def _near_trim_controls(scn, L, seed):
     return c
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "n3_partial", "n12_noise", "n24", "n1", "dense332_n3",
-                                  "dense444_c2", "dense442_n1", "dense_n20"])
-def test_rollout_parity(smc, case):
+def _ring_scenario(n):
+    """All-active snapshot of n aircraft (half arrivals): every separation-ring
+    instance R in {6, 10, 12, 14, 20, 24, 28} of K2 is reached by some n."""
+    scn = sc.snapshot((n + 1) // 2, n // 2, seed=40 + n)
+    scn["nominal"] = [5.0, -3.0]
+    scn["turb_sigma"] = 1.0
+    return scn
+
+
+ROLLOUT_CASES = ["c1", "c2", "n3_partial", "n12_noise", "n24", "n1", "n6", "n14", "n20", "n28", "dense332_n3",
+                 "dense444_c2", "dense442_n1", "dense_n20"]
+
+
+def _rollout_case(case):
     if case == "c1":
         scn, cfg = sc.config(1)
-        L, S, seed = 40, 4, cfg.seed
-    elif case == "c2":
+        return scn, 400, 4, cfg.seed
+    if case == "c2":
         scn, cfg = sc.config(2)
-        L, S, seed = 70, 3, cfg.seed
-    elif case == "n3_partial":
+        return scn, 300, 4, cfg.seed
+    if case == "n3_partial":
         scn = sc.small(2, 1, H=7, seed=5)
         scn["first_step"] = np.array([0, 3, 7], np.int32)
-        L, S, seed = 90, 3, 99
-    elif case == "n12_noise":
+        return scn, 400, 3, 99
+    if case == "n12_noise":
         scn, cfg = sc.config(4, noise_w=0.2)
-        L, S, seed = 40, 2, cfg.seed
-    elif case == "n24":
+        return scn, 200, 2, cfg.seed
+    if case == "n24":
         scn, cfg = sc.config(3)
-        L, S, seed = 12, 2, cfg.seed
-    elif case == "dense332_n3":            # denser wind grids (N3): 18 points, W = 4
+        return scn, 60, 2, cfg.seed
+    if case in ("n6", "n14", "n28"):
+        n = int(case[1:])
+        return _ring_scenario(n), max(40, 1200 // n), 2, 0x5EED0100 + n
+    if case == "n20":                       # the 20-aircraft latency config (--config 7, R = 20)
+        scn, cfg = sc.config(7)
+        return scn, 60, 2, cfg.seed
+    if case == "dense332_n3":               # denser wind grids (N3, P:454): 18 points, W = 4
         scn = sc.small(2, 1, H=7, seed=5)
         scn.update(wind_n=(3, 3, 2), sigma_lo=3.0, sigma_hi=6.0)
-        L, S, seed = 90, 3, 99
-    elif case == "dense444_c2":            # 64 points, W = 8
+        return scn, 300, 3, 99
+    if case == "dense444_c2":               # 64 points, W = 8
         scn, cfg = sc.config(2)
         scn.update(wind_n=(4, 4, 4), sigma_lo=3.0, sigma_hi=6.0)
-        L, S, seed = 70, 3, cfg.seed
-    elif case == "dense442_n1":            # one aircraft: segment padded to W = 4
+        return scn, 150, 3, cfg.seed
+    if case == "dense442_n1":               # one aircraft: segment padded to W = 4
         scn = sc.small(1, 0, H=6, seed=3)
         scn.update(wind_n=(4, 4, 2), sigma_lo=3.0, sigma_hi=6.0)
-        L, S, seed = 200, 2, 5
-    elif case == "dense_n20":              # 5x3x2 grid, 20 aircraft (W = 32)
+        return scn, 1000, 2, 5
+    if case == "dense_n20":                 # 5x3x2 grid, 20 aircraft (W = 32)
         scn = sc.snapshot(12, 8, seed=21)
         scn.update(wind_n=(5, 3, 2), sigma_lo=3.0, sigma_hi=6.0)
-        L, S, seed = 16, 2, 31
-    else:
-        scn = sc.small(1, 0, H=6, seed=3)
-        L, S, seed = 200, 2, 5
+        return scn, 60, 2, 31
+    scn = sc.small(1, 0, H=6, seed=3)       # n1
+    return scn, 1000, 2, 5
+
+
+@pytest.mark.parametrize("case", ROLLOUT_CASES)
+def test_rollout_parity(smc, case):
+    scn, L, S, seed = _rollout_case(case)
     ctrl = _near_trim_controls(scn, L, seed=11)
-    _compare_rollouts(smc, scn, L, S, k=2, seed=seed, ctrl=ctrl, l0=1000)
+    _compare_rollouts(smc, scn, L, S, k=2, seed=seed, ctrl=ctrl, l0=1000, name=f"rollout {case}")
 
 
 def test_rollout_landing_exercised(smc):
@@ -126,7 +199,7 @@ def test_rollout_landing_exercised(smc):
     scn["x0"][1] = [-20000.0, -20000.0, 5000.0, 140.0, -2.3, 70000.0]
     P = O.Problem(scn)
     rng = np.random.default_rng(1)
-    L = 64
+    L = 256
     ctrl = np.zeros((L, 2, 8, 3), np.float32)
     for l in range(L):
         st = scn["x0"][0].copy()
@@ -138,42 +211,128 @@ def test_rollout_landing_exercised(smc):
     ctrl[:, 1, :, 0] = 50000.0
     landed_o = sum(P.rollout(ctrl[l].astype(np.float64), l, 0, 0, 7)["landed_step"][0] > 0 for l in range(L))
     assert landed_o > L // 4
-    _compare_rollouts(smc, scn, L, 2, k=0, seed=7, ctrl=ctrl)
+    _compare_rollouts(smc, scn, L, 4, k=0, seed=7, ctrl=ctrl, name="rollout landing")
+
+
+def test_violator_keeps_flying_on_gpu(smc):
+    """Alg.1 l.11-13 / Eq. avoidance on the GPU: an aircraft
+    that breaks its envelope at step 0 keeps flying and, at step 2, conflicts with a
+    neighbour that broke nothing -- both are zeroed, as in the oracle's pin
+    (test_oracle_conventions.test_violator_keeps_flying_and_zeroes_a_later_neighbour)."""
+    scn = sc.snapshot(0, 2, seed=1)
+    scn.update(sigma_lo=0.0, sigma_hi=0.0, nominal=[0.0, 0.0], turb_sigma=0.0)
+    scn["x0"][0] = [-8000.0, 0.0, 3000.0, 100.0, 0.0, 73500.0]
+    scn["x0"][1] = [0.0, 0.0, 3000.0, 100.0, math.pi, 73500.0]
+    P = O.Problem(scn)
+    u = np.zeros((1, 2, scn["H"], 3), np.float32)
+    for i in range(2):
+        st = scn["x0"][i].copy()
+        for t in range(scn["H"]):
+            _, D = P.lift_drag(i, st, 0.0)
+            u[0, i, t] = [D, 0.0, 0.0]
+            st = P.step(i, st, u[0, i, t].astype(np.float64))
+    u[0, 1, 0, 0] = 1.5 * scn["T_max"][1]
+    sol = _solver(smc, scn, L=1, S=1, seed=3)
+    g = sol.debug_rollout(u, 1, 0, traj=True)
+    r = P.rollout(u[0].astype(np.float64), 0, 0, 0, 3)
+    assert g["viol"][0, 0].tolist() == [1, 1] and r["viol"].tolist() == [1, 1]
+    assert np.allclose(g["traj"][0, 0], r["traj"], rtol=1e-5, atol=0.1)
+    assert g["traj"][0, 0, 1, -1, 0] < g["traj"][0, 0, 1, 1, 0] - 4000.0       # the violator kept flying West
+    sol.close()
 
 
 @pytest.mark.parametrize("case,sp", [("c2", "1"), ("c2", "0"), ("table1", "1"), ("n24", "1"), ("n12_noise", "1"),
-                                     ("n24", "0")])
+                                     ("n24", "0"), ("n6", "1"), ("n14", "1"), ("n20", "1"), ("n28", "1"),
+                                     ("n28", "0")])
 def test_evaluate_parity(smc, case, sp, monkeypatch):
-    """Single-candidate evaluation (round 0 / paper mode) against the oracle: sample pairs in
-    the float2 slots (SMC_K2_SP, default) or one sample per lane, S odd (last pair half
-    used), and the exact-count separation rings (n = 10, 12, 24)."""
+    """Single-candidate evaluation (round 0 / paper mode) in the production K2 instances
+    against the oracle, element by element: sample pairs in the float2 slots
+    (SMC_K2_SP, default) or one sample per lane, S odd (last pair half used), and every
+    separation-ring instance (n = 6, 10, 12, 14, 20, 24, 28)."""
     monkeypatch.setenv("SMC_K2_SP", sp)
     if case == "table1":
         scn, cfg = sc.config(6)
+        seed = cfg.seed
     elif case == "n24":
         scn, cfg = sc.config(3)
+        seed = cfg.seed
     elif case == "n12_noise":
         scn, cfg = sc.config(4, noise_w=0.2)
+        seed = cfg.seed
+    elif case == "n20":
+        scn, cfg = sc.config(7)
+        seed = cfg.seed
+    elif case in ("n6", "n14", "n28"):
+        scn = _ring_scenario(int(case[1:]))
+        seed = 0x5EED0200 + int(case[1:])
     else:
         scn, cfg = sc.config(2)
-    L, S = (96, 5) if scn["n"] <= 12 else (24, 3)
+        seed = cfg.seed
+    n = scn["n"]
+    S = 5
+    L = max(64, 12000 // (n * S))
     ctrl = _near_trim_controls(scn, L, seed=3)
-    sol = _solver(smc, scn, L=L, S=S, seed=cfg.seed)
+    sol = _solver(smc, scn, L=L, S=S, seed=seed)
     ell_g = sol.debug_evaluate(ctrl, S, 4).astype(np.float64)
+    ell_o, mg = O.Problem(scn).evaluate(ctrl.astype(np.float64), S, 4, seed, margin=True)
+    _check_ell(ell_g, ell_o, mg, S, f"evaluate {case} sp={sp}")
+    sol.close()
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "n6", "n12_noise", "n14", "n16", "n20", "n24", "n28"])
+def test_production_rounds_parity(smc, case):
+    """Real SMC rounds through smc_iterate -- round 0 (single candidate, sample pairs)
+    and rounds 1-2 (both MH candidates, packed FP32) -- on every separation-ring
+    instance: each candidate's log2 weight per (particle, aircraft) against the oracle
+    evaluating the GPU's own controls, lambda of both candidates, the survivor's weights
+    (the candidate its mask bit names) and the MH decisions replayed bit-exactly on the
+    GPU's lambdas."""
+    if case in ("n6", "n14", "n28"):
+        scn = _ring_scenario(int(case[1:]))
+        seed = 0x5EED0300 + int(case[1:])
+    elif case == "n16":
+        scn, cfg = sc.config(5)
+        seed = cfg.seed
+    elif case == "n20":
+        scn, cfg = sc.config(7)
+        seed = cfg.seed
+    elif case == "n24":
+        scn, cfg = sc.config(3)
+        seed = cfg.seed
+    elif case == "n12_noise":
+        scn, cfg = sc.config(4, noise_w=0.2)
+        seed = cfg.seed
+    else:
+        scn, cfg = sc.config(int(case[1:]))
+        seed = cfg.seed
+    n = scn["n"]
+    S = 4
+    L = max(128, 16000 // (n * S * 2))
+    sol = _solver(smc, scn, L=L, S=S, K=4, seed=seed)
     P = O.Problem(scn)
-    ell_o = P.evaluate(ctrl.astype(np.float64), S, 4, cfg.seed)
-    bad = 0
-    for l in range(L):
-        amb = any(np.min(P.rollout(ctrl[l].astype(np.float64), l, s, 4, cfg.seed)["margin"]) < MARGIN for s in range(S))
-        if amb:
-            bad += 1
+    for k in range(3):
+        sol.iterate(1)
+        pop = sol.population()
+        ell_c, mg_c = P.evaluate(pop["cur"].astype(np.float64), S, k, seed, margin=True)
+        if k == 0:
+            _check_ell(pop["ell"].T, ell_c, mg_c, S, f"rounds {case} k=0", lam_g=pop["lam"])
             continue
-        fin = np.isfinite(ell_o[l])
-        assert np.array_equal(fin, np.isfinite(ell_g[l])), l
-        assert np.allclose(ell_g[l][fin], ell_o[l][fin], rtol=0, atol=1e-4 * (np.abs(ell_o[l][fin]).max() + S)), l
-    # R30: rollouts within 1e-4 of a decision threshold are excluded and must stay rare (the
-    # 12-aircraft noise scenario has more thresholds: landing cone, envelope and noise kink)
-    assert bad < (0.1 if case == "n12_noise" else 0.05) * L
+        ell_p, mg_p = P.evaluate(pop["prop"].astype(np.float64), S, k, seed, margin=True)
+        lc_g, lp_g = pop["lam_cand"]
+        acc = np.array([O.mh_accept(lc_g[l], lp_g[l], l, k, seed) for l in range(L)])
+        assert np.array_equal(pop["surv"].astype(bool), acc), case            # MH bit-exact on the GPU's lambdas
+        sv = pop["surv"][:, None] == 1
+        ell_o = np.where(sv, ell_p, ell_c)
+        mg = np.where(sv, mg_p, mg_c)
+        # both candidates' lambdas: checked through particles with no excluded entry
+        rows_c, rows_p = ~(mg_c < EPS).any(1), ~(mg_p < EPS).any(1)
+        for lg, eo, rows in ((lc_g, ell_c, rows_c), (lp_g, ell_p, rows_p)):
+            lo = np.where(np.isfinite(eo).all(1), np.where(np.isfinite(eo), eo, 0).sum(1), -np.inf)
+            assert np.array_equal(np.isfinite(lg[rows]), np.isfinite(lo[rows])), (case, k)
+            f = rows & np.isfinite(lo)
+            assert np.all(np.abs(lg[f] - lo[f]) <= 1e-4 * (np.abs(lo[f]) + n * S)), (case, k)
+        _check_ell(pop["ell"].T, ell_o, mg, S, f"rounds {case} k={k}", lam_g=pop["lam"])
+    sol.close()
 
 
 def test_mh_bitexact(smc):
@@ -209,12 +368,11 @@ def test_mh_aircraft_bitexact(smc):
             assert mask[l] == ref, (l, k)
 
 
-@pytest.mark.parametrize("layout", ["segment", "transposed"])
-def test_per_aircraft_mh_rounds(smc, layout, monkeypatch):
+def test_per_aircraft_mh_rounds(smc):
     """mh = 2 (R46) in real rounds: every survivor row is the candidate its mask bit names,
-    its log-weight is the oracle's for that candidate, the decisions replay on the GPU's
-    candidate weights, and the final pick is the best jointly evaluated candidate."""
-    monkeypatch.setenv("SMC_K2_LAYOUT", layout)
+    its log-weight is the oracle's for that candidate (element by element), the decisions
+    replay bit-exactly on the GPU's candidate weights, and the final pick is the best
+    jointly evaluated candidate."""
     scn, cfg = sc.config(2)
     L, S, K = 512, 3, 4
     sol = _solver(smc, scn, L=L, S=S, K=K, seed=cfg.seed, mh=2)
@@ -225,19 +383,21 @@ def test_per_aircraft_mh_rounds(smc, layout, monkeypatch):
         sol.iterate(1)
         pop = sol.population()
         mask = pop["surv_mask"]
-        ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
-        ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
+        ell_c, mg_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed, margin=True)
+        ell_p, mg_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed, margin=True)
         bits = ((mask[:, None] >> np.arange(n)[None, :]) & 1).astype(bool)
         ell_o = np.where(bits, ell_p, ell_c)
+        mg = np.where(bits, mg_p, mg_c)
         ell_g = pop["ell"].T.astype(np.float64)
-        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
-        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
-        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+        _check_ell(ell_g, ell_o, mg, S, f"per-aircraft MH k={k}")
         assert np.allclose(pop["lam"], np.where(np.isfinite(ell_g).all(1), ell_g.sum(1), -np.inf), rtol=1e-12)
-        # oracle decisions on the oracle's weights agree except at near-ties
+        # the decisions on the oracle's weights agree wherever neither candidate is ambiguous
+        clear = (mg_c >= EPS) & (mg_p >= EPS)
         dec = np.array([[O.mh_accept_aircraft(ell_c[l, i], ell_p[l, i], l, i, k, cfg.seed) for i in range(n)]
                         for l in range(L)])
-        assert (dec == bits).mean() > 0.98
+        both_inf = ~np.isfinite(ell_c) & ~np.isfinite(ell_p)
+        near = np.abs(ell_p - ell_c) < 1e-3                # MH on float vs double weights: near-ties may differ
+        assert np.all((dec == bits)[clear & ~near] | both_inf[clear & ~near])
         assert 0.02 < bits.mean() < 0.98                 # both outcomes occur
     _, lam_best, idx = sol.best_controls(allow_infeasible=True)
     pop = sol.population()
@@ -341,16 +501,17 @@ def test_shrinking_population_rounds(smc, L, Lf, S, K, mode, monkeypatch):
                 if r["Q"] == 0:
                     continue
                 assert np.array_equal(pop["cur"][:, i], chosen[r["anc"], i]), (k, i)
-        ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
+        sub = slice(0, min(Lk, 4000))              # the oracle checks the first 4000 particles
+        ell_c, mg_c = P.evaluate(pop["cur"][sub].astype(np.float64), S, k, cfg.seed, margin=True,
+                                 ell0=-math.log2(Lk))
         if k > 0:
-            ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
-            ell_o = np.where(pop["surv"][:, None] == 1, ell_p, ell_c)
+            ell_p, mg_p = P.evaluate(pop["prop"][sub].astype(np.float64), S, k, cfg.seed, margin=True,
+                                     ell0=-math.log2(Lk))
+            sv = pop["surv"][sub][:, None] == 1
+            ell_o, mg = np.where(sv, ell_p, ell_c), np.where(sv, mg_p, mg_c)
         else:
-            ell_o = ell_c
-        ell_g = pop["ell"].T.astype(np.float64)
-        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
-        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
-        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+            ell_o, mg = ell_c, mg_c
+        _check_ell(pop["ell"].T[sub], ell_o, mg, S, f"shrinking L={L} k={k}")
         chosen = np.where(pop["surv"][:, None, None, None] == 1, pop["prop"], pop["cur"])
         prev = (chosen, pop["ell"], k)
     sol.close()
@@ -398,28 +559,18 @@ def test_round_replay_bitexact(smc):
         sol.iterate(1)
         pop = sol.population()
         if k == 0:
-            ell_o = P.evaluate(pop["cur"].astype(np.float64), S, 0, cfg.seed)
+            ell_o, mg = P.evaluate(pop["cur"].astype(np.float64), S, 0, cfg.seed, margin=True)
             assert np.all(pop["surv"] == 0)
         else:
-            ell_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed)
-            ell_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed)
-            lam_c = np.where(np.isfinite(ell_c).all(1), ell_c.sum(1), -np.inf)
-            lam_p = np.where(np.isfinite(ell_p).all(1), ell_p.sum(1), -np.inf)
+            ell_c, mg_c = P.evaluate(pop["cur"].astype(np.float64), S, k, cfg.seed, margin=True)
+            ell_p, mg_p = P.evaluate(pop["prop"].astype(np.float64), S, k, cfg.seed, margin=True)
             # MH replay on the GPU's own lambdas is bit-exact
             lc_g, lp_g = pop["lam_cand"]
             acc_ref = np.array([O.mh_accept(lc_g[l], lp_g[l], l, k, cfg.seed) for l in range(L)])
             assert np.array_equal(pop["surv"].astype(bool), acc_ref)
-            # and the GPU's lambdas agree with the oracle's (tolerance) where both finite
-            for lg, lo in ((lc_g, lam_c), (lp_g, lam_p)):
-                f = np.isfinite(lg) & np.isfinite(lo)
-                assert (np.isfinite(lg) == np.isfinite(lo)).mean() > 0.99
-                assert np.allclose(lg[f], lo[f], rtol=0, atol=1e-4 * (np.abs(lo[f]).max() + n * S))
-            ell_o = np.where(pop["surv"][:, None] == 1, ell_p, ell_c)
-        ell_g = pop["ell"].T.astype(np.float64)
-        fin = np.isfinite(ell_o) & np.isfinite(ell_g)
-        agree = np.isfinite(ell_o) == np.isfinite(ell_g)
-        assert agree.mean() > 0.99
-        assert np.allclose(ell_g[fin], ell_o[fin], rtol=0, atol=1e-4 * (np.abs(ell_o[fin]).max() + S))
+            sv = pop["surv"][:, None] == 1
+            ell_o, mg = np.where(sv, ell_p, ell_c), np.where(sv, mg_p, mg_c)
+        _check_ell(pop["ell"].T, ell_o, mg, S, f"round replay c1 k={k}", lam_g=pop["lam"])
         # resampling replay: the oracle on the GPU's survivor ell gives the GPU's ancestors
         if k < 3:
             anc_g, _ = sol.debug_resample(pop["ell"], k)
@@ -484,9 +635,9 @@ def test_graph_replay_matches_direct_launches(smc):
 @pytest.mark.parametrize("num", [2, 3, 4, 5])
 def test_full_size_sampled_parity(smc, num):
     """Configs c2-c5 at full size (c5: L = 2^20, N = 16, S = 64) in the bench's
-    launch configuration (CUDA graph, chunked K2 where planned): two rounds on
-    the GPU; 24 sampled survivors of round 1 re-evaluated by the oracle one by
-    one, and their MH decisions replayed bit-exactly on the GPU's lambdas."""
+    launch configuration (CUDA graph): two rounds on the GPU; 48 sampled
+    survivors of round 1 re-evaluated by the oracle one by one (element by
+    element), and 2000 MH decisions replayed bit-exactly on the GPU's lambdas."""
     scn, cfg = sc.config(num)
     sol = smc.Solver(scn, L=cfg.L, S=cfg.S, K=cfg.K, sigma=cfg.sigma, seed=cfg.seed, use_graph=True)
     sol.iterate(2)
@@ -497,21 +648,20 @@ def test_full_size_sampled_parity(smc, num):
         assert pop["surv"][l] == O.mh_accept(lc[l], lp[l], int(l), 1, cfg.seed)
     P = O.Problem(scn)
     rng = np.random.default_rng(0)
-    idx = rng.choice(cfg.L, 24, replace=False)
-    for l in idx:
-        ell_o = np.full(scn["n"], -np.log2(cfg.L))
-        amb = False
-        ctrl = (pop["prop"][l] if pop["surv"][l] else pop["cur"][l]).astype(np.float64)
+    idx = np.sort(rng.choice(cfg.L, 48, replace=False))
+    ctrl = np.stack([(pop["prop"][l] if pop["surv"][l] else pop["cur"][l]) for l in idx]).astype(np.float64)
+    ell_o = np.full((len(idx), scn["n"]), -np.log2(cfg.L))
+    mg = np.full((len(idx), scn["n"]), np.inf)
+    for j, l in enumerate(idx):                # particle l's global index keys its streams
+        r_ell = ell_o[j].copy()
         for s in range(cfg.S):
-            r = P.rollout(ctrl, int(l), s, 1, cfg.seed)
-            amb |= np.min(r["margin"]) < MARGIN
-            ell_o = np.where(r["viol"].astype(bool) | (r["J"] <= 0), -np.inf, ell_o + np.log2(np.maximum(r["J"], 1e-300)))
-        if amb:
-            continue
-        g = pop["ell"][:, l].astype(np.float64)
-        assert np.array_equal(np.isfinite(g), np.isfinite(ell_o)), l
-        f = np.isfinite(g)
-        assert np.allclose(g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + cfg.S)), l
+            r = P.rollout(ctrl[j], int(l), s, 1, cfg.seed)
+            lmin = r["margin_land"].min()
+            mg[j] = np.minimum(mg[j], np.minimum(r["margin"], lmin))
+            r_ell = np.where(r["viol"].astype(bool) | (r["J"] <= 0), -np.inf,
+                             r_ell + np.log2(np.maximum(r["J"], 1e-300)))
+        ell_o[j] = r_ell
+    _check_ell(pop["ell"][:, idx].T, ell_o, mg, cfg.S, f"full size c{num}")
 
 
 def test_mpc_loop_rolling_window(smc):
@@ -550,11 +700,8 @@ def test_paper_literal_mode_replay(smc):
         else:
             assert np.all(pop["surv"] == 1)
             ctrl = pop["prop"]
-        ell_o = P.evaluate(ctrl.astype(np.float64), O.sample_schedule(k), k, cfg.seed)
-        ell_g = pop["ell"].T.astype(np.float64)
-        assert (np.isfinite(ell_o) == np.isfinite(ell_g)).mean() > 0.99
-        f = np.isfinite(ell_o) & np.isfinite(ell_g)
-        assert np.allclose(ell_g[f], ell_o[f], rtol=0, atol=1e-4 * (np.abs(ell_o[f]).max() + 20))
+        ell_o, mg = P.evaluate(ctrl.astype(np.float64), O.sample_schedule(k), k, cfg.seed, margin=True)
+        _check_ell(pop["ell"].T, ell_o, mg, O.sample_schedule(k), f"paper-literal k={k}", lam_g=pop["lam"])
 
 
 @pytest.mark.parametrize("num,vw,mh", [(1, 2, 1), (2, 3, 1), (5, 4, 1), (2, 3, 2)])
@@ -580,14 +727,6 @@ def test_virtual_ranks_bitexact(smc, num, vw, mh, exchange, monkeypatch):
     for key in ("cur", "prop", "surv_mask", "ell", "lam"):
         assert np.array_equal(a[key], b[key]), key
     assert np.array_equal(ba[0], bb[0]) and ba[1] == bb[1] and ba[2] == bb[2]
-
-
-@pytest.mark.parametrize("case", ["n12_noise", "n24", "n3_partial"])
-def test_rollout_parity_transposed_layout(smc, case, monkeypatch):
-    """The alternative K2 layout (warp = aircraft; SMC_K2_LAYOUT=transposed)
-    passes the same rollout parity as the default segment layout."""
-    monkeypatch.setenv("SMC_K2_LAYOUT", "transposed")
-    test_rollout_parity(smc, case)
 
 
 @pytest.mark.parametrize("use_graph", [False, True])

@@ -51,43 +51,45 @@ def test_zero_weight_absorbs(ora):
 
 def test_separation_flags_match_bruteforce(ora):
     """Re-derive every violation flag from the oracle's own trajectories with
-    a brute-force O(N^2) pair scan of Eq. avoidance plus the unary bounds."""
+    a brute-force O(N^2) pair scan of Eq. avoidance plus the unary bounds:
+    every aircraft is in every pair test at every step, violated or not
+    (Alg.1 l.11-13; Eq. avoidance "for every time step ... i != j")."""
     scn = sc.snapshot(3, 3, seed=21)
     # crowd the aircraft so that conflicts actually occur
-    scn["x0"][:, 0] *= 0.15
-    scn["x0"][:, 1] *= 0.15
+    scn["x0"][:, 0] *= 0.5
+    scn["x0"][:, 1] *= 0.5
     scn["x0"][:, 2] = 3000.0 + 150.0 * np.arange(scn["n"])
     scn["kind"][:] = 1                      # departures: no landing removals
     P = ora.Problem(scn)
     n, H = scn["n"], scn["H"]
     ctrl = sc.random_controls(scn, 40, seed=8, spread=0.5).astype(np.float64)
-    n_conf = 0
+    n_conf = n_late = 0
     for l in range(40):
         r = P.rollout(ctrl[l], l, 0, 0, 5)
         tr = r["traj"]
         viol = np.zeros(n, bool)
         for j in range(1, H + 1):
-            present = ~viol.copy()
+            before = viol.copy()
             for i in range(n):
-                if present[i]:
-                    u = ctrl[l, i, j - 1]
-                    st = tr[i, j]
-                    bad = (abs(u[2]) > scn["gamma_max"][i] or not abs(u[1]) < scn["phi_max"][i]
-                           or u[0] < scn["T_min"][i] or u[0] > scn["T_max"][i]
-                           or not scn["z_min"][i] <= st[2] <= scn["z_max"][i]
-                           or not scn["v_min"][i] <= st[3] <= scn["v_max"][i]
-                           or st[5] < scn["m_empty"][i])
-                    if bad:
-                        viol[i] = True
+                u = ctrl[l, i, j - 1]
+                st = tr[i, j]
+                bad = (abs(u[2]) > scn["gamma_max"][i] or not abs(u[1]) < scn["phi_max"][i]
+                       or u[0] < scn["T_min"][i] or u[0] > scn["T_max"][i]
+                       or not scn["z_min"][i] <= st[2] <= scn["z_max"][i]
+                       or not scn["v_min"][i] <= st[3] <= scn["v_max"][i]
+                       or st[5] < scn["m_empty"][i])
+                if bad:
+                    viol[i] = True
             for i in range(n):
                 for q in range(i + 1, n):
-                    if present[i] and present[q]:
-                        d2 = (tr[i, j, 0] - tr[q, j, 0]) ** 2 + (tr[i, j, 1] - tr[q, j, 1]) ** 2
-                        if d2 < (2 * 2500.0) ** 2 and abs(tr[i, j, 2] - tr[q, j, 2]) < 600.0:
-                            viol[i] = viol[q] = True
-                            n_conf += 1
+                    d2 = (tr[i, j, 0] - tr[q, j, 0]) ** 2 + (tr[i, j, 1] - tr[q, j, 1]) ** 2
+                    if d2 < (2 * 2500.0) ** 2 and abs(tr[i, j, 2] - tr[q, j, 2]) < 600.0:
+                        n_late += int(before[i] != before[q])     # one side already violated earlier
+                        viol[i] = viol[q] = True
+                        n_conf += 1
         assert np.array_equal(viol, r["viol"].astype(bool)), l
-    assert n_conf > 0
+    assert n_conf > 0 and not np.all(viol)
+    assert n_late > 0          # conflicts of an earlier violator with a clean aircraft are exercised
 
 
 def test_head_on_conflict_step(ora):
@@ -115,8 +117,8 @@ def test_head_on_conflict_step(ora):
         if expect:
             first = int(np.argmax(gap < 5000.0))
             assert first == 6
-            # after the conflict both are removed (frozen) (R42)
-            assert np.all(r["traj"][0, 7:] == r["traj"][0, 6])
+            # after the conflict both keep flying their controls (Alg.1 l.11-13)
+            assert r["traj"][0, 8, 0] > r["traj"][0, 7, 0] > r["traj"][0, 6, 0]
 
 
 def test_landing_freezes_and_bonus(ora):
