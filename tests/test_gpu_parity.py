@@ -686,7 +686,7 @@ def test_paper_literal_mode_replay(smc):
     paper's SampleSchedule floor(3 + 5 e^{0.05 J}).  Replayed against
     the oracle round by round; the oracle's own full run uses the same rules."""
     scn, cfg = sc.config(1)
-    L = 256
+    L = 2048
     sol = smc.Solver(scn, L=L, S=cfg.S, K=4, sigma=cfg.sigma, seed=cfg.seed, mh=False, sched_paper=True)
     P = O.Problem(scn)
     stats = []
@@ -772,6 +772,7 @@ def test_fuel_estimates_parity(smc):
     traces = np.zeros((n, max_len, 5))
     lens = rng.integers(1, max_len + 1, n)
     lens[:3] = [1, 2, max_len]
+    lens[13] = max_len
     m0 = rng.uniform(55000, 75000, n)
     for j in range(n):
         K = int(lens[j])
@@ -786,6 +787,7 @@ def test_fuel_estimates_parity(smc):
                        rng.normal(0, 150), rng.normal(0, 4), rng.normal(0, 0.1)]
             if j % 50 == 11:                      # implausible climb
                 st[2] += 1e5
+    traces[13, 3, 3] = np.nan                     # a missing airspeed: undefined burn, none booked
     ty = np.array([scn["S"][0], scn["cd0"][0], scn["cd2"][0], Cf[0], Cf[1], scn["gamma_max"][0]])
     out = smc.fuel_estimates(traces, lens, m0, np.tile(ty, (n, 1)), dt, g=scn["g"], density_mode=scn["density_mode"])
     for j in range(n):

@@ -482,3 +482,140 @@ def test_fuel_estimate2_properties(ora):
     bad = np.array([[0.0, 0.0, 0.0, 10.0, 0.0], [600.0, 0.0, 5000.0, 10.0, 0.0]])
     _, _, f4 = P.fuel_estimate1(0, bad, dt, 68000.0, Cf)
     assert f4 & 1
+
+
+# ---------------------------------------------------------------- ISA density (R12)
+@pytest.mark.parametrize("z,rho", [(0.0, 1.2250), (5000.0, 0.73643), (11000.0, 0.36392)])
+def test_isa_density_table_values(ora, z, rho):
+    """The drag model's density is the ICAO standard atmosphere (troposphere):
+    tabulated 1.2250 / 0.73643 / 0.36392 kg m^-3 at 0 / 5 / 11 km.  Exposed through
+    the parabolic polar: D = q (C_D0 + C_D2 C_L^2), q = rho v^2 S / 2, C_L = m g / q."""
+    scn = _calm(sc.snapshot(0, 1, seed=1))
+    P = ora.Problem(scn)
+    v, m = 160.0, 62000.0
+    _, D = P.lift_drag(0, [0, 0, z, v, 0, m], 0.0)
+    q = 0.5 * rho * v * v * scn["S"][0]
+    cl = m * scn["g"] / q
+    assert D == pytest.approx(q * (scn["cd0"][0] + scn["cd2"][0] * cl * cl), rel=2e-4)
+
+
+# ---------------------------------------------------------------- AR(1) for t >= 1 (P:459-466)
+def _node0_wind_series(ora, lam, L=3000, H=6):
+    """The x wind at grid node 0 for steps t = 0..H-1 of L independent samples.  The
+    aircraft flies level at z = 0 heading South-West from the corner (-30 km, -30 km):
+    its clamped position is node 0 every step (R14), so w_x(t) = (x_{t+1} - x_t)/dt -
+    v_t cos(chi) (Eq. hor a with gamma = 0)."""
+    scn = _calm(sc.snapshot(0, 1, seed=1, H=H))
+    scn.update(sigma_lo=1.5, sigma_hi=4.0, lambda_t=lam)
+    chi = -0.75 * math.pi
+    scn["x0"][0] = [-30000.0, -30000.0, 0.0, 130.0, chi, 70000.0]
+    P = ora.Problem(scn)
+    u = np.zeros((1, H, 3))
+    u[..., 0] = 30000.0
+    out = np.zeros((L, H))
+    for l in range(L):
+        tr = P.rollout(u, l, 0, 0, 1234)["traj"][0]
+        out[l] = (tr[1:, 0] - tr[:-1, 0]) / scn["dt"] - tr[:-1, 3] * math.cos(chi)
+    return out, P
+
+
+def test_ar1_stationary_variance_and_lag_correlation(ora):
+    """W(t) = a W(t-1) + Q v(t), Q = sqrt(1 - a^2) Qhat keeps the field
+    stationary: Var W(t) = sigma(z)^2 at every step, Corr(W(t), W(t+1)) = a,
+    Corr(W(t), W(t+2)) = a^2, with a = exp(-lambda dt) (R14).  A large lambda
+    (a = e^{-0.5}) makes the pin sharp: dropping the innovation (b) decays the
+    variance as a^{2t}, dropping the carry (a) zeroes the correlation."""
+    lam = 0.05
+    w, P = _node0_wind_series(ora, lam)
+    a, b = P.ab
+    assert a == pytest.approx(math.exp(-lam * 10.0), rel=1e-15) and b == pytest.approx(math.sqrt(1 - a * a), rel=1e-15)
+    n = w.shape[0]
+    for t in range(w.shape[1]):
+        assert w[:, t].var() == pytest.approx(1.5 ** 2, rel=0.09), t
+        assert abs(w[:, t].mean()) < 4 * 1.5 / math.sqrt(n)
+    c1 = np.mean([np.corrcoef(w[:, t], w[:, t + 1])[0, 1] for t in range(5)])
+    c2 = np.mean([np.corrcoef(w[:, t], w[:, t + 2])[0, 1] for t in range(4)])
+    assert c1 == pytest.approx(a, abs=0.03)
+    assert c2 == pytest.approx(a * a, abs=0.03)
+
+
+def test_ar1_slow_field_is_nearly_frozen(ora):
+    """At the paper's lambda = 6e-6 s^-1 (R14) a = 0.99994: successive steps of a
+    sample see almost the same field (the forecast error drifts slowly)."""
+    w, P = _node0_wind_series(ora, 6e-6, L=400)
+    d = w[:, 1:] - w[:, :-1]
+    assert np.sqrt(np.mean(d * d)) < 0.05 * 1.5
+
+
+# ---------------------------------------------------------------- departure altitude and speed terms
+def _level_departure(ora, H, z0, v, climb=0.0, zt=6000.0):
+    scn = _calm(sc.snapshot(0, 1, seed=1, H=H))
+    scn["density_mode"] = 1
+    scn["x0"][0] = [3000.0, 0.0, z0, v, 0.0, 70000.0]
+    scn["theta_F"][0] = 0.0
+    scn["z_tf"][0] = zt
+    P = ora.Problem(scn)
+    u = np.zeros((1, H, 3))
+    st = scn["x0"][0].copy()
+    for t in range(H):                              # trimmed: airspeed constant (Eq. hor d)
+        _, D = P.lift_drag(0, st, 0.0)
+        u[0, t] = [D + st[5] * 9.81 * math.sin(climb), 0.0, climb]
+        st = P.step(0, st, u[0, t])
+    return scn, P, u
+
+
+def test_departure_altitude_term_level_flight_is_one_half(ora):
+    """Departure altitude term B with the reachability sup/inf (R21): per
+    step j the reachable band is z0 +- j dt v_max sin(gamma_max); a level departure
+    below the band-limited target deviates by z_tf - z0 every step, and
+    sup_j = z_tf - z0 + r_j, inf_j = z_tf - z0 - r_j give J3 = (mean r)/(2 mean r) = 1/2."""
+    H = 6
+    scn, P, u = _level_departure(ora, H, 3000.0, 150.0)
+    r = P.rollout(u, 0, 0, 0, 1)
+    reach = np.array([j * scn["dt"] * scn["v_max"][0] * math.sin(scn["gamma_max"][0]) for j in range(1, H + 1)])
+    assert reach.max() < 3000.0                      # the band stays inside [z_min, z_tf]
+    supB, infB = P.supinfB()
+    assert supB[0] == pytest.approx(3000.0 + reach.mean(), rel=1e-12)
+    assert infB[0] == pytest.approx(3000.0 - reach.mean(), rel=1e-12)
+    assert r["comp"][0, 2] == pytest.approx(0.5, abs=1e-12)
+
+
+def test_departure_altitude_term_max_climb_is_one(ora):
+    """Climbing at gamma_max with v = v_max every step reaches the top of the reachable
+    band, z_j = z0 + j dt v_max sin(gamma_max) = the inf of the deviation: J3 = 1."""
+    H = 5
+    scn, P, u = _level_departure(ora, H, 3000.0, 180.0, climb=6.0 * DEG)
+    r = P.rollout(u, 0, 0, 0, 1)
+    assert r["comp"][0, 2] == pytest.approx(1.0, abs=1e-9)
+
+
+@pytest.mark.parametrize("v,expect", [(150.0, 1.0), (110.0, 0.5), (130.0, 0.75)])
+def test_departure_speed_term(ora, v, expect):
+    """Speed term C at constant airspeed: J4 = 1 - |v - v_D| / sup_C with
+    sup_C = max(v_max - v_D, v_D - v_min) = max(30, 80) = 80 m/s (R21)."""
+    scn, P, u = _level_departure(ora, 6, 3000.0, v)
+    r = P.rollout(u, 0, 0, 0, 1)
+    assert r["comp"][0, 3] == pytest.approx(expect, abs=1e-9)
+
+
+def test_fuel_estimates_never_gain_weight(ora):
+    """P:755: "aircraft were restricted from burning negative fuel and gaining weight":
+    the mass series of both estimates is non-increasing, also across an interval whose
+    burn is undefined (a recorded airspeed missing as NaN gives T = NaN) -- that
+    interval burns nothing and the series continues from the same mass (R47)."""
+    scn = sc.snapshot(0, 1, seed=1)
+    P = ora.Problem(scn)
+    dt, Cf = 60.0, (1.1e-5, 500.0)
+    rng = np.random.default_rng(4)
+    tr = np.zeros((12, 5))
+    st = np.array([0.0, 0.0, 3000.0, 150.0, 0.2])
+    for k in range(12):
+        tr[k] = st
+        st = st + [dt * st[3] * math.cos(st[4]), dt * st[3] * math.sin(st[4]), rng.normal(0, 100),
+                   rng.normal(0, 15), rng.normal(0, 0.05)]
+    tr[5, 3] = float("nan")
+    m1, _, _ = P.fuel_estimate1(0, tr, dt, 68000.0, Cf)
+    m2, _ = P.fuel_estimate2(0, tr, dt, 68000.0, Cf)
+    for m in (m1, m2):
+        assert np.all(np.isfinite(m)) and np.all(np.diff(m) <= 0.0)
+    assert m1[5] == m1[6] or m1[4] == m1[5]          # the NaN sample's interval burns nothing

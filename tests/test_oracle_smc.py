@@ -414,3 +414,86 @@ def test_per_aircraft_mh_single_aircraft_reduces_to_joint(ora):
     r2 = P.run_smc(128, 3, 5, 77, sig, mh=2)
     assert np.array_equal(r1["stats"], r2["stats"])
     assert r2["best_lambda"] >= r1["best_lambda"]
+
+
+# ---------------------------------------------------------------- init and perturbation
+def _ks_uniform(x):
+    x = np.sort(x)
+    n = len(x)
+    i = np.arange(1, n + 1)
+    return max(np.max(i / n - x), np.max(x - (i - 1) / n))
+
+
+def test_init_population_uniform_in_bounds(ora):
+    """Alg.1 l.5 draws every control uniformly over the envelope of P:240:
+    T in [T_min, T_max], phi in [-phi_max, phi_max], gamma in [-gamma_max, gamma_max].
+    Each component, scaled to [0, 1], passes a Kolmogorov-Smirnov test (alpha ~ 1e-3);
+    components, aircraft and steps are uncorrelated."""
+    scn = sc.snapshot(2, 2, seed=3)
+    P = ora.Problem(scn)
+    L = 3000
+    c = P.init_population(L, 0x5EED0042)
+    lo = np.array([scn["T_min"][0], -scn["phi_max"][0], -scn["gamma_max"][0]])
+    hi = np.array([scn["T_max"][0], scn["phi_max"][0], scn["gamma_max"][0]])
+    assert np.all(c > lo) and np.all(c < hi)
+    u = (c - lo) / (hi - lo)
+    n = u[..., 0].size
+    for q in range(3):
+        assert _ks_uniform(u[..., q].ravel()) < 1.95 / math.sqrt(n), q
+    flat = u.reshape(L, -1)
+    cc = np.corrcoef(flat[:, :24].T)
+    assert np.max(np.abs(cc - np.eye(24))) < 0.08
+
+
+def test_perturbation_residuals_are_standard_normal(ora):
+    """Alg.1 l.23: x* = x' + Gaussian white noise with the per-component
+    sigma.  The standardised residuals (x* - x')/sigma are N(0, 1) in every component
+    (mean, variance, KS against the normal CDF), independent across steps and
+    aircraft; sigma = 0 returns the parent exactly; without the clamp option nothing is
+    clipped (an out-of-envelope proposal is a constraint violation, R16), with it every
+    component lands in the envelope."""
+    scn = sc.snapshot(2, 1, seed=3)
+    P = ora.Problem(scn)
+    sig = np.array([6000.0, 0.035, 0.0087])
+    parent = np.tile(np.array([60000.0, 0.1, -0.02]), (scn["H"], 1))
+    z = []
+    for l in range(600):
+        for i in range(scn["n"]):
+            x = P.perturb_row(i, parent, l, 7, 0x77, sig)
+            z.append((x - parent) / sig)
+    z = np.array(z)                                    # [600 n][H][3]
+    from math import erf
+    for q in range(3):
+        v = z[..., q].ravel()
+        assert abs(v.mean()) < 4 / math.sqrt(v.size) and v.var() == pytest.approx(1.0, rel=0.06)
+        cdf = np.array([0.5 * (1 + erf(s / math.sqrt(2))) for s in np.sort(v)])
+        i = np.arange(1, v.size + 1)
+        assert max(np.max(i / v.size - cdf), np.max(cdf - (i - 1) / v.size)) < 1.95 / math.sqrt(v.size)
+    flat = z.reshape(z.shape[0], -1)
+    cc = np.corrcoef(flat.T)
+    assert np.max(np.abs(cc - np.eye(cc.shape[0]))) < 0.15
+    assert np.array_equal(P.perturb_row(0, parent, 3, 7, 0x77, (0.0, 0.0, 0.0)), parent)
+    big = P.perturb_row(0, parent, 3, 7, 0x77, (1e6, 10.0, 10.0))
+    assert np.any(big[:, 0] > scn["T_max"][0]) or np.any(big[:, 0] < scn["T_min"][0])
+    cl = P.perturb_row(0, parent, 3, 7, 0x77, (1e6, 10.0, 10.0), clamp=True)
+    assert np.all((cl[:, 0] >= scn["T_min"][0]) & (cl[:, 0] <= scn["T_max"][0]))
+    assert np.all(np.abs(cl[:, 1]) <= scn["phi_max"][0]) and np.all(np.abs(cl[:, 2]) <= scn["gamma_max"][0])
+
+
+def test_proposal_spread_anneals(ora):
+    """The proposal spread of round k is sigma * anneal^k (R16): with a single
+    particle per aircraft and a calm, deterministic scenario, the paper-literal run
+    (mh = 0) reproduces the oracle's own perturbation with sigma 0.98^k for the
+    proposal of round k -- its selected controls after K = 3 rounds equal
+    perturb(perturb(init, k = 0, sigma), k = 1, 0.98 sigma)."""
+    scn = _calm(sc.snapshot(0, 1, seed=5, H=3))
+    P = ora.Problem(scn)
+    sig = (3000.0, 0.02, 0.004)
+    res = P.run_smc(L=1, S=1, K=3, seed=0x32, sigma=sig, mh=False, anneal=0.98)
+    assert res["rc"] == 0
+    x = P.init_population(1, 0x32)[0, 0]
+    x = P.perturb_row(0, x, 0, 0, 0x32, sig)
+    x1 = P.perturb_row(0, x, 0, 1, 0x32, tuple(0.98 * s for s in sig))
+    assert np.allclose(res["best_ctrl"][0], x1, rtol=0, atol=1e-9)
+    x1_flat = P.perturb_row(0, x, 0, 1, 0x32, sig)           # without annealing: a different row
+    assert not np.allclose(res["best_ctrl"][0], x1_flat, rtol=0, atol=1e-6)
