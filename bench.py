@@ -4,16 +4,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl smcatm|reference]
                     [--config 2] [--no-cpu-baseline]
 
-A step is one MPC update of BASELINE.json's configs[1] workload (c2: 8
-aircraft, L = 16384 particles, S = 16 wind samples, K = 101 SMC rounds): fresh
-population, K rounds of rollout + MH + reduce + systematic resampling +
-proposal, final selection and the plant step -- every row of SURVEY.md 8(a).
-`value` is aircraft-step rollouts per second over the whole job (device
-time, inputs resident); `e2e` is the same metric through the public C ABI
-call mpc_step() with pinned host buffers, host<->device copies inside the
-timed region.  N > 1 (torchrun): one MPC problem with L particles per GPU
-sharded over the N GPUs, NCCL exchange each round (weak scaling) -- see
-DESIGN.md section 9.
+A step is one MPC update of the workload BASELINE.json's metric is quoted on,
+configs[4] (c5: 16 aircraft, L = 2^20 particles, S = 64 wind samples, H = 6,
+K = 101 SMC rounds): fresh population, K rounds of rollout + MH + reduce +
+systematic resampling + proposal, final selection and the plant step --
+every row of SURVEY.md 8(a).  `value` is aircraft-step rollouts per second
+over the whole job (device time, inputs resident); `e2e` is the same metric
+through the public C ABI call mpc_step() with pinned host buffers,
+host<->device copies inside the timed region.  N > 1 (torchrun): the same
+2^20 particles sharded over the N GPUs, NCCL exchange each round (strong
+scaling).  --config 2|3|4|6|7 selects the other
+workloads (c2-c4, the paper's Table-1 workload, the 20-aircraft latency
+target).
 """
 from __future__ import annotations
 
@@ -42,9 +44,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="smcatm", choices=["smcatm", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--phase-steps", type=int, default=2,
+                    help="steps of the second (per-kernel timed) pass")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--traffic", default="c3", choices=["c3", "mixed", "congested"],
                     help="traffic stream of --loop")
@@ -127,29 +131,63 @@ def load_traffic(cfgname):
         return None
 
 
-def cpu_baseline(scn, cfg, seconds=12.0):
-    """The FP64 oracle, as it stands, on this host's cores: evaluation (Alg.1
-    l.9-18) of a bounded particle sample of the same workload, repeated for
-    ~`seconds`.  Returns aircraft-steps/s and the sample description."""
-    import numpy as np
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
+
+def cpu_baseline(scn, cfg, seconds=8.0):
+    """The FP64 oracle, as it stands, on this host's cores: evaluation (Alg.1 l.9-18)
+    of a bounded particle sample of the same workload (one SMC round's rollouts),
+    repeated for ~`seconds` at nproc threads and at one thread; plus c1 (the parity
+    config) run in full through the oracle's Alg.1.  Returns the baseline dict."""
     import oracle as O
+    from paper_1506_02869_b200 import scenarios as sc
     P = O.Problem(scn)
-    nthreads = os.cpu_count() or 1
-    Lp = min(cfg.L, 2048)
+    nproc = os.cpu_count() or 1
     S = cfg.S or 8                                          # paper schedule: S_0 = 8 (P:559)
-    ctrl = P.init_population(Lp, cfg.seed)
     Ha = int(sum(scn["H"] - e for e in scn["first_step"]))
-    done, t0 = 0, time.perf_counter()
-    k = 0
-    while True:
-        P.evaluate(ctrl, S, k + 1, cfg.seed, nthreads=nthreads)
-        done += Lp * S * Ha
-        k += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    return done / el, nthreads, f"oracle evaluate of {Lp} particles x S={S} x {Ha} aircraft-steps, {k} reps, {el:.1f}s"
+
+    def rate(nthreads, Lp, budget):
+        ctrl = P.init_population(Lp, cfg.seed)
+        done, k, t0 = 0, 0, time.perf_counter()
+        while True:
+            P.evaluate(ctrl, S, k + 1, cfg.seed, nthreads=nthreads)
+            done += Lp * S * Ha
+            k += 1
+            el = time.perf_counter() - t0
+            if el >= budget:
+                return done / el, k, el
+
+    Lp = min(cfg.L, 2048)
+    v, reps, el = rate(nproc, Lp, seconds)
+    v1, reps1, el1 = rate(1, min(cfg.L, 128), seconds / 2)
+    scn1, cfg1 = sc.config(1)
+    t0 = time.perf_counter()
+    O.Problem(scn1).run_smc(L=cfg1.L, S=cfg1.S, K=cfg1.K, seed=cfg1.seed, sigma=cfg1.sigma, nthreads=nproc)
+    c1_s = time.perf_counter() - t0
+    return {"value": v, "unit": UNIT, "cores": nproc, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"oracle evaluate of {Lp} particles x S={S} x {Ha} aircraft-steps (one round's rollouts), "
+                      f"{reps} reps, {el:.1f}s, {nproc} threads",
+            "value_1thread": v1, "sample_1thread": f"{min(cfg.L, 128)} particles x S={S}, {reps1} reps, {el1:.1f}s",
+            "c1_full_mpc_step_s": c1_s,
+            "c1_full": f"c1 (2 aircraft, L={cfg1.L}, S={cfg1.S}, H={scn1['H']}, K={cfg1.K}) whole Alg.1 + MH solve, "
+                       f"{nproc} threads"}
+
+
+def workload_str(scn, cfg, args):
+    return (f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
+            f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
+            + (f"->{args.lfinal}" if args.lfinal else "")
+            + (", S_k=floor(3+5e^(0.05k))" if cfg.sched_paper else f", S={cfg.S}")
+            + f", H={scn['H']}, K={cfg.K} rounds, "
+            + {0: "paper Alg.1 (no MH)", 1: "MH on", 2: "per-aircraft MH"}[int(cfg.mh)]
+            + (f", wind grid {'x'.join(str(v) for v in scn['wind_n'])}" if args.wind_grid else ""))
 
 
 def run_reference(args):
@@ -180,12 +218,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {scn['n']} aircraft, L={cfg.L}, S={cfg.S}, H={scn['H']}, K={cfg.K}",
-                   "sample": f"one evaluation round of {Lp} particles per step"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_str(scn, cfg, args),
+                   "sample": f"each step: one evaluation round (Alg.1 l.9-18) of {Lp} of the {cfg.L} particles"},
         "mpc_step_latency_ms_extrapolated": 1000 * steps_full / value,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-                         "sample": f"oracle evaluate of {Lp} particles x S={S} per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": f"oracle evaluate of {Lp} particles x S={S} x {Ha} aircraft-steps per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -225,6 +263,19 @@ def run_loop(args):
     return 0
 
 
+def run_pipe_micro():
+    """The pipe microbenchmarks (tools/micro/pipes.cu, built by __graft_entry__.build()) on this
+    GPU in this run; [] if the binary is absent."""
+    exe = os.path.join(ROOT, "tools", "micro", "pipes")
+    if not os.path.exists(exe):
+        return []
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+        return [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+    except Exception:
+        return []
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -248,9 +299,12 @@ def main():
     if args.wind_grid:
         scn["wind_n"] = tuple(int(v) for v in args.wind_grid.split(","))
     stream = torch.cuda.Stream(device=local)
-    # N > 1: one MPC problem whose particles are sharded over the N GPUs (NCCL
-    # exchange each round), L = configs' L per GPU -> weak scaling
-    L_glob = cfg.L * world
+    # N > 1: the config's L particles sharded over the N GPUs (NCCL exchange each round):
+    # strong scaling -- the whole job is one MPC problem of fixed size
+    L_glob = cfg.L
+    L_loc = smcatm.shard_range(L_glob, world, rank)
+    L_loc = L_loc[1] - L_loc[0]
+    micro = run_pipe_micro() if rank == 0 else []
 
     def make_solver(profile):
         # profile=True brackets every kernel with CUDA events on the library's stream (graph
@@ -286,15 +340,15 @@ def main():
             barrier()
         step_ms = [a.elapsed_time(b) for a, b in evs]
         launches = sol.launches - n0
-        # per-kernel pass: the same W + K steps with CUDA events around every launch on the
-        # launching stream (smc_phase_times) -> K2's average launch duration for the roofline
+        # per-kernel pass: 1 warm-up + phase_steps steps with CUDA events around every launch on
+        # the launching stream (smc_phase_times) -> K2's average launch duration for the roofline
+        psteps = max(1, min(args.phase_steps, args.steps))
         psol = make_solver(True)
-        for _ in range(args.warmup):
-            psol.solve()
+        psol.solve()
         barrier()
         psol.phase_times()                                  # reset phase accumulators
-        pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for s in range(args.steps):
+        pevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(psteps)]
+        for s in range(psteps):
             flush.fill_(s & 0xFF)
             pevs[s][0].record(stream)
             psol.solve()
@@ -324,7 +378,7 @@ def main():
         sol.io_bytes()                                      # reset the library's copy counters
         for s in range(args.e2e_steps):
             flush.fill_(s & 0xFF)
-            torch.cuda.synchronize()
+            barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             sol.mpc_step_ptr(meas.data_ptr(), applied.data_ptr(), nxt.data_ptr(), flags.data_ptr())
@@ -347,18 +401,19 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (K2 rollout + MH)
+    # ---- roofline of the dominant kernel (K2 rollout + MH): max over the pipes of the algorithmic
+    # op count / the pipe's measured peak (roofline.py), against K2's measured time
     peaks, peak_src = load_peaks()
     clocks = clk.summary()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    pipe_pk, pipe_src = roofline.load_pipe_peaks(ROOT, micro)
     k2_ms, k2_n = phases["rollout"]
-    ops_k2 = 0.0
-    for k, S in enumerate(S_list):
-        C = 1 if (k == 0 or not cfg.mh) else 2
-        Lk = roofline.particles_of(L_glob // world, args.lfinal, cfg.K, k)
-        ops_k2 += roofline.ops_per_aircraft_step(scn, C) * Lk * C * S * int(sum(scn["H"] - e for e in scn["first_step"]))
-    ops_k2 *= args.steps
-    achieved = ops_k2 / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
-    peak = roofline.peak_alu_ops(float(peaks.get("sm_max_mhz", 1965.0)))
+    rounds = [(st * psteps * L_loc / L_glob, C, S) for st, C, S in
+              roofline.round_list(scn, L_glob, S_list, cfg.mh, args.lfinal)]
+    rf = roofline.k2_roofline(scn, rounds, k2_ms / 1000.0, sm_mhz, pipe_pk)
+    bind = rf["binding_pipe"]
+    peak_ops = pipe_pk[bind] * roofline.SMS * sm_mhz * 1e6
+    achieved = rf["ops"][bind] / (k2_ms / 1000.0) if k2_ms > 0 else 0.0
     all_ms = sum(v[0] for v in phases.values())
     # Table 1's workload (config 6) is the one with a printed number: 56 s per MPC update on
     # a GTX 580, i.e. ac_steps / 56 aircraft-steps/s
@@ -367,19 +422,12 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": vs_baseline, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {scn['n']} aircraft ({int((scn['kind'] == 0).sum())} arr / "
-                               f"{int((scn['kind'] == 1).sum())} dep), L={cfg.L}"
-                               + (f"->{args.lfinal}" if args.lfinal else "")
-                               + (", S_k=floor(3+5e^(0.05k))" if cfg.sched_paper else f", S={cfg.S}")
-                               + f", H={scn['H']}, K={cfg.K} rounds, "
-                               + {0: "paper Alg.1 (no MH)", 1: "MH on", 2: "per-aircraft MH"}[int(cfg.mh)]
-                               + (f", wind grid {'x'.join(str(v) for v in scn['wind_n'])}" if args.wind_grid else ""),
-                   "parallelism": (f"particles sharded over {world} GPUs (L = {cfg.L} per GPU; per round NCCL "
-                                   "all-reduce of column maxima + all-gather of integer CDFs, parent rows "
-                                   + ("all-gathered" if os.environ.get("SMC_P2P") == "0"
-                                      else "read in place from their owner over NVLink (CUDA IPC peer mappings)")
-                                   + ")" if world > 1 else "single GPU"),
+        "scaling": "strong", "vs_baseline": vs_baseline, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_str(scn, cfg, args),
+                   "parallelism": (f"{L_glob} particles sharded over {world} GPUs ({L_loc} on rank 0; per round NCCL "
+                                   "all-reduce of column maxima + all-gather of per-rank weight totals, parent rows "
+                                   "read in place from their owner over NVLink (CUDA IPC peer mappings))"
+                                   if world > 1 else "single GPU"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "cuda_graph": not args.no_graph,
                    "aircraft_steps_per_step": ac_steps},
@@ -388,29 +436,36 @@ def main():
         "e2e": ({"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                  "mpc_step_latency_ms": sum(e2e_ms) / len(e2e_ms)} if e2e_ms else None),
         "gpu_launches": launches,
-        "phase_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
-        "phase_pass": {"what": "second pass of the same warmup + steps with CUDA events around every kernel "
+        "phase_ms_per_step": {k: v[0] / psteps for k, v in phases.items()},
+        "phase_pass": {"what": f"second pass: 1 warm-up + {psteps} steps with CUDA events around every kernel "
                                "launch (its event nodes lengthen the step, so value is timed without them)",
                        "ms_per_step": sum(pstep_ms) / len(pstep_ms)},
-        "roofline": {"kernel": "k_rollout (K2: rollout + MH)", "bound": "alu", "achieved": achieved / 1e9,
-                     "peak": peak / 1e9, "unit": "Gop/s (FP32-lane-equivalent)", "frac": achieved / peak,
-                     "traffic": load_traffic(cfg.name),
-                     "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz {peaks.get('sm_max_mhz')} ({peak_src})",
-                     "ops_per_aircraft_step": {"C=1": roofline.ops_per_aircraft_step(scn, 1),
-                                               "C=2": roofline.ops_per_aircraft_step(scn, 2)},
+        "roofline": {"kernel": "k_rollout (K2: rollout + MH)", "bound": "alu", "pipe": bind,
+                     "achieved": achieved / 1e9, "peak": peak_ops / 1e9,
+                     "unit": f"Gop/s on the {bind} pipe (algorithmic ops, roofline.py)",
+                     "frac": rf["frac"], "traffic": load_traffic(cfg.name),
+                     "t_roof_ms_per_pipe": {p: 1e3 * t / psteps for p, t in rf["t_pipe_s"].items()},
+                     "k2_ms_per_step": k2_ms / psteps,
+                     "peak_source": f"{pipe_pk[bind]:.2f} ops/SM/clk ({pipe_src}) x 148 SMs x sm_max_mhz {sm_mhz} "
+                                    f"({peak_src})",
+                     "pipe_peaks_per_sm_clk": pipe_pk,
+                     "ops_per_aircraft_step": {f"C={c}": {p: round(float(v), 2) for p, v in
+                                                          roofline.pipe_ops(scn, c, cfg.S or 8).items()}
+                                               for c in (1, 2)},
                      "k2_share_of_step": k2_ms / all_ms if all_ms else None},
         "clocks": clocks,
     }
     # resample/propose phase vs HBM
     rs_ms = phases["resample"][0] + phases["propose"][0]
     if rs_ms > 0:
-        rb = roofline.resample_bytes(scn["n"], L_glob // world, scn["H"]) * (cfg.K - 1) * args.steps
+        rb = roofline.resample_bytes(scn["n"], L_loc, scn["H"]) * (cfg.K - 1) * psteps
         line["roofline_resample"] = {"bound": "hbm", "achieved": rb / (rs_ms / 1000.0) / 1e9,
                                      "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s",
                                      "frac": rb / (rs_ms / 1000.0) / 1e9 / float(peaks.get("hbm_gbs", 6650.0))}
+    if micro:
+        line["pipe_micro"] = micro
     if not args.no_cpu_baseline:
-        v, cores, sample = cpu_baseline(scn, cfg)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = cpu_baseline(scn, cfg)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
