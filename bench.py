@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--rounds", type=int, default=0,
+                    help="SMC rounds per MPC step (0: the config's K; other values are for quick A/B only)")
     ap.add_argument("--phase-steps", type=int, default=2,
                     help="steps of the second (per-kernel timed) pass")
     ap.add_argument("--no-graph", action="store_true")
@@ -296,6 +298,8 @@ def main():
     scn, cfg = sc.config(args.config)
     if args.mh >= 0:
         cfg = dataclasses.replace(cfg, mh=args.mh)
+    if args.rounds:
+        cfg = dataclasses.replace(cfg, K=args.rounds)
     if args.wind_grid:
         scn["wind_n"] = tuple(int(v) for v in args.wind_grid.split(","))
     stream = torch.cuda.Stream(device=local)

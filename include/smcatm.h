@@ -105,6 +105,19 @@ typedef struct {
                                               paper's runs use 2 x 2 x 2 */
 } smc_scenario;
 
+/* Host-side collectives (optional; a test shim for world_size > 1 without NCCL, e.g. two
+ * processes sharing one GPU over a CPU process group).  Each call is collective over the
+ * world_size ranks and operates on HOST buffers the library owns for the call: the library
+ * synchronises its stream, copies the device operand to the host, calls the function and
+ * copies the result back.  allreduce_max_u32: element-wise maximum of `count` words in
+ * place.  allgather: rank r's `bytes` bytes land at recv + r * bytes on every rank.  Return
+ * 0 on success.  Incompatible with use_graph (a captured graph cannot call the host). */
+typedef struct {
+    void *user;
+    int (*allreduce_max_u32)(void *user, uint32_t *buf, size_t count);
+    int (*allgather)(void *user, const void *send, void *recv, size_t bytes);
+} smc_host_collectives;
+
 /* Solver configuration. */
 typedef struct {
     uint32_t n_particles;      /* L, global over all ranks; L < 2^30 and
@@ -140,6 +153,7 @@ typedef struct {
                                   each solve start from the previous solve's winner shifted one
                                   step (aircraft matched by smc_aircraft.id; particle 0 exact, the
                                   others + N(0, sigma^2)); 0 = fresh uniform init */
+    const smc_host_collectives *host_coll; /* NULL: NCCL (world_size > 1 needs nccl_unique_id) */
 } smc_config;
 
 /* Per-round diagnostics (smc_iterate). */
@@ -158,19 +172,22 @@ typedef struct {
 size_t smc_workspace_bytes(const smc_config *cfg);
 
 /* Create a context.  Validates cfg, carves the workspace, creates events.
- * With world_size > 1 also joins the NCCL communicator (R43): rank r owns the
- * global particles [L r / G, L (r+1) / G); every random stream is keyed by the
- * global particle index, so rollouts, MH decisions and ancestors are identical
- * for any world size.  Each round then exchanges the column maxima
- * (all-reduce MAX) and the per-rank integer CDFs (all-gather) on cfg.stream,
- * and each rank's gather reads its parents' control rows where their owner
- * keeps them (peer mode, the default): smc_init exports the allocation holding
- * cfg.workspace as a CUDA IPC handle, all-gathers the handles and maps every
- * peer's workspace (NVLink/NVSwitch loads; the mappings are closed by
- * smc_destroy, so every rank's workspace must outlive every rank's context).
- * With the environment variable SMC_P2P=0 (read by smc_workspace_bytes and
- * smc_init alike) the compacted survivor rows are all-gathered instead.
- * Selection all-gathers per-rank winners.  SMC_ECUDA if the IPC mapping fails. */
+ * With world_size > 1 also joins the NCCL communicator (R43; or uses
+ * cfg.host_coll): rank r owns the global particles [L r / G, L (r+1) / G);
+ * every random stream is keyed by the global particle index, so rollouts, MH
+ * decisions and ancestors are identical for any world size.  Each round then
+ * exchanges the column maxima (all-reduce MAX, N words) and the per-rank
+ * column totals of the integer weights (all-gather, N uint64 per rank) on
+ * cfg.stream; each rank's gather searches the owning rank's CDF and reads its
+ * parents' control rows where their owner keeps them (peer mode, the
+ * default): smc_init exports the allocation holding cfg.workspace as a CUDA
+ * IPC handle, all-gathers the handles and maps every peer's workspace
+ * (NVLink/NVSwitch loads; the mappings are closed by smc_destroy, so every
+ * rank's workspace must outlive every rank's context).  If a mapping cannot
+ * be opened, or with the environment variable SMC_P2P=0 (read by
+ * smc_workspace_bytes and smc_init alike), the per-rank CDFs and compacted
+ * survivor rows are all-gathered instead (the workspace size accounts for
+ * both).  Selection all-gathers per-rank winners. */
 smc_status smc_init(const smc_config *cfg, smc_ctx **out);
 
 /* Copy the scenario, precompute (Qhat = chol(Rhat) P:463-465, normalisers

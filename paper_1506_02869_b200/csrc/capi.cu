@@ -70,7 +70,8 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, centres,
-        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Sc, Sall, survp, ipc, pZ, pzi, pstates, pnext, pflags, papplied, lohi, wmap,
+        part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Qall, Csall, Sc, Sall, survp, ipc, pZ, pzi, pstates,
+        pnext, pflags, papplied, lohi, wmap, flag, infround, infcol,
         qf, qd, total;
 };
 
@@ -117,7 +118,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.QR = take(2 * nmax * sizeof(unsigned long long));
     o.anc = take(world > 1 ? 0 : (size_t)nmax * Lloc * sizeof(int32_t));   // K5 ancestors (single rank)
     o.splits = take(world > 1 ? 0 : (size_t)nmax * mp_split_words(Lloc, Lloc) * sizeof(uint32_t));
-    o.Cs = take(world > 1 ? 0 : (size_t)nmax * cdf_samples(Lloc) * sizeof(unsigned long long));   // CDF samples
+    o.Cs = take((size_t)nmax * cdf_samples(Lloc) * sizeof(unsigned long long));   // CDF samples (stride cdf_samples(Lloc))
     o.accept = take(8);
     o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
@@ -129,11 +130,19 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.best_lam = take(record_bytes(nmax, Hmax));               // local selection record
     o.best_idx = take(record_bytes(nmax, Hmax));               // final (merged) record
     o.best_row = take(G > 1 ? record_bytes(nmax, Hmax) * G : 0);           // all-gathered records
+    // multi-rank exchange: per-rank CDFs (all-gather mode / virtual ranks), column totals, CDF samples
+    // (virtual ranks), compacted survivor rows; real ranks reserve the all-gather buffers even in peer
+    // mode, which falls back to them when an IPC mapping cannot be opened
     o.Call = take(G > 1 ? (size_t)G * nmax * Lx * 8 : 0);
-    o.Sc = take(world > 1 && !p2p ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
-    o.Sall = take(G > 1 && !p2p ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
-    o.survp = take(world > 1 && p2p ? 2 * (size_t)Lloc * sizeof(uint32_t) : 0);   // published masks, by round parity
-    o.ipc = take(world > 1 && p2p ? (size_t)(G + 1) * kIpcRec : 0);              // IPC handle exchange
+    o.Qall = take(G > 1 ? (size_t)G * nmax * 8 : 0);
+    o.Csall = take(world == 1 && G > 1 ? (size_t)G * nmax * cdf_samples(Lx) * 8 : 0);
+    o.Sc = take(world > 1 ? (size_t)Lloc * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.Sall = take((world > 1 || (G > 1 && !p2p)) ? (size_t)G * Lx * nmax * Hmax * 3 * sizeof(float) : 0);
+    o.survp = take(world > 1 ? 2 * (size_t)Lloc * sizeof(uint32_t) : 0);   // published masks, by round parity
+    o.ipc = take(world > 1 ? (size_t)(G + 1) * kIpcRec : 0);              // IPC handle exchange
+    o.flag = take(16);
+    o.infround = take(nmax * sizeof(int32_t));
+    o.infcol = take(nmax * sizeof(uint32_t));
     o.pZ = take(2 * kMaxWindNodes * sizeof(double));
     o.pzi = take(sizeof(int));
     o.pstates = take(nmax * 6 * sizeof(double));
@@ -208,13 +217,18 @@ struct smc_ctx {
     uint32_t solved_H = 0;
     uint32_t Lmax = 0;
     ncclComm_t comm = nullptr;
-    unsigned long long *Call = nullptr;
+    unsigned long long *Call = nullptr, *Qall = nullptr, *Csall = nullptr;
     float *Sc = nullptr, *Sall = nullptr;
+    uint32_t *dflag = nullptr;
+    int32_t *inf_round = nullptr;       // [nmax] first round with an all-zero column (-1: none)
+    uint32_t *infcol = nullptr;         // [nmax] scratch: column maxima for the EINFEASIBLE report
+    const smc_host_collectives *hcoll = nullptr;   // host-side collectives (test shim) instead of NCCL
     // peer mode (world > 1): every rank's population buffers mapped into this process
     bool p2p = false;
     uint32_t *survp = nullptr;                 // [2][Lmax] this rank's published survivor masks
     const float *peer_ctrl[8] = {};            // rank r's control buffers (4 x prow floats)
     const uint32_t *peer_survp[8] = {};        // rank r's published masks
+    const unsigned long long *peer_C[8] = {}, *peer_Cs[8] = {};   // rank r's CDF and CDF samples
     void *peer_open[8] = {};                   // IPC mappings to close
 
     bool have_scn = false;
@@ -323,6 +337,47 @@ static cudaError_t d2h(smc_ctx *c, void *dst, const void *src, size_t bytes) {
 #define LAUNCH(expr) LAUNCHP(3, expr)
 enum { PH_ROLLOUT = 0, PH_RESAMPLE = 1, PH_PROPOSE = 2, PH_OTHER = 3 };
 
+// ---------------------------------------------------------------- collectives
+// NCCL on the context's communicator, or the host-side shim (cfg.host_coll: test mode, the
+// operands round-trip through the host around the caller's collective).
+static smc_status coll_allreduce_max_u32(smc_ctx *ctx, uint32_t *dev, size_t count) {
+    if (ctx->hcoll) {
+        std::vector<uint32_t> h(count);
+        CK(cudaMemcpyAsync(h.data(), dev, 4 * count, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (ctx->hcoll->allreduce_max_u32(ctx->hcoll->user, h.data(), count) != 0)
+            return fail(ctx, SMC_ENCCL, "host all-reduce failed");
+        CK(cudaMemcpyAsync(dev, h.data(), 4 * count, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        ++ctx->launches;
+        return SMC_OK;
+    }
+    NCK(nccl_api()->AllReduce(dev, dev, count, ncclUint32_, ncclMax_, ctx->comm, ctx->st));
+    return SMC_OK;
+}
+
+static smc_status coll_allgather(smc_ctx *ctx, const void *dev_send, void *dev_recv, size_t bytes) {
+    if (ctx->hcoll) {
+        std::vector<unsigned char> hs(bytes), hr(bytes * (size_t)ctx->world);
+        CK(cudaMemcpyAsync(hs.data(), dev_send, bytes, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (ctx->hcoll->allgather(ctx->hcoll->user, hs.data(), hr.data(), bytes) != 0)
+            return fail(ctx, SMC_ENCCL, "host all-gather failed");
+        CK(cudaMemcpyAsync(dev_recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        ++ctx->launches;
+        return SMC_OK;
+    }
+    NCK(nccl_api()->AllGather(dev_send, dev_recv, bytes, ncclUint8_, ctx->comm, ctx->st));
+    return SMC_OK;
+}
+
+#define COLL(expr)                                                                                 \
+    do {                                                                                           \
+        smc_status _s = (expr);                                                                    \
+        if (_s != SMC_OK) return _s;                                                               \
+    } while (0)
+
 // ---------------------------------------------------------------- partition helpers
 extern "C" void smc_shard_range(uint32_t L, int32_t world, int32_t rank, uint32_t *begin, uint32_t *end) {
     if (world < 1) world = 1;
@@ -422,22 +477,40 @@ static void ipc_release(void *mapping) {
         }
 }
 
+// Peer mode: every rank maps every other rank's workspace.  A rank that cannot open a mapping
+// reports it through an all-reduce, and then every rank falls back to the all-gather exchange
+// (the modes must agree: they issue different collectives).
 static smc_status map_peers(smc_ctx *ctx) {
     unsigned char rec[kIpcRec];
-    CK(ipc_record(ctx->ws, rec));
     const int G = ctx->world;
+    uint32_t bad = ipc_record(ctx->ws, rec) == cudaSuccess ? 0u : 1u;
     unsigned char *dipc = (unsigned char *)ctx->ws + ctx->lay.ipc;
     CK(cudaMemcpyAsync(dipc + (size_t)G * kIpcRec, rec, kIpcRec, cudaMemcpyHostToDevice, ctx->st));
-    NCK(nccl_api()->AllGather(dipc + (size_t)G * kIpcRec, dipc, kIpcRec, ncclUint8_, ctx->comm, ctx->st));
+    COLL(coll_allgather(ctx, dipc + (size_t)G * kIpcRec, dipc, kIpcRec));
     std::vector<unsigned char> all((size_t)G * kIpcRec);
     CK(cudaMemcpyAsync(all.data(), dipc, all.size(), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    for (int r = 0; r < G; ++r) {
+    for (int r = 0; r < G && !bad; ++r) {
         char *pws = (char *)ctx->ws;
-        if (r != ctx->rank) CK(ipc_open(all.data() + (size_t)r * kIpcRec, &ctx->peer_open[r], &pws));
+        if (r != ctx->rank && ipc_open(all.data() + (size_t)r * kIpcRec, &ctx->peer_open[r], &pws) != cudaSuccess) {
+            cudaGetLastError();
+            bad = 1u;
+            break;
+        }
         // every rank carves the same layout (same config), so offsets agree
         ctx->peer_ctrl[r] = (const float *)(pws + ctx->lay.ctrl);
         ctx->peer_survp[r] = (const uint32_t *)(pws + ctx->lay.survp);
+        ctx->peer_C[r] = (const unsigned long long *)(pws + ctx->lay.C);
+        ctx->peer_Cs[r] = (const unsigned long long *)(pws + ctx->lay.Cs);
+    }
+    CK(cudaMemcpyAsync(ctx->dflag, &bad, 4, cudaMemcpyHostToDevice, ctx->st));
+    COLL(coll_allreduce_max_u32(ctx, ctx->dflag, 1));
+    CK(cudaMemcpyAsync(&bad, ctx->dflag, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (bad) {                                       // some rank could not map a peer: all-gather mode
+        for (void *&m : ctx->peer_open)
+            if (m) { ipc_release(m); m = nullptr; }
+        ctx->p2p = false;
     }
     return SMC_OK;
 }
@@ -464,8 +537,9 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     smc_ctx *ctx = new smc_ctx();
     ctx->cfg = *cfg;
     const int world = cfg->world_size < 1 ? 1 : cfg->world_size;
-    if (world > 8 || cfg->rank < 0 || cfg->rank >= world || (world > 1 && !cfg->nccl_unique_id) ||
-        cfg->n_particles < (uint32_t)world) {
+    if (world > 8 || cfg->rank < 0 || cfg->rank >= world || (world > 1 && !cfg->nccl_unique_id && !cfg->host_coll) ||
+        cfg->n_particles < (uint32_t)world || (cfg->host_coll && cfg->use_graph) ||
+        (cfg->host_coll && (!cfg->host_coll->allreduce_max_u32 || !cfg->host_coll->allgather))) {
         delete ctx;
         return SMC_EINVAL;
     }
@@ -557,6 +631,12 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->best_row = (float *)(ctx->rec_final + 16);
     ctx->Lmax = world > 1 ? max_local(ctx->Lg, world) : max_local(ctx->Lg, ctx->vworld);
     ctx->Call = (unsigned long long *)(ws + L.Call);
+    ctx->Qall = (unsigned long long *)(ws + L.Qall);
+    ctx->Csall = (unsigned long long *)(ws + L.Csall);
+    ctx->dflag = (uint32_t *)(ws + L.flag);
+    ctx->inf_round = (int32_t *)(ws + L.infround);
+    ctx->infcol = (uint32_t *)(ws + L.infcol);
+    ctx->hcoll = world > 1 ? cfg->host_coll : nullptr;
     ctx->Sc = (float *)(ws + L.Sc);
     ctx->Sall = (float *)(ws + L.Sall);
     ctx->p2p = p2p_mode() && (world > 1 || ctx->vworld > 1);
@@ -584,11 +664,13 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     }
     ctx->wmap_h.assign(ctx->nmax, 0xFFFFFFFFu);
     if (world > 1) {
-        NcclApi *api = nccl_api();
-        if (!api) { delete ctx; return SMC_ENCCL; }
-        ncclUniqueId id;
-        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
-        if (api->CommInitRank(&ctx->comm, world, id, cfg->rank) != 0) { ctx->comm = nullptr; delete ctx; return SMC_ENCCL; }
+        if (!ctx->hcoll) {
+            NcclApi *api = nccl_api();
+            if (!api) { delete ctx; return SMC_ENCCL; }
+            ncclUniqueId id;
+            memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+            if (api->CommInitRank(&ctx->comm, world, id, cfg->rank) != 0) { ctx->comm = nullptr; delete ctx; return SMC_ENCCL; }
+        }
         if (ctx->p2p) {
             const smc_status s = map_peers(ctx);
             if (s != SMC_OK) { delete ctx; return s; }
@@ -835,6 +917,7 @@ static smc_status init_population(smc_ctx *ctx) {
     pa.clamp = (int)ctx->cfg.clamp_proposals;
     pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
     LAUNCH(launch_init_population(ctx->dsc, pa, ctx->ctrl[0][0], ctx->st));
+    CK(cudaMemsetAsync(ctx->inf_round, 0xFF, sizeof(int32_t) * ctx->nmax, ctx->st));
     ctx->k = 0;
     ctx->cur = 0;
     ctx->last_eval = -1;
@@ -973,11 +1056,12 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         CK(cudaMemcpyAsync(ctx->survp + (size_t)(k & 1) * ctx->Lmax, ctx->surv, 4 * (size_t)ctx->Lloc,
                            cudaMemcpyDeviceToDevice, ctx->st));
     if (ctx->world > 1)                    // global column maxima (reduce step 1)
-        NCK(nccl_api()->AllReduce(ctx->colmax, ctx->colmax, n, ncclUint32_, ncclMax_, ctx->comm, ctx->st));
+        COLL(coll_allreduce_max_u32(ctx, ctx->colmax, (size_t)n));
     ResampleArgs rs{};
     rs.n = n; rs.L = Lk; rs.k = k; rs.key0 = ctx->dsc.key0; rs.key1 = ctx->dsc.key1; rs.mpcp = ctx->mpc_dev;
     rs.ell = ctx->ell; rs.colmax = ctx->colmax; rs.Q = ctx->Q; rs.ess = ctx->ess; rs.status = ctx->status;
     rs.tile_ctr = ctx->tiles; rs.C = ctx->C; rs.QR = ctx->QR; rs.Cstride = ctx->world > 1 ? ctx->Lmax : 0;
+    rs.inf_round = ctx->inf_round;
     uint32_t cm[32];
     double ess[64];
     unsigned long long acc = 0;
@@ -996,18 +1080,19 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         // look-back status words the next round's scan (over Ln particles) will read
         const size_t nt = (size_t)std::max(scan_tiles(Lk), scan_tiles(Ln));
         rs.Q = nullptr;
-        // single rank, bisection in K6: K4 also writes every 16th prefix for the two-level search
         const bool single = ctx->world == 1 && ctx->vworld == 1, mp = single && use_merge_path(ctx, Lk);
-        const bool two_level = single && !mp && ctx->cdf_sample;
-        if (two_level) { rs.Cs = ctx->Cs; rs.Cs_stride = cdf_samples(Lk); }
-        LAUNCHP(PH_RESAMPLE, single && use_cluster_scan(ctx, Lk) ? launch_scan_cluster(rs, ctx->st)
-                                                                 : launch_scan(rs, ctx->st));
+        // bisection in K6 / the multi-rank gather: K4 also writes every 16th prefix (two-level search)
+        const bool two_level = !mp && ctx->cdf_sample;
+        if (two_level) { rs.Cs = ctx->Cs; rs.Cs_stride = cdf_samples(single ? Lk : ctx->Lmax); }
+        if (ctx->world > 1) rs.Q = ctx->Q;     // this rank's column totals, all-gathered below
+        if (ctx->vworld == 1)
+            LAUNCHP(PH_RESAMPLE, use_cluster_scan(ctx, Lk) ? launch_scan_cluster(rs, ctx->st) : launch_scan(rs, ctx->st));
         ProposeArgs pa{};
         pa.n = n; pa.H = H; pa.L = Ln; pa.Lsrc = Lk; pa.l0 = ctx->l0; pa.k = k; pa.mpcp = ctx->mpc_dev;
         pa.key0 = ctx->dsc.key0; pa.key1 = ctx->dsc.key1;
         pa.src[0] = ctx->ctrl[P][0]; pa.src[1] = ctx->ctrl[P][1];
         pa.surv = ctx->surv; pa.anc = nullptr; pa.C = ctx->C; pa.QR = ctx->QR;
-        if (two_level) { pa.Cs = ctx->Cs; pa.Cs_stride = cdf_samples(Lk); }
+        if (two_level && single) { pa.Cs = ctx->Cs; pa.Cs_stride = cdf_samples(Lk); }
         if (mp) {
             rs.anc = ctx->anc; rs.M = Ln; rs.splits = ctx->splits;
             LAUNCHP(PH_RESAMPLE, launch_ancestors(rs, ctx->st));
@@ -1020,17 +1105,27 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
         pa.lo3 = ctx->lohi; pa.hi3 = ctx->lohi + 3 * ctx->nmax;
         pa.reset_n = n; pa.reset_colmax = ctx->colmax; pa.reset_tiles = ctx->tiles; pa.reset_accept = ctx->accept;
         pa.reset_status = ctx->status; pa.reset_status_n = nt * n;
+        const int rowlen = n * H * 3;
         if (ctx->vworld > 1) {
-            // virtual ranks (test mode): the multi-GPU path with the exchange done in place
+            // virtual ranks (test mode): the multi-GPU path with the exchange done in place -- rank r's
+            // CDF, CDF samples and column totals in its slices of Call / Csall / Qall, its rows a row
+            // slice of this context's buffers (peer mode) or compacted into Sall (all-gather mode)
             const int G = ctx->vworld;
-            const int rowlen = n * H * 3;
+            const uint32_t css = cdf_samples(ctx->Lmax);
             const size_t ntv = (size_t)scan_tiles(ctx->Lmax);
+            MultiArgs ma{};
+            ma.Lg = ctx->Lg; ma.G = G; ma.Qall = ctx->Qall; ma.Qstride = (uint32_t)ctx->nmax;
+            ma.Cstride = ctx->Lmax; ma.Cs_stride = css; ma.Lmax = ctx->Lmax;
+            ma.prow = (size_t)(ctx->ctrl[P][1] - ctx->ctrl[P][0]);
+            ma.Sall = ctx->p2p ? nullptr : ctx->Sall;
             for (int r = 0; r < G; ++r) {
                 uint32_t b, e;
                 smc_shard_range(ctx->Lg, G, r, &b, &e);
                 ResampleArgs rr = rs;
                 rr.L = e - b; rr.ell = ctx->ell + b; rr.ell_stride = ctx->Lloc;
                 rr.C = ctx->Call + (size_t)r * n * ctx->Lmax; rr.Cstride = ctx->Lmax;
+                rr.Q = ctx->Qall + (size_t)r * ctx->nmax;
+                rr.Cs = two_level ? ctx->Csall + (size_t)r * n * css : nullptr; rr.Cs_stride = css;
                 CK(cudaMemsetAsync(ctx->status, 0, 8 * ntv * n, ctx->st));
                 CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
                 LAUNCHP(PH_RESAMPLE, launch_scan(rr, ctx->st));
@@ -1039,47 +1134,55 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
                                                                  ctx->ctrl[P][1] + (size_t)b * rowlen, ctx->surv + b, e - b,
                                                                  n, rowlen, ctx->Sall + (size_t)r * ctx->Lmax * rowlen,
                                                                  ctx->st));
+                ma.peer_C[r] = rr.C;
+                ma.peer_Cs[r] = rr.Cs;
+                ma.len[r] = e - b;
+                ma.peer_ctrl[r] = ctx->ctrl[P][0] + (size_t)b * rowlen;
+                ma.peer_surv[r] = ctx->surv + b;
             }
             for (int r = 0; r < G; ++r) {
                 uint32_t b, e;
                 smc_shard_range(ctx->Lg, G, r, &b, &e);
-                ProposeArgs pr = pa;
-                pr.L = e - b; pr.l0 = b;
-                pr.xp = ctx->ctrl[P ^ 1][0] + (size_t)b * rowlen; pr.xs = ctx->ctrl[P ^ 1][1] + (size_t)b * rowlen;
-                pr.reset_status_n = 0;
-                MultiArgs ma{pr, ctx->Lg, ctx->Lmax, G, ctx->Call, ctx->p2p ? nullptr : ctx->Sall, {}, {}, 0};
-                if (ctx->p2p) {
-                    // virtual rank q's buffers are the row slice [b_q, e_q) of this context's own
-                    ma.prow = (size_t)(ctx->ctrl[P][1] - ctx->ctrl[P][0]);
-                    for (int q = 0; q < G; ++q) {
-                        uint32_t bq, eq;
-                        smc_shard_range(ctx->Lg, G, q, &bq, &eq);
-                        ma.peer_ctrl[q] = ctx->ctrl[P][0] + (size_t)bq * rowlen;
-                        ma.peer_surv[q] = ctx->surv + bq;
-                    }
-                }
-                LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
+                MultiArgs mr = ma;
+                mr.p = pa;
+                mr.p.L = e - b; mr.p.l0 = b;
+                mr.p.xp = ctx->ctrl[P ^ 1][0] + (size_t)b * rowlen; mr.p.xs = ctx->ctrl[P ^ 1][1] + (size_t)b * rowlen;
+                mr.p.reset_status_n = 0;
+                LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(mr, ctx->st));
             }
             CK(cudaMemsetAsync(ctx->status, 0, 8 * nt * n, ctx->st));
             CK(cudaMemsetAsync(ctx->tiles, 0, 4 * n, ctx->st));
         } else if (ctx->world > 1) {
-            // exchange: per-rank CDFs and compacted survivor rows, then gather + propose
-            NCK(nccl_api()->AllGather(ctx->C, ctx->Call, (size_t)n * ctx->Lmax, ncclUint64_, ctx->comm, ctx->st));
-            MultiArgs ma{pa, ctx->Lg, ctx->Lmax, ctx->world, ctx->Call, nullptr, {}, {}, 0};
+            // exchange: all-gather of the per-rank column totals (N uint64 per
+            // rank); the owner's CDF is searched in place through the IPC mappings (peer mode), or the
+            // per-rank CDFs and compacted survivor rows are all-gathered (all-gather mode)
+            COLL(coll_allgather(ctx, ctx->Q, ctx->Qall, sizeof(unsigned long long) * ctx->nmax));
+            MultiArgs ma{};
+            ma.p = pa;
+            ma.Lg = ctx->Lg; ma.G = ctx->world; ma.Qall = ctx->Qall; ma.Qstride = (uint32_t)ctx->nmax;
+            ma.Cstride = ctx->Lmax; ma.Cs_stride = cdf_samples(ctx->Lmax); ma.Lmax = ctx->Lmax;
+            for (int r = 0; r < ctx->world; ++r) ma.len[r] = local_count(ctx->Lg, ctx->world, r);
             if (ctx->p2p) {
-                // parents read in place over NVLink: rank r's current pair and published masks
+                // parents read in place over NVLink: rank r's current pair, published masks and CDF
                 const size_t prow = (size_t)(ctx->ctrl[0][1] - ctx->ctrl[0][0]);
                 ma.prow = prow;
                 for (int r = 0; r < ctx->world; ++r) {
                     ma.peer_ctrl[r] = ctx->peer_ctrl[r] + (size_t)(2 * P) * prow;
                     ma.peer_surv[r] = ctx->peer_survp[r] + (size_t)(k & 1) * ctx->Lmax;
+                    ma.peer_C[r] = ctx->peer_C[r];
+                    ma.peer_Cs[r] = two_level ? ctx->peer_Cs[r] : nullptr;
                 }
             } else {
+                COLL(coll_allgather(ctx, ctx->C, ctx->Call, sizeof(unsigned long long) * n * ctx->Lmax));
                 LAUNCHP(PH_PROPOSE, launch_compact_survivors(ctx->ctrl[P][0], ctx->ctrl[P][1], ctx->surv, ctx->Lloc, n,
-                                                             n * H * 3, ctx->Sc, ctx->st));
-                NCK(nccl_api()->AllGather(ctx->Sc, ctx->Sall, (size_t)ctx->Lmax * n * H * 3, ncclFloat32_, ctx->comm,
-                                          ctx->st));
+                                                             rowlen, ctx->Sc, ctx->st));
+                COLL(coll_allgather(ctx, ctx->Sc, ctx->Sall, sizeof(float) * ctx->Lmax * rowlen));
                 ma.Sall = ctx->Sall;
+                ma.Cstride = ctx->Lmax;
+                for (int r = 0; r < ctx->world; ++r) {
+                    ma.peer_C[r] = ctx->Call + (size_t)r * n * ctx->Lmax;
+                    ma.peer_Cs[r] = nullptr;
+                }
             }
             LAUNCHP(PH_PROPOSE, launch_gather_propose_multi(ma, ctx->st));
         } else {
@@ -1151,11 +1254,40 @@ static smc_status select_best(smc_ctx *ctx) {
                   cand ? ctx->lam2 : nullptr, ctx->Leval ? ctx->Leval : ctx->Lloc};
     LAUNCH(launch_select(sa, ctx->st));
     if (ctx->world > 1) {                 // all-gather the per-rank records, merge on every rank
-        NCK(nccl_api()->AllGather(ctx->rec_local, ctx->rec_all, ctx->rec_bytes, ncclUint8_, ctx->comm, ctx->st));
+        COLL(coll_allgather(ctx, ctx->rec_local, ctx->rec_all, ctx->rec_bytes));
         LAUNCH(launch_select_merge(ctx->rec_all, ctx->world, ctx->rec_bytes, ctx->dsc.n * ctx->dsc.H * 3,
                                    ctx->rec_final, ctx->st));
     }
     return SMC_OK;
+}
+
+// SMC_EINFEASIBLE report: which aircraft has no nonzero weight in any particle
+// of the last evaluated round (column maxima of the survivor weights), and the first round in
+// which each such column was all zero (recorded by K4).  Synchronises; failure path only.
+static smc_status infeasible(smc_ctx *ctx, const char *what) {
+    const int n = ctx->dsc.n;
+    const uint32_t Lk = ctx->Leval ? ctx->Leval : ctx->Lloc;
+    uint32_t cm[32];
+    int32_t fr[32];
+    if (cudaMemsetAsync(ctx->infcol, 0, 4 * n, ctx->st) == cudaSuccess &&
+        launch_colmax(ctx->ell, n, Lk, ctx->infcol, ctx->st) == cudaSuccess &&
+        cudaMemcpyAsync(cm, ctx->infcol, 4 * n, cudaMemcpyDeviceToHost, ctx->st) == cudaSuccess &&
+        cudaMemcpyAsync(fr, ctx->inf_round, 4 * n, cudaMemcpyDeviceToHost, ctx->st) == cudaSuccess &&
+        cudaStreamSynchronize(ctx->st) == cudaSuccess) {
+        std::string msg;
+        char buf[96];
+        for (int i = 0; i < n; ++i)
+            if (cm[i] == 0u || cm[i] == 0x007FFFFFu) {      // ordered -inf (or nothing written)
+                snprintf(buf, sizeof buf, "%saircraft %d (index in the scenario) zero in every particle", msg.empty() ? "" : "; ", i);
+                msg += buf;
+                if (fr[i] >= 0) { snprintf(buf, sizeof buf, " since round %d", fr[i]); msg += buf; }
+                else { snprintf(buf, sizeof buf, " in the last round %u", ctx->k ? ctx->k - 1 : 0); msg += buf; }
+            }
+        if (msg.empty()) msg = "no single aircraft is zero everywhere, but every particle has a zero-weight aircraft";
+        return fail(ctx, SMC_EINFEASIBLE, "%s: every particle has a zero weight (P:423): %s", what, msg.c_str());
+    }
+    cudaGetLastError();
+    return fail(ctx, SMC_EINFEASIBLE, "%s: every particle has a zero weight (P:423)", what);
 }
 
 extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *lambda, int64_t *particle) {
@@ -1172,7 +1304,7 @@ extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *
     CK(cudaStreamSynchronize(ctx->st));
     if (lambda) *lambda = bl;
     if (particle) *particle = bi;
-    if (bi < 0) return fail(ctx, SMC_EINFEASIBLE, "every particle has a zero weight (P:423)");
+    if (bi < 0) return infeasible(ctx, "selection");
     return SMC_OK;
 }
 
@@ -1268,7 +1400,11 @@ extern "C" smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_cont
     const uint32_t m = ctx->mpc;
     ctx->mpc += 1;
     ctx->mpc_dirty = true;
-    if (bi < 0) return fail(ctx, SMC_EINFEASIBLE, "MPC step %u: every particle has a zero weight (P:423)", m);
+    if (bi < 0) {
+        char what[48];
+        snprintf(what, sizeof what, "MPC step %u", m);
+        return infeasible(ctx, what);
+    }
     return SMC_OK;
 }
 

@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const ResampleArgs r, int
                 r.Cs[(size_t)i * r.Cs_stride + l / kCdfSample] = pre + inc[it];
         }
     }
+    if (inf && tile == 0 && threadIdx.x == 0 && r.inf_round) atomicCAS(&r.inf_round[i], -1, (int)r.k);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const uint64_t Q = s_pre + agg;
         const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
@@ -373,6 +374,7 @@ k_scan_cluster(const ResampleArgs r) {
             r.Cs[(size_t)i * r.Cs_stride + l / kCdfSample] = v;
     }
     if (rank == 0 && threadIdx.x == 0) {
+        if (inf && r.inf_round) atomicCAS(&r.inf_round[i], -1, (int)r.k);
         const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, r.k, *r.mpcp, r.key0, r.key1);
         r.QR[2 * i] = Q;
         r.QR[2 * i + 1] = __umul64hi(rw, Q);                  // R = floor(r64 Q / 2^64)
@@ -385,11 +387,10 @@ bool cluster_scan_fits(uint32_t L) { return L >= 1 && L <= kClusterScanMax; }
 cudaError_t launch_scan_cluster(const ResampleArgs &r, cudaStream_t st) {
     const uint32_t seg = (((r.L + kClusterCtas - 1) / kClusterCtas) + 7u) & ~7u;
     const size_t smem = (size_t)seg * sizeof(unsigned long long);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_scan_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kClusterSeg * sizeof(unsigned long long)));
-        attr = true;
+    if (smem > 48 * 1024) {   // per device and cheap: set on every launch that needs it, checked
+        const cudaError_t e = cudaFuncSetAttribute(k_scan_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(kClusterSeg * sizeof(unsigned long long)));
+        if (e != cudaSuccess) return e;
     }
     k_scan_cluster<<<dim3(kClusterCtas, r.n), kScanThreads, smem, st>>>(r);
     return cudaGetLastError();
@@ -595,14 +596,58 @@ __device__ __forceinline__ void reset_round_state(const ProposeArgs &p) {
 #endif
 constexpr int kRowsPerBlock = SMC_K6_ROWS;   // = blockDim: every thread runs one bisection in phase 1
 
+// Phase 2 of K6 for the block's rows q0 .. q0 + kRowsPerBlock - 1: copy each parent's control
+// triples (s_src[r] + 3 t) to x' and write the Gaussian proposal x* (P:221).  Batches of
+// kBatch elements per thread: all parent loads (read-only path) are issued before any store, so
+// their latencies overlap.
+__device__ __forceinline__ void propose_rows(const ProposeArgs &p, const float *const *s_src, const uint32_t *s_j,
+                                             const uint32_t *s_perturb_x2, uint32_t q0, uint32_t rows, uint32_t mpc,
+                                             uint32_t invH) {
+    const int H = p.H;
+    const int tot = (int)(min((uint32_t)kRowsPerBlock, rows - q0) * (uint32_t)H);
+    float *const xp = p.xp + (size_t)q0 * H * 3, *const xs = p.xs + (size_t)q0 * H * 3;
+    constexpr int kBatch = SMC_K6_BATCH;
+    for (int e0 = 0; e0 < tot; e0 += kBatch * (int)blockDim.x) {
+        float cv[kBatch][3];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            if (e < tot) {
+                const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
+                const float *src = s_src[r] + 3 * t;
+                cv[u][0] = __ldg(src); cv[u][1] = __ldg(src + 1); cv[u][2] = __ldg(src + 2);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            if (e >= tot) break;
+            const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
+            const uint32_t x2 = s_perturb_x2[r];
+            const float c0 = cv[u][0], c1 = cv[u][1], c2 = cv[u][2];
+            xp[3 * e] = c0; xp[3 * e + 1] = c1; xp[3 * e + 2] = c2;
+            const uint4 w = draw_ks(TAG_PERTURB, p.l0 + s_j[r], p.k << 16, (uint32_t)t | x2, mpc, p.ks);
+            const float4 z = box_muller4(w);
+            float o0 = fmaf(p.sig[0], z.x, c0), o1 = fmaf(p.sig[1], z.y, c1), o2 = fmaf(p.sig[2], z.z, c2);
+            if (p.clamp) {
+                const int i = (int)(x2 >> 8);
+                const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
+                o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
+                o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
+                o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
+            }
+            xs[3 * e] = o0; xs[3 * e + 1] = o1; xs[3 * e + 2] = o2;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kRowsPerBlock) k_gather_propose(const ProposeArgs p) {
     __shared__ const float *s_src[kRowsPerBlock];
     __shared__ uint32_t s_j[kRowsPerBlock];
     __shared__ uint32_t s_perturb_x2[kRowsPerBlock];     // (i << 8): the aircraft part of the PERTURB counter
     const uint32_t rows = p.L * (uint32_t)p.n;            // < 2^31 (smc_init bounds L n)
     const uint32_t mpc = *p.mpcp;
-    const int H = p.H;
-    const uint32_t invH = 0xFFFFFFFFu / (uint32_t)H + 1u;    // e / H = umulhi(e, invH) for e < 2^32 / H^2
+    const uint32_t invH = 0xFFFFFFFFu / (uint32_t)p.H + 1u;  // e / H = umulhi(e, invH) for e < 2^32 / H^2
     for (uint32_t q0 = blockIdx.x * kRowsPerBlock; q0 < rows; q0 += gridDim.x * kRowsPerBlock) {
         {
             const uint32_t q = q0 + threadIdx.x;
@@ -619,50 +664,14 @@ __global__ void __launch_bounds__(kRowsPerBlock) k_gather_propose(const ProposeA
                                               Q, R, j)
                              : find_ancestor(p.C + (size_t)i * p.Lsrc, p.Lsrc, p.L, Q, R, j);
                 }
-                src = p.src[(__ldg(&p.surv[a]) >> i) & 1u] + ((size_t)a * p.n + i) * H * 3;
+                src = p.src[(__ldg(&p.surv[a]) >> i) & 1u] + ((size_t)a * p.n + i) * p.H * 3;
                 s_j[threadIdx.x] = j;
                 s_perturb_x2[threadIdx.x] = (uint32_t)i << 8;
             }
             s_src[threadIdx.x] = src;
         }
         __syncthreads();
-        const int tot = (int)(min((uint32_t)kRowsPerBlock, rows - q0) * (uint32_t)H);
-        float *const xp = p.xp + (size_t)q0 * H * 3, *const xs = p.xs + (size_t)q0 * H * 3;
-        // batches of kBatch elements per thread: all parent loads (read-only path) are issued
-        // before any store, so their latencies overlap
-        constexpr int kBatch = SMC_K6_BATCH;
-        for (int e0 = 0; e0 < tot; e0 += kBatch * (int)blockDim.x) {
-            float cv[kBatch][3];
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
-                if (e < tot) {
-                    const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
-                    const float *src = s_src[r] + 3 * t;
-                    cv[u][0] = __ldg(src); cv[u][1] = __ldg(src + 1); cv[u][2] = __ldg(src + 2);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
-                if (e >= tot) break;
-                const int r = (int)__umulhi((uint32_t)e, invH), t = e - r * H;
-                const uint32_t x2 = s_perturb_x2[r];
-                const float c0 = cv[u][0], c1 = cv[u][1], c2 = cv[u][2];
-                xp[3 * e] = c0; xp[3 * e + 1] = c1; xp[3 * e + 2] = c2;
-                const uint4 w = draw_ks(TAG_PERTURB, p.l0 + s_j[r], p.k << 16, (uint32_t)t | x2, mpc, p.ks);
-                const float4 z = box_muller4(w);
-                float o0 = fmaf(p.sig[0], z.x, c0), o1 = fmaf(p.sig[1], z.y, c1), o2 = fmaf(p.sig[2], z.z, c2);
-                if (p.clamp) {
-                    const int i = (int)(x2 >> 8);
-                    const float *lo = p.lo3 + 3 * i, *hi = p.hi3 + 3 * i;
-                    o0 = fminf(fmaxf(o0, lo[0]), hi[0]);
-                    o1 = fminf(fmaxf(o1, lo[1]), hi[1]);
-                    o2 = fminf(fmaxf(o2, lo[2]), hi[2]);
-                }
-                xs[3 * e] = o0; xs[3 * e + 1] = o1; xs[3 * e + 2] = o2;
-            }
-        }
+        propose_rows(p, s_src, s_j, s_perturb_x2, q0, rows, mpc, invH);
         __syncthreads();
     }
     reset_round_state(p);
@@ -963,10 +972,7 @@ cudaError_t launch_colmax(const float *ell, int n, uint32_t L, uint32_t *colmax,
 
 namespace smc {
 // ============================================================== multi-GPU (R43)
-// Particle sharding: rank r owns global particles [L r / G, L (r+1) / G).
-__host__ __device__ static inline uint32_t shard_begin(uint32_t L, int G, int r) {
-    return (uint32_t)((uint64_t)L * (uint64_t)r / (uint64_t)G);
-}
+// Particle sharding: rank r owns global particles [L r / G, L (r+1) / G) (smc_shard_range).
 
 // Compact this rank's survivor rows (x' or x* per survivor flag) for the all-gather.
 __global__ void k_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
@@ -990,75 +996,93 @@ cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uin
     return cudaGetLastError();
 }
 
-// Gather + propose for this rank's new particles from the all-gathered
-// per-rank CDFs Call[G][n][Lmax] (local inclusive sums) and the parents'
-// survivor rows -- read in place from their owner (peer mode) or from the
-// all-gathered compacted rows Sall[G][Lmax][n][H][3].  Global CDF = rank offset
-// + local CDF, so the ancestors equal the single-GPU ones bit for bit (G-invariance).
-__global__ void k_gather_propose_multi(const MultiArgs m) {
+// Gather + propose for this rank's new particles, on K6's two-phase
+// structure.  Every rank holds only its own inclusive CDF; the ranks' column totals Q_r were
+// all-gathered (Qall), so slot j's target t_j = floor((j Q + R) / L) on the global total
+// Q = sum_r Q_r names its owner rho (the rank whose cumulative offset range holds t_j) and
+// the owner-local target t_j - off_rho.  Phase 1 searches the owner's CDF in place -- two-
+// level through its every-16th samples, over NVLink through CUDA IPC mappings (peer mode), in
+// the all-gathered CDFs (all-gather mode) or in slices of one buffer (virtual ranks) -- and
+// points at the parent's survivor row where its owner keeps it (x' or x* by the published
+// mask bit) or in the all-gathered compacted rows.  Phase 2 is K6's (copy + proposal).  The
+// ancestors equal the single-GPU ones bit for bit: the global CDF is the concatenation of the
+// per-rank CDFs shifted by the rank offsets (G-invariance).
+__device__ __forceinline__ uint32_t first_above_t(const unsigned long long *C, const unsigned long long *Cs,
+                                                 uint32_t L, uint64_t tj) {
+    if (Cs) {
+        const uint32_t g = first_above<SMC_K6_ARY>(Cs, 0, cdf_samples(L) - 1, tj);
+        const uint32_t a = g * kCdfSample, b = min(a + kCdfSample, L) - 1;
+        return first_above<SMC_K6_ARY>(C, a, b, tj);
+    }
+    return first_above<2>(C, 0, L - 1, tj);
+}
+
+__global__ void __launch_bounds__(kRowsPerBlock) k_gather_propose_multi(const MultiArgs m) {
     const ProposeArgs &p = m.p;
-    const size_t total = (size_t)p.L * p.n;
+    __shared__ const float *s_src[kRowsPerBlock];
+    __shared__ uint32_t s_j[kRowsPerBlock];
+    __shared__ uint32_t s_perturb_x2[kRowsPerBlock];
+    __shared__ uint64_t s_qd[kMaxAc], s_qm[kMaxAc], s_R[kMaxAc], s_off[kMaxAc][9];
     const uint32_t mpc = *p.mpcp;
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx % p.n);
-        const uint32_t jl = (uint32_t)(idx / p.n);
-        const uint32_t j = p.l0 + jl;
-        uint64_t Qr[8], Q = 0;
+    const int n = p.n;
+    if (threadIdx.x < (unsigned)n) {                       // per column: global total, offset R, rank offsets
+        const int i = threadIdx.x;
+        uint64_t Q = 0;
         for (int r = 0; r < m.G; ++r) {
-            const uint32_t len = shard_begin(m.Lg, m.G, r + 1) - shard_begin(m.Lg, m.G, r);
-            Qr[r] = len ? m.Call[((size_t)r * p.n + i) * m.Lmax + len - 1] : 0ull;
-            Q += Qr[r];
+            s_off[i][r] = Q;
+            Q += m.Qall[(size_t)r * m.Qstride + i];
         }
+        s_off[i][m.G] = Q;
         const uint64_t rw = r64(TAG_RESAMPLE, (uint32_t)i, p.k, mpc, p.key0, p.key1);
-        const uint64_t R = __umul64hi(rw, Q);
-        const uint64_t t = slot_t(j, Q / m.Lg, Q % m.Lg, R, m.Lg);
-        int rho = 0;
-        uint64_t off = 0;
-        while (rho < m.G - 1 && t >= off + Qr[rho]) { off += Qr[rho]; ++rho; }
-        const uint32_t len = shard_begin(m.Lg, m.G, rho + 1) - shard_begin(m.Lg, m.G, rho);
-        const unsigned long long *C = m.Call + ((size_t)rho * p.n + i) * m.Lmax;
-        const uint64_t tl = t - off;
-        uint32_t lo = 0, hi = len - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(&C[mid]) > tl) hi = mid; else lo = mid + 1;
-        }
-        const float *src;
-        if (m.Sall) {
-            src = m.Sall + (((size_t)rho * m.Lmax + lo) * p.n + i) * p.H * 3;
-        } else {
-            // the parent's survivor row where its owner keeps it: x' or x* by its mask bit
-            const uint32_t bit = (__ldg(&m.peer_surv[rho][lo]) >> i) & 1u;
-            src = m.peer_ctrl[rho] + bit * m.prow + ((size_t)lo * p.n + i) * p.H * 3;
-        }
-        float *dp = p.xp + idx * p.H * 3;
-        float *ds = p.xs + idx * p.H * 3;
-        const float *lo3 = p.lo3 + 3 * i, *hi3 = p.hi3 + 3 * i;
-        for (int tt = 0; tt < p.H; ++tt) {
-            const float c0 = src[3 * tt], c1 = src[3 * tt + 1], c2 = src[3 * tt + 2];
-            dp[3 * tt] = c0; dp[3 * tt + 1] = c1; dp[3 * tt + 2] = c2;
-            const uint4 w = draw(TAG_PERTURB, j, p.k << 16, (uint32_t)tt | ((uint32_t)i << 8), mpc, p.key0, p.key1);
-            const float2 z01 = box_muller(w.x, w.y);
-            const float2 z23 = box_muller(w.z, w.w);
-            float o0 = fmaf(p.sig[0], z01.x, c0), o1 = fmaf(p.sig[1], z01.y, c1), o2 = fmaf(p.sig[2], z23.x, c2);
-            if (p.clamp) {
-                o0 = fminf(fmaxf(o0, lo3[0]), hi3[0]);
-                o1 = fminf(fmaxf(o1, lo3[1]), hi3[1]);
-                o2 = fminf(fmaxf(o2, lo3[2]), hi3[2]);
+        s_R[i] = __umul64hi(rw, Q);
+        s_qd[i] = Q / m.Lg;
+        s_qm[i] = Q % m.Lg;
+    }
+    __syncthreads();
+    const uint32_t rows = p.L * (uint32_t)n;
+    const uint32_t invH = 0xFFFFFFFFu / (uint32_t)p.H + 1u;
+    for (uint32_t q0 = blockIdx.x * kRowsPerBlock; q0 < rows; q0 += gridDim.x * kRowsPerBlock) {
+        {
+            const uint32_t q = q0 + threadIdx.x;
+            const float *src = nullptr;
+            if (q < rows) {
+                const uint32_t jl = q / (uint32_t)n;
+                const int i = (int)(q - jl * (uint32_t)n);
+                const uint64_t t = slot_t(p.l0 + jl, s_qd[i], s_qm[i], s_R[i], m.Lg);
+                int rho = 0;
+                while (rho < m.G - 1 && t >= s_off[i][rho + 1]) ++rho;
+                const uint64_t tl = t - s_off[i][rho];
+                const unsigned long long *Cs = m.peer_Cs[rho] ? m.peer_Cs[rho] + (size_t)i * m.Cs_stride : nullptr;
+                const uint32_t a = first_above_t(m.peer_C[rho] + (size_t)i * m.Cstride, Cs, m.len[rho], tl);
+                if (m.Sall) {
+                    src = m.Sall + (((size_t)rho * m.Lmax + a) * n + i) * p.H * 3;
+                } else {
+                    const uint32_t bit = (__ldg(&m.peer_surv[rho][a]) >> i) & 1u;
+                    src = m.peer_ctrl[rho] + bit * m.prow + ((size_t)a * n + i) * p.H * 3;
+                }
+                s_j[threadIdx.x] = jl;
+                s_perturb_x2[threadIdx.x] = (uint32_t)i << 8;
             }
-            ds[3 * tt] = o0; ds[3 * tt + 1] = o1; ds[3 * tt + 2] = o2;
+            s_src[threadIdx.x] = src;
         }
+        __syncthreads();
+        propose_rows(p, s_src, s_j, s_perturb_x2, q0, rows, mpc, invH);
+        __syncthreads();
     }
     reset_round_state(p);
 }
 
-cudaError_t launch_gather_propose_multi(const MultiArgs &m, cudaStream_t st) {
-    const size_t total = (size_t)m.p.L * m.p.n;
-    if (!total) return cudaSuccess;
-    size_t g = (total + 127) / 128;
-    if (g > 148 * 32) g = 148 * 32;
-    k_gather_propose_multi<<<(unsigned)g, 128, 0, st>>>(m);
+cudaError_t launch_gather_propose_multi(const MultiArgs &m0, cudaStream_t st) {
+    const size_t rows = (size_t)m0.p.L * m0.p.n;
+    if (!rows) return cudaSuccess;
+    MultiArgs m = m0;
+    for (int r = 0; r < 10; ++r) {
+        m.p.ks[2 * r] = m.p.key0 + (uint32_t)r * 0x9E3779B9u;
+        m.p.ks[2 * r + 1] = m.p.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    size_t g = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
+    if (g > 148 * 16 * 256 / kRowsPerBlock) g = 148 * 16 * 256 / kRowsPerBlock;
+    k_gather_propose_multi<<<(unsigned)g, kRowsPerBlock, 0, st>>>(m);
     return cudaGetLastError();
 }
 

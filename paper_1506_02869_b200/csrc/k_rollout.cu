@@ -453,7 +453,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                 gxb = fmaf(sc.turb_sigma, ggb.x, gxb);
                 gyb = fmaf(sc.turb_sigma, ggb.y, gyb);
             }
-            const float c0x = (DENSE || SP) ? gx : Wn[0] + gx, c0y = (DENSE || SP) ? gy : Wn[8] + gy;   // nominal + gust (+ c0)
+            float c0x = gx, c0y = gy;                                   // nominal + gust (+ c0)
+            if constexpr (!DENSE && !SP) { c0x += Wn[0]; c0y += Wn[8]; }
             const float2 *const sW2 = reinterpret_cast<const float2 *>(&s_W[seg * 32]);   // SP: [k](slot a, slot b)
 
             // ---------------- 2-3. dynamics, unary checks and geometry, both candidates at once
@@ -549,8 +550,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const float zc = cget(nz, c), vc = cget(nv, c);
-                const bool bad = ((cbad[c] >> t) & 1u) || !(zc >= zmin && zc <= zmax) || !(vc >= vmin && vc <= vmax) ||
-                                 !(cget(nm, c) >= mempty);
+                // unordered compares (a NaN fails every bound), OR-ed without short-circuit branches
+                const bool bad = (((cbad[c] >> t) & 1u) != 0u) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) |
+                                 !(vc <= vmax) | !(cget(nm, c) >= mempty);
                 // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
                 vnowm |= (bad ? 1 : 0) << c;
             }
@@ -570,8 +572,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             int lnowm = 0;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const bool ln = cget(rh, c) <= sc.P_runway && cget(beta, c) <= sc.P_beta && cget(at, c) <= sc.P_chi &&
-                                fabsf(cget(hdw, c)) <= sc.P_chi && cget(nv, c) <= sc.P_vs;
+                const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta, c) <= sc.P_beta) & (cget(at, c) <= sc.P_chi) &
+                                (fabsf(cget(hdw, c)) <= sc.P_chi) & (cget(nv, c) <= sc.P_vs);
                 lnowm |= (ln ? 1 : 0) << c;
             }
             if (kind != 0) lnowm = 0;                            // only arrivals land (Eq. TO_init)
@@ -598,7 +600,12 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             // ---------------- 4. separation (Eq. avoidance), each unordered pair once:
             // lane checks partner lane+d (d = 1..R/2) and hands the verdict to that
             // partner with a segment-wide shuffle (for d = R/2, R even, both lanes check).
-            int confm = 0;
+            // A pair conflicts iff d^2 < (2P_r)^2 and |dz| < 2P_h, i.e. iff u = d^2 - (2P_r)^2 and
+            // w = |dz| - 2P_h are both negative: the verdict is the sign bit of bits(u) & bits(w)
+            // (equality gives +0: separated; a NaN or infinite coordinate gives a
+            // non-negative u or w: no conflict).  Candidate c's verdict sits in bit 31 - 8c of the
+            // word that is OR-ed over the partners and shuffled to them.
+            uint32_t confw = 0u;
 #pragma unroll
             for (int d = 1; d <= R / 2; ++d) {
                 V dx, dy, dz;
@@ -611,17 +618,22 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     const float4 q = s_pxy[pb + d];
                     dx = px - q.x; dy = ny - q.y; dz = nz - q.z;
                 }
-                const V d2 = vfma(dx, dx, dy * dy);
-                int hits = 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    hits |= ((cget(d2, c) < sc.twoPr2) && (fabsf(cget(dz, c)) < sc.twoPh) ? 1 : 0) << c;
-                confm |= hits;
+                const V u = vfma(dx, dx, vfma(dy, dy, -sc.twoPr2));
+                const V w = vabs(dz) - sc.twoPh;
+                uint32_t hv;
+                if constexpr (NC == 2)       // byte 3 of each candidate's word: bits 31 (c = 0) and 23 (c = 1)
+                    hv = __byte_perm(__float_as_uint(u.x) & __float_as_uint(w.x),
+                                     __float_as_uint(u.y) & __float_as_uint(w.y), 0x3700);
+                else
+                    hv = __float_as_uint(u) & __float_as_uint(w);
                 // one shuffle hands both candidates' verdicts to the partner, from lane - d (mod R);
                 // lanes >= R (R < W) compute ignored verdicts
                 if (2 * d < R)
-                    confm |= __shfl_sync(0xffffffffu, hits, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
+                    confw |= hv | __shfl_sync(0xffffffffu, hv, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
+                else
+                    confw |= hv;
             }
+            const int confm = NC == 2 ? (int)((confw >> 31) | ((confw >> 22) & 2u)) : (int)(confw >> 31);
             // ---------------- 5. per-step cost terms at j = t+1 (frozen aircraft add 0), state update
             // departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
             // arrival:   D = |wrap(chi - chi_hat)|, chi_hat = pi + 2 theta (R8); E = |beta - beta_f|

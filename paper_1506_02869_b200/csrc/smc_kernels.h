@@ -76,6 +76,7 @@ struct ResampleArgs {
     uint32_t *splits;           // [n][mp_split_words(L, M)] K5 merge-path split points
     unsigned long long *Cs;     // [n][Cs_stride] every kCdfSample-th inclusive prefix (nullable):
     uint32_t Cs_stride;         //   Cs[g] = C[min(16 g + 15, L - 1)], for K6's two-level search
+    int32_t *inf_round;         // [n] first round whose column had no nonzero weight (-1: none; nullable)
 };
 constexpr int kCdfSample = 16;
 __host__ __device__ inline uint32_t cdf_samples(uint32_t L) { return (L + kCdfSample - 1) / kCdfSample; }
@@ -118,18 +119,23 @@ cudaError_t launch_gather_propose(const ProposeArgs &p, cudaStream_t st);
 
 // Multi-GPU gather + propose
 struct MultiArgs {
-    ProposeArgs p;              // p.L = local particles, p.l0 = global offset
-    uint32_t Lg, Lmax;          // global particles, per-rank stride
+    ProposeArgs p;              // p.L = local new particles, p.l0 = global offset of this rank
+    uint32_t Lg;                // global particles
     int G;                      // ranks (<= 8)
-    const unsigned long long *Call;   // [G][n][Lmax] per-rank inclusive CDFs
-    const float *Sall;          // [G][Lmax][n][H][3] per-rank survivor rows (all-gather mode)
-    // peer mode (Sall == NULL): parent rows read in place from the owning rank's population
-    // buffers -- over NVLink through CUDA IPC mappings, or slices of one buffer (virtual ranks).
-    // Rank r's survivor pair is peer_ctrl[r] + c * prow (c = 0: x', 1: x*, rows [Lmax][n][H][3]);
-    // its survivor masks peer_surv[r][0, Lmax).
+    const unsigned long long *Qall;     // [G][Qstride] per-rank column totals (all-gathered)
+    uint32_t Qstride;
+    // rank r's local inclusive CDF [n][Cstride] and its every-16th samples [n][Cs_stride]
+    // (NULL: plain bisection) -- NVLink peer mappings, all-gathered copies or buffer slices
+    const unsigned long long *peer_C[8], *peer_Cs[8];
+    uint32_t Cstride, Cs_stride;
+    uint32_t len[8];            // particles of rank r
+    // parents' survivor rows: rank r's pair at peer_ctrl[r] (+ prow: x*), masks peer_surv[r]
+    // (peer mode), or the all-gathered compacted rows Sall [G][Lmax][n][H][3] (all-gather mode)
     const float *peer_ctrl[8];
     const uint32_t *peer_surv[8];
-    size_t prow;                // floats between x' and x* of one pair
+    size_t prow;
+    const float *Sall;
+    uint32_t Lmax;
 };
 cudaError_t launch_compact_survivors(const float *xp, const float *xs, const uint32_t *surv, uint32_t Lloc, int n,
                                      int rowlen, float *out, cudaStream_t st);

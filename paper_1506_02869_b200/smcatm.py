@@ -83,8 +83,49 @@ class Config(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("stream", C.c_void_p), ("max_aircraft", C.c_uint32), ("max_horizon", C.c_uint32),
         ("use_graph", C.c_uint32), ("profile", C.c_uint32), ("virtual_world", C.c_uint32),
-        ("n_particles_final", C.c_uint32), ("warm_fraction", C.c_double),
+        ("n_particles_final", C.c_uint32), ("warm_fraction", C.c_double), ("host_coll", C.c_void_p),
     ]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint32), C.c_size_t)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class HostCollectives(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_max_u32", ALLREDUCE_FN), ("allgather", ALLGATHER_FN)]
+
+
+def gloo_host_collectives(world: int, rank: int):
+    """smc_host_collectives over the default torch.distributed process group (CPU / gloo):
+    a test shim for world_size > 1 contexts without NCCL (include/smcatm.h).  Returns the
+    structure and the callback objects that must stay alive with it."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(user, buf, count):
+        try:
+            a = np.ctypeslib.as_array(buf, shape=(count,))
+            t = torch.from_numpy(a.astype(np.int64))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            a[:] = t.numpy().astype(np.uint32)
+            return 0
+        except Exception:
+            return 1
+
+    def allgather(user, send, recv, nbytes):
+        try:
+            src = np.frombuffer((C.c_char * nbytes).from_address(send), dtype=np.uint8).copy()
+            out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(out, torch.from_numpy(src))
+            for r in range(world):
+                C.memmove(recv + r * nbytes, out[r].numpy().ctypes.data, nbytes)
+            return 0
+        except Exception:
+            return 1
+
+    fa, fg = ALLREDUCE_FN(allreduce), ALLGATHER_FN(allgather)
+    hc = HostCollectives(None, fa, fg)
+    return hc, (fa, fg)
 
 
 class RoundStats(C.Structure):
@@ -212,7 +253,8 @@ class Solver:
                  mh: int = 1, sched_paper: bool = False, clamp: bool = False, device: int = 0,
                  max_aircraft: int | None = None, max_horizon: int | None = None, stream=None,
                  rank: int = 0, world_size: int = 1, use_graph: bool = False, profile: bool = False,
-                 virtual_world: int = 0, L_final: int = 0, warm_fraction: float = 0.0):
+                 virtual_world: int = 0, L_final: int = 0, warm_fraction: float = 0.0,
+                 host_collectives: bool = False):
         import torch
         self.lib = load()
         self.torch = torch
@@ -234,7 +276,11 @@ class Solver:
         cfg.n_particles_final = int(L_final)
         cfg.warm_fraction = float(warm_fraction)
         cfg.stream = C.c_void_p(self.stream.cuda_stream)
-        if world_size > 1:
+        if world_size > 1 and host_collectives:
+            # test shim: collectives over the CPU process group (no NCCL; e.g. ranks sharing a GPU)
+            self._hc, self._hc_keep = gloo_host_collectives(world_size, rank)
+            cfg.host_coll = C.cast(C.pointer(self._hc), C.c_void_p)
+        elif world_size > 1:
             # rank 0 creates the NCCL id; torch.distributed (any backend) shares it
             import torch.distributed as dist
             buf = (C.c_char * 128)()

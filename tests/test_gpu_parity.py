@@ -822,3 +822,22 @@ def test_peer_mapping_ipc(smc, tmp_path):
     subprocess.run([sys.executable, "-c", code], check=True, timeout=300)
     assert out.read_bytes() == pop["cur"].tobytes()
     sol.close()
+
+
+def test_infeasible_report_names_aircraft_and_round(smc):
+    """SMC_EINFEASIBLE names the aircraft that is zero in every particle and
+    the first round its column was all zero: aircraft 1 starts below its empty mass, so the
+    mass bound fails at every step of every particle from round 0 on."""
+    scn, cfg = sc.config(2)
+    scn["x0"][1, 5] = scn["m_empty"][1] - 10.0
+    sol = _solver(smc, scn, L=2048, S=2, K=3, seed=cfg.seed)
+    sol.iterate(3)
+    with pytest.raises(smc.SmcError) as e:
+        sol.best_controls()
+    msg = str(e.value)
+    assert "SMC_EINFEASIBLE" in msg and "aircraft 1 " in msg and "since round 0" in msg, msg
+    assert "aircraft 0 " not in msg
+    with pytest.raises(smc.SmcError) as e2:
+        sol.mpc_step(scn["x0"])
+    assert "MPC step 0" in str(e2.value) and "aircraft 1 " in str(e2.value), str(e2.value)
+    sol.close()
