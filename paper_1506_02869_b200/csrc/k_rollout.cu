@@ -54,9 +54,18 @@ __device__ __forceinline__ float clamp01(float v) { return fminf(fmaxf(v, 0.0f),
 
 // a - 2 pi rint(a / 2 pi) by FRND per candidate.  (The magic-number form -- one packed FMA
 // adding 1.5 * 2^23, one packed subtract -- measured slower on B200: 28.62 vs 28.13 ms of K2.)
+#ifndef SMC_K2_WRAPMAGIC
+#define SMC_K2_WRAPMAGIC 0
+#endif
 template <class V>
 __device__ __forceinline__ V wrap_pi(V a) {
+#if SMC_K2_WRAPMAGIC
+    // rint(a / 2 pi) on the FMA pipe: adding 1.5 * 2^23 rounds to an integer (|a| < 2^22 pi)
+    const V k = vfma(a, 1.0f / kTwoPi, 12582912.0f) - 12582912.0f;
+    return vfma(k, -kTwoPi, a);
+#else
     return vfma(vmap(a * (1.0f / kTwoPi), [](float u) { return rintf(u); }), -kTwoPi, a);
+#endif
 }
 
 // popdense bilinear lookup on the 1 km grid, clamped at its edge.
@@ -100,7 +109,7 @@ __device__ __forceinline__ V fast_atan2(V y, V x) {
         cset(mx, c, fmaxf(cget(ax, c), cget(ay, c)));
         cset(mn, c, fminf(cget(ax, c), cget(ay, c)));
     }
-    const V a = mn * vmap(mx, [](float u) { return u > 0.0f ? rcp_approx(u) : 0.0f; });
+    const V a = mn * vmap(mx, [](float u) { return rcp_approx(fmaxf(u, 1e-30f)); });   // mx = 0 -> mn = 0 -> a = 0
     const V s = a * a;
     V p = vfma(s, -0.0040731243789196014f, 0.021945973858237267f);
     p = vfma(p, s, -0.056062303483486176f);
@@ -133,7 +142,7 @@ __device__ __forceinline__ V fast_atan2_xpos(V y, V x) {
         cset(mx, c, fmaxf(cget(ax, c), cget(ay, c)));
         cset(mn, c, fminf(cget(ax, c), cget(ay, c)));
     }
-    const V a = mn * vmap(mx, [](float u) { return u > 0.0f ? rcp_approx(u) : 0.0f; });
+    const V a = mn * vmap(mx, [](float u) { return rcp_approx(fmaxf(u, 1e-30f)); });   // mx = 0 -> mn = 0 -> a = 0
     const V s = a * a;
     V p = vfma(s, -0.0040731243789196014f, 0.021945973858237267f);
     p = vfma(p, s, -0.056062303483486176f);
@@ -385,11 +394,15 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             // AR(1) and W = Cq Z with both components of a node packed in one float2:
             // lane owns (node, slot) pair lane + q W (q < ENS; node = pair & 7, slot = pair >> 3);
             // Z is kept node-major [slot][node](x, y) in shared memory
+            // (segments wider than the 8 NSL pairs: every lane computes pair lane mod 8 NSL -- the
+            // duplicates store identical values -- so no lane branches around the work)
             float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16 * NSL);
+            constexpr bool FULL = W >= 8 * NSL;
 #pragma unroll
             for (int q = 0; q < ENS; ++q) {
-                const int pq = lane + q * W, node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
-                if (pq < 8 * NSL) {
+                const int pq = FULL ? (lane & (8 * NSL - 1)) : lane + q * W;
+                const int node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
+                if (FULL || pq < 8 * NSL) {
                     const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
                     const float2 ve = make_float2(vv[node], vv[8 + node]);
                     Zr[q] = (t == 0) ? ve : vfma(Zr[q], sc.a, ve * sc.b);
@@ -399,8 +412,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < ENS; ++q) {
-                const int pq = lane + q * W, node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
-                if (pq < 8 * NSL) {
+                const int pq = FULL ? (lane & (8 * NSL - 1)) : lane + q * W;
+                const int node = SP ? (pq & 7) : pq, sl = SP ? (pq >> 3) : 0;
+                if (FULL || pq < 8 * NSL) {
                     const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
                     const float *qr = (W >= 8) ? qrow : &s_Q[node * 9];
                     float2 acc = make_float2(0.0f, 0.0f);
@@ -562,10 +576,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const V r2 = vfma(nx, nx, ny * ny);
             const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
             const V at = vabs(th);
-            V sarc;
+            const V sfull = (r2 * at) * vmap(ny, [](float a) { return rcp_approx(fabsf(a)); });   // unconditional:
+            V sarc;                                                                             // no branch
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-                cset(sarc, c, cget(at, c) > 1e-4f ? cget(r2, c) * cget(at, c) * rcp_approx(fabsf(cget(ny, c))) : cget(rh, c));
+            for (int c = 0; c < NC; ++c) cset(sarc, c, cget(at, c) > 1e-4f ? cget(sfull, c) : cget(rh, c));
             const V beta = fast_atan2_xpos(nz, sarc);              // s >= 0: right half-plane
             const V hd = nchi - kPi;                              // heading relative to the runway (West)
             const V hdw = wrap_pi(hd);

@@ -14,6 +14,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsmcatm.so")
+# A/B tooling only (tools/gpu_variants.sh): load a variant build of the same library instead
+if os.environ.get("SMC_LIB"):
+    LIB_PATH = os.environ["SMC_LIB"]
 _lib = None
 
 SMC_OK, SMC_EINVAL, SMC_EINFEASIBLE, SMC_ECUDA, SMC_ENCCL, SMC_ENOMEM, SMC_ESTATE = range(7)
