@@ -796,7 +796,7 @@ def test_fuel_estimates_parity(smc):
         m2, f2 = P.fuel_estimate2(0, traces[j, :K], dt, m0[j], Cf)
         assert np.allclose(out["m1"][j, :K], m1, rtol=1e-12, atol=0), j
         assert np.allclose(out["m2"][j, :K], m2, rtol=1e-12, atol=0), j
-        assert np.allclose(out["wres"][j, :K], w, rtol=1e-10, atol=1e-9), j
+        assert np.allclose(out["wres"][j, :K], w, rtol=1e-10, atol=1e-9, equal_nan=True), j
         assert out["flags"][j] == (f1 | f2), j
         assert out["fuel"][j, 0] == pytest.approx(m0[j] - m1[-1], rel=1e-12, abs=1e-9)
     assert (out["flags"] & 2).any() and (out["flags"] & 1).any()
