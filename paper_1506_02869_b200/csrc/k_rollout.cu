@@ -801,6 +801,411 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     }
 }
 
+// ============================================================== K2, two sample chains per lane
+// NC = 2 launches (both MH candidates) on the 2x2x2 grid with W >= 8: every lane carries samples s
+// and s + 1 of its aircraft as two independent chains, each a float2 over the candidates, so a
+// warp has two independent dependency chains in flight (the scheduler can issue from one while
+// the other waits on a fixed-latency result) at the same arithmetic per aircraft-step.  Shared by
+// both chains: the staged controls (one pair of LDS.128 per step), the per-lane constants, one
+// separation exchange (three LDS.128 per partner for four (sample, candidate) positions instead
+// of two per two) and one verdict shuffle per partner (four verdict bytes).  The two samples'
+// wind fields are drawn like the sample-pair instances' (two slots per segment).  Results are
+// identical to k_rollout<W, 2>: the same operations in the same order per (sample, candidate).
+#ifndef SMC_K2_MINB2S
+#define SMC_K2_MINB2S 3
+#endif
+#ifndef SMC_K2_TUNROLL2S
+#define SMC_K2_TUNROLL2S 1
+#endif
+size_t rollout2s_smem_bytes(int W, int H) {
+    const int SEGS = kBlock / W, GB = W / 4;
+    return sizeof(float4) * ((size_t)H * 2 * kBlock)              // controls
+           + sizeof(float) * (SEGS * 2 * GB * 16                  // normals [SEGS][slot][GB][16]
+                              + SEGS * 2 * 16                     // AR(1) state [SEGS][slot][8] (x, y)
+                              + SEGS * 2 * 16)                    // coefficients [SEGS][slot][16]
+           + sizeof(float4) * 6 * kBlock                          // positions x4, y4, z4, each twice
+           + sizeof(float) * 72 + 16;
+}
+
+template <int W, int R>
+__global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
+    static_assert(W >= 8, "two-chain instances need W >= 8 (eight AR(1) nodes per slot)");
+    constexpr int NSL = 2, SEGS = kBlock / W, GB = W / 4;
+    constexpr int ENS = W >= 16 ? 1 : 2;                          // (node, slot) pairs a lane owns
+    constexpr int TU2 = SMC_K2_TUNROLL2S;
+    extern __shared__ __align__(16) float smem[];
+    const int H = sc.H, n = sc.n;
+    float4 *s_ctrl = reinterpret_cast<float4 *>(smem);           // [H][2][kBlock]
+    float *s_V = reinterpret_cast<float *>(s_ctrl + H * 2 * kBlock);
+    float *s_Z = s_V + SEGS * NSL * GB * 16;
+    float *s_W = s_Z + SEGS * NSL * 16;
+    float4 *s_p4 = reinterpret_cast<float4 *>(s_W + SEGS * NSL * 16);   // [3][2 kBlock]: x4, y4, z4
+    float *s_Q = reinterpret_cast<float *>(s_p4 + 6 * kBlock);
+
+    const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
+    const uint32_t lloc = blockIdx.x * SEGS + seg;
+    const bool valid = lloc < args.L;
+    const uint32_t l = args.l0 + lloc;
+    const bool isac = lane < n;
+    const uint32_t k = args.k, mpc = *args.mpcp;
+    if (tid < 64) s_Q[(tid >> 3) * 9 + (tid & 7)] = sc.Cq[tid];
+
+    const DevAircraft *Ap = sc.ac + (isac ? lane : 0);
+    const int kind = Ap->kind;
+    const int first = isac ? Ap->first_step : (1 << 20);
+    const float halfS = Ap->halfS, cd0 = Ap->cd0, cd2 = Ap->cd2, dt_eta = Ap->dt_eta;
+    const float zmin = Ap->z_min, zmax = Ap->z_max, vmin = Ap->v_min, vmax = Ap->v_max, mempty = Ap->m_empty;
+    const float gA = kind ? Ap->theta_F : Ap->beta_f;
+    const float z_tf = Ap->z_tf, v_D = Ap->v_D;
+
+    uint32_t cbad[2];
+    {
+        const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
+        const float *src[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            cbad[c] = 0;
+            src[c] = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
+        }
+        for (int t = 0; t < H; ++t) {
+            float q[2][4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float T = 0.f, ph = 0.f, ga = 0.f;
+                if (isac && valid) { T = src[c][3 * t]; ph = src[c][3 * t + 1]; ga = src[c][3 * t + 2]; }
+                float sph, cph, sga, cga;
+                __sincosf(ph, &sph, &cph);
+                __sincosf(ga, &sga, &cga);
+                q[c][0] = T; q[c][1] = sph * rcp_approx(cph); q[c][2] = sga; q[c][3] = cga;
+                const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
+                cbad[c] |= (bad ? 1u : 0u) << t;
+            }
+            s_ctrl[(2 * t) * kBlock + tid] = make_float4(q[0][0], q[1][0], q[0][1], q[1][1]);
+            s_ctrl[(2 * t + 1) * kBlock + tid] = make_float4(q[0][2], q[1][2], q[0][3], q[1][3]);
+        }
+    }
+    __syncthreads();
+    float qrow[8];
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) qrow[mm] = s_Q[(lane & 7) * 9 + mm];
+
+    float ell[2] = {args.ell0, args.ell0};
+    using V = float2;
+    const float dt = sc.dt, g = sc.g;
+    const float inv0 = sc.wind_inv_ext[0], inv1 = sc.wind_inv_ext[1], inv2 = sc.wind_inv_ext[2];
+    const float nlo0 = -sc.wind_lo[0] * inv0, nlo1 = -sc.wind_lo[1] * inv1, nlo2 = -sc.wind_lo[2] * inv2;
+    const float cq = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
+    const float cA_th = kind ? 1.0f : -2.0f, cA_chi = kind ? 0.0f : 1.0f, cA_0 = kind ? -gA : -kPi;
+    const float cB_z = kind ? -1.0f : 0.0f, cB_b = kind ? 0.0f : 1.0f, cB_0 = kind ? z_tf : -gA;
+    const int pb = seg * 2 * W + lane;                             // own entry; + R: duplicate
+    float4 *const s_px = s_p4, *const s_py = s_p4 + 2 * kBlock, *const s_pz = s_p4 + 4 * kBlock;
+    const uint32_t S = args.S;
+
+    for (uint32_t s = 0; s < S; s += 2) {
+        const bool two = s + 1 < S;                                // odd S: the second chain is not counted
+        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            x[q] = vsplat<V>(Ap->x0[0]); y[q] = vsplat<V>(Ap->x0[1]); z[q] = vsplat<V>(Ap->x0[2]);
+            v[q] = vsplat<V>(Ap->x0[3]); chi[q] = vsplat<V>(Ap->x0[4]); m[q] = vsplat<V>(Ap->x0[5]);
+            fuel[q] = sA[q] = sB[q] = sC[q] = sN[q] = vsplat<V>(0.0f);
+        }
+        int landedm[2] = {0, 0}, violm[2] = {0, 0};
+        float2 Zr[ENS];
+        float2 gust_odd[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const uint32_t x1[2] = {(s & 0xFFFFu) | (k << 16), ((s + 1) & 0xFFFFu) | (k << 16)};
+
+#pragma unroll TU2
+        for (int t = 0; t < H; ++t) {
+            // ---------------- 1. both samples' wind fields for step t (Alg.1 l.10)
+            const int tb = t % GB;
+            if (tb == 0) {
+#pragma unroll
+                for (int task0 = 0; task0 < 4 * GB * NSL; task0 += W) {
+                    const int task = task0 + lane, sl = task / (4 * GB), tk = task - sl * 4 * GB;
+                    const int b = tk & 3, ts = t + (tk >> 2);
+                    if (ts < H) {
+                        const uint4 w = draw_ks(TAG_WIND, l, x1[sl], (uint32_t)ts | ((uint32_t)b << 16), mpc, sc.ks);
+                        *reinterpret_cast<float4 *>(&s_V[((seg * NSL + sl) * GB + (tk >> 2)) * 16 + 4 * b]) = box_muller4(w);
+                    }
+                }
+            }
+            __syncwarp();
+            float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16 * NSL);
+#pragma unroll
+            for (int e = 0; e < ENS; ++e) {
+                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
+                const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
+                const float2 ve = make_float2(vv[node], vv[8 + node]);
+                Zr[e] = (t == 0) ? ve : vfma(Zr[e], sc.a, ve * sc.b);
+                sZ2[sl * 8 + node] = Zr[e];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < ENS; ++e) {
+                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
+                const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
+                float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int mm = 0; mm < 4; ++mm) {
+                    const float4 zz = z4[mm];
+                    acc = vfma(make_float2(zz.x, zz.y), qrow[2 * mm], acc);
+                    acc = vfma(make_float2(zz.z, zz.w), qrow[2 * mm + 1], acc);
+                }
+                s_W[(seg * NSL + sl) * 16 + node] = acc.x;
+                s_W[(seg * NSL + sl) * 16 + 8 + node] = acc.y;
+            }
+            __syncwarp();
+            // gusts (R15): one Philox call per sample covers steps 2u and 2u+1
+            float gxq[2] = {sc.nominal[0], sc.nominal[0]}, gyq[2] = {sc.nominal[1], sc.nominal[1]};
+            if (sc.turb_sigma > 0.0f) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    float2 gg;
+                    if ((t & 1) == 0) {
+                        const uint4 w = draw_ks(TAG_TURB, l, x1[q], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
+                        const float4 g4 = box_muller4(w);
+                        gg = make_float2(g4.x, g4.y);
+                        gust_odd[q] = make_float2(g4.z, g4.w);
+                    } else {
+                        gg = gust_odd[q];
+                    }
+                    gxq[q] = fmaf(sc.turb_sigma, gg.x, gxq[q]);
+                    gyq[q] = fmaf(sc.turb_sigma, gg.y, gyq[q]);
+                }
+            }
+            // controls of step t, shared by both chains
+            const float4 ca = s_ctrl[(2 * t) * kBlock + tid], cb = s_ctrl[(2 * t + 1) * kBlock + tid];
+            const V T = make_float2(ca.x, ca.y), tph = make_float2(ca.z, ca.w);
+            const V sga = make_float2(cb.x, cb.y), cga = make_float2(cb.z, cb.w);
+            const bool act = first <= t;
+
+            // ---------------- 2-3. per chain: dynamics, unary checks, geometry, landing test
+            V nx[2], ny[2], nz[2], nv[2], nchi[2], nm[2], th[2], beta[2], px[2], flyf[2], dtef[2];
+            int flym[2], vnowm[2], lnowm[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                flym[q] = act ? (~landedm[q] & 3) : 0;
+                flyf[q] = make_float2((flym[q] & 1) ? 1.0f : 0.0f, (flym[q] & 2) ? 1.0f : 0.0f);
+                const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[(seg * NSL + q) * 16]);
+                float Wn[16];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float4 a4 = w4[e];
+                    Wn[4 * e] = a4.x; Wn[4 * e + 1] = a4.y; Wn[4 * e + 2] = a4.z; Wn[4 * e + 3] = a4.w;
+                }
+                const V fx = vmap(x[q], [&](float p) { return __saturatef(fmaf(p, inv0, nlo0)); });
+                const V fy = vmap(y[q], [&](float p) { return __saturatef(fmaf(p, inv1, nlo1)); });
+                const V fz = vmap(z[q], [&](float p) { return __saturatef(fmaf(p, inv2, nlo2)); });
+                const V wx = tripoly(Wn, Wn[0] + gxq[q], fx, fy, fz);
+                const V wy = tripoly(Wn + 8, Wn[8] + gyq[q], fx, fy, fz);
+                V qd = cq * v[q] * v[q];
+                if (sc.density_mode == 0) {
+                    const V base = vmap(vfma(z[q], -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
+                    qd = qd * vmap(vmap(base, [](float a) { return __log2f(a); }) * 4.2559f, ex2_approx);
+                }
+                const V mgq = (m[q] * g) * vmap(qd, rcp_approx);
+                const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
+                const V chr = wrap_pi(chi[q]);
+                V sch, cch;
+                __sincosf(chr.x, &sch.x, &cch.x);
+                __sincosf(chr.y, &sch.y, &cch.y);
+                const V dtf = flyf[q] * dt;
+                dtef[q] = flyf[q] * dt_eta;
+                const V vcg = v[q] * cga;
+                nx[q] = vfma(dtf, vfma(vcg, cch, wx), x[q]);
+                ny[q] = vfma(dtf, vfma(vcg, sch, wy), y[q]);
+                nz[q] = vfma(dtf * v[q], sga, z[q]);
+                nv[q] = vfma(dtf, vfma(T - D, vmap(m[q], rcp_approx), sga * (-g)), v[q]);
+                nchi[q] = vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]);
+                nm[q] = vfma(-dtef[q], T, m[q]);
+                vnowm[q] = 0;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const float zc = cget(nz[q], c), vc = cget(nv[q], c);
+                    const bool bad = (((cbad[c] >> t) & 1u) != 0u) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) |
+                                     !(vc <= vmax) | !(cget(nm[q], c) >= mempty);
+                    vnowm[q] |= (bad ? 1 : 0) << c;
+                }
+                th[q] = fast_atan2(ny[q], nx[q]);
+                const V r2 = vfma(nx[q], nx[q], ny[q] * ny[q]);
+                const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
+                const V at = vabs(th[q]);
+                const V sfull = (r2 * at) * vmap(ny[q], [](float a) { return rcp_approx(fabsf(a)); });
+                V sarc;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) cset(sarc, c, cget(at, c) > 1e-4f ? cget(sfull, c) : cget(rh, c));
+                beta[q] = fast_atan2_xpos(nz[q], sarc);
+                const V hdw = wrap_pi(nchi[q] - kPi);
+                lnowm[q] = 0;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta[q], c) <= sc.P_beta) &
+                                    (cget(at, c) <= sc.P_chi) & (fabsf(cget(hdw, c)) <= sc.P_chi) &
+                                    (cget(nv[q], c) <= sc.P_vs);
+                    lnowm[q] |= (ln ? 1 : 0) << c;
+                }
+                if (kind != 0) lnowm[q] = 0;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    cset(px[q], c, ((flym[q] >> c) & 1) ? cget(nx[q], c) : __int_as_float(0x7fffffff));
+            }
+            // ---------------- 4. separation (Eq. avoidance): one exchange for both chains
+            if (R == W || lane < R) {
+                const float4 ex = make_float4(px[0].x, px[0].y, px[1].x, px[1].y);
+                const float4 ey = make_float4(ny[0].x, ny[0].y, ny[1].x, ny[1].y);
+                const float4 ez = make_float4(nz[0].x, nz[0].y, nz[1].x, nz[1].y);
+                s_px[pb] = ex; s_px[pb + R] = ex;
+                s_py[pb] = ey; s_py[pb + R] = ey;
+                s_pz[pb] = ez; s_pz[pb + R] = ez;
+            }
+            __syncwarp();
+            // verdict bytes: bit 31 (sample s, candidate 0), 23 (s, 1), 15 (s + 1, 0), 7 (s + 1, 1)
+            uint32_t confw = 0u;
+#pragma unroll
+            for (int d = 1; d <= R / 2; ++d) {
+                const float4 qx = s_px[pb + d], qy = s_py[pb + d], qz = s_pz[pb + d];
+                const V dx0 = px[0] - make_float2(qx.x, qx.y), dx1 = px[1] - make_float2(qx.z, qx.w);
+                const V dy0 = ny[0] - make_float2(qy.x, qy.y), dy1 = ny[1] - make_float2(qy.z, qy.w);
+                const V dz0 = nz[0] - make_float2(qz.x, qz.y), dz1 = nz[1] - make_float2(qz.z, qz.w);
+                const V u0 = vfma(dx0, dx0, vfma(dy0, dy0, -sc.twoPr2)), u1 = vfma(dx1, dx1, vfma(dy1, dy1, -sc.twoPr2));
+                const V w0 = vabs(dz0) - sc.twoPh, w1 = vabs(dz1) - sc.twoPh;
+                const uint32_t hi = __byte_perm(__float_as_uint(u0.x) & __float_as_uint(w0.x),
+                                                __float_as_uint(u0.y) & __float_as_uint(w0.y), 0x3737);
+                const uint32_t lo = __byte_perm(__float_as_uint(u1.x) & __float_as_uint(w1.x),
+                                                __float_as_uint(u1.y) & __float_as_uint(w1.y), 0x3737);
+                const uint32_t hv = (hi & 0xFFFF0000u) | (lo & 0x0000FFFFu);
+                if (2 * d < R)
+                    confw |= hv | __shfl_sync(0xffffffffu, hv, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
+                else
+                    confw |= hv;
+            }
+            const int confm[2] = {(int)((confw >> 31) | ((confw >> 22) & 2u)), (int)(((confw >> 15) & 1u) | ((confw >> 6) & 2u))};
+            // ---------------- 5. per chain: cost terms, flags, state update
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const V argA = vfma(th[q], cA_th, vfma(nchi[q], cA_chi, cA_0));
+                const V wA = wrap_pi(argA);
+                sA[q] = vfma(vabs(wA), flyf[q], sA[q]);
+                sB[q] = vfma(vabs(vfma(nz[q], cB_z, vfma(beta[q], cB_b, cB_0))), flyf[q], sB[q]);
+                sC[q] = vfma(vabs(nv[q] - v_D), flyf[q], sC[q]);
+                fuel[q] = vfma(dtef[q], T, fuel[q]);
+                if (sc.has_noise) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const float zz = cget(nz[q], c) * sc.inv_Ac;
+                        const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, cget(nx[q], c), cget(ny[q], c));
+                        cset(sN[q], c, cget(sN[q], c) + (((flym[q] >> c) & 1) ? nzs
+                                                                               : ((act && ((landedm[q] >> c) & 1)) ? 1.0f : 0.0f)));
+                    }
+                }
+                violm[q] |= flym[q] & (vnowm[q] | confm[q]);
+                landedm[q] |= flym[q] & lnowm[q];
+                x[q] = nx[q]; y[q] = ny[q]; z[q] = nz[q]; v[q] = nv[q]; chi[q] = nchi[q]; m[q] = nm[q];
+            }
+        }  // t
+
+        // ---------------- utility J_T and weight, both chains
+        {
+            const int Ha = Ap->Ha;
+            const float invHa = Ap->invHa, invFmax = Ap->invFmax;
+            const float supB = Ap->supB, invDenB = Ap->invDenB, invSupC = Ap->invSupC, invSupE = Ap->invSupE;
+            const int flagB = Ap->flagB;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && !two) continue;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float J = 1.0f;
+                    if (Ha > 0 && isac) {
+                        const float Jfuel = clamp01(1.0f - cget(fuel[q], c) * invFmax);
+                        const float J1 = clamp01(1.0f - cget(sA[q], c) * invHa * (1.0f / kPi));
+                        if (kind == 1) {
+                            const float c2 = flagB ? 1.0f : clamp01((supB - cget(sB[q], c) * invHa) * invDenB);
+                            const float c3 = clamp01(1.0f - cget(sC[q], c) * invHa * invSupC);
+                            J = sc.alpha_dep[0] * J1 + sc.alpha_dep[1] * Jfuel + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
+                        } else {
+                            const float c1 = clamp01(1.0f - cget(sB[q], c) * invHa * invSupE);
+                            J = sc.alpha_arr[0] * J1 + sc.alpha_arr[1] * c1 + sc.alpha_arr[2] * Jfuel;
+                        }
+                        if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * cget(sN[q], c) * invHa;
+                    }
+                    ell[c] = (((violm[q] >> c) & 1) || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
+                }
+            }
+        }
+    }  // s
+
+    // ---------------- epilogue: lambda (double, ascending i), MH (R1, R46), survivor
+    __syncthreads();
+    float *s_ell = reinterpret_cast<float *>(s_p4);
+    int *s_dec = reinterpret_cast<int *>(s_V);
+    s_ell[tid] = ell[0];
+    s_ell[kBlock + tid] = ell[1];
+    __syncwarp();
+    double lam[2] = {0.0, 0.0};
+    for (int i = 0; i < n; ++i) {
+        lam[0] += (double)s_ell[seg * W + i];
+        lam[1] += (double)s_ell[kBlock + seg * W + i];
+    }
+    uint32_t mask;
+    int nacc;
+    float ell_s;
+    double lam_s;
+    if (args.mh_mode == 2) {
+        const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[1], l, (uint32_t)lane, k, mpc, sc.key0,
+                                                   sc.key1);
+        const unsigned b = __ballot_sync(0xffffffffu, ai);
+        mask = (W == 32) ? b : ((b >> ((tid & 31) & ~(W - 1))) & ((1u << (W & 31)) - 1u));
+        ell_s = ai ? ell[1] : ell[0];
+        lam_s = 0.0;
+        for (int i = 0; i < n; ++i) lam_s += (double)s_ell[(((mask >> i) & 1u) ? kBlock : 0) + seg * W + i];
+        nacc = __popc(mask);
+    } else {
+        const bool acc = mh_decide(lam[0], lam[1], l, k, mpc, sc.key0, sc.key1);
+        mask = acc ? 0xFFFFFFFFu : 0u;
+        ell_s = acc ? ell[1] : ell[0];
+        lam_s = acc ? lam[1] : lam[0];
+        nacc = acc ? 1 : 0;
+    }
+    if (valid && isac) args.ell_out[(size_t)lane * args.L + lloc] = ell_s;
+    if (valid && lane == 0) {
+        args.lam_out[lloc] = lam_s;
+        args.surv_out[lloc] = mask;
+        if (args.lam_cand) {
+            args.lam_cand[lloc] = lam[0];
+            args.lam_cand[args.L + lloc] = lam[1];
+        }
+    }
+    if (lane == 0) s_dec[seg] = valid ? nacc : 0;
+    __syncthreads();
+    uint32_t *s_cm = reinterpret_cast<uint32_t *>(s_ctrl);
+    s_cm[tid] = (valid && isac) ? f2ord(ell_s) : 0u;
+    __syncthreads();
+    if (tid < n) {
+        uint32_t mx = 0u;
+        for (int sg = 0; sg < SEGS; ++sg) mx = max(mx, s_cm[sg * W + tid]);
+        if (mx) atomicMax(&args.colmax[tid], mx);
+    }
+    if (tid == 0) {
+        unsigned long long cnt = 0;
+        for (int sg = 0; sg < SEGS; ++sg) cnt += s_dec[sg];
+        if (cnt) atomicAdd(args.n_accept, cnt);
+    }
+}
+
+template <int W, int R>
+static cudaError_t launch_2s_r(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    const size_t smem = rollout2s_smem_bytes(W, sc.H);
+    auto kern = k_rollout_2s<W, R>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (a.L + kBlock / W - 1) / (kBlock / W);
+    if (grid == 0) return cudaSuccess;
+    kern<<<grid, kBlock, smem, st>>>(sc, a);
+    return cudaGetLastError();
+}
+
 size_t rollout_smem_bytes(int W, int NC, int H, int ng, bool sp) {
     const int SEGS = kBlock / W, NSL = sp ? 2 : 1;
     if (ng > 8) {
@@ -918,6 +1323,29 @@ static bool ring_enabled() {
     return on;
 }
 
+static bool ns2_enabled() {
+    static const bool on = [] { const char *e = getenv("SMC_K2_2S"); return !(e && strcmp(e, "0") == 0); }();
+    return on;
+}
+
+// Two-candidate launches on the 2x2x2 grid with W >= 16: two sample chains per lane (k_rollout_2s);
+// SMC_K2_2S=0 runs one sample per lane (k_rollout<W, 2>).
+static cudaError_t launch_2s(int W, int R, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    switch (W) {
+        case 16:
+            if (R == 10) return launch_2s_r<16, 10>(sc, a, st);
+            if (R == 12) return launch_2s_r<16, 12>(sc, a, st);
+            if (R == 14) return launch_2s_r<16, 14>(sc, a, st);
+            return launch_2s_r<16, 16>(sc, a, st);
+        case 32:
+            if (R == 20) return launch_2s_r<32, 20>(sc, a, st);
+            if (R == 24) return launch_2s_r<32, 24>(sc, a, st);
+            if (R == 28) return launch_2s_r<32, 28>(sc, a, st);
+            return launch_2s_r<32, 32>(sc, a, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
 static bool sp_enabled() {
     static const bool on = [] { const char *e = getenv("SMC_K2_SP"); return !(e && strcmp(e, "0") == 0); }();
     return on;
@@ -1001,6 +1429,10 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     const bool dense = sc.wng > 8;
     const int W = segment_width(sc.n, dense);
     if (NC == 1 && !debug && !dense && W >= 8 && sp_enabled()) return launch_sp(W, sc, a, st);
+    // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
+    // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
+    // 26.68: one chain)
+    if (NC == 2 && !debug && !dense && W >= 16 && !a.part && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }
