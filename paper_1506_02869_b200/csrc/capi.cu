@@ -747,6 +747,7 @@ static smc_status build_constants(smc_ctx *ctx) {
     d.n = n; d.H = H; d.density_mode = s.density_mode;
     d.dt = (float)s.dt; d.g = (float)s.g; d.rho_const = (float)s.rho_const;
     d.P_runway = (float)s.P_runway; d.P_beta = (float)s.P_beta; d.P_chi = (float)s.P_chi; d.P_vs = (float)s.P_vs;
+    d.P_chi_west = (float)(3.14159265358979323846 - s.P_chi);
     d.twoPr2 = (float)((2.0 * s.P_r) * (2.0 * s.P_r));
     d.twoPh = (float)(2.0 * s.P_h);
     for (int q = 0; q < 4; ++q) d.alpha_dep[q] = (float)s.alpha_dep[q];
@@ -838,6 +839,7 @@ static smc_status build_constants(smc_ctx *ctx) {
         A.Ha = H - (int)a.first_step;
         const double x0[6] = {a.x0.x, a.x0.y, a.x0.z, a.x0.v, a.x0.chi, a.x0.m};
         for (int q = 0; q < 6; ++q) A.x0[q] = (float)x0[q];
+        A.x0[4] = (float)std::remainder(x0[4], 2.0 * 3.14159265358979323846);   // K2 keeps chi in [-pi, pi]
         A.theta_F = (float)a.theta_F; A.z_tf = (float)a.z_tf; A.v_D = (float)a.v_D; A.beta_f = (float)a.beta_f;
         A.halfS = (float)(0.5 * ty.S); A.cd0 = (float)ty.cd0; A.cd2 = (float)ty.cd2; A.dt_eta = (float)(s.dt * ty.eta);
         A.m_empty = (float)ty.m_empty; A.T_min = (float)ty.T_min; A.T_max = (float)ty.T_max;

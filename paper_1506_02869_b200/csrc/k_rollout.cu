@@ -543,7 +543,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             }
             const V mgq = (m * g) * vmap(qd, rcp_approx);
             const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
-            const V chr = wrap_pi(chi);
+            const V chr = chi;                                    // kept in [-pi, pi] (wrapped once per step)
             V sch, cch;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
@@ -557,7 +557,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const V ny = vfma(dtf, vfma(vcg, sch, wy), y);
             const V nz = vfma(dtf * v, sga, z);
             const V nv = vfma(dtf, vfma(T - D, vmap(m, rcp_approx), sga * (-g)), v);
-            const V nchi = vfma((dtf * g) * tph, vmap(v, rcp_approx), chi);
+            const V nchi = wrap_pi(vfma((dtf * g) * tph, vmap(v, rcp_approx), chi));   // heading, wrapped (R32)
             const V nm = vfma(-dtef, T, m);
             // envelope and mass at j = t+1 (R17)
             int vnowm = 0;
@@ -581,13 +581,11 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) cset(sarc, c, cget(at, c) > 1e-4f ? cget(sfull, c) : cget(rh, c));
             const V beta = fast_atan2_xpos(nz, sarc);              // s >= 0: right half-plane
-            const V hd = nchi - kPi;                              // heading relative to the runway (West)
-            const V hdw = wrap_pi(hd);
             int lnowm = 0;
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta, c) <= sc.P_beta) & (cget(at, c) <= sc.P_chi) &
-                                (fabsf(cget(hdw, c)) <= sc.P_chi) & (cget(nv, c) <= sc.P_vs);
+                                (fabsf(cget(nchi, c)) >= sc.P_chi_west) & (cget(nv, c) <= sc.P_vs);
                 lnowm |= (ln ? 1 : 0) << c;
             }
             if (kind != 0) lnowm = 0;                            // only arrivals land (Eq. TO_init)
@@ -1006,7 +1004,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 }
                 const V mgq = (m[q] * g) * vmap(qd, rcp_approx);
                 const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
-                const V chr = wrap_pi(chi[q]);
+                const V chr = chi[q];                             // kept in [-pi, pi]
                 V sch, cch;
                 __sincosf(chr.x, &sch.x, &cch.x);
                 __sincosf(chr.y, &sch.y, &cch.y);
@@ -1017,7 +1015,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 ny[q] = vfma(dtf, vfma(vcg, sch, wy), y[q]);
                 nz[q] = vfma(dtf * v[q], sga, z[q]);
                 nv[q] = vfma(dtf, vfma(T - D, vmap(m[q], rcp_approx), sga * (-g)), v[q]);
-                nchi[q] = vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]);
+                nchi[q] = wrap_pi(vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]));
                 nm[q] = vfma(-dtef[q], T, m[q]);
                 vnowm[q] = 0;
 #pragma unroll
@@ -1036,12 +1034,11 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 #pragma unroll
                 for (int c = 0; c < 2; ++c) cset(sarc, c, cget(at, c) > 1e-4f ? cget(sfull, c) : cget(rh, c));
                 beta[q] = fast_atan2_xpos(nz[q], sarc);
-                const V hdw = wrap_pi(nchi[q] - kPi);
                 lnowm[q] = 0;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta[q], c) <= sc.P_beta) &
-                                    (cget(at, c) <= sc.P_chi) & (fabsf(cget(hdw, c)) <= sc.P_chi) &
+                                    (cget(at, c) <= sc.P_chi) & (fabsf(cget(nchi[q], c)) >= sc.P_chi_west) &
                                     (cget(nv[q], c) <= sc.P_vs);
                     lnowm[q] |= (ln ? 1 : 0) << c;
                 }

@@ -37,6 +37,8 @@ struct DevScen {
     int n, H, density_mode, has_noise;
     float dt, g, rho_const;
     float P_runway, P_beta, P_chi, P_vs, twoPr2, twoPh;
+    float P_chi_west;                     // pi - P_chi: with chi in [-pi, pi], |wrap(chi - pi)| <= P_chi
+                                          // (landing heading, Eq. TO_init) is |chi| >= pi - P_chi
     float alpha_dep[4], alpha_arr[3];
     float noise_w, inv_Ac;
     int pop_nx, pop_ny;

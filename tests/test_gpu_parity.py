@@ -75,7 +75,10 @@ def _compare_rollouts(smc, scn, L, S, k, seed, ctrl, l0=0, name=None):
             assert np.array_equal(g["landed"][l, s], r["landed_step"]), (l, s)
             tg, to = g["traj"][l, s].astype(np.float64), r["traj"]
             dom = _in_domain(to)
-            err = np.abs(tg - to) - (1e-4 * np.abs(to) + tol)
+            dif = np.abs(tg - to)
+            # the GPU keeps the heading wrapped to [-pi, pi], the oracle does not (R32): compare modulo 2 pi
+            dif[..., 4] = np.abs(np.remainder(tg[..., 4] - to[..., 4] + np.pi, 2 * np.pi) - np.pi)
+            err = dif - (1e-4 * np.abs(np.where(np.arange(6) == 4, np.pi, to)) + tol)
             err[~dom] = -1.0
             assert np.all(err <= 0), (l, s, np.unravel_index(np.argmax(err), err.shape), tg, to)
             full = dom.all(1)                      # aircraft whose whole rollout stayed in the domain
@@ -236,7 +239,11 @@ def test_violator_keeps_flying_on_gpu(smc):
     g = sol.debug_rollout(u, 1, 0, traj=True)
     r = P.rollout(u[0].astype(np.float64), 0, 0, 0, 3)
     assert g["viol"][0, 0].tolist() == [1, 1] and r["viol"].tolist() == [1, 1]
-    assert np.allclose(g["traj"][0, 0], r["traj"], rtol=1e-5, atol=0.1)
+    gt, ot = g["traj"][0, 0].astype(np.float64), r["traj"]
+    keep = [0, 1, 2, 3, 5]
+    assert np.allclose(gt[..., keep], ot[..., keep], rtol=1e-5, atol=0.1)
+    dchi = np.remainder(gt[..., 4] - ot[..., 4] + np.pi, 2 * np.pi) - np.pi  # heading modulo 2 pi (R32)
+    assert np.all(np.abs(dchi) < 1e-4)
     assert g["traj"][0, 0, 1, -1, 0] < g["traj"][0, 0, 1, 1, 0] - 4000.0       # the violator kept flying West
     sol.close()
 
