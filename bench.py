@@ -62,6 +62,7 @@ def parse():
                     help="warm-start fraction of the population from the previous winner (R45)")
     ap.add_argument("--lfinal", type=int, default=0,
                     help="shrink the population linearly to this many particles by the last round (P:1225)")
+    ap.add_argument("--loop-config", type=int, default=3, help="solver configuration of --loop")
     ap.add_argument("--loop", type=int, default=0,
                     help="run the rolling-window MPC loop of c3's traffic for this many steps instead")
     return ap.parse_args()
@@ -239,7 +240,8 @@ def run_loop(args):
     landings / exits, realised separation, fuel.  --traffic picks c3's stream (16 arr /
     8 dep) or the paper's mixed (10 + 10) / congested (24 arrivals) shapes."""
     from paper_1506_02869_b200 import mpc_loop, scenarios as sc
-    base, cfg = sc.config(args.config if args.config != 2 else 3)
+    # the loop runs c3's solver unless --loop-config names another configuration
+    base, cfg = sc.config(args.loop_config)
     if args.mh >= 0:
         cfg = dataclasses.replace(cfg, mh=args.mh)
     if args.traffic == "mixed":

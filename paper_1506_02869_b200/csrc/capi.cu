@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: host ranges for nsys / ncu --nvtx (no-op untraced)
+
 #include "../../include/smcatm.h"
 #include "smc_device.cuh"
 #include "smc_kernels.h"
@@ -302,6 +304,11 @@ static smc_status fail(smc_ctx *c, smc_status s, const char *fmt, ...) {
     return s;
 }
 
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static cudaError_t h2d(smc_ctx *c, void *dst, const void *src, size_t bytes) {
     c->io_h2d += bytes;
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st);
@@ -561,7 +568,9 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         const char *cs = getenv("SMC_CDF_SAMPLE");          // K6 two-level search (default on)
         ctx->cdf_sample = !(cs && strcmp(cs, "0") == 0);
         const char *am = getenv("SMC_ANC");
-        ctx->anc_mode = am ? (strcmp(am, "mp") == 0 ? 1 : (strcmp(am, "bisect") == 0 ? 0 : -1)) : -1;
+        // "bisect2": debug_resample runs K6's two-level search (production default below 2^17)
+        ctx->anc_mode = am ? (strcmp(am, "mp") == 0 ? 1 : (strcmp(am, "bisect") == 0 ? 0 :
+                                                          (strcmp(am, "bisect2") == 0 ? 2 : -1))) : -1;
     }
     ctx->Lg = cfg->n_particles;
     smc_shard_range(ctx->Lg, world, cfg->rank, &ctx->l0, &ctx->Lloc);
@@ -998,11 +1007,13 @@ static bool use_cluster_scan(const smc_ctx *ctx, uint32_t Lk) {
 }
 
 static bool use_merge_path(const smc_ctx *ctx, uint32_t Lk) {
-    if (ctx->anc_mode >= 0) return ctx->anc_mode == 1;
+    if (ctx->anc_mode == 0 || ctx->anc_mode == 1) return ctx->anc_mode == 1;
+    if (ctx->anc_mode == 2) return false;
     return Lk >= (1u << 17);
 }
 
 static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
+    NvtxRange nvtx_round("smc_round");
     const uint32_t k = ctx->k;
     const int n = ctx->dsc.n, H = ctx->dsc.H;
     const int P = ctx->cur;
@@ -1294,6 +1305,7 @@ static smc_status infeasible(smc_ctx *ctx, const char *what) {
 
 extern "C" smc_status smc_best_controls(smc_ctx *ctx, smc_control *out, double *lambda, int64_t *particle) {
     if (!ctx) return SMC_EINVAL;
+    NvtxRange nvtx_sel("smc_best_controls");
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
     smc_status s = select_best(ctx);
     if (s != SMC_OK) return s;
@@ -1330,6 +1342,7 @@ static smc_status solve_body(smc_ctx *ctx, uint32_t advance_plant) {
 
 extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
     if (!ctx) return SMC_EINVAL;
+    NvtxRange nvtx_solve("smc_solve");
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "smc_solve before smc_set_scenario");
     if (!ctx->cfg.use_graph || ctx->st == nullptr) {
         smc_status s = solve_body(ctx, advance_plant);
@@ -1382,6 +1395,7 @@ extern "C" smc_status smc_solve(smc_ctx *ctx, uint32_t advance_plant) {
 extern "C" smc_status mpc_step(smc_ctx *ctx, const smc_state *measured, smc_control *applied, smc_state *next,
                                uint32_t *flags) {
     if (!ctx || !measured) return SMC_EINVAL;
+    NvtxRange nvtx_step("mpc_step");
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "mpc_step before smc_set_scenario");
     const int n = ctx->dsc.n;
     for (int i = 0; i < n; ++i) ctx->ac[i].x0 = measured[i];
@@ -1563,6 +1577,7 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     unsigned long long *dC = tmp.alloc<unsigned long long>((size_t)N * L);
     double *dess = tmp.alloc<double>(2 * N);
     unsigned long long *st1 = tmp.alloc<unsigned long long>((size_t)N * nt);
+    unsigned long long *dCs = tmp.alloc<unsigned long long>((size_t)N * cdf_samples(L));
     uint32_t *tiles = tmp.alloc<uint32_t>(2 * N);
     int32_t *danc = tmp.alloc<int32_t>((size_t)N * M);
     uint32_t *dspl = tmp.alloc<uint32_t>((size_t)N * mp_split_words(L, M));
@@ -1579,8 +1594,10 @@ extern "C" smc_status smc_debug_resample(smc_ctx *ctx, const float *ell, uint32_
     rs.key0 = (uint32_t)ctx->cfg.seed; rs.key1 = (uint32_t)(ctx->cfg.seed >> 32);
     rs.ell = dell; rs.colmax = dcm; rs.Q = dQ; rs.ess = dess; rs.status = st1;
     rs.tile_ctr = tiles; rs.C = dC; rs.QR = dQR; rs.anc = danc; rs.M = M; rs.splits = dspl;
+    if (ctx->anc_mode == 2) { rs.Cs = dCs; rs.Cs_stride = cdf_samples(L); }
     LAUNCH(use_cluster_scan(ctx, L) ? launch_scan_cluster(rs, ctx->st) : launch_scan(rs, ctx->st));
-    LAUNCH(ctx->anc_mode == 0 ? launch_ancestors_bisect(rs, ctx->st) : launch_ancestors(rs, ctx->st));
+    LAUNCH(ctx->anc_mode == 0 ? launch_ancestors_bisect(rs, ctx->st)
+                              : (ctx->anc_mode == 2 ? launch_ancestors_two_level(rs, ctx->st) : launch_ancestors(rs, ctx->st)));
     CK(cudaMemcpyAsync(anc, danc, 4 * (size_t)N * M, cudaMemcpyDeviceToHost, ctx->st));
     if (Q) CK(cudaMemcpyAsync(Q, dQ, 8 * N, cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));

@@ -460,6 +460,23 @@ __global__ void k_ancestors(const ResampleArgs r) {
         r.anc[(size_t)i * r.M + j] = find_ancestor(r.C + (size_t)i * r.L, r.L, r.M, Q, R, j);
 }
 
+// The production K6 search (find_ancestor2: K-ary rounds over the every-16th samples Cs, then
+// inside one 128-byte line of C) as a stand-alone pass, for the bit-exact debug sweep.
+__global__ void k_ancestors2(const ResampleArgs r) {
+    const int i = blockIdx.y;
+    const uint64_t Q = r.QR[2 * i], R = r.QR[2 * i + 1];
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < r.M; j += gridDim.x * blockDim.x)
+        r.anc[(size_t)i * r.M + j] = find_ancestor2(r.C + (size_t)i * r.L, r.Cs + (size_t)i * r.Cs_stride, r.L, r.M,
+                                                    Q, R, j);
+}
+
+cudaError_t launch_ancestors_two_level(const ResampleArgs &r, cudaStream_t st) {
+    unsigned gx = (r.M + 255) / 256;
+    if (gx > 1024) gx = 1024;
+    k_ancestors2<<<dim3(gx, r.n), 256, 0, st>>>(r);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st) {
     unsigned gx = (r.M + 255) / 256;
     if (gx > 1024) gx = 1024;

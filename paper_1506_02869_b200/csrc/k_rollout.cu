@@ -69,7 +69,8 @@ __device__ __forceinline__ V wrap_pi(V a) {
 }
 
 // popdense bilinear lookup on the 1 km grid, clamped at its edge.
-__device__ __forceinline__ float popdense(const DevScen &sc, float x, float y) {
+// pop: the grid in global memory (read-only path) or staged in shared memory by the caller
+__device__ __forceinline__ float popdense(const DevScen &sc, const float *pop, float x, float y) {
     float gx = (x - sc.pop_x0) * sc.pop_inv_dx, gy = (y - sc.pop_y0) * sc.pop_inv_dx;
     const float mx = (float)(sc.pop_nx - 1), my = (float)(sc.pop_ny - 1);
     gx = fminf(fmaxf(gx, 0.0f), mx);
@@ -79,8 +80,8 @@ __device__ __forceinline__ float popdense(const DevScen &sc, float x, float y) {
     const float fx = sc.pop_nx > 1 ? gx - (float)ix : 0.0f;
     const float fy = sc.pop_ny > 1 ? gy - (float)iy : 0.0f;
     const int ix1 = sc.pop_nx > 1 ? ix + 1 : ix, iy1 = sc.pop_ny > 1 ? iy + 1 : iy;
-    const float v00 = __ldg(&sc.pop[iy * sc.pop_nx + ix]), v10 = __ldg(&sc.pop[iy * sc.pop_nx + ix1]);
-    const float v01 = __ldg(&sc.pop[iy1 * sc.pop_nx + ix]), v11 = __ldg(&sc.pop[iy1 * sc.pop_nx + ix1]);
+    const float v00 = pop[iy * sc.pop_nx + ix], v10 = pop[iy * sc.pop_nx + ix1];
+    const float v01 = pop[iy1 * sc.pop_nx + ix], v11 = pop[iy1 * sc.pop_nx + ix1];
     const float a = fmaf(fx, v10 - v00, v00), b = fmaf(fx, v11 - v01, v01);
     return fmaf(fy, b - a, a);
 }
@@ -659,7 +660,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const float zz = cget(nz, c) * sc.inv_Ac;
-                    const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, cget(nx, c), cget(ny, c));
+                    const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, sc.pop, cget(nx, c), cget(ny, c));
                     // "best possible cost, 1, for all remaining steps" after landing
                     cset(sN, c, cget(sN, c) + (((flym >> c) & 1) ? nzs : ((act && ((landedm >> c) & 1)) ? 1.0f : 0.0f)));
                 }
@@ -812,12 +813,19 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #ifndef SMC_K2_MINB2S
 #define SMC_K2_MINB2S 3
 #endif
+#ifndef SMC_K2_INVM
+#define SMC_K2_INVM 0   // 1/m carried by one Newton step per step instead of a MUFU reciprocal
+#endif
 #ifndef SMC_K2_TUNROLL2S
 #define SMC_K2_TUNROLL2S 1
 #endif
-size_t rollout2s_smem_bytes(int W, int H) {
+// the 1 km population grid is staged in shared memory when it fits (c4: 81 x 81, 26 KB)
+constexpr int kPopSmem = 8192;
+__host__ __device__ inline int pop_smem_floats(int nx, int ny) { return nx * ny <= kPopSmem ? nx * ny : 0; }
+
+size_t rollout2s_smem_bytes(int W, int H, int npop) {
     const int SEGS = kBlock / W, GB = W / 4;
-    return sizeof(float4) * ((size_t)H * 2 * kBlock)              // controls
+    return sizeof(float) * (size_t)npop + sizeof(float4) * ((size_t)H * 2 * kBlock)              // controls
            + sizeof(float) * (SEGS * 2 * GB * 16                  // normals [SEGS][slot][GB][16]
                               + SEGS * 2 * 16                     // AR(1) state [SEGS][slot][8] (x, y)
                               + SEGS * 2 * 16)                    // coefficients [SEGS][slot][16]
@@ -831,8 +839,15 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     constexpr int NSL = 2, SEGS = kBlock / W, GB = W / 4;
     constexpr int ENS = W >= 16 ? 1 : 2;                          // (node, slot) pairs a lane owns
     constexpr int TU2 = SMC_K2_TUNROLL2S;
-    extern __shared__ __align__(16) float smem[];
+    extern __shared__ __align__(16) float smem_all[];
     const int H = sc.H, n = sc.n;
+    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx, sc.pop_ny) : 0;
+    const float *s_pop = sc.pop;                                 // the grid, staged below when it fits
+    float *smem = smem_all + ((npop + 3) & ~3);
+    if (npop) {
+        for (int e = threadIdx.x; e < npop; e += kBlock) smem_all[e] = __ldg(&sc.pop[e]);
+        s_pop = smem_all;
+    }
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);           // [H][2][kBlock]
     float *s_V = reinterpret_cast<float *>(s_ctrl + H * 2 * kBlock);
     float *s_Z = s_V + SEGS * NSL * GB * 16;
@@ -855,6 +870,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     const float zmin = Ap->z_min, zmax = Ap->z_max, vmin = Ap->v_min, vmax = Ap->v_max, mempty = Ap->m_empty;
     const float gA = kind ? Ap->theta_F : Ap->beta_f;
     const float z_tf = Ap->z_tf, v_D = Ap->v_D;
+    const float inv_m0 = 1.0f / Ap->x0[5];
 
     uint32_t cbad[2];
     {
@@ -901,12 +917,13 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 
     for (uint32_t s = 0; s < S; s += 2) {
         const bool two = s + 1 < S;                                // odd S: the second chain is not counted
-        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2];
+        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2], im[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             x[q] = vsplat<V>(Ap->x0[0]); y[q] = vsplat<V>(Ap->x0[1]); z[q] = vsplat<V>(Ap->x0[2]);
             v[q] = vsplat<V>(Ap->x0[3]); chi[q] = vsplat<V>(Ap->x0[4]); m[q] = vsplat<V>(Ap->x0[5]);
             fuel[q] = sA[q] = sB[q] = sC[q] = sN[q] = vsplat<V>(0.0f);
+            im[q] = vsplat<V>(inv_m0);
         }
         int landedm[2] = {0, 0}, violm[2] = {0, 0};
         float2 Zr[ENS];
@@ -1014,9 +1031,18 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 nx[q] = vfma(dtf, vfma(vcg, cch, wx), x[q]);
                 ny[q] = vfma(dtf, vfma(vcg, sch, wy), y[q]);
                 nz[q] = vfma(dtf * v[q], sga, z[q]);
+#if SMC_K2_INVM
+                nv[q] = vfma(dtf, vfma(T - D, im[q], sga * (-g)), v[q]);
+#else
                 nv[q] = vfma(dtf, vfma(T - D, vmap(m[q], rcp_approx), sga * (-g)), v[q]);
+#endif
                 nchi[q] = wrap_pi(vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]));
                 nm[q] = vfma(-dtef[q], T, m[q]);
+#if SMC_K2_INVM
+                // 1/m_{t+1} by one Newton step from 1/m_t: the mass changes by dt eta T ~ 1e-4 m per step,
+                // so the relative error squares to ~1e-8 and does not accumulate
+                im[q] = im[q] * vfma(-nm[q], im[q], 2.0f);
+#endif
                 vnowm[q] = 0;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -1091,7 +1117,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         const float zz = cget(nz[q], c) * sc.inv_Ac;
-                        const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, cget(nx[q], c), cget(ny[q], c));
+                        const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, s_pop, cget(nx[q], c), cget(ny[q], c));
                         cset(sN[q], c, cget(sN[q], c) + (((flym[q] >> c) & 1) ? nzs
                                                                                : ((act && ((landedm[q] >> c) & 1)) ? 1.0f : 0.0f)));
                     }
@@ -1193,7 +1219,8 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 
 template <int W, int R>
 static cudaError_t launch_2s_r(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
-    const size_t smem = rollout2s_smem_bytes(W, sc.H);
+    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx, sc.pop_ny) : 0;
+    const size_t smem = rollout2s_smem_bytes(W, sc.H, (npop + 3) & ~3);
     auto kern = k_rollout_2s<W, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -90,6 +90,7 @@ cudaError_t launch_scan_cluster(const ResampleArgs &r, cudaStream_t st);
 cudaError_t launch_ancestors(const ResampleArgs &r, cudaStream_t st);          // K5 merge path (needs r.splits)
 size_t mp_split_words(uint32_t L, uint32_t M);
 cudaError_t launch_ancestors_bisect(const ResampleArgs &r, cudaStream_t st);   // one bisection per slot
+cudaError_t launch_ancestors_two_level(const ResampleArgs &r, cudaStream_t st); // K6's search (needs r.Cs)
 
 // K6: gather survivors' rows by ancestor, Gaussian proposal (Alg.1 l.22-23)
 struct ProposeArgs {

@@ -414,11 +414,11 @@ def test_per_aircraft_mh_rounds(smc):
     sol.close()
 
 
-@pytest.mark.parametrize("mode", ["mp", "bisect"])
+@pytest.mark.parametrize("mode", ["mp", "bisect", "bisect2"])
 @pytest.mark.parametrize("L", [1, 7, 2048, 2049, 5000, 70001, 300001])
 def test_resample_bitexact(smc, L, mode, monkeypatch):
-    """Ancestors bit-exact against the oracle, by the merge-path K5 and by the
-    per-slot bisection (SMC_ANC)."""
+    """Ancestors bit-exact against the oracle, by the merge-path K5, the per-slot bisection
+    and K6's production two-level search through K4's every-16th CDF samples (SMC_ANC)."""
     monkeypatch.setenv("SMC_ANC", mode)
     scn, cfg = sc.config(1)
     sol = _solver(smc, scn, seed=cfg.seed)
@@ -455,8 +455,9 @@ def test_resample_scan_variants_bitexact(smc, L, scan, monkeypatch):
         assert Q[i] == r["Q"] and np.array_equal(anc[i], r["anc"]), i
 
 
-@pytest.mark.parametrize("mode", ["mp", "bisect"])
-@pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000), (1, 1), (3, 1)])
+@pytest.mark.parametrize("mode", ["mp", "bisect", "bisect2"])
+@pytest.mark.parametrize("L,M", [(5000, 1), (5000, 777), (5000, 4999), (2049, 1500), (70001, 30000), (1, 1), (3, 1),
+                                 (4099, 4099), (17, 5)])
 def test_resample_to_fewer_bitexact(smc, L, M, mode, monkeypatch):
     """Shrinking populations: M < L slots drawn from L particles."""
     monkeypatch.setenv("SMC_ANC", mode)
