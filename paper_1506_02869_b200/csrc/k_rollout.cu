@@ -813,9 +813,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #ifndef SMC_K2_MINB2S
 #define SMC_K2_MINB2S 3
 #endif
-#ifndef SMC_K2_INVM
-#define SMC_K2_INVM 0   // 1/m carried by one Newton step per step instead of a MUFU reciprocal
-#endif
+
 #ifndef SMC_K2_TUNROLL2S
 #define SMC_K2_TUNROLL2S 1
 #endif
@@ -870,7 +868,6 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     const float zmin = Ap->z_min, zmax = Ap->z_max, vmin = Ap->v_min, vmax = Ap->v_max, mempty = Ap->m_empty;
     const float gA = kind ? Ap->theta_F : Ap->beta_f;
     const float z_tf = Ap->z_tf, v_D = Ap->v_D;
-    const float inv_m0 = 1.0f / Ap->x0[5];
 
     uint32_t cbad[2];
     {
@@ -917,13 +914,12 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 
     for (uint32_t s = 0; s < S; s += 2) {
         const bool two = s + 1 < S;                                // odd S: the second chain is not counted
-        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2], im[2];
+        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             x[q] = vsplat<V>(Ap->x0[0]); y[q] = vsplat<V>(Ap->x0[1]); z[q] = vsplat<V>(Ap->x0[2]);
             v[q] = vsplat<V>(Ap->x0[3]); chi[q] = vsplat<V>(Ap->x0[4]); m[q] = vsplat<V>(Ap->x0[5]);
             fuel[q] = sA[q] = sB[q] = sC[q] = sN[q] = vsplat<V>(0.0f);
-            im[q] = vsplat<V>(inv_m0);
         }
         int landedm[2] = {0, 0}, violm[2] = {0, 0};
         float2 Zr[ENS];
@@ -1031,18 +1027,9 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 nx[q] = vfma(dtf, vfma(vcg, cch, wx), x[q]);
                 ny[q] = vfma(dtf, vfma(vcg, sch, wy), y[q]);
                 nz[q] = vfma(dtf * v[q], sga, z[q]);
-#if SMC_K2_INVM
-                nv[q] = vfma(dtf, vfma(T - D, im[q], sga * (-g)), v[q]);
-#else
                 nv[q] = vfma(dtf, vfma(T - D, vmap(m[q], rcp_approx), sga * (-g)), v[q]);
-#endif
                 nchi[q] = wrap_pi(vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]));
                 nm[q] = vfma(-dtef[q], T, m[q]);
-#if SMC_K2_INVM
-                // 1/m_{t+1} by one Newton step from 1/m_t: the mass changes by dt eta T ~ 1e-4 m per step,
-                // so the relative error squares to ~1e-8 and does not accumulate
-                im[q] = im[q] * vfma(-nm[q], im[q], 2.0f);
-#endif
                 vnowm[q] = 0;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
