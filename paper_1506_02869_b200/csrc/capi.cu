@@ -71,18 +71,11 @@ constexpr size_t kIpcRec = 128;     // cudaIpcMemHandle_t (64 B) + workspace off
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, part, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, centres,
+    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Qall, Csall, Sc, Sall, survp, ipc, pZ, pzi, pstates,
         pnext, pflags, papplied, lohi, wmap, flag, infround, infcol,
         qf, qd, total;
 };
-
-// Partial log-weight buffer of chunked K2 launches: up to 8 sample chunks x 2
-// candidates, capped at 64 MiB (large populations fill the GPU without chunking).
-size_t part_bytes(uint32_t Lloc, int nmax) {
-    const size_t full = (size_t)8 * 2 * nmax * Lloc * sizeof(float);
-    return full < ((size_t)64 << 20) ? full : ((size_t)64 << 20);
-}
 
 // Bump-allocate every device buffer from the caller's workspace.
 size_t record_bytes(int nmax, int Hmax) { return (16 + (size_t)nmax * Hmax * 12 + 15) & ~(size_t)15; }
@@ -106,7 +99,6 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     auto take = [&](size_t bytes) { size_t at = off; off += align_up(bytes); return at; };
     const size_t row = (size_t)Lloc * nmax * Hmax * 3 * sizeof(float);
     o.ctrl = take(4 * row);
-    o.part = take(part_bytes(Lloc, nmax));
     o.ell = take((size_t)nmax * Lloc * sizeof(float));
     o.lam = take((size_t)Lloc * sizeof(double));
     o.lam2 = take(2 * (size_t)Lloc * sizeof(double));
@@ -181,9 +173,8 @@ struct smc_ctx {
     char *ws = nullptr;
     Layout lay{};
     float *ctrl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    float *ell = nullptr, *part = nullptr;
-    size_t part_cap = 0;
-    int nsm = 148, bps[2] = {0, 0};
+    float *ell = nullptr;
+    int nsm = 148;
     double *lam = nullptr, *lam2 = nullptr;
     uint32_t *surv = nullptr;          // survivor masks (bit i: aircraft i's row from x*)
     int last_nc = 1;                   // candidates evaluated by the last round
@@ -246,7 +237,6 @@ struct smc_ctx {
     int cur = 0, last_eval = -1;
     uint64_t launches = 0;
     uint64_t io_h2d = 0, io_d2h = 0;   // host<->device bytes of the production path
-    bool chunking = false;             // SMC_K2_CHUNKS=1: sample-chunked K2 launches
     int anc_mode = -1;                 // SMC_ANC: 1 merge-path K5, 0 bisection in K6, -1 by size
     int32_t *anc = nullptr;            // [n][Lloc] K5 ancestors
     uint32_t *splits = nullptr;        // K5 merge-path split points
@@ -559,8 +549,6 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
         return SMC_EINVAL;
     }
     {
-        const char *ch = getenv("SMC_K2_CHUNKS");
-        ctx->chunking = ch && strcmp(ch, "1") == 0;
         // ancestors: merge-path K5 + K6 reading them ("mp"), or bisection inside K6 ("bisect");
         // default by population size
         const char *sm = getenv("SMC_SCAN");
@@ -604,8 +592,6 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->ctrl[1][0] = cb + 2 * prow;
     ctx->ctrl[1][1] = cb + 3 * prow;
     ctx->ell = (float *)(ws + L.ell);
-    ctx->part = (float *)(ws + L.part);
-    ctx->part_cap = part_bytes(max_local(ctx->Lg, world), ctx->nmax);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
     ctx->lam = (double *)(ws + L.lam);
     ctx->lam2 = (double *)(ws + L.lam2);
@@ -976,8 +962,6 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
                           scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
-    ctx->bps[0] = rollout_blocks_per_sm((int)n, (int)H, 1, ctx->dsc.wng);
-    ctx->bps[1] = rollout_blocks_per_sm((int)n, (int)H, 2, ctx->dsc.wng);
     ctx->have_scn = true;
     return init_population(ctx);
 }
@@ -1043,22 +1027,6 @@ static smc_status run_round(smc_ctx *ctx, bool tail, smc_round_stats *stats) {
     ra.ell0 = (float)(-std::log2((double)(ctx->Lfinal ? Lk : ctx->Lg)));
     ra.ell_out = ctx->ell; ra.lam_out = ctx->lam; ra.surv_out = ctx->surv; ra.colmax = ctx->colmax;
     ra.n_accept = ctx->accept; ra.lam_cand = ctx->lam2;
-    {
-        // wave planning: split the S samples into chunks when the particle grid
-        // alone would leave a large partial wave (fixed-order partial sums)
-        const int W = segment_width(n, ctx->dsc.wng > 8);
-        const double B = std::ceil((double)ctx->Lloc / (double)(128 / W));
-        const double slots = (double)std::max(1, ctx->bps[NC - 1]) * ctx->nsm;
-        auto eff = [&](int c) { const double w = B * c / slots; return w / std::ceil(w); };
-        int best = 1;
-        double be = eff(1);
-        for (int c = 2; c <= 8 && (uint32_t)c <= S; ++c) {
-            const size_t need = (size_t)c * NC * n * ctx->Lloc * sizeof(float);
-            if (need > ctx->part_cap) break;
-            if (eff(c) > be + 0.03) { be = eff(c); best = c; }
-        }
-        if (best > 1 && ctx->chunking) { ra.part = ctx->part; ra.chunks = best; }
-    }
     LAUNCHP(PH_ROLLOUT, launch_rollout(ctx->dsc, ra, NC, false, ctx->st));
     ctx->last_eval = P;
     ctx->Leval = Lk;

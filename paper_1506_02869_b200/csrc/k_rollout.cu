@@ -274,7 +274,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
     float ell[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) ell[c] = (args.part || (SP && c == 1)) ? 0.0f : args.ell0;
+    for (int c = 0; c < NC; ++c) ell[c] = (SP && c == 1) ? 0.0f : args.ell0;
 
     using V = vec_t<NC>;
     const float dt = sc.dt, g = sc.g;
@@ -287,9 +287,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     //   departure A = theta - theta_F, B = z_tf - z;  arrival A = chi - pi - 2 theta (R8), B = beta - beta_f
     const float cA_th = kind ? 1.0f : -2.0f, cA_chi = kind ? 0.0f : 1.0f, cA_0 = kind ? -gA : -kPi;
     const float cB_z = kind ? -1.0f : 0.0f, cB_b = kind ? 0.0f : 1.0f, cB_0 = kind ? z_tf : -gA;
-    // sample chunk of this block (gridDim.y > 1: partial sums, combined by k_combine)
-    const uint32_t s_lo = (uint32_t)(((uint64_t)args.S * blockIdx.y) / gridDim.y);
-    const uint32_t s_hi = (uint32_t)(((uint64_t)args.S * (blockIdx.y + 1)) / gridDim.y);
+    const uint32_t s_lo = 0, s_hi = args.S;
     for (uint32_t s = s_lo; s < s_hi; s += NSL) {
         V x = vsplat<V>(Ap->x0[0]), y = vsplat<V>(Ap->x0[1]), z = vsplat<V>(Ap->x0[2]);
         V v = vsplat<V>(Ap->x0[3]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
@@ -723,14 +721,6 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 
     constexpr int ENC = SP ? 1 : NC;               // candidates in the epilogue
     if constexpr (SP) ell[0] = ell[0] + ell[1];    // both slots' samples of the single candidate
-    if (args.part) {      // chunked evaluation: partial log2 weights, MH in k_combine
-        if (valid && isac) {
-#pragma unroll
-            for (int c = 0; c < ENC; ++c)
-                args.part[(((size_t)blockIdx.y * ENC + c) * n + lane) * args.L + lloc] = ell[c];
-        }
-        return;
-    }
     // ---------------- epilogue: lambda (double, ascending i), MH (R1), survivor
     __syncthreads();
     float *s_ell = reinterpret_cast<float *>(s_pos);          // reuse [NC][kBlock]
@@ -1230,68 +1220,6 @@ size_t rollout_smem_bytes(int W, int NC, int H, int ng, bool sp) {
            sizeof(float4) * 3 * kBlock + sizeof(float) * 72 + 16;
 }
 
-// Combine the sample chunks of a chunked K2 launch (fixed chunk order):
-// ell_c,i = ell0 + sum_y part[y][c][i] (-inf absorbs), lambda in double over
-// ascending i, MH decision (R1), survivor stores and the column max.
-template <int NC>
-__global__ void k_combine(const DevScen sc, const RolloutArgs args, int chunks) {
-    const uint32_t lloc = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = lloc < args.L;
-    const int n = sc.n;
-    const uint32_t L = args.L;
-    double lam[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        lam[c] = 0.0;
-        for (int i = 0; i < n && valid; ++i) {
-            float e = args.ell0;
-            for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + c) * n + i) * L + lloc];
-            lam[c] += (double)e;
-        }
-    }
-    const uint32_t l = args.l0 + lloc;
-    auto ell_of = [&](int c, int i) {
-        float e = args.ell0;
-        for (int y = 0; y < chunks; ++y) e += args.part[(((size_t)y * NC + c) * n + i) * L + lloc];
-        return e;
-    };
-    uint32_t mask = args.surv_single;
-    if (NC == 2 && valid) {
-        if (args.mh_mode == 2) {             // per-aircraft MH (R46)
-            mask = 0u;
-            for (int i = 0; i < n; ++i)
-                if (mh_decide_aircraft((double)ell_of(0, i), (double)ell_of(1, i), l, (uint32_t)i, args.k, *args.mpcp,
-                                       sc.key0, sc.key1))
-                    mask |= 1u << i;
-        } else {
-            mask = mh_decide(lam[0], lam[1], l, args.k, *args.mpcp, sc.key0, sc.key1) ? 0xFFFFFFFFu : 0u;
-        }
-    }
-    double lam_s = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const int cs = (NC == 2 && ((mask >> i) & 1u)) ? 1 : 0;
-        float e = args.ell0;
-        if (valid) {
-            e = ell_of(cs, i);
-            args.ell_out[(size_t)i * L + lloc] = e;
-            lam_s += (double)e;
-        }
-        const uint32_t mx = __reduce_max_sync(0xffffffffu, valid ? f2ord(e) : 0u);
-        if ((threadIdx.x & 31) == 0 && mx) atomicMax(&args.colmax[i], mx);
-    }
-    if (valid) {
-        args.lam_out[lloc] = lam_s;
-        args.surv_out[lloc] = mask;
-        if (args.lam_cand) { args.lam_cand[lloc] = lam[0]; args.lam_cand[L + lloc] = lam[NC - 1]; }
-    }
-    if (NC == 2) {
-        const int mine = valid ? (args.mh_mode == 2 ? __popc(mask & (n == 32 ? 0xFFFFFFFFu : ((1u << n) - 1u)))
-                                                    : (mask ? 1 : 0)) : 0;
-        const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)mine);
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(args.n_accept, (unsigned long long)cnt);
-    }
-}
-
 template <int W, int NC, bool DEBUG, bool DENSE, int R = W, bool SP = false>
 static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     const size_t smem = rollout_smem_bytes(W, NC, sc.H, DENSE ? sc.wng : 8, SP);
@@ -1301,32 +1229,8 @@ static cudaError_t launch_w(const DevScen &sc, const RolloutArgs &a, cudaStream_
     const int segs = kBlock / W;
     const unsigned grid = (a.L + segs - 1) / segs;
     if (grid == 0) return cudaSuccess;
-    const int chunks = (a.part && !DEBUG) ? (a.chunks < 1 ? 1 : a.chunks) : 1;
-    RolloutArgs b = a;
-    if (chunks == 1) b.part = nullptr;
-    kern<<<dim3(grid, chunks), kBlock, smem, st>>>(sc, b);
-    e = cudaGetLastError();
-    if (e != cudaSuccess || chunks == 1) return e;
-    k_combine<SP ? 1 : NC><<<(a.L + 127) / 128, 128, 0, st>>>(sc, b, chunks);
+    kern<<<grid, kBlock, smem, st>>>(sc, a);
     return cudaGetLastError();
-}
-
-// Resident K2 blocks per SM for this problem shape (wave-quantisation planning).
-int rollout_blocks_per_sm(int n, int H, int NC, int ng) {
-    const bool dense = ng > 8;
-    const int W = segment_width(n, dense);
-    const size_t smem = rollout_smem_bytes(W, NC, H, ng);
-    int nb = 0;
-#define SMC_OCC(WW, DN)                                                                                \
-    if (W == WW && dense == DN) {                                                                      \
-        auto kern = NC == 2 ? k_rollout<WW, 2, false, DN> : k_rollout<WW, 1, false, DN>;               \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem);                        \
-    }
-    SMC_OCC(1, false) SMC_OCC(2, false) SMC_OCC(4, false) SMC_OCC(8, false) SMC_OCC(16, false) SMC_OCC(32, false)
-    SMC_OCC(4, true) SMC_OCC(8, true) SMC_OCC(16, true) SMC_OCC(32, true)
-#undef SMC_OCC
-    return nb;
 }
 
 static bool ring_enabled() {
@@ -1443,7 +1347,7 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
-    if (NC == 2 && !debug && !dense && W >= 16 && !a.part && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
+    if (NC == 2 && !debug && !dense && W >= 16 && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }

@@ -21,8 +21,6 @@ struct RolloutArgs {
     uint32_t *surv_out;        // [L] survivor mask: bit i set = aircraft i's row comes from x*
     uint32_t *colmax;          // [n] ordered-float max of ell_out (atomicMax)
     unsigned long long *n_accept;
-    float *part;               // [chunks][NC][n][L] partial log2 weights (chunked launch) or NULL
-    int chunks;                // sample chunks (grid.y) when part != NULL
     // debug outputs (candidate 0), per (l, s, i)
     float *dbg_J, *dbg_comp, *dbg_fuel, *dbg_traj, *dbg_ell_c;
     uint8_t *dbg_viol;
@@ -31,7 +29,6 @@ struct RolloutArgs {
 
 constexpr int kMaxWindNodes = 64;   // N_x N_y N_z
 int segment_width(int n, bool dense = false);
-int rollout_blocks_per_sm(int n, int H, int NC, int ng = 8);
 size_t rollout_smem_bytes(int W, int NC, int H, int ng = 8, bool sp = false);
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st);
 
