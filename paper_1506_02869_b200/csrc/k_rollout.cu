@@ -811,22 +811,35 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 constexpr int kPopSmem = 8192;
 __host__ __device__ inline int pop_smem_floats(int nx, int ny) { return nx * ny <= kPopSmem ? nx * ny : 0; }
 
+// Segments of W lanes that do not divide a warp (W = 12, 20, 24, ...) are packed contiguously over
+// the block and cross warp boundaries: their exchanges synchronise the block and the verdict
+// hand-back goes through shared memory.  The block's last kBlock mod W threads form a phantom
+// segment (own scratch, no particle).
+__host__ __device__ constexpr bool k2_cross_warp(int W) { return (32 % W) != 0; }
+__host__ __device__ constexpr int k2_segs_alloc(int W) { return kBlock / W + (k2_cross_warp(W) && kBlock % W ? 1 : 0); }
+
 size_t rollout2s_smem_bytes(int W, int H, int npop) {
-    const int SEGS = kBlock / W, GB = W / 4;
+    const int SEGA = k2_segs_alloc(W), GB = W / 4;
+    const size_t pos = (size_t)2 * SEGA * W;                      // entries per position array
     return sizeof(float) * (size_t)npop + sizeof(float4) * ((size_t)H * 2 * kBlock)              // controls
-           + sizeof(float) * (SEGS * 2 * GB * 16                  // normals [SEGS][slot][GB][16]
-                              + SEGS * 2 * 16                     // AR(1) state [SEGS][slot][8] (x, y)
-                              + SEGS * 2 * 16)                    // coefficients [SEGS][slot][16]
-           + sizeof(float4) * 6 * kBlock                          // positions x4, y4, z4, each twice
+           + sizeof(float) * (SEGA * 2 * GB * 16                  // normals [SEGA][slot][GB][16]
+                              + SEGA * 2 * 16                     // AR(1) state [SEGA][slot][8] (x, y)
+                              + SEGA * 2 * 16)                    // coefficients [SEGA][slot][16]
+           + sizeof(float4) * 3 * pos                             // positions x4, y4, z4, each twice
+           + (k2_cross_warp(W) ? sizeof(uint32_t) * (size_t)(W / 2) * SEGA * W : 0)   // verdicts
            + sizeof(float) * 72 + 16;
 }
 
 template <int W, int R>
 __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
-    static_assert(W >= 8, "two-chain instances need W >= 8 (eight AR(1) nodes per slot)");
-    constexpr int NSL = 2, SEGS = kBlock / W, GB = W / 4;
+    static_assert(W >= 8 && W % 4 == 0, "two-chain instances need W >= 8 (eight AR(1) nodes per slot), W = 4 GB");
+    constexpr bool XW = k2_cross_warp(W);
+    static_assert(!XW || R == W, "packed segments use the whole segment as the separation ring");
+    constexpr int NSL = 2, SEGS = kBlock / W, SEGA = k2_segs_alloc(W), GB = W / 4;
     constexpr int ENS = W >= 16 ? 1 : 2;                          // (node, slot) pairs a lane owns
     constexpr int TU2 = SMC_K2_TUNROLL2S;
+    // exchange barrier of a segment: its warp, or the block when segments cross warps
+    auto seg_sync = [] { if constexpr (XW) __syncthreads(); else __syncwarp(); };
     extern __shared__ __align__(16) float smem_all[];
     const int H = sc.H, n = sc.n;
     const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx, sc.pop_ny) : 0;
@@ -836,16 +849,18 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
         for (int e = threadIdx.x; e < npop; e += kBlock) smem_all[e] = __ldg(&sc.pop[e]);
         s_pop = smem_all;
     }
+    constexpr int NPOS = 2 * SEGA * W;                           // entries per position array
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);           // [H][2][kBlock]
     float *s_V = reinterpret_cast<float *>(s_ctrl + H * 2 * kBlock);
-    float *s_Z = s_V + SEGS * NSL * GB * 16;
-    float *s_W = s_Z + SEGS * NSL * 16;
-    float4 *s_p4 = reinterpret_cast<float4 *>(s_W + SEGS * NSL * 16);   // [3][2 kBlock]: x4, y4, z4
-    float *s_Q = reinterpret_cast<float *>(s_p4 + 6 * kBlock);
+    float *s_Z = s_V + SEGA * NSL * GB * 16;
+    float *s_W = s_Z + SEGA * NSL * 16;
+    float4 *s_p4 = reinterpret_cast<float4 *>(s_W + SEGA * NSL * 16);   // [3][NPOS]: x4, y4, z4
+    uint32_t *s_hv = reinterpret_cast<uint32_t *>(s_p4 + 3 * NPOS);   // [W/2][SEGA W] verdicts (XW)
+    float *s_Q = reinterpret_cast<float *>(s_hv + (XW ? (W / 2) * SEGA * W : 0));
 
     const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
     const uint32_t lloc = blockIdx.x * SEGS + seg;
-    const bool valid = lloc < args.L;
+    const bool valid = seg < SEGS && lloc < args.L;
     const uint32_t l = args.l0 + lloc;
     const bool isac = lane < n;
     const uint32_t k = args.k, mpc = *args.mpcp;
@@ -899,7 +914,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     const float cA_th = kind ? 1.0f : -2.0f, cA_chi = kind ? 0.0f : 1.0f, cA_0 = kind ? -gA : -kPi;
     const float cB_z = kind ? -1.0f : 0.0f, cB_b = kind ? 0.0f : 1.0f, cB_0 = kind ? z_tf : -gA;
     const int pb = seg * 2 * W + lane;                             // own entry; + R: duplicate
-    float4 *const s_px = s_p4, *const s_py = s_p4 + 2 * kBlock, *const s_pz = s_p4 + 4 * kBlock;
+    float4 *const s_px = s_p4, *const s_py = s_p4 + NPOS, *const s_pz = s_p4 + 2 * NPOS;
     const uint32_t S = args.S;
 
     for (uint32_t s = 0; s < S; s += 2) {
@@ -931,32 +946,40 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                     }
                 }
             }
-            __syncwarp();
+            seg_sync();
             float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16 * NSL);
+            // (node, slot) pair pq of the 16 a segment advances: W >= 16: pair lane mod 16 (duplicates
+            // store identical values); W = 8: pairs lane and lane + 8; W = 12: lane and lane + 12 < 16
+            constexpr bool QREG = (W % 8) == 0;                 // node = lane mod 8 for every pair
 #pragma unroll
             for (int e = 0; e < ENS; ++e) {
                 const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
-                const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
-                const float2 ve = make_float2(vv[node], vv[8 + node]);
-                Zr[e] = (t == 0) ? ve : vfma(Zr[e], sc.a, ve * sc.b);
-                sZ2[sl * 8 + node] = Zr[e];
-            }
-            __syncwarp();
-#pragma unroll
-            for (int e = 0; e < ENS; ++e) {
-                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
-                const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
-                float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-                for (int mm = 0; mm < 4; ++mm) {
-                    const float4 zz = z4[mm];
-                    acc = vfma(make_float2(zz.x, zz.y), qrow[2 * mm], acc);
-                    acc = vfma(make_float2(zz.z, zz.w), qrow[2 * mm + 1], acc);
+                if (W >= 16 || pq < 16) {
+                    const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
+                    const float2 ve = make_float2(vv[node], vv[8 + node]);
+                    Zr[e] = (t == 0) ? ve : vfma(Zr[e], sc.a, ve * sc.b);
+                    sZ2[sl * 8 + node] = Zr[e];
                 }
-                s_W[(seg * NSL + sl) * 16 + node] = acc.x;
-                s_W[(seg * NSL + sl) * 16 + 8 + node] = acc.y;
             }
-            __syncwarp();
+            seg_sync();
+#pragma unroll
+            for (int e = 0; e < ENS; ++e) {
+                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
+                if (W >= 16 || pq < 16) {
+                    const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
+                    const float *qr = QREG ? qrow : &s_Q[node * 9];
+                    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float4 zz = z4[mm];
+                        acc = vfma(make_float2(zz.x, zz.y), qr[2 * mm], acc);
+                        acc = vfma(make_float2(zz.z, zz.w), qr[2 * mm + 1], acc);
+                    }
+                    s_W[(seg * NSL + sl) * 16 + node] = acc.x;
+                    s_W[(seg * NSL + sl) * 16 + 8 + node] = acc.y;
+                }
+            }
+            seg_sync();
             // gusts (R15): one Philox call per sample covers steps 2u and 2u+1
             float gxq[2] = {sc.nominal[0], sc.nominal[0]}, gyq[2] = {sc.nominal[1], sc.nominal[1]};
             if (sc.turb_sigma > 0.0f) {
@@ -1059,7 +1082,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 s_py[pb] = ey; s_py[pb + R] = ey;
                 s_pz[pb] = ez; s_pz[pb + R] = ez;
             }
-            __syncwarp();
+            seg_sync();
             // verdict bytes: bit 31 (sample s, candidate 0), 23 (s, 1), 15 (s + 1, 0), 7 (s + 1, 1)
             uint32_t confw = 0u;
 #pragma unroll
@@ -1075,10 +1098,21 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 const uint32_t lo = __byte_perm(__float_as_uint(u1.x) & __float_as_uint(w1.x),
                                                 __float_as_uint(u1.y) & __float_as_uint(w1.y), 0x3737);
                 const uint32_t hv = (hi & 0xFFFF0000u) | (lo & 0x0000FFFFu);
-                if (2 * d < R)
-                    confw |= hv | __shfl_sync(0xffffffffu, hv, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
-                else
+                if constexpr (XW) {
+                    // partner lane + d learns this verdict from shared memory after the scan
+                    if (2 * d < R) s_hv[(d - 1) * (SEGA * W) + seg * W + lane] = hv;
                     confw |= hv;
+                } else if (2 * d < R) {
+                    confw |= hv | __shfl_sync(0xffffffffu, hv, R == W ? lane + W - d : (lane >= d ? lane - d : lane - d + R), W);
+                } else {
+                    confw |= hv;
+                }
+            }
+            if constexpr (XW) {
+                seg_sync();
+#pragma unroll
+                for (int d = 1; 2 * d < R; ++d)
+                    confw |= s_hv[(d - 1) * (SEGA * W) + seg * W + (lane >= d ? lane - d : lane - d + R)];
             }
             const int confm[2] = {(int)((confw >> 31) | ((confw >> 22) & 2u)), (int)(((confw >> 15) & 1u) | ((confw >> 6) & 2u))};
             // ---------------- 5. per chain: cost terms, flags, state update
@@ -1142,7 +1176,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     int *s_dec = reinterpret_cast<int *>(s_V);
     s_ell[tid] = ell[0];
     s_ell[kBlock + tid] = ell[1];
-    __syncwarp();
+    seg_sync();
     double lam[2] = {0.0, 0.0};
     for (int i = 0; i < n; ++i) {
         lam[0] += (double)s_ell[seg * W + i];
@@ -1155,8 +1189,16 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     if (args.mh_mode == 2) {
         const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[1], l, (uint32_t)lane, k, mpc, sc.key0,
                                                    sc.key1);
-        const unsigned b = __ballot_sync(0xffffffffu, ai);
-        mask = (W == 32) ? b : ((b >> ((tid & 31) & ~(W - 1))) & ((1u << (W & 31)) - 1u));
+        if constexpr (XW) {                                       // segments cross warps: via shared memory
+            uint32_t *s_ai = reinterpret_cast<uint32_t *>(s_ell + 2 * kBlock);
+            s_ai[tid] = ai ? 1u : 0u;
+            __syncthreads();
+            mask = 0u;
+            for (int i = 0; i < n; ++i) mask |= s_ai[seg * W + i] << i;
+        } else {
+            const unsigned b = __ballot_sync(0xffffffffu, ai);
+            mask = (W == 32) ? b : ((b >> ((tid & 31) & ~(W - 1))) & ((1u << (W & 31)) - 1u));
+        }
         ell_s = ai ? ell[1] : ell[0];
         lam_s = 0.0;
         for (int i = 0; i < n; ++i) lam_s += (double)s_ell[(((mask >> i) & 1u) ? kBlock : 0) + seg * W + i];
@@ -1245,7 +1287,19 @@ static bool ns2_enabled() {
 
 // Two-candidate launches on the 2x2x2 grid with W >= 16: two sample chains per lane (k_rollout_2s);
 // SMC_K2_2S=0 runs one sample per lane (k_rollout<W, 2>).
+static bool pack_enabled() {
+    static const bool on = [] { const char *e = getenv("SMC_K2_PACK"); return !(e && strcmp(e, "0") == 0); }();
+    return on;
+}
+
 static cudaError_t launch_2s(int W, int R, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
+    // packed segments (W not dividing a warp, ring = segment): 9-12 aircraft in 12 lanes (10 per block),
+    // 17-20 in 20 (6 per block), 21-24 in 24 (5 per block) -- instead of 16- / 32-lane segments
+    if (pack_enabled()) {
+        if (sc.n >= 9 && sc.n <= 12) return launch_2s_r<12, 12>(sc, a, st);
+        if (sc.n >= 17 && sc.n <= 20) return launch_2s_r<20, 20>(sc, a, st);
+        if (sc.n >= 21 && sc.n <= 24) return launch_2s_r<24, 24>(sc, a, st);
+    }
     switch (W) {
         case 16:
             if (R == 10) return launch_2s_r<16, 10>(sc, a, st);
