@@ -804,6 +804,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #define SMC_K2_MINB2S 3
 #endif
 
+#ifndef SMC_K2_2S_MINW
+#define SMC_K2_2S_MINW 16   // narrowest segment launched with two sample chains (c2's W = 8 measured faster with one)
+#endif
 #ifndef SMC_K2_TUNROLL2S
 #define SMC_K2_TUNROLL2S 1
 #endif
@@ -1301,6 +1304,11 @@ static cudaError_t launch_2s(int W, int R, const DevScen &sc, const RolloutArgs 
         if (sc.n >= 21 && sc.n <= 24) return launch_2s_r<24, 24>(sc, a, st);
     }
     switch (W) {
+#if SMC_K2_2S_MINW <= 8
+        case 8:
+            if (R == 6) return launch_2s_r<8, 6>(sc, a, st);
+            return launch_2s_r<8, 8>(sc, a, st);
+#endif
         case 16:
             if (R == 10) return launch_2s_r<16, 10>(sc, a, st);
             if (R == 12) return launch_2s_r<16, 12>(sc, a, st);
@@ -1401,7 +1409,7 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
-    if (NC == 2 && !debug && !dense && W >= 16 && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
+    if (NC == 2 && !debug && !dense && W >= SMC_K2_2S_MINW && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }
