@@ -71,7 +71,7 @@ constexpr size_t kIpcRec = 128;     // cudaIpcMemHandle_t (64 B) + workspace off
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, centres,
+    size_t ctrl, ell, lam, lam2, surv, colmax, Q, ess, status, tiles, C, QR, anc, splits, Cs, accept, mpc, dac, pop, popp, centres,
         part_lam, part_idx, done, best_lam, best_idx, best_row, Call, Qall, Csall, Sc, Sall, survp, ipc, pZ, pzi, pstates,
         pnext, pflags, papplied, lohi, wmap, flag, infround, infcol,
         qf, qd, total;
@@ -117,6 +117,7 @@ Layout layout(uint32_t Lloc, int nmax, int Hmax, int world = 1, int vworld = 1) 
     o.mpc = take(sizeof(uint32_t));
     o.dac = take(nmax * sizeof(DevAircraft));
     o.pop = take(kPopCap * sizeof(float));
+    o.popp = take((2 * kPopCap + 2) * sizeof(float));           // (nx + 1)(ny + 1) <= 2 nx ny + 2
     o.centres = take(kCentreCap * 3 * sizeof(double));
     o.part_lam = take(512 * sizeof(double));
     o.part_idx = take(512 * sizeof(long long));
@@ -183,7 +184,7 @@ struct smc_ctx {
     double *ess = nullptr;
     uint32_t *mpc_dev = nullptr;
     DevAircraft *dac = nullptr;
-    float *pop = nullptr, *best_row = nullptr, *papplied = nullptr, *lohi = nullptr;
+    float *pop = nullptr, *popp = nullptr, *best_row = nullptr, *papplied = nullptr, *lohi = nullptr;
     double *centres = nullptr, *part_lam = nullptr, *best_lam = nullptr, *pZ = nullptr, *pstates = nullptr,
            *pnext = nullptr;
     long long *part_idx = nullptr, *best_idx = nullptr;
@@ -610,6 +611,7 @@ extern "C" smc_status smc_init(const smc_config *cfg, smc_ctx **out) {
     ctx->mpc_dev = (uint32_t *)(ws + L.mpc);
     ctx->dac = (DevAircraft *)(ws + L.dac);
     ctx->pop = (float *)(ws + L.pop);
+    ctx->popp = (float *)(ws + L.popp);
     ctx->centres = (double *)(ws + L.centres);
     ctx->part_lam = (double *)(ws + L.part_lam);
     ctx->part_idx = (long long *)(ws + L.part_idx);
@@ -752,6 +754,12 @@ static smc_status build_constants(smc_ctx *ctx) {
     d.inv_Ac = (float)(1.0 / s.A_c);
     d.pop_nx = (int)s.pop_nx; d.pop_ny = (int)s.pop_ny;
     d.pop_x0 = (float)s.pop_x0; d.pop_y0 = (float)s.pop_y0; d.pop_inv_dx = (float)(1.0 / s.pop_dx);
+    {
+        const double mx = s.pop_nx > 1 ? (double)(s.pop_nx - 1) : 0.0, my = s.pop_ny > 1 ? (double)(s.pop_ny - 1) : 0.0;
+        d.pop_mx = (float)mx; d.pop_my = (float)my;
+        d.pop_ax = mx > 0 ? (float)(1.0 / (s.pop_dx * mx)) : 0.0f; d.pop_bx = mx > 0 ? (float)(-s.pop_x0 / (s.pop_dx * mx)) : 0.0f;
+        d.pop_ay = my > 0 ? (float)(1.0 / (s.pop_dx * my)) : 0.0f; d.pop_by = my > 0 ? (float)(-s.pop_y0 / (s.pop_dx * my)) : 0.0f;
+    }
     for (int a = 0; a < 3; ++a) {
         d.wind_lo[a] = (float)s.wind_lo[a];
         d.wind_inv_ext[a] = (float)(1.0 / (s.wind_hi[a] - s.wind_lo[a]));
@@ -817,6 +825,7 @@ static smc_status build_constants(smc_ctx *ctx) {
     }
     d.ac = ctx->dac;
     d.pop = ctx->pop;
+    d.popp = ctx->popp;
     p.dt = s.dt; p.g = s.g; p.rho_const = s.rho_const; p.density_mode = s.density_mode;
     for (int a = 0; a < 3; ++a) { p.wind_lo[a] = s.wind_lo[a]; p.wind_hi[a] = s.wind_hi[a]; }
     p.nominal[0] = s.nominal[0]; p.nominal[1] = s.nominal[1];
@@ -960,7 +969,7 @@ extern "C" smc_status smc_set_scenario(smc_ctx *ctx, const smc_scenario *scn) {
         CK(h2d(ctx, ctx->centres, scn->centres, sizeof(double) * 3 * scn->n_centres));
     }
     LAUNCH(launch_popgrid(ctx->centres, (int)scn->n_centres, (int)scn->pop_nx, (int)scn->pop_ny, scn->pop_x0,
-                          scn->pop_y0, scn->pop_dx, ctx->pop, ctx->st));
+                          scn->pop_y0, scn->pop_dx, ctx->pop, ctx->popp, ctx->st));
     ctx->drop_graph();            // (the realised plant wind persists across scenarios: mpc loop)
     ctx->have_scn = true;
     return init_population(ctx);

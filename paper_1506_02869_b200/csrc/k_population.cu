@@ -911,10 +911,13 @@ cudaError_t launch_plant(const PlantScen &ps, const PlantArgs &p, cudaStream_t s
 }
 
 // ============================================================== popdense grid
-__global__ void k_popgrid(const double *centres, int nc, int nx, int ny, double x0, double y0, double dx, float *out) {
+__global__ void k_popgrid(const double *centres, int nc, int nx, int ny, double x0, double y0, double dx, float *out,
+                          int pad) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nx * ny) return;
-    const double x = x0 + (idx % nx) * dx, y = y0 + (idx / nx) * dx;
+    const int sx = nx + pad;                                  // row stride
+    if (idx >= sx * (ny + pad)) return;
+    const int ix = min(idx % sx, nx - 1), iy = min(idx / sx, ny - 1);   // padding repeats the edge
+    const double x = x0 + ix * dx, y = y0 + iy * dx;
     double sum = 0.0;
     for (int c = 0; c < nc; ++c) {
         const double bx = (x - centres[3 * c]) * 1e-3, by = (y - centres[3 * c + 1]) * 1e-3;
@@ -925,9 +928,11 @@ __global__ void k_popgrid(const double *centres, int nc, int nx, int ny, double 
 }
 
 cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny, double x0, double y0,
-                           double dx, float *out, cudaStream_t st) {
+                           double dx, float *out, float *outp, cudaStream_t st) {
     if (nx * ny == 0) return cudaSuccess;
-    k_popgrid<<<(nx * ny + 255) / 256, 256, 0, st>>>(centres, n_centres, nx, ny, x0, y0, dx, out);
+    k_popgrid<<<(nx * ny + 255) / 256, 256, 0, st>>>(centres, n_centres, nx, ny, x0, y0, dx, out, 0);
+    const int np = (nx + 1) * (ny + 1);
+    k_popgrid<<<(np + 255) / 256, 256, 0, st>>>(centres, n_centres, nx, ny, x0, y0, dx, outp, 1);
     return cudaGetLastError();
 }
 

@@ -86,6 +86,37 @@ __device__ __forceinline__ float popdense(const DevScen &sc, const float *pop, f
     return fmaf(fy, b - a, a);
 }
 
+// popdense on the edge-padded grid pp = [pop_ny + 1][pop_nx + 1], both candidates of a
+// chain.  u = clamp((x - x0) / dx, 0, nx - 1) / (nx - 1) is one saturated FMA; the cell comes from
+// adding 1.5 * 2^23 to u (nx - 1) - 1/2 (round to nearest: floor, or one cell lower at an integer
+// coordinate, whose weight is then 1), read off the float's low bits -- no F2I, no index clamp (the
+// padding makes column nx and row ny valid).  pp: shared memory or global (inlined per space).
+template <class V>
+__device__ __forceinline__ V popdense_pad(const DevScen &sc, const float *pp, V x, V y) {
+    constexpr int NCV = (int)(sizeof(V) / sizeof(float));
+    constexpr float kMagic = 12582912.0f;                       // 1.5 * 2^23
+    V ux, uy;
+#pragma unroll
+    for (int c = 0; c < NCV; ++c) {
+        cset(ux, c, __saturatef(fmaf(cget(x, c), sc.pop_ax, sc.pop_bx)));
+        cset(uy, c, __saturatef(fmaf(cget(y, c), sc.pop_ay, sc.pop_by)));
+    }
+    const V kx = vfma(ux, sc.pop_mx, -0.5f) + kMagic, ky = vfma(uy, sc.pop_my, -0.5f) + kMagic;
+    const V fx = vfma(ux, sc.pop_mx, kMagic - kx), fy = vfma(uy, sc.pop_my, kMagic - ky);
+    const int P = sc.pop_nx + 1;
+    V v00, v10, v01, v11;
+#pragma unroll
+    for (int c = 0; c < NCV; ++c) {
+        const uint32_t e = __float_as_uint(cget(ky, c)) * (uint32_t)P + __float_as_uint(cget(kx, c)) -
+                           0x4B400000u * (uint32_t)(P + 1);
+        const float *r0 = pp + e, *r1 = r0 + P;
+        cset(v00, c, r0[0]); cset(v10, c, r0[1]);
+        cset(v01, c, r1[0]); cset(v11, c, r1[1]);
+    }
+    const V a = vfma(fx, v10 - v00, v00), b = vfma(fx, v11 - v01, v01);
+    return vfma(fy, b - a, a);
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -845,13 +876,9 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     auto seg_sync = [] { if constexpr (XW) __syncthreads(); else __syncwarp(); };
     extern __shared__ __align__(16) float smem_all[];
     const int H = sc.H, n = sc.n;
-    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx, sc.pop_ny) : 0;
-    const float *s_pop = sc.pop;                                 // the grid, staged below when it fits
+    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;   // padded grid
     float *smem = smem_all + ((npop + 3) & ~3);
-    if (npop) {
-        for (int e = threadIdx.x; e < npop; e += kBlock) smem_all[e] = __ldg(&sc.pop[e]);
-        s_pop = smem_all;
-    }
+    for (int e = threadIdx.x; e < npop; e += kBlock) smem_all[e] = __ldg(&sc.popp[e]);   // staged when it fits
     constexpr int NPOS = 2 * SEGA * W;                           // entries per position array
     float4 *s_ctrl = reinterpret_cast<float4 *>(smem);           // [H][2][kBlock]
     float *s_V = reinterpret_cast<float *>(s_ctrl + H * 2 * kBlock);
@@ -1128,13 +1155,16 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 sC[q] = vfma(vabs(nv[q] - v_D), flyf[q], sC[q]);
                 fuel[q] = vfma(dtef[q], T, fuel[q]);
                 if (sc.has_noise) {
+                    const V pd = popdense_pad(sc, smem_all, nx[q], ny[q]);   // staged (launch_rollout checks it fits)
+                    const V zz = nz[q] * sc.inv_Ac;
+                    V f;
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const float zz = cget(nz[q], c) * sc.inv_Ac;
-                        const float nzs = 1.0f - fmaxf(1.0f - zz * zz, 0.0f) * popdense(sc, s_pop, cget(nx[q], c), cget(ny[q], c));
-                        cset(sN[q], c, cget(sN[q], c) + (((flym[q] >> c) & 1) ? nzs
+                    for (int c = 0; c < 2; ++c) cset(f, c, __saturatef(fmaf(-cget(zz, c), cget(zz, c), 1.0f)));   // max(1 - zz^2, 0)
+                    const V nzs = vfma(f, -pd, 1.0f);
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        cset(sN[q], c, cget(sN[q], c) + (((flym[q] >> c) & 1) ? cget(nzs, c)
                                                                                : ((act && ((landedm[q] >> c) & 1)) ? 1.0f : 0.0f)));
-                    }
                 }
                 violm[q] |= flym[q] & (vnowm[q] | confm[q]);
                 landedm[q] |= flym[q] & lnowm[q];
@@ -1241,7 +1271,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 
 template <int W, int R>
 static cudaError_t launch_2s_r(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
-    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx, sc.pop_ny) : 0;
+    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;
     const size_t smem = rollout2s_smem_bytes(W, sc.H, (npop + 3) & ~3);
     auto kern = k_rollout_2s<W, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1409,7 +1439,11 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
-    if (NC == 2 && !debug && !dense && W >= SMC_K2_2S_MINW && ns2_enabled()) return launch_2s(W, ring_for(W, sc.n), sc, a, st);
+    // the two-chain kernel reads the noise grid from shared memory only: a grid too large for it
+    // (more than kPopSmem padded entries) takes the one-chain kernel
+    const bool pop_fits = !sc.has_noise || pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) > 0;
+    if (NC == 2 && !debug && !dense && pop_fits && W >= SMC_K2_2S_MINW && ns2_enabled())
+        return launch_2s(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }

@@ -43,6 +43,8 @@ struct DevScen {
     float noise_w, inv_Ac;
     int pop_nx, pop_ny;
     float pop_x0, pop_y0, pop_inv_dx;
+    float pop_ax, pop_bx, pop_ay, pop_by; // grid coordinate / (n - 1) = sat(a x + b) (0 for a 1-wide axis)
+    float pop_mx, pop_my;                 // n - 1 per axis
     float wind_lo[3], wind_inv_ext[3];
     float Qhat[64];                       // lower-triangular, row-major
     float Cq[64];                         // M Qhat: row r gives coefficient r of the trilinear
@@ -55,6 +57,7 @@ struct DevScen {
     const float *Qf;                      // [wng][wng] Qhat (FP32), read by the dense-grid path (wng > 8)
     const DevAircraft *ac;
     const float *pop;                     // [pop_ny][pop_nx] popdense grid
+    const float *popp;                    // [pop_ny + 1][pop_nx + 1] the same, last row/column repeated
 };
 
 // ---------------------------------------------------------------- Philox4x32-10

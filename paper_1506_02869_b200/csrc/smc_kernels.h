@@ -188,9 +188,10 @@ struct PlantScen {              // FP64 constants for the plant
 };
 cudaError_t launch_plant(const PlantScen &ps, const PlantArgs &p, cudaStream_t st);
 
-// popdense grid, computed in FP64 on the device
+// popdense grid, computed in FP64 on the device: out [ny][nx], and outp [ny + 1][nx + 1]
+// with the last row and column repeated (K2's cell lookup needs no index clamp)
 cudaError_t launch_popgrid(const double *centres, int n_centres, int nx, int ny, double x0, double y0,
-                           double dx, float *out, cudaStream_t st);
+                           double dx, float *out, float *outp, cudaStream_t st);
 
 // MH decisions for injected lambdas (debug hook)
 cudaError_t launch_mh_debug(const double *lc, const double *lp, uint32_t L, uint32_t k, const uint32_t *mpcp,

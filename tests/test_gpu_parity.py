@@ -286,7 +286,8 @@ def test_evaluate_parity(smc, case, sp, monkeypatch):
     sol.close()
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "n6", "n12_noise", "n14", "n16", "n20", "n24", "n28"])
+@pytest.mark.parametrize("case", ["c1", "c2", "n6", "n12_noise", "n12_noise_rect", "n12_noise_big", "n14", "n16", "n20",
+                                  "n24", "n28"])
 def test_production_rounds_parity(smc, case):
     """Real SMC rounds through smc_iterate -- round 0 (single candidate, sample pairs)
     and rounds 1-2 (both MH candidates, packed FP32) -- on every separation-ring
@@ -306,9 +307,16 @@ def test_production_rounds_parity(smc, case):
     elif case == "n24":
         scn, cfg = sc.config(3)
         seed = cfg.seed
-    elif case == "n12_noise":
+    elif case.startswith("n12_noise"):
         scn, cfg = sc.config(4, noise_w=0.2)
         seed = cfg.seed
+        if case == "n12_noise_rect":
+            # 13 x 7 grid over part of the airspace: row stride != column count, most aircraft
+            # clamped to an edge (the two-chain kernel's padded shared-memory grid)
+            scn.update(pop_nx=13, pop_ny=7, pop_x0=-15000.0, pop_y0=-9000.0, pop_dx=2500.0)
+        elif case == "n12_noise_big":
+            # 121 x 121 grid: too large for shared memory, one-chain kernel reads it from global
+            scn.update(pop_nx=121, pop_ny=121, pop_x0=-42000.0, pop_y0=-42000.0, pop_dx=700.0)
     else:
         scn, cfg = sc.config(int(case[1:]))
         seed = cfg.seed
