@@ -164,18 +164,15 @@ __device__ __forceinline__ V fast_atan2(V y, V x) {
     return out;
 }
 
-// atan2(y, x) for x >= 0 (right half-plane: no x < 0 fix-up), same polynomial.
+// atan2(y, x) for x >= 0 (right half-plane), without octant selects: for a, b >= 0,
+// atan2(a, b) = pi/4 + atan(t), t = (a - b) / (a + b) in [-1, 1], where the same odd polynomial
+// holds; the sign of y is restored by copysign.  Absolute error ~2e-7 rad, but not relative
+// accuracy near 0 (pi/4 - pi/4 cancels) -- used for beta, which enters only absolute terms.
 template <class V>
 __device__ __forceinline__ V fast_atan2_xpos(V y, V x) {
-    const V ax = x, ay = vabs(y);
-    V mx, mn;
-#pragma unroll
-    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c) {
-        cset(mx, c, fmaxf(cget(ax, c), cget(ay, c)));
-        cset(mn, c, fminf(cget(ax, c), cget(ay, c)));
-    }
-    const V a = mn * vmap(mx, [](float u) { return rcp_approx(fmaxf(u, 1e-30f)); });   // mx = 0 -> mn = 0 -> a = 0
-    const V s = a * a;
+    const V ay = vabs(y);
+    const V t = (ay - x) * vmap(ay + (x + 1e-37f), [](float u) { return rcp_approx(u); });   // x = y = 0 -> t = 0
+    const V s = t * t;
     V p = vfma(s, -0.0040731243789196014f, 0.021945973858237267f);
     p = vfma(p, s, -0.056062303483486176f);
     p = vfma(p, s, 0.0965619683265686f);
@@ -183,12 +180,10 @@ __device__ __forceinline__ V fast_atan2_xpos(V y, V x) {
     p = vfma(p, s, 0.19948504865169525f);
     p = vfma(p, s, -0.3333010673522949f);
     p = vfma(p, s, 0.999999463558197f);
-    const V r = p * a;
-    const V r1 = 1.57079632679489662f - r;
+    const V r = vfma(p, t, 0.78539816339744831f);
     V out;
 #pragma unroll
-    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c)
-        cset(out, c, copysignf(cget(ay, c) > cget(ax, c) ? cget(r1, c) : cget(r, c), cget(y, c)));
+    for (int c = 0; c < (int)(sizeof(V) / sizeof(float)); ++c) cset(out, c, copysignf(cget(r, c), cget(y, c)));
     return out;
 }
 
@@ -569,7 +564,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             V qd = cq * v * v;
             if (sc.density_mode == 0) {
                 const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
-                qd = qd * vmap(vmap(base, [](float a) { return __log2f(a); }) * 4.2559f, ex2_approx);
+                qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
             }
             const V mgq = (m * g) * vmap(qd, rcp_approx);
             const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
@@ -604,7 +599,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10):
             // s = rho_h |theta| / sin|theta| with sin|theta| = |y| / rho_h, i.e. s = rho_h^2 |theta| / |y|
             const V r2 = vfma(nx, nx, ny * ny);
-            const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
+            const V rh = r2 * vmap(r2, [](float a) { return rsqrt_approx(fmaxf(a, 1e-30f)); });
             const V at = vabs(th);
             const V sfull = (r2 * at) * vmap(ny, [](float a) { return rcp_approx(fabsf(a)); });   // unconditional:
             V sarc;                                                                             // no branch
@@ -1056,7 +1051,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 V qd = cq * v[q] * v[q];
                 if (sc.density_mode == 0) {
                     const V base = vmap(vfma(z[q], -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
-                    qd = qd * vmap(vmap(base, [](float a) { return __log2f(a); }) * 4.2559f, ex2_approx);
+                    qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
                 }
                 const V mgq = (m[q] * g) * vmap(qd, rcp_approx);
                 const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
@@ -1083,7 +1078,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 }
                 th[q] = fast_atan2(ny[q], nx[q]);
                 const V r2 = vfma(nx[q], nx[q], ny[q] * ny[q]);
-                const V rh = r2 * vmap(r2, [](float a) { return rsqrtf(fmaxf(a, 1e-30f)); });
+                const V rh = r2 * vmap(r2, [](float a) { return rsqrt_approx(fmaxf(a, 1e-30f)); });
                 const V at = vabs(th[q]);
                 const V sfull = (r2 * at) * vmap(ny[q], [](float a) { return rcp_approx(fabsf(a)); });
                 V sarc;

@@ -113,6 +113,22 @@ __device__ __forceinline__ float2 tripoly2(const float2 *c, float2 c0, float2 fx
     return vfma(fx, A, B);
 }
 
+// MUFU lg2 / rsqrt without the denormal-input fix-up (FSETP + two predicated ops) that __log2f and
+// rsqrtf carry.  Every use has a normal input (uniforms >= 2^-24, -2 ln u >= 1.1e-7, clamps to
+// >= 1e-30) or feeds ex2 of a large negative multiple (the ISA base), where a flushed denormal
+// gives the same 0: results are bit-identical to the non-ftz forms.
+__device__ __forceinline__ float lg2_approx(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Uniform (2k+1) 2^-24, k = w >> 9: exact in binary32 (R37).
 __device__ __forceinline__ float unif(uint32_t w) {
     return __fmaf_rn(__uint2float_rn(w >> 9), 0x1.0p-23f, 0x1.0p-24f);
@@ -122,8 +138,8 @@ __device__ __forceinline__ float unif(uint32_t w) {
 // pi + 2 pi (u2 - 1/2) so the fast sin/cos see an argument in [-pi, pi).
 __device__ __forceinline__ float2 box_muller(uint32_t w0, uint32_t w1) {
     const float u1 = unif(w0), u2 = unif(w1);
-    const float r2 = -2.0f * 0.69314718055994531f * __log2f(u1);
-    const float r = r2 * rsqrtf(r2);
+    const float r2 = -2.0f * 0.69314718055994531f * lg2_approx(u1);
+    const float r = r2 * rsqrt_approx(r2);
     float s, c;
     __sincosf(kTwoPi * (u2 - 0.5f), &s, &c);
     return make_float2(-r * c, -r * s);
@@ -135,8 +151,8 @@ __device__ __forceinline__ float2 box_muller(uint32_t w0, uint32_t w1) {
 __device__ __forceinline__ float4 box_muller4(uint4 w) {
     const float2 u1 = vfma(make_float2(__uint2float_rn(w.x >> 9), __uint2float_rn(w.z >> 9)), 0x1.0p-23f, 0x1.0p-24f);
     const float2 u2 = vfma(make_float2(__uint2float_rn(w.y >> 9), __uint2float_rn(w.w >> 9)), 0x1.0p-23f, 0x1.0p-24f);
-    const float2 r2 = make_float2(__log2f(u1.x), __log2f(u1.y)) * (-2.0f * 0.69314718055994531f);
-    const float2 r = r2 * make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+    const float2 r2 = make_float2(lg2_approx(u1.x), lg2_approx(u1.y)) * (-2.0f * 0.69314718055994531f);
+    const float2 r = r2 * make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
     const float2 ang = vfma(u2, kTwoPi, -kPi);
     float2 sn, cs;
     __sincosf(ang.x, &sn.x, &cs.x);
