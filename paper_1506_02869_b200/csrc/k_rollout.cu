@@ -52,10 +52,13 @@ constexpr int kTUnroll = SMC_K2_TUNROLL;
 
 __device__ __forceinline__ float clamp01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
 
-// a - 2 pi rint(a / 2 pi) by FRND per candidate.  (The magic-number form -- one packed FMA
-// adding 1.5 * 2^23, one packed subtract -- measured slower on B200: 28.62 vs 28.13 ms of K2.)
+// a - 2 pi rint(a / 2 pi): the integer by the magic-number form (one packed FMA adding
+// 1.5 * 2^23, one packed subtract: FMA pipe) instead of FRND per candidate on the XU pipe, which
+// the MUFU work keeps busy (c5 K2 2166 -> 2154 ms over 21 rounds; round 1, before the XU load
+// grew, it measured slower: 28.62 vs 28.13 ms of c2 K2).  A tie at an odd multiple of pi may
+// round either way: +pi and -pi are the same heading for every later use (sin, cos, |chi|).
 #ifndef SMC_K2_WRAPMAGIC
-#define SMC_K2_WRAPMAGIC 0
+#define SMC_K2_WRAPMAGIC 1
 #endif
 template <class V>
 __device__ __forceinline__ V wrap_pi(V a) {
