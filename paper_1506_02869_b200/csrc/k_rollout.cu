@@ -94,7 +94,7 @@ __device__ __forceinline__ float popdense(const DevScen &sc, const float *pop, f
 // adding 1.5 * 2^23 to u (nx - 1) - 1/2 (round to nearest: floor, or one cell lower at an integer
 // coordinate, whose weight is then 1), read off the float's low bits -- no F2I, no index clamp (the
 // padding makes column nx and row ny valid).  pp: shared memory or global (inlined per space).
-template <class V>
+template <class V, bool LDG = false>
 __device__ __forceinline__ V popdense_pad(const DevScen &sc, const float *pp, V x, V y) {
     constexpr int NCV = (int)(sizeof(V) / sizeof(float));
     constexpr float kMagic = 12582912.0f;                       // 1.5 * 2^23
@@ -113,8 +113,13 @@ __device__ __forceinline__ V popdense_pad(const DevScen &sc, const float *pp, V 
         const uint32_t e = __float_as_uint(cget(ky, c)) * (uint32_t)P + __float_as_uint(cget(kx, c)) -
                            0x4B400000u * (uint32_t)(P + 1);
         const float *r0 = pp + e, *r1 = r0 + P;
-        cset(v00, c, r0[0]); cset(v10, c, r0[1]);
-        cset(v01, c, r1[0]); cset(v11, c, r1[1]);
+        if constexpr (LDG) {
+            cset(v00, c, __ldg(r0)); cset(v10, c, __ldg(r0 + 1));
+            cset(v01, c, __ldg(r1)); cset(v11, c, __ldg(r1 + 1));
+        } else {
+            cset(v00, c, r0[0]); cset(v10, c, r0[1]);
+            cset(v01, c, r1[0]); cset(v11, c, r1[1]);
+        }
     }
     const V a = vfma(fx, v10 - v00, v00), b = vfma(fx, v11 - v01, v01);
     return vfma(fy, b - a, a);
@@ -839,6 +844,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #ifndef SMC_K2_TUNROLL2S
 #define SMC_K2_TUNROLL2S 1
 #endif
+#ifndef SMC_K2_POP_SMEM
+#define SMC_K2_POP_SMEM 0   // 1: stage the noise grid in shared memory (c4: 27 KB per block -> 2 blocks/SM)
+#endif
 // the 1 km population grid is staged in shared memory when it fits (c4: 81 x 81, 26 KB)
 constexpr int kPopSmem = 8192;
 __host__ __device__ inline int pop_smem_floats(int nx, int ny) { return nx * ny <= kPopSmem ? nx * ny : 0; }
@@ -853,11 +861,11 @@ __host__ __device__ constexpr int k2_segs_alloc(int W) { return kBlock / W + (k2
 size_t rollout2s_smem_bytes(int W, int H, int npop) {
     const int SEGA = k2_segs_alloc(W), GB = W / 4;
     const size_t pos = (size_t)2 * SEGA * W;                      // entries per position array
-    return sizeof(float) * (size_t)npop + sizeof(float4) * ((size_t)H * 2 * kBlock)              // controls
+    return sizeof(float) * (size_t)npop + sizeof(float) * ((size_t)H * 10 * kBlock)   // airframe records
            + sizeof(float) * (SEGA * 2 * GB * 16                  // normals [SEGA][slot][GB][16]
                               + SEGA * 2 * 16                     // AR(1) state [SEGA][slot][8] (x, y)
                               + SEGA * 2 * 16)                    // coefficients [SEGA][slot][16]
-           + sizeof(float4) * 3 * pos                             // positions x4, y4, z4, each twice
+           + sizeof(float4) * 2 * pos + sizeof(float2) * pos      // positions x4, y4, z2, each twice
            + (k2_cross_warp(W) ? sizeof(uint32_t) * (size_t)(W / 2) * SEGA * W : 0)   // verdicts
            + sizeof(float) * 72 + 16;
 }
@@ -874,16 +882,15 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     auto seg_sync = [] { if constexpr (XW) __syncthreads(); else __syncwarp(); };
     extern __shared__ __align__(16) float smem_all[];
     const int H = sc.H, n = sc.n;
-    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;   // padded grid
+    const int npop = (SMC_K2_POP_SMEM && sc.has_noise) ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;
     float *smem = smem_all + ((npop + 3) & ~3);
     for (int e = threadIdx.x; e < npop; e += kBlock) smem_all[e] = __ldg(&sc.popp[e]);   // staged when it fits
     constexpr int NPOS = 2 * SEGA * W;                           // entries per position array
-    float4 *s_ctrl = reinterpret_cast<float4 *>(smem);           // [H][2][kBlock]
-    float *s_V = reinterpret_cast<float *>(s_ctrl + H * 2 * kBlock);
+    float *s_V = smem + (size_t)H * 10 * kBlock;                 // after the airframe records (below)
     float *s_Z = s_V + SEGA * NSL * GB * 16;
     float *s_W = s_Z + SEGA * NSL * 16;
-    float4 *s_p4 = reinterpret_cast<float4 *>(s_W + SEGA * NSL * 16);   // [3][NPOS]: x4, y4, z4
-    uint32_t *s_hv = reinterpret_cast<uint32_t *>(s_p4 + 3 * NPOS);   // [W/2][SEGA W] verdicts (XW)
+    float4 *s_p4 = reinterpret_cast<float4 *>(s_W + SEGA * NSL * 16);   // [2][NPOS] x4, y4; [NPOS] z2
+    uint32_t *s_hv = reinterpret_cast<uint32_t *>(s_p4 + 2 * NPOS + NPOS / 2);   // [W/2][SEGA W] verdicts (XW)
     float *s_Q = reinterpret_cast<float *>(s_hv + (XW ? (W / 2) * SEGA * W : 0));
 
     const int tid = threadIdx.x, lane = tid % W, seg = tid / W;
@@ -902,30 +909,88 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     const float gA = kind ? Ap->theta_F : Ap->beta_f;
     const float z_tf = Ap->z_tf, v_D = Ap->v_D;
 
-    uint32_t cbad[2];
+    // ---------------- airframe trajectory (Eq. hor), once per particle.  z, v, chi and m
+    // do not depend on the wind -- it enters only dx/dt and dy/dt -- so for both candidates they are
+    // integrated here and every sample reads them; samples differ only in the ground track and what
+    // depends on it.  Per step t: the air-relative ground velocity (v cos g cos chi, v cos g sin chi)
+    // at t, z and chi at t+1, the fuel increment; the envelope (with the control bounds) and the
+    // landing sector's speed / heading conditions at t+1 as bit masks (bit 2t + c).  A trajectory
+    // that becomes non-finite (v reached 0: already outside the envelope, so every sample flying it
+    // is violated) is replaced by a far-away finite sentinel: it fails the envelope and can no longer
+    // conflict (the oracle's non-finite rule), and a sample in which the aircraft has landed before
+    // keeps finite cost terms.
+    float4 *const s_r0 = reinterpret_cast<float4 *>(smem);                // [H][kBlock] (ax0, ax1, ay0, ay1)
+    float4 *const s_r1 = s_r0 + H * kBlock;                                 // [H][kBlock] (z'0, z'1, chi'0, chi'1)
+    float2 *const s_rf = reinterpret_cast<float2 *>(s_r1 + H * kBlock);     // [H][kBlock] fuel increments
+    using V = float2;
+    const float dt = sc.dt, g = sc.g;
+    uint32_t vbadm = 0u, lokm = 0u;
+    V sCc = make_float2(0.0f, 0.0f);           // departures (never land): sum of |v - v_D| over active steps
     {
         const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
+        const float cq = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
         const float *src[2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            cbad[c] = 0;
-            src[c] = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
-        }
+        for (int c = 0; c < 2; ++c) src[c] = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
+        V v = vsplat<V>(Ap->x0[3]), z = vsplat<V>(Ap->x0[2]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
+        int broken = 0;
         for (int t = 0; t < H; ++t) {
-            float q[2][4];
+            V T, tph, sga, cga;
+            int cb = 0;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                float T = 0.f, ph = 0.f, ga = 0.f;
-                if (isac && valid) { T = src[c][3 * t]; ph = src[c][3 * t + 1]; ga = src[c][3 * t + 2]; }
-                float sph, cph, sga, cga;
+                float Tc = 0.f, ph = 0.f, ga = 0.f;
+                if (isac && valid) { Tc = src[c][3 * t]; ph = src[c][3 * t + 1]; ga = src[c][3 * t + 2]; }
+                float sph, cph, sg, cg;
                 __sincosf(ph, &sph, &cph);
-                __sincosf(ga, &sga, &cga);
-                q[c][0] = T; q[c][1] = sph * rcp_approx(cph); q[c][2] = sga; q[c][3] = cga;
-                const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
-                cbad[c] |= (bad ? 1u : 0u) << t;
+                __sincosf(ga, &sg, &cg);
+                cset(T, c, Tc); cset(tph, c, sph * rcp_approx(cph)); cset(sga, c, sg); cset(cga, c, cg);
+                const bool bad = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (Tc < Tmin) || (Tc > Tmax);
+                cb |= (bad ? 1 : 0) << c;
             }
-            s_ctrl[(2 * t) * kBlock + tid] = make_float4(q[0][0], q[1][0], q[0][1], q[1][1]);
-            s_ctrl[(2 * t + 1) * kBlock + tid] = make_float4(q[0][2], q[1][2], q[0][3], q[1][3]);
+            const bool act = first <= t;
+            const float dta = act ? dt : 0.0f, dtea = act ? dt_eta : 0.0f;
+            V qd = cq * v * v;
+            if (sc.density_mode == 0) {
+                const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
+                qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
+            }
+            const V mgq = (m * g) * vmap(qd, rcp_approx);
+            const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
+            V sch, cch;
+            __sincosf(chi.x, &sch.x, &cch.x);
+            __sincosf(chi.y, &sch.y, &cch.y);
+            const V vcg = v * cga;
+            V ax = vcg * cch, ay = vcg * sch;
+            V nz = vfma(dta * v, sga, z);
+            const V nv = vfma(vsplat<V>(dta), vfma(T - D, vmap(m, rcp_approx), sga * (-g)), v);
+            V nchi = wrap_pi(vfma((dta * g) * tph, vmap(v, rcp_approx), chi));
+            const V nm = vfma(vsplat<V>(-dtea), T, m);
+            V fi = T * dtea;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const bool fin = (fabsf(cget(ax, c)) < INFINITY) & (fabsf(cget(ay, c)) < INFINITY) &
+                                 (fabsf(cget(nz, c)) < INFINITY) & (fabsf(cget(nv, c)) < INFINITY) &
+                                 (fabsf(cget(nchi, c)) < INFINITY) & (fabsf(cget(nm, c)) < INFINITY);
+                if (!fin) broken |= 1 << c;
+                int bad, lok;
+                if ((broken >> c) & 1) {
+                    cset(ax, c, 1e30f); cset(ay, c, 1e30f); cset(nz, c, 1e30f); cset(nchi, c, 0.0f); cset(fi, c, 0.0f);
+                    bad = 1; lok = 0;
+                } else {
+                    const float zc = cget(nz, c), vc = cget(nv, c);
+                    bad = (((cb >> c) & 1) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) | !(vc <= vmax) |
+                           !(cget(nm, c) >= mempty)) ? 1 : 0;
+                    lok = ((vc <= sc.P_vs) & (fabsf(cget(nchi, c)) >= sc.P_chi_west)) ? 1 : 0;
+                    if (act) cset(sCc, c, cget(sCc, c) + fabsf(vc - v_D));
+                }
+                vbadm |= (uint32_t)bad << (2 * t + c);
+                lokm |= (uint32_t)lok << (2 * t + c);
+            }
+            s_r0[t * kBlock + tid] = make_float4(ax.x, ax.y, ay.x, ay.y);
+            s_r1[t * kBlock + tid] = make_float4(nz.x, nz.y, nchi.x, nchi.y);
+            s_rf[t * kBlock + tid] = fi;
+            v = nv; z = nz; chi = nchi; m = nm;
         }
     }
     __syncthreads();
@@ -934,25 +999,23 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     for (int mm = 0; mm < 8; ++mm) qrow[mm] = s_Q[(lane & 7) * 9 + mm];
 
     float ell[2] = {args.ell0, args.ell0};
-    using V = float2;
-    const float dt = sc.dt, g = sc.g;
     const float inv0 = sc.wind_inv_ext[0], inv1 = sc.wind_inv_ext[1], inv2 = sc.wind_inv_ext[2];
     const float nlo0 = -sc.wind_lo[0] * inv0, nlo1 = -sc.wind_lo[1] * inv1, nlo2 = -sc.wind_lo[2] * inv2;
-    const float cq = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
     const float cA_th = kind ? 1.0f : -2.0f, cA_chi = kind ? 0.0f : 1.0f, cA_0 = kind ? -gA : -kPi;
     const float cB_z = kind ? -1.0f : 0.0f, cB_b = kind ? 0.0f : 1.0f, cB_0 = kind ? z_tf : -gA;
     const int pb = seg * 2 * W + lane;                             // own entry; + R: duplicate
-    float4 *const s_px = s_p4, *const s_py = s_p4 + NPOS, *const s_pz = s_p4 + 2 * NPOS;
+    float4 *const s_px = s_p4, *const s_py = s_p4 + NPOS;
+    float2 *const s_pz = reinterpret_cast<float2 *>(s_p4 + 2 * NPOS);   // z: shared by the two samples
     const uint32_t S = args.S;
 
     for (uint32_t s = 0; s < S; s += 2) {
         const bool two = s + 1 < S;                                // odd S: the second chain is not counted
-        V x[2], y[2], z[2], v[2], chi[2], m[2], fuel[2], sA[2], sB[2], sC[2], sN[2];
+        V x[2], y[2], fuel[2], sA[2], sB[2], sN[2];
+        V z = vsplat<V>(Ap->x0[2]);                                // the airframe altitude (both samples)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            x[q] = vsplat<V>(Ap->x0[0]); y[q] = vsplat<V>(Ap->x0[1]); z[q] = vsplat<V>(Ap->x0[2]);
-            v[q] = vsplat<V>(Ap->x0[3]); chi[q] = vsplat<V>(Ap->x0[4]); m[q] = vsplat<V>(Ap->x0[5]);
-            fuel[q] = sA[q] = sB[q] = sC[q] = sN[q] = vsplat<V>(0.0f);
+            x[q] = vsplat<V>(Ap->x0[0]); y[q] = vsplat<V>(Ap->x0[1]);
+            fuel[q] = sA[q] = sB[q] = sN[q] = vsplat<V>(0.0f);
         }
         int landedm[2] = {0, 0}, violm[2] = {0, 0};
         float2 Zr[ENS];
@@ -1026,15 +1089,18 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                     gyq[q] = fmaf(sc.turb_sigma, gg.y, gyq[q]);
                 }
             }
-            // controls of step t, shared by both chains
-            const float4 ca = s_ctrl[(2 * t) * kBlock + tid], cb = s_ctrl[(2 * t + 1) * kBlock + tid];
-            const V T = make_float2(ca.x, ca.y), tph = make_float2(ca.z, ca.w);
-            const V sga = make_float2(cb.x, cb.y), cga = make_float2(cb.z, cb.w);
+            // airframe state of step t (shared by both chains: wind-independent)
+            const float4 r0 = s_r0[t * kBlock + tid], r1 = s_r1[t * kBlock + tid];
+            const V fi = s_rf[t * kBlock + tid];
+            const V ax = make_float2(r0.x, r0.y), ay = make_float2(r0.z, r0.w);
+            const V nz = make_float2(r1.x, r1.y), nchi = make_float2(r1.z, r1.w);
             const bool act = first <= t;
+            const int vbt = (int)((vbadm >> (2 * t)) & 3u), lkt = (int)((lokm >> (2 * t)) & 3u);
+            const V fz = vmap(z, [&](float p) { return __saturatef(fmaf(p, inv2, nlo2)); });
 
-            // ---------------- 2-3. per chain: dynamics, unary checks, geometry, landing test
-            V nx[2], ny[2], nz[2], nv[2], nchi[2], nm[2], th[2], beta[2], px[2], flyf[2], dtef[2];
-            int flym[2], vnowm[2], lnowm[2];
+            // ---------------- 2-3. per chain: ground track, geometry, landing test
+            V nx[2], ny[2], th[2], beta[2], px[2], flyf[2];
+            int flym[2], lnowm[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 flym[q] = act ? (~landedm[q] & 3) : 0;
@@ -1048,37 +1114,11 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 }
                 const V fx = vmap(x[q], [&](float p) { return __saturatef(fmaf(p, inv0, nlo0)); });
                 const V fy = vmap(y[q], [&](float p) { return __saturatef(fmaf(p, inv1, nlo1)); });
-                const V fz = vmap(z[q], [&](float p) { return __saturatef(fmaf(p, inv2, nlo2)); });
                 const V wx = tripoly(Wn, Wn[0] + gxq[q], fx, fy, fz);
                 const V wy = tripoly(Wn + 8, Wn[8] + gyq[q], fx, fy, fz);
-                V qd = cq * v[q] * v[q];
-                if (sc.density_mode == 0) {
-                    const V base = vmap(vfma(z[q], -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
-                    qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
-                }
-                const V mgq = (m[q] * g) * vmap(qd, rcp_approx);
-                const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
-                const V chr = chi[q];                             // kept in [-pi, pi]
-                V sch, cch;
-                __sincosf(chr.x, &sch.x, &cch.x);
-                __sincosf(chr.y, &sch.y, &cch.y);
                 const V dtf = flyf[q] * dt;
-                dtef[q] = flyf[q] * dt_eta;
-                const V vcg = v[q] * cga;
-                nx[q] = vfma(dtf, vfma(vcg, cch, wx), x[q]);
-                ny[q] = vfma(dtf, vfma(vcg, sch, wy), y[q]);
-                nz[q] = vfma(dtf * v[q], sga, z[q]);
-                nv[q] = vfma(dtf, vfma(T - D, vmap(m[q], rcp_approx), sga * (-g)), v[q]);
-                nchi[q] = wrap_pi(vfma((dtf * g) * tph, vmap(v[q], rcp_approx), chi[q]));
-                nm[q] = vfma(-dtef[q], T, m[q]);
-                vnowm[q] = 0;
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const float zc = cget(nz[q], c), vc = cget(nv[q], c);
-                    const bool bad = (((cbad[c] >> t) & 1u) != 0u) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) |
-                                     !(vc <= vmax) | !(cget(nm[q], c) >= mempty);
-                    vnowm[q] |= (bad ? 1 : 0) << c;
-                }
+                nx[q] = vfma(dtf, ax + wx, x[q]);
+                ny[q] = vfma(dtf, ay + wy, y[q]);
                 th[q] = fast_atan2(ny[q], nx[q]);
                 const V r2 = vfma(nx[q], nx[q], ny[q] * ny[q]);
                 const V rh = r2 * vmap(r2, [](float a) { return rsqrt_approx(fmaxf(a, 1e-30f)); });
@@ -1087,16 +1127,15 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                 V sarc;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) cset(sarc, c, cget(at, c) > 1e-4f ? cget(sfull, c) : cget(rh, c));
-                beta[q] = fast_atan2_xpos(nz[q], sarc);
+                beta[q] = fast_atan2_xpos(nz, sarc);
                 lnowm[q] = 0;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta[q], c) <= sc.P_beta) &
-                                    (cget(at, c) <= sc.P_chi) & (fabsf(cget(nchi[q], c)) >= sc.P_chi_west) &
-                                    (cget(nv[q], c) <= sc.P_vs);
+                                    (cget(at, c) <= sc.P_chi);
                     lnowm[q] |= (ln ? 1 : 0) << c;
                 }
-                if (kind != 0) lnowm[q] = 0;
+                lnowm[q] &= kind == 0 ? lkt : 0;                  // speed / heading conditions: precomputed
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
                     cset(px[q], c, ((flym[q] >> c) & 1) ? cget(nx[q], c) : __int_as_float(0x7fffffff));
@@ -1105,26 +1144,25 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
             if (R == W || lane < R) {
                 const float4 ex = make_float4(px[0].x, px[0].y, px[1].x, px[1].y);
                 const float4 ey = make_float4(ny[0].x, ny[0].y, ny[1].x, ny[1].y);
-                const float4 ez = make_float4(nz[0].x, nz[0].y, nz[1].x, nz[1].y);
                 s_px[pb] = ex; s_px[pb + R] = ex;
                 s_py[pb] = ey; s_py[pb + R] = ey;
-                s_pz[pb] = ez; s_pz[pb + R] = ez;
+                s_pz[pb] = nz; s_pz[pb + R] = nz;
             }
             seg_sync();
             // verdict bytes: bit 31 (sample s, candidate 0), 23 (s, 1), 15 (s + 1, 0), 7 (s + 1, 1)
             uint32_t confw = 0u;
 #pragma unroll
             for (int d = 1; d <= R / 2; ++d) {
-                const float4 qx = s_px[pb + d], qy = s_py[pb + d], qz = s_pz[pb + d];
+                const float4 qx = s_px[pb + d], qy = s_py[pb + d];
+                const float2 qz = s_pz[pb + d];
                 const V dx0 = px[0] - make_float2(qx.x, qx.y), dx1 = px[1] - make_float2(qx.z, qx.w);
                 const V dy0 = ny[0] - make_float2(qy.x, qy.y), dy1 = ny[1] - make_float2(qy.z, qy.w);
-                const V dz0 = nz[0] - make_float2(qz.x, qz.y), dz1 = nz[1] - make_float2(qz.z, qz.w);
+                const V w = vabs(nz - qz) - sc.twoPh;
                 const V u0 = vfma(dx0, dx0, vfma(dy0, dy0, -sc.twoPr2)), u1 = vfma(dx1, dx1, vfma(dy1, dy1, -sc.twoPr2));
-                const V w0 = vabs(dz0) - sc.twoPh, w1 = vabs(dz1) - sc.twoPh;
-                const uint32_t hi = __byte_perm(__float_as_uint(u0.x) & __float_as_uint(w0.x),
-                                                __float_as_uint(u0.y) & __float_as_uint(w0.y), 0x3737);
-                const uint32_t lo = __byte_perm(__float_as_uint(u1.x) & __float_as_uint(w1.x),
-                                                __float_as_uint(u1.y) & __float_as_uint(w1.y), 0x3737);
+                const uint32_t hi = __byte_perm(__float_as_uint(u0.x) & __float_as_uint(w.x),
+                                                __float_as_uint(u0.y) & __float_as_uint(w.y), 0x3737);
+                const uint32_t lo = __byte_perm(__float_as_uint(u1.x) & __float_as_uint(w.x),
+                                                __float_as_uint(u1.y) & __float_as_uint(w.y), 0x3737);
                 const uint32_t hv = (hi & 0xFFFF0000u) | (lo & 0x0000FFFFu);
                 if constexpr (XW) {
                     // partner lane + d learns this verdict from shared memory after the scan
@@ -1146,15 +1184,18 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
             // ---------------- 5. per chain: cost terms, flags, state update
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const V argA = vfma(th[q], cA_th, vfma(nchi[q], cA_chi, cA_0));
+                const V argA = vfma(th[q], cA_th, vfma(nchi, cA_chi, cA_0));
                 const V wA = wrap_pi(argA);
                 sA[q] = vfma(vabs(wA), flyf[q], sA[q]);
-                sB[q] = vfma(vabs(vfma(nz[q], cB_z, vfma(beta[q], cB_b, cB_0))), flyf[q], sB[q]);
-                sC[q] = vfma(vabs(nv[q] - v_D), flyf[q], sC[q]);
-                fuel[q] = vfma(dtef[q], T, fuel[q]);
+                sB[q] = vfma(vabs(vfma(nz, cB_z, vfma(beta[q], cB_b, cB_0))), flyf[q], sB[q]);
+                fuel[q] = vfma(flyf[q], fi, fuel[q]);
                 if (sc.has_noise) {
+#if SMC_K2_POP_SMEM
                     const V pd = popdense_pad(sc, smem_all, nx[q], ny[q]);   // staged (launch_rollout checks it fits)
-                    const V zz = nz[q] * sc.inv_Ac;
+#else
+                    const V pd = popdense_pad<V, true>(sc, sc.popp, nx[q], ny[q]);   // L1-resident, read-only path
+#endif
+                    const V zz = nz * sc.inv_Ac;
                     V f;
 #pragma unroll
                     for (int c = 0; c < 2; ++c) cset(f, c, __saturatef(fmaf(-cget(zz, c), cget(zz, c), 1.0f)));   // max(1 - zz^2, 0)
@@ -1164,10 +1205,11 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                         cset(sN[q], c, cget(sN[q], c) + (((flym[q] >> c) & 1) ? cget(nzs, c)
                                                                                : ((act && ((landedm[q] >> c) & 1)) ? 1.0f : 0.0f)));
                 }
-                violm[q] |= flym[q] & (vnowm[q] | confm[q]);
+                violm[q] |= flym[q] & (vbt | confm[q]);
                 landedm[q] |= flym[q] & lnowm[q];
-                x[q] = nx[q]; y[q] = ny[q]; z[q] = nz[q]; v[q] = nv[q]; chi[q] = nchi[q]; m[q] = nm[q];
+                x[q] = nx[q]; y[q] = ny[q];
             }
+            z = nz;
         }  // t
 
         // ---------------- utility J_T and weight, both chains
@@ -1187,7 +1229,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
                         const float J1 = clamp01(1.0f - cget(sA[q], c) * invHa * (1.0f / kPi));
                         if (kind == 1) {
                             const float c2 = flagB ? 1.0f : clamp01((supB - cget(sB[q], c) * invHa) * invDenB);
-                            const float c3 = clamp01(1.0f - cget(sC[q], c) * invHa * invSupC);
+                            const float c3 = clamp01(1.0f - cget(sCc, c) * invHa * invSupC);
                             J = sc.alpha_dep[0] * J1 + sc.alpha_dep[1] * Jfuel + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
                         } else {
                             const float c1 = clamp01(1.0f - cget(sB[q], c) * invHa * invSupE);
@@ -1252,7 +1294,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
     }
     if (lane == 0) s_dec[seg] = valid ? nacc : 0;
     __syncthreads();
-    uint32_t *s_cm = reinterpret_cast<uint32_t *>(s_ctrl);
+    uint32_t *s_cm = reinterpret_cast<uint32_t *>(s_r0);
     s_cm[tid] = (valid && isac) ? f2ord(ell_s) : 0u;
     __syncthreads();
     if (tid < n) {
@@ -1269,7 +1311,7 @@ __global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevS
 
 template <int W, int R>
 static cudaError_t launch_2s_r(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
-    const int npop = sc.has_noise ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;
+    const int npop = (SMC_K2_POP_SMEM && sc.has_noise) ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;
     const size_t smem = rollout2s_smem_bytes(W, sc.H, (npop + 3) & ~3);
     auto kern = k_rollout_2s<W, R>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1437,10 +1479,11 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
-    // the two-chain kernel reads the noise grid from shared memory only: a grid too large for it
-    // (more than kPopSmem padded entries) takes the one-chain kernel
-    const bool pop_fits = !sc.has_noise || pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) > 0;
-    if (NC == 2 && !debug && !dense && pop_fits && W >= SMC_K2_2S_MINW && ns2_enabled())
+    // the two-chain kernel: its per-step flag masks hold 2 H <= 32 bits; built to stage the noise
+    // grid in shared memory (SMC_K2_POP_SMEM), a grid larger than kPopSmem padded entries takes the
+    // one-chain kernel
+    const bool pop_fits = !SMC_K2_POP_SMEM || !sc.has_noise || pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) > 0;
+    if (NC == 2 && !debug && !dense && pop_fits && sc.H <= 16 && W >= SMC_K2_2S_MINW && ns2_enabled())
         return launch_2s(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);

@@ -23,9 +23,12 @@ A pipe count is the minimum the equations need: e.g. the trilinear
 interpolation of the 2x2x2 field is counted in its 7-coefficient polynomial
 form, the lower-triangular 8x8 factor as 36 FMA per component, atan2 as
 its degree-15 odd polynomial on the MUFU reciprocal.  Work shared by several
-aircraft-steps (the wind field of a (particle, sample, step) is shared by
-the N aircraft and, under common random numbers, by both MH candidates) is
-divided among them.
+aircraft-steps is divided among them: the wind field of a (particle, sample,
+step) is shared by the N aircraft and, under common random numbers, by both
+MH candidates; the airframe states z, v, chi, m of Eq. hor do not depend on
+the wind (it enters only dx/dt, dy/dt), so their integration, the envelope
+and the departures' altitude / speed terms are shared by the S samples of a
+(particle, candidate, aircraft, step).
 
 K4-K6 (scans, gather/propose) are HBM-bound; their algorithmic bytes per
 (aircraft, particle) per round are 8 + 36 H.
@@ -50,23 +53,28 @@ def _v(fma=0.0, alu=0.0, xu=0.0, imadw=0.0, shfl=0.0):
     return np.array([fma, alu, xu, imadw, shfl], dtype=np.float64)
 
 
-# --- per aircraft-step of one candidate (Eq. hor; R12) -------------------------------------
-# rho(z): 1 FMA + max + lg2 + mul + ex2; q = c v^2 rho: 3; m g / q: rcp + 2; D = q (cd0 + cd2 (1 + tan^2)
-# (mg/q)^2): 5; sin/cos chi + wrap (2 FMA, FRND); x, y, z, v, chi, m, fuel updates: 15 FMA + rcp m + rcp v
-DYN = _v(fma=2 + 3 + 2 + 5 + 2 + 15, alu=1, xu=2 + 1 + 2 + 1 + 2)
+# --- airframe, per (particle, candidate, aircraft, step) -- shared by the S samples (Eq. hor, P:246-255;
+# R12): rho(z): 1 FMA + max + lg2 + mul + ex2; q = c v^2 rho: 3; m g / q: rcp + 2; D = q (cd0 + cd2 (1 +
+# tan^2) (mg/q)^2): 5; sin/cos chi + wrap (2 FMA, FRND); z, v, chi, m updates: 9 FMA + rcp m + rcp v; the
+# air-relative ground velocity v cos g (cos chi, sin chi): 3; envelope and mass at the new state:
+# 5 compares; the control bounds: 4 compares
+AIRFRAME = _v(fma=2 + 3 + 2 + 5 + 2 + 9 + 3, alu=1 + 5 + 4, xu=2 + 1 + 2 + 1 + 2)
+# --- ground track per aircraft-step (one sample, one candidate): x, y (wind added, 2 FMA each), fuel
+TRACK = _v(fma=4 + 1)
 # trilinear wind at the aircraft: 3 normalised coordinates, 4 shared products, 7 FMA per component,
 # nominal + gust
 WIND_INTERP = _v(fma=3 + 4 + 14 + 2)
-# envelope and mass at the new state: 5 compares (control bounds: 4 per step per round, /S)
-CHECKS = _v(alu=5)
-CTRL_CHECKS = _v(alu=4)                     # per (particle, candidate, step, aircraft) per round -> / S
 # theta = atan2(y, x): rcp, 11 FMA (polynomial), max/min, 2 selects, sign
 THETA = _v(fma=12, alu=5, xu=1)
 # arrival: rho_h (rsqrt), arc s (rcp), beta = atan2(z, s) (right half-plane), heading wrap, landing sector
-# (5 compares), deviation D (chi_hat = pi + 2 theta, wrap) and E
-ARR = _v(fma=2 + 1 + 2 + 10 + 1 + 2 + 2 + 2 + 1 + 2, alu=1 + 3 + 5 + 1, xu=1 + 1 + 1 + 1 + 1)
-# departure: A = |wrap(theta - theta_F)|, B = |z_tf - z|, C = |v - v_D|
-DEP = _v(fma=8, xu=1)
+# (3 position compares per sample; speed and heading: 2 compares per airframe step), deviation D
+# (chi_hat = pi + 2 theta, wrap) and E
+ARR = _v(fma=2 + 1 + 2 + 10 + 1 + 2 + 2 + 2 + 1 + 2, alu=1 + 3 + 3 + 1, xu=1 + 1 + 1 + 1 + 1)
+ARR_AIRFRAME = _v(alu=2)
+# departure: A = |wrap(theta - theta_F)| per sample; B = |z_tf - z|, C = |v - v_D| per airframe step
+# (a departure never lands: both are sample-independent)
+DEP = _v(fma=4, xu=1)
+DEP_AIRFRAME = _v(fma=4)
 # noise (bilinear 1 km grid): q(z), cell index, 3 lerps, J_noise
 NOISE = _v(fma=14, alu=11)
 # one unordered pair of Eq. avoidance: dx dy dz d^2 (5), 2 compares + and + or, one exchange
@@ -90,8 +98,9 @@ def ops_vector(scn: dict, C: int, S: int = 16) -> np.ndarray:
     """Algorithmic ops per aircraft-step [fma, alu, xu, imadw, shfl] (all-active horizon)."""
     n, H = int(scn["n"]), int(scn["H"])
     f_arr = float((np.asarray(scn["kind"]) == 0).sum()) / n
-    v = DYN + WIND_INTERP + CHECKS + CTRL_CHECKS / max(S, 1) + THETA
-    v = v + f_arr * ARR + (1 - f_arr) * DEP
+    Sd = max(S, 1)
+    v = TRACK + WIND_INTERP + THETA + AIRFRAME / Sd
+    v = v + f_arr * (ARR + ARR_AIRFRAME / Sd) + (1 - f_arr) * (DEP + DEP_AIRFRAME / Sd)
     if float(scn["noise_w"]) > 0 and int(scn["pop_nx"]) > 0:
         v = v + NOISE
     v = v + PAIR * (n - 1) / 2.0

@@ -315,7 +315,7 @@ def test_production_rounds_parity(smc, case):
             # clamped to an edge (the two-chain kernel's padded shared-memory grid)
             scn.update(pop_nx=13, pop_ny=7, pop_x0=-15000.0, pop_y0=-9000.0, pop_dx=2500.0)
         elif case == "n12_noise_big":
-            # 121 x 121 grid: too large for shared memory, one-chain kernel reads it from global
+            # 121 x 121 grid: larger than the shared-memory staging limit (read from global)
             scn.update(pop_nx=121, pop_ny=121, pop_x0=-42000.0, pop_y0=-42000.0, pop_dx=700.0)
     else:
         scn, cfg = sc.config(int(case[1:]))
