@@ -265,7 +265,65 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
     // interleaved so each quantity loads as a float2 pair -- (T0, T1, tphi0, tphi1) and
     // (sg0, sg1, cg0, cg1) at s_ctrl[(2t + h) kBlock + tid], h = 0, 1.
     uint32_t cbad[NC];
-    {
+    // SP (one candidate, sample pairs): the airframe -- z, v, chi, m; wind-independent (Eq. hor,
+    // P:246-251) -- is integrated once per particle here, as in k_rollout_2s: per step the
+    // air-relative ground velocity, z and chi after the step (s_rec) and the fuel increment
+    // (s_rfi); envelope / landing speed-heading flags as bit t of vbadm / lokm
+    float4 *const s_rec = reinterpret_cast<float4 *>(s_ctrl);              // SP: [H][kBlock]
+    float *const s_rfi = reinterpret_cast<float *>(s_rec + H * kBlock);      // SP: [H][kBlock]
+    uint32_t vbadm = 0u, lokm = 0u;
+    float sCc = 0.0f;
+    if constexpr (SP) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cbad[c] = 0;
+        const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
+        const float cq1 = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
+        const float *src = args.ctrl[0] + ((size_t)lloc * n + lane) * H * 3;
+        float v = Ap->x0[3], z = Ap->x0[2], chi = Ap->x0[4], m = Ap->x0[5];
+        const float dt1 = sc.dt, g1 = sc.g;
+        bool broken = false;
+        for (int t = 0; t < H; ++t) {
+            float T = 0.f, ph = 0.f, ga = 0.f;
+            if (isac && valid) { T = src[3 * t]; ph = src[3 * t + 1]; ga = src[3 * t + 2]; }
+            float sph, cph, sga, cga;
+            __sincosf(ph, &sph, &cph);
+            __sincosf(ga, &sga, &cga);
+            const float tph = sph * rcp_approx(cph);
+            const bool cbd = (fabsf(ga) > gmax) || !(fabsf(ph) < pmax) || (T < Tmin) || (T > Tmax);
+            const bool act = first <= t;
+            const float dta = act ? dt1 : 0.0f, dtea = act ? dt_eta : 0.0f;
+            float qd = cq1 * v * v;
+            if (sc.density_mode == 0) qd = qd * ex2_approx(lg2_approx(fmaxf(fmaf(z, -2.2558e-5f, 1.0f), 0.0f)) * 4.2559f);
+            const float mgq = (m * g1) * rcp_approx(qd);
+            const float D = qd * fmaf(fmaf(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
+            float sch, cch;
+            __sincosf(chi, &sch, &cch);
+            const float vcg = v * cga;
+            float ax = vcg * cch, ay = vcg * sch;
+            float nz = fmaf(dta * v, sga, z);
+            const float nv = fmaf(dta, fmaf(T - D, rcp_approx(m), sga * (-g1)), v);
+            float nchi = wrap_pi(fmaf((dta * g1) * tph, rcp_approx(v), chi));
+            const float nm = fmaf(-dtea, T, m);
+            float fi = T * dtea;
+            const bool fin = (fabsf(ax) < INFINITY) & (fabsf(ay) < INFINITY) & (fabsf(nz) < INFINITY) &
+                             (fabsf(nv) < INFINITY) & (fabsf(nchi) < INFINITY) & (fabsf(nm) < INFINITY);
+            broken |= !fin;
+            bool bad, lok;
+            if (broken) {                       // non-finite: far-away sentinel (see k_rollout_2s)
+                ax = ay = nz = 1e30f; nchi = 0.0f; fi = 0.0f;
+                bad = true; lok = false;
+            } else {
+                bad = cbd | !(nz >= zmin) | !(nz <= zmax) | !(nv >= vmin) | !(nv <= vmax) | !(nm >= mempty);
+                lok = (nv <= sc.P_vs) & (fabsf(nchi) >= sc.P_chi_west);
+                if (act) sCc += fabsf(nv - v_D);
+            }
+            vbadm |= (bad ? 1u : 0u) << t;
+            lokm |= (lok ? 1u : 0u) << t;
+            s_rec[t * kBlock + tid] = make_float4(ax, ay, nz, nchi);
+            s_rfi[t * kBlock + tid] = fi;
+            v = nv; z = nz; chi = nchi; m = nm;
+        }
+    } else {
         const float gmax = Ap->gamma_max, pmax = Ap->phi_max, Tmin = Ap->T_min, Tmax = Ap->T_max;
         const float *src[NC];
 #pragma unroll
@@ -514,7 +572,9 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) cset(flyf, c, ((flym >> c) & 1) ? 1.0f : 0.0f);
             V T, tph, sga, cga;
-            if constexpr (NC == 2) {
+            if constexpr (SP) {
+                T = tph = sga = cga = vsplat<V>(0.0f);           // (airframe from the records)
+            } else if constexpr (NC == 2) {
                 const float4 a = s_ctrl[(2 * t) * kBlock + tid], b = s_ctrl[(2 * t + 1) * kBlock + tid];
                 T = make_float2(a.x, a.y); tph = make_float2(a.z, a.w);
                 sga = make_float2(b.x, b.y); cga = make_float2(b.z, b.w);
@@ -566,42 +626,54 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                     wy = tripoly(Wn + 8, c0y, fx, fy, fz);
                 }
             }
-            // Eq. hor, coordinated-turn lift and parabolic drag (R12):
-            // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a landed / inactive aircraft advances with
-            // dt_f = 0 (its state stays frozen, R18/R20)
-            V qd = cq * v * v;
-            if (sc.density_mode == 0) {
-                const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
-                qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
-            }
-            const V mgq = (m * g) * vmap(qd, rcp_approx);
-            const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
-            const V chr = chi;                                    // kept in [-pi, pi] (wrapped once per step)
-            V sch, cch;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                float s_, c_;
-                __sincosf(cget(chr, c), &s_, &c_);
-                cset(sch, c, s_); cset(cch, c, c_);
-            }
+            V nx, ny, nz, nv, nchi, nm;
+            int vnowm = 0, lokt = ALLC;
             const V dtf = flyf * dt, dtef = flyf * dt_eta;
-            const V vcg = v * cga;
-            const V nx = vfma(dtf, vfma(vcg, cch, wx), x);
-            const V ny = vfma(dtf, vfma(vcg, sch, wy), y);
-            const V nz = vfma(dtf * v, sga, z);
-            const V nv = vfma(dtf, vfma(T - D, vmap(m, rcp_approx), sga * (-g)), v);
-            const V nchi = wrap_pi(vfma((dtf * g) * tph, vmap(v, rcp_approx), chi));   // heading, wrapped (R32)
-            const V nm = vfma(-dtef, T, m);
-            // envelope and mass at j = t+1 (R17)
-            int vnowm = 0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const float zc = cget(nz, c), vc = cget(nv, c);
-                // unordered compares (a NaN fails every bound), OR-ed without short-circuit branches
-                const bool bad = (((cbad[c] >> t) & 1u) != 0u) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) |
-                                 !(vc <= vmax) | !(cget(nm, c) >= mempty);
-                // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
-                vnowm |= (bad ? 1 : 0) << c;
+            if constexpr (SP) {
+                // the candidate's airframe after the step (both samples): per-particle records
+                const float4 rec = s_rec[t * kBlock + tid];
+                nx = vfma(dtf, wx + rec.x, x);
+                ny = vfma(dtf, wy + rec.y, y);
+                nz = vsplat<V>(rec.z); nchi = vsplat<V>(rec.w);
+                nv = nm = vsplat<V>(0.0f);                       // (flags precomputed)
+                vnowm = ((vbadm >> t) & 1u) ? ALLC : 0;
+                lokt = ((lokm >> t) & 1u) ? ALLC : 0;
+            } else {
+                // Eq. hor, coordinated-turn lift and parabolic drag (R12):
+                // C_L^2 = (m g / q)^2 (1 + tan^2 phi); a landed / inactive aircraft advances with
+                // dt_f = 0 (its state stays frozen, R18/R20)
+                V qd = cq * v * v;
+                if (sc.density_mode == 0) {
+                    const V base = vmap(vfma(z, -2.2558e-5f, 1.0f), [](float a) { return fmaxf(a, 0.0f); });
+                    qd = qd * vmap(vmap(base, lg2_approx) * 4.2559f, ex2_approx);
+                }
+                const V mgq = (m * g) * vmap(qd, rcp_approx);
+                const V D = qd * vfma(vfma(tph, tph, 1.0f) * cd2, mgq * mgq, cd0);
+                const V chr = chi;                                    // kept in [-pi, pi] (wrapped once per step)
+                V sch, cch;
+    #pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    float s_, c_;
+                    __sincosf(cget(chr, c), &s_, &c_);
+                    cset(sch, c, s_); cset(cch, c, c_);
+                }
+                const V vcg = v * cga;
+                nx = vfma(dtf, vfma(vcg, cch, wx), x);
+                ny = vfma(dtf, vfma(vcg, sch, wy), y);
+                nz = vfma(dtf * v, sga, z);
+                nv = vfma(dtf, vfma(T - D, vmap(m, rcp_approx), sga * (-g)), v);
+                nchi = wrap_pi(vfma((dtf * g) * tph, vmap(v, rcp_approx), chi));   // heading, wrapped (R32)
+                nm = vfma(-dtef, T, m);
+                // envelope and mass at j = t+1 (R17)
+    #pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const float zc = cget(nz, c), vc = cget(nv, c);
+                    // unordered compares (a NaN fails every bound), OR-ed without short-circuit branches
+                    const bool bad = (((cbad[c] >> t) & 1u) != 0u) | !(zc >= zmin) | !(zc <= zmax) | !(vc >= vmin) |
+                                     !(vc <= vmax) | !(cget(nm, c) >= mempty);
+                    // (x, y, chi stay finite whenever v, z, m and the controls pass: no extra test needed)
+                    vnowm |= (bad ? 1 : 0) << c;
+                }
             }
             const V th = fast_atan2(ny, nx);
             // descent angle on the flow-field arc (Eq. flow, R9) and landing test (R10):
@@ -618,9 +690,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const bool ln = (cget(rh, c) <= sc.P_runway) & (cget(beta, c) <= sc.P_beta) & (cget(at, c) <= sc.P_chi) &
-                                (fabsf(cget(nchi, c)) >= sc.P_chi_west) & (cget(nv, c) <= sc.P_vs);
+                                (SP || ((fabsf(cget(nchi, c)) >= sc.P_chi_west) & (cget(nv, c) <= sc.P_vs)));
                 lnowm |= (ln ? 1 : 0) << c;
             }
+            if constexpr (SP) lnowm &= lokt;                     // speed / heading: precomputed
             if (kind != 0) lnowm = 0;                            // only arrivals land (Eq. TO_init)
             // a landed / inactive aircraft is a NaN position: every comparison fails (as it does for a
             // violator whose state has become non-finite)
@@ -686,8 +759,12 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             const V wA = wrap_pi(argA);
             sA = vfma(vabs(wA), flyf, sA);
             sB = vfma(vabs(vfma(nz, cB_z, vfma(beta, cB_b, cB_0))), flyf, sB);
-            sC = vfma(vabs(nv - v_D), flyf, sC);
-            fuel = vfma(dtef, T, fuel);
+            if constexpr (SP) {
+                fuel = vfma(flyf, vsplat<V>(s_rfi[t * kBlock + tid]), fuel);
+            } else {
+                sC = vfma(vabs(nv - v_D), flyf, sC);
+                fuel = vfma(dtef, T, fuel);
+            }
             if (sc.has_noise) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
@@ -699,7 +776,8 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
             }
             violm |= flym & (vnowm | confm);
             landedm |= flym & lnowm;
-            x = nx; y = ny; z = nz; v = nv; chi = nchi; m = nm;
+            x = nx; y = ny; z = nz;
+            if constexpr (!SP) { v = nv; chi = nchi; m = nm; }
             if (DEBUG && valid && isac && args.dbg_traj) {
                 float *tr = args.dbg_traj + ((((size_t)lloc * args.S + s) * n + lane) * (H + 1) + t + 1) * 6;
                 tr[0] = cget(x, 0); tr[1] = cget(y, 0); tr[2] = cget(z, 0);
@@ -730,7 +808,7 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
                         c0 = J1;
                         c1 = Jfuel;
                         c2 = flagB ? 1.0f : clamp01((supB - cget(sB, c) * invHa) * invDenB);
-                        c3 = clamp01(1.0f - cget(sC, c) * invHa * invSupC);
+                        c3 = clamp01(1.0f - (SP ? sCc : cget(sC, c)) * invHa * invSupC);
                         J = sc.alpha_dep[0] * c0 + sc.alpha_dep[1] * c1 + sc.alpha_dep[2] * c2 + sc.alpha_dep[3] * c3;
                     } else {
                         c0 = J1;
@@ -1475,7 +1553,7 @@ int segment_width(int n, bool dense) {
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st) {
     const bool dense = sc.wng > 8;
     const int W = segment_width(sc.n, dense);
-    if (NC == 1 && !debug && !dense && W >= 8 && sp_enabled()) return launch_sp(W, sc, a, st);
+    if (NC == 1 && !debug && !dense && W >= 8 && sc.H <= 32 && sp_enabled()) return launch_sp(W, sc, a, st);   // flags: bit t
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
