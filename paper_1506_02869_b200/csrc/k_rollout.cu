@@ -913,7 +913,10 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 // wind fields are drawn like the sample-pair instances' (two slots per segment).  Results are
 // identical to k_rollout<W, 2>: the same operations in the same order per (sample, candidate).
 #ifndef SMC_K2_MINB2S
-#define SMC_K2_MINB2S 3
+#define SMC_K2_MINB2S 4     // 128 registers: no spill once the airframe left the sample loop (c2 -5.6 %, c4 -4.3 %)
+#endif
+#ifndef SMC_K2_MINB2S32
+#define SMC_K2_MINB2S32 3   // 32-lane segments (25-32 aircraft): more live state per lane
 #endif
 
 #ifndef SMC_K2_2S_MINW
@@ -949,7 +952,7 @@ size_t rollout2s_smem_bytes(int W, int H, int npop) {
 }
 
 template <int W, int R>
-__global__ void __launch_bounds__(kBlock, SMC_K2_MINB2S) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
+__global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MINB2S) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
     static_assert(W >= 8 && W % 4 == 0, "two-chain instances need W >= 8 (eight AR(1) nodes per slot), W = 4 GB");
     constexpr bool XW = k2_cross_warp(W);
     static_assert(!XW || R == W, "packed segments use the whole segment as the separation ring");
