@@ -1240,11 +1240,10 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
                 const V dy0 = ny[0] - make_float2(qy.x, qy.y), dy1 = ny[1] - make_float2(qy.z, qy.w);
                 const V w = vabs(nz - qz) - sc.twoPh;
                 const V u0 = vfma(dx0, dx0, vfma(dy0, dy0, -sc.twoPr2)), u1 = vfma(dx1, dx1, vfma(dy1, dy1, -sc.twoPr2));
-                const uint32_t hi = __byte_perm(__float_as_uint(u0.x) & __float_as_uint(w.x),
-                                                __float_as_uint(u0.y) & __float_as_uint(w.y), 0x3737);
-                const uint32_t lo = __byte_perm(__float_as_uint(u1.x) & __float_as_uint(w.x),
-                                                __float_as_uint(u1.y) & __float_as_uint(w.y), 0x3737);
-                const uint32_t hv = (hi & 0xFFFF0000u) | (lo & 0x0000FFFFu);
+                // sign bytes first, then one AND: w (per candidate) is shared by the two chains
+                const uint32_t pu = __byte_perm(__byte_perm(__float_as_uint(u0.x), __float_as_uint(u0.y), 0x3737),
+                                                __byte_perm(__float_as_uint(u1.x), __float_as_uint(u1.y), 0x3737), 0x3254);
+                const uint32_t hv = pu & __byte_perm(__float_as_uint(w.x), __float_as_uint(w.y), 0x3737);
                 if constexpr (XW) {
                     // partner lane + d learns this verdict from shared memory after the scan
                     if (2 * d < R) s_hv[(d - 1) * (SEGA * W) + seg * W + lane] = hv;
