@@ -274,6 +274,11 @@ smc_status smc_debug_rollout(smc_ctx *ctx, const float *controls, uint32_t L, ui
 smc_status smc_debug_evaluate(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t S,
                               uint32_t k, float *ell);
 
+/* The same through the two-candidate production kernel (both MH candidates = controls, so the
+ * survivor's weights are the candidates' whatever MH decides): the kernel of rounds k >= 1. */
+smc_status smc_debug_evaluate2(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t S,
+                               uint32_t k, float *ell);
+
 /* MH decisions (R1) for injected joint log2 weights: acc[l] = 1 accept. */
 smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_prop, uint32_t L,
                         uint32_t k, uint8_t *acc);

@@ -1440,7 +1440,7 @@ struct DevTmp {
 
 static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t l0, uint32_t S,
                                      uint32_t k, bool debug, float *J, uint8_t *viol, float *comp, float *fuel,
-                                     int32_t *landed, float *traj, float *ell) {
+                                     int32_t *landed, float *traj, float *ell, int nc = 1) {
     if (!ctx || !controls || L == 0 || S == 0) return SMC_EINVAL;
     if (!ctx->have_scn) return fail(ctx, SMC_ESTATE, "no scenario");
     const int n = ctx->dsc.n, H = ctx->dsc.H;
@@ -1470,7 +1470,8 @@ static smc_status debug_rollout_impl(smc_ctx *ctx, const float *controls, uint32
     ra.ell_out = dell; ra.lam_out = dlam; ra.surv_out = dsurv; ra.colmax = dcm; ra.n_accept = dacc;
     ra.dbg_J = dJ; ra.dbg_comp = dcomp; ra.dbg_fuel = dfuel; ra.dbg_traj = dtraj; ra.dbg_viol = dviol;
     ra.dbg_landed = dland;
-    LAUNCH(launch_rollout(ctx->dsc, ra, 1, debug, ctx->st));
+    if (nc == 2) ra.ctrl[1] = dctrl;          // both candidates alike: the survivor's weights are theirs
+    LAUNCH(launch_rollout(ctx->dsc, ra, nc, debug, ctx->st));
     if (debug) {
         if (J) CK(cudaMemcpyAsync(J, dJ, sizeof(float) * nu, cudaMemcpyDeviceToHost, ctx->st));
         if (viol) CK(cudaMemcpyAsync(viol, dviol, nu, cudaMemcpyDeviceToHost, ctx->st));
@@ -1501,6 +1502,12 @@ extern "C" smc_status smc_debug_evaluate(smc_ctx *ctx, const float *controls, ui
                                          float *ell) {
     return debug_rollout_impl(ctx, controls, L, 0, S, k, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                               ell);
+}
+
+extern "C" smc_status smc_debug_evaluate2(smc_ctx *ctx, const float *controls, uint32_t L, uint32_t S, uint32_t k,
+                                          float *ell) {
+    return debug_rollout_impl(ctx, controls, L, 0, S, k, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              ell, 2);
 }
 
 extern "C" smc_status smc_debug_mh(smc_ctx *ctx, const double *lam_cur, const double *lam_prop, uint32_t L, uint32_t k,

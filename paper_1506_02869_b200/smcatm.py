@@ -167,6 +167,7 @@ def load():
         "smc_debug_rollout": (st, [v, f32p, u32, u32, u32, u32, f32p, P(C.c_uint8), f32p, f32p,
                                    P(C.c_int32), f32p]),
         "smc_debug_evaluate": (st, [v, f32p, u32, u32, u32, f32p]),
+        "smc_debug_evaluate2": (st, [v, f32p, u32, u32, u32, f32p]),
         "smc_debug_mh": (st, [v, f64p, f64p, u32, u32, P(C.c_uint8)]),
         "smc_debug_resample": (st, [v, f32p, u32, u32, u32, u32, P(C.c_int32), P(u64)]),
         "smc_debug_propose": (st, [v, f32p, P(C.c_int32), u32, u32, f32p, f32p]),
@@ -189,7 +190,7 @@ def load():
 
 EXPORTED = ["smc_workspace_bytes", "smc_init", "smc_set_scenario", "smc_iterate", "smc_best_controls",
             "mpc_step", "smc_solve", "smc_phase_times", "smc_last_error", "smc_destroy", "smc_set_mpc_index", "smc_get_mpc_index",
-            "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_mh", "smc_debug_mh_aircraft",
+            "smc_launch_count", "smc_io_bytes", "smc_nccl_unique_id", "smc_debug_rollout", "smc_debug_evaluate", "smc_debug_evaluate2", "smc_debug_mh", "smc_debug_mh_aircraft",
             "smc_debug_resample", "smc_debug_propose", "smc_debug_population", "smc_shard_range",
             "smc_shard_offsets", "smc_slot_count", "smc_fuel_estimates", "smc_ipc_record", "smc_ipc_peek"]
 
@@ -428,11 +429,14 @@ class Solver:
             out["traj"] = tr
         return out
 
-    def debug_evaluate(self, controls, S, k):
+    def debug_evaluate(self, controls, S, k, two=False):
+        """smc_debug_evaluate (single-candidate kernel) or, two=True, smc_debug_evaluate2 (the
+        two-candidate kernel with both candidates = controls)."""
         c = np.ascontiguousarray(np.asarray(controls, dtype=np.float32))
         L = c.shape[0]
         ell = np.zeros((L, self.n), np.float32)
-        self._check(self.lib.smc_debug_evaluate(self.ctx, _p(c, C.c_float), L, S, k, _p(ell, C.c_float)))
+        fn = self.lib.smc_debug_evaluate2 if two else self.lib.smc_debug_evaluate
+        self._check(fn(self.ctx, _p(c, C.c_float), L, S, k, _p(ell, C.c_float)))
         return ell
 
     def debug_mh(self, lam_cur, lam_prop, k):

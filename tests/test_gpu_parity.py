@@ -286,14 +286,15 @@ def test_evaluate_parity(smc, case, sp, monkeypatch):
     sol.close()
 
 
-def test_stalled_airframe_parity(smc):
+@pytest.mark.parametrize("two", [False, True])
+def test_stalled_airframe_parity(smc, two):
     """An aircraft that leaves the model's domain: thrust 0 and a climb beyond gamma_max at dt = 20 s
     (c4) drive v through 0 within the horizon.  The oracle propagates the state literally (P:250,
     R42's replacement: violated aircraft keep flying); with gamma = 0.6 the FP32 state overflows and
     K2's once-per-particle airframe replaces it by a far-away sentinel (no conflict, envelope failed),
     with the legal maximum climb it stays finite with v < 0 on both sides.  The stalled aircraft is
     infeasible on both sides and every other aircraft's weight matches the oracle's (no spurious or
-    missed conflict)."""
+    missed conflict).  two: through the two-candidate kernel (both candidates = the controls)."""
     scn, cfg = sc.config(4, noise_w=0.0)
     n, H = scn["n"], scn["H"]
     L, S = 512, 5
@@ -306,10 +307,10 @@ def test_stalled_airframe_parity(smc):
     r1 = P.rollout(ctrl[4].astype(np.float64), 4, 0, 4, cfg.seed)
     assert np.abs(r6["traj"][0, -1, 3]) > 1e38 and r1["traj"][0, -1, 3] < 0.0     # overflow / reversed flight
     sol = _solver(smc, scn, L=L, S=S, seed=cfg.seed)
-    ell_g = sol.debug_evaluate(ctrl, S, 4).astype(np.float64)
+    ell_g = sol.debug_evaluate(ctrl, S, 4, two=two).astype(np.float64)
     ell_o, mg = P.evaluate(ctrl.astype(np.float64), S, 4, cfg.seed, margin=True)
     assert not np.isfinite(ell_o[stall, 0]).any() and not np.isfinite(ell_g[stall, 0]).any()
-    _check_ell(ell_g, ell_o, mg, S, "stalled airframe")
+    _check_ell(ell_g, ell_o, mg, S, f"stalled airframe two={two}")
     sol.close()
 
 
