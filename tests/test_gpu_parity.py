@@ -250,13 +250,15 @@ def test_violator_keeps_flying_on_gpu(smc):
 
 @pytest.mark.parametrize("case,sp", [("c2", "1"), ("c2", "0"), ("table1", "1"), ("n24", "1"), ("n12_noise", "1"),
                                      ("n24", "0"), ("n6", "1"), ("n14", "1"), ("n20", "1"), ("n28", "1"),
-                                     ("n28", "0")])
+                                     ("n28", "0"), ("c2", "2"), ("table1", "2"), ("n6", "2"), ("n12_noise", "2"),
+                                     ("n14", "2"), ("n20", "2"), ("n24", "2"), ("n28", "2")])
 def test_evaluate_parity(smc, case, sp, monkeypatch):
-    """Single-candidate evaluation (round 0 / paper mode) in the production K2 instances
-    against the oracle, element by element: sample pairs in the float2 slots
-    (SMC_K2_SP, default) or one sample per lane, S odd (last pair half used), and every
-    separation-ring instance (n = 6, 10, 12, 14, 20, 24, 28)."""
-    monkeypatch.setenv("SMC_K2_SP", sp)
+    """Evaluation of caller controls in the production K2 instances against the oracle,
+    element by element: single candidate (round 0 / paper mode) with sample pairs in the
+    float2 slots (SMC_K2_SP, default) or one sample per lane, or (sp = "2") the two-candidate
+    two-chain kernel with both candidates = the controls; S odd (last pair half used), and
+    every separation-ring instance (n = 6, 10, 12, 14, 20, 24, 28)."""
+    monkeypatch.setenv("SMC_K2_SP", "1" if sp == "2" else sp)
     if case == "table1":
         scn, cfg = sc.config(6)
         seed = cfg.seed
@@ -280,7 +282,7 @@ def test_evaluate_parity(smc, case, sp, monkeypatch):
     L = max(64, 12000 // (n * S))
     ctrl = _near_trim_controls(scn, L, seed=3)
     sol = _solver(smc, scn, L=L, S=S, seed=seed)
-    ell_g = sol.debug_evaluate(ctrl, S, 4).astype(np.float64)
+    ell_g = sol.debug_evaluate(ctrl, S, 4, two=sp == "2").astype(np.float64)
     ell_o, mg = O.Problem(scn).evaluate(ctrl.astype(np.float64), S, 4, seed, margin=True)
     _check_ell(ell_g, ell_o, mg, S, f"evaluate {case} sp={sp}")
     sol.close()
