@@ -402,6 +402,7 @@ def main():
     h2d = io_h2d // max(1, args.e2e_steps)
     d2h = io_d2h // max(1, args.e2e_steps)
 
+    sol.close()                      # every rank tears its communicator down at the same point
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -470,7 +471,7 @@ def main():
                                      "frac": rb / (rs_ms / 1000.0) / 1e9 / float(peaks.get("hbm_gbs", 6650.0))}
     if micro:
         line["pipe_micro"] = micro
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:      # the oracle on the host cores: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(scn, cfg)
     print(json.dumps(line), flush=True)
     if world > 1:
