@@ -251,7 +251,8 @@ def test_violator_keeps_flying_on_gpu(smc):
 @pytest.mark.parametrize("case,sp", [("c2", "1"), ("c2", "0"), ("table1", "1"), ("n24", "1"), ("n12_noise", "1"),
                                      ("n24", "0"), ("n6", "1"), ("n14", "1"), ("n20", "1"), ("n28", "1"),
                                      ("n28", "0"), ("c2", "2"), ("table1", "2"), ("n6", "2"), ("n12_noise", "2"),
-                                     ("n14", "2"), ("n20", "2"), ("n24", "2"), ("n28", "2")])
+                                     ("n14", "2"), ("n20", "2"), ("n24", "2"), ("n28", "2"), ("n9_partial", "1"),
+                                     ("n9_partial", "2")])
 def test_evaluate_parity(smc, case, sp, monkeypatch):
     """Evaluation of caller controls in the production K2 instances against the oracle,
     element by element: single candidate (round 0 / paper mode) with sample pairs in the
@@ -274,6 +275,13 @@ def test_evaluate_parity(smc, case, sp, monkeypatch):
     elif case in ("n6", "n14", "n28"):
         scn = _ring_scenario(int(case[1:]))
         seed = 0x5EED0200 + int(case[1:])
+    elif case == "n9_partial":
+        # aircraft entering the horizon late (simulated from their first step): the
+        # once-per-particle airframe pass must hold their state until then
+        scn = _ring_scenario(9)
+        scn["H"] = 8
+        scn["first_step"] = np.array([0, 3, 0, 7, 1, 0, 5, 2, 8], np.int32)
+        seed = 0x5EED0209
     else:
         scn, cfg = sc.config(2)
         seed = cfg.seed
