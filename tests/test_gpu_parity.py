@@ -217,6 +217,42 @@ def test_rollout_landing_exercised(smc):
     _compare_rollouts(smc, scn, L, 4, k=0, seed=7, ctrl=ctrl, name="rollout landing")
 
 
+@pytest.mark.parametrize("two", [False, True])
+def test_landing_hoisted_parity(smc, two):
+    """An arrival set up to land in the first step of an 8-step horizon (a near-trimmed 3 deg
+    descent along the runway axis, every landing condition met with a margin) among 6 aircraft,
+    through the production kernels that integrate the airframe
+    once per particle: the landing sector's speed / heading conditions come from the airframe
+    pass, the position conditions per sample, and a landed sample stops accumulating -- weights
+    element by element against the oracle (single-candidate kernel, or two=True the two-chain
+    kernel)."""
+    scn = sc.small(3, 3, H=8, seed=2)
+    DEG = math.pi / 180
+    # 4.5 km out on the axis: the 4 km circle is crossed with a margin in the first step
+    scn["x0"][0] = [4500.0, 150.0, 4500.0 * math.tan(3 * DEG), 76.0, math.pi, 64000.0]
+    scn["first_step"] = np.array([0, 0, 0, 8, 0, 0], np.int32)     # the departure on the runway never enters
+    P = O.Problem(scn)
+    rng = np.random.default_rng(11)
+    L, H = 384, 8
+    ctrl = _near_trim_controls(scn, L, seed=11)
+    for a in range(1):
+        for l in range(L):
+            st = scn["x0"][a].copy()
+            for t in range(H):
+                _, D = P.lift_drag(a, st, 0.0)
+                g = -3 * DEG + rng.uniform(-0.005, 0.005)
+                ctrl[l, a, t] = [D + st[5] * 9.81 * math.sin(g) + rng.uniform(-2000, 2000), rng.uniform(-0.01, 0.01), g]
+                st = P.step(a, st, ctrl[l, a, t].astype(np.float64))
+    landed = sum(int(P.rollout(ctrl[l].astype(np.float64), l, 0, 4, 7)["landed_step"][0] > 0) for l in range(0, L, 8))
+    assert landed > L // 16                                      # landings happen in the sample
+    S = 5
+    sol = _solver(smc, scn, L=L, S=S, seed=7)
+    ell_g = sol.debug_evaluate(ctrl, S, 4, two=two).astype(np.float64)
+    ell_o, mg = P.evaluate(ctrl.astype(np.float64), S, 4, 7, margin=True)
+    _check_ell(ell_g, ell_o, mg, S, f"landing hoisted two={two}")
+    sol.close()
+
+
 def test_violator_keeps_flying_on_gpu(smc):
     """Alg.1 l.11-13 / Eq. avoidance on the GPU: an aircraft
     that breaks its envelope at step 0 keeps flying and, at step 2, conflicts with a
