@@ -288,7 +288,8 @@ def test_violator_keeps_flying_on_gpu(smc):
                                      ("n24", "0"), ("n6", "1"), ("n14", "1"), ("n20", "1"), ("n28", "1"),
                                      ("n28", "0"), ("c2", "2"), ("table1", "2"), ("n6", "2"), ("n12_noise", "2"),
                                      ("n14", "2"), ("n20", "2"), ("n24", "2"), ("n28", "2"), ("n9_partial", "1"),
-                                     ("n9_partial", "2")])
+                                     ("n9_partial", "2"), ("n9_h20", "1"), ("n9_h20", "2"), ("n9_h32", "1"),
+                                     ("n9_h32", "2")])
 def test_evaluate_parity(smc, case, sp, monkeypatch):
     """Evaluation of caller controls in the production K2 instances against the oracle,
     element by element: single candidate (round 0 / paper mode) with sample pairs in the
@@ -311,6 +312,13 @@ def test_evaluate_parity(smc, case, sp, monkeypatch):
     elif case in ("n6", "n14", "n28"):
         scn = _ring_scenario(int(case[1:]))
         seed = 0x5EED0200 + int(case[1:])
+    elif case in ("n9_h20", "n9_h32"):
+        # long horizons (H <= 32, include/smcatm.h): beyond the two-chain kernel's 2 H <= 32 flag
+        # bits two-candidate launches take the one-chain kernel; H = 32 fills the sample-pair
+        # kernel's flag word
+        scn = _ring_scenario(9)
+        scn["H"] = int(case[4:])
+        seed = 0x5EED0300 + scn["H"]
     elif case == "n9_partial":
         # aircraft entering the horizon late (simulated from their first step): the
         # once-per-particle airframe pass must hold their state until then
