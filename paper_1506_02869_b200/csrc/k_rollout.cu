@@ -20,6 +20,7 @@
 // After S samples: ell += sum_s log2 J_T (R24); lambda = sum_i ell in
 // double; MH decision (R1); survivor ell / lambda / flag written; per-column
 // max of ell folded into an atomicMax (first step of the resampling reduce).
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -915,6 +916,12 @@ k_rollout(const DevScen sc, const RolloutArgs args) {
 #ifndef SMC_K2_MINB2S
 #define SMC_K2_MINB2S 4     // 128 registers: no spill once the airframe left the sample loop (c2 -5.6 %, c4 -4.3 %)
 #endif
+#ifndef SMC_K2_SP4
+#define SMC_K2_SP4 1
+#endif
+#ifndef SMC_K2_MINB2SP4
+#define SMC_K2_MINB2SP4 3   // single-candidate four-sample instances (four wind slots)
+#endif
 #ifndef SMC_K2_MINB2S32
 #define SMC_K2_MINB2S32 3   // 32-lane segments (25-32 aircraft): more live state per lane
 #endif
@@ -939,25 +946,28 @@ __host__ __device__ inline int pop_smem_floats(int nx, int ny) { return nx * ny 
 __host__ __device__ constexpr bool k2_cross_warp(int W) { return (32 % W) != 0; }
 __host__ __device__ constexpr int k2_segs_alloc(int W) { return kBlock / W + (k2_cross_warp(W) && kBlock % W ? 1 : 0); }
 
-size_t rollout2s_smem_bytes(int W, int H, int npop) {
+size_t rollout2s_smem_bytes(int W, int H, int npop, int nsl) {
     const int SEGA = k2_segs_alloc(W), GB = W / 4;
     const size_t pos = (size_t)2 * SEGA * W;                      // entries per position array
     return sizeof(float) * (size_t)npop + sizeof(float) * ((size_t)H * 10 * kBlock)   // airframe records
-           + sizeof(float) * (SEGA * 2 * GB * 16                  // normals [SEGA][slot][GB][16]
-                              + SEGA * 2 * 16                     // AR(1) state [SEGA][slot][8] (x, y)
-                              + SEGA * 2 * 16)                    // coefficients [SEGA][slot][16]
+           + sizeof(float) * (SEGA * nsl * GB * 16                // normals [SEGA][slot][GB][16]
+                              + SEGA * nsl * 16                   // AR(1) state [SEGA][slot][8] (x, y)
+                              + SEGA * nsl * 16)                  // coefficients [SEGA][slot][16]
            + sizeof(float4) * 2 * pos + sizeof(float2) * pos      // positions x4, y4, z2, each twice
            + (k2_cross_warp(W) ? sizeof(uint32_t) * (size_t)(W / 2) * SEGA * W : 0)   // verdicts
            + sizeof(float) * 72 + 16;
 }
 
-template <int W, int R>
-__global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MINB2S) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
+// SP4: a single-candidate round (round 0, the paper-literal Alg. 1): the two float2 components of a
+// chain are two more samples of the one candidate (4 samples per lane and pass, 4 wind slots).
+template <int W, int R, bool SP4 = false>
+__global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : (SP4 ? SMC_K2_MINB2SP4 : SMC_K2_MINB2S)) k_rollout_2s(const DevScen sc, const RolloutArgs args) {
     static_assert(W >= 8 && W % 4 == 0, "two-chain instances need W >= 8 (eight AR(1) nodes per slot), W = 4 GB");
     constexpr bool XW = k2_cross_warp(W);
     static_assert(!XW || R == W, "packed segments use the whole segment as the separation ring");
-    constexpr int NSL = 2, SEGS = kBlock / W, SEGA = k2_segs_alloc(W), GB = W / 4;
-    constexpr int ENS = W >= 16 ? 1 : 2;                          // (node, slot) pairs a lane owns
+    constexpr int NSL = SP4 ? 4 : 2, SEGS = kBlock / W, SEGA = k2_segs_alloc(W), GB = W / 4;
+    constexpr int NP = 8 * NSL;                                   // (node, slot) pairs of a segment
+    constexpr int ENS = W >= NP ? 1 : (NP + W - 1) / W;           // pairs a lane owns
     constexpr int TU2 = SMC_K2_TUNROLL2S;
     // exchange barrier of a segment: its warp, or the block when segments cross warps
     auto seg_sync = [] { if constexpr (XW) __syncthreads(); else __syncwarp(); };
@@ -1012,7 +1022,7 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
         const float cq = (sc.density_mode == 0 ? 1.225f : sc.rho_const) * halfS;
         const float *src[2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) src[c] = args.ctrl[c] + ((size_t)lloc * n + lane) * H * 3;
+        for (int c = 0; c < 2; ++c) src[c] = args.ctrl[SP4 ? 0 : c] + ((size_t)lloc * n + lane) * H * 3;
         V v = vsplat<V>(Ap->x0[3]), z = vsplat<V>(Ap->x0[2]), chi = vsplat<V>(Ap->x0[4]), m = vsplat<V>(Ap->x0[5]);
         int broken = 0;
         for (int t = 0; t < H; ++t) {
@@ -1089,7 +1099,7 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
     float2 *const s_pz = reinterpret_cast<float2 *>(s_p4 + 2 * NPOS);   // z: shared by the two samples
     const uint32_t S = args.S;
 
-    for (uint32_t s = 0; s < S; s += 2) {
+    for (uint32_t s = 0; s < S; s += NSL) {
         const bool two = s + 1 < S;                                // odd S: the second chain is not counted
         V x[2], y[2], fuel[2], sA[2], sB[2], sN[2];
         V z = vsplat<V>(Ap->x0[2]);                                // the airframe altitude (both samples)
@@ -1100,8 +1110,13 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
         }
         int landedm[2] = {0, 0}, violm[2] = {0, 0};
         float2 Zr[ENS];
-        float2 gust_odd[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        const uint32_t x1[2] = {(s & 0xFFFFu) | (k << 16), ((s + 1) & 0xFFFFu) | (k << 16)};
+        float2 gust_odd[NSL];
+        uint32_t x1[NSL];                                          // slot sl: sample s + sl (SP4: chain sl / 2, component sl % 2)
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+            gust_odd[sl] = make_float2(0.f, 0.f);
+            x1[sl] = ((s + sl) & 0xFFFFu) | (k << 16);
+        }
 
 #pragma unroll TU2
         for (int t = 0; t < H; ++t) {
@@ -1120,13 +1135,13 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
             }
             seg_sync();
             float2 *const sZ2 = reinterpret_cast<float2 *>(s_Z + seg * 16 * NSL);
-            // (node, slot) pair pq of the 16 a segment advances: W >= 16: pair lane mod 16 (duplicates
-            // store identical values); W = 8: pairs lane and lane + 8; W = 12: lane and lane + 12 < 16
+            // (node, slot) pair pq of the NP a segment advances: W >= NP: pair lane mod NP (duplicates
+            // store identical values); else pairs lane + e W < NP
             constexpr bool QREG = (W % 8) == 0;                 // node = lane mod 8 for every pair
 #pragma unroll
             for (int e = 0; e < ENS; ++e) {
-                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
-                if (W >= 16 || pq < 16) {
+                const int pq = W >= NP ? (lane & (NP - 1)) : lane + e * W, node = pq & 7, sl = pq >> 3;
+                if (W >= NP || pq < NP) {
                     const float *vv = &s_V[((seg * NSL + sl) * GB + tb) * 16];
                     const float2 ve = make_float2(vv[node], vv[8 + node]);
                     Zr[e] = (t == 0) ? ve : vfma(Zr[e], sc.a, ve * sc.b);
@@ -1136,8 +1151,8 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
             seg_sync();
 #pragma unroll
             for (int e = 0; e < ENS; ++e) {
-                const int pq = W >= 16 ? (lane & 15) : lane + e * W, node = pq & 7, sl = pq >> 3;
-                if (W >= 16 || pq < 16) {
+                const int pq = W >= NP ? (lane & (NP - 1)) : lane + e * W, node = pq & 7, sl = pq >> 3;
+                if (W >= NP || pq < NP) {
                     const float4 *z4 = reinterpret_cast<const float4 *>(sZ2 + sl * 8);
                     const float *qr = QREG ? qrow : &s_Q[node * 9];
                     float2 acc = make_float2(0.0f, 0.0f);
@@ -1147,27 +1162,41 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
                         acc = vfma(make_float2(zz.x, zz.y), qr[2 * mm], acc);
                         acc = vfma(make_float2(zz.z, zz.w), qr[2 * mm + 1], acc);
                     }
-                    s_W[(seg * NSL + sl) * 16 + node] = acc.x;
-                    s_W[(seg * NSL + sl) * 16 + 8 + node] = acc.y;
+                    if constexpr (SP4) {                         // [seg][chain][k](component): float2 pairs
+                        s_W[((seg * 2 + (sl >> 1)) * 16 + node) * 2 + (sl & 1)] = acc.x;
+                        s_W[((seg * 2 + (sl >> 1)) * 16 + 8 + node) * 2 + (sl & 1)] = acc.y;
+                    } else {
+                        s_W[(seg * NSL + sl) * 16 + node] = acc.x;
+                        s_W[(seg * NSL + sl) * 16 + 8 + node] = acc.y;
+                    }
                 }
             }
             seg_sync();
-            // gusts (R15): one Philox call per sample covers steps 2u and 2u+1
-            float gxq[2] = {sc.nominal[0], sc.nominal[0]}, gyq[2] = {sc.nominal[1], sc.nominal[1]};
+            // gusts (R15): one Philox call per sample covers steps 2u and 2u+1; slot sl's gust goes to
+            // chain sl (both candidates) or, SP4, to chain sl / 2, component sl % 2
+            using GT = std::conditional_t<SP4, V, float>;
+            GT gxq[2], gyq[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) { gxq[q] = vsplat<GT>(sc.nominal[0]); gyq[q] = vsplat<GT>(sc.nominal[1]); }
             if (sc.turb_sigma > 0.0f) {
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
+                for (int sl = 0; sl < NSL; ++sl) {
                     float2 gg;
                     if ((t & 1) == 0) {
-                        const uint4 w = draw_ks(TAG_TURB, l, x1[q], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
+                        const uint4 w = draw_ks(TAG_TURB, l, x1[sl], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
                         const float4 g4 = box_muller4(w);
                         gg = make_float2(g4.x, g4.y);
-                        gust_odd[q] = make_float2(g4.z, g4.w);
+                        gust_odd[sl] = make_float2(g4.z, g4.w);
                     } else {
-                        gg = gust_odd[q];
+                        gg = gust_odd[sl];
                     }
-                    gxq[q] = fmaf(sc.turb_sigma, gg.x, gxq[q]);
-                    gyq[q] = fmaf(sc.turb_sigma, gg.y, gyq[q]);
+                    if constexpr (SP4) {
+                        cset(gxq[sl >> 1], sl & 1, fmaf(sc.turb_sigma, gg.x, sc.nominal[0]));
+                        cset(gyq[sl >> 1], sl & 1, fmaf(sc.turb_sigma, gg.y, sc.nominal[1]));
+                    } else {
+                        gxq[sl] = fmaf(sc.turb_sigma, gg.x, sc.nominal[0]);
+                        gyq[sl] = fmaf(sc.turb_sigma, gg.y, sc.nominal[1]);
+                    }
                 }
             }
             // airframe state of step t (shared by both chains: wind-independent)
@@ -1186,17 +1215,24 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
             for (int q = 0; q < 2; ++q) {
                 flym[q] = act ? (~landedm[q] & 3) : 0;
                 flyf[q] = make_float2((flym[q] & 1) ? 1.0f : 0.0f, (flym[q] & 2) ? 1.0f : 0.0f);
-                const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[(seg * NSL + q) * 16]);
-                float Wn[16];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float4 a4 = w4[e];
-                    Wn[4 * e] = a4.x; Wn[4 * e + 1] = a4.y; Wn[4 * e + 2] = a4.z; Wn[4 * e + 3] = a4.w;
-                }
                 const V fx = vmap(x[q], [&](float p) { return __saturatef(fmaf(p, inv0, nlo0)); });
                 const V fy = vmap(y[q], [&](float p) { return __saturatef(fmaf(p, inv1, nlo1)); });
-                const V wx = tripoly(Wn, Wn[0] + gxq[q], fx, fy, fz);
-                const V wy = tripoly(Wn + 8, Wn[8] + gyq[q], fx, fy, fz);
+                V wx, wy;
+                if constexpr (SP4) {                               // per-component coefficients
+                    const float2 *c2 = reinterpret_cast<const float2 *>(&s_W[(seg * 2 + q) * 32]);
+                    wx = tripoly2(c2, c2[0] + gxq[q], fx, fy, fz);
+                    wy = tripoly2(c2 + 8, c2[8] + gyq[q], fx, fy, fz);
+                } else {
+                    const float4 *w4 = reinterpret_cast<const float4 *>(&s_W[(seg * NSL + q) * 16]);
+                    float Wn[16];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float4 a4 = w4[e];
+                        Wn[4 * e] = a4.x; Wn[4 * e + 1] = a4.y; Wn[4 * e + 2] = a4.z; Wn[4 * e + 3] = a4.w;
+                    }
+                    wx = tripoly(Wn, Wn[0] + gxq[q], fx, fy, fz);
+                    wy = tripoly(Wn + 8, Wn[8] + gyq[q], fx, fy, fz);
+                }
                 const V dtf = flyf[q] * dt;
                 nx[q] = vfma(dtf, ax + wx, x[q]);
                 ny[q] = vfma(dtf, ay + wy, y[q]);
@@ -1300,9 +1336,10 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
             const int flagB = Ap->flagB;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                if (q == 1 && !two) continue;
+                if (!SP4 && q == 1 && !two) continue;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
+                    if (SP4 && s + 2 * q + c >= S) continue;          // sample count not a multiple of 4
                     float J = 1.0f;
                     if (Ha > 0 && isac) {
                         const float Jfuel = clamp01(1.0f - cget(fuel[q], c) * invFmax);
@@ -1317,7 +1354,8 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
                         }
                         if (sc.has_noise) J = (1.0f - sc.noise_w) * J + sc.noise_w * cget(sN[q], c) * invHa;
                     }
-                    ell[c] = (((violm[q] >> c) & 1) || !(J > 0.0f)) ? -INFINITY : ell[c] + __log2f(J);
+                    float &e = ell[SP4 ? 0 : c];                      // SP4: every sample adds to the one candidate
+                    e = (((violm[q] >> c) & 1) || !(J > 0.0f)) ? -INFINITY : e + __log2f(J);
                 }
             }
         }
@@ -1327,6 +1365,7 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
     __syncthreads();
     float *s_ell = reinterpret_cast<float *>(s_p4);
     int *s_dec = reinterpret_cast<int *>(s_V);
+    if constexpr (SP4) ell[1] = ell[0];                         // one candidate
     s_ell[tid] = ell[0];
     s_ell[kBlock + tid] = ell[1];
     seg_sync();
@@ -1339,7 +1378,12 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
     int nacc;
     float ell_s;
     double lam_s;
-    if (args.mh_mode == 2) {
+    if (SP4) {                                                  // no MH: the caller's survivor mask
+        mask = args.surv_single;
+        ell_s = ell[0];
+        lam_s = lam[0];
+        nacc = 0;
+    } else if (args.mh_mode == 2) {
         const bool ai = isac && mh_decide_aircraft((double)ell[0], (double)ell[1], l, (uint32_t)lane, k, mpc, sc.key0,
                                                    sc.key1);
         if constexpr (XW) {                                       // segments cross warps: via shared memory
@@ -1389,11 +1433,11 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : SMC_K2_MIN
     }
 }
 
-template <int W, int R>
+template <int W, int R, bool SP4 = false>
 static cudaError_t launch_2s_r(const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     const int npop = (SMC_K2_POP_SMEM && sc.has_noise) ? pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) : 0;
-    const size_t smem = rollout2s_smem_bytes(W, sc.H, (npop + 3) & ~3);
-    auto kern = k_rollout_2s<W, R>;
+    const size_t smem = rollout2s_smem_bytes(W, sc.H, (npop + 3) & ~3, SP4 ? 4 : 2);
+    auto kern = k_rollout_2s<W, R, SP4>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (a.L + kBlock / W - 1) / (kBlock / W);
@@ -1445,30 +1489,31 @@ static bool pack_enabled() {
     return on;
 }
 
+template <bool SP4>
 static cudaError_t launch_2s(int W, int R, const DevScen &sc, const RolloutArgs &a, cudaStream_t st) {
     // packed segments (W not dividing a warp, ring = segment): 9-12 aircraft in 12 lanes (10 per block),
     // 17-20 in 20 (6 per block), 21-24 in 24 (5 per block) -- instead of 16- / 32-lane segments
-    if (pack_enabled()) {
-        if (sc.n >= 9 && sc.n <= 12) return launch_2s_r<12, 12>(sc, a, st);
-        if (sc.n >= 17 && sc.n <= 20) return launch_2s_r<20, 20>(sc, a, st);
-        if (sc.n >= 21 && sc.n <= 24) return launch_2s_r<24, 24>(sc, a, st);
+    if (!SP4 && pack_enabled()) {   // (SP4 instances: segments within warps only)
+        if (sc.n >= 9 && sc.n <= 12) return launch_2s_r<12, 12, SP4>(sc, a, st);
+        if (sc.n >= 17 && sc.n <= 20) return launch_2s_r<20, 20, SP4>(sc, a, st);
+        if (sc.n >= 21 && sc.n <= 24) return launch_2s_r<24, 24, SP4>(sc, a, st);
     }
     switch (W) {
 #if SMC_K2_2S_MINW <= 8
         case 8:
-            if (R == 6) return launch_2s_r<8, 6>(sc, a, st);
-            return launch_2s_r<8, 8>(sc, a, st);
+            if (R == 6) return launch_2s_r<8, 6, SP4>(sc, a, st);
+            return launch_2s_r<8, 8, SP4>(sc, a, st);
 #endif
         case 16:
-            if (R == 10) return launch_2s_r<16, 10>(sc, a, st);
-            if (R == 12) return launch_2s_r<16, 12>(sc, a, st);
-            if (R == 14) return launch_2s_r<16, 14>(sc, a, st);
-            return launch_2s_r<16, 16>(sc, a, st);
+            if (R == 10) return launch_2s_r<16, 10, SP4>(sc, a, st);
+            if (R == 12) return launch_2s_r<16, 12, SP4>(sc, a, st);
+            if (R == 14) return launch_2s_r<16, 14, SP4>(sc, a, st);
+            return launch_2s_r<16, 16, SP4>(sc, a, st);
         case 32:
-            if (R == 20) return launch_2s_r<32, 20>(sc, a, st);
-            if (R == 24) return launch_2s_r<32, 24>(sc, a, st);
-            if (R == 28) return launch_2s_r<32, 28>(sc, a, st);
-            return launch_2s_r<32, 32>(sc, a, st);
+            if (R == 20) return launch_2s_r<32, 20, SP4>(sc, a, st);
+            if (R == 24) return launch_2s_r<32, 24, SP4>(sc, a, st);
+            if (R == 28) return launch_2s_r<32, 28, SP4>(sc, a, st);
+            return launch_2s_r<32, 32, SP4>(sc, a, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -1555,7 +1600,18 @@ int segment_width(int n, bool dense) {
 cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool debug, cudaStream_t st) {
     const bool dense = sc.wng > 8;
     const int W = segment_width(sc.n, dense);
-    if (NC == 1 && !debug && !dense && W >= 8 && sc.H <= 32 && sp_enabled()) return launch_sp(W, sc, a, st);   // flags: bit t
+    if (NC == 1 && !debug && !dense && W >= 8 && sp_enabled()) {
+        // one candidate: four samples per lane in the two-chain kernel for 16-lane segments (flags:
+        // 2 H <= 32 bits; Table-1 123.7 -> 112.8 ms), else sample pairs in the one-chain kernel
+        // (flags: bit t; at W = 8 four samples per lane measured slower, c2's 1024 blocks filling
+        // 2.3 waves)
+        if (SMC_K2_SP4 && sc.H <= 16 && W == 16) {
+            RolloutArgs b = a;
+            b.ctrl[1] = a.ctrl[0];
+            return launch_2s<true>(W, ring_for(W, sc.n), sc, b, st);
+        }
+        if (sc.H <= 32) return launch_sp(W, sc, a, st);
+    }
     // two sample chains per lane where they measured faster (B200, K2 per MPC step, 2 interleaved repeats:
     // c5 2376 -> 2330 ms (21 rounds), c4 23.6 -> 22.3, c3 89.4 -> 83.6 (11 rounds); c2 (W = 8) 26.40 ->
     // 26.68: one chain)
@@ -1564,7 +1620,7 @@ cudaError_t launch_rollout(const DevScen &sc, const RolloutArgs &a, int NC, bool
     // one-chain kernel
     const bool pop_fits = !SMC_K2_POP_SMEM || !sc.has_noise || pop_smem_floats(sc.pop_nx + 1, sc.pop_ny + 1) > 0;
     if (NC == 2 && !debug && !dense && pop_fits && sc.H <= 16 && W >= SMC_K2_2S_MINW && ns2_enabled())
-        return launch_2s(W, ring_for(W, sc.n), sc, a, st);
+        return launch_2s<false>(W, ring_for(W, sc.n), sc, a, st);
     if (debug) return NC == 2 ? launch_nc<2, true>(W, dense, sc, a, st) : launch_nc<1, true>(W, dense, sc, a, st);
     return NC == 2 ? launch_nc<2, false>(W, dense, sc, a, st) : launch_nc<1, false>(W, dense, sc, a, st);
 }
