@@ -18,4 +18,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rollout -s 2 -c 1 -o gpurun_out/prof_k2c5_$tag python tools/prof_step.py 5 4 > gpurun_out/ncu_k2c5_$tag.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rollout -s 2 -c 1 -o gpurun_out/prof_k2c2_$tag python tools/prof_step.py 2 4 > gpurun_out/ncu_k2c2_$tag.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:"k_scan|k_gather|k_mp|k_ancestors" -c 4 -o gpurun_out/prof_rsc5_$tag python tools/prof_step.py 5 3 > gpurun_out/ncu_rsc5_$tag.log 2>&1
+# keep the merged output under gpurun's 64 MiB: metrics of every capture as JSON, only the c5 K2 report kept
+for r in prof_k2c2_$tag prof_rsc5_$tag prof_k2c5_$tag; do
+  [ -f gpurun_out/$r.ncu-rep ] && python tools/ncu_full_json.py gpurun_out/$r.ncu-rep > gpurun_out/$r.json
+done
+rm -f gpurun_out/prof_k2c2_$tag.ncu-rep gpurun_out/prof_rsc5_$tag.ncu-rep
 echo done

@@ -30,10 +30,14 @@ subprocess.run(["cp", G(f"launches_c5_{tag}.csv"), P("r02_launches_bench_c5.csv"
 with open(P("r02_launches_bench_c5_summary.txt"), "w") as f:
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), G(f"launches_c5_{tag}.csv")],
                    stdout=f, check=True)
-for src, dst in ((f"prof_k2c5_{tag}.ncu-rep", "r02_ncu_full_c5_k2.json"), (f"prof_k2c2_{tag}.ncu-rep",
-                 "r02_ncu_full_c2_k2.json"), (f"prof_rsc5_{tag}.ncu-rep", "r02_ncu_full_c5_resample.json")):
+for src, dst in ((f"prof_k2c5_{tag}", "r02_ncu_full_c5_k2.json"), (f"prof_k2c2_{tag}", "r02_ncu_full_c2_k2.json"),
+                 (f"prof_rsc5_{tag}", "r02_ncu_full_c5_resample.json")):
+    if os.path.exists(G(src + ".json")):                    # converted on the box (gpu_round2.sh)
+        subprocess.run(["cp", G(src + ".json"), P(dst)], check=True)
+        continue
     with open(P(dst), "w") as f:
-        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_full_json.py"), G(src)], stdout=f, check=True)
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_full_json.py"), G(src + ".ncu-rep")], stdout=f,
+                       check=True)
 
 
 def gb(v):
