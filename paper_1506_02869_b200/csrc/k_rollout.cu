@@ -1112,10 +1112,16 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : (SP4 ? SMC
         float2 Zr[ENS];
         float2 gust_odd[NSL];
         uint32_t x1[NSL];                                          // slot sl: sample s + sl (SP4: chain sl / 2, component sl % 2)
+        if constexpr (SP4) {
 #pragma unroll
-        for (int sl = 0; sl < NSL; ++sl) {
-            gust_odd[sl] = make_float2(0.f, 0.f);
-            x1[sl] = ((s + sl) & 0xFFFFu) | (k << 16);
+            for (int sl = 0; sl < NSL; ++sl) {
+                gust_odd[sl] = make_float2(0.f, 0.f);
+                x1[sl] = ((s + sl) & 0xFFFFu) | (k << 16);
+            }
+        } else {
+            gust_odd[0] = gust_odd[1] = make_float2(0.f, 0.f);
+            x1[0] = (s & 0xFFFFu) | (k << 16);
+            x1[1] = ((s + 1) & 0xFFFFu) | (k << 16);
         }
 
 #pragma unroll TU2
@@ -1176,26 +1182,42 @@ __global__ void __launch_bounds__(kBlock, W >= 32 ? SMC_K2_MINB2S32 : (SP4 ? SMC
             // chain sl (both candidates) or, SP4, to chain sl / 2, component sl % 2
             using GT = std::conditional_t<SP4, V, float>;
             GT gxq[2], gyq[2];
+            if constexpr (SP4) {
 #pragma unroll
-            for (int q = 0; q < 2; ++q) { gxq[q] = vsplat<GT>(sc.nominal[0]); gyq[q] = vsplat<GT>(sc.nominal[1]); }
-            if (sc.turb_sigma > 0.0f) {
+                for (int q = 0; q < 2; ++q) { gxq[q] = vsplat<GT>(sc.nominal[0]); gyq[q] = vsplat<GT>(sc.nominal[1]); }
+                if (sc.turb_sigma > 0.0f) {
 #pragma unroll
-                for (int sl = 0; sl < NSL; ++sl) {
-                    float2 gg;
-                    if ((t & 1) == 0) {
-                        const uint4 w = draw_ks(TAG_TURB, l, x1[sl], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
-                        const float4 g4 = box_muller4(w);
-                        gg = make_float2(g4.x, g4.y);
-                        gust_odd[sl] = make_float2(g4.z, g4.w);
-                    } else {
-                        gg = gust_odd[sl];
-                    }
-                    if constexpr (SP4) {
+                    for (int sl = 0; sl < NSL; ++sl) {
+                        float2 gg;
+                        if ((t & 1) == 0) {
+                            const uint4 w = draw_ks(TAG_TURB, l, x1[sl], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
+                            const float4 g4 = box_muller4(w);
+                            gg = make_float2(g4.x, g4.y);
+                            gust_odd[sl] = make_float2(g4.z, g4.w);
+                        } else {
+                            gg = gust_odd[sl];
+                        }
                         cset(gxq[sl >> 1], sl & 1, fmaf(sc.turb_sigma, gg.x, sc.nominal[0]));
                         cset(gyq[sl >> 1], sl & 1, fmaf(sc.turb_sigma, gg.y, sc.nominal[1]));
-                    } else {
-                        gxq[sl] = fmaf(sc.turb_sigma, gg.x, sc.nominal[0]);
-                        gyq[sl] = fmaf(sc.turb_sigma, gg.y, sc.nominal[1]);
+                    }
+                }
+            } else {
+                gxq[0] = gxq[1] = sc.nominal[0];
+                gyq[0] = gyq[1] = sc.nominal[1];
+                if (sc.turb_sigma > 0.0f) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        float2 gg;
+                        if ((t & 1) == 0) {
+                            const uint4 w = draw_ks(TAG_TURB, l, x1[q], ((uint32_t)t >> 1) | ((uint32_t)lane << 8), mpc, sc.ks);
+                            const float4 g4 = box_muller4(w);
+                            gg = make_float2(g4.x, g4.y);
+                            gust_odd[q] = make_float2(g4.z, g4.w);
+                        } else {
+                            gg = gust_odd[q];
+                        }
+                        gxq[q] = fmaf(sc.turb_sigma, gg.x, gxq[q]);
+                        gyq[q] = fmaf(sc.turb_sigma, gg.y, gyq[q]);
                     }
                 }
             }
